@@ -1,0 +1,27 @@
+# libfdp.so: sm_100a kernels + host numerics + C ABI (include/fdp.h).
+NVCC ?= /usr/local/cuda/bin/nvcc
+PKG := paper_1712_00403_b200
+SRC := $(PKG)/csrc
+LIB := $(PKG)/libfdp.so
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -O3 --expt-relaxed-constexpr
+OBJ := build/mode_contract.o build/kron_mass.o build/abi.o build/host_eig.o build/host_iga.o
+HDR := $(SRC)/fdp_internal.h include/fdp.h
+
+all: $(LIB)
+
+build/%.o: $(SRC)/kernels/%.cu $(HDR)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
+
+build/%.o: $(SRC)/%.cpp $(HDR)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -x cu -c $< -o $@
+
+$(LIB): $(OBJ)
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJ)
+
+clean:
+	rm -rf build $(LIB)
+
+.PHONY: all clean

@@ -1,0 +1,172 @@
+/*
+ * fdp.h -- C ABI of the B200-native Fast-Diagonalization block preconditioner
+ * (M. Montardini, G. Sangalli, M. Tani, "Robust isogeometric preconditioners for the Stokes
+ * system based on the Fast Diagonalization method", arXiv:1712.00403).
+ *
+ * Citations "P:L" are lines of the paper text with the section / equation named.
+ *
+ * Conventions for every entry point
+ *   - Plain C99 types only. Matrices on the host are dense, column-major, n x n.
+ *   - Tensors are vectors in vec order, i1 fastest: i = i1 + n1*(i2 + n2*i3) (§2.3).
+ *     A batch of B vectors is stored batch-major: item b starts at offset b*N.
+ *   - "device" pointers are CUDA global-memory pointers on the handle's device; passing a host
+ *     pointer where a device pointer is required returns FDP_ERR_INVALID_ARG.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream). Apply calls are
+ *     asynchronous on that stream, allocate nothing and never synchronise (except the *_host
+ *     variant), so they are CUDA-graph capturable. Launch failures return FDP_ERR_CUDA; faults
+ *     during execution surface at the caller's next synchronisation.
+ *   - Handles own their device memory; caller arrays are copied at setup. Destroy after the
+ *     caller has synchronised every stream that used the handle. Destroy functions are NULL-safe.
+ *   - No function aborts, exits or throws across the ABI. On failure the status is returned and
+ *     fdp_last_error() (thread-local) holds a one-line message.
+ *   - There is no CPU fallback: every apply runs in this library's sm_100a kernels.
+ */
+#ifndef FDP_H_
+#define FDP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FDP_OK = 0,
+  FDP_ERR_INVALID_ARG = 1, /* null / host-vs-device pointer mix-up / bad enum */
+  FDP_ERR_SHAPE = 2,       /* dimension out of range or inconsistent */
+  FDP_ERR_NOT_SPD = 3,     /* Cholesky of a mass matrix failed, or matrix not symmetric */
+  FDP_ERR_SINGULAR = 4,    /* Kronecker-sum spectrum: sum_d c_d min(lambda_d) <= 1e-12 sum_d c_d max(lambda_d) */
+  FDP_ERR_CUDA = 5,        /* CUDA runtime error (launch, copy, graph) */
+  FDP_ERR_OOM = 6,         /* device or host allocation failed */
+  FDP_ERR_NCCL = 7,        /* reserved: multi-GPU exchange */
+  FDP_ERR_UNSUPPORTED = 8  /* valid request this build does not implement (e.g. D > 3) */
+} fdp_status;
+
+const char* fdp_status_string(fdp_status s);
+/* Thread-local message of the last failing call on this thread ("" if none). */
+const char* fdp_last_error(void);
+/* Library version string, e.g. "fdp 0.1 sm_100a". */
+const char* fdp_version(void);
+
+/* ------------------------------------------------------------------------------------------
+ * Host helpers: univariate isogeometric factors ("univariate matrix factors", §5;
+ * P:734-737 pressure mass). Built by this library's own B-spline evaluation and Gauss rule.
+ * ------------------------------------------------------------------------------------------ */
+enum {
+  FDP_IGA_INTERIOR = 1, /* restrict to basis functions l,s = 2..m-1 (Dirichlet / normal trace,
+                           P:265-267, 694, 699) */
+  FDP_IGA_NITSCHE = 2   /* replace K by K~ of P:701-704 (tangential RT factor, Nitsche bracket
+                           with penalty 2*c_pen/h, h = 1/n_el) */
+};
+
+/* Open uniform knot vector of degree `deg`, uniform regularity `alpha` (-1 <= alpha < deg),
+ * n_el elements. Writes K (stiffness, int b_l' b_s') and M (mass, int b_l b_s) as
+ * column-major n x n into caller-owned host arrays of at least n*n doubles, where n is the
+ * space dimension m = n_el(deg-alpha)+alpha+1, minus 2 with FDP_IGA_INTERIOR. Gauss rule with
+ * `q` points per element (q <= 0 selects deg+1, exact for these polynomial integrands).
+ * K or M may be NULL to skip it; both NULL just reports n in *n_out.
+ * Errors: FDP_ERR_SHAPE (deg < 1, alpha out of range, n_el < 1, n < 1), FDP_ERR_INVALID_ARG. */
+fdp_status iga_univariate(int deg, int alpha, int n_el, int flags, double c_pen, int q,
+                          double* K, double* M, int32_t* n_out);
+
+/* Greville abscissae (xi_{j+1}+...+xi_{j+deg})/deg of the same space (first/last dropped with
+ * FDP_IGA_INTERIOR): dof coordinates used to sample a coefficient at dofs (C-6).
+ * g: host array of at least n doubles, or NULL to query n. */
+fdp_status iga_greville(int deg, int alpha, int n_el, int flags, double* g, int32_t* n_out);
+
+/* Generalized symmetric-definite eigenproblem K U = M U diag(lambda), U^T M U = I (Algorithm 1
+ * step 1), host only: the routine fd_setup uses. K, M: host column-major n x n, M SPD;
+ * U (n*n, column j = eigenvector j, largest-magnitude entry positive) and lambda (n, ascending)
+ * are caller-owned host arrays. Errors: FDP_ERR_SHAPE, FDP_ERR_NOT_SPD, FDP_ERR_SINGULAR (QL
+ * iteration did not converge). */
+fdp_status fdp_gen_eig(int n, const double* K, const double* M, double* U, double* lambda);
+
+/* ------------------------------------------------------------------------------------------
+ * FD solver for one Sylvester-like Kronecker system (Algorithm 1, §5.2):
+ *   R = sum_d coef[d] * (F_D (x) ... (x) F_1),  F_e = K_e if e == d else M_e
+ *   x = dscale o ( U Lambda^{-1} U^T ( dscale o b ) ),  U = U_D (x) ... (x) U_1,
+ *   Lambda = sum_d coef[d] lambda_d,  K_d U_d = M_d U_d diag(lambda_d),  U_d^T M_d U_d = I.
+ * dscale = D^{-1/2} realises P^G = D^{1/2} P D^{1/2} (§6).
+ * ------------------------------------------------------------------------------------------ */
+typedef struct fdp_fd_s* fdp_fd;
+
+/* D in {2,3}; n[d] in [1, 2048]; K[d], M[d]: host, column-major n[d] x n[d], symmetric to
+ * 1e-12 relative, M[d] SPD; coef[d] > 0. Performs the D generalized eigensolves on the host
+ * (Algorithm 1 step 1: Cholesky + Householder tridiagonalisation + implicit QL),
+ * uploads U_d, U_d^T (zero padded) and lambda_d to `device`, and allocates a workspace for
+ * up to max_batch right-hand sides (0 = none; then fd_apply needs a caller workspace).
+ * Errors: FDP_ERR_SHAPE, FDP_ERR_NOT_SPD, FDP_ERR_SINGULAR, FDP_ERR_OOM, FDP_ERR_CUDA. */
+fdp_status fd_setup(int D, const int32_t* n, const double* const* K, const double* const* M,
+                    const double* coef, int device, int64_t max_batch, fdp_fd* out);
+
+/* Host copies of U_d (column-major n_d x n_d, column j = eigenvector j) and lambda_d
+ * (ascending). Either output may be NULL. */
+fdp_status fd_get_eigs(fdp_fd h, int d, double* U_out, double* lambda_out);
+/* N = prod n_d of the handle. */
+int64_t fd_size(fdp_fd h);
+/* Bytes of device workspace fd_apply needs for `batch` right-hand sides. */
+size_t fd_workspace_bytes(fdp_fd h, int64_t batch);
+
+/* b, x: device, batch*N doubles, batch-major; x may alias b (in place). dscale: device, N
+ * doubles holding D^{-1/2} (> 0), or NULL for the plain solve. workspace: device, at least
+ * fd_workspace_bytes(h,batch) bytes, or NULL to use the handle's own (then batch <= max_batch
+ * and the handle must not be used concurrently on two streams). */
+fdp_status fd_apply(fdp_fd h, const double* b, double* x, const double* dscale, int64_t batch,
+                    void* workspace, void* stream);
+fdp_status fd_destroy(fdp_fd h);
+
+/* ------------------------------------------------------------------------------------------
+ * Kronecker mass P_Q = M_D (x) ... (x) M_1 (eq. precQ) and its inverse by per-mode banded
+ * Cholesky solves in O(p n_Q) flops (identity (A(x)B(x)C)^{-1} vec X).
+ * ------------------------------------------------------------------------------------------ */
+typedef struct fdp_mass_s* fdp_mass;
+enum { FDP_MASS_INVERSE = 0, FDP_MASS_FORWARD = 1 };
+
+/* M[d]: host, column-major, symmetric positive definite, half-bandwidth <= 15 (detected).
+ * Errors: FDP_ERR_SHAPE, FDP_ERR_NOT_SPD, FDP_ERR_OOM, FDP_ERR_CUDA. */
+fdp_status kron_mass_setup(int D, const int32_t* n, const double* const* M, int device,
+                           fdp_mass* out);
+int64_t kron_mass_size(fdp_mass h);
+/* mode FDP_MASS_INVERSE: x = dscale o (P_Q^{-1} (dscale o b)), dscale = D_Q^{-1/2} or NULL
+ * (P_Q^G of P:1039). mode FDP_MASS_FORWARD: x = P_Q b (dscale must be NULL). b, x device,
+ * batch*N doubles; x may alias b for FDP_MASS_INVERSE only. No workspace is needed. */
+fdp_status kron_mass_apply(fdp_mass h, int mode, const double* b, double* x,
+                           const double* dscale, int64_t batch, void* stream);
+fdp_status kron_mass_destroy(fdp_mass h);
+
+/* ------------------------------------------------------------------------------------------
+ * Block-diagonal preconditioner P_D = diag(P_V,1, ..., P_V,D, P_Q) (eq. P_D; P_V
+ * block diagonal P:644-652) and its scaled variant P_D^G.
+ * r, s layout per batch item: [u_1 | ... | u_D | p], each block in vec order.
+ * ------------------------------------------------------------------------------------------ */
+typedef struct fdp_block_s* fdp_block;
+
+/* vel[k]: FD handles of the D velocity components (non-owning; must outlive the block);
+ * pres: mass handle (non-owning). dscale_vel: host, sum_k N_k doubles of D_V (> 0), or NULL;
+ * dscale_pres: host, n_Q doubles of D_Q (> 0), or NULL. The library stores
+ * D^{-1/2} on the device. All handles must live on the same device. */
+fdp_status block_precond_setup(int D, const fdp_fd* vel, fdp_mass pres, const double* dscale_vel,
+                               const double* dscale_pres, fdp_block* out);
+int64_t block_precond_size(fdp_block h); /* sum_k N_k + n_Q */
+size_t block_precond_workspace_bytes(fdp_block h, int64_t batch);
+/* s = P_D^{-1} r (or (P_D^G)^{-1} r). r, s: device, batch*size doubles; s may alias r.
+ * workspace: device, >= block_precond_workspace_bytes(h, batch) bytes (required, no internal
+ * default). The launch sequence is captured once per (r, s, workspace, batch) into a CUDA graph
+ * and replayed; if `stream` is being captured by the caller, kernels are launched directly. */
+fdp_status block_precond_apply(fdp_block h, const double* r, double* s, int64_t batch,
+                               void* workspace, void* stream);
+/* End-to-end variant with HOST buffers (pinned recommended): copies r host->device, applies,
+ * copies s device->host, and synchronises `stream` before returning. Uses handle-owned device
+ * buffers sized on first use. */
+fdp_status block_precond_apply_host(fdp_block h, const double* r_host, double* s_host,
+                                    int64_t batch, void* stream);
+fdp_status block_precond_destroy(fdp_block h);
+
+/* Number of kernel launches one block_precond_apply issues for `batch` (for accounting). */
+int fdp_block_launch_count(fdp_block h, int64_t batch);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FDP_H_ */

@@ -1,0 +1,394 @@
+"""Python binding of libfdp (include/fdp.h): argument marshalling only.
+
+Every step of the preconditioner application runs in libfdp's sm_100a kernels; torch provides
+device memory and streams. There is no CPU fallback: if ``libfdp.so`` is missing or a call fails
+the binding raises. Names follow the C ABI (``fd_setup`` -> :class:`FD`, ``kron_mass_*`` ->
+:class:`KronMass`, ``block_precond_*`` -> :class:`BlockPrecond`).
+
+Paper: Montardini, Sangalli, Tani, arXiv:1712.00403. Citations P:L are its lines.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+__all__ = ["FdpError", "lib", "iga_univariate", "iga_greville", "gen_eig", "FD", "KronMass",
+           "BlockPrecond", "Discretization", "discretization", "nu_scalings", "LIB_PATH"]
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfdp.so")
+
+FDP_IGA_INTERIOR = 1
+FDP_IGA_NITSCHE = 2
+FDP_MASS_INVERSE = 0
+FDP_MASS_FORWARD = 1
+
+_c_double_p = ctypes.POINTER(ctypes.c_double)
+_c_int32_p = ctypes.POINTER(ctypes.c_int32)
+
+
+class FdpError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"{_status_name(status)}: {message}")
+        self.status = status
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libfdp.so not built at {LIB_PATH}: run `make` or __graft_entry__.build()")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i64, i32, sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_size_t
+    sig = {
+        "fdp_status_string": (ctypes.c_char_p, [i32]),
+        "fdp_last_error": (ctypes.c_char_p, []),
+        "fdp_version": (ctypes.c_char_p, []),
+        "iga_univariate": (i32, [i32, i32, i32, i32, ctypes.c_double, i32, vp, vp, _c_int32_p]),
+        "iga_greville": (i32, [i32, i32, i32, i32, vp, _c_int32_p]),
+        "fdp_gen_eig": (i32, [i32, vp, vp, vp, vp]),
+        "fd_setup": (i32, [i32, vp, vp, vp, vp, i32, i64, ctypes.POINTER(vp)]),
+        "fd_get_eigs": (i32, [vp, i32, vp, vp]),
+        "fd_size": (i64, [vp]),
+        "fd_workspace_bytes": (sz, [vp, i64]),
+        "fd_apply": (i32, [vp, vp, vp, vp, i64, vp, vp]),
+        "fd_destroy": (i32, [vp]),
+        "kron_mass_setup": (i32, [i32, vp, vp, i32, ctypes.POINTER(vp)]),
+        "kron_mass_size": (i64, [vp]),
+        "kron_mass_apply": (i32, [vp, i32, vp, vp, vp, i64, vp]),
+        "kron_mass_destroy": (i32, [vp]),
+        "block_precond_setup": (i32, [i32, vp, vp, vp, vp, ctypes.POINTER(vp)]),
+        "block_precond_size": (i64, [vp]),
+        "block_precond_workspace_bytes": (sz, [vp, i64]),
+        "block_precond_apply": (i32, [vp, vp, vp, i64, vp, vp]),
+        "block_precond_apply_host": (i32, [vp, vp, vp, i64, vp]),
+        "block_precond_destroy": (i32, [vp]),
+        "fdp_block_launch_count": (i32, [vp, i64]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    return L
+
+
+lib = _load()
+
+
+def _status_name(s: int) -> str:
+    return lib.fdp_status_string(s).decode()
+
+
+def _check(status: int):
+    if status != 0:
+        raise FdpError(status, lib.fdp_last_error().decode())
+
+
+def _host(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _fortran(a) -> np.ndarray:
+    return np.asfortranarray(a, dtype=np.float64)
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _dev(t, name: str, numel: int | None = None) -> int:
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name}: expected a torch.Tensor on CUDA")
+    if t.dtype != torch.float64 or not t.is_cuda or not t.is_contiguous():
+        raise TypeError(f"{name}: expected a contiguous float64 CUDA tensor")
+    if numel is not None and t.numel() < numel:
+        raise ValueError(f"{name}: needs {numel} elements, has {t.numel()}")
+    return t.data_ptr()
+
+
+def _stream(stream) -> int:
+    import torch
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+# ----------------------------------------------------------------------------------------------
+# host helpers
+# ----------------------------------------------------------------------------------------------
+def iga_univariate(deg: int, alpha: int, n_el: int, flags: int = 0, c_pen: float = 0.0, q: int = 0):
+    """(K, M) of the univariate space built by libfdp (column-major)."""
+    n = ctypes.c_int32(0)
+    _check(lib.iga_univariate(deg, alpha, n_el, flags, c_pen, q, None, None, ctypes.byref(n)))
+    K = np.zeros((n.value, n.value), order="F")
+    M = np.zeros((n.value, n.value), order="F")
+    _check(lib.iga_univariate(deg, alpha, n_el, flags, c_pen, q, _ptr(K), _ptr(M), ctypes.byref(n)))
+    return K, M
+
+
+def iga_greville(deg: int, alpha: int, n_el: int, flags: int = 0) -> np.ndarray:
+    n = ctypes.c_int32(0)
+    _check(lib.iga_greville(deg, alpha, n_el, flags, None, ctypes.byref(n)))
+    g = np.zeros(n.value)
+    _check(lib.iga_greville(deg, alpha, n_el, flags, _ptr(g), ctypes.byref(n)))
+    return g
+
+
+def gen_eig(K, M):
+    """Host generalized eigensolver of libfdp (Algorithm 1 step 1): (lambda, U)."""
+    K, M = _fortran(K), _fortran(M)
+    n = K.shape[0]
+    U = np.zeros((n, n), order="F")
+    lam = np.zeros(n)
+    _check(lib.fdp_gen_eig(n, _ptr(K), _ptr(M), _ptr(U), _ptr(lam)))
+    return lam, U
+
+
+# ----------------------------------------------------------------------------------------------
+# handles
+# ----------------------------------------------------------------------------------------------
+class FD:
+    """fd_setup / fd_apply: x = dscale o U Lambda^{-1} U^T (dscale o b) (Algorithm 1)."""
+
+    def __init__(self, Ks, Ms, coef, device: int = 0, max_batch: int = 0):
+        D = len(Ks)
+        self.D = D
+        self.dims = [int(K.shape[0]) for K in Ks]
+        self._K = [_fortran(K) for K in Ks]
+        self._M = [_fortran(M) for M in Ms]
+        n = (ctypes.c_int32 * D)(*self.dims)
+        Kp = (ctypes.c_void_p * D)(*[k.ctypes.data for k in self._K])
+        Mp = (ctypes.c_void_p * D)(*[m.ctypes.data for m in self._M])
+        c = (ctypes.c_double * D)(*[float(x) for x in coef])
+        h = ctypes.c_void_p()
+        _check(lib.fd_setup(D, n, Kp, Mp, c, device, max_batch, ctypes.byref(h)))
+        self.h = h
+        self.N = int(lib.fd_size(h))
+        self.device = device
+
+    def workspace_bytes(self, batch: int) -> int:
+        return int(lib.fd_workspace_bytes(self.h, batch))
+
+    def get_eigs(self, d: int):
+        n = self.dims[d]
+        U = np.zeros((n, n), order="F")
+        lam = np.zeros(n)
+        _check(lib.fd_get_eigs(self.h, d, _ptr(U), _ptr(lam)))
+        return lam, U
+
+    def apply(self, b, x=None, dscale=None, batch: int = 1, workspace=None, stream=None):
+        import torch
+        if x is None:
+            x = torch.empty_like(b)
+        numel = self.N * batch
+        ws = None
+        if workspace is None:
+            workspace = torch.empty(numel, dtype=torch.float64, device=b.device)
+        ws = _dev(workspace, "workspace", numel)
+        _check(lib.fd_apply(self.h, _dev(b, "b", numel), _dev(x, "x", numel),
+                            None if dscale is None else _dev(dscale, "dscale", self.N), batch, ws,
+                            _stream(stream)))
+        return x
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.fd_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class KronMass:
+    """kron_mass_setup / kron_mass_apply: P_Q = M_D (x) .. (x) M_1 and its inverse."""
+
+    def __init__(self, Ms, device: int = 0):
+        D = len(Ms)
+        self.D = D
+        self.dims = [int(M.shape[0]) for M in Ms]
+        self._M = [_fortran(M) for M in Ms]
+        n = (ctypes.c_int32 * D)(*self.dims)
+        Mp = (ctypes.c_void_p * D)(*[m.ctypes.data for m in self._M])
+        h = ctypes.c_void_p()
+        _check(lib.kron_mass_setup(D, n, Mp, device, ctypes.byref(h)))
+        self.h = h
+        self.N = int(lib.kron_mass_size(h))
+        self.device = device
+
+    def apply(self, b, x=None, mode: int = FDP_MASS_INVERSE, dscale=None, batch: int = 1, stream=None):
+        import torch
+        if x is None:
+            x = torch.empty_like(b)
+        numel = self.N * batch
+        _check(lib.kron_mass_apply(self.h, mode, _dev(b, "b", numel), _dev(x, "x", numel),
+                                   None if dscale is None else _dev(dscale, "dscale", self.N),
+                                   batch, _stream(stream)))
+        return x
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.kron_mass_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class BlockPrecond:
+    """block_precond_setup / _apply: P_D^{-1} r (or (P_D^G)^{-1} r).
+
+    Owns its FD / KronMass sub-handles (kept alive for the block's lifetime)."""
+
+    def __init__(self, fds, mass, dscale_vel=None, dscale_pres=None):
+        D = len(fds)
+        self.D = D
+        self.fds = list(fds)
+        self.mass = mass
+        hv = (ctypes.c_void_p * D)(*[f.h.value for f in fds])
+        self._dv = None if dscale_vel is None else _host(dscale_vel)
+        self._dq = None if dscale_pres is None else _host(dscale_pres)
+        h = ctypes.c_void_p()
+        _check(lib.block_precond_setup(D, hv, mass.h, None if self._dv is None else _ptr(self._dv),
+                                       None if self._dq is None else _ptr(self._dq), ctypes.byref(h)))
+        self.h = h
+        self.size = int(lib.block_precond_size(h))
+        self.sizes = [f.N for f in fds] + [mass.N]
+        self.device = mass.device
+
+    def workspace_bytes(self, batch: int = 1) -> int:
+        return int(lib.block_precond_workspace_bytes(self.h, batch))
+
+    def workspace(self, batch: int = 1):
+        import torch
+        return torch.empty(max(1, self.workspace_bytes(batch) // 8), dtype=torch.float64,
+                           device=f"cuda:{self.device}")
+
+    def launch_count(self, batch: int = 1) -> int:
+        return int(lib.fdp_block_launch_count(self.h, batch))
+
+    def apply(self, r, s=None, batch: int = 1, workspace=None, stream=None):
+        import torch
+        if s is None:
+            s = torch.empty_like(r)
+        if workspace is None:
+            workspace = self.workspace(batch)
+        numel = self.size * batch
+        _check(lib.block_precond_apply(self.h, _dev(r, "r", numel), _dev(s, "s", numel), batch,
+                                       _dev(workspace, "workspace", self.workspace_bytes(batch) // 8),
+                                       _stream(stream)))
+        return s
+
+    def apply_host(self, r_host: np.ndarray, s_host: np.ndarray, batch: int = 1, stream=None):
+        """End-to-end call with host buffers (H2D, apply, D2H, stream sync inside libfdp)."""
+        if r_host.dtype != np.float64 or s_host.dtype != np.float64:
+            raise TypeError("apply_host: float64 buffers required")
+        if not (r_host.flags.c_contiguous and s_host.flags.c_contiguous):
+            raise TypeError("apply_host: contiguous buffers required")
+        _check(lib.block_precond_apply_host(self.h, ctypes.c_void_p(r_host.ctypes.data),
+                                            ctypes.c_void_p(s_host.ctypes.data), batch, _stream(stream)))
+        return s_host
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.block_precond_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ----------------------------------------------------------------------------------------------
+# discretization (product side; built from libfdp's own univariate assembly)
+# ----------------------------------------------------------------------------------------------
+@dataclass
+class Discretization:
+    D: int
+    disc: str
+    p: int
+    n_el: int
+    Ks: list = field(default_factory=list)     # per component: list of D factors (direction d)
+    Ms: list = field(default_factory=list)
+    coef: list = field(default_factory=list)
+    grev: list = field(default_factory=list)
+    Mq: list = field(default_factory=list)
+    grev_q: list = field(default_factory=list)
+
+    @property
+    def comp_dims(self):
+        return [[K.shape[0] for K in Kc] for Kc in self.Ks]
+
+    @property
+    def q_dims(self):
+        return [M.shape[0] for M in self.Mq]
+
+    @property
+    def sizes(self):
+        return [int(np.prod(d)) for d in self.comp_dims] + [int(np.prod(self.q_dims))]
+
+    @property
+    def n_total(self):
+        return int(sum(self.sizes))
+
+
+def discretization(D: int, disc: str, p: int, n_el: int) -> Discretization:
+    """Pencils of P_V,k and P_Q with alpha = p-1, C_pen = 5p.
+
+    TH: velocity degree p+1 interior in every direction, c_d = 1 + [d = k].
+    RT component k: degree p+1 / regularity p interior in direction k; degree p full with the
+    Nitsche K~ elsewhere."""
+    a = p - 1
+    out = Discretization(D, disc, p, n_el)
+    if disc == "TH":
+        K, M = iga_univariate(p + 1, a, n_el, FDP_IGA_INTERIOR)
+        g = iga_greville(p + 1, a, n_el, FDP_IGA_INTERIOR)
+        for k in range(D):
+            out.Ks.append([K] * D)
+            out.Ms.append([M] * D)
+            out.coef.append([1.0 + (d == k) for d in range(D)])
+            out.grev.append([g] * D)
+    elif disc == "RT":
+        Kn, Mn = iga_univariate(p + 1, a + 1, n_el, FDP_IGA_INTERIOR)
+        Kt, Mt = iga_univariate(p, a, n_el, FDP_IGA_NITSCHE, 5.0 * p)
+        gn = iga_greville(p + 1, a + 1, n_el, FDP_IGA_INTERIOR)
+        gt = iga_greville(p, a, n_el)
+        for k in range(D):
+            out.Ks.append([Kn if d == k else Kt for d in range(D)])
+            out.Ms.append([Mn if d == k else Mt for d in range(D)])
+            out.coef.append([1.0 + (d == k) for d in range(D)])
+            out.grev.append([gn if d == k else gt for d in range(D)])
+    else:
+        raise ValueError(disc)
+    _, Mq = iga_univariate(p, a, n_el)
+    out.Mq = [Mq] * D
+    out.grev_q = [iga_greville(p, a, n_el)] * D
+    return out
+
+
+def _grid(f, grevs):
+    G = np.meshgrid(*grevs, indexing="ij")
+    return np.reshape(f(*G), -1, order="F")
+
+
+def nu_scalings(d: Discretization, nu):
+    """Config 3: D_V = nu at velocity dof Greville points, D_Q = 1/nu at pressure dofs (C-6)."""
+    dv = np.concatenate([_grid(nu, g) for g in d.grev])
+    dq = 1.0 / _grid(nu, d.grev_q)
+    return dv, dq
+
+
+def build_block(d: Discretization, device: int = 0, dscale_vel=None, dscale_pres=None) -> BlockPrecond:
+    fds = [FD(d.Ks[k], d.Ms[k], d.coef[k], device=device) for k in range(d.D)]
+    mass = KronMass(d.Mq, device=device)
+    return BlockPrecond(fds, mass, dscale_vel, dscale_pres)

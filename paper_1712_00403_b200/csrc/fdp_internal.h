@@ -1,0 +1,114 @@
+// Internal declarations shared by the host (C++) and device (CUDA) translation units of libfdp.
+// Nothing here crosses the C ABI (include/fdp.h).
+#pragma once
+
+#include <cstdint>
+#include <cstddef>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/fdp.h"
+
+namespace fdp {
+
+// ---------------------------------------------------------------------------------------------
+// Mode-d contraction (PAPER.md P:389-398 m-mode product; Algorithm 1 steps 2/4).
+// The tensor is viewed as (P, n, Q): element (p, k, q) at p + P*(k + n*q), i1 fastest, with the
+// batch folded into Q. Output Y(p, a, q) = sum_k X(p, k, q) * W[k*ldw + a].
+//   forward transform  (x_d U_d^T): W[k][a] = U_d[k][a]
+//   backward transform (x_d U_d)  : W[k][a] = U_d[a][k]
+// Flattened GEMM rows m = p + P*q; "KMAJ" (P == 1, mode 1) rows are contiguous along k.
+// ---------------------------------------------------------------------------------------------
+enum Epilogue : int {
+  EPI_NONE = 0,
+  EPI_LAMBDA = 1,  // divide by Lambda[i] = lamrow(p) + lamcol[a]   (Algorithm 1 step 3)
+  EPI_SCALE = 2,   // multiply by dscale[index within item]           (P^G post-scaling)
+};
+
+struct ModeProb {
+  const double* X;
+  double* Y;
+  const double* W;        // kpad x ldw row-major, zero padded
+  const double* scale;    // EPI_SCALE: length N (one batch item)
+  const double* lam0;     // EPI_LAMBDA: coef-scaled eigenvalues c_d*lambda_d, d = 1 (index i1)
+  const double* lam1;     //             d = 2 (3D only; nullptr in 2D)
+  const double* lamcol;   //             d = D (the contracted, last direction)
+  long long N;            // elements per batch item (of this tensor)
+  long long xbs, ybs;     // batch-item strides of X and Y (elements)
+  int P, n, Q;            // per item; GEMM rows M = P * Q * batch
+  int batch;
+  int ldw;
+  int n1;                 // size of direction 1 (Lambda row decomposition in 3D)
+  int epi;
+  int tiles_m, tiles_n;
+  int cta_begin;          // first CTA of this problem in the grouped grid
+};
+
+constexpr int kMaxGroup = 4;
+struct ModeGroup {
+  ModeProb prob[kMaxGroup];
+  int count;
+  int total_ctas;
+};
+
+// Tile configuration chosen for a problem size n (same for all problems of one launch).
+struct TileCfg {
+  int MT;      // m8 tiles per warp (warps stacked along M: BM = 4*8*MT)
+  int NT;      // n8 tiles per warp (BN = 8*NT)
+  int tiles_n; // ceil(n / BN)
+  int ldw;     // tiles_n * BN
+  int kpad;    // round_up(n, 16)
+};
+TileCfg choose_tile(int n);
+
+// Launch one grouped mode-contraction stage. kmaj: P == 1 for every problem (mode 1).
+cudaError_t launch_mode_group(const ModeGroup& g, const TileCfg& cfg, bool kmaj, cudaStream_t s);
+
+// y[b*ys + i] = x[b*xs + i] * s[i], i < N  (P^G pre-scaling), over `batch` items.
+cudaError_t launch_scale(const double* x, double* y, const double* s, long long N, long long batch,
+                         long long xs, long long ys, cudaStream_t st);
+// Set the dynamic shared-memory attribute of the kernels a tile config uses (call outside capture).
+cudaError_t prepare_mode_kernels(const TileCfg& cfg);
+
+// ---------------------------------------------------------------------------------------------
+// Banded Kronecker mass solve: per mode, along every fiber of the (P, n, Q) view,
+// forward substitution with the banded Cholesky factor L then back substitution with L^T.
+// Lb[i*(b+1) + j] = L[i][i-b+j] (j = b is the diagonal, entries with i-b+j < 0 are 0);
+// invd[i] = 1/L[i][i]. pre/post: optional scale vectors (length N = P*n*Q/batch) applied on the
+// first read / last write.
+// ---------------------------------------------------------------------------------------------
+struct MassMode {
+  const double* in;
+  double* out;
+  const double* Lb;
+  const double* invd;
+  const double* Mb;       // FORWARD: band of M, Mb[i*(2b+1) + (j-i+b)] = M[i][j]
+  const double* pre;
+  const double* post;
+  long long N;            // elements per batch item
+  long long bs;           // batch-item stride of in/out (elements)
+  int P, n, Q, batch;
+  int band;
+  int forward;            // 1: y = M x along fibers (FDP_MASS_FORWARD)
+};
+cudaError_t launch_mass_mode(const MassMode& m, cudaStream_t s);
+
+// ---------------------------------------------------------------------------------------------
+// Host numerics (host_eig.cpp, host_iga.cpp): own implementations, no LAPACK.
+// ---------------------------------------------------------------------------------------------
+// Generalized symmetric-definite eigenproblem K U = M U diag(lam), U^T M U = I.
+// Column-major n x n. Returns 0, or FDP_ERR_NOT_SPD / FDP_ERR_SINGULAR-like codes.
+int gen_eig(int n, const double* K, const double* M, double* U, double* lam, std::string* err);
+// Banded Cholesky of a symmetric positive definite column-major matrix with half bandwidth b.
+int band_cholesky(int n, int b, const double* M, std::vector<double>* Lb, std::vector<double>* invd,
+                  std::string* err);
+int detect_bandwidth(int n, const double* M);
+
+int iga_build(int deg, int alpha, int n_el, int flags, double c_pen, int q, double* K, double* M,
+              int* n_out, std::string* err);
+int iga_greville_build(int deg, int alpha, int n_el, int flags, double* g, int* n_out,
+                       std::string* err);
+
+}  // namespace fdp

@@ -1,0 +1,306 @@
+// K1: mode-d contraction on FP64 tensor cores (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4 on
+// sm_100a; tcgen05 has no f64 kind, DESIGN.md §"FP64 tensor cores").
+//
+// Implements one stage of Algorithm 1 steps 2 and 4: the m-mode product
+// of P:389-398 against an n x n eigenvector matrix, for up to kMaxGroup independent problems
+// (velocity components / batch) in one grouped launch. Optional fused epilogues: division by the
+// Kronecker-sum spectrum Lambda (step 3) and the P^G post-scaling D^{-1/2}.
+//
+// CTA tile: BM = 4 warps x (8*MT) rows  by  BN = 8*NT columns, K in chunks of BK = 16 through a
+// STAGES-deep cp.async ring in shared memory. Each warp owns MT x NT DMMA accumulators (FP64
+// registers). Shared-memory strides are == 4 (mod 16) doubles so the 8x4 / 4x8 fragment loads
+// are bank-conflict free.
+#include "../fdp_internal.h"
+
+namespace fdp {
+namespace {
+
+constexpr int BK = 16;
+constexpr int STAGES = 3;
+constexpr int WARPS = 4;
+constexpr int THREADS = WARPS * 32;
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int sz = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+template <int MT, int NT, bool KMAJ>
+struct Smem {
+  static constexpr int BM = WARPS * 8 * MT;
+  static constexpr int BN = 8 * NT;
+  static constexpr int SA = KMAJ ? (BK + 4) : (BM + 4);      // KMAJ: [BM][SA]; else [BK][SA]
+  static constexpr int A_ELEMS = KMAJ ? BM * SA : BK * SA;
+  static constexpr int SB = ((BN + 15) / 16) * 16 + 4;       // [BK][SB]
+  static constexpr int B_ELEMS = BK * SB;
+  static constexpr int STAGE = A_ELEMS + B_ELEMS;
+  static constexpr size_t BYTES = sizeof(double) * STAGE * STAGES;
+};
+
+template <int MT, int NT, bool KMAJ>
+__global__ void __launch_bounds__(THREADS)
+mode_contract_kernel(const __grid_constant__ ModeGroup grp) {
+  using S = Smem<MT, NT, KMAJ>;
+  constexpr int BM = S::BM, BN = S::BN;
+  extern __shared__ __align__(16) double smem[];
+
+  // ---- which problem / tile ----
+  int pi = 0;
+#pragma unroll
+  for (int i = 1; i < kMaxGroup; ++i)
+    if (i < grp.count && (int)blockIdx.x >= grp.prob[i].cta_begin) pi = i;
+  const ModeProb& pb = grp.prob[pi];
+  const int t = blockIdx.x - pb.cta_begin;
+  const int tn = t % pb.tiles_n;
+  const int tm = t / pb.tiles_n;
+  const long long m0 = (long long)tm * BM;
+  const int n0 = tn * BN;
+  const long long M = (long long)pb.P * pb.Q * pb.batch;
+  const int P = pb.P, n = pb.n, ldw = pb.ldw;
+  const long long Pn = (long long)P * n;
+  const double* __restrict__ X = pb.X;
+  const double* __restrict__ W = pb.W;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  // ---- per-thread load assignments (fixed across the K loop) ----
+  // KMAJ: thread loads k = tid % 16 of rows m = tid/16 + 8*j, j < BM/8.
+  // else : thread loads row m = tid % BM for k = tid/BM + (THREADS/BM)*j.
+  constexpr int A_ROWS_PER_THREAD = KMAJ ? BM / 8 : 1;
+  long long a_off[A_ROWS_PER_THREAD];
+  bool a_ok[A_ROWS_PER_THREAD];
+  const int Qn = pb.Q;
+  if (KMAJ) {
+#pragma unroll
+    for (int j = 0; j < A_ROWS_PER_THREAD; ++j) {
+      long long m = m0 + tid / 16 + 8 * j;
+      a_ok[j] = m < M;
+      // P == 1: row m = q + Q*b at n*q + xbs*b, contiguous in k
+      a_off[j] = a_ok[j] ? (long long)n * (m % Qn) + pb.xbs * (m / Qn) : 0;
+    }
+  } else {
+    long long m = m0 + tid % BM;
+    a_ok[0] = m < M;
+    if (a_ok[0]) {
+      const long long p = m % P, r = m / P;
+      a_off[0] = p + Pn * (r % Qn) + pb.xbs * (r / Qn);
+    } else {
+      a_off[0] = 0;
+    }
+  }
+
+  auto load_stage = [&](int stage, int k0) {
+    double* As = smem + stage * S::STAGE;
+    double* Bs = As + S::A_ELEMS;
+    if (KMAJ) {
+      const int k = tid % 16;
+      const bool kv = (k0 + k) < n;
+#pragma unroll
+      for (int j = 0; j < A_ROWS_PER_THREAD; ++j) {
+        const int mr = tid / 16 + 8 * j;
+        const bool v = a_ok[j] && kv;
+        cp_async8(&As[mr * S::SA + k], X + (v ? a_off[j] + k0 + k : 0), v);
+      }
+    } else {
+      constexpr int KSTEP = THREADS / BM;  // rows of k handled per pass
+      const int mr = tid % BM;
+#pragma unroll
+      for (int kk = tid / BM; kk < BK; kk += KSTEP) {
+        const bool v = a_ok[0] && (k0 + kk) < n;
+        cp_async8(&As[kk * S::SA + mr], X + (v ? a_off[0] + (long long)P * (k0 + kk) : 0), v);
+      }
+    }
+    // B: BK rows x BN cols from W (always in bounds: W is kpad x ldw, zero padded).
+    constexpr int CHUNKS = BK * BN / 2;  // 16-byte chunks
+#pragma unroll
+    for (int c = tid; c < CHUNKS; c += THREADS) {
+      const int kr = c / (BN / 2), cc = (c % (BN / 2)) * 2;
+      cp_async16(&Bs[kr * S::SB + cc], W + (size_t)(k0 + kr) * ldw + n0 + cc);
+    }
+  };
+
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int KT = (n + BK - 1) / BK;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) load_stage(s, s * BK);
+    cp_async_commit();
+  }
+
+  const int fr = lane >> 2, fc = lane & 3;  // fragment row (0..7) / k or col index (0..3)
+  const int wm = warp * 8 * MT;
+
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nk = kt + STAGES - 1;
+      if (nk < KT) load_stage(nk % STAGES, nk * BK);
+      cp_async_commit();
+    }
+    const double* As = smem + (kt % STAGES) * S::STAGE;
+    const double* Bs = As + S::A_ELEMS;
+    const int kvalid = min(BK, n - kt * BK);
+#pragma unroll
+    for (int k4 = 0; k4 < BK; k4 += 4) {
+      if (k4 < kvalid) {
+        double a[MT], b[NT];
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+          const int mr = wm + 8 * i + fr;
+          a[i] = KMAJ ? As[mr * S::SA + k4 + fc] : As[(k4 + fc) * S::SA + mr];
+        }
+#pragma unroll
+        for (int j = 0; j < NT; ++j) b[j] = Bs[(k4 + fc) * S::SB + 8 * j + fr];
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+          for (int j = 0; j < NT; ++j) dmma(acc[i][j], a[i], b[j]);
+      }
+    }
+  }
+  cp_async_wait<0>();
+
+  // ---- epilogue: C[m][a], m = wm + 8i + fr, a = 8j + 2fc + {0,1} ----
+  const int epi = pb.epi;
+  double* __restrict__ Y = pb.Y;
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    const long long m = m0 + wm + 8 * i + fr;
+    if (m >= M) continue;
+    long long row_off;
+    long long sidx;  // index within the batch item (for EPI_SCALE)
+    double lrow = 0.0;
+    if (KMAJ) {
+      sidx = (long long)n * (m % Qn);
+      row_off = sidx + pb.ybs * (m / Qn);
+    } else {
+      const long long p = m % P, r = m / P;
+      sidx = p + Pn * (r % Qn);
+      row_off = sidx + pb.ybs * (r / Qn);
+      if (epi == EPI_LAMBDA) {
+        if (pb.lam1) {
+          lrow = pb.lam0[p % pb.n1] + pb.lam1[p / pb.n1];
+        } else {
+          lrow = pb.lam0[p];
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int a = n0 + 8 * j + 2 * fc + h;
+        if (a < n) {
+          double v = acc[i][j][h];
+          if (epi == EPI_LAMBDA) v = v / (lrow + pb.lamcol[a]);
+          else if (epi == EPI_SCALE) v = v * pb.scale[sidx + (long long)P * a];
+          Y[row_off + (long long)P * a] = v;
+        }
+      }
+    }
+  }
+}
+
+template <int MT, int NT, bool KMAJ>
+cudaError_t launch_t(const ModeGroup* g, cudaStream_t s) {
+  using S = Smem<MT, NT, KMAJ>;
+  if (!g)  // prepare: raise the dynamic shared-memory limit (outside any stream capture)
+    return cudaFuncSetAttribute(mode_contract_kernel<MT, NT, KMAJ>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES);
+  mode_contract_kernel<MT, NT, KMAJ><<<g->total_ctas, THREADS, S::BYTES, s>>>(*g);
+  return cudaGetLastError();
+}
+
+template <int MT, bool KMAJ>
+cudaError_t dispatch_nt(const ModeGroup* g, int NT, cudaStream_t s) {
+  switch (NT) {
+    case 1: return launch_t<MT, 1, KMAJ>(g, s);
+    case 2: return launch_t<MT, 2, KMAJ>(g, s);
+    case 3: return launch_t<MT, 3, KMAJ>(g, s);
+    case 4: return launch_t<MT, 4, KMAJ>(g, s);
+    case 5: return launch_t<MT, 5, KMAJ>(g, s);
+    case 6: return launch_t<MT, 6, KMAJ>(g, s);
+    case 7: return launch_t<MT, 7, KMAJ>(g, s);
+    case 8: return launch_t<MT, 8, KMAJ>(g, s);
+    case 9: return launch_t<MT, 9, KMAJ>(g, s);
+    case 10: return launch_t<MT, 10, KMAJ>(g, s);
+    case 11: return launch_t<MT, 11, KMAJ>(g, s);
+    case 12: return launch_t<MT, 12, KMAJ>(g, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace
+
+TileCfg choose_tile(int n) {
+  TileCfg c;
+  const int n8 = (n + 7) / 8;
+  int split = (n8 + 11) / 12;            // number of column tiles, each <= 12 n8-tiles
+  c.NT = (n8 + split - 1) / split;
+  c.tiles_n = (n8 + c.NT - 1) / c.NT;
+  c.MT = 2;
+  c.ldw = c.tiles_n * 8 * c.NT;
+  c.kpad = ((n + 15) / 16) * 16;
+  return c;
+}
+
+cudaError_t launch_mode_group(const ModeGroup& g, const TileCfg& cfg, bool kmaj, cudaStream_t s) {
+  if (g.total_ctas <= 0) return cudaSuccess;
+  if (cfg.MT != 2) return cudaErrorInvalidValue;
+  return kmaj ? dispatch_nt<2, true>(&g, cfg.NT, s) : dispatch_nt<2, false>(&g, cfg.NT, s);
+}
+
+cudaError_t prepare_mode_kernels(const TileCfg& cfg) {
+  if (cfg.MT != 2) return cudaErrorInvalidValue;
+  cudaError_t e = dispatch_nt<2, true>(nullptr, cfg.NT, 0);
+  if (e != cudaSuccess) return e;
+  return dispatch_nt<2, false>(nullptr, cfg.NT, 0);
+}
+
+// ---------------------------------------------------------------------------------------------
+// K2: streaming diagonal scaling y = x o s (period N over the batch), double2-vectorised when
+// aligned. HBM-bound: 24 B per element (read x, s (L2-resident across the batch), write y).
+// ---------------------------------------------------------------------------------------------
+namespace {
+__global__ void scale_kernel(const double* __restrict__ x, double* __restrict__ y,
+                             const double* __restrict__ s, long long N, long long total,
+                             long long xs, long long ys) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (; i < total; i += stride) {
+    const long long b = i / N, j = i - b * N;
+    y[b * ys + j] = x[b * xs + j] * s[j];
+  }
+}
+}  // namespace
+
+cudaError_t launch_scale(const double* x, double* y, const double* s, long long N, long long batch,
+                         long long xs, long long ys, cudaStream_t st) {
+  long long total = N * batch;
+  if (total == 0) return cudaSuccess;
+  int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+  scale_kernel<<<blocks, 256, 0, st>>>(x, y, s, N, total, xs, ys);
+  return cudaGetLastError();
+}
+
+}  // namespace fdp

@@ -1,0 +1,179 @@
+"""GPU parity: libfdp (through the C ABI via the thin binding) vs the CPU oracle, element by
+element on the same seeded inputs. Tolerance: relative L2 <= 1e-9 (BASELINE.json north_star);
+expected ~1e-14 (two different eigensolvers, FP64 throughout)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_1712_00403_b200 as fdp  # noqa: E402
+import synth  # noqa: E402
+from oracle import fd as ofd  # noqa: E402
+from oracle import mass as omass  # noqa: E402
+from oracle import precond as oprec  # noqa: E402
+from oracle import spaces as ospaces  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def _rand_spd(n, rng, shift):
+    A = rng.standard_normal((n, n))
+    return A @ A.T + shift * n * np.eye(n)
+
+
+@pytest.mark.parametrize("dims,coef,batch", [
+    ((37, 70, 19), (2.0, 1.0, 1.0), 3),      # ragged in every mode, several tiles
+    ((5, 33, 100), (1.0, 2.0, 1.0), 2),
+    ((133, 9, 17), (1.0, 1.0, 2.0), 1),
+    ((150, 67), (2.0, 1.0), 4),             # 2D, two column tiles in mode 1
+    ((1, 7, 3), (1.0, 1.0, 1.0), 2),        # degenerate extent 1
+    ((96, 96, 2), (0.5, 1.5, 3.0), 1),
+])
+def test_fd_apply_random_pencils(dims, coef, batch):
+    rng = np.random.default_rng(sum(dims) + batch)
+    Ks = [_rand_spd(n, rng, 1.0) for n in dims]
+    Ms = [_rand_spd(n, rng, 2.0) for n in dims]
+    N = int(np.prod(dims))
+    b = rng.standard_normal((batch, N))
+    S = fdp.FD(Ks, Ms, coef)
+    x = S.apply(dev(b), batch=batch).cpu().numpy()
+    ref = ofd.FDSolver(Ks, Ms, coef)
+    for i in range(batch):
+        assert rel(x[i], ref.apply(b[i])) < TOL
+
+
+def test_fd_apply_dscale_and_inplace():
+    d = ospaces.build(3, "RT", 2, 6)
+    c = d.comps[1]
+    rng = np.random.default_rng(5)
+    N = c.size
+    b = rng.standard_normal(N)
+    dsc = rng.uniform(0.5, 1.5, N)
+    S = fdp.FD(c.Ks, c.Ms, c.coef)
+    bt = dev(b)
+    S.apply(bt, bt, dscale=dev(1.0 / np.sqrt(dsc)))  # in place
+    ref = ofd.scaled_apply(ofd.FDSolver(c.Ks, c.Ms, c.coef), b, dsc)
+    assert rel(bt.cpu().numpy(), ref) < TOL
+
+
+def test_kron_mass_inverse_and_forward():
+    rng = np.random.default_rng(8)
+    from oracle import univariate
+    Ms = [univariate.pressure_mass(3, 5), univariate.pressure_mass(3, 7), univariate.pressure_mass(3, 4)]
+    km = omass.KronMass(Ms)
+    N = int(np.prod(km.dims))
+    b = rng.standard_normal((2, N))
+    K = fdp.KronMass(Ms)
+    x = K.apply(dev(b), batch=2).cpu().numpy()
+    y = K.apply(dev(b), mode=fdp.FDP_MASS_FORWARD, batch=2).cpu().numpy()
+    dq = rng.uniform(0.5, 2.0, N)
+    z = K.apply(dev(b), dscale=dev(1 / np.sqrt(dq)), batch=2).cpu().numpy()
+    for i in range(2):
+        assert rel(x[i], km.inverse(b[i])) < TOL
+        assert rel(y[i], km.forward(b[i])) < 1e-13
+        assert rel(z[i], km.scaled_inverse(b[i], dq)) < TOL
+
+
+def _both(cfg_id):
+    w = synth.CONFIGS[cfg_id]
+    od = ospaces.build(w.dim, w.disc, w.p, w.n_el)
+    gd = fdp.discretization(w.dim, w.disc, w.p, w.n_el)
+    return w, od, gd
+
+
+@pytest.mark.parametrize("cfg_id", [1, 2, 3])
+def test_block_precond_configs(cfg_id):
+    w, od, gd = _both(cfg_id)
+    assert gd.comp_dims == [c.dims for c in od.comps] and gd.q_dims == od.q_dims
+    r = synth.rhs(w.seed, od.n_total, w.batch)
+    dv = dq = None
+    if w.variable_nu:
+        dv, dq = ospaces.nu_scalings(od, synth.viscosity)
+        gdv, gdq = fdp.nu_scalings(gd, synth.viscosity)
+        assert np.max(np.abs(gdv - dv)) < 1e-14 and np.max(np.abs(gdq - dq)) < 1e-14
+    P = fdp.build_block(gd, dscale_vel=dv, dscale_pres=dq)
+    s = P.apply(dev(r), batch=w.batch).cpu().numpy()
+    ref = oprec.BlockPrecond(od, dv, dq).apply(r)
+    o = od.offsets()
+    for i in range(w.batch):
+        for k in range(len(o) - 1):
+            assert rel(s[i, o[k]:o[k + 1]], ref[i, o[k]:o[k + 1]]) < TOL, (cfg_id, k)
+
+
+def test_block_precond_plain_vs_scaled_config3():
+    # P_D (no scaling) on the RT config too, and in-place application with batch 2
+    w, od, gd = _both(3)
+    r = synth.rhs(7, od.n_total, 2)
+    P = fdp.build_block(gd)
+    rt = dev(r)
+    ws = P.workspace(2)
+    P.apply(rt, rt, batch=2, workspace=ws)
+    ref = oprec.BlockPrecond(od).apply(r)
+    assert rel(rt.cpu().numpy(), ref) < TOL
+
+
+def test_graph_replay_and_host_e2e():
+    w, od, gd = _both(1)
+    P = fdp.build_block(gd)
+    rng = np.random.default_rng(3)
+    ref = oprec.BlockPrecond(od)
+    r1 = dev(rng.standard_normal(od.n_total))
+    s1 = torch.empty_like(r1)
+    ws = P.workspace(1)
+    P.apply(r1, s1, workspace=ws)
+    # same pointers -> graph replay with new contents
+    r_new = rng.standard_normal(od.n_total)
+    r1.copy_(dev(r_new))
+    P.apply(r1, s1, workspace=ws)
+    assert rel(s1.cpu().numpy(), ref.apply(r_new)) < TOL
+    # host end-to-end path
+    rh = rng.standard_normal(od.n_total)
+    sh = np.zeros_like(rh)
+    P.apply_host(rh, sh)
+    assert rel(sh, ref.apply(rh)) < TOL
+
+
+def test_errors_are_reported():
+    w, od, gd = _both(1)
+    P = fdp.build_block(gd)
+    rh = np.zeros(od.n_total)
+    with pytest.raises(fdp.FdpError) as e:
+        import ctypes
+        fdp._check(fdp.lib.block_precond_apply(P.h, ctypes.c_void_p(rh.ctypes.data),
+                                               ctypes.c_void_p(rh.ctypes.data), 1,
+                                               ctypes.c_void_p(rh.ctypes.data), None))
+    assert e.value.status == 1  # FDP_ERR_INVALID_ARG: host pointer where device required
+    # batch = 0 is a no-op
+    fdp._check(fdp.lib.block_precond_apply(P.h, None, None, 0, None, None))
+
+
+def test_fd_eigs_match_oracle_spectrum():
+    K, M = fdp.iga_univariate(6, 4, 128, fdp.FDP_IGA_INTERIOR)
+    S = fdp.FD([K, K, K], [M, M, M], (2, 1, 1))
+    lam, U = S.get_eigs(0)
+    lo, _ = ofd.gen_eig(K, M)
+    assert np.max(np.abs(lam - lo)) / lo.max() < 1e-13
+    assert np.max(np.abs(U.T @ M @ U - np.eye(len(lam)))) < 1e-11
+
+
+@pytest.mark.slow
+def test_block_precond_config4_full_size_bench_launch():
+    """Config 4 at full size in the bench launch configuration (batch 8 in one call); items 0 and
+    7 compared with the oracle element by element."""
+    w, od, gd = _both(4)
+    r = synth.rhs(w.seed, od.n_total, w.batch)
+    P = fdp.build_block(gd)
+    s = P.apply(dev(r), batch=w.batch)
+    ref = oprec.BlockPrecond(od)
+    for i in (0, w.batch - 1):
+        si = s[i].cpu().numpy()
+        assert rel(si, ref.apply(r[i])) < TOL

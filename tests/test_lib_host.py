@@ -1,0 +1,112 @@
+"""CPU-side checks of libfdp: the shared library loads, exports every symbol include/fdp.h
+declares, and its host numerics (univariate assembly, Greville points, generalized eigensolver)
+agree with the oracle. No compute kernels run here."""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import paper_1712_00403_b200 as fdp
+from oracle import fd as ofd
+from oracle import splines, univariate
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "fdp.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"^\s*(?:const\s+)?[\w\s\*]+?\b(\w+)\s*\(", src, flags=re.M)
+    return sorted(set(n for n in names if n not in ("if", "defined")))
+
+
+def test_header_symbols_exported():
+    out = subprocess.run(["nm", "-D", "--defined-only", fdp.LIB_PATH], capture_output=True, text=True,
+                         check=True).stdout
+    exported = set(l.split()[-1] for l in out.splitlines() if " T " in l)
+    declared = _declared()
+    assert len(declared) >= 20
+    missing = [n for n in declared if n not in exported]
+    assert not missing, missing
+
+
+def test_status_strings_and_version():
+    assert fdp.lib.fdp_status_string(0) == b"FDP_OK"
+    assert fdp.lib.fdp_status_string(4) == b"FDP_ERR_SINGULAR"
+    assert b"sm_100a" in fdp.lib.fdp_version()
+
+
+@pytest.mark.parametrize("deg,alpha,n_el,flags", [(3, 1, 16, 1), (4, 2, 32, 1), (5, 4, 64, 1),
+                                                   (4, 3, 64, 0), (6, 4, 20, 1), (2, 0, 5, 0), (1, 0, 3, 1)])
+def test_iga_univariate_matches_oracle(deg, alpha, n_el, flags):
+    K, M = fdp.iga_univariate(deg, alpha, n_el, flags)
+    Ko, Mo = univariate.stiffness_mass(deg, alpha, n_el)
+    if flags & 1:
+        Ko, Mo = univariate.interior(Ko), univariate.interior(Mo)
+    assert K.shape == Ko.shape
+    assert np.max(np.abs(K - Ko)) <= 1e-13 * np.max(np.abs(Ko))
+    assert np.max(np.abs(M - Mo)) <= 1e-13 * np.max(np.abs(Mo))
+
+
+@pytest.mark.parametrize("p,n_el", [(1, 1), (2, 4), (4, 64), (4, 512)])
+def test_iga_nitsche_matches_oracle(p, n_el):
+    K, M = fdp.iga_univariate(p, p - 1, n_el, fdp.FDP_IGA_NITSCHE, 5.0 * p)
+    Ko = univariate.nitsche_stiffness(p, p - 1, n_el, univariate.c_pen(p))
+    assert np.max(np.abs(K - Ko)) <= 1e-13 * np.max(np.abs(Ko))
+
+
+def test_greville_matches_oracle():
+    for deg, a, n, fl in [(4, 2, 8, 1), (4, 3, 8, 0), (5, 4, 6, 1)]:
+        g = fdp.iga_greville(deg, a, n, fl)
+        go = splines.greville(splines.open_uniform_knots(deg, a, n), deg)
+        if fl:
+            go = go[1:-1]
+        assert np.allclose(g, go, rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("pencil", ["th65", "rt_t68", "rt_n67", "q35"])
+def test_gen_eig_matches_oracle(pencil):
+    K, M = {"th65": lambda: univariate.th_velocity_pencil(3, 32),
+            "rt_t68": lambda: univariate.rt_tangential_pencil(4, 64),
+            "rt_n67": lambda: univariate.rt_normal_pencil(4, 64),
+            "q35": lambda: univariate.stiffness_mass(3, 2, 32)}[pencil]()
+    lam, U = fdp.gen_eig(K, M)
+    lo, _ = ofd.gen_eig(K, M)
+    assert np.max(np.abs(lam - lo) / np.abs(lo).max()) < 1e-13
+    assert np.max(np.abs(U.T @ M @ U - np.eye(len(lam)))) < 1e-12
+    assert np.max(np.abs(K @ U - M @ U * lam)) < 1e-11 * np.abs(lo).max()
+
+
+def test_gen_eig_rejects_non_spd():
+    with pytest.raises(fdp.FdpError) as e:
+        fdp.gen_eig(np.eye(3), -np.eye(3))
+    assert e.value.status == 3  # FDP_ERR_NOT_SPD
+
+
+def test_setup_argument_errors_without_gpu():
+    h = ctypes.c_void_p()
+    n = (ctypes.c_int32 * 4)(2, 2, 2, 2)
+    assert fdp.lib.fd_setup(4, n, None, None, None, 0, 0, ctypes.byref(h)) == 8   # UNSUPPORTED
+    assert fdp.lib.fd_setup(3, None, None, None, None, 0, 0, ctypes.byref(h)) == 1  # INVALID_ARG
+    n0 = (ctypes.c_int32 * 3)(0, 2, 2)
+    K = np.eye(2)
+    Kp = (ctypes.c_void_p * 3)(*[K.ctypes.data] * 3)
+    c = (ctypes.c_double * 3)(1, 1, 1)
+    assert fdp.lib.fd_setup(3, n0, Kp, Kp, c, 0, 0, ctypes.byref(h)) == 2         # SHAPE
+    assert fdp.lib.kron_mass_setup(1, n0, Kp, 0, ctypes.byref(h)) == 8
+    assert fdp.lib.iga_univariate(0, 0, 1, 0, 0.0, 0, None, None, ctypes.byref(ctypes.c_int32())) == 2
+
+
+def test_discretization_matches_oracle_sizes():
+    import synth
+    from oracle import spaces
+    for cid in (1, 2, 3):
+        w = synth.CONFIGS[cid]
+        g = fdp.discretization(w.dim, w.disc, w.p, w.n_el)
+        o = spaces.build(w.dim, w.disc, w.p, w.n_el)
+        assert g.comp_dims == [c.dims for c in o.comps]
+        assert g.n_total == o.n_total
+        assert g.coef == [c.coef for c in o.comps]
