@@ -1,0 +1,382 @@
+#!/usr/bin/env python
+"""Benchmark of the FD block-preconditioner application (BASELINE.json metric: preconditioner
+applications/s and DOF/s in FP64, % of the FP64 tensor-core roofline).
+
+One step = one block_precond_apply (P_D^{-1} r, or (P_D^G)^{-1} r for config 3) over one batch of
+synthetic RHS already resident in HBM: the whole hot path. Default workload
+= BASELINE.json configs[1] (config 2: 3D Taylor-Hood p=3, 32^3 elements). --config selects others.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl {fdp,reference}]
+
+N > 1 runs under torchrun, one rank per GPU. Configs 1-3 have no natural sharding ("replicas
+only": each rank applies the preconditioner to its own RHS stream); config 4 shards its batch of
+8 RHS across ranks (weak in per-rank work only when 8 % N == 0; reported as "strong").
+--impl reference times the CPU oracle (the reference arm of this tier) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+PEAKS_FILE = os.path.join(ROOT, "profiles", "r01_fp64_peaks.json")
+L2_FLUSH_BYTES = 512 << 20  # > 126 MB L2
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--impl", default="fdp", choices=["fdp", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the oracle sample")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ----------------------------------------------------------------------------------------------
+# workload description (counts only; no method arithmetic beyond sizes)
+# ----------------------------------------------------------------------------------------------
+def workload_config(cid, w, n_total, batch_total, gpus, flush):
+    return {
+        "workload": w.name,
+        "config_index": cid,
+        "discretization": f"{w.dim}D {w.disc} pressure p={w.p}, velocity p={w.p + 1}, alpha=p-1, {w.n_el}^{w.dim} elements",
+        "preconditioner": "P_D^G (D_V=nu, D_Q=1/nu at dofs)" if w.variable_nu else "P_D",
+        "dofs_per_rhs": n_total,
+        "global_batch": batch_total,
+        "parallelism": ("batch-shard" if cid == 4 else "replicas") + f"x{gpus}",
+        "l2": flush,
+        "rhs": f"numpy default_rng(seed={w.seed}).standard_normal, FP64",
+    }
+
+
+def nvsmi_sampler(stop, out, dev):
+    q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+    while not stop.is_set():
+        try:
+            r = subprocess.run(["nvidia-smi", f"--id={dev}", f"--query-gpu={q}",
+                                "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                               timeout=5)
+            if r.returncode == 0 and r.stdout.strip():
+                out.append([x.strip() for x in r.stdout.strip().split(",")])
+        except Exception:
+            pass
+        stop.wait(0.2)
+
+
+def summarize_clocks(samples):
+    if not samples:
+        return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+    sm = [float(s[0]) for s in samples if s[0].replace(".", "").isdigit()]
+    mx = [float(s[1]) for s in samples if s[1].replace(".", "").isdigit()]
+    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    reasons = set()
+    for s in samples:
+        for nm, v in zip(names, s[3:7]):
+            if v.lower() == "active":
+                reasons.add(nm)
+    return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+            "reasons": sorted(reasons), "samples": len(samples)}
+
+
+# ----------------------------------------------------------------------------------------------
+# CPU oracle timing (cpu_baseline and --impl reference)
+# ----------------------------------------------------------------------------------------------
+def oracle_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        return max([i.get("num_threads", 1) for i in info] + [1])
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def oracle_sample(w, budget_s, max_steps=None):
+    """Time the oracle's block-preconditioner apply on this workload's RHS, one RHS per call,
+    for about budget_s seconds. Returns (applies/s, dofs/apply, n_calls, seconds, setup_s)."""
+    from oracle import precond, spaces
+    t0 = time.perf_counter()
+    od = spaces.build(w.dim, w.disc, w.p, w.n_el)
+    dv = dq = None
+    if w.variable_nu:
+        dv, dq = spaces.nu_scalings(od, synth.viscosity)
+    P = precond.BlockPrecond(od, dv, dq)
+    setup = time.perf_counter() - t0
+    r = synth.rhs(w.seed, od.n_total, 1)[0]
+    P.apply(r)  # warm
+    n, t = 0, 0.0
+    times = []
+    while (t < budget_s or n == 0) and (max_steps is None or n < max_steps):
+        a = time.perf_counter()
+        P.apply(r)
+        dt = time.perf_counter() - a
+        times.append(dt)
+        t += dt
+        n += 1
+    return n / t, od.n_total, n, t, setup, times
+
+
+def run_reference(args, w, cid):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    # each step = one oracle application to one RHS (bounded: the whole run stays within minutes)
+    steps, warm = args.steps, args.warmup
+    from oracle import precond, spaces
+    od = spaces.build(w.dim, w.disc, w.p, w.n_el)
+    dv = dq = None
+    if w.variable_nu:
+        dv, dq = spaces.nu_scalings(od, synth.viscosity)
+    P = precond.BlockPrecond(od, dv, dq)
+    r = synth.rhs(w.seed, od.n_total, 1)[0]
+    for _ in range(warm):
+        P.apply(r)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        P.apply(r)
+    dt = time.perf_counter() - t0
+    value = steps / dt
+    cores = oracle_threads()
+    line = {
+        "impl": "reference", "metric": "preconditioner_applications_per_s", "value": value,
+        "unit": "apply/s", "n_gpus": args.gpus, "steps": steps, "warmup": warm,
+        "ms_per_step": 1e3 * dt / steps, "higher_is_better": True, "scaling": "replicas",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "dof_per_s": value * od.n_total,
+        "config": workload_config(cid, w, od.n_total, 1, 1, "n/a (CPU)"),
+        "cpu_baseline": {"value": value, "unit": "apply/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{steps} oracle applications to one RHS of {w.name} (batch item 0)"},
+        "e2e": {"value": value, "unit": "apply/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------------------------
+# GPU arm
+# ----------------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    cid = args.config
+    w = synth.CONFIGS[cid]
+    if args.impl == "reference":
+        run_reference(args, w, cid)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_1712_00403_b200 as fdp
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+    torch.cuda.init()
+
+    # ---- setup (excluded from timing) ----
+    t0 = time.perf_counter()
+    gd = fdp.discretization(w.dim, w.disc, w.p, w.n_el)
+    dv = dq = None
+    if w.variable_nu:
+        dv, dq = fdp.nu_scalings(gd, synth.viscosity)
+    P = fdp.build_block(gd, device=dev, dscale_vel=dv, dscale_pres=dq)
+    setup_s = time.perf_counter() - t0
+    n_total = gd.n_total
+
+    # batch per rank: config 4 shards its 8 RHS across ranks; others replicate one RHS stream
+    if cid == 4:
+        items = list(range(rank, w.batch, world))
+        batch_total = w.batch
+    else:
+        items = list(range(w.batch))
+        batch_total = w.batch * world
+    batch = len(items)
+    if batch == 0:
+        raise SystemExit("more ranks than RHS for this config")
+    rhs_all = synth.rhs(w.seed + (rank if cid != 4 else 0), n_total, w.batch)
+    r_host = np.ascontiguousarray(rhs_all[items])
+    del rhs_all
+    r = torch.from_numpy(r_host).to(dev)
+    s = torch.empty_like(r)
+    ws = P.workspace(batch)
+    working_set = 2 * r.numel() * 8 + ws.numel() * 8
+    flush = working_set < 2 * (126 << 20)
+    flush_buf = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev) if flush else None
+    stream = torch.cuda.current_stream()
+
+    def step():
+        P.apply(r, s, batch=batch, workspace=ws, stream=stream)
+
+    # ---- warmup ----
+    for _ in range(max(args.warmup, 3)):
+        if flush:
+            flush_buf.zero_()
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region (device events per step; L2 flushed between steps when resident) ----
+    stop = threading.Event()
+    samples = []
+    th = threading.Thread(target=nvsmi_sampler, args=(stop, samples, dev), daemon=True)
+    th.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    wall0 = time.perf_counter()
+    for i in range(args.steps):
+        if flush:
+            flush_buf.zero_()
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    if world > 1:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    dev_ms = float(sum(step_ms))
+
+    # ---- per-launch roofline pass (events between launches, same graph path) ----
+    P.profile(True)
+    prof_runs = []
+    for i in range(max(3, min(args.steps, 20))):
+        if flush:
+            flush_buf.zero_()
+        step()
+        torch.cuda.synchronize()
+        if i >= 1:
+            prof_runs.append(P.profile_read())
+    P.profile(False)
+
+    # ---- end-to-end through the public host-buffer API (H2D + apply + D2H inside) ----
+    r_pin = torch.from_numpy(r_host).pin_memory().numpy()
+    s_pin = torch.empty(r_host.shape, dtype=torch.float64).pin_memory().numpy()
+    P.apply_host(r_pin, s_pin, batch=batch)
+    torch.cuda.synchronize()
+    e2e_steps = max(3, min(args.steps, 20))
+    if world > 1:
+        dist.barrier()
+    e0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        P.apply_host(r_pin, s_pin, batch=batch)
+    e2e_s = time.perf_counter() - e0
+    stop.set()
+    th.join(timeout=5)
+
+    # ---- reduce over ranks ----
+    stats = torch.tensor([dev_ms, e2e_s, wall], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(stats, op=dist.ReduceOp.MAX)
+    dev_ms_max, e2e_max, wall_max = [float(x) for x in stats.cpu()]
+    apps_total = batch_total * args.steps
+    value = apps_total / (dev_ms_max * 1e-3)
+    e2e_value = batch_total * e2e_steps / e2e_max
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # roofline of the dominant kernel (K1 mode contraction): algorithmic flops / event duration
+    peaks = json.load(open(PEAKS_FILE))
+    fp64_peak = peaks["dmma_tflops_w32"]
+    k1_ms = k1_fl = 0.0
+    k1_n = 0
+    tot_ms = 0.0
+    per_kind = {0: 0.0, 1: 0.0, 2: 0.0}
+    k3_ms = k3_by = 0.0
+    for run in prof_runs:
+        for kind, ms, fl, by in run:
+            tot_ms += ms
+            per_kind[kind] += ms
+            if kind == 0:
+                k1_ms += ms
+                k1_fl += fl
+                k1_n += 1
+            if kind == 2:
+                k3_ms += ms
+                k3_by += by
+    achieved = (k1_fl / (k1_ms * 1e-3)) / 1e12 if k1_ms > 0 else None
+    launches = P.launch_count(batch)
+    clocks = summarize_clocks(samples)
+    cpu = None
+    if not args.no_cpu_baseline:
+        os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
+        v, nd, n, t, setup_o, _ = oracle_sample(w, args.cpu_seconds)
+        cpu = {"value": v, "unit": "apply/s", "cores": oracle_threads(), "kind": "oracle",
+               "sample": f"{n} oracle applications (numpy/scipy FP64) to one RHS of {w.name} in {t:.1f} s; setup {setup_o:.2f} s excluded"}
+    line = {
+        "metric": "preconditioner_applications_per_s",
+        "value": value,
+        "unit": "apply/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": max(args.warmup, 3),
+        "ms_per_step": dev_ms_max / args.steps,
+        "higher_is_better": True,
+        "scaling": "strong" if cid == 4 else "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "dof_per_s": value * n_total,
+        "config": workload_config(cid, w, n_total, batch_total, world,
+                                  "flushed (512 MB write) before every timed step" if flush
+                                  else "working set > L2"),
+        "roofline": {
+            "bound": "tensor",
+            "kernel": "K1 mode_contract (FP64 mma.sync m8n8k4 -> DMMA)",
+            "achieved": achieved,
+            "peak": fp64_peak,
+            "unit": "TFLOP/s",
+            "frac": (achieved / fp64_peak) if achieved else None,
+            "traffic": None,
+            "peak_source": "measured all-SM DMMA register loop, profiles/r01_fp64_peaks.json (MEASURED_PEAKS.json has no FP64 entry)",
+            "k1_share_of_step": per_kind[0] / tot_ms if tot_ms else None,
+            "k1_launches_per_step": k1_n // max(1, len(prof_runs)),
+            "k3_mass_gbs": (k3_by / (k3_ms * 1e-3) / 1e9) if k3_ms else None,
+            "step_ms_profiled": tot_ms / max(1, len(prof_runs)),
+        },
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "apply/s",
+                "h2d_bytes_per_step": int(r_host.nbytes), "d2h_bytes_per_step": int(r_host.nbytes),
+                "api": "block_precond_apply_host (pinned host buffers, H2D+apply+D2H+sync)"},
+        "gpu_launches": launches * args.steps,
+        "clocks": clocks,
+        "setup_s": setup_s,
+        "wall_s_timed_region": wall_max,
+        "step_ms_p50": float(np.median(step_ms)),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

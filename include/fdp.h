@@ -166,6 +166,19 @@ fdp_status block_precond_destroy(fdp_block h);
 /* Number of kernel launches one block_precond_apply issues for `batch` (for accounting). */
 int fdp_block_launch_count(fdp_block h, int64_t batch);
 
+/* Per-launch timing of block_precond_apply (roofline diagnostics). With enable != 0 every later
+ * apply records a CUDA event on its stream before each kernel launch and after the last one (the
+ * events become nodes of the cached graph, which is re-captured when the flag changes).
+ * block_precond_profile_read fills, for the most recent apply, up to `max` entries: kind (0 = K1
+ * mode contraction, 1 = K2 diagonal scaling, 2 = K3 banded mass solve), elapsed milliseconds
+ * between the launch's start event and the next event, and the launch's ALGORITHMIC flops and
+ * DRAM bytes (flops 2*N*n_d per contracted element set; bytes = one read + one write of the
+ * tensor, plus scale vectors). Returns the number of launches (or -1 on error); call it after
+ * the apply's stream has been synchronised. Any array may be NULL. */
+fdp_status block_precond_profile(fdp_block h, int enable);
+int block_precond_profile_read(fdp_block h, int max, int32_t* kind, float* ms, double* flops,
+                               double* bytes);
+
 #ifdef __cplusplus
 }
 #endif

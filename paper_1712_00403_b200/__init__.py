@@ -64,6 +64,8 @@ def _load():
         "block_precond_apply_host": (i32, [vp, vp, vp, i64, vp]),
         "block_precond_destroy": (i32, [vp]),
         "fdp_block_launch_count": (i32, [vp, i64]),
+        "block_precond_profile": (i32, [vp, i32]),
+        "block_precond_profile_read": (i32, [vp, i32, vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -274,6 +276,21 @@ class BlockPrecond:
 
     def launch_count(self, batch: int = 1) -> int:
         return int(lib.fdp_block_launch_count(self.h, batch))
+
+    def profile(self, enable: bool = True):
+        _check(lib.block_precond_profile(self.h, 1 if enable else 0))
+
+    def profile_read(self):
+        """[(kind, ms, flops, bytes)] of the last apply (after a stream sync)."""
+        cap = 64
+        kind = np.zeros(cap, dtype=np.int32)
+        ms = np.zeros(cap, dtype=np.float32)
+        fl = np.zeros(cap)
+        by = np.zeros(cap)
+        n = lib.block_precond_profile_read(self.h, cap, _ptr(kind), _ptr(ms), _ptr(fl), _ptr(by))
+        if n < 0:
+            raise FdpError(5, "profile_read failed (profiling off or events not complete)")
+        return [(int(kind[i]), float(ms[i]), float(fl[i]), float(by[i])) for i in range(n)]
 
     def apply(self, r, s=None, batch: int = 1, workspace=None, stream=None):
         import torch

@@ -97,6 +97,33 @@ static bool symmetric(int n, const double* A) {
 }
 
 // ------------------------------------------------------------------------------------------------
+// per-launch profiling (events recorded on the launching stream, optionally into a graph)
+// ------------------------------------------------------------------------------------------------
+struct LaunchInfo {
+  int kind;      // 0 K1 mode contraction, 1 K2 scaling, 2 K3 mass
+  double flops;  // algorithmic
+  double bytes;  // algorithmic DRAM bytes
+};
+struct Recorder {
+  std::vector<cudaEvent_t>* ev = nullptr;
+  std::vector<LaunchInfo>* info = nullptr;
+  cudaStream_t s = nullptr;
+  cudaError_t before(int kind, double flops, double bytes) {
+    if (!ev) return cudaSuccess;
+    size_t i = info->size();
+    if (i >= ev->size()) return cudaErrorInvalidValue;
+    info->push_back({kind, flops, bytes});
+    return cudaEventRecordWithFlags((*ev)[i], s, cudaEventRecordExternal);
+  }
+  cudaError_t finish() {
+    if (!ev) return cudaSuccess;
+    size_t i = info->size();
+    if (i >= ev->size()) return cudaErrorInvalidValue;
+    return cudaEventRecordWithFlags((*ev)[i], s, cudaEventRecordExternal);
+  }
+};
+
+// ------------------------------------------------------------------------------------------------
 // host helpers
 // ------------------------------------------------------------------------------------------------
 extern "C" fdp_status iga_univariate(int deg, int alpha, int n_el, int flags, double c_pen, int q,
@@ -295,7 +322,7 @@ static ModeProb make_mode_prob(const fdp_fd_s* h, int d, bool fwd, const double*
 // Stage = one mode/direction for a set of FD problems. Problems with the same tile config share a
 // launch (up to kMaxGroup); others get their own.
 static cudaError_t launch_stage(std::vector<ModeProb>& probs, const std::vector<TileCfg>& cfgs,
-                                bool kmaj, cudaStream_t s, int* nlaunch) {
+                                bool kmaj, cudaStream_t s, int* nlaunch, Recorder* rec) {
   std::vector<bool> done(probs.size(), false);
   for (size_t i = 0; i < probs.size(); ++i) {
     if (done[i]) continue;
@@ -311,6 +338,17 @@ static cudaError_t launch_stage(std::vector<ModeProb>& probs, const std::vector<
       done[j] = true;
     }
     g.total_ctas = ctas;
+    if (rec) {
+      double fl = 0.0, by = 0.0;
+      for (int j = 0; j < g.count; ++j) {
+        const ModeProb& p = g.prob[j];
+        const double elems = (double)p.P * p.Q * p.batch * p.n;
+        fl += 2.0 * elems * p.n;
+        by += 16.0 * elems + (p.epi == EPI_SCALE ? 8.0 * p.N : 0.0);
+      }
+      cudaError_t e0 = rec->before(0, fl, by);
+      if (e0 != cudaSuccess) return e0;
+    }
     cudaError_t e = launch_mode_group(g, cfgs[i], kmaj, s);
     if (e != cudaSuccess) return e;
     if (nlaunch) ++*nlaunch;
@@ -327,7 +365,7 @@ static cudaError_t enqueue_fd(const std::vector<const fdp_fd_s*>& hs,
                               const std::vector<double*>& out, long long obs,
                               const std::vector<double*>& T,
                               const std::vector<const double*>& dscale, int64_t batch,
-                              cudaStream_t s, int* nlaunch) {
+                              cudaStream_t s, int* nlaunch, Recorder* rec = nullptr) {
   const int D = hs[0]->D;
   const size_t K = hs.size();
   // pass sequence: forward d = 0..D-1, backward d = D-1..0; 2D passes alternate T <- src, out <- T
@@ -352,7 +390,7 @@ static cudaError_t enqueue_fd(const std::vector<const fdp_fd_s*>& hs,
         probs.push_back(make_mode_prob(hs[k], d, fwd, src, sbs, dst, dbs, batch, epi, sc));
         cfgs.push_back(hs[k]->cfg[d]);
       }
-      cudaError_t e = launch_stage(probs, cfgs, d == 0, s, nlaunch);
+      cudaError_t e = launch_stage(probs, cfgs, d == 0, s, nlaunch, rec);
       if (e != cudaSuccess) return e;
       ++pass;
     }
@@ -474,7 +512,7 @@ extern "C" int64_t kron_mass_size(fdp_mass h) { return h ? h->N : 0; }
 // Enqueue the D per-mode passes of the mass inverse (or forward product) for in -> out.
 static cudaError_t enqueue_mass(const fdp_mass_s* h, int mode, const double* in, double* out,
                                 long long bs, const double* dscale, int64_t batch, cudaStream_t s,
-                                int* nlaunch) {
+                                int* nlaunch, Recorder* rec = nullptr) {
   for (int d = 0; d < h->D; ++d) {
     MassMode m{};
     long long P = 1, Q = 1;
@@ -495,6 +533,12 @@ static cudaError_t enqueue_mass(const fdp_mass_s* h, int mode, const double* in,
     m.batch = (int)batch;
     m.band = h->band[d];
     m.forward = mode == FDP_MASS_FORWARD;
+    if (rec) {
+      const double elems = (double)h->N * batch;
+      cudaError_t e0 = rec->before(2, 2.0 * 2.0 * (2 * m.band + 1) * elems,
+                                   16.0 * elems + (m.pre || m.post ? 8.0 * h->N : 0.0));
+      if (e0 != cudaSuccess) return e0;
+    }
     cudaError_t e = launch_mass_mode(m, s);
     if (e != cudaSuccess) return e;
     if (nlaunch) ++*nlaunch;
@@ -584,6 +628,10 @@ struct fdp_block_s {
   void* g_ws = nullptr;
   int64_t g_batch = -1;
   cudaGraphExec_t exec = nullptr;
+  // profiling
+  bool prof = false;
+  std::vector<cudaEvent_t> ev;
+  std::vector<LaunchInfo> info;
   // host e2e buffers
   double* e2e_r = nullptr;
   double* e2e_s = nullptr;
@@ -593,6 +641,7 @@ struct fdp_block_s {
 
 static void free_block(fdp_block h) {
   if (!h) return;
+  for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
   if (h->exec) cudaGraphExecDestroy(h->exec);
   if (h->cap) cudaStreamDestroy(h->cap);
   cudaFree(h->dv);
@@ -668,6 +717,15 @@ extern "C" size_t block_precond_workspace_bytes(fdp_block h, int64_t batch) {
 
 static cudaError_t enqueue_block(fdp_block h, const double* r, double* s, int64_t batch, double* ws,
                                  cudaStream_t st, int* nlaunch) {
+  Recorder recv;
+  Recorder* rec = nullptr;
+  if (h->prof) {
+    h->info.clear();
+    recv.ev = &h->ev;
+    recv.info = &h->info;
+    recv.s = st;
+    rec = &recv;
+  }
   const int D = h->D;
   const long long sz = h->size;
   std::vector<const double*> in(D), dsc(D);
@@ -682,16 +740,62 @@ static cudaError_t enqueue_block(fdp_block h, const double* r, double* s, int64_
   }
   if (h->dv) {
     // s_vel <- D_V^{-1/2} r_vel (one streaming launch over all velocity components)
+    if (rec) {
+      cudaError_t e0 = rec->before(1, (double)h->nvel * batch, 16.0 * h->nvel * batch + 8.0 * h->nvel);
+      if (e0 != cudaSuccess) return e0;
+    }
     cudaError_t e = launch_scale(r, s, h->dv, h->nvel, batch, sz, sz, st);
     if (e != cudaSuccess) return e;
     if (nlaunch) ++*nlaunch;
     for (int k = 0; k < D; ++k) in[k] = s + h->off[k];
   }
-  cudaError_t e = enqueue_fd(h->vel, in, sz, out, sz, T, dsc, batch, st, nlaunch);
+  cudaError_t e = enqueue_fd(h->vel, in, sz, out, sz, T, dsc, batch, st, nlaunch, rec);
   if (e != cudaSuccess) return e;
   // pressure block: r_p -> s_p
-  return enqueue_mass(h->pres, FDP_MASS_INVERSE, r + h->off[D], s + h->off[D], sz, h->dq, batch,
-                      st, nlaunch);
+  e = enqueue_mass(h->pres, FDP_MASS_INVERSE, r + h->off[D], s + h->off[D], sz, h->dq, batch, st,
+                   nlaunch, rec);
+  if (e != cudaSuccess) return e;
+  return rec ? rec->finish() : cudaSuccess;
+}
+
+extern "C" fdp_status block_precond_profile(fdp_block h, int enable) {
+  if (!h) return fail(FDP_ERR_INVALID_ARG, "block_precond_profile: NULL handle");
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard dg(h->device);
+  if (enable && h->ev.empty()) {
+    h->ev.resize(64);
+    for (auto& e : h->ev) FDP_CUDA(cudaEventCreate(&e), "block_precond_profile: event");
+  }
+  if ((enable != 0) != h->prof) {
+    h->prof = enable != 0;
+    if (h->exec) {  // force re-capture with / without event nodes
+      cudaGraphExecDestroy(h->exec);
+      h->exec = nullptr;
+    }
+  }
+  return FDP_OK;
+}
+
+extern "C" int block_precond_profile_read(fdp_block h, int max, int32_t* kind, float* ms,
+                                          double* flops, double* bytes) {
+  if (!h || !h->prof) return -1;
+  std::lock_guard<std::mutex> lk(h->mu);
+  DeviceGuard dg(h->device);
+  const int n = (int)h->info.size();
+  for (int i = 0; i < n && i < max; ++i) {
+    if (kind) kind[i] = h->info[i].kind;
+    if (flops) flops[i] = h->info[i].flops;
+    if (bytes) bytes[i] = h->info[i].bytes;
+    if (ms) {
+      float t = 0.f;
+      if (cudaEventElapsedTime(&t, h->ev[i], h->ev[i + 1]) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+      }
+      ms[i] = t;
+    }
+  }
+  return n;
 }
 
 extern "C" int fdp_block_launch_count(fdp_block h, int64_t batch) {
