@@ -2,8 +2,10 @@
 // launch orchestration of the preconditioner application (§4-§5: P_D of P:591-598,
 // Algorithm 1 of P:1003-1011, P_Q solve of P:975-976, diagonal scaling of P:1038-1059).
 #include <algorithm>
+#include <functional>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -60,6 +62,15 @@ static bool is_device_ptr(const void* p) {
     return false;
   }
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+static int num_sms() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess &&
+      cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+    return n;
+  cudaGetLastError();
+  return 148;
 }
 
 struct DeviceGuard {  // select the handle's device for the duration of a call, then restore
@@ -237,7 +248,8 @@ extern "C" fdp_status fd_setup(int D, const int32_t* n, const double* const* K,
     const int nd = n[d];
     TileCfg c = choose_tile(nd);
     raw->cfg[d] = c;
-    std::vector<double> wf((size_t)c.kpad * c.ldw, 0.0), wb((size_t)c.kpad * c.ldw, 0.0);
+    const int wrows = std::max(c.kpad, c.ldw);  // the fused small kernel reads W^T rows < ldw
+    std::vector<double> wf((size_t)wrows * c.ldw, 0.0), wb((size_t)wrows * c.ldw, 0.0);
     const std::vector<double>& U = raw->U_host[d];  // column-major: U[i + n*j]
     for (int k = 0; k < nd; ++k)
       for (int a = 0; a < nd; ++a) {
@@ -256,7 +268,7 @@ extern "C" fdp_status fd_setup(int D, const int32_t* n, const double* const* K,
     if ((e = cudaMemcpy(raw->Wf[d], wf.data(), wf.size() * 8, cudaMemcpyHostToDevice)) ||
         (e = cudaMemcpy(raw->Wb[d], wb.data(), wb.size() * 8, cudaMemcpyHostToDevice)) ||
         (e = cudaMemcpy(raw->lamc[d], lc.data(), lc.size() * 8, cudaMemcpyHostToDevice)) ||
-        (e = prepare_mode_kernels(c))) {
+        (e = prepare_mode_kernels(c)) || (e = prepare_mode_small(c.NT))) {
       free_fd(raw);
       return cuda_fail(e, "fd_setup: upload");
     }
@@ -307,7 +319,7 @@ static ModeProb make_mode_prob(const fdp_fd_s* h, int d, bool fwd, const double*
   p.n1 = h->n[0];
   p.epi = epi;
   p.scale = scale;
-  if (epi == EPI_LAMBDA) {
+  if (epi == EPI_LAMBDA || epi == EPI_FUSED) {
     p.lam0 = h->lamc[0];
     p.lam1 = h->D == 3 ? h->lamc[1] : nullptr;
     p.lamcol = h->lamc[h->D - 1];
@@ -316,11 +328,16 @@ static ModeProb make_mode_prob(const fdp_fd_s* h, int d, bool fwd, const double*
   const long long M = P * Q * batch;
   p.tiles_m = (int)((M + BM - 1) / BM);
   p.tiles_n = h->cfg[d].tiles_n;
+  p.fd_work = 1;
   return p;
 }
 
 // Stage = one mode/direction for a set of FD problems. Problems with the same tile config share a
 // launch (up to kMaxGroup); others get their own.
+// diagnostics (fdp_debug_trace): per-warp phase timestamps of small-path launches
+static unsigned long long* g_trace = nullptr;
+static size_t g_trace_cap = 0, g_trace_used = 0;
+
 static cudaError_t launch_stage(std::vector<ModeProb>& probs, const std::vector<TileCfg>& cfgs,
                                 bool kmaj, cudaStream_t s, int* nlaunch, Recorder* rec) {
   std::vector<bool> done(probs.size(), false);
@@ -338,18 +355,72 @@ static cudaError_t launch_stage(std::vector<ModeProb>& probs, const std::vector<
       done[j] = true;
     }
     g.total_ctas = ctas;
+    // small-n path: every problem fits one column tile of <= 96 columns
+    bool small = std::getenv("FDP_NO_SMALL") == nullptr;
+    for (int j = 0; j < g.count; ++j) small = small && g.prob[j].n <= kSmallMaxN && g.prob[j].tiles_n == 1;
+    if (small) {
+      const int total = num_sms();
+      double wsum = 0.0;
+      std::vector<double> w(g.count);
+      for (int j = 0; j < g.count; ++j) {
+        ModeProb& p = g.prob[j];
+        const long long M = (long long)p.P * p.Q * p.batch;
+        p.tiles_m = (int)((M + 7) / 8);
+        w[j] = (double)p.tiles_m * ((p.n + 3) / 4) * (p.epi == EPI_FUSED ? 2 : 1);
+        wsum += w[j];
+      }
+      int used = 0;
+      for (int j = 0; j < g.count; ++j) {
+        ModeProb& p = g.prob[j];
+        int c = std::max(1, (int)(total * w[j] / wsum));
+        c = std::min(c, std::max(1, (p.tiles_m + 7) / 8));  // no more warps than 8-row tiles
+        p.ctas = c;
+        used += c;
+      }
+      // hand leftover CTAs to the problems with the most work per CTA
+      while (used < total) {
+        int best = -1;
+        double bw = 0.0;
+        for (int j = 0; j < g.count; ++j) {
+          const double per = w[j] / g.prob[j].ctas;
+          if (g.prob[j].ctas * 8 < g.prob[j].tiles_m && per > bw) { bw = per; best = j; }
+        }
+        if (best < 0) break;
+        ++g.prob[best].ctas;
+        ++used;
+      }
+      int begin = 0;
+      for (int j = 0; j < g.count; ++j) {
+        g.prob[j].cta_begin = begin;
+        begin += g.prob[j].ctas;
+      }
+      g.total_ctas = begin;
+    } else {
+      for (int j = 0; j < g.count; ++j)
+        if (g.prob[j].epi == EPI_FUSED) return cudaErrorInvalidValue;  // fused needs small path
+    }
     if (rec) {
       double fl = 0.0, by = 0.0;
       for (int j = 0; j < g.count; ++j) {
         const ModeProb& p = g.prob[j];
         const double elems = (double)p.P * p.Q * p.batch * p.n;
-        fl += 2.0 * elems * p.n;
+        // dense-inverse pressure passes ride along but are not FD work: count their bytes only
+        if (p.fd_work) fl += (p.epi == EPI_FUSED ? 4.0 : 2.0) * elems * p.n;
         by += 16.0 * elems + (p.epi == EPI_SCALE ? 8.0 * p.N : 0.0);
       }
       cudaError_t e0 = rec->before(0, fl, by);
       if (e0 != cudaSuccess) return e0;
     }
-    cudaError_t e = launch_mode_group(g, cfgs[i], kmaj, s);
+    g.trace = nullptr;
+    if (small && g_trace) {
+      const size_t need = (size_t)g.total_ctas * 16 * kTracePhases;
+      if (g_trace_used + need <= g_trace_cap) {
+        g.trace = g_trace + g_trace_used;
+        g_trace_used += need;
+      }
+    }
+    cudaError_t e = small ? launch_mode_small(g, cfgs[i].NT, kmaj, s)
+                          : launch_mode_group(g, cfgs[i], kmaj, s);
     if (e != cudaSuccess) return e;
     if (nlaunch) ++*nlaunch;
   }
@@ -360,40 +431,59 @@ static cudaError_t launch_stage(std::vector<ModeProb>& probs, const std::vector<
 // in[k], out[k] with batch strides ibs/obs; T[k] workspace with stride N_k. dscale[k] may be NULL.
 // Pre-scaling (if any) must already have been applied by the caller (into out[k]) and `in` point
 // at it.
+using StageHook = std::function<void(int pass, bool fwd, int d, std::vector<ModeProb>&,
+                                     std::vector<TileCfg>&)>;
 static cudaError_t enqueue_fd(const std::vector<const fdp_fd_s*>& hs,
                               const std::vector<const double*>& in, long long ibs,
                               const std::vector<double*>& out, long long obs,
                               const std::vector<double*>& T,
                               const std::vector<const double*>& dscale, int64_t batch,
-                              cudaStream_t s, int* nlaunch, Recorder* rec = nullptr) {
+                              cudaStream_t s, int* nlaunch, Recorder* rec = nullptr,
+                              const StageHook& hook = nullptr) {
   const int D = hs[0]->D;
   const size_t K = hs.size();
-  // pass sequence: forward d = 0..D-1, backward d = D-1..0; 2D passes alternate T <- src, out <- T
-  int pass = 0;
-  for (int dir = 0; dir < 2; ++dir) {
-    for (int step = 0; step < D; ++step) {
-      const int d = dir == 0 ? step : D - 1 - step;
-      const bool fwd = dir == 0;
-      std::vector<ModeProb> probs;
-      std::vector<TileCfg> cfgs;
-      for (size_t k = 0; k < K; ++k) {
-        const double* src;
-        long long sbs;
-        double* dst;
-        long long dbs;
-        if (pass == 0) { src = in[k]; sbs = ibs; } else if (pass % 2 == 1) { src = T[k]; sbs = hs[k]->N; } else { src = out[k]; sbs = obs; }
-        if (pass % 2 == 0) { dst = T[k]; dbs = hs[k]->N; } else { dst = out[k]; dbs = obs; }
-        int epi = EPI_NONE;
-        const double* sc = nullptr;
-        if (fwd && d == D - 1) epi = EPI_LAMBDA;
-        if (!fwd && d == 0 && dscale[k]) { epi = EPI_SCALE; sc = dscale[k]; }
-        probs.push_back(make_mode_prob(hs[k], d, fwd, src, sbs, dst, dbs, batch, epi, sc));
-        cfgs.push_back(hs[k]->cfg[d]);
+  // Stage list: forward d = 0..D-1, backward d = D-1..0. When every mode of every component is
+  // small (single column tile, n <= 96) the mode-D forward / Lambda / mode-D backward triple is
+  // one fused pass. Destinations alternate so that the last pass lands in `out`.
+  bool fuse = std::getenv("FDP_NO_FUSE") == nullptr && std::getenv("FDP_NO_SMALL") == nullptr;
+  for (size_t k = 0; k < K; ++k)
+    for (int d = 0; d < D; ++d)
+      fuse = fuse && hs[k]->n[d] <= kSmallMaxN && hs[k]->cfg[d].tiles_n == 1;
+  struct Stage { int d; bool fwd; bool fused; };
+  std::vector<Stage> stages;
+  for (int d = 0; d < D; ++d) stages.push_back({d, true, fuse && d == D - 1});
+  for (int d = D - 1; d >= 0; --d)
+    if (!(fuse && d == D - 1)) stages.push_back({d, false, false});
+  const int npass = (int)stages.size();
+  for (int pass = 0; pass < npass; ++pass) {
+    const Stage& st = stages[pass];
+    const int d = st.d;
+    const bool dst_out = ((npass - 1 - pass) % 2) == 0;
+    std::vector<ModeProb> probs;
+    std::vector<TileCfg> cfgs;
+    for (size_t k = 0; k < K; ++k) {
+      const double* src;
+      long long sbs;
+      if (pass == 0) {
+        src = in[k]; sbs = ibs;
+      } else if (dst_out) {  // previous pass wrote T
+        src = T[k]; sbs = hs[k]->N;
+      } else {
+        src = out[k]; sbs = obs;
       }
-      cudaError_t e = launch_stage(probs, cfgs, d == 0, s, nlaunch, rec);
-      if (e != cudaSuccess) return e;
-      ++pass;
+      double* dst = dst_out ? out[k] : T[k];
+      const long long dbs = dst_out ? obs : hs[k]->N;
+      int epi = EPI_NONE;
+      const double* sc = nullptr;
+      if (st.fused) epi = EPI_FUSED;
+      else if (st.fwd && d == D - 1) epi = EPI_LAMBDA;
+      if (!st.fwd && d == 0 && dscale[k]) { epi = EPI_SCALE; sc = dscale[k]; }
+      probs.push_back(make_mode_prob(hs[k], d, st.fwd, src, sbs, dst, dbs, batch, epi, sc));
+      cfgs.push_back(hs[k]->cfg[d]);
     }
+    if (hook) hook(pass, st.fwd, d, probs, cfgs);
+    cudaError_t e = launch_stage(probs, cfgs, d == 0, s, nlaunch, rec);
+    if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
 }
@@ -444,6 +534,7 @@ struct fdp_mass_s {
   double* Lb[3] = {nullptr, nullptr, nullptr};
   double* invd[3] = {nullptr, nullptr, nullptr};
   double* Mb[3] = {nullptr, nullptr, nullptr};
+  std::vector<double> Lb_host[3];
 };
 
 static void free_mass(fdp_mass h) {
@@ -488,6 +579,7 @@ extern "C" fdp_status kron_mass_setup(int D, const int32_t* n, const double* con
   DeviceGuard dg(device);
   if (!dg.ok) return fail(FDP_ERR_CUDA, "kron_mass_setup: cannot select device");
   fdp_mass raw = h.release();
+  for (int d = 0; d < D; ++d) raw->Lb_host[d] = Lb[d];
   for (int d = 0; d < D; ++d) {
     fdp_status st;
     if ((st = dalloc(&raw->Lb[d], Lb[d].size())) || (st = dalloc(&raw->invd[d], invd[d].size())) ||
@@ -620,6 +712,13 @@ struct fdp_block_s {
   long long nvel = 0;
   double* dv = nullptr;        // D_V^{-1/2} (sum N_k) or NULL
   double* dq = nullptr;        // D_Q^{-1/2} (n_Q) or NULL
+  double* dall = nullptr;      // [D_V^{-1/2} | D_Q^{-1/2}] (ones where absent), dense-P_Q path
+  // dense-inverse P_Q path: M_d^{-1} padded to the velocity tile config of mode d, so the
+  // pressure passes join the velocity launches of stages 0..D-1 (C-9)
+  bool pres_dense = false;
+  double* Wq[3] = {nullptr, nullptr, nullptr};
+  int q_tiles_n[3] = {0, 0, 0};
+  int q_ldw[3] = {0, 0, 0};
   cudaStream_t cap = nullptr;  // private capture stream
   // graph cache
   std::mutex mu;
@@ -646,6 +745,8 @@ static void free_block(fdp_block h) {
   if (h->cap) cudaStreamDestroy(h->cap);
   cudaFree(h->dv);
   cudaFree(h->dq);
+  cudaFree(h->dall);
+  for (int d = 0; d < 3; ++d) cudaFree(h->Wq[d]);
   cudaFree(h->e2e_r);
   cudaFree(h->e2e_s);
   cudaFree(h->e2e_ws);
@@ -698,6 +799,46 @@ extern "C" fdp_status block_precond_setup(int D, const fdp_fd* vel, fdp_mass pre
   fdp_status st = FDP_OK;
   if (dscale_vel) st = upload_isqrt(dscale_vel, raw->nvel, &raw->dv);
   if (!st && dscale_pres) st = upload_isqrt(dscale_pres, pres->N, &raw->dq);
+  // P_Q by dense per-mode inverses when every factor is small (2 n flops/entry/mode beat the
+  // banded recurrences' latency and ride in the velocity launches); banded otherwise.
+  const char* env = std::getenv("FDP_PRESSURE");
+  bool dense = true;
+  for (int d = 0; d < D; ++d) dense = dense && pres->n[d] <= 160;
+  if (env && std::string(env) == "banded") dense = false;
+  if (env && std::string(env) == "dense") dense = true;
+  for (int d = 0; d < D && dense; ++d)
+    for (int k = 1; k < D; ++k) dense = dense && raw->vel[k]->cfg[d].NT == raw->vel[0]->cfg[d].NT;
+  if (!st && dense) {
+    raw->pres_dense = true;
+    for (int d = 0; d < D && !st; ++d) {
+      const int nq = pres->n[d];
+      const TileCfg& vc = raw->vel[0]->cfg[d];
+      const int BN = 8 * vc.NT;
+      raw->q_tiles_n[d] = (nq + BN - 1) / BN;
+      raw->q_ldw[d] = raw->q_tiles_n[d] * BN;
+      const int kpad = ((nq + 15) / 16) * 16;
+      std::vector<double> X;
+      spd_inverse_from_band(nq, pres->band[d], pres->Lb_host[d], &X);
+      std::vector<double> w((size_t)kpad * raw->q_ldw[d], 0.0);
+      for (int k = 0; k < nq; ++k)
+        for (int a = 0; a < nq; ++a) w[(size_t)k * raw->q_ldw[d] + a] = X[a + (size_t)nq * k];
+      st = dalloc(&raw->Wq[d], w.size());
+      if (!st) {
+        cudaError_t e = cudaMemcpy(raw->Wq[d], w.data(), w.size() * 8, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) st = cuda_fail(e, "block_precond_setup: upload");
+      }
+    }
+    if (!st && (dscale_vel || dscale_pres)) {
+      std::vector<double> v(raw->size, 1.0);
+      for (long long i = 0; i < raw->nvel && dscale_vel; ++i) v[i] = 1.0 / std::sqrt(dscale_vel[i]);
+      for (long long i = 0; i < pres->N && dscale_pres; ++i) v[raw->nvel + i] = 1.0 / std::sqrt(dscale_pres[i]);
+      st = dalloc(&raw->dall, v.size());
+      if (!st) {
+        cudaError_t e = cudaMemcpy(raw->dall, v.data(), v.size() * 8, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) st = cuda_fail(e, "block_precond_setup: upload");
+      }
+    }
+  }
   if (!st) {
     cudaError_t e = cudaStreamCreateWithFlags(&raw->cap, cudaStreamNonBlocking);
     if (e != cudaSuccess) st = cuda_fail(e, "block_precond_setup: stream");
@@ -711,8 +852,11 @@ extern "C" fdp_status block_precond_setup(int D, const fdp_fd* vel, fdp_mass pre
 }
 
 extern "C" int64_t block_precond_size(fdp_block h) { return h ? h->size : 0; }
+static long long block_ws_elems(const fdp_block_s* h, int64_t batch) {
+  return batch * (h->nvel + (h->pres_dense ? 2 * h->pres->N : 0));
+}
 extern "C" size_t block_precond_workspace_bytes(fdp_block h, int64_t batch) {
-  return h && batch > 0 ? (size_t)(batch * h->nvel) * sizeof(double) : 0;
+  return h && batch > 0 ? (size_t)block_ws_elems(h, batch) * sizeof(double) : 0;
 }
 
 static cudaError_t enqueue_block(fdp_block h, const double* r, double* s, int64_t batch, double* ws,
@@ -738,7 +882,22 @@ static cudaError_t enqueue_block(fdp_block h, const double* r, double* s, int64_
     toff += h->vel[k]->N * batch;
     dsc[k] = h->dv ? h->dv + h->off[k] : nullptr;
   }
-  if (h->dv) {
+  const long long nq = h->pres->N;
+  double* Tq1 = ws + toff;
+  double* Tq2 = Tq1 + nq * batch;
+  const double* rq = r + h->off[D];
+  if (h->pres_dense && h->dall) {
+    // s <- [D_V^{-1/2} | D_Q^{-1/2}] o r over the whole item (one streaming launch)
+    if (rec) {
+      cudaError_t e0 = rec->before(1, (double)sz * batch, 16.0 * sz * batch + 8.0 * sz);
+      if (e0 != cudaSuccess) return e0;
+    }
+    cudaError_t e = launch_scale(r, s, h->dall, sz, batch, sz, sz, st);
+    if (e != cudaSuccess) return e;
+    if (nlaunch) ++*nlaunch;
+    for (int k = 0; k < D; ++k) in[k] = s + h->off[k];
+    rq = s + h->off[D];
+  } else if (h->dv) {
     // s_vel <- D_V^{-1/2} r_vel (one streaming launch over all velocity components)
     if (rec) {
       cudaError_t e0 = rec->before(1, (double)h->nvel * batch, 16.0 * h->nvel * batch + 8.0 * h->nvel);
@@ -749,12 +908,47 @@ static cudaError_t enqueue_block(fdp_block h, const double* r, double* s, int64_
     if (nlaunch) ++*nlaunch;
     for (int k = 0; k < D; ++k) in[k] = s + h->off[k];
   }
-  cudaError_t e = enqueue_fd(h->vel, in, sz, out, sz, T, dsc, batch, st, nlaunch, rec);
+  StageHook hook = nullptr;
+  if (h->pres_dense) {
+    // pressure pass d joins forward stage d: rq -> Tq1 -> Tq2 -> s_p (x_d M_d^{-1})
+    hook = [&](int pass, bool fwd, int d, std::vector<ModeProb>& probs, std::vector<TileCfg>& cfgs) {
+      if (!fwd) return;
+      ModeProb p{};
+      long long P = 1, Q = 1;
+      for (int e = 0; e < d; ++e) P *= h->pres->n[e];
+      for (int e = d + 1; e < D; ++e) Q *= h->pres->n[e];
+      p.X = d == 0 ? rq : (d % 2 == 1 ? Tq1 : Tq2);
+      p.xbs = d == 0 ? sz : nq;
+      const bool last = d == D - 1;
+      p.Y = last ? s + h->off[D] : (d % 2 == 0 ? Tq1 : Tq2);
+      p.ybs = last ? sz : nq;
+      p.W = h->Wq[d];
+      p.N = nq;
+      p.P = (int)P;
+      p.n = h->pres->n[d];
+      p.Q = (int)Q;
+      p.batch = (int)batch;
+      p.ldw = h->q_ldw[d];
+      p.n1 = h->pres->n[0];
+      p.epi = (last && h->dall) ? EPI_SCALE : EPI_NONE;
+      p.scale = (last && h->dall) ? h->dall + h->off[D] : nullptr;
+      const int BM = 4 * 8 * cfgs[0].MT;
+      p.tiles_m = (int)((P * Q * batch + BM - 1) / BM);
+      p.tiles_n = h->q_tiles_n[d];
+      p.fd_work = 0;
+      probs.push_back(p);
+      cfgs.push_back(cfgs[0]);
+      (void)pass;
+    };
+  }
+  cudaError_t e = enqueue_fd(h->vel, in, sz, out, sz, T, dsc, batch, st, nlaunch, rec, hook);
   if (e != cudaSuccess) return e;
-  // pressure block: r_p -> s_p
-  e = enqueue_mass(h->pres, FDP_MASS_INVERSE, r + h->off[D], s + h->off[D], sz, h->dq, batch, st,
-                   nlaunch, rec);
-  if (e != cudaSuccess) return e;
+  if (!h->pres_dense) {
+    // pressure block by banded per-mode solves: r_p -> s_p
+    e = enqueue_mass(h->pres, FDP_MASS_INVERSE, r + h->off[D], s + h->off[D], sz, h->dq, batch, st,
+                     nlaunch, rec);
+    if (e != cudaSuccess) return e;
+  }
   return rec ? rec->finish() : cudaSuccess;
 }
 
@@ -811,7 +1005,12 @@ extern "C" int fdp_block_launch_count(fdp_block h, int64_t batch) {
     int groups = (int)(std::unique(nts.begin(), nts.end()) - nts.begin());
     n += 2 * groups;
   }
-  n += h->pres->D;
+  bool fuse = std::getenv("FDP_NO_FUSE") == nullptr && std::getenv("FDP_NO_SMALL") == nullptr;
+  for (int k = 0; k < D; ++k)
+    for (int d = 0; d < D; ++d) fuse = fuse && h->vel[k]->n[d] <= kSmallMaxN && h->vel[k]->cfg[d].tiles_n == 1;
+  if (fuse) n -= 1;
+  if (!h->pres_dense) n += h->pres->D;
+  else if (h->dall) n += h->dv ? 0 : 1;
   return n;
 }
 
@@ -882,7 +1081,7 @@ extern "C" fdp_status block_precond_apply_host(fdp_block h, const double* r_host
     fdp_status st;
     if ((st = dalloc(&h->e2e_r, (size_t)(batch * h->size))) ||
         (st = dalloc(&h->e2e_s, (size_t)(batch * h->size))) ||
-        (st = dalloc(reinterpret_cast<double**>(&h->e2e_ws), (size_t)(batch * h->nvel))))
+        (st = dalloc(reinterpret_cast<double**>(&h->e2e_ws), (size_t)block_ws_elems(h, batch))))
       return st;
     h->e2e_batch = batch;
   }
@@ -901,4 +1100,14 @@ extern "C" fdp_status block_precond_destroy(fdp_block h) {
   DeviceGuard dg(h->device);
   free_block(h);
   return FDP_OK;
+}
+
+// Diagnostics only (not part of include/fdp.h): route per-warp phase timestamps of subsequent
+// small-path launches into a device buffer of `cap` uint64 (NULL disables). Invalidates nothing:
+// callers must use fresh buffers / handles so graphs are re-captured.
+extern "C" int fdp_debug_trace(unsigned long long* dev_buf, size_t cap) {
+  g_trace = dev_buf;
+  g_trace_cap = dev_buf ? cap : 0;
+  g_trace_used = 0;
+  return 0;
 }

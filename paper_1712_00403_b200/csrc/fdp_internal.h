@@ -25,6 +25,7 @@ enum Epilogue : int {
   EPI_NONE = 0,
   EPI_LAMBDA = 1,  // divide by Lambda[i] = lamrow(p) + lamcol[a]   (Algorithm 1 step 3)
   EPI_SCALE = 2,   // multiply by dscale[index within item]           (P^G post-scaling)
+  EPI_FUSED = 3,   // small-n only: x_D U_D^T, divide by Lambda, x_D U_D in one pass
 };
 
 struct ModeProb {
@@ -44,6 +45,8 @@ struct ModeProb {
   int epi;
   int tiles_m, tiles_n;
   int cta_begin;          // first CTA of this problem in the grouped grid
+  int fd_work;            // host-side accounting only: 1 = FD contraction, 0 = dense P_Q pass
+  int ctas;               // small-n kernel: CTAs assigned to this problem
 };
 
 constexpr int kMaxGroup = 4;
@@ -51,7 +54,11 @@ struct ModeGroup {
   ModeProb prob[kMaxGroup];
   int count;
   int total_ctas;
+  // diagnostics: when non-null, lane 0 of every warp records %globaltimer at kTracePhases points
+  // of its first tile into trace[(blockIdx * warps + warp) * kTracePhases + phase]
+  unsigned long long* trace;
 };
+constexpr int kTracePhases = 6;
 
 // Tile configuration chosen for a problem size n (same for all problems of one launch).
 struct TileCfg {
@@ -65,6 +72,15 @@ TileCfg choose_tile(int n);
 
 // Launch one grouped mode-contraction stage. kmaj: P == 1 for every problem (mode 1).
 cudaError_t launch_mode_group(const ModeGroup& g, const TileCfg& cfg, bool kmaj, cudaStream_t s);
+
+// Small-n path (n <= 96, one column tile): persistent row-streaming kernel, W resident in shared
+// memory, whole-K A panels per warp (8 rows) double-buffered with cp.async, programmatic
+// dependent launch. Problems with epi == EPI_FUSED do mode-D forward, Lambda^{-1} and mode-D
+// backward in one pass (the middle of Algorithm 1). The caller fills prob[i].ctas
+// (CTAs per problem, sum = total_ctas) and prob[i].tiles_m = ceil(M/8).
+constexpr int kSmallMaxN = 96;
+cudaError_t launch_mode_small(const ModeGroup& g, int NT, bool kmaj, cudaStream_t s);
+cudaError_t prepare_mode_small(int NT);
 
 // y[b*ys + i] = x[b*xs + i] * s[i], i < N  (P^G pre-scaling), over `batch` items.
 cudaError_t launch_scale(const double* x, double* y, const double* s, long long N, long long batch,
@@ -105,6 +121,7 @@ int gen_eig(int n, const double* K, const double* M, double* U, double* lam, std
 int band_cholesky(int n, int b, const double* M, std::vector<double>* Lb, std::vector<double>* invd,
                   std::string* err);
 int detect_bandwidth(int n, const double* M);
+int spd_inverse_from_band(int n, int b, const std::vector<double>& Lb, std::vector<double>* X);
 
 int iga_build(int deg, int alpha, int n_el, int flags, double c_pen, int q, double* K, double* M,
               int* n_out, std::string* err);

@@ -250,4 +250,26 @@ int band_cholesky(int n, int b, const double* M, std::vector<double>* Lb, std::v
   return FDP_OK;
 }
 
+// Dense inverse of an SPD banded matrix from its band Cholesky factor: solve L L^T X = I column
+// by column (X symmetric). Used for the dense-inverse variant of the P_Q solve (C-9).
+int spd_inverse_from_band(int n, int b, const std::vector<double>& Lb, std::vector<double>* X) {
+  X->assign((size_t)n * n, 0.0);
+  auto L = [&](int i, int j) -> double { return Lb[(size_t)i * (b + 1) + (j - i + b)]; };
+  std::vector<double> y(n);
+  for (int c = 0; c < n; ++c) {
+    for (int i = 0; i < n; ++i) {
+      double v = (i == c) ? 1.0 : 0.0;
+      for (int k = std::max(0, i - b); k < i; ++k) v -= L(i, k) * y[k];
+      y[i] = v / L(i, i);
+    }
+    for (int i = n - 1; i >= 0; --i) {
+      double v = y[i];
+      for (int k = i + 1; k <= std::min(n - 1, i + b); ++k) v -= L(k, i) * y[k];
+      y[i] = v / L(i, i);
+    }
+    for (int i = 0; i < n; ++i) (*X)[i + (size_t)n * c] = y[i];
+  }
+  return FDP_OK;
+}
+
 }  // namespace fdp

@@ -177,3 +177,42 @@ def test_block_precond_config4_full_size_bench_launch():
     for i in (0, w.batch - 1):
         si = s[i].cpu().numpy()
         assert rel(si, ref.apply(r[i])) < TOL
+
+
+@pytest.mark.parametrize("env", [{"FDP_NO_SMALL": "1"}, {"FDP_NO_FUSE": "1"}, {"FDP_PRESSURE": "banded"},
+                                 {"FDP_PRESSURE": "dense"}, {}])
+@pytest.mark.parametrize("cfg_id", [1, 2, 3])
+def test_block_precond_kernel_paths(cfg_id, env, monkeypatch):
+    """Every kernel path (big/small K1, fused middle, banded/dense P_Q) against the oracle."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    w, od, gd = _both(cfg_id)
+    r = synth.rhs(100 + cfg_id, od.n_total, 2)
+    dv = dq = None
+    if w.variable_nu:
+        dv, dq = ospaces.nu_scalings(od, synth.viscosity)
+    P = fdp.build_block(gd, dscale_vel=dv, dscale_pres=dq)
+    s = P.apply(dev(r), batch=2).cpu().numpy()
+    ref = oprec.BlockPrecond(od, dv, dq).apply(r)
+    o = od.offsets()
+    for i in range(2):
+        for k in range(len(o) - 1):
+            assert rel(s[i, o[k]:o[k + 1]], ref[i, o[k]:o[k + 1]]) < TOL, (cfg_id, env, k)
+
+
+@pytest.mark.parametrize("dims", [(96, 5, 7), (8, 96, 33), (17, 3, 96), (9, 11)])
+def test_fd_apply_small_path_edges(dims):
+    """n = 96 (largest small-path extent), tiny extents, 2D; fused middle + in-place pass 0."""
+    rng = np.random.default_rng(sum(dims))
+    Ks = [_rand_spd(n, rng, 1.0) for n in dims]
+    Ms = [_rand_spd(n, rng, 2.0) for n in dims]
+    coef = [1.0 + 0.5 * d for d in range(len(dims))]
+    N = int(np.prod(dims))
+    b = rng.standard_normal((3, N))
+    S = fdp.FD(Ks, Ms, coef)
+    bt = dev(b)
+    S.apply(bt, bt, batch=3)
+    ref = ofd.FDSolver(Ks, Ms, coef)
+    x = bt.cpu().numpy()
+    for i in range(3):
+        assert rel(x[i], ref.apply(b[i])) < TOL
