@@ -52,3 +52,8 @@ def test_minres_iteration_counts_identical(cid):
     assert np.linalg.norm(x1 - x2) / np.linalg.norm(x1) < 1e-6
     res = np.linalg.norm(op.matvec(x2) - f) / np.linalg.norm(f)
     assert res < 1e-5
+    import json, os
+    if os.path.isdir("gpurun_out"):
+        with open("gpurun_out/minres_counts.jsonl", "a") as fh:
+            fh.write(json.dumps({"config": cid, "its_oracle_P": it1, "its_gpu_P": it2,
+                                 "max_rel_hist_diff": rel, "true_rel_residual": res}) + "\n")
