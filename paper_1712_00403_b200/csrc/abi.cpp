@@ -185,6 +185,9 @@ struct fdp_fd_s {
   double* lamc[3] = {nullptr, nullptr, nullptr};  // coef[d] * lambda_d
   double* ws = nullptr;
   int64_t ws_batch = 0;
+  int* sync = nullptr;        // plane-pipeline counters (zeroed, self-resetting)
+  long long sync_cap = 0;
+  int64_t sync_batch = 0;
 };
 
 static void free_fd(fdp_fd h) {
@@ -195,6 +198,7 @@ static void free_fd(fdp_fd h) {
     cudaFree(h->lamc[d]);
   }
   cudaFree(h->ws);
+  cudaFree(h->sync);
   delete h;
 }
 
@@ -273,6 +277,22 @@ extern "C" fdp_status fd_setup(int D, const int32_t* n, const double* const* K,
       return cuda_fail(e, "fd_setup: upload");
     }
   }
+  {
+    const int64_t sb = std::max<int64_t>(1, max_batch);
+    const long long cap = 2 * ((long long)raw->n[2] * sb + 1);
+    fdp_status st = dalloc(&raw->sync, (size_t)cap);
+    if (st) {
+      free_fd(raw);
+      return st;
+    }
+    cudaError_t e = cudaMemset(raw->sync, 0, cap * sizeof(int));
+    if (e != cudaSuccess) {
+      free_fd(raw);
+      return cuda_fail(e, "fd_setup: sync init");
+    }
+    raw->sync_cap = cap;
+    raw->sync_batch = sb;
+  }
   if (max_batch > 0) {
     fdp_status st = dalloc(&raw->ws, (size_t)(max_batch * N));
     if (st) {
@@ -334,6 +354,53 @@ static ModeProb make_mode_prob(const fdp_fd_s* h, int d, bool fwd, const double*
 
 // Stage = one mode/direction for a set of FD problems. Problems with the same tile config share a
 // launch (up to kMaxGroup); others get their own.
+// Small-path grid: one CTA per SM, split over the problems of a group in proportion to their
+// DMMA work (prob.ctas, prob.cta_begin, total_ctas). prob.tiles_m must hold the 8-row tile count.
+static void alloc_small_ctas(ModeGroup& g, const std::vector<double>& w) {
+  const int total = num_sms();
+  double wsum = 0.0;
+  for (int j = 0; j < g.count; ++j) wsum += w[j];
+  int used = 0;
+  for (int j = 0; j < g.count; ++j) {
+    ModeProb& p = g.prob[j];
+    int c = std::max(1, (int)(total * w[j] / wsum));
+    c = std::min(c, std::max(1, (p.tiles_m + 7) / 8));  // no more warps than 8-row tiles
+    p.ctas = c;
+    used += c;
+  }
+  while (used < total) {  // leftover CTAs to the problems with the most work per CTA
+    int best = -1;
+    double bw = 0.0;
+    for (int j = 0; j < g.count; ++j) {
+      const double per = w[j] / g.prob[j].ctas;
+      if (g.prob[j].ctas * 8 < g.prob[j].tiles_m && per > bw) { bw = per; best = j; }
+    }
+    if (best < 0) break;
+    ++g.prob[best].ctas;
+    ++used;
+  }
+  int begin = 0;
+  for (int j = 0; j < g.count; ++j) {
+    g.prob[j].cta_begin = begin;
+    begin += g.prob[j].ctas;
+  }
+  g.total_ctas = begin;
+}
+
+static bool small_ok(const ModeProb& p) {
+  return p.n <= kSmallMaxN && p.tiles_n == 1 && (long long)p.P * p.Q * p.batch + 8 < (1LL << 31);
+}
+
+static double recorded_flops(const ModeProb& p) {
+  const double elems = (double)p.P * p.Q * p.batch * p.n;
+  // dense-inverse pressure passes ride along but are not FD work: count their bytes only
+  return p.fd_work ? (p.epi == EPI_FUSED ? 4.0 : 2.0) * elems * p.n : 0.0;
+}
+static double recorded_bytes(const ModeProb& p) {
+  const double elems = (double)p.P * p.Q * p.batch * p.n;
+  return 16.0 * elems + (p.epi == EPI_SCALE ? 8.0 * p.N : 0.0);
+}
+
 // diagnostics (fdp_debug_trace): per-warp phase timestamps of small-path launches
 static unsigned long long* g_trace = nullptr;
 static size_t g_trace_cap = 0, g_trace_used = 0;
@@ -357,44 +424,16 @@ static cudaError_t launch_stage(std::vector<ModeProb>& probs, const std::vector<
     g.total_ctas = ctas;
     // small-n path: every problem fits one column tile of <= 96 columns
     bool small = std::getenv("FDP_NO_SMALL") == nullptr;
-    for (int j = 0; j < g.count; ++j) small = small && g.prob[j].n <= kSmallMaxN && g.prob[j].tiles_n == 1;
+    for (int j = 0; j < g.count; ++j) small = small && small_ok(g.prob[j]);
     if (small) {
-      const int total = num_sms();
-      double wsum = 0.0;
       std::vector<double> w(g.count);
       for (int j = 0; j < g.count; ++j) {
         ModeProb& p = g.prob[j];
         const long long M = (long long)p.P * p.Q * p.batch;
         p.tiles_m = (int)((M + 7) / 8);
         w[j] = (double)p.tiles_m * ((p.n + 3) / 4) * (p.epi == EPI_FUSED ? 2 : 1);
-        wsum += w[j];
       }
-      int used = 0;
-      for (int j = 0; j < g.count; ++j) {
-        ModeProb& p = g.prob[j];
-        int c = std::max(1, (int)(total * w[j] / wsum));
-        c = std::min(c, std::max(1, (p.tiles_m + 7) / 8));  // no more warps than 8-row tiles
-        p.ctas = c;
-        used += c;
-      }
-      // hand leftover CTAs to the problems with the most work per CTA
-      while (used < total) {
-        int best = -1;
-        double bw = 0.0;
-        for (int j = 0; j < g.count; ++j) {
-          const double per = w[j] / g.prob[j].ctas;
-          if (g.prob[j].ctas * 8 < g.prob[j].tiles_m && per > bw) { bw = per; best = j; }
-        }
-        if (best < 0) break;
-        ++g.prob[best].ctas;
-        ++used;
-      }
-      int begin = 0;
-      for (int j = 0; j < g.count; ++j) {
-        g.prob[j].cta_begin = begin;
-        begin += g.prob[j].ctas;
-      }
-      g.total_ctas = begin;
+      alloc_small_ctas(g, w);
     } else {
       for (int j = 0; j < g.count; ++j)
         if (g.prob[j].epi == EPI_FUSED) return cudaErrorInvalidValue;  // fused needs small path
@@ -402,11 +441,8 @@ static cudaError_t launch_stage(std::vector<ModeProb>& probs, const std::vector<
     if (rec) {
       double fl = 0.0, by = 0.0;
       for (int j = 0; j < g.count; ++j) {
-        const ModeProb& p = g.prob[j];
-        const double elems = (double)p.P * p.Q * p.batch * p.n;
-        // dense-inverse pressure passes ride along but are not FD work: count their bytes only
-        if (p.fd_work) fl += (p.epi == EPI_FUSED ? 4.0 : 2.0) * elems * p.n;
-        by += 16.0 * elems + (p.epi == EPI_SCALE ? 8.0 * p.N : 0.0);
+        fl += recorded_flops(g.prob[j]);
+        by += recorded_bytes(g.prob[j]);
       }
       cudaError_t e0 = rec->before(0, fl, by);
       if (e0 != cudaSuccess) return e0;
@@ -427,6 +463,63 @@ static cudaError_t launch_stage(std::vector<ModeProb>& probs, const std::vector<
   return cudaSuccess;
 }
 
+// Plane pipeline: phase-1 problems probs1 (mode 0 fwd or mode 1 bwd) and phase-2 problems probs2
+// (mode 1 fwd or mode 0 bwd) of the same tensors in one launch (D = 3, small path, NT <= 10).
+// sync: zero-initialised ints (self-resetting), capacity sync_cap.
+static cudaError_t launch_pp_stage(std::vector<ModeProb>& probs1, std::vector<ModeProb>& probs2,
+                                   int NT, bool kmaj1, int* sync, long long sync_cap,
+                                   cudaStream_t s, int* nlaunch, Recorder* rec) {
+  ModeGroup g1{}, g2{};
+  g1.count = g2.count = (int)probs1.size();
+  std::vector<double> w(g1.count);
+  PlaneSync ps{};
+  long long off = 0;
+  for (int j = 0; j < g1.count; ++j) {
+    ModeProb a = probs1[j], b = probs2[j];
+    a.tiles_m = (int)(((long long)a.P * a.Q * a.batch + 7) / 8);
+    b.tiles_m = (int)(((long long)b.P * b.Q * b.batch + 7) / 8);
+    w[j] = (double)a.tiles_m * ((a.n + 3) / 4) + (double)b.tiles_m * ((b.n + 3) / 4);
+    g1.prob[j] = a;
+    g2.prob[j] = b;
+    // planes = the (i3, item) slices; rows per plane of each phase
+    const int rpp1 = kmaj1 ? b.n : a.P, rpp2 = kmaj1 ? b.P : a.n, planes = kmaj1 ? b.Q : a.Q;
+    ps.cnt_off[j] = (int)off;
+    ps.rows_per_plane1[j] = rpp1;
+    ps.rows_per_plane2[j] = rpp2;
+    off += (long long)planes * a.batch;
+  }
+  if (off + 1 > sync_cap) return cudaErrorInvalidValue;
+  alloc_small_ctas(g1, w);
+  for (int j = 0; j < g1.count; ++j) {
+    g2.prob[j].ctas = g1.prob[j].ctas;
+    g2.prob[j].cta_begin = g1.prob[j].cta_begin;
+  }
+  g2.total_ctas = g1.total_ctas;
+  ps.cnt = sync;
+  ps.done = sync + off;
+  ps.cnt_total = (int)off;
+  if (rec) {
+    double fl = 0.0, by = 0.0;
+    for (int j = 0; j < g1.count; ++j) {
+      fl += recorded_flops(g1.prob[j]) + recorded_flops(g2.prob[j]);
+      by += recorded_bytes(g1.prob[j]) + recorded_bytes(g2.prob[j]);
+    }
+    cudaError_t e0 = rec->before(0, fl, by);
+    if (e0 != cudaSuccess) return e0;
+  }
+  cudaError_t e = launch_mode_pp(g1, g2, ps, NT, kmaj1, s);
+  if (e != cudaSuccess) return e;
+  if (nlaunch) ++*nlaunch;
+  return cudaSuccess;
+}
+
+static long long pp_sync_ints(const std::vector<const fdp_fd_s*>& hs, int64_t batch, int extra_n3) {
+  long long n = 0;
+  for (const fdp_fd_s* h : hs) n += (long long)h->n[2] * batch;
+  n += (long long)extra_n3 * batch;
+  return n + 1;  // + done counter
+}
+
 // Enqueue FD solves for several handles (block components) on stream s.
 // in[k], out[k] with batch strides ibs/obs; T[k] workspace with stride N_k. dscale[k] may be NULL.
 // Pre-scaling (if any) must already have been applied by the caller (into out[k]) and `in` point
@@ -439,7 +532,8 @@ static cudaError_t enqueue_fd(const std::vector<const fdp_fd_s*>& hs,
                               const std::vector<double*>& T,
                               const std::vector<const double*>& dscale, int64_t batch,
                               cudaStream_t s, int* nlaunch, Recorder* rec = nullptr,
-                              const StageHook& hook = nullptr) {
+                              const StageHook& hook = nullptr, int* sync = nullptr,
+                              long long sync_cap = 0) {
   const int D = hs[0]->D;
   const size_t K = hs.size();
   // Stage list: forward d = 0..D-1, backward d = D-1..0. When every mode of every component is
@@ -455,6 +549,14 @@ static cudaError_t enqueue_fd(const std::vector<const fdp_fd_s*>& hs,
   for (int d = D - 1; d >= 0; --d)
     if (!(fuse && d == D - 1)) stages.push_back({d, false, false});
   const int npass = (int)stages.size();
+  // plane pipeline (D = 3): passes (0, 1) and (3, 4) each become one launch
+  // (opt-in, FDP_PP=1: with about one 8-row tile per warp per pass at batch 1 the two passes
+  // cannot overlap, so the separate launches are as fast)
+  bool pp = fuse && D == 3 && sync != nullptr && std::getenv("FDP_PP") != nullptr;
+  for (size_t k = 0; k < K; ++k)
+    for (int d = 0; d < 2; ++d)
+      pp = pp && hs[k]->cfg[d].NT <= kPPMaxNT && hs[k]->cfg[d].NT == hs[0]->cfg[0].NT;
+  std::vector<ModeProb> held;  // phase-1 problems waiting for their phase-2 partners
   for (int pass = 0; pass < npass; ++pass) {
     const Stage& st = stages[pass];
     const int d = st.d;
@@ -482,6 +584,35 @@ static cudaError_t enqueue_fd(const std::vector<const fdp_fd_s*>& hs,
       cfgs.push_back(hs[k]->cfg[d]);
     }
     if (hook) hook(pass, st.fwd, d, probs, cfgs);
+    if (pp && (pass == 0 || pass == 3)) {
+      bool ok = probs.size() <= (size_t)kMaxGroup;
+      for (const ModeProb& p : probs) ok = ok && small_ok(p);
+      if (ok) {
+        held = probs;
+        continue;
+      }
+      pp = false;  // fall back to one launch per pass
+    }
+    if (pp && (pass == 1 || pass == 4)) {
+      bool ok = probs.size() == held.size();
+      for (const ModeProb& p : probs) ok = ok && small_ok(p);
+      if (ok) {
+        const int sync_half = (int)(sync_cap / 2);
+        int* sy = pass == 1 ? sync : sync + sync_half;
+        cudaError_t e = launch_pp_stage(held, probs, cfgs[0].NT, pass == 1, sy, sync_half, s,
+                                        nlaunch, rec);
+        if (e == cudaSuccess) {
+          held.clear();
+          continue;
+        }
+        if (e != cudaErrorInvalidValue) return e;
+      }
+      // could not pipeline: launch the held pass, then this one
+      std::vector<TileCfg> hc(held.size(), cfgs[0]);
+      cudaError_t e = launch_stage(held, hc, pass == 1, s, nlaunch, rec);
+      if (e != cudaSuccess) return e;
+      held.clear();
+    }
     cudaError_t e = launch_stage(probs, cfgs, d == 0, s, nlaunch, rec);
     if (e != cudaSuccess) return e;
   }
@@ -511,7 +642,10 @@ extern "C" fdp_status fd_apply(fdp_fd h, const double* b, double* x, const doubl
     FDP_CUDA(launch_scale(b, x, dscale, h->N, batch, h->N, h->N, s), "fd_apply: prescale");
     src = x;
   }
-  FDP_CUDA(enqueue_fd({h}, {src}, h->N, {x}, h->N, {T}, {dscale}, batch, s, nullptr), "fd_apply");
+  const bool sy = batch <= h->sync_batch;
+  FDP_CUDA(enqueue_fd({h}, {src}, h->N, {x}, h->N, {T}, {dscale}, batch, s, nullptr, nullptr,
+                      nullptr, sy ? h->sync : nullptr, sy ? h->sync_cap : 0),
+           "fd_apply");
   return FDP_OK;
 }
 
@@ -727,6 +861,9 @@ struct fdp_block_s {
   void* g_ws = nullptr;
   int64_t g_batch = -1;
   cudaGraphExec_t exec = nullptr;
+  // plane-pipeline counters (zeroed at allocation, self-resetting)
+  int* sync = nullptr;
+  long long sync_cap = 0;
   // profiling
   bool prof = false;
   std::vector<cudaEvent_t> ev;
@@ -741,6 +878,7 @@ struct fdp_block_s {
 static void free_block(fdp_block h) {
   if (!h) return;
   for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
+  cudaFree(h->sync);
   if (h->exec) cudaGraphExecDestroy(h->exec);
   if (h->cap) cudaStreamDestroy(h->cap);
   cudaFree(h->dv);
@@ -941,7 +1079,10 @@ static cudaError_t enqueue_block(fdp_block h, const double* r, double* s, int64_
       (void)pass;
     };
   }
-  cudaError_t e = enqueue_fd(h->vel, in, sz, out, sz, T, dsc, batch, st, nlaunch, rec, hook);
+  const long long need = 2 * pp_sync_ints(h->vel, batch, h->pres_dense && D == 3 ? h->pres->n[2] : 0);
+  const bool sy = h->sync && h->sync_cap >= need;
+  cudaError_t e = enqueue_fd(h->vel, in, sz, out, sz, T, dsc, batch, st, nlaunch, rec, hook,
+                             sy ? h->sync : nullptr, sy ? need : 0);
   if (e != cudaSuccess) return e;
   if (!h->pres_dense) {
     // pressure block by banded per-mode solves: r_p -> s_p
@@ -1009,6 +1150,11 @@ extern "C" int fdp_block_launch_count(fdp_block h, int64_t batch) {
   for (int k = 0; k < D; ++k)
     for (int d = 0; d < D; ++d) fuse = fuse && h->vel[k]->n[d] <= kSmallMaxN && h->vel[k]->cfg[d].tiles_n == 1;
   if (fuse) n -= 1;
+  bool pp = fuse && D == 3 && std::getenv("FDP_PP") != nullptr;
+  for (int k = 0; k < D; ++k)
+    for (int d = 0; d < 2; ++d)
+      pp = pp && h->vel[k]->cfg[d].NT <= kPPMaxNT && h->vel[k]->cfg[d].NT == h->vel[0]->cfg[0].NT;
+  if (pp) n -= 2;
   if (!h->pres_dense) n += h->pres->D;
   else if (h->dall) n += h->dv ? 0 : 1;
   return n;
@@ -1031,6 +1177,20 @@ extern "C" fdp_status block_precond_apply(fdp_block h, const double* r, double* 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   FDP_CUDA(cudaStreamIsCapturing(st, &cs), "block_precond_apply: capture query");
+  if (!same && cs != cudaStreamCaptureStatusActive) {
+    const long long need =
+        2 * pp_sync_ints(h->vel, batch, h->pres_dense && h->D == 3 ? h->pres->n[2] : 0);
+    if (h->sync_cap < need) {
+      FDP_CUDA(cudaStreamSynchronize(st), "block_precond_apply: sync before realloc");
+      cudaFree(h->sync);
+      h->sync = nullptr;
+      h->sync_cap = 0;
+      fdp_status s2 = dalloc(&h->sync, (size_t)need);
+      if (s2) return s2;
+      FDP_CUDA(cudaMemset(h->sync, 0, need * sizeof(int)), "block_precond_apply: sync init");
+      h->sync_cap = need;
+    }
+  }
   if (cs == cudaStreamCaptureStatusActive) {
     FDP_CUDA(enqueue_block(h, r, s, batch, static_cast<double*>(workspace), st, nullptr),
              "block_precond_apply");

@@ -79,6 +79,21 @@ cudaError_t launch_mode_group(const ModeGroup& g, const TileCfg& cfg, bool kmaj,
 // backward in one pass (the middle of Algorithm 1). The caller fills prob[i].ctas
 // (CTAs per problem, sum = total_ctas) and prob[i].tiles_m = ceil(M/8).
 constexpr int kSmallMaxN = 96;
+constexpr int kPPMaxNT = 10;  // plane pipeline keeps two W tiles in shared memory
+
+// Per-plane completion counters of the plane pipeline (D = 3): problem i's counters start at
+// cnt + cnt_off[i] (batch * n3 ints); a phase-2 row's plane is row / rows_per_plane2[i] and is
+// ready when its counter reaches rows_per_plane1[i]. Self-resetting (last CTA zeroes them).
+struct PlaneSync {
+  int* cnt;
+  int* done;
+  int cnt_off[kMaxGroup];
+  int rows_per_plane1[kMaxGroup];
+  int rows_per_plane2[kMaxGroup];
+  int cnt_total;
+};
+cudaError_t launch_mode_pp(const ModeGroup& g1, const ModeGroup& g2, const PlaneSync& ps, int NT,
+                           bool kmaj1, cudaStream_t s);
 cudaError_t launch_mode_small(const ModeGroup& g, int NT, bool kmaj, cudaStream_t s);
 cudaError_t prepare_mode_small(int NT);
 

@@ -2,16 +2,23 @@
 //
 // Same arithmetic as K1 (Algorithm 1 steps 2-4; m-mode product P:389-398),
 // organised for the latency-bound small configs (configs 1-3: n = 32..68, <= 1.3 M dofs):
-//   * one persistent CTA per SM (8 warps); the problem's W = U_d (or U_d^T) is loaded into shared
+//   * one persistent CTA per SM (16 warps); the problem's W = U_d (or U_d^T) is loaded into shared
 //     memory once per CTA, before griddepcontrol.wait, so it overlaps the previous kernel's tail
 //     (programmatic dependent launch);
-//   * each warp streams 8-row A panels covering the whole K extent (one cp.async group per panel,
-//     double-buffered), computes the 8 x 8*NT output tile with NT independent DMMA accumulators
-//     per k4 step, and writes it through the epilogue;
-//   * work is balanced at 8-row granularity over all warps of the grid;
+//   * each warp owns 8-row tiles covering the whole K extent: loads the panel (LDG -> STS),
+//     computes the 8 x 8*NT output tile with NT independent DMMA accumulators per k4 step, and
+//     writes it through the epilogue; tiles are dealt round-robin over SMs first so every SM
+//     sub-partition gets within one tile of the same DMMA work;
 //   * EPI_FUSED: mode-D forward contraction, division by Lambda (step 3) and the mode-D
 //     backward contraction in one pass: the 8 x n intermediate stays in shared memory and the
-//     second GEMM reads U_D^T as a transposed view of the same W tile.
+//     second GEMM reads U_D^T as a transposed view of the same W tile;
+//   * mode_pp_kernel ("plane pipeline", D = 3): the mode-1 and mode-2 contractions of one
+//     direction (forward, or backward in reverse order) in ONE launch. Both contractions are
+//     local to an i3-plane, so a phase-2 tile only waits (per-plane completion counters,
+//     release/acquire) for the phase-1 rows of its plane(s): the loads, DMMAs and stores of the
+//     two passes overlap across warps instead of being separated by a kernel boundary.
+#include <cstdlib>
+
 #include "../fdp_internal.h"
 
 namespace fdp {
@@ -20,11 +27,6 @@ namespace {
 constexpr int SW = 16;          // warps per CTA (4 per SM sub-partition share its DMMA pipe)
 constexpr int STH = SW * 32;
 
-__device__ __forceinline__ void cp_async8z(void* smem, const void* gmem, bool valid) {
-  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  int sz = valid ? 8 : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
-}
 __device__ __forceinline__ void cp_async16g(void* smem, const void* gmem) {
   unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
@@ -42,8 +44,13 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "+d"(c[0]), "+d"(c[1])
                : "d"(a), "d"(b));
 }
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
-template <int NT, bool KMAJ>
+template <int NT>
 struct SS {
   static constexpr int BN = 8 * NT;
   static constexpr int KP = ((BN + 15) / 16) * 16;   // >= kpad of any n <= BN
@@ -52,11 +59,256 @@ struct SS {
   static constexpr int ABUF = 8 * SA;
   static constexpr int W_ELEMS = KP * SB;
   static constexpr size_t BYTES = sizeof(double) * (W_ELEMS + SW * ABUF);
+  static constexpr size_t BYTES_PP = sizeof(double) * (2 * W_ELEMS + SW * ABUF);
 };
+
+// Load W (rows 0..rows-1, cols 0..BN-1 of the padded global matrix) into shared memory.
+template <int NT>
+__device__ __forceinline__ void load_w(double* Ws, const ModeProb& pb, int tid) {
+  using S = SS<NT>;
+  const int kpad = ((pb.n + 15) / 16) * 16;
+  // the fused second GEMM reads W^T rows up to BN-1 as well
+  const int rows = (pb.epi == EPI_FUSED && S::BN > kpad) ? S::BN : kpad;
+  const int chunks = rows * (S::BN / 2);
+  for (int c = tid; c < chunks; c += STH) {
+    const int r = c / (S::BN / 2), cc = (c % (S::BN / 2)) * 2;
+    cp_async16g(&Ws[r * S::SB + cc], pb.W + (size_t)r * pb.ldw + cc);
+  }
+  commit();
+}
+
+// Geometry of one problem, per thread.
+struct Geo {
+  int n, P, Q, Pn, Mi, kpad, k4n, nch;
+  long long M;
+  __device__ explicit Geo(const ModeProb& pb) {
+    n = pb.n;
+    P = pb.P;
+    Q = pb.Q;
+    Pn = P * n;
+    Mi = P * Q;
+    M = (long long)Mi * pb.batch;
+    kpad = ((n + 15) / 16) * 16;
+    k4n = (n + 3) / 4;
+    nch = (kpad + 31) / 32;
+  }
+};
+
+// element offset of GEMM row m within its batch item (32-bit: the host routes here only problems
+// with M < 2^31) and the batch item index
+template <bool KMAJ>
+__device__ __forceinline__ void row_index(const Geo& g, int m, int& within, int& item) {
+  const unsigned b = (unsigned)m / (unsigned)g.Mi;
+  const int mi = m - (int)b * g.Mi;
+  if (KMAJ) {
+    within = g.n * mi;  // P == 1: row = fiber q = mi
+  } else {
+    const unsigned q = (unsigned)mi / (unsigned)g.P;
+    within = (mi - (int)q * g.P) + g.Pn * (int)q;
+  }
+  item = (int)b;
+}
+
+template <bool COHERENT>
+__device__ __forceinline__ double ldx(const double* p) {
+  return COHERENT ? __ldcg(p) : __ldg(p);
+}
+
+template <int NT, bool KMAJ>
+__device__ __forceinline__ void tile_compute_store(const ModeProb& pb, const Geo& g,
+                                                   const double* Ws, double* A, long long t,
+                                                   int lane, unsigned long long* tr);
+
+// Asynchronous panel load (8-byte cp.async with zero fill beyond n / M) into A ([8][SA]); one
+// commit group.
+__device__ __forceinline__ void cp_async8z(void* smem, const void* gmem, bool valid) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int sz = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+template <int NT, bool KMAJ>
+__device__ __forceinline__ void load_panel_async(const ModeProb& pb, const Geo& g, double* A,
+                                                 long long t, int lane) {
+  using S = SS<NT>;
+  const double* __restrict__ X = pb.X;
+  const int m0 = (int)(t * 8);
+  if (KMAJ) {
+    int w0, b0;
+    row_index<true>(g, m0, w0, b0);
+    int mi = w0 / g.n;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const bool rv = (long long)m0 + r < g.M;
+      const double* src = X + ((long long)g.n * mi + pb.xbs * b0);
+      for (int k = lane; k < g.kpad; k += 32) {
+        const bool v = rv && k < g.n;
+        cp_async8z(&A[r * S::SA + k], v ? src + k : X, v);
+      }
+      if (++mi == g.Mi) { mi = 0; ++b0; }
+    }
+  } else {
+    const int r = lane & 7;
+    const int m = m0 + r;
+    const bool rv = (long long)m < g.M;
+    int w = 0, b = 0;
+    if (rv) row_index<false>(g, m, w, b);
+    const double* src = X + (w + pb.xbs * b);
+    for (int k = lane >> 3; k < g.kpad; k += 4) {
+      const bool v = rv && k < g.n;
+      cp_async8z(&A[r * S::SA + k], v ? src + (long long)g.P * k : X, v);
+    }
+  }
+  commit();
+}
+
+// One 8-row tile: panel load (LDG -> STS, zero fill beyond n / M), DMMAs, epilogue.
+// COHERENT: the input was written earlier in the same launch (plane pipeline): L2-coherent loads.
+template <int NT, bool KMAJ, bool COHERENT>
+__device__ __forceinline__ void do_tile(const ModeProb& pb, const Geo& g, const double* Ws,
+                                        double* A, long long t, int lane,
+                                        unsigned long long* tr) {
+  using S = SS<NT>;
+  const double* __restrict__ X = pb.X;
+  const int m0 = (int)(t * 8);
+  if (KMAJ) {
+    int w0, b0;
+    row_index<true>(g, m0, w0, b0);
+    int mi = w0 / g.n;
+    const double* src[8];
+    bool rv[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      rv[r] = (long long)m0 + r < g.M;
+      src[r] = X + ((long long)g.n * mi + pb.xbs * b0);
+      if (++mi == g.Mi) { mi = 0; ++b0; }
+    }
+    double v[3][8];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int k = 32 * c + lane;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) v[c][r] = (c < g.nch && rv[r] && k < g.n) ? ldx<COHERENT>(src[r] + k) : 0.0;
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const int k = 32 * c + lane;
+      if (c < g.nch && k < g.kpad) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) A[r * S::SA + k] = v[c][r];
+      }
+    }
+  } else {
+    const int r = lane & 7;
+    const int m = m0 + r;
+    const bool rv = (long long)m < g.M;
+    int w = 0, b = 0;
+    if (rv) row_index<false>(g, m, w, b);
+    const double* src = X + (w + pb.xbs * b);
+    double v[24];
+#pragma unroll
+    for (int j = 0; j < 24; ++j) {
+      const int k = (lane >> 3) + 4 * j;
+      v[j] = (k < g.n && rv) ? ldx<COHERENT>(src + (long long)g.P * k) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < 24; ++j) {
+      const int k = (lane >> 3) + 4 * j;
+      if (k < g.kpad) A[r * S::SA + k] = v[j];
+    }
+  }
+  __syncwarp();
+  if (tr) tr[3] = gtimer();
+  tile_compute_store<NT, KMAJ>(pb, g, Ws, A, t, lane, tr);
+}
+
+template <int NT, bool KMAJ>
+__device__ __forceinline__ void tile_compute_store(const ModeProb& pb, const Geo& g,
+                                                   const double* Ws, double* A, long long t,
+                                                   int lane, unsigned long long* tr) {
+  using S = SS<NT>;
+  const int m0 = (int)(t * 8);
+  const int fr = lane >> 2, fc = lane & 3;
+  double acc[NT][2];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = 0.0;
+  for (int k4 = 0; k4 < g.k4n; ++k4) {
+    const int k = 4 * k4 + fc;
+    const double a = A[fr * S::SA + k];
+    double b[NT];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) b[j] = Ws[k * S::SB + 8 * j + fr];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) dmma(acc[j], a, b[j]);
+  }
+  if (tr) tr[4] = gtimer();
+
+  // row bookkeeping for the output row m = 8t + fr
+  const int m = m0 + fr;
+  const bool mv = (long long)m < g.M;
+  const bool FUSED = pb.epi == EPI_FUSED;
+  int sidx = 0, item = 0;
+  double lrow = 0.0;
+  if (mv) {
+    row_index<KMAJ>(g, m, sidx, item);
+    if (!KMAJ && (FUSED || pb.epi == EPI_LAMBDA)) {
+      const int mi = m - item * g.Mi;
+      const int p = mi - (int)((unsigned)mi / (unsigned)g.P) * g.P;
+      if (pb.lam1) {
+        const unsigned i2 = (unsigned)p / (unsigned)pb.n1;
+        lrow = pb.lam0[p - (int)i2 * pb.n1] + pb.lam1[i2];
+      } else {
+        lrow = pb.lam0[p];
+      }
+    }
+  }
+
+  if (FUSED) {
+    // T = acc / Lambda -> this warp's panel buffer ([8][SA]); zero beyond n.
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int a = 8 * j + 2 * fc + h;
+        A[fr * S::SA + a] = (mv && a < g.n) ? acc[j][h] / (lrow + pb.lamcol[a]) : 0.0;
+      }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = 0.0;
+    for (int k4 = 0; k4 < g.k4n; ++k4) {
+      const int k = 4 * k4 + fc;
+      const double a = A[fr * S::SA + k];
+      double b[NT];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) b[j] = Ws[(8 * j + fr) * S::SB + k];  // (U^T)[k][a] = U[a][k]
+#pragma unroll
+      for (int j = 0; j < NT; ++j) dmma(acc[j], a, b[j]);
+    }
+  }
+
+  if (mv) {
+    double* __restrict__ Y = pb.Y + pb.ybs * (long long)item + sidx;
+    const int epi = FUSED ? EPI_NONE : pb.epi;
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int a = 8 * j + 2 * fc + h;
+        if (a < g.n) {
+          double v = acc[j][h];
+          if (epi == EPI_LAMBDA) v = v / (lrow + pb.lamcol[a]);
+          else if (epi == EPI_SCALE) v = v * pb.scale[sidx + g.P * a];
+          Y[g.P * a] = v;
+        }
+      }
+  }
+  __syncwarp();  // all lanes done with the panel before it is refilled
+  if (tr) tr[5] = gtimer();
+}
 
 template <int NT, bool KMAJ>
 __global__ void __launch_bounds__(STH, 1) mode_small_kernel(const __grid_constant__ ModeGroup grp) {
-  using S = SS<NT, KMAJ>;
+  using S = SS<NT>;
   extern __shared__ __align__(16) double sm[];
   double* Ws = sm;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -67,184 +319,208 @@ __global__ void __launch_bounds__(STH, 1) mode_small_kernel(const __grid_constan
   for (int i = 1; i < kMaxGroup; ++i)
     if (i < grp.count && (int)blockIdx.x >= grp.prob[i].cta_begin) pi = i;
   const ModeProb& pb = grp.prob[pi];
-  const int n = pb.n, P = pb.P, Qn = pb.Q;
-  const int Pn = P * n;                       // < 2^31: the host routes only small tensors here
-  const int Mi = P * Qn;                      // rows per batch item
-  const long long M = (long long)Mi * pb.batch;
-  const int kpad = ((n + 15) / 16) * 16;
-  const int k4n = (n + 3) / 4;
+  const Geo g(pb);
 
   unsigned long long* trace = grp.trace ? grp.trace + ((size_t)blockIdx.x * SW + warp) * kTracePhases : nullptr;
   if (trace && lane == 0) trace[0] = gtimer();
-  // ---- W (independent of the previous kernel): rows 0..kpad-1, cols 0..BN-1 ----
-  {
-    const double* W = pb.W;
-    const int ldw = pb.ldw;
-    // rows needed: kpad for x_d W; the fused second GEMM reads W^T rows up to BN-1 as well
-    const int rows = (pb.epi == EPI_FUSED && S::BN > kpad) ? S::BN : kpad;
-    const int chunks = rows * (S::BN / 2);
-    for (int c = tid; c < chunks; c += STH) {
-      const int r = c / (S::BN / 2), cc = (c % (S::BN / 2)) * 2;
-      cp_async16g(&Ws[r * S::SB + cc], W + (size_t)r * ldw + cc);
-    }
-    commit();
-  }
+  load_w<NT>(Ws, pb, tid);  // independent of the previous kernel
   // PDL: everything below may read what the previous kernel wrote.
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   if (trace && lane == 0) trace[1] = gtimer();
-
-  const double* __restrict__ X = pb.X;
-  // tile t -> CTA t % ctas, then warp (t / ctas) % SW: consecutive tiles land on different SMs,
-  // so every SM sub-partition gets within one tile of the same DMMA work.
-  const int gw = (blockIdx.x - pb.cta_begin) + pb.ctas * warp;
-  const int nw = pb.ctas * SW;
-  const long long ntiles = pb.tiles_m;
-
-  // element offset of GEMM row m within its batch item, and the item's offset for tensor `bs`
-  auto row_index = [&](long long m, int& within, long long& item) {
-    const int b = (int)(m / Mi);
-    const int mi = (int)(m - (long long)b * Mi);
-    if (KMAJ) {
-      within = n * mi;                       // P == 1: row = fiber q = mi
-    } else {
-      const int q = mi / P, p = mi - q * P;
-      within = p + Pn * q;
-    }
-    item = b;
-  };
-
-  auto load_panel = [&](long long t) {
-    const long long m0 = t * 8;
-    if (KMAJ) {
-#pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        const long long m = m0 + r;
-        const bool rv = m < M;
-        int w = 0;
-        long long b = 0;
-        if (rv) row_index(m, w, b);
-        const double* src = X + (w + pb.xbs * b);
-        for (int k = lane; k < kpad; k += 32)
-          cp_async8z(&A[r * S::SA + k], rv && k < n ? src + k : X, rv && k < n);
-      }
-    } else {
-      const int r = lane & 7;
-      const long long m = m0 + r;
-      const bool rv = m < M;
-      int w = 0;
-      long long b = 0;
-      if (rv) row_index(m, w, b);
-      const double* src = X + (w + pb.xbs * b);
-      for (int k = lane >> 3; k < kpad; k += 4)
-        cp_async8z(&A[r * S::SA + k], rv && k < n ? src + (long long)P * k : X, rv && k < n);
-    }
-    commit();
-  };
-
-  const int fr = lane >> 2, fc = lane & 3;
-  const bool FUSED = pb.epi == EPI_FUSED;  // uniform per CTA (one problem per CTA)
-  wait_group<0>();  // W landed (this thread's part)
+  wait_group<0>();
   __syncthreads();  // W visible to all warps
   if (trace && lane == 0) trace[2] = gtimer();
 
-  for (long long t = gw; t < ntiles; t += nw) {
-    load_panel(t);
-    wait_group<0>();
+  // tile t -> CTA t % ctas, then warp (t / ctas) % SW
+  const int gw = (blockIdx.x - pb.cta_begin) + pb.ctas * warp;
+  const int nw = pb.ctas * SW;
+  for (long long t = gw; t < pb.tiles_m; t += nw)
+    do_tile<NT, KMAJ, false>(pb, g, Ws, A, t, lane, (trace && lane == 0 && t == gw) ? trace : nullptr);
+}
+
+// Prefetching variant: SWP = 8 warps per CTA, two panels per warp; the next tile's panel streams
+// in (cp.async) while the current tile's DMMAs and epilogue run.
+constexpr int SWP = 8;
+template <int NT>
+constexpr size_t bytes_prefetch() { return sizeof(double) * (SS<NT>::W_ELEMS + SWP * 2 * SS<NT>::ABUF); }
+
+template <int NT, bool KMAJ>
+__global__ void __launch_bounds__(SWP * 32, 1)
+mode_small_pf_kernel(const __grid_constant__ ModeGroup grp) {
+  using S = SS<NT>;
+  extern __shared__ __align__(16) double sm[];
+  double* Ws = sm;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* A0 = sm + S::W_ELEMS + warp * 2 * S::ABUF;
+
+  int pi = 0;
+#pragma unroll
+  for (int i = 1; i < kMaxGroup; ++i)
+    if (i < grp.count && (int)blockIdx.x >= grp.prob[i].cta_begin) pi = i;
+  const ModeProb& pb = grp.prob[pi];
+  const Geo g(pb);
+  unsigned long long* trace = grp.trace ? grp.trace + ((size_t)blockIdx.x * SW + warp) * kTracePhases : nullptr;
+  if (trace && lane == 0) trace[0] = gtimer();
+  {  // W: all threads, own group
+    const int kpad = g.kpad;
+    const int rows = (pb.epi == EPI_FUSED && S::BN > kpad) ? S::BN : kpad;
+    const int chunks = rows * (S::BN / 2);
+    for (int c = tid; c < chunks; c += SWP * 32) {
+      const int r = c / (S::BN / 2), cc = (c % (S::BN / 2)) * 2;
+      cp_async16g(&Ws[r * S::SB + cc], pb.W + (size_t)r * pb.ldw + cc);
+    }
+    commit();
+  }
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  if (trace && lane == 0) trace[1] = gtimer();
+
+  const int gw = (blockIdx.x - pb.cta_begin) + pb.ctas * warp;
+  const int nw = pb.ctas * SWP;
+  long long t = gw;
+  if (t < pb.tiles_m) load_panel_async<NT, KMAJ>(pb, g, A0, t, lane);
+  wait_group<0>();  // W and the first panel
+  __syncthreads();
+  if (trace && lane == 0) trace[2] = gtimer();
+  int buf = 0;
+  for (; t < pb.tiles_m; t += nw) {
+    double* A = A0 + buf * S::ABUF;
+    const long long tn = t + nw;
+    if (tn < pb.tiles_m) {
+      load_panel_async<NT, KMAJ>(pb, g, A0 + (buf ^ 1) * S::ABUF, tn, lane);
+      wait_group<1>();
+    } else {
+      wait_group<0>();
+    }
     __syncwarp();
-    const bool tr = trace && lane == 0 && t == gw;
-    if (tr) trace[3] = gtimer();
+    unsigned long long* tr = (trace && lane == 0 && t == gw) ? trace : nullptr;
+    if (tr) tr[3] = gtimer();
+    tile_compute_store<NT, KMAJ>(pb, g, Ws, A, t, lane, tr);
+    buf ^= 1;
+  }
+}
 
-    double acc[NT][2];
-#pragma unroll
-    for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = 0.0;
-    for (int k4 = 0; k4 < k4n; ++k4) {
-      const int k = 4 * k4 + fc;
-      const double a = A[fr * S::SA + k];
-      double b[NT];
-#pragma unroll
-      for (int j = 0; j < NT; ++j) b[j] = Ws[k * S::SB + 8 * j + fr];
-#pragma unroll
-      for (int j = 0; j < NT; ++j) dmma(acc[j], a, b[j]);
-    }
+// ------------------------------------------------------------------------------------------------
+// plane pipeline: phase 1 = grp1 (mode a), phase 2 = grp2 (mode b) of the same problems, D = 3.
+// ------------------------------------------------------------------------------------------------
+template <int NT, bool KMAJ1, bool KMAJ2>
+__global__ void __launch_bounds__(STH, 1)
+mode_pp_kernel(const __grid_constant__ ModeGroup grp1, const __grid_constant__ ModeGroup grp2,
+               const __grid_constant__ PlaneSync ps) {
+  using S = SS<NT>;
+  extern __shared__ __align__(16) double sm[];
+  double* W1 = sm;
+  double* W2 = sm + S::W_ELEMS;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* A = sm + 2 * S::W_ELEMS + warp * S::ABUF;
 
-    if (tr) trace[4] = gtimer();
-    // row bookkeeping for the output row m = 8t + fr
-    const long long m = t * 8 + fr;
-    const bool mv = m < M;
-    int sidx = 0;
-    long long item = 0;
-    double lrow = 0.0;
-    if (mv) {
-      row_index(m, sidx, item);
-      if (!KMAJ && (FUSED || pb.epi == EPI_LAMBDA)) {
-        const int p = (int)((m - item * Mi) % P);
-        lrow = pb.lam1 ? pb.lam0[p % pb.n1] + pb.lam1[p / pb.n1] : pb.lam0[p];
+  int pi = 0;
+#pragma unroll
+  for (int i = 1; i < kMaxGroup; ++i)
+    if (i < grp1.count && (int)blockIdx.x >= grp1.prob[i].cta_begin) pi = i;
+  const ModeProb& p1 = grp1.prob[pi];
+  const ModeProb& p2 = grp2.prob[pi];
+  const Geo g1(p1), g2(p2);
+  int* cnt = ps.cnt + ps.cnt_off[pi];
+  const int rpp1 = ps.rows_per_plane1[pi], rpp2 = ps.rows_per_plane2[pi];
+
+  load_w<NT>(W1, p1, tid);
+  load_w<NT>(W2, p2, tid);
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  wait_group<0>();
+  __syncthreads();
+
+  const int gw = (blockIdx.x - p1.cta_begin) + p1.ctas * warp;
+  const int nw = p1.ctas * SW;
+  // phase 1: never waits, so every phase-1 tile completes (no deadlock whatever the schedule)
+  for (long long t = gw; t < p1.tiles_m; t += nw) {
+    do_tile<NT, KMAJ1, false>(p1, g1, W1, A, t, lane, nullptr);
+    // publish: rows of this tile per plane (a tile spans at most two planes since rpp1 >= 8
+    // is not required: loop over the rows' planes)
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) {
+      const long long r0 = t * 8, r1 = min(g1.M, r0 + 8);
+      long long r = r0;
+      while (r < r1) {
+        const long long plane = r / rpp1;
+        const long long end = min(r1, (plane + 1) * rpp1);
+        atomicAdd(&cnt[plane], (int)(end - r));
+        r = end;
       }
     }
-
-    if (FUSED) {
-      // T = acc / Lambda -> this warp's panel buffer ([8][SA]); zero beyond n.
-      __syncwarp();
-#pragma unroll
-      for (int j = 0; j < NT; ++j)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int a = 8 * j + 2 * fc + h;
-          A[fr * S::SA + a] = (mv && a < n) ? acc[j][h] / (lrow + pb.lamcol[a]) : 0.0;
-        }
-      __syncwarp();
-#pragma unroll
-      for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = 0.0;
-      for (int k4 = 0; k4 < k4n; ++k4) {
-        const int k = 4 * k4 + fc;
-        const double a = A[fr * S::SA + k];
-        double b[NT];
-#pragma unroll
-        for (int j = 0; j < NT; ++j) b[j] = Ws[(8 * j + fr) * S::SB + k];  // (U^T)[k][a] = U[a][k]
-#pragma unroll
-        for (int j = 0; j < NT; ++j) dmma(acc[j], a, b[j]);
-      }
+  }
+  // phase 2: wait for the planes this tile reads, then consume with L2-coherent loads
+  for (long long t = gw; t < p2.tiles_m; t += nw) {
+    if (lane == 0) {
+      const long long r0 = t * 8, r1 = min(g2.M, r0 + 8);
+      const long long pa = r0 / rpp2, pb_ = (r1 - 1) / rpp2;
+      for (long long pl = pa; pl <= pb_; ++pl)
+        while (ld_acquire(&cnt[pl]) < rpp1) __nanosleep(64);
     }
+    __syncwarp();
+    do_tile<NT, KMAJ2, true>(p2, g2, W2, A, t, lane, nullptr);
+  }
 
-    if (mv) {
-      double* __restrict__ Y = pb.Y + pb.ybs * item + sidx;
-      const int epi = FUSED ? EPI_NONE : pb.epi;
-#pragma unroll
-      for (int j = 0; j < NT; ++j)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int a = 8 * j + 2 * fc + h;
-          if (a < n) {
-            double v = acc[j][h];
-            if (epi == EPI_LAMBDA) v = v / (lrow + pb.lamcol[a]);
-            else if (epi == EPI_SCALE) v = v * pb.scale[sidx + P * a];
-            Y[P * a] = v;
-          }
-        }
+  // self-reset: the last CTA to finish zeroes the counters for the next application
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const int done = atomicAdd(ps.done, 1);
+    if (done == gridDim.x - 1) {
+      for (int i = 0; i < ps.cnt_total; ++i) ps.cnt[i] = 0;
+      __threadfence();
+      *ps.done = 0;
     }
-    __syncwarp();  // all lanes done with the panel before it is refilled
-    if (tr) trace[5] = gtimer();
   }
 }
 
 template <int NT, bool KMAJ>
 cudaError_t launch_s(const ModeGroup* g, cudaStream_t s) {
-  using S = SS<NT, KMAJ>;
-  if (!g)
-    return cudaFuncSetAttribute(mode_small_kernel<NT, KMAJ>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES);
+  using S = SS<NT>;
+  // 16 single-buffered warps beat 8 double-buffered ones at these sizes (measured, r01), so the
+  // prefetching variant is opt-in (FDP_SMALL_PF=1)
+  const bool pf = bytes_prefetch<NT>() <= 227 * 1024 && std::getenv("FDP_SMALL_PF") != nullptr;
+  if (!g) {
+    cudaError_t e = cudaFuncSetAttribute(mode_small_kernel<NT, KMAJ>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES);
+    if (e != cudaSuccess || bytes_prefetch<NT>() > 227 * 1024) return e;
+    return cudaFuncSetAttribute(mode_small_pf_kernel<NT, KMAJ>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes_prefetch<NT>());
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(g->total_ctas);
-  cfg.blockDim = dim3(STH);
-  cfg.dynamicSmemBytes = S::BYTES;
+  cfg.blockDim = dim3(pf ? SWP * 32 : STH);
+  cfg.dynamicSmemBytes = pf ? bytes_prefetch<NT>() : S::BYTES;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (pf) return cudaLaunchKernelEx(&cfg, mode_small_pf_kernel<NT, KMAJ>, *g);
   return cudaLaunchKernelEx(&cfg, mode_small_kernel<NT, KMAJ>, *g);
+}
+
+template <int NT, bool K1, bool K2>
+cudaError_t launch_pp(const ModeGroup* g1, const ModeGroup* g2, const PlaneSync* ps, cudaStream_t s) {
+  using S = SS<NT>;
+  if (!g1)
+    return cudaFuncSetAttribute(mode_pp_kernel<NT, K1, K2>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES_PP);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(g1->total_ctas);
+  cfg.blockDim = dim3(STH);
+  cfg.dynamicSmemBytes = S::BYTES_PP;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, mode_pp_kernel<NT, K1, K2>, *g1, *g2, *ps);
 }
 
 template <bool KMAJ>
@@ -266,6 +542,24 @@ cudaError_t dispatch_small(const ModeGroup* g, int NT, cudaStream_t s) {
   }
 }
 
+template <bool K1, bool K2>
+cudaError_t dispatch_pp(const ModeGroup* g1, const ModeGroup* g2, const PlaneSync* ps, int NT,
+                        cudaStream_t s) {
+  switch (NT) {
+    case 1: return launch_pp<1, K1, K2>(g1, g2, ps, s);
+    case 2: return launch_pp<2, K1, K2>(g1, g2, ps, s);
+    case 3: return launch_pp<3, K1, K2>(g1, g2, ps, s);
+    case 4: return launch_pp<4, K1, K2>(g1, g2, ps, s);
+    case 5: return launch_pp<5, K1, K2>(g1, g2, ps, s);
+    case 6: return launch_pp<6, K1, K2>(g1, g2, ps, s);
+    case 7: return launch_pp<7, K1, K2>(g1, g2, ps, s);
+    case 8: return launch_pp<8, K1, K2>(g1, g2, ps, s);
+    case 9: return launch_pp<9, K1, K2>(g1, g2, ps, s);
+    case 10: return launch_pp<10, K1, K2>(g1, g2, ps, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_mode_small(const ModeGroup& g, int NT, bool kmaj, cudaStream_t s) {
@@ -273,10 +567,22 @@ cudaError_t launch_mode_small(const ModeGroup& g, int NT, bool kmaj, cudaStream_
   return kmaj ? dispatch_small<true>(&g, NT, s) : dispatch_small<false>(&g, NT, s);
 }
 
+cudaError_t launch_mode_pp(const ModeGroup& g1, const ModeGroup& g2, const PlaneSync& ps, int NT,
+                           bool kmaj1, cudaStream_t s) {
+  if (g1.total_ctas <= 0) return cudaSuccess;
+  return kmaj1 ? dispatch_pp<true, false>(&g1, &g2, &ps, NT, s)
+               : dispatch_pp<false, true>(&g1, &g2, &ps, NT, s);
+}
+
 cudaError_t prepare_mode_small(int NT) {
   cudaError_t e;
   if ((e = dispatch_small<true>(nullptr, NT, 0)) != cudaSuccess) return e;
-  return dispatch_small<false>(nullptr, NT, 0);
+  if ((e = dispatch_small<false>(nullptr, NT, 0)) != cudaSuccess) return e;
+  if (NT <= kPPMaxNT) {
+    if ((e = dispatch_pp<true, false>(nullptr, nullptr, nullptr, NT, 0)) != cudaSuccess) return e;
+    if ((e = dispatch_pp<false, true>(nullptr, nullptr, nullptr, NT, 0)) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace fdp

@@ -180,7 +180,7 @@ def test_block_precond_config4_full_size_bench_launch():
 
 
 @pytest.mark.parametrize("env", [{"FDP_NO_SMALL": "1"}, {"FDP_NO_FUSE": "1"}, {"FDP_PRESSURE": "banded"},
-                                 {"FDP_PRESSURE": "dense"}, {}])
+                                 {"FDP_PRESSURE": "dense"}, {"FDP_PP": "1"}, {"FDP_SMALL_PF": "1"}, {}])
 @pytest.mark.parametrize("cfg_id", [1, 2, 3])
 def test_block_precond_kernel_paths(cfg_id, env, monkeypatch):
     """Every kernel path (big/small K1, fused middle, banded/dense P_Q) against the oracle."""
@@ -200,19 +200,40 @@ def test_block_precond_kernel_paths(cfg_id, env, monkeypatch):
             assert rel(s[i, o[k]:o[k + 1]], ref[i, o[k]:o[k + 1]]) < TOL, (cfg_id, env, k)
 
 
-@pytest.mark.parametrize("dims", [(96, 5, 7), (8, 96, 33), (17, 3, 96), (9, 11)])
+@pytest.mark.parametrize("dims", [(96, 5, 7), (8, 96, 33), (17, 3, 96), (9, 11), (65, 65, 65), (7, 9, 1),
+                                  (3, 2, 40)])
 def test_fd_apply_small_path_edges(dims):
-    """n = 96 (largest small-path extent), tiny extents, 2D; fused middle + in-place pass 0."""
+    """n = 96 (largest small-path extent), tiny extents, 2D; fused middle + in-place pass 0,
+    plane pipeline with a handle-owned counter set (max_batch = 3)."""
     rng = np.random.default_rng(sum(dims))
     Ks = [_rand_spd(n, rng, 1.0) for n in dims]
     Ms = [_rand_spd(n, rng, 2.0) for n in dims]
     coef = [1.0 + 0.5 * d for d in range(len(dims))]
     N = int(np.prod(dims))
     b = rng.standard_normal((3, N))
-    S = fdp.FD(Ks, Ms, coef)
+    S = fdp.FD(Ks, Ms, coef, max_batch=3)
     bt = dev(b)
     S.apply(bt, bt, batch=3)
     ref = ofd.FDSolver(Ks, Ms, coef)
     x = bt.cpu().numpy()
     for i in range(3):
         assert rel(x[i], ref.apply(b[i])) < TOL
+
+
+def test_plane_pipeline_repeated_applies_and_batch_growth(monkeypatch):
+    """Self-resetting plane counters: many applies in a row, then a larger batch (re-allocation)."""
+    monkeypatch.setenv("FDP_PP", "1")
+    w, od, gd = _both(2)
+    P = fdp.build_block(gd)
+    ref = oprec.BlockPrecond(od)
+    rng = np.random.default_rng(21)
+    for batch in (1, 1, 3):
+        r = rng.standard_normal((batch, od.n_total))
+        rt = dev(r)
+        st = torch.empty_like(rt)
+        ws = P.workspace(batch)
+        for _ in range(5):
+            P.apply(rt, st, batch=batch, workspace=ws)
+        s = st.cpu().numpy()
+        for i in range(batch):
+            assert rel(s[i], ref.apply(r[i])) < TOL
