@@ -179,6 +179,37 @@ fdp_status block_precond_profile(fdp_block h, int enable);
 int block_precond_profile_read(fdp_block h, int max, int32_t* kind, float* ms, double* flops,
                                double* bytes);
 
+/* ------------------------------------------------------------------------------------------
+ * Slab decomposition for multi-GPU application: the slowest axis i3
+ * is partitioned over `nranks` ranks (even split, the first n mod G ranks own one more plane).
+ * Modes 1-2 are local to an i3-slab; mode 3 runs on i2-slabs after an all-to-all exchange (done
+ * by the caller, e.g. NCCL over NVLink through torch.distributed) and is followed by the reverse
+ * exchange. Batch 1. Rank r's pieces:
+ *   z-slab (n1, n2, nz_r), planes [z0_r, z0_r + nz_r);  y-slab (n1, ny_r, n3), i2 in [y0_r, ...).
+ *   A "piece buffer" of rank g holds, for every rank h in order, the block
+ *   [i3 local][i2 - y0_h][i1] of size n1*ny_h*nz_g at offset n1*nz_g*y0_h.
+ * Exchange 1 sends piece h of every rank's forward output to rank h; concatenating what rank h
+ * receives, in source-rank order, IS its y-slab. Exchange 2 sends the contiguous planes
+ * [z0_g, z0_g+nz_g) of every y-slab back to rank g, forming rank g's piece buffer.
+ * ------------------------------------------------------------------------------------------ */
+fdp_status fdp_slab_range(int64_t n, int nranks, int rank, int64_t* lo, int64_t* len);
+
+/* FD phases (D = 3): phase 0 (fwd): in = b z-slab, out = piece buffer, dscale = D^{-1/2} on the
+ * z-slab or NULL; computes x_1 U_1^T, x_2 U_2^T. Phase 1 (mid): in = out = y-slab (in place);
+ * computes x_3 U_3^T, / Lambda, x_3 U_3 (Algorithm 1 steps 2-4 on the mode-3 fibers).
+ * Phase 2 (bwd): in = piece buffer received in exchange 2, out = x z-slab; computes x_2 U_2,
+ * x_1 U_1 and the post-scaling. workspace >= fd_slab_workspace_bytes(h, nranks, rank). */
+size_t fd_slab_workspace_bytes(fdp_fd h, int nranks, int rank);
+fdp_status fd_apply_slab(fdp_fd h, int phase, int nranks, int rank, const double* in, double* out,
+                         const double* dscale, void* workspace, void* stream);
+
+/* Kronecker mass inverse phases (banded solves): phase 0: modes 1-2 on the z-slab
+ * (pre-scaling) then pack; phase 1: mode 3 on the y-slab in place; phase 2: unpack (post-scaling
+ * with dscale on the z-slab). */
+size_t kron_mass_slab_workspace_bytes(fdp_mass h, int nranks, int rank);
+fdp_status kron_mass_apply_slab(fdp_mass h, int phase, int nranks, int rank, const double* in,
+                                double* out, const double* dscale, void* workspace, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -65,6 +65,11 @@ def _load():
         "block_precond_destroy": (i32, [vp]),
         "fdp_block_launch_count": (i32, [vp, i64]),
         "block_precond_profile": (i32, [vp, i32]),
+        "fdp_slab_range": (i32, [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
+        "fd_slab_workspace_bytes": (sz, [vp, i32, i32]),
+        "fd_apply_slab": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, vp]),
+        "kron_mass_slab_workspace_bytes": (sz, [vp, i32, i32]),
+        "kron_mass_apply_slab": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, vp]),
         "block_precond_profile_read": (i32, [vp, i32, vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
@@ -205,6 +210,28 @@ class FD:
             self.close()
         except Exception:
             pass
+
+
+def slab_range(n: int, nranks: int, rank: int):
+    """(lo, len) of rank's share of an axis of length n (fdp_slab_range)."""
+    lo, ln = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib.fdp_slab_range(n, nranks, rank, ctypes.byref(lo), ctypes.byref(ln)))
+    return lo.value, ln.value
+
+
+def fd_apply_slab(h, phase: int, nranks: int, rank: int, x_in, x_out, dscale, workspace, stream=None):
+    """libfdp slab phase (0 fwd + pack, 1 mid in place, 2 unpack + bwd); see include/fdp.h."""
+    _check(lib.fd_apply_slab(h.h, phase, nranks, rank, _dev(x_in, "in"), _dev(x_out, "out"),
+                             None if dscale is None else _dev(dscale, "dscale"),
+                             _dev(workspace, "workspace"), _stream(stream)))
+
+
+def kron_mass_apply_slab(h, phase: int, nranks: int, rank: int, x_in, x_out, dscale, workspace,
+                         stream=None):
+    _check(lib.kron_mass_apply_slab(h.h, phase, nranks, rank, _dev(x_in, "in"), _dev(x_out, "out"),
+                                    None if dscale is None else _dev(dscale, "dscale"),
+                                    None if workspace is None else _dev(workspace, "workspace"),
+                                    _stream(stream)))
 
 
 class KronMass:

@@ -360,6 +360,7 @@ static void alloc_small_ctas(ModeGroup& g, const std::vector<double>& w) {
   const int total = num_sms();
   double wsum = 0.0;
   for (int j = 0; j < g.count; ++j) wsum += w[j];
+  if (!(wsum > 0.0)) wsum = 1.0;
   int used = 0;
   for (int j = 0; j < g.count; ++j) {
     ModeProb& p = g.prob[j];
@@ -405,8 +406,16 @@ static double recorded_bytes(const ModeProb& p) {
 static unsigned long long* g_trace = nullptr;
 static size_t g_trace_cap = 0, g_trace_used = 0;
 
-static cudaError_t launch_stage(std::vector<ModeProb>& probs, const std::vector<TileCfg>& cfgs,
+static cudaError_t launch_stage(std::vector<ModeProb>& probs_in, const std::vector<TileCfg>& cfgs_in,
                                 bool kmaj, cudaStream_t s, int* nlaunch, Recorder* rec) {
+  // drop empty problems (e.g. a rank that owns no plane of a short axis)
+  std::vector<ModeProb> probs;
+  std::vector<TileCfg> cfgs;
+  for (size_t i = 0; i < probs_in.size(); ++i)
+    if ((long long)probs_in[i].P * probs_in[i].Q * probs_in[i].batch > 0) {
+      probs.push_back(probs_in[i]);
+      cfgs.push_back(cfgs_in[i]);
+    }
   std::vector<bool> done(probs.size(), false);
   for (size_t i = 0; i < probs.size(); ++i) {
     if (done[i]) continue;
@@ -1270,4 +1279,178 @@ extern "C" int fdp_debug_trace(unsigned long long* dev_buf, size_t cap) {
   g_trace_cap = dev_buf ? cap : 0;
   g_trace_used = 0;
   return 0;
+}
+
+// ------------------------------------------------------------------------------------------------
+// slab decomposition (multi-GPU phases)
+// ------------------------------------------------------------------------------------------------
+static void part_range(long long n, int G, int r, long long* lo, long long* len) {
+  const long long q = n / G, rem = n % G;
+  *lo = r * q + std::min<long long>(r, rem);
+  *len = q + (r < rem ? 1 : 0);
+}
+
+extern "C" fdp_status fdp_slab_range(int64_t n, int nranks, int rank, int64_t* lo, int64_t* len) {
+  if (nranks < 1 || rank < 0 || rank >= nranks || n < 0 || !lo || !len)
+    return fail(FDP_ERR_INVALID_ARG, "fdp_slab_range: bad arguments");
+  long long a, b;
+  part_range(n, nranks, rank, &a, &b);
+  *lo = a;
+  *len = b;
+  return FDP_OK;
+}
+
+extern "C" size_t fd_slab_workspace_bytes(fdp_fd h, int nranks, int rank) {
+  if (!h || h->D != 3 || nranks < 1 || rank < 0 || rank >= nranks) return 0;
+  long long z0, nz, y0, ny;
+  part_range(h->n[2], nranks, rank, &z0, &nz);
+  part_range(h->n[1], nranks, rank, &y0, &ny);
+  const long long zs = (long long)h->n[0] * h->n[1] * nz, ys = (long long)h->n[0] * ny * h->n[2];
+  return (size_t)std::max(2 * zs, ys) * sizeof(double);
+}
+
+// Mode contraction of a (P, n, Q) view with the handle's direction-d matrices (batch 1).
+static ModeProb slab_prob(const fdp_fd_s* h, int d, bool fwd, const double* X, double* Y,
+                          long long P, long long Q, int epi, const double* scale,
+                          const double* lam1) {
+  ModeProb p{};
+  p.X = X;
+  p.Y = Y;
+  p.W = fwd ? h->Wf[d] : h->Wb[d];
+  p.P = (int)P;
+  p.n = h->n[d];
+  p.Q = (int)Q;
+  p.N = P * h->n[d] * Q;
+  p.xbs = p.ybs = 0;
+  p.batch = 1;
+  p.ldw = h->cfg[d].ldw;
+  p.n1 = h->n[0];
+  p.epi = epi;
+  p.scale = scale;
+  if (epi == EPI_LAMBDA || epi == EPI_FUSED) {
+    p.lam0 = h->lamc[0];
+    p.lam1 = lam1;
+    p.lamcol = h->lamc[2];
+  }
+  const int BM = 4 * 8 * h->cfg[d].MT;
+  p.tiles_m = (int)((P * Q + BM - 1) / BM);
+  p.tiles_n = h->cfg[d].tiles_n;
+  p.fd_work = 1;
+  return p;
+}
+
+static cudaError_t run1(ModeProb p, const TileCfg& c, bool kmaj, cudaStream_t s) {
+  std::vector<ModeProb> v{p};
+  std::vector<TileCfg> cv{c};
+  return launch_stage(v, cv, kmaj, s, nullptr, nullptr);
+}
+
+extern "C" fdp_status fd_apply_slab(fdp_fd h, int phase, int nranks, int rank, const double* in,
+                                    double* out, const double* dscale, void* workspace,
+                                    void* stream) {
+  if (!h) return fail(FDP_ERR_INVALID_ARG, "fd_apply_slab: NULL handle");
+  if (h->D != 3) return fail(FDP_ERR_UNSUPPORTED, "fd_apply_slab: D must be 3");
+  if (nranks < 1 || rank < 0 || rank >= nranks || phase < 0 || phase > 2)
+    return fail(FDP_ERR_INVALID_ARG, "fd_apply_slab: bad phase / rank");
+  const long long n1 = h->n[0], n2 = h->n[1], n3 = h->n[2];
+  long long z0, nz, y0, ny;
+  part_range(n3, nranks, rank, &z0, &nz);
+  part_range(n2, nranks, rank, &y0, &ny);
+  if ((phase == 1 ? ny : nz) == 0) return FDP_OK;  // this rank owns nothing of that axis
+  if (!is_device_ptr(in) || !is_device_ptr(out) || !is_device_ptr(workspace) ||
+      (dscale && !is_device_ptr(dscale)))
+    return fail(FDP_ERR_INVALID_ARG, "fd_apply_slab: device pointers required");
+  DeviceGuard dg(h->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double* T1 = static_cast<double*>(workspace);
+  double* T2 = T1 + n1 * n2 * nz;
+  if (phase == 0) {
+    const double* src = in;
+    if (dscale) {
+      FDP_CUDA(launch_scale(in, T2, dscale, n1 * n2 * nz, 1, 0, 0, s), "fd_apply_slab: prescale");
+      src = T2;
+    }
+    FDP_CUDA(run1(slab_prob(h, 0, true, src, T1, 1, n2 * nz, EPI_NONE, nullptr, nullptr), h->cfg[0], true, s),
+             "fd_apply_slab: mode 1");
+    FDP_CUDA(run1(slab_prob(h, 1, true, T1, T2, n1, nz, EPI_NONE, nullptr, nullptr), h->cfg[1], false, s),
+             "fd_apply_slab: mode 2");
+    FDP_CUDA(launch_slab_copy(T2, out, (int)n1, (int)n2, (int)nz, nranks, 0, nullptr, s), "fd_apply_slab: pack");
+  } else if (phase == 1) {
+    const double* lam1 = h->lamc[1] + y0;
+    const bool fuse = std::getenv("FDP_NO_FUSE") == nullptr && std::getenv("FDP_NO_SMALL") == nullptr &&
+                      n3 <= kSmallMaxN && h->cfg[2].tiles_n == 1;
+    if (fuse) {  // in place: each 8-row tile is read whole before it is written
+      FDP_CUDA(run1(slab_prob(h, 2, true, in, out, n1 * ny, 1, EPI_FUSED, nullptr, lam1), h->cfg[2], false, s),
+               "fd_apply_slab: fused mode 3");
+    } else {
+      FDP_CUDA(run1(slab_prob(h, 2, true, in, T1, n1 * ny, 1, EPI_LAMBDA, nullptr, lam1), h->cfg[2], false, s),
+               "fd_apply_slab: mode 3 fwd");
+      FDP_CUDA(run1(slab_prob(h, 2, false, T1, out, n1 * ny, 1, EPI_NONE, nullptr, nullptr), h->cfg[2], false, s),
+               "fd_apply_slab: mode 3 bwd");
+    }
+  } else {
+    FDP_CUDA(launch_slab_copy(in, T1, (int)n1, (int)n2, (int)nz, nranks, 1, nullptr, s), "fd_apply_slab: unpack");
+    FDP_CUDA(run1(slab_prob(h, 1, false, T1, T2, n1, nz, EPI_NONE, nullptr, nullptr), h->cfg[1], false, s),
+             "fd_apply_slab: mode 2 bwd");
+    FDP_CUDA(run1(slab_prob(h, 0, false, T2, out, 1, n2 * nz, dscale ? EPI_SCALE : EPI_NONE, dscale, nullptr),
+                  h->cfg[0], true, s),
+             "fd_apply_slab: mode 1 bwd");
+  }
+  return FDP_OK;
+}
+
+extern "C" size_t kron_mass_slab_workspace_bytes(fdp_mass h, int nranks, int rank) {
+  if (!h || h->D != 3 || nranks < 1 || rank < 0 || rank >= nranks) return 0;
+  long long z0, nz;
+  part_range(h->n[2], nranks, rank, &z0, &nz);
+  return (size_t)((long long)h->n[0] * h->n[1] * nz) * sizeof(double);
+}
+
+extern "C" fdp_status kron_mass_apply_slab(fdp_mass h, int phase, int nranks, int rank,
+                                           const double* in, double* out, const double* dscale,
+                                           void* workspace, void* stream) {
+  if (!h) return fail(FDP_ERR_INVALID_ARG, "kron_mass_apply_slab: NULL handle");
+  if (h->D != 3) return fail(FDP_ERR_UNSUPPORTED, "kron_mass_apply_slab: D must be 3");
+  if (nranks < 1 || rank < 0 || rank >= nranks || phase < 0 || phase > 2)
+    return fail(FDP_ERR_INVALID_ARG, "kron_mass_apply_slab: bad phase / rank");
+  const long long n1 = h->n[0], n2 = h->n[1], n3 = h->n[2];
+  long long z0, nz, y0, ny;
+  part_range(n3, nranks, rank, &z0, &nz);
+  part_range(n2, nranks, rank, &y0, &ny);
+  if ((phase == 1 ? ny : nz) == 0) return FDP_OK;
+  if (!is_device_ptr(in) || !is_device_ptr(out) || (phase == 0 && !is_device_ptr(workspace)) ||
+      (dscale && !is_device_ptr(dscale)))
+    return fail(FDP_ERR_INVALID_ARG, "kron_mass_apply_slab: device pointers required");
+  DeviceGuard dg(h->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto mode = [&](int d, const double* src, double* dst, long long P, long long Q, const double* pre) {
+    MassMode m{};
+    m.in = src;
+    m.out = dst;
+    m.Lb = h->Lb[d];
+    m.invd = h->invd[d];
+    m.Mb = h->Mb[d];
+    m.pre = pre;
+    m.N = P * h->n[d] * Q;
+    m.bs = 0;
+    m.P = (int)P;
+    m.n = h->n[d];
+    m.Q = (int)Q;
+    m.batch = 1;
+    m.band = h->band[d];
+    return launch_mass_mode(m, s);
+  };
+  double* T = static_cast<double*>(workspace);
+  if (phase == 0) {
+    FDP_CUDA(mode(0, in, T, 1, n2 * nz, dscale), "kron_mass_apply_slab: mode 1");
+    FDP_CUDA(mode(1, T, T, n1, nz, nullptr), "kron_mass_apply_slab: mode 2");
+    FDP_CUDA(launch_slab_copy(T, out, (int)n1, (int)n2, (int)nz, nranks, 0, nullptr, s),
+             "kron_mass_apply_slab: pack");
+  } else if (phase == 1) {
+    FDP_CUDA(mode(2, in, out, n1 * ny, 1, nullptr), "kron_mass_apply_slab: mode 3");
+  } else {
+    FDP_CUDA(launch_slab_copy(in, out, (int)n1, (int)n2, (int)nz, nranks, 1, dscale, s),
+             "kron_mass_apply_slab: unpack");
+  }
+  return FDP_OK;
 }

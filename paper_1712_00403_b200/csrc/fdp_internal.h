@@ -103,6 +103,10 @@ cudaError_t launch_scale(const double* x, double* y, const double* s, long long 
 // Set the dynamic shared-memory attribute of the kernels a tile config uses (call outside capture).
 cudaError_t prepare_mode_kernels(const TileCfg& cfg);
 
+// Slab pack (dir 0: z-slab -> piece buffer) / unpack (dir 1, optional scale on the z-slab).
+cudaError_t launch_slab_copy(const double* src, double* dst, int n1, int n2, int nz, int G, int dir,
+                             const double* scale, cudaStream_t s);
+
 // ---------------------------------------------------------------------------------------------
 // Banded Kronecker mass solve: per mode, along every fiber of the (P, n, Q) view,
 // forward substitution with the banded Cholesky factor L then back substitution with L^T.

@@ -1,0 +1,186 @@
+"""Multi-GPU plumbing for the FD block preconditioner.
+
+* Batch sharding (config 4): independent right-hand sides dealt round-robin to ranks; no
+  collective in the apply (``batch_shard``).
+* Slab decomposition (config 5): the slowest axis i3 of every block is partitioned over ranks;
+  modes 1-2 run locally on i3-slabs, mode 3 on i2-slabs between two all-to-all exchanges
+  (NCCL over NVLink / NVSwitch through ``torch.distributed``), computed by libfdp's slab phases
+  (``fd_apply_slab`` / ``kron_mass_apply_slab``). The exchange plan below is pure index
+  arithmetic; every floating-point operation runs in libfdp's kernels.
+
+The same plan drives ``SlabBlockPrecond`` (one process per GPU) and ``emulate_slab_apply`` (all
+ranks in one process on one device, exchanges as device copies) used by the single-GPU tests.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+def part(n: int, G: int, r: int):
+    """Even split of n over G ranks (first n mod G ranks own one more): (lo, len)."""
+    q, rem = divmod(n, G)
+    lo = r * q + min(r, rem)
+    return lo, q + (1 if r < rem else 0)
+
+
+def batch_shard(batch: int, world: int, rank: int):
+    """Items {rank, rank + world, ...} of a batch (config 4's RHS sharding)."""
+    return list(range(rank, batch, world))
+
+
+@dataclass
+class BlockPlan:
+    """Exchange plan of one 3D block (n1, n2, n3) over G ranks, from rank g's point of view."""
+    dims: tuple
+    G: int
+    g: int
+
+    @property
+    def z(self):
+        return part(self.dims[2], self.G, self.g)
+
+    @property
+    def y(self):
+        return part(self.dims[1], self.G, self.g)
+
+    @property
+    def zslab_size(self):
+        n1, n2, _ = self.dims
+        return n1 * n2 * self.z[1]
+
+    @property
+    def yslab_size(self):
+        n1, _, n3 = self.dims
+        return n1 * self.y[1] * n3
+
+    def ex1_splits(self):
+        """(send sizes, recv sizes) of exchange 1 (piece buffer -> y-slab), in rank order."""
+        n1, n2, n3 = self.dims
+        nz = self.z[1]
+        ny = self.y[1]
+        send = [n1 * part(n2, self.G, h)[1] * nz for h in range(self.G)]
+        recv = [n1 * ny * part(n3, self.G, h)[1] for h in range(self.G)]
+        return send, recv
+
+    def ex2_splits(self):
+        """(send sizes, recv sizes) of exchange 2 (y-slab -> piece buffer)."""
+        s, r = self.ex1_splits()
+        return r, s
+
+    def zslab_offset(self):
+        """Offset of this rank's z-slab in the full (unsharded) block vector."""
+        n1, n2, _ = self.dims
+        return n1 * n2 * self.z[0]
+
+
+class SlabBlockPrecond:
+    """P_D^{-1} with every block slab-decomposed over a torch.distributed process group.
+
+    The local vector layout is [u_1 z-slab | ... | u_D z-slab | p z-slab]. D = 3 only."""
+
+    def __init__(self, block, group=None):
+        import torch
+        import torch.distributed as dist
+        from . import fd_apply_slab, kron_mass_apply_slab  # noqa: F401
+
+        self.torch = torch
+        self.dist = dist
+        self.group = group
+        self.G = dist.get_world_size(group)
+        self.g = dist.get_rank(group)
+        self.block = block
+        self.fds = block.fds
+        self.mass = block.mass
+        dev = f"cuda:{block.device}"
+        self.plans = [BlockPlan(tuple(f.dims), self.G, self.g) for f in self.fds]
+        self.plans.append(BlockPlan(tuple(self.mass.dims), self.G, self.g))
+        self.local_sizes = [p.zslab_size for p in self.plans]
+        self.local_off = np.concatenate([[0], np.cumsum(self.local_sizes)]).astype(np.int64)
+        self.local_n = int(self.local_off[-1])
+        zs = lambda p: torch.empty(p.zslab_size, dtype=torch.float64, device=dev)
+        ys = lambda p: torch.empty(p.yslab_size, dtype=torch.float64, device=dev)
+        self.send = [zs(p) for p in self.plans]
+        self.ybuf = [ys(p) for p in self.plans]
+        self.recv = [zs(p) for p in self.plans]
+        from . import lib
+        wsb = [lib.fd_slab_workspace_bytes(f.h, self.G, self.g) for f in self.fds]
+        wsb.append(lib.kron_mass_slab_workspace_bytes(self.mass.h, self.G, self.g))
+        self.ws = torch.empty(max(wsb) // 8 + 1, dtype=torch.float64, device=dev)
+
+    def _exchange(self, k, src, dst, splits):
+        send, recv = splits
+        self.dist.all_to_all_single(dst, src, output_split_sizes=recv, input_split_sizes=send,
+                                    group=self.group)
+
+    def apply(self, r, s, dscale_vel=None, dscale_pres=None, stream=None):
+        from . import fd_apply_slab, kron_mass_apply_slab
+        G, g = self.G, self.g
+        o = self.local_off
+        nk = len(self.fds)
+        for k, f in enumerate(self.fds):
+            fd_apply_slab(f, 0, G, g, r[o[k]:o[k + 1]], self.send[k], None, self.ws, stream)
+        kron_mass_apply_slab(self.mass, 0, G, g, r[o[nk]:o[nk + 1]], self.send[nk], None, self.ws, stream)
+        for k, p in enumerate(self.plans):
+            self._exchange(k, self.send[k], self.ybuf[k], p.ex1_splits())
+        for k, f in enumerate(self.fds):
+            fd_apply_slab(f, 1, G, g, self.ybuf[k], self.ybuf[k], None, self.ws, stream)
+        kron_mass_apply_slab(self.mass, 1, G, g, self.ybuf[nk], self.ybuf[nk], None, None, stream)
+        for k, p in enumerate(self.plans):
+            self._exchange(k, self.ybuf[k], self.recv[k], p.ex2_splits())
+        for k, f in enumerate(self.fds):
+            fd_apply_slab(f, 2, G, g, self.recv[k], s[o[k]:o[k + 1]], None, self.ws, stream)
+        kron_mass_apply_slab(self.mass, 2, G, g, self.recv[nk], s[o[nk]:o[nk + 1]], None, None, stream)
+        return s
+
+
+def emulate_slab_apply(block, r_full, G: int):
+    """Run the slab-decomposed application for G virtual ranks in one process on one device,
+    performing the two exchanges as device copies. Returns the full result vector (torch)."""
+    import torch
+    from . import fd_apply_slab, kron_mass_apply_slab, lib
+
+    dev = r_full.device
+    blocks = [("fd", f, tuple(f.dims)) for f in block.fds] + [("mass", block.mass, tuple(block.mass.dims))]
+    full_off = np.concatenate([[0], np.cumsum([int(np.prod(b[2])) for b in blocks])]).astype(np.int64)
+    out = torch.empty_like(r_full)
+    for bi, (kind, h, dims) in enumerate(blocks):
+        plans = [BlockPlan(dims, G, g) for g in range(G)]
+        base = int(full_off[bi])
+        wsb = max((lib.fd_slab_workspace_bytes(h.h, G, g) if kind == "fd"
+                   else lib.kron_mass_slab_workspace_bytes(h.h, G, g)) for g in range(G))
+        ws = torch.empty(wsb // 8 + 1, dtype=torch.float64, device=dev)
+        run = fd_apply_slab if kind == "fd" else kron_mass_apply_slab
+        sends = []
+        for g, p in enumerate(plans):
+            zo = base + p.zslab_offset()
+            xs = r_full[zo:zo + p.zslab_size].contiguous()
+            snd = torch.empty(p.zslab_size, dtype=torch.float64, device=dev)
+            run(h, 0, G, g, xs, snd, None, ws)
+            sends.append(snd)
+        # exchange 1: rank g's y-slab = concatenation over sources h of piece g of h's send buffer
+        ybufs = []
+        for g, p in enumerate(plans):
+            pieces = []
+            for hsrc in range(G):
+                ssz, _ = plans[hsrc].ex1_splits()
+                off = int(np.sum(ssz[:g]))
+                pieces.append(sends[hsrc][off:off + ssz[g]])
+            yb = torch.cat(pieces).contiguous()
+            assert yb.numel() == p.yslab_size
+            run(h, 1, G, g, yb, yb, None, ws if kind == "fd" else None)
+            ybufs.append(yb)
+        # exchange 2: rank g receives from every h the planes of g's z-range of h's y-slab
+        for g, p in enumerate(plans):
+            pieces = []
+            for hsrc in range(G):
+                ssz, _ = plans[hsrc].ex2_splits()
+                off = int(np.sum(ssz[:g]))
+                pieces.append(ybufs[hsrc][off:off + ssz[g]])
+            rc = torch.cat(pieces).contiguous()
+            xs = torch.empty(p.zslab_size, dtype=torch.float64, device=dev)
+            run(h, 2, G, g, rc, xs, None, ws if kind == "fd" else None)
+            zo = base + p.zslab_offset()
+            out[zo:zo + p.zslab_size] = xs
+    return out
