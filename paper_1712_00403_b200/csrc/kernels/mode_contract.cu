@@ -212,7 +212,7 @@ mode_contract_kernel(const __grid_constant__ ModeGroup grp) {
         const int a = n0 + 8 * j + 2 * fc + h;
         if (a < n) {
           double v = acc[i][j][h];
-          if (epi == EPI_LAMBDA) v = v / (lrow + pb.lamcol[a]);
+          if (epi == EPI_LAMBDA) v = fdp_div(v, lrow + pb.lamcol[a]);
           else if (epi == EPI_SCALE) v = v * pb.scale[sidx + (long long)P * a];
           Y[row_off + (long long)P * a] = v;
         }

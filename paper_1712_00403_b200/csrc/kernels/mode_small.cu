@@ -270,7 +270,7 @@ __device__ __forceinline__ void tile_compute_store(const ModeProb& pb, const Geo
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int a = 8 * j + 2 * fc + h;
-        A[fr * S::SA + a] = (mv && a < g.n) ? acc[j][h] / (lrow + pb.lamcol[a]) : 0.0;
+        A[fr * S::SA + a] = (mv && a < g.n) ? fdp_div(acc[j][h], lrow + pb.lamcol[a]) : 0.0;
       }
     __syncwarp();
 #pragma unroll
@@ -296,7 +296,7 @@ __device__ __forceinline__ void tile_compute_store(const ModeProb& pb, const Geo
         const int a = 8 * j + 2 * fc + h;
         if (a < g.n) {
           double v = acc[j][h];
-          if (epi == EPI_LAMBDA) v = v / (lrow + pb.lamcol[a]);
+          if (epi == EPI_LAMBDA) v = fdp_div(v, lrow + pb.lamcol[a]);
           else if (epi == EPI_SCALE) v = v * pb.scale[sidx + g.P * a];
           Y[g.P * a] = v;
         }
