@@ -18,7 +18,8 @@ import numpy as np
 __all__ = ["FdpError", "lib", "iga_univariate", "iga_greville", "gen_eig", "FD", "KronMass",
            "BlockPrecond", "Discretization", "discretization", "nu_scalings", "LIB_PATH"]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfdp.so")
+LIB_PATH = os.environ.get("FDP_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                           "libfdp.so")
 
 FDP_IGA_INTERIOR = 1
 FDP_IGA_NITSCHE = 2
@@ -191,10 +192,10 @@ class FD:
         if x is None:
             x = torch.empty_like(b)
         numel = self.N * batch
-        ws = None
+        wsn = max(1, self.workspace_bytes(batch) // 8)
         if workspace is None:
-            workspace = torch.empty(numel, dtype=torch.float64, device=b.device)
-        ws = _dev(workspace, "workspace", numel)
+            workspace = torch.empty(wsn, dtype=torch.float64, device=b.device)
+        ws = _dev(workspace, "workspace", wsn)
         _check(lib.fd_apply(self.h, _dev(b, "b", numel), _dev(x, "x", numel),
                             None if dscale is None else _dev(dscale, "dscale", self.N), batch, ws,
                             _stream(stream)))

@@ -5,6 +5,7 @@
 #include <functional>
 #include <cmath>
 #include <cstdio>
+#include <cstdint>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -190,6 +191,11 @@ struct fdp_fd_s {
   int64_t sync_batch = 0;
 };
 
+// Intermediate tensors between passes use an even leading dimension n1p (16-byte aligned rows
+// and row pairs for vector memory operations); the C-ABI input/output stay unpadded.
+static int n1pad(const fdp_fd_s* h) { return h->n[0] + (h->n[0] & 1); }
+static long long Npad(const fdp_fd_s* h) { return h->N / h->n[0] * n1pad(h); }
+
 static void free_fd(fdp_fd h) {
   if (!h) return;
   for (int d = 0; d < 3; ++d) {
@@ -294,7 +300,7 @@ extern "C" fdp_status fd_setup(int D, const int32_t* n, const double* const* K,
     raw->sync_batch = sb;
   }
   if (max_batch > 0) {
-    fdp_status st = dalloc(&raw->ws, (size_t)(max_batch * N));
+    fdp_status st = dalloc(&raw->ws, (size_t)(2 * max_batch * Npad(raw)));
     if (st) {
       free_fd(raw);
       return st;
@@ -315,15 +321,20 @@ extern "C" fdp_status fd_get_eigs(fdp_fd h, int d, double* U_out, double* lambda
 
 extern "C" int64_t fd_size(fdp_fd h) { return h ? h->N : 0; }
 extern "C" size_t fd_workspace_bytes(fdp_fd h, int64_t batch) {
-  return h && batch > 0 ? (size_t)(batch * h->N) * sizeof(double) : 0;
+  return h && batch > 0 ? (size_t)(2 * batch * Npad(h)) * sizeof(double) : 0;
 }
 
-// One FD problem inside a grouped stage: mode d (0-based), direction fwd/bwd.
+// One FD problem inside a grouped stage: mode d (0-based), direction fwd/bwd. xld / yld: fiber
+// strides of X / Y (n1, or n1p for padded intermediates); mode >= 1 always runs on padded
+// intermediates (P counts the n1p leading rows, pad rows stay zero).
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 static ModeProb make_mode_prob(const fdp_fd_s* h, int d, bool fwd, const double* X, long long xbs,
-                               double* Y, long long ybs, int64_t batch, int epi, const double* scale) {
+                               double* Y, long long ybs, int64_t batch, int epi, const double* scale,
+                               int xld, int yld) {
   ModeProb p{};
+  const int n1p = n1pad(h);
   long long P = 1, Q = 1;
-  for (int e = 0; e < d; ++e) P *= h->n[e];
+  for (int e = 0; e < d; ++e) P *= (e == 0 ? n1p : h->n[e]);
   for (int e = d + 1; e < h->D; ++e) Q *= h->n[e];
   p.X = X;
   p.Y = Y;
@@ -336,7 +347,18 @@ static ModeProb make_mode_prob(const fdp_fd_s* h, int d, bool fwd, const double*
   p.Q = (int)Q;
   p.batch = (int)batch;
   p.ldw = h->cfg[d].ldw;
-  p.n1 = h->n[0];
+  p.n1 = n1p;
+  p.n1v = h->n[0];
+  p.xld = xld;
+  p.yld = yld;
+  if (d == 0) {
+    p.vx = (xld % 2 == 0) && (xbs % 2 == 0) && aligned16(X);
+    p.vy = (yld % 2 == 0) && (ybs % 2 == 0) && aligned16(Y);
+  } else {
+    p.vx = (P % 2 == 0) && (xbs % 2 == 0) && aligned16(X);
+    p.vy = (P % 2 == 0) && (ybs % 2 == 0) && aligned16(Y);
+  }
+  if (std::getenv("FDP_NO_VEC")) p.vx = p.vy = 0;
   p.epi = epi;
   p.scale = scale;
   if (epi == EPI_LAMBDA || epi == EPI_FUSED) {
@@ -352,8 +374,6 @@ static ModeProb make_mode_prob(const fdp_fd_s* h, int d, bool fwd, const double*
   return p;
 }
 
-// Stage = one mode/direction for a set of FD problems. Problems with the same tile config share a
-// launch (up to kMaxGroup); others get their own.
 // Small-path grid: one CTA per SM, split over the problems of a group in proportion to their
 // DMMA work (prob.ctas, prob.cta_begin, total_ctas). prob.tiles_m must hold the 8-row tile count.
 static void alloc_small_ctas(ModeGroup& g, const std::vector<double>& w) {
@@ -569,27 +589,26 @@ static cudaError_t enqueue_fd(const std::vector<const fdp_fd_s*>& hs,
   for (int pass = 0; pass < npass; ++pass) {
     const Stage& st = stages[pass];
     const int d = st.d;
-    const bool dst_out = ((npass - 1 - pass) % 2) == 0;
+    const bool first = pass == 0, last = pass == npass - 1;
     std::vector<ModeProb> probs;
     std::vector<TileCfg> cfgs;
     for (size_t k = 0; k < K; ++k) {
-      const double* src;
-      long long sbs;
-      if (pass == 0) {
-        src = in[k]; sbs = ibs;
-      } else if (dst_out) {  // previous pass wrote T
-        src = T[k]; sbs = hs[k]->N;
-      } else {
-        src = out[k]; sbs = obs;
-      }
-      double* dst = dst_out ? out[k] : T[k];
-      const long long dbs = dst_out ? obs : hs[k]->N;
+      // T[k] holds two padded intermediates (batch x Np each): passes alternate between them
+      const long long np = Npad(hs[k]);
+      double* buf0 = T[k];
+      double* buf1 = T[k] + np * batch;
+      const double* src = first ? in[k] : ((pass - 1) % 2 == 0 ? buf0 : buf1);
+      const long long sbs = first ? ibs : np;
+      double* dst = last ? out[k] : (pass % 2 == 0 ? buf0 : buf1);
+      const long long dbs = last ? obs : np;
+      const int xld = first ? hs[k]->n[0] : n1pad(hs[k]);
+      const int yld = last ? hs[k]->n[0] : n1pad(hs[k]);
       int epi = EPI_NONE;
       const double* sc = nullptr;
       if (st.fused) epi = EPI_FUSED;
       else if (st.fwd && d == D - 1) epi = EPI_LAMBDA;
       if (!st.fwd && d == 0 && dscale[k]) { epi = EPI_SCALE; sc = dscale[k]; }
-      probs.push_back(make_mode_prob(hs[k], d, st.fwd, src, sbs, dst, dbs, batch, epi, sc));
+      probs.push_back(make_mode_prob(hs[k], d, st.fwd, src, sbs, dst, dbs, batch, epi, sc, xld, yld));
       cfgs.push_back(hs[k]->cfg[d]);
     }
     if (hook) hook(pass, st.fwd, d, probs, cfgs);
@@ -1000,7 +1019,9 @@ extern "C" fdp_status block_precond_setup(int D, const fdp_fd* vel, fdp_mass pre
 
 extern "C" int64_t block_precond_size(fdp_block h) { return h ? h->size : 0; }
 static long long block_ws_elems(const fdp_block_s* h, int64_t batch) {
-  return batch * (h->nvel + (h->pres_dense ? 2 * h->pres->N : 0));
+  long long v = 0;
+  for (const fdp_fd_s* f : h->vel) v += 2 * Npad(f);
+  return batch * (v + (h->pres_dense ? 2 * h->pres->N : 0));
 }
 extern "C" size_t block_precond_workspace_bytes(fdp_block h, int64_t batch) {
   return h && batch > 0 ? (size_t)block_ws_elems(h, batch) * sizeof(double) : 0;
@@ -1025,8 +1046,8 @@ static cudaError_t enqueue_block(fdp_block h, const double* r, double* s, int64_
   for (int k = 0; k < D; ++k) {
     in[k] = r + h->off[k];
     out[k] = s + h->off[k];
-    T[k] = ws + toff;  // component k workspace: batch x N_k, compact
-    toff += h->vel[k]->N * batch;
+    T[k] = ws + toff;  // component k workspace: two padded intermediates, 2 x batch x Np_k
+    toff += 2 * Npad(h->vel[k]) * batch;
     dsc[k] = h->dv ? h->dv + h->off[k] : nullptr;
   }
   const long long nq = h->pres->N;
@@ -1076,7 +1097,9 @@ static cudaError_t enqueue_block(fdp_block h, const double* r, double* s, int64_
       p.Q = (int)Q;
       p.batch = (int)batch;
       p.ldw = h->q_ldw[d];
-      p.n1 = h->pres->n[0];
+      p.n1 = p.n1v = h->pres->n[0];
+      p.xld = p.yld = h->pres->n[0];
+      p.vx = p.vy = 0;
       p.epi = (last && h->dall) ? EPI_SCALE : EPI_NONE;
       p.scale = (last && h->dall) ? h->dall + h->off[D] : nullptr;
       const int BM = 4 * 8 * cfgs[0].MT;
@@ -1324,7 +1347,9 @@ static ModeProb slab_prob(const fdp_fd_s* h, int d, bool fwd, const double* X, d
   p.xbs = p.ybs = 0;
   p.batch = 1;
   p.ldw = h->cfg[d].ldw;
-  p.n1 = h->n[0];
+  p.n1 = p.n1v = h->n[0];
+  p.xld = p.yld = h->n[0];
+  p.vx = p.vy = 0;
   p.epi = epi;
   p.scale = scale;
   if (epi == EPI_LAMBDA || epi == EPI_FUSED) {

@@ -41,7 +41,10 @@ struct ModeProb {
   int P, n, Q;            // per item; GEMM rows M = P * Q * batch
   int batch;
   int ldw;
-  int n1;                 // size of direction 1 (Lambda row decomposition in 3D)
+  int n1;                 // leading dimension of direction 1 (Lambda row decomposition)
+  int n1v;                // valid extent of direction 1 (rows with i1 >= n1v are padding)
+  int xld, yld;           // KMAJ (mode 1): row (fiber) strides of X and Y (n1 or padded n1p)
+  int vx, vy;             // 16-byte vector loads of X / stores of Y are aligned (host-checked)
   int epi;
   int tiles_m, tiles_n;
   int cta_begin;          // first CTA of this problem in the grouped grid

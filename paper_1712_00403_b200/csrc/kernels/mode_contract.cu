@@ -15,8 +15,14 @@
 namespace fdp {
 namespace {
 
-constexpr int BK = 16;
-constexpr int STAGES = 3;
+#ifndef FDP_K1_BK
+#define FDP_K1_BK 16
+#endif
+#ifndef FDP_K1_STAGES
+#define FDP_K1_STAGES 3
+#endif
+constexpr int BK = FDP_K1_BK;
+constexpr int STAGES = FDP_K1_STAGES;
 constexpr int WARPS = 4;
 constexpr int THREADS = WARPS * 32;
 
@@ -89,8 +95,8 @@ mode_contract_kernel(const __grid_constant__ ModeGroup grp) {
     for (int j = 0; j < A_ROWS_PER_THREAD; ++j) {
       long long m = m0 + tid / 16 + 8 * j;
       a_ok[j] = m < M;
-      // P == 1: row m = q + Q*b at n*q + xbs*b, contiguous in k
-      a_off[j] = a_ok[j] ? (long long)n * (m % Qn) + pb.xbs * (m / Qn) : 0;
+      // P == 1: row m = q + Q*b at xld*q + xbs*b, contiguous in k
+      a_off[j] = a_ok[j] ? (long long)pb.xld * (m % Qn) + pb.xbs * (m / Qn) : 0;
     }
   } else {
     long long m = m0 + tid % BM;
@@ -190,29 +196,29 @@ mode_contract_kernel(const __grid_constant__ ModeGroup grp) {
     long long row_off;
     long long sidx;  // index within the batch item (for EPI_SCALE)
     double lrow = 0.0;
+    bool pad_row = false;
     if (KMAJ) {
-      sidx = (long long)n * (m % Qn);
+      sidx = (long long)pb.yld * (m % Qn);
       row_off = sidx + pb.ybs * (m / Qn);
     } else {
       const long long p = m % P, r = m / P;
       sidx = p + Pn * (r % Qn);
       row_off = sidx + pb.ybs * (r / Qn);
       if (epi == EPI_LAMBDA) {
-        if (pb.lam1) {
-          lrow = pb.lam0[p % pb.n1] + pb.lam1[p / pb.n1];
-        } else {
-          lrow = pb.lam0[p];
-        }
+        const int i1 = (int)(p % pb.n1);
+        pad_row = i1 >= pb.n1v;  // padding row of a padded intermediate: stays 0
+        if (!pad_row) lrow = pb.lam1 ? pb.lam0[i1] + pb.lam1[p / pb.n1] : pb.lam0[p];
       }
     }
+    const int ncols = KMAJ ? pb.yld : n;  // padded outputs also get their zero pad column
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int a = n0 + 8 * j + 2 * fc + h;
-        if (a < n) {
+        if (a < ncols) {
           double v = acc[i][j][h];
-          if (epi == EPI_LAMBDA) v = fdp_div(v, lrow + pb.lamcol[a]);
+          if (epi == EPI_LAMBDA) v = pad_row ? 0.0 : fdp_div(v, lrow + pb.lamcol[a]);
           else if (epi == EPI_SCALE) v = v * pb.scale[sidx + (long long)P * a];
           Y[row_off + (long long)P * a] = v;
         }

@@ -95,13 +95,13 @@ struct Geo {
 };
 
 // element offset of GEMM row m within its batch item (32-bit: the host routes here only problems
-// with M < 2^31) and the batch item index
+// with M < 2^31) and the batch item index; ld = fiber stride of the tensor (KMAJ)
 template <bool KMAJ>
-__device__ __forceinline__ void row_index(const Geo& g, int m, int& within, int& item) {
+__device__ __forceinline__ void row_index(const Geo& g, int m, int& within, int& item, int ld) {
   const unsigned b = (unsigned)m / (unsigned)g.Mi;
   const int mi = m - (int)b * g.Mi;
   if (KMAJ) {
-    within = g.n * mi;  // P == 1: row = fiber q = mi
+    within = ld * mi;  // P == 1: row = fiber q = mi
   } else {
     const unsigned q = (unsigned)mi / (unsigned)g.P;
     within = (mi - (int)q * g.P) + g.Pn * (int)q;
@@ -134,12 +134,12 @@ __device__ __forceinline__ void load_panel_async(const ModeProb& pb, const Geo& 
   const int m0 = (int)(t * 8);
   if (KMAJ) {
     int w0, b0;
-    row_index<true>(g, m0, w0, b0);
-    int mi = w0 / g.n;
+    row_index<true>(g, m0, w0, b0, 1);
+    int mi = w0;
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       const bool rv = (long long)m0 + r < g.M;
-      const double* src = X + ((long long)g.n * mi + pb.xbs * b0);
+      const double* src = X + ((long long)pb.xld * mi + pb.xbs * b0);
       for (int k = lane; k < g.kpad; k += 32) {
         const bool v = rv && k < g.n;
         cp_async8z(&A[r * S::SA + k], v ? src + k : X, v);
@@ -151,7 +151,7 @@ __device__ __forceinline__ void load_panel_async(const ModeProb& pb, const Geo& 
     const int m = m0 + r;
     const bool rv = (long long)m < g.M;
     int w = 0, b = 0;
-    if (rv) row_index<false>(g, m, w, b);
+    if (rv) row_index<false>(g, m, w, b, 0);
     const double* src = X + (w + pb.xbs * b);
     for (int k = lane >> 3; k < g.kpad; k += 4) {
       const bool v = rv && k < g.n;
@@ -171,30 +171,76 @@ __device__ __forceinline__ void do_tile(const ModeProb& pb, const Geo& g, const 
   const double* __restrict__ X = pb.X;
   const int m0 = (int)(t * 8);
   if (KMAJ) {
-    int w0, b0;
-    row_index<true>(g, m0, w0, b0);
-    int mi = w0 / g.n;
+    int mi, b0;
+    row_index<true>(g, m0, mi, b0, 1);  // fiber index of the tile's first row
     const double* src[8];
     bool rv[8];
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       rv[r] = (long long)m0 + r < g.M;
-      src[r] = X + ((long long)g.n * mi + pb.xbs * b0);
+      src[r] = X + ((long long)pb.xld * mi + pb.xbs * b0);
       if (++mi == g.Mi) { mi = 0; ++b0; }
     }
-    double v[3][8];
+    if (pb.vx) {
+      // 16-byte loads: rows of an even-stride (padded) tensor; element n of an odd-n row is the
+      // zero pad column
+      double2 v[2][8];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const int k = 32 * c + lane;
+      for (int c = 0; c < 2; ++c) {
+        const int k = 64 * c + 2 * lane;
 #pragma unroll
-      for (int r = 0; r < 8; ++r) v[c][r] = (c < g.nch && rv[r] && k < g.n) ? ldx<COHERENT>(src[r] + k) : 0.0;
+        for (int r = 0; r < 8; ++r)
+          v[c][r] = (rv[r] && k < g.n) ? (COHERENT ? __ldcg(reinterpret_cast<const double2*>(src[r] + k))
+                                                 : __ldg(reinterpret_cast<const double2*>(src[r] + k)))
+                                      : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int k = 64 * c + 2 * lane;
+        if (k < g.kpad) {
+#pragma unroll
+          for (int r = 0; r < 8; ++r) *reinterpret_cast<double2*>(&A[r * S::SA + k]) = v[c][r];
+        }
+      }
+    } else {
+      double v[3][8];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const int k = 32 * c + lane;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) v[c][r] = (c < g.nch && rv[r] && k < g.n) ? ldx<COHERENT>(src[r] + k) : 0.0;
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const int k = 32 * c + lane;
+        if (c < g.nch && k < g.kpad) {
+#pragma unroll
+          for (int r = 0; r < 8; ++r) A[r * S::SA + k] = v[c][r];
+        }
+      }
+    }
+  } else if (pb.vx) {
+    // 16-byte loads of row pairs (p, p+1), p even, of an even-P tensor; lane = (pair, k)
+    const int rp = lane & 3, kk = lane >> 2;
+    const int m = m0 + 2 * rp;
+    const bool rv = (long long)m < g.M;  // M is even here, so the pair is all or nothing
+    int w = 0, b = 0;
+    if (rv) row_index<false>(g, m, w, b, 0);
+    const double* src = X + (w + pb.xbs * b);
+    double2 v[12];
+#pragma unroll
+    for (int j = 0; j < 12; ++j) {
+      const int k = kk + 8 * j;
+      v[j] = (k < g.n && rv) ? (COHERENT ? __ldcg(reinterpret_cast<const double2*>(src + (long long)g.P * k))
+                                         : __ldg(reinterpret_cast<const double2*>(src + (long long)g.P * k)))
+                             : make_double2(0.0, 0.0);
     }
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const int k = 32 * c + lane;
-      if (c < g.nch && k < g.kpad) {
-#pragma unroll
-        for (int r = 0; r < 8; ++r) A[r * S::SA + k] = v[c][r];
+    for (int j = 0; j < 12; ++j) {
+      const int k = kk + 8 * j;
+      if (k < g.kpad) {
+        A[(2 * rp) * S::SA + k] = v[j].x;
+        A[(2 * rp + 1) * S::SA + k] = v[j].y;
       }
     }
   } else {
@@ -202,7 +248,7 @@ __device__ __forceinline__ void do_tile(const ModeProb& pb, const Geo& g, const 
     const int m = m0 + r;
     const bool rv = (long long)m < g.M;
     int w = 0, b = 0;
-    if (rv) row_index<false>(g, m, w, b);
+    if (rv) row_index<false>(g, m, w, b, 0);
     const double* src = X + (w + pb.xbs * b);
     double v[24];
 #pragma unroll
@@ -248,29 +294,28 @@ __device__ __forceinline__ void tile_compute_store(const ModeProb& pb, const Geo
   const bool FUSED = pb.epi == EPI_FUSED;
   int sidx = 0, item = 0;
   double lrow = 0.0;
+  bool pad_row = false;  // padding row (i1 >= n1v) of a padded intermediate: output stays 0
   if (mv) {
-    row_index<KMAJ>(g, m, sidx, item);
+    row_index<KMAJ>(g, m, sidx, item, pb.yld);
     if (!KMAJ && (FUSED || pb.epi == EPI_LAMBDA)) {
       const int mi = m - item * g.Mi;
       const int p = mi - (int)((unsigned)mi / (unsigned)g.P) * g.P;
-      if (pb.lam1) {
-        const unsigned i2 = (unsigned)p / (unsigned)pb.n1;
-        lrow = pb.lam0[p - (int)i2 * pb.n1] + pb.lam1[i2];
-      } else {
-        lrow = pb.lam0[p];
-      }
+      const unsigned i2 = (unsigned)p / (unsigned)pb.n1;
+      const int i1 = p - (int)i2 * pb.n1;
+      pad_row = i1 >= pb.n1v;
+      if (!pad_row) lrow = pb.lam1 ? pb.lam0[i1] + pb.lam1[i2] : pb.lam0[p];
     }
   }
 
   if (FUSED) {
-    // T = acc / Lambda -> this warp's panel buffer ([8][SA]); zero beyond n.
+    // T = acc / Lambda -> this warp's panel buffer ([8][SA]); zero beyond n and on pad rows.
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < NT; ++j)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int a = 8 * j + 2 * fc + h;
-        A[fr * S::SA + a] = (mv && a < g.n) ? fdp_div(acc[j][h], lrow + pb.lamcol[a]) : 0.0;
+        A[fr * S::SA + a] = (mv && !pad_row && a < g.n) ? fdp_div(acc[j][h], lrow + pb.lamcol[a]) : 0.0;
       }
     __syncwarp();
 #pragma unroll
@@ -286,20 +331,51 @@ __device__ __forceinline__ void tile_compute_store(const ModeProb& pb, const Geo
     }
   }
 
-  if (mv) {
-    double* __restrict__ Y = pb.Y + pb.ybs * (long long)item + sidx;
-    const int epi = FUSED ? EPI_NONE : pb.epi;
+  // epilogue values (Lambda / scale applied), then stores
+  const int epi = FUSED ? EPI_NONE : pb.epi;
+  const int ncols = KMAJ ? pb.yld : g.n;  // padded KMAJ outputs also get their zero pad column
+#pragma unroll
+  for (int j = 0; j < NT; ++j)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int a = 8 * j + 2 * fc + h;
+      double v = acc[j][h];
+      if (epi == EPI_LAMBDA) v = (pad_row || a >= g.n) ? 0.0 : fdp_div(v, lrow + pb.lamcol[a]);
+      else if (epi == EPI_SCALE && mv && a < g.n) v = v * pb.scale[sidx + g.P * a];
+      acc[j][h] = v;
+    }
+  double* __restrict__ Y = pb.Y + pb.ybs * (long long)item + sidx;
+  if (pb.vy && KMAJ) {
+    // (a, a+1) adjacent in a row of an even-stride tensor
+    if (mv) {
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        const int a = 8 * j + 2 * fc;
+        if (a < ncols) *reinterpret_cast<double2*>(Y + a) = make_double2(acc[j][0], acc[j][1]);
+      }
+    }
+  } else if (pb.vy) {
+    // rows (p, p+1), p even, are adjacent: swap halves with the partner lane (fr ^ 1) and store
+    // 16-byte row pairs; even fr stores column c0, odd fr column c0 + 1 of the pair (fr & ~1)
+    const bool odd = fr & 1;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      const double send = odd ? acc[j][0] : acc[j][1];
+      const double got = __shfl_xor_sync(0xffffffffu, send, 4);
+      const int c = 8 * j + 2 * fc + (odd ? 1 : 0);
+      if (mv && c < ncols) {
+        double* dst = odd ? Y - 1 : Y;
+        *reinterpret_cast<double2*>(dst + (long long)g.P * c) =
+            odd ? make_double2(got, acc[j][1]) : make_double2(acc[j][0], got);
+      }
+    }
+  } else if (mv) {
 #pragma unroll
     for (int j = 0; j < NT; ++j)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int a = 8 * j + 2 * fc + h;
-        if (a < g.n) {
-          double v = acc[j][h];
-          if (epi == EPI_LAMBDA) v = fdp_div(v, lrow + pb.lamcol[a]);
-          else if (epi == EPI_SCALE) v = v * pb.scale[sidx + g.P * a];
-          Y[g.P * a] = v;
-        }
+        if (a < ncols) Y[(KMAJ ? 1 : g.P) * a] = acc[j][h];
       }
   }
   __syncwarp();  // all lanes done with the panel before it is refilled
