@@ -366,7 +366,7 @@ static ModeProb make_mode_prob(const fdp_fd_s* h, int d, bool fwd, const double*
     p.lam1 = h->D == 3 ? h->lamc[1] : nullptr;
     p.lamcol = h->lamc[h->D - 1];
   }
-  const int BM = 4 * 8 * h->cfg[d].MT;
+  const int BM = kK1Warps * 8 * h->cfg[d].MT;
   const long long M = P * Q * batch;
   p.tiles_m = (int)((M + BM - 1) / BM);
   p.tiles_n = h->cfg[d].tiles_n;
@@ -1102,7 +1102,7 @@ static cudaError_t enqueue_block(fdp_block h, const double* r, double* s, int64_
       p.vx = p.vy = 0;
       p.epi = (last && h->dall) ? EPI_SCALE : EPI_NONE;
       p.scale = (last && h->dall) ? h->dall + h->off[D] : nullptr;
-      const int BM = 4 * 8 * cfgs[0].MT;
+      const int BM = kK1Warps * 8 * cfgs[0].MT;
       p.tiles_m = (int)((P * Q * batch + BM - 1) / BM);
       p.tiles_n = h->q_tiles_n[d];
       p.fd_work = 0;
@@ -1357,7 +1357,7 @@ static ModeProb slab_prob(const fdp_fd_s* h, int d, bool fwd, const double* X, d
     p.lam1 = lam1;
     p.lamcol = h->lamc[2];
   }
-  const int BM = 4 * 8 * h->cfg[d].MT;
+  const int BM = kK1Warps * 8 * h->cfg[d].MT;
   p.tiles_m = (int)((P * Q + BM - 1) / BM);
   p.tiles_n = h->cfg[d].tiles_n;
   p.fd_work = 1;

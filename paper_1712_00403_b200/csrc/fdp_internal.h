@@ -53,13 +53,13 @@ struct ModeProb {
 };
 
 // Quotient a / b for the Lambda^{-1} epilogues (b = Lambda > 0, normal): hardware reciprocal
-// approximation, two Newton steps and one Markstein correction of the quotient -- 7 FP64 ops and
-// no slow-path branch, within one ulp of the IEEE quotient (C-11).
+// approximation (~2^-23), one Newton step (~2^-46) and one Markstein correction of the quotient
+// -- 5 FP64 ops (they share the FP64 datapath with DMMA) and no slow-path branch; within one
+// ulp of the IEEE quotient (C-11).
 #ifdef __CUDACC__
 __device__ __forceinline__ double fdp_div(double a, double b) {
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(b));
-  y = fma(fma(-b, y, 1.0), y, y);
   y = fma(fma(-b, y, 1.0), y, y);
   const double q = a * y;
   return fma(fma(-b, q, a), y, q);
@@ -76,6 +76,12 @@ struct ModeGroup {
   unsigned long long* trace;
 };
 constexpr int kTracePhases = 6;
+
+// K1 CTA: kK1Warps warps stacked along M (BM = kK1Warps * 8 * MT rows).
+#ifndef FDP_K1_WARPS
+#define FDP_K1_WARPS 4
+#endif
+constexpr int kK1Warps = FDP_K1_WARPS;
 
 // Tile configuration chosen for a problem size n (same for all problems of one launch).
 struct TileCfg {

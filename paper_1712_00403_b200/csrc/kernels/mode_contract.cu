@@ -23,7 +23,7 @@ namespace {
 #endif
 constexpr int BK = FDP_K1_BK;
 constexpr int STAGES = FDP_K1_STAGES;
-constexpr int WARPS = 4;
+constexpr int WARPS = kK1Warps;
 constexpr int THREADS = WARPS * 32;
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
@@ -84,16 +84,17 @@ mode_contract_kernel(const __grid_constant__ ModeGroup grp) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   // ---- per-thread load assignments (fixed across the K loop) ----
-  // KMAJ: thread loads k = tid % 16 of rows m = tid/16 + 8*j, j < BM/8.
+  // KMAJ: thread loads k = tid % BK of rows m = tid/BK + (THREADS/BK)*j, j < BM*BK/THREADS.
   // else : thread loads row m = tid % BM for k = tid/BM + (THREADS/BM)*j.
-  constexpr int A_ROWS_PER_THREAD = KMAJ ? BM / 8 : 1;
+  constexpr int RSTEP = THREADS / BK;  // KMAJ rows covered per pass
+  constexpr int A_ROWS_PER_THREAD = KMAJ ? BM / RSTEP : 1;
   long long a_off[A_ROWS_PER_THREAD];
   bool a_ok[A_ROWS_PER_THREAD];
   const int Qn = pb.Q;
   if (KMAJ) {
 #pragma unroll
     for (int j = 0; j < A_ROWS_PER_THREAD; ++j) {
-      long long m = m0 + tid / 16 + 8 * j;
+      long long m = m0 + tid / BK + RSTEP * j;
       a_ok[j] = m < M;
       // P == 1: row m = q + Q*b at xld*q + xbs*b, contiguous in k
       a_off[j] = a_ok[j] ? (long long)pb.xld * (m % Qn) + pb.xbs * (m / Qn) : 0;
@@ -113,11 +114,11 @@ mode_contract_kernel(const __grid_constant__ ModeGroup grp) {
     double* As = smem + stage * S::STAGE;
     double* Bs = As + S::A_ELEMS;
     if (KMAJ) {
-      const int k = tid % 16;
+      const int k = tid % BK;
       const bool kv = (k0 + k) < n;
 #pragma unroll
       for (int j = 0; j < A_ROWS_PER_THREAD; ++j) {
-        const int mr = tid / 16 + 8 * j;
+        const int mr = tid / BK + RSTEP * j;
         const bool v = a_ok[j] && kv;
         cp_async8(&As[mr * S::SA + k], X + (v ? a_off[j] + k0 + k : 0), v);
       }
@@ -266,7 +267,7 @@ TileCfg choose_tile(int n) {
   c.tiles_n = (n8 + c.NT - 1) / c.NT;
   c.MT = 2;
   c.ldw = c.tiles_n * 8 * c.NT;
-  c.kpad = ((n + 15) / 16) * 16;
+  c.kpad = ((n + 31) / 32) * 32;  // covers any K-tile depth <= 32
   return c;
 }
 
