@@ -352,6 +352,14 @@ def main():
                 k3_ms += ms
                 k3_by += by
     achieved = (k1_fl / (k1_ms * 1e-3)) / 1e12 if k1_ms > 0 else None
+    # DRAM traffic per K1 launch from the committed ncu --set full capture of this config
+    traffic = traffic_src = None
+    ncu_json = os.path.join(ROOT, "profiles", f"r01_ncu_cfg{cid}.json")
+    if os.path.exists(ncu_json):
+        ks = [k for k in json.load(open(ncu_json)).get("kernels", []) if "mode_" in k["kernel"]]
+        if ks:
+            traffic = float(np.mean([(k["dram_read_bytes"] or 0) + (k["dram_write_bytes"] or 0) for k in ks]))
+            traffic_src = f"{os.path.relpath(ncu_json, ROOT)} (mean of {len(ks)} K1 launches, bytes per launch)"
     launches = P.launch_count(batch)
     roof_kind = "per-launch CUDA events of K1 inside the apply graph"
     if slab:
@@ -394,7 +402,8 @@ def main():
             "peak": fp64_peak,
             "unit": "TFLOP/s",
             "frac": (achieved / fp64_peak) if achieved else None,
-            "traffic": None,
+            "traffic": traffic,
+            "traffic_source": traffic_src,
             "peak_source": "measured all-SM DMMA register loop, profiles/r01_fp64_peaks.json (MEASURED_PEAKS.json has no FP64 entry)",
             "measured_as": roof_kind,
             "k1_share_of_step": per_kind[0] / tot_ms if tot_ms else None,

@@ -180,6 +180,41 @@ int block_precond_profile_read(fdp_block h, int max, int32_t* kind, float* ms, d
                                double* bytes);
 
 /* ------------------------------------------------------------------------------------------
+ * Matrix-free sums of Kronecker products (the Stokes system blocks of the
+ * GPU-resident MINRES), y = beta*y + alpha * sum_t c_t (F_{t,D} (x) ... (x) F_{t,1}) x, with
+ * rectangular factors F_{t,d} (nout_d x nin_d) applied as mode products (eq. kronvec).
+ * ------------------------------------------------------------------------------------------ */
+typedef struct fdp_kron_s* fdp_kron;
+/* factors: host, nterms*D pointers, term-major (factor of term t, direction d at t*D + d), each
+ * column-major nout[d] x nin[d]; coef: nterms scalars. D in {2,3}, extents in [1, 2048]. */
+fdp_status kron_op_setup(int D, int nterms, const int32_t* nin, const int32_t* nout,
+                         const double* const* factors, const double* coef, int device,
+                         fdp_kron* out);
+size_t kron_op_workspace_bytes(fdp_kron h, int64_t batch);
+/* x: device, batch items of prod(nin) doubles at stride xbs; y: device, prod(nout) at stride ybs
+ * (must not overlap x). beta = 0 overwrites y (NaNs in y ignored). Asynchronous on `stream`. */
+fdp_status kron_op_apply(fdp_kron h, const double* x, int64_t xbs, double* y, int64_t ybs,
+                         double alpha, double beta, int64_t batch, void* workspace, void* stream);
+fdp_status kron_op_destroy(fdp_kron h);
+
+/* Mixed univariate matrix out[i, j] = int wt(x) b_test_i^(dtest)(x) b_trial_j^(dtrial)(x) dx on
+ * [0,1] over n_el uniform elements with q Gauss points per element (q <= 0: deg_test+deg_trial+1
+ * ... exact for unweighted products). wq: weights at the points iga_quadrature returns (n_el*q)
+ * or NULL for wt = 1. flags as iga_univariate (FDP_IGA_INTERIOR per space). out: host,
+ * column-major n_test x n_trial. */
+fdp_status iga_quadrature(int n_el, int q, double* x, double* w);
+fdp_status iga_mixed(int deg_test, int alpha_test, int flags_test, int deg_trial, int alpha_trial,
+                     int flags_trial, int n_el, int dtest, int dtrial, int q, const double* wq,
+                     double* out, int32_t* n_test, int32_t* n_trial);
+
+/* Vector kernels for the GPU Krylov driver (device pointers, asynchronous):
+ * result[0] = x . y (FP64, deterministic two-level reduction); out = a x + b y + c z (z may be
+ * NULL, out may alias any input). */
+fdp_status fdp_vec_dot(const double* x, const double* y, int64_t n, double* result, void* stream);
+fdp_status fdp_vec_lincomb(double a, const double* x, double b, const double* y, double c,
+                           const double* z, double* out, int64_t n, void* stream);
+
+/* ------------------------------------------------------------------------------------------
  * Slab decomposition for multi-GPU application: the slowest axis i3
  * is partitioned over `nranks` ranks (even split, the first n mod G ranks own one more plane).
  * Modes 1-2 are local to an i3-slab; mode 3 runs on i2-slabs after an all-to-all exchange (done

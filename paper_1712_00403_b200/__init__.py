@@ -67,6 +67,14 @@ def _load():
         "fdp_block_launch_count": (i32, [vp, i64]),
         "block_precond_profile": (i32, [vp, i32]),
         "fdp_slab_range": (i32, [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
+        "kron_op_setup": (i32, [i32, i32, vp, vp, vp, vp, i32, ctypes.POINTER(vp)]),
+        "kron_op_workspace_bytes": (sz, [vp, i64]),
+        "kron_op_apply": (i32, [vp, vp, i64, vp, i64, ctypes.c_double, ctypes.c_double, i64, vp, vp]),
+        "kron_op_destroy": (i32, [vp]),
+        "iga_quadrature": (i32, [i32, i32, vp, vp]),
+        "iga_mixed": (i32, [i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, vp, vp, _c_int32_p, _c_int32_p]),
+        "fdp_vec_dot": (i32, [vp, vp, i64, vp, vp]),
+        "fdp_vec_lincomb": (i32, [ctypes.c_double, vp, ctypes.c_double, vp, ctypes.c_double, vp, vp, i64, vp]),
         "fd_slab_workspace_bytes": (sz, [vp, i32, i32]),
         "fd_apply_slab": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, vp]),
         "kron_mass_slab_workspace_bytes": (sz, [vp, i32, i32]),
@@ -211,6 +219,79 @@ class FD:
             self.close()
         except Exception:
             pass
+
+
+def iga_quadrature(n_el: int, q: int):
+    """Gauss points / weights of libfdp's element quadrature on [0, 1] (n_el * q each)."""
+    x = np.zeros(n_el * q)
+    w = np.zeros(n_el * q)
+    _check(lib.iga_quadrature(n_el, q, _ptr(x), _ptr(w)))
+    return x, w
+
+
+def iga_mixed(test, trial, n_el: int, dtest: int = 0, dtrial: int = 0, q: int = 0, wq=None):
+    """int wt b_test^(dtest) b_trial^(dtrial); test/trial = (deg, alpha, flags)."""
+    nt, nr = ctypes.c_int32(0), ctypes.c_int32(0)
+    _check(lib.iga_mixed(*test, *trial, n_el, dtest, dtrial, q, None, None, ctypes.byref(nt), ctypes.byref(nr)))
+    out = np.zeros((nt.value, nr.value), order="F")
+    wq_ = None if wq is None else _host(wq)
+    _check(lib.iga_mixed(*test, *trial, n_el, dtest, dtrial, q, None if wq_ is None else _ptr(wq_), _ptr(out),
+                         ctypes.byref(nt), ctypes.byref(nr)))
+    return out
+
+
+class KronOp:
+    """kron_op_*: y = beta y + alpha sum_t c_t (F_{t,D} (x) .. (x) F_{t,1}) x, rectangular factors."""
+
+    def __init__(self, terms, coef, device: int = 0):
+        D = len(terms[0])
+        self.D = D
+        self.nin = [int(F.shape[1]) for F in terms[0]]
+        self.nout = [int(F.shape[0]) for F in terms[0]]
+        self._F = [_fortran(F) for T in terms for F in T]
+        nin = (ctypes.c_int32 * D)(*self.nin)
+        nout = (ctypes.c_int32 * D)(*self.nout)
+        Fp = (ctypes.c_void_p * len(self._F))(*[F.ctypes.data for F in self._F])
+        c = (ctypes.c_double * len(coef))(*[float(x) for x in coef])
+        h = ctypes.c_void_p()
+        _check(lib.kron_op_setup(D, len(terms), nin, nout, Fp, c, device, ctypes.byref(h)))
+        self.h = h
+        self.device = device
+
+    def workspace_bytes(self, batch: int = 1) -> int:
+        return int(lib.kron_op_workspace_bytes(self.h, batch))
+
+    def apply(self, x, y, alpha=1.0, beta=0.0, workspace=None, batch=1, xbs=0, ybs=0, stream=None):
+        import torch
+        if workspace is None:
+            workspace = torch.empty(max(1, self.workspace_bytes(batch) // 8), dtype=torch.float64,
+                                    device=x.device)
+        _check(lib.kron_op_apply(self.h, _dev(x, "x"), xbs, _dev(y, "y"), ybs, alpha, beta, batch,
+                                 _dev(workspace, "workspace"), _stream(stream)))
+        return y
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.kron_op_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def vec_dot(x, y, out, stream=None):
+    _check(lib.fdp_vec_dot(_dev(x, "x"), _dev(y, "y"), x.numel(), _dev(out, "out"), _stream(stream)))
+    return out
+
+
+def vec_lincomb(a, x, b, y, c, z, out, stream=None):
+    _check(lib.fdp_vec_lincomb(a, _dev(x, "x"), b, None if y is None else _dev(y, "y"), c,
+                               None if z is None else _dev(z, "z"), _dev(out, "out"), out.numel(),
+                               _stream(stream)))
+    return out
 
 
 def slab_range(n: int, nranks: int, rank: int):

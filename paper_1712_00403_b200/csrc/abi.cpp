@@ -343,7 +343,7 @@ static ModeProb make_mode_prob(const fdp_fd_s* h, int d, bool fwd, const double*
   p.xbs = xbs;
   p.ybs = ybs;
   p.P = (int)P;
-  p.n = h->n[d];
+  p.n = p.nout = h->n[d];
   p.Q = (int)Q;
   p.batch = (int)batch;
   p.ldw = h->cfg[d].ldw;
@@ -1093,7 +1093,7 @@ static cudaError_t enqueue_block(fdp_block h, const double* r, double* s, int64_
       p.W = h->Wq[d];
       p.N = nq;
       p.P = (int)P;
-      p.n = h->pres->n[d];
+      p.n = p.nout = h->pres->n[d];
       p.Q = (int)Q;
       p.batch = (int)batch;
       p.ldw = h->q_ldw[d];
@@ -1341,7 +1341,7 @@ static ModeProb slab_prob(const fdp_fd_s* h, int d, bool fwd, const double* X, d
   p.Y = Y;
   p.W = fwd ? h->Wf[d] : h->Wb[d];
   p.P = (int)P;
-  p.n = h->n[d];
+  p.n = p.nout = h->n[d];
   p.Q = (int)Q;
   p.N = P * h->n[d] * Q;
   p.xbs = p.ybs = 0;
@@ -1477,5 +1477,218 @@ extern "C" fdp_status kron_mass_apply_slab(fdp_mass h, int phase, int nranks, in
     FDP_CUDA(launch_slab_copy(in, out, (int)n1, (int)n2, (int)nz, nranks, 1, dscale, s),
              "kron_mass_apply_slab: unpack");
   }
+  return FDP_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+// host helpers: quadrature points and mixed univariate matrices
+// ------------------------------------------------------------------------------------------------
+extern "C" fdp_status iga_quadrature(int n_el, int q, double* x, double* w) {
+  if (n_el < 1 || q < 1) return fail(FDP_ERR_SHAPE, "iga_quadrature: n_el, q >= 1");
+  iga_quadrature_build(n_el, q, x, w);
+  return FDP_OK;
+}
+
+extern "C" fdp_status iga_mixed(int deg_test, int alpha_test, int flags_test, int deg_trial,
+                                int alpha_trial, int flags_trial, int n_el, int dtest, int dtrial,
+                                int q, const double* wq, double* out, int32_t* n_test,
+                                int32_t* n_trial) {
+  if (!n_test || !n_trial) return fail(FDP_ERR_INVALID_ARG, "iga_mixed: NULL size outputs");
+  std::string err;
+  int a = 0, b = 0;
+  int st = iga_mixed_build(deg_test, alpha_test, flags_test, deg_trial, alpha_trial, flags_trial,
+                           n_el, dtest, dtrial, q, wq, out, &a, &b, &err);
+  if (st) return fail((fdp_status)st, err);
+  *n_test = a;
+  *n_trial = b;
+  return FDP_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+// vector kernels
+// ------------------------------------------------------------------------------------------------
+static double* dot_scratch(int dev) {
+  static double* scratch[64] = {nullptr};
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!scratch[dev] && cudaMalloc(&scratch[dev], dot_scratch_doubles() * sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    scratch[dev] = nullptr;
+  }
+  return scratch[dev];
+}
+
+extern "C" fdp_status fdp_vec_dot(const double* x, const double* y, int64_t n, double* result,
+                                  void* stream) {
+  if (n < 0) return fail(FDP_ERR_SHAPE, "fdp_vec_dot: n < 0");
+  if (!is_device_ptr(result) || (n > 0 && (!is_device_ptr(x) || !is_device_ptr(y))))
+    return fail(FDP_ERR_INVALID_ARG, "fdp_vec_dot: device pointers required");
+  int dev = 0;
+  cudaGetDevice(&dev);
+  double* sc = dot_scratch(dev);
+  if (!sc) return fail(FDP_ERR_OOM, "fdp_vec_dot: scratch");
+  FDP_CUDA(launch_dot(x, y, n, result, sc, static_cast<cudaStream_t>(stream)), "fdp_vec_dot");
+  return FDP_OK;
+}
+
+extern "C" fdp_status fdp_vec_lincomb(double a, const double* x, double b, const double* y,
+                                      double c, const double* z, double* out, int64_t n,
+                                      void* stream) {
+  if (n < 0) return fail(FDP_ERR_SHAPE, "fdp_vec_lincomb: n < 0");
+  if (n == 0) return FDP_OK;
+  if (!is_device_ptr(x) || !is_device_ptr(out) || (y && !is_device_ptr(y)) || (z && !is_device_ptr(z)))
+    return fail(FDP_ERR_INVALID_ARG, "fdp_vec_lincomb: device pointers required");
+  FDP_CUDA(launch_lincomb(a, x, b, y, c, z, out, n, static_cast<cudaStream_t>(stream)), "fdp_vec_lincomb");
+  return FDP_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+// matrix-free sums of Kronecker products (NEXT-1 Stokes operator blocks)
+// ------------------------------------------------------------------------------------------------
+struct KronFactor {
+  int nin = 0, nout = 0;
+  TileCfg cfg{};
+  double* W = nullptr;  // W[k][a] = F[a][k], kpad x ldw
+};
+struct fdp_kron_s {
+  int D = 0, nterms = 0, device = 0;
+  int nin[3] = {1, 1, 1}, nout[3] = {1, 1, 1};
+  std::vector<double> coef;
+  std::vector<KronFactor> f;  // nterms * D
+};
+
+static void free_kron(fdp_kron h) {
+  if (!h) return;
+  for (auto& k : h->f) cudaFree(k.W);
+  delete h;
+}
+
+extern "C" fdp_status kron_op_setup(int D, int nterms, const int32_t* nin, const int32_t* nout,
+                                    const double* const* factors, const double* coef, int device,
+                                    fdp_kron* out) {
+  if (!out) return fail(FDP_ERR_INVALID_ARG, "kron_op_setup: out is NULL");
+  *out = nullptr;
+  if (D < 2 || D > 3) return fail(FDP_ERR_UNSUPPORTED, "kron_op_setup: D must be 2 or 3");
+  if (nterms < 1 || !nin || !nout || !factors || !coef)
+    return fail(FDP_ERR_INVALID_ARG, "kron_op_setup: bad arguments");
+  std::unique_ptr<fdp_kron_s> h(new (std::nothrow) fdp_kron_s);
+  if (!h) return fail(FDP_ERR_OOM, "kron_op_setup: host allocation");
+  h->D = D;
+  h->nterms = nterms;
+  h->device = device;
+  for (int d = 0; d < D; ++d) {
+    if (nin[d] < 1 || nin[d] > 2048 || nout[d] < 1 || nout[d] > 2048)
+      return fail(FDP_ERR_SHAPE, "kron_op_setup: extents must be in [1, 2048]");
+    h->nin[d] = nin[d];
+    h->nout[d] = nout[d];
+  }
+  h->coef.assign(coef, coef + nterms);
+  DeviceGuard dg(device);
+  fdp_kron raw = h.release();
+  raw->f.resize((size_t)nterms * D);
+  for (int t = 0; t < nterms; ++t)
+    for (int d = 0; d < D; ++d) {
+      const double* F = factors[t * D + d];
+      if (!F) {
+        free_kron(raw);
+        return fail(FDP_ERR_INVALID_ARG, "kron_op_setup: NULL factor");
+      }
+      KronFactor& kf = raw->f[t * D + d];
+      kf.nin = nin[d];
+      kf.nout = nout[d];
+      // columns tile over nout; the small path also needs BN >= nin (W rows staged in smem)
+      TileCfg c = choose_tile(std::max(nin[d], nout[d]) <= kSmallMaxN ? std::max(nin[d], nout[d]) : nout[d]);
+      c.kpad = ((nin[d] + 31) / 32) * 32;
+      kf.cfg = c;
+      const int rows = std::max(c.kpad, c.ldw);
+      std::vector<double> w((size_t)rows * c.ldw, 0.0);
+      for (int k = 0; k < nin[d]; ++k)
+        for (int a = 0; a < nout[d]; ++a) w[(size_t)k * c.ldw + a] = F[a + (size_t)nout[d] * k];
+      fdp_status st = dalloc(&kf.W, w.size());
+      cudaError_t e = st ? cudaSuccess : cudaMemcpy(kf.W, w.data(), w.size() * 8, cudaMemcpyHostToDevice);
+      if (!st && e == cudaSuccess) e = prepare_mode_kernels(c);
+      if (!st && e == cudaSuccess) e = prepare_mode_small(c.NT);
+      if (st || e != cudaSuccess) {
+        free_kron(raw);
+        return st ? st : cuda_fail(e, "kron_op_setup: upload");
+      }
+    }
+  *out = raw;
+  return FDP_OK;
+}
+
+static long long kron_max_inter(const fdp_kron_s* h) {
+  long long mx = 1;
+  for (int d = 0; d < h->D; ++d) {  // after contracting modes 0..d: nout for e <= d, nin after
+    long long sz = 1;
+    for (int e = 0; e < h->D; ++e) sz *= (e <= d ? h->nout[e] : h->nin[e]);
+    mx = std::max(mx, sz);
+  }
+  return mx;
+}
+
+extern "C" size_t kron_op_workspace_bytes(fdp_kron h, int64_t batch) {
+  return h && batch > 0 ? (size_t)(2 * kron_max_inter(h) * batch) * sizeof(double) : 0;
+}
+
+extern "C" fdp_status kron_op_apply(fdp_kron h, const double* x, int64_t xbs, double* y,
+                                    int64_t ybs, double alpha, double beta, int64_t batch,
+                                    void* workspace, void* stream) {
+  if (!h) return fail(FDP_ERR_INVALID_ARG, "kron_op_apply: NULL handle");
+  if (batch < 0) return fail(FDP_ERR_SHAPE, "kron_op_apply: batch < 0");
+  if (batch == 0) return FDP_OK;
+  if (!is_device_ptr(x) || !is_device_ptr(y) || !is_device_ptr(workspace))
+    return fail(FDP_ERR_INVALID_ARG, "kron_op_apply: device pointers required");
+  DeviceGuard dg(h->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int D = h->D;
+  const long long inter = kron_max_inter(h);
+  double* buf[2] = {static_cast<double*>(workspace), static_cast<double*>(workspace) + inter * batch};
+  for (int t = 0; t < h->nterms; ++t) {
+    const double* src = x;
+    long long sbs = xbs;
+    for (int d = 0; d < D; ++d) {
+      const KronFactor& kf = h->f[t * D + d];
+      long long P = 1, Q = 1;
+      for (int e = 0; e < d; ++e) P *= h->nout[e];
+      for (int e = d + 1; e < D; ++e) Q *= h->nin[e];
+      const bool last = d == D - 1;
+      double* dst = last ? y : buf[d % 2];
+      const long long dbs = last ? ybs : P * kf.nout * Q;
+      ModeProb p{};
+      p.X = src;
+      p.Y = dst;
+      p.W = kf.W;
+      p.P = (int)P;
+      p.n = kf.nin;
+      p.nout = kf.nout;
+      p.Q = (int)Q;
+      p.N = P * kf.nout * Q;
+      p.xbs = sbs;
+      p.ybs = dbs;
+      p.batch = (int)batch;
+      p.ldw = kf.cfg.ldw;
+      p.n1 = p.n1v = 1;
+      p.xld = kf.nin;
+      p.yld = kf.nout;
+      p.vx = p.vy = 0;
+      p.epi = last ? EPI_AXPBY : EPI_NONE;
+      p.alpha = alpha * h->coef[t];
+      p.beta = t == 0 ? beta : 1.0;
+      const int BM = kK1Warps * 8 * kf.cfg.MT;
+      p.tiles_m = (int)((P * Q * batch + BM - 1) / BM);
+      p.tiles_n = kf.cfg.tiles_n;
+      p.fd_work = 0;
+      FDP_CUDA(run1(p, kf.cfg, d == 0, s), "kron_op_apply");
+      src = dst;
+      sbs = dbs;
+    }
+  }
+  return FDP_OK;
+}
+
+extern "C" fdp_status kron_op_destroy(fdp_kron h) {
+  if (!h) return FDP_OK;
+  DeviceGuard dg(h->device);
+  free_kron(h);
   return FDP_OK;
 }

@@ -26,6 +26,7 @@ enum Epilogue : int {
   EPI_LAMBDA = 1,  // divide by Lambda[i] = lamrow(p) + lamcol[a]   (Algorithm 1 step 3)
   EPI_SCALE = 2,   // multiply by dscale[index within item]           (P^G post-scaling)
   EPI_FUSED = 3,   // small-n only: x_D U_D^T, divide by Lambda, x_D U_D in one pass
+  EPI_AXPBY = 4,   // Y = alpha * result + beta * Y (Kronecker operator terms accumulate)
 };
 
 struct ModeProb {
@@ -38,7 +39,9 @@ struct ModeProb {
   const double* lamcol;   //             d = D (the contracted, last direction)
   long long N;            // elements per batch item (of this tensor)
   long long xbs, ybs;     // batch-item strides of X and Y (elements)
-  int P, n, Q;            // per item; GEMM rows M = P * Q * batch
+  int P, n, Q;            // per item; GEMM rows M = P * Q * batch; n = contracted extent
+  int nout;               // output extent of the mode (= n for the square FD transforms)
+  double alpha, beta;     // EPI_AXPBY
   int batch;
   int ldw;
   int n1;                 // leading dimension of direction 1 (Lambda row decomposition)
@@ -125,6 +128,17 @@ cudaError_t launch_scale(const double* x, double* y, const double* s, long long 
                          long long xs, long long ys, cudaStream_t st);
 // Set the dynamic shared-memory attribute of the kernels a tile config uses (call outside capture).
 cudaError_t prepare_mode_kernels(const TileCfg& cfg);
+
+// Vector kernels (vec.cu)
+cudaError_t launch_dot(const double* x, const double* y, long long n, double* result,
+                       double* scratch, cudaStream_t s);
+int dot_scratch_doubles();
+cudaError_t launch_lincomb(double a, const double* x, double b, const double* y, double c,
+                           const double* z, double* out, long long n, cudaStream_t s);
+int iga_mixed_build(int deg_t, int alpha_t, int flags_t, int deg_r, int alpha_r, int flags_r,
+                    int n_el, int dtest, int dtrial, int q, const double* wq, double* out,
+                    int* n_test, int* n_trial, std::string* err);
+int iga_quadrature_build(int n_el, int q, double* x, double* w);
 
 // Slab pack (dir 0: z-slab -> piece buffer) / unpack (dir 1, optional scale on the z-slab).
 cudaError_t launch_slab_copy(const double* src, double* dst, int n1, int n2, int nz, int G, int dir,

@@ -186,4 +186,60 @@ int iga_greville_build(int deg, int alpha, int n_el, int flags, double* g, int* 
   return FDP_OK;
 }
 
+int iga_quadrature_build(int n_el, int q, double* x, double* w) {
+  std::vector<double> gx, gw;
+  gauss_rule(q, &gx, &gw);
+  for (int e = 0; e < n_el; ++e) {
+    const double a = (double)e / n_el, b = (double)(e + 1) / n_el;
+    for (int g = 0; g < q; ++g) {
+      if (x) x[e * q + g] = 0.5 * (a + b) + 0.5 * (b - a) * gx[g];
+      if (w) w[e * q + g] = 0.5 * (b - a) * gw[g];
+    }
+  }
+  return FDP_OK;
+}
+
+// out[i, j] = int wt b_test_i^(dtest) b_trial_j^(dtrial) over the uniform mesh (both spaces live
+// on the same n_el elements; each element has exactly one non-empty span in each knot vector).
+int iga_mixed_build(int deg_t, int alpha_t, int flags_t, int deg_r, int alpha_r, int flags_r,
+                    int n_el, int dtest, int dtrial, int q, const double* wq, double* out,
+                    int* n_test, int* n_trial, std::string* err) {
+  int nt = 0, nr = 0;
+  int st = iga_build(deg_t, alpha_t, n_el, flags_t & FDP_IGA_INTERIOR, 0.0, 0, nullptr, nullptr, &nt, err);
+  if (st) return st;
+  st = iga_build(deg_r, alpha_r, n_el, flags_r & FDP_IGA_INTERIOR, 0.0, 0, nullptr, nullptr, &nr, err);
+  if (st) return st;
+  *n_test = nt;
+  *n_trial = nr;
+  if (!out) return FDP_OK;
+  if (q <= 0) q = (deg_t + deg_r) / 2 + 2;
+  const std::vector<double> xt = knot_vector(deg_t, alpha_t, n_el), xr = knot_vector(deg_r, alpha_r, n_el);
+  const int mt = (int)xt.size() - deg_t - 1, mr = (int)xr.size() - deg_r - 1;
+  const int ot = (flags_t & FDP_IGA_INTERIOR) ? 1 : 0, orr = (flags_r & FDP_IGA_INTERIOR) ? 1 : 0;
+  std::vector<double> full((size_t)mt * mr, 0.0);
+  std::vector<double> gx, gw;
+  gauss_rule(q, &gx, &gw);
+  std::vector<double> Nt(deg_t + 1), dNt(deg_t + 1), Nr(deg_r + 1), dNr(deg_r + 1);
+  for (int e = 0; e < n_el; ++e) {
+    const double a = (double)e / n_el, b = (double)(e + 1) / n_el;
+    const double mid = 0.5 * (a + b);
+    const int st_ = find_span(xt, deg_t, mt, mid), sr = find_span(xr, deg_r, mr, mid);
+    for (int g = 0; g < q; ++g) {
+      const double u = mid + 0.5 * (b - a) * gx[g];
+      double wt = 0.5 * (b - a) * gw[g];
+      if (wq) wt *= wq[e * q + g];
+      span_basis(xt, deg_t, st_, u, Nt.data(), dNt.data());
+      span_basis(xr, deg_r, sr, u, Nr.data(), dNr.data());
+      for (int i = 0; i <= deg_t; ++i)
+        for (int j = 0; j <= deg_r; ++j) {
+          const double vt = dtest ? dNt[i] : Nt[i], vr = dtrial ? dNr[j] : Nr[j];
+          full[(st_ - deg_t + i) + (size_t)mt * (sr - deg_r + j)] += wt * vt * vr;
+        }
+    }
+  }
+  for (int j = 0; j < nr; ++j)
+    for (int i = 0; i < nt; ++i) out[i + (size_t)nt * j] = full[(i + ot) + (size_t)mt * (j + orr)];
+  return FDP_OK;
+}
+
 }  // namespace fdp

@@ -76,8 +76,8 @@ mode_contract_kernel(const __grid_constant__ ModeGroup grp) {
   const long long m0 = (long long)tm * BM;
   const int n0 = tn * BN;
   const long long M = (long long)pb.P * pb.Q * pb.batch;
-  const int P = pb.P, n = pb.n, ldw = pb.ldw;
-  const long long Pn = (long long)P * n;
+  const int P = pb.P, n = pb.n, ldw = pb.ldw, nout = pb.nout;
+  const long long Pn = (long long)P * n, Pno = (long long)P * nout;
   const double* __restrict__ X = pb.X;
   const double* __restrict__ W = pb.W;
 
@@ -203,7 +203,7 @@ mode_contract_kernel(const __grid_constant__ ModeGroup grp) {
       row_off = sidx + pb.ybs * (m / Qn);
     } else {
       const long long p = m % P, r = m / P;
-      sidx = p + Pn * (r % Qn);
+      sidx = p + Pno * (r % Qn);
       row_off = sidx + pb.ybs * (r / Qn);
       if (epi == EPI_LAMBDA) {
         const int i1 = (int)(p % pb.n1);
@@ -211,7 +211,7 @@ mode_contract_kernel(const __grid_constant__ ModeGroup grp) {
         if (!pad_row) lrow = pb.lam1 ? pb.lam0[i1] + pb.lam1[p / pb.n1] : pb.lam0[p];
       }
     }
-    const int ncols = KMAJ ? pb.yld : n;  // padded outputs also get their zero pad column
+    const int ncols = KMAJ ? pb.yld : nout;  // padded outputs also get their zero pad column
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
 #pragma unroll
@@ -219,9 +219,11 @@ mode_contract_kernel(const __grid_constant__ ModeGroup grp) {
         const int a = n0 + 8 * j + 2 * fc + h;
         if (a < ncols) {
           double v = acc[i][j][h];
+          double* yp = Y + row_off + (long long)P * a;
           if (epi == EPI_LAMBDA) v = pad_row ? 0.0 : fdp_div(v, lrow + pb.lamcol[a]);
           else if (epi == EPI_SCALE) v = v * pb.scale[sidx + (long long)P * a];
-          Y[row_off + (long long)P * a] = v;
+          else if (epi == EPI_AXPBY) v = pb.alpha * v + (pb.beta != 0.0 ? pb.beta * *yp : 0.0);
+          *yp = v;
         }
       }
     }

@@ -79,13 +79,15 @@ __device__ __forceinline__ void load_w(double* Ws, const ModeProb& pb, int tid) 
 
 // Geometry of one problem, per thread.
 struct Geo {
-  int n, P, Q, Pn, Mi, kpad, k4n, nch;
+  int n, nout, P, Q, Pn, Pno, Mi, kpad, k4n, nch;
   long long M;
   __device__ explicit Geo(const ModeProb& pb) {
     n = pb.n;
+    nout = pb.nout;
     P = pb.P;
     Q = pb.Q;
     Pn = P * n;
+    Pno = P * nout;
     Mi = P * Q;
     M = (long long)Mi * pb.batch;
     kpad = ((n + 15) / 16) * 16;
@@ -97,14 +99,15 @@ struct Geo {
 // element offset of GEMM row m within its batch item (32-bit: the host routes here only problems
 // with M < 2^31) and the batch item index; ld = fiber stride of the tensor (KMAJ)
 template <bool KMAJ>
-__device__ __forceinline__ void row_index(const Geo& g, int m, int& within, int& item, int ld) {
+__device__ __forceinline__ void row_index(const Geo& g, int m, int& within, int& item, int ld,
+                                          int pn) {
   const unsigned b = (unsigned)m / (unsigned)g.Mi;
   const int mi = m - (int)b * g.Mi;
   if (KMAJ) {
     within = ld * mi;  // P == 1: row = fiber q = mi
   } else {
     const unsigned q = (unsigned)mi / (unsigned)g.P;
-    within = (mi - (int)q * g.P) + g.Pn * (int)q;
+    within = (mi - (int)q * g.P) + pn * (int)q;  // pn = P * (extent of the mode in that tensor)
   }
   item = (int)b;
 }
@@ -134,7 +137,7 @@ __device__ __forceinline__ void load_panel_async(const ModeProb& pb, const Geo& 
   const int m0 = (int)(t * 8);
   if (KMAJ) {
     int w0, b0;
-    row_index<true>(g, m0, w0, b0, 1);
+    row_index<true>(g, m0, w0, b0, 1, 0);
     int mi = w0;
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
@@ -151,7 +154,7 @@ __device__ __forceinline__ void load_panel_async(const ModeProb& pb, const Geo& 
     const int m = m0 + r;
     const bool rv = (long long)m < g.M;
     int w = 0, b = 0;
-    if (rv) row_index<false>(g, m, w, b, 0);
+    if (rv) row_index<false>(g, m, w, b, 0, g.Pn);
     const double* src = X + (w + pb.xbs * b);
     for (int k = lane >> 3; k < g.kpad; k += 4) {
       const bool v = rv && k < g.n;
@@ -172,7 +175,7 @@ __device__ __forceinline__ void do_tile(const ModeProb& pb, const Geo& g, const 
   const int m0 = (int)(t * 8);
   if (KMAJ) {
     int mi, b0;
-    row_index<true>(g, m0, mi, b0, 1);  // fiber index of the tile's first row
+    row_index<true>(g, m0, mi, b0, 1, 0);  // fiber index of the tile's first row
     const double* src[8];
     bool rv[8];
 #pragma unroll
@@ -225,7 +228,7 @@ __device__ __forceinline__ void do_tile(const ModeProb& pb, const Geo& g, const 
     const int m = m0 + 2 * rp;
     const bool rv = (long long)m < g.M;  // M is even here, so the pair is all or nothing
     int w = 0, b = 0;
-    if (rv) row_index<false>(g, m, w, b, 0);
+    if (rv) row_index<false>(g, m, w, b, 0, g.Pn);
     const double* src = X + (w + pb.xbs * b);
     double2 v[12];
 #pragma unroll
@@ -248,7 +251,7 @@ __device__ __forceinline__ void do_tile(const ModeProb& pb, const Geo& g, const 
     const int m = m0 + r;
     const bool rv = (long long)m < g.M;
     int w = 0, b = 0;
-    if (rv) row_index<false>(g, m, w, b, 0);
+    if (rv) row_index<false>(g, m, w, b, 0, g.Pn);
     const double* src = X + (w + pb.xbs * b);
     double v[24];
 #pragma unroll
@@ -296,7 +299,7 @@ __device__ __forceinline__ void tile_compute_store(const ModeProb& pb, const Geo
   double lrow = 0.0;
   bool pad_row = false;  // padding row (i1 >= n1v) of a padded intermediate: output stays 0
   if (mv) {
-    row_index<KMAJ>(g, m, sidx, item, pb.yld);
+    row_index<KMAJ>(g, m, sidx, item, pb.yld, g.Pno);
     if (!KMAJ && (FUSED || pb.epi == EPI_LAMBDA)) {
       const int mi = m - item * g.Mi;
       const int p = mi - (int)((unsigned)mi / (unsigned)g.P) * g.P;
@@ -333,7 +336,7 @@ __device__ __forceinline__ void tile_compute_store(const ModeProb& pb, const Geo
 
   // epilogue values (Lambda / scale applied), then stores
   const int epi = FUSED ? EPI_NONE : pb.epi;
-  const int ncols = KMAJ ? pb.yld : g.n;  // padded KMAJ outputs also get their zero pad column
+  const int ncols = KMAJ ? pb.yld : g.nout;  // padded KMAJ outputs also get their zero pad column
 #pragma unroll
   for (int j = 0; j < NT; ++j)
 #pragma unroll
@@ -345,6 +348,20 @@ __device__ __forceinline__ void tile_compute_store(const ModeProb& pb, const Geo
       acc[j][h] = v;
     }
   double* __restrict__ Y = pb.Y + pb.ybs * (long long)item + sidx;
+  if (epi == EPI_AXPBY && mv) {  // kron-operator terms: Y = alpha * result + beta * Y (scalar path)
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int a = 8 * j + 2 * fc + h;
+        if (a < ncols) {
+          double* yp = Y + (KMAJ ? 1 : g.P) * a;
+          *yp = pb.alpha * acc[j][h] + (pb.beta != 0.0 ? pb.beta * *yp : 0.0);
+        }
+      }
+    __syncwarp();
+    return;
+  }
   if (pb.vy && KMAJ) {
     // (a, a+1) adjacent in a row of an even-stride tensor
     if (mv) {

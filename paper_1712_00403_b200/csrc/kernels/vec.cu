@@ -1,0 +1,77 @@
+// Vector kernels of the GPU-resident Krylov driver: dot products with a
+// deterministic two-level reduction (fixed grid, fixed order) and fused linear combinations.
+// HBM-bound streaming (16-24 B per element).
+#include "../fdp_internal.h"
+
+namespace fdp {
+namespace {
+
+constexpr int kDotBlocks = 296;  // 2 x 148 SMs, fixed so the reduction order is reproducible
+constexpr int kDotThreads = 256;
+
+__global__ void dot_partial_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                                   long long n, double* __restrict__ partial) {
+  __shared__ double sh[kDotThreads / 32];
+  double s = 0.0;
+  for (long long i = blockIdx.x * (long long)kDotThreads + threadIdx.x; i < n;
+       i += (long long)gridDim.x * kDotThreads)
+    s = fma(x[i], y[i], s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < kDotThreads / 32 ? sh[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) partial[blockIdx.x] = v;
+  }
+}
+
+__global__ void dot_final_kernel(const double* __restrict__ partial, double* __restrict__ out) {
+  __shared__ double sh[kDotThreads / 32];
+  double v = 0.0;
+  for (int i = threadIdx.x; i < kDotBlocks; i += kDotThreads) v += partial[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double w = threadIdx.x < kDotThreads / 32 ? sh[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) w += __shfl_down_sync(0xffffffffu, w, o);
+    if (threadIdx.x == 0) out[0] = w;
+  }
+}
+
+__global__ void lincomb_kernel(double a, const double* x, double b, const double* y, double c,
+                               const double* z, double* out, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double v = a * x[i];
+    if (y) v = fma(b, y[i], v);
+    if (z) v = fma(c, z[i], v);
+    out[i] = v;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_dot(const double* x, const double* y, long long n, double* result,
+                       double* scratch, cudaStream_t s) {
+  dot_partial_kernel<<<kDotBlocks, kDotThreads, 0, s>>>(x, y, n, scratch);
+  dot_final_kernel<<<1, kDotThreads, 0, s>>>(scratch, result);
+  return cudaGetLastError();
+}
+
+int dot_scratch_doubles() { return kDotBlocks; }
+
+cudaError_t launch_lincomb(double a, const double* x, double b, const double* y, double c,
+                           const double* z, double* out, long long n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 8);
+  lincomb_kernel<<<blocks, 256, 0, s>>>(a, x, b, y, c, z, out, n);
+  return cudaGetLastError();
+}
+
+}  // namespace fdp

@@ -1,0 +1,169 @@
+"""GPU-resident preconditioned MINRES with a matrix-free Kronecker Stokes operator on the unit
+cube / square ("making P_D-MINRES end-to-end on B200").
+
+Operator (§3; identity map): a(w, v) = int 2 nu grad^s w : grad^s v gives
+A_kk = sum_d c_d (K_d at d, M elsewhere) [+ Nitsche K~ for the RT tangential factors, P:701-704]
+and, for r != s, A_rs = (G at s, G^T-type at r, M elsewhere) with G = int b'_test b_trial;
+B_r = -( D^QV at r, M^QV elsewhere ), b(v, q) = -int q div v. Every block is a libfdp KronOp
+(rectangular DMMA mode contractions with an accumulating epilogue); the 1D factors come from
+libfdp's own quadrature (iga_mixed / iga_univariate). A separable viscosity
+nu = sum_t c_t prod_d w_t(x_d) enters as extra weighted Kronecker terms; it must equal 1 on the
+boundary so the Nitsche terms keep weight 1 (true for config 3's nu).
+
+MINRES is Paige & Saunders' recurrence (tolerance 1e-8, x0 = 0) with every
+vector operation in libfdp kernels (fdp_vec_dot / fdp_vec_lincomb); only the scalar recurrence
+runs on the host. Stopping rule: preconditioned residual phibar_k / phibar_0 <= tol (C-15).
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from . import (FDP_IGA_INTERIOR, FDP_IGA_NITSCHE, KronOp, iga_mixed, iga_quadrature,
+               iga_univariate, vec_dot, vec_lincomb)
+
+
+def _spaces(D, disc, p):
+    a = p - 1
+    Q = (p, a, 0)
+    if disc == "TH":
+        V = [[(p + 1, a, FDP_IGA_INTERIOR)] * D for _ in range(D)]
+    elif disc == "RT":
+        N = (p + 1, a + 1, FDP_IGA_INTERIOR)
+        T = (p, a, 0)
+        V = [[N if d == k else T for d in range(D)] for k in range(D)]
+    else:
+        raise ValueError(disc)
+    return V, Q
+
+
+class StokesOperator:
+    """y = calA x for x = [u_1 | .. | u_D | p] (vec order, i1 fastest), on cuda:device."""
+
+    def __init__(self, D: int, disc: str, p: int, n_el: int, nu_terms=None, device: int = 0):
+        import torch
+        self.torch = torch
+        self.D = D
+        nu_terms = nu_terms or [(1.0, None)]
+        weighted = any(w is not None for _, w in nu_terms)
+        q = p + 3 + (4 if weighted else 0)
+        V, Qs = _spaces(D, disc, p)
+        xq, _ = iga_quadrature(n_el, q)
+        mixed = lambda t, r, dt=0, dr=0, w=None: iga_mixed(t, r, n_el, dt, dr, q, None if w is None else w(xq))
+        cp = 5.0 * p
+        self.diag, self.off, self.B, self.BT = [], {}, [], []
+        for k in range(D):
+            terms, coef = [], []
+            for ct, ws in nu_terms:
+                wd = (lambda d: None) if ws is None else (lambda d, ws=ws: ws[d])
+                Ms = [mixed(V[k][d], V[k][d], w=wd(d)) for d in range(D)]
+                Ks = []
+                for d in range(D):
+                    if disc == "RT" and d != k and ws is None:
+                        Kt, _ = iga_univariate(p, p - 1, n_el, FDP_IGA_NITSCHE, cp)
+                        Ks.append(Kt)
+                    else:
+                        Ks.append(mixed(V[k][d], V[k][d], 1, 1, wd(d)))
+                for d in range(D):
+                    terms.append([Ks[e] if e == d else Ms[e] for e in range(D)])
+                    coef.append(ct * (1.0 + (d == k)))
+            self.diag.append(KronOp(terms, coef, device))
+        for r in range(D):
+            for s in range(D):
+                if r == s:
+                    continue
+                terms, coef = [], []
+                for ct, ws in nu_terms:
+                    F = [mixed(V[r][d], V[s][d], int(d == s), int(d == r), None if ws is None else ws[d])
+                         for d in range(D)]
+                    terms.append(F)
+                    coef.append(ct)
+                self.off[(r, s)] = KronOp(terms, coef, device)
+        for r in range(D):
+            F = [mixed(Qs, V[r][d], 0, int(d == r)) for d in range(D)]
+            self.B.append(KronOp([F], [-1.0], device))
+            self.BT.append(KronOp([[np.asfortranarray(f.T) for f in F]], [-1.0], device))
+        self.vel_dims = [self.diag[k].nin for k in range(D)]
+        self.q_dims = self.B[0].nout
+        self.sizes = [int(np.prod(v)) for v in self.vel_dims] + [int(np.prod(self.q_dims))]
+        self.off_idx = np.concatenate([[0], np.cumsum(self.sizes)]).astype(np.int64)
+        self.n = int(self.off_idx[-1])
+        ops = self.diag + list(self.off.values()) + self.B + self.BT
+        self.ws = torch.empty(max(op.workspace_bytes(1) for op in ops) // 8 + 1, dtype=torch.float64,
+                              device=f"cuda:{device}")
+
+    def apply(self, x, y):
+        o = self.off_idx
+        D = self.D
+        blk = lambda v, k: v[o[k]:o[k + 1]]
+        for r in range(D):
+            yr = blk(y, r)
+            self.diag[r].apply(blk(x, r), yr, 1.0, 0.0, self.ws)
+            for s in range(D):
+                if s != r:
+                    self.off[(r, s)].apply(blk(x, s), yr, 1.0, 1.0, self.ws)
+            self.BT[r].apply(blk(x, D), yr, 1.0, 1.0, self.ws)
+        yp = blk(y, D)
+        for r in range(D):
+            self.B[r].apply(blk(x, r), yp, 1.0, 0.0 if r == 0 else 1.0, self.ws)
+        return y
+
+
+def minres(apply_A, apply_P, b, tol: float = 1e-8, maxit: int = 20000):
+    """GPU MINRES: b (cuda float64), apply_A(x, y) / apply_P(r, z) write into y / z.
+    Returns (x, iterations, history of phibar/beta1)."""
+    import torch
+    n = b.numel()
+    dev = b.device
+    z = lambda: torch.zeros(n, dtype=torch.float64, device=dev)
+    x, r1, r2, y, v, w, w1, w2 = z(), b.clone(), b.clone(), z(), z(), z(), z(), z()
+    dbuf = torch.zeros(2, dtype=torch.float64, device=dev)
+
+    def dot(a, c, slot=0):
+        vec_dot(a, c, dbuf[slot:slot + 1])
+        return float(dbuf[slot].item())
+
+    apply_P(r1, y)
+    beta1 = dot(r1, y)
+    if beta1 < 0:
+        raise ValueError("preconditioner is not positive definite")
+    beta1 = math.sqrt(beta1)
+    if beta1 == 0.0:
+        return x, 0, [0.0]
+    oldb, beta, dbar, epsln, phibar = 0.0, beta1, 0.0, 0.0, beta1
+    cs, sn = -1.0, 0.0
+    hist = [1.0]
+    eps = np.finfo(np.float64).eps
+    for itn in range(1, maxit + 1):
+        vec_lincomb(1.0 / beta, y, 0.0, None, 0.0, None, v)           # v = y / beta
+        apply_A(v, y)                                                  # y = A v
+        if itn >= 2:
+            vec_lincomb(1.0, y, -beta / oldb, r1, 0.0, None, y)       # y -= (beta/oldb) r1
+        alfa = dot(v, y)
+        vec_lincomb(1.0, y, -alfa / beta, r2, 0.0, None, y)           # y -= (alfa/beta) r2
+        r1, r2 = r2, r1
+        r2.copy_(y)                                                     # r1 <- r2, r2 <- y
+        apply_P(r2, y)
+        oldb = beta
+        beta = dot(r2, y)
+        if beta < 0:
+            raise ValueError("preconditioner is not positive definite")
+        beta = math.sqrt(beta)
+        oldeps = epsln
+        delta = cs * dbar + sn * alfa
+        gbar = sn * dbar - cs * alfa
+        epsln = sn * beta
+        dbar = -cs * beta
+        gamma = max(math.hypot(gbar, beta), eps)
+        cs = gbar / gamma
+        sn = beta / gamma
+        phi = cs * phibar
+        phibar = sn * phibar
+        w1, w2, w = w2, w, w1                                          # rotate buffers
+        vec_lincomb(1.0 / gamma, v, -oldeps / gamma, w1, -delta / gamma, w2, w)
+        vec_lincomb(1.0, x, phi, w, 0.0, None, x)
+        hist.append(phibar / beta1)
+        if phibar / beta1 <= tol:
+            return x, itn, hist
+    return x, maxit, hist

@@ -17,7 +17,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-__all__ = ["Workload", "CONFIGS", "rhs", "viscosity"]
+__all__ = ["Workload", "CONFIGS", "rhs", "viscosity", "viscosity_separable"]
 
 
 @dataclass(frozen=True)
@@ -60,3 +60,10 @@ def viscosity(x, y, z=None):
     if z is not None:
         s = s * np.sin(2 * math.pi * np.asarray(z))
     return 1.0 + 0.5 * s
+
+
+def viscosity_separable(dim: int = 3):
+    """The same nu as ``viscosity`` written as separable terms [(c_t, [w_t1(x), .., w_tD(x)])]:
+    1 + 0.5 prod_d sin(2 pi x_d) (None = constant-1 term)."""
+    s = lambda x: np.sin(2 * math.pi * np.asarray(x))
+    return [(1.0, None), (0.5, [s] * dim)]

@@ -1,0 +1,98 @@
+"""NEXT-1: GPU-resident P_D-MINRES with libfdp's matrix-free Kronecker Stokes
+operator. Parity against the oracle: the Kronecker operator (rectangular factors, accumulating
+epilogue), the full Stokes operator (configs 1-3, ν = 1 and config 3's variable ν), the vector
+kernels, and MINRES iteration counts (GPU operator + GPU P_D vs oracle operator + oracle P_D)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_1712_00403_b200 as fdp  # noqa: E402
+import synth  # noqa: E402
+from paper_1712_00403_b200 import krylov  # noqa: E402
+from oracle import kron as okron  # noqa: E402
+from oracle import minres as ominres  # noqa: E402
+from oracle import precond as oprec  # noqa: E402
+from oracle import spaces as ospaces  # noqa: E402
+from oracle import stokes as ostokes  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b)))
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+@pytest.mark.parametrize("nin,nout", [((5, 7, 3), (4, 9, 6)), ((65, 33, 9), (35, 40, 9)),
+                                      ((120, 3, 5), (7, 130, 2)), ((6, 11), (13, 4))])
+def test_kron_op_rectangular_terms(nin, nout):
+    rng = np.random.default_rng(len(nin) + nin[0])
+    terms = [[rng.standard_normal((o, i)) for i, o in zip(nin, nout)] for _ in range(3)]
+    coef = [1.5, -0.25, 2.0]
+    op = fdp.KronOp(terms, coef)
+    x = rng.standard_normal((2, int(np.prod(nin))))
+    y0 = rng.standard_normal((2, int(np.prod(nout))))
+    X = dev(x)
+    Y = dev(y0)
+    op.apply(X, Y, alpha=0.5, beta=-2.0, batch=2, xbs=x.shape[1], ybs=y0.shape[1])
+    for b in range(2):
+        ref = -2.0 * y0[b] + 0.5 * sum(c * okron.kron_matvec(list(reversed(T)), x[b]) for c, T in zip(coef, terms))
+        assert rel(Y[b].cpu().numpy(), ref) < 1e-13
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3])
+def test_stokes_operator_matches_oracle(cid):
+    w = synth.CONFIGS[cid]
+    nu_o = ostokes.config3_nu_terms(w.dim) if w.variable_nu else None
+    nu_g = synth.viscosity_separable(w.dim) if w.variable_nu else None
+    op = ostokes.StokesCube(w.dim, w.disc, w.p, w.n_el, nu_terms=nu_o)
+    gop = krylov.StokesOperator(w.dim, w.disc, w.p, w.n_el, nu_terms=nu_g)
+    assert gop.n == op.n
+    x = np.random.default_rng(cid).standard_normal(op.n)
+    y = torch.empty(op.n, dtype=torch.float64, device="cuda")
+    gop.apply(dev(x), y)
+    ref = op.matvec(x)
+    for k in range(len(op.sizes)):
+        a, b = op.off_idx[k], op.off_idx[k + 1]
+        assert rel(y[a:b].cpu().numpy(), ref[a:b]) < 1e-12, k
+
+
+def test_vector_kernels():
+    rng = np.random.default_rng(3)
+    x, y, z = rng.standard_normal((3, 1_000_003))
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    fdp.vec_dot(dev(x), dev(y), out)
+    assert abs(out.item() - x @ y) < 1e-12 * np.abs(x * y).sum()
+    o = torch.empty(x.size, dtype=torch.float64, device="cuda")
+    fdp.vec_lincomb(2.0, dev(x), -1.0, dev(y), 0.5, dev(z), o)
+    assert np.max(np.abs(o.cpu().numpy() - (2 * x - y + 0.5 * z))) < 1e-14 * 10
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3])
+def test_gpu_minres_iteration_counts(cid):
+    """Whole P_D-MINRES on the GPU (libfdp operator, preconditioner and vector kernels) vs the
+    oracle's MINRES with the oracle operator and P_D: identical iteration counts."""
+    w = synth.CONFIGS[cid]
+    nu_o = ostokes.config3_nu_terms(w.dim) if w.variable_nu else None
+    nu_g = synth.viscosity_separable(w.dim) if w.variable_nu else None
+    op = ostokes.StokesCube(w.dim, w.disc, w.p, w.n_el, nu_terms=nu_o)
+    od = ospaces.build(w.dim, w.disc, w.p, w.n_el)
+    gd = fdp.discretization(w.dim, w.disc, w.p, w.n_el)
+    dv = dq = None
+    if w.variable_nu:
+        dv, dq = ospaces.nu_scalings(od, synth.viscosity)
+    f = ostokes.project_rhs(synth.rhs(w.seed, op.n, 1)[0], op.sizes[-1])
+    x_o, it_o, h_o = ominres.minres(op.matvec, f, oprec.BlockPrecond(od, dv, dq).apply)
+
+    gop = krylov.StokesOperator(w.dim, w.disc, w.p, w.n_el, nu_terms=nu_g)
+    P = fdp.build_block(gd, dscale_vel=dv, dscale_pres=dq)
+    ws = P.workspace(1)
+    x_g, it_g, h_g = krylov.minres(gop.apply, lambda r, z: P.apply(r, z, workspace=ws), dev(f))
+    assert it_g == it_o, (cid, it_g, it_o)
+    n = min(len(h_o), len(h_g))
+    assert max(abs(a - b) / a for a, b in zip(h_o[:n], h_g[:n])) < 1e-6
+    assert rel(x_g.cpu().numpy(), x_o) < 1e-6

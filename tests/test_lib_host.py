@@ -110,3 +110,30 @@ def test_discretization_matches_oracle_sizes():
         assert g.comp_dims == [c.dims for c in o.comps]
         assert g.n_total == o.n_total
         assert g.coef == [c.coef for c in o.comps]
+
+
+@pytest.mark.parametrize("case", [
+    ((3, 1, 1), (3, 1, 1), 0, 1), ((2, 1, 0), (3, 1, 1), 0, 1), ((2, 1, 0), (3, 1, 1), 0, 0),
+    ((4, 3, 1), (3, 2, 0), 1, 0), ((5, 4, 1), (5, 4, 1), 1, 1)])
+def test_iga_mixed_matches_oracle(case):
+    from oracle import stokes as ost
+    (dt, at, ft), (dr, ar, fr), dtest, dtrial = case
+    n_el = 5
+    q = max(dt, dr) + 3
+    A = fdp.iga_mixed((dt, at, ft), (dr, ar, fr), n_el, dtest, dtrial, q)
+    Ao = ost._mixed(ost._space(dt, at, n_el, bool(ft & 1)), ost._space(dr, ar, n_el, bool(fr & 1)),
+                    n_el, q, bool(dtest), bool(dtrial))
+    assert A.shape == Ao.shape
+    assert np.max(np.abs(A - Ao)) <= 1e-13 * np.max(np.abs(Ao))
+
+
+def test_iga_mixed_weighted_and_quadrature():
+    from oracle import stokes as ost
+    n_el, q = 6, 7
+    x, w = fdp.iga_quadrature(n_el, q)
+    assert abs(w.sum() - 1.0) < 1e-14 and np.all((x > 0) & (x < 1))
+    wt = np.sin(2 * np.pi * x)
+    A = fdp.iga_mixed((3, 2, 1), (3, 2, 1), n_el, 1, 1, q, wt)
+    Ao = ost._mixed(ost._space(3, 2, n_el, True), ost._space(3, 2, n_el, True), n_el, q, True, True,
+                    weight=lambda t: np.sin(2 * np.pi * t))
+    assert np.max(np.abs(A - Ao)) <= 1e-13 * np.max(np.abs(Ao))
