@@ -884,11 +884,16 @@ struct fdp_block_s {
   cudaStream_t cap = nullptr;  // private capture stream
   // graph cache
   std::mutex mu;
-  const double* g_r = nullptr;
-  double* g_s = nullptr;
-  void* g_ws = nullptr;
-  int64_t g_batch = -1;
-  cudaGraphExec_t exec = nullptr;
+  struct GraphEntry {
+    const double* r;
+    double* s;
+    void* ws;
+    int64_t batch;
+    cudaGraphExec_t exec;
+    unsigned long long used;
+  };
+  std::vector<GraphEntry> graphs;  // small LRU cache keyed by (r, s, workspace, batch)
+  unsigned long long tick = 0;
   // plane-pipeline counters (zeroed at allocation, self-resetting)
   int* sync = nullptr;
   long long sync_cap = 0;
@@ -907,7 +912,7 @@ static void free_block(fdp_block h) {
   if (!h) return;
   for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
   cudaFree(h->sync);
-  if (h->exec) cudaGraphExecDestroy(h->exec);
+  for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);
   if (h->cap) cudaStreamDestroy(h->cap);
   cudaFree(h->dv);
   cudaFree(h->dq);
@@ -1135,10 +1140,8 @@ extern "C" fdp_status block_precond_profile(fdp_block h, int enable) {
   }
   if ((enable != 0) != h->prof) {
     h->prof = enable != 0;
-    if (h->exec) {  // force re-capture with / without event nodes
-      cudaGraphExecDestroy(h->exec);
-      h->exec = nullptr;
-    }
+    for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);  // re-capture with / without events
+    h->graphs.clear();
   }
   return FDP_OK;
 }
@@ -1198,7 +1201,10 @@ extern "C" fdp_status block_precond_apply(fdp_block h, const double* r, double* 
   if (batch < 0) return fail(FDP_ERR_SHAPE, "block_precond_apply: batch < 0");
   if (batch == 0) return FDP_OK;
   std::lock_guard<std::mutex> lk(h->mu);
-  const bool same = h->exec && r == h->g_r && s == h->g_s && workspace == h->g_ws && batch == h->g_batch;
+  fdp_block_s::GraphEntry* hit = nullptr;
+  for (auto& g : h->graphs)
+    if (g.r == r && g.s == s && g.ws == workspace && g.batch == batch) hit = &g;
+  const bool same = hit != nullptr;
   if (!same) {
     if (!is_device_ptr(r) || !is_device_ptr(s))
       return fail(FDP_ERR_INVALID_ARG, "block_precond_apply: r and s must be device pointers");
@@ -1229,9 +1235,14 @@ extern "C" fdp_status block_precond_apply(fdp_block h, const double* r, double* 
     return FDP_OK;
   }
   if (!same) {
-    if (h->exec) {
-      cudaGraphExecDestroy(h->exec);
-      h->exec = nullptr;
+    constexpr size_t kMaxGraphs = 4;
+    if (h->graphs.size() >= kMaxGraphs) {  // evict the least recently used
+      size_t lru = 0;
+      for (size_t i = 1; i < h->graphs.size(); ++i)
+        if (h->graphs[i].used < h->graphs[lru].used) lru = i;
+      FDP_CUDA(cudaStreamSynchronize(st), "block_precond_apply: evict sync");
+      cudaGraphExecDestroy(h->graphs[lru].exec);
+      h->graphs.erase(h->graphs.begin() + lru);
     }
     cudaGraph_t g = nullptr;
     FDP_CUDA(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal), "capture begin");
@@ -1242,18 +1253,15 @@ extern "C" fdp_status block_precond_apply(fdp_block h, const double* r, double* 
       return cuda_fail(e, "block_precond_apply: enqueue");
     }
     if (e2 != cudaSuccess) return cuda_fail(e2, "block_precond_apply: capture end");
-    e = cudaGraphInstantiate(&h->exec, g, 0);
+    cudaGraphExec_t ex = nullptr;
+    e = cudaGraphInstantiate(&ex, g, 0);
     cudaGraphDestroy(g);
-    if (e != cudaSuccess) {
-      h->exec = nullptr;
-      return cuda_fail(e, "block_precond_apply: instantiate");
-    }
-    h->g_r = r;
-    h->g_s = s;
-    h->g_ws = workspace;
-    h->g_batch = batch;
+    if (e != cudaSuccess) return cuda_fail(e, "block_precond_apply: instantiate");
+    h->graphs.push_back({r, s, workspace, batch, ex, 0});
+    hit = &h->graphs.back();
   }
-  FDP_CUDA(cudaGraphLaunch(h->exec, st), "block_precond_apply: graph launch");
+  hit->used = ++h->tick;
+  FDP_CUDA(cudaGraphLaunch(hit->exec, st), "block_precond_apply: graph launch");
   return FDP_OK;
 }
 

@@ -94,6 +94,24 @@ class StokesOperator:
                               device=f"cuda:{device}")
 
     def apply(self, x, y):
+        """y = calA x. The ~20 KronOp launches are captured once per (x, y) pair into a CUDA graph
+        and replayed (no allocation or host synchronisation inside)."""
+        torch = self.torch
+        key = (x.data_ptr(), y.data_ptr())
+        if not hasattr(self, "_graphs"):
+            self._graphs = {}
+        g = self._graphs.get(key)
+        if g is None:
+            self._apply_direct(x, y)  # warm (kernel attributes, lazy module state)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._apply_direct(x, y)
+            self._graphs[key] = g
+        g.replay()
+        return y
+
+    def _apply_direct(self, x, y):
         o = self.off_idx
         D = self.D
         blk = lambda v, k: v[o[k]:o[k + 1]]
@@ -110,15 +128,26 @@ class StokesOperator:
         return y
 
 
+_BUFFERS = {}
+
+
 def minres(apply_A, apply_P, b, tol: float = 1e-8, maxit: int = 20000):
     """GPU MINRES: b (cuda float64), apply_A(x, y) / apply_P(r, z) write into y / z.
     Returns (x, iterations, history of phibar/beta1)."""
     import torch
     n = b.numel()
     dev = b.device
-    z = lambda: torch.zeros(n, dtype=torch.float64, device=dev)
-    x, r1, r2, y, v, w, w1, w2 = z(), b.clone(), b.clone(), z(), z(), z(), z(), z()
-    dbuf = torch.zeros(2, dtype=torch.float64, device=dev)
+    # persistent buffers per (n, device): repeated solves hit the operator / preconditioner graph
+    # caches (they are keyed by buffer addresses)
+    key = (n, str(dev))
+    if key not in _BUFFERS:
+        _BUFFERS[key] = [torch.empty(n, dtype=torch.float64, device=dev) for _ in range(8)] + \
+                        [torch.empty(2, dtype=torch.float64, device=dev)]
+    x, r1, r2, y, v, w, w1, w2, dbuf = _BUFFERS[key]
+    for t in (x, y, v, w, w1, w2):
+        t.zero_()
+    r1.copy_(b)
+    r2.copy_(b)
 
     def dot(a, c, slot=0):
         vec_dot(a, c, dbuf[slot:slot + 1])
@@ -130,7 +159,7 @@ def minres(apply_A, apply_P, b, tol: float = 1e-8, maxit: int = 20000):
         raise ValueError("preconditioner is not positive definite")
     beta1 = math.sqrt(beta1)
     if beta1 == 0.0:
-        return x, 0, [0.0]
+        return x.clone(), 0, [0.0]
     oldb, beta, dbar, epsln, phibar = 0.0, beta1, 0.0, 0.0, beta1
     cs, sn = -1.0, 0.0
     hist = [1.0]
@@ -165,5 +194,5 @@ def minres(apply_A, apply_P, b, tol: float = 1e-8, maxit: int = 20000):
         vec_lincomb(1.0, x, phi, w, 0.0, None, x)
         hist.append(phibar / beta1)
         if phibar / beta1 <= tol:
-            return x, itn, hist
-    return x, maxit, hist
+            return x.clone(), itn, hist
+    return x.clone(), maxit, hist
