@@ -196,6 +196,14 @@ size_t kron_op_workspace_bytes(fdp_kron h, int64_t batch);
 fdp_status kron_op_apply(fdp_kron h, const double* x, int64_t xbs, double* y, int64_t ybs,
                          double alpha, double beta, int64_t batch, void* workspace, void* stream);
 fdp_status kron_op_destroy(fdp_kron h);
+/* Several operators in few launches (batch 1): for every distinct output pointer Y among y[i],
+ * Y = beta * Y + sum_{i : y[i] == Y} alpha[i] * ops[i] x[i]. All terms of all operators run as one
+ * grouped launch per mode (independent problems), each writing a private partial; one summation
+ * pass per distinct output then combines them (no read-modify-write races). workspace >=
+ * kron_ops_workspace_bytes(nops, ops). x[i] must not overlap any y. */
+size_t kron_ops_workspace_bytes(int nops, const fdp_kron* ops);
+fdp_status kron_ops_apply(int nops, const fdp_kron* ops, const double* const* x, double* const* y,
+                          const double* alpha, double beta, void* workspace, void* stream);
 
 /* Mixed univariate matrix out[i, j] = int wt(x) b_test_i^(dtest)(x) b_trial_j^(dtrial)(x) dx on
  * [0,1] over n_el uniform elements with q Gauss points per element (q <= 0: deg_test+deg_trial+1

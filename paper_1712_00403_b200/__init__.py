@@ -71,6 +71,9 @@ def _load():
         "kron_op_workspace_bytes": (sz, [vp, i64]),
         "kron_op_apply": (i32, [vp, vp, i64, vp, i64, ctypes.c_double, ctypes.c_double, i64, vp, vp]),
         "kron_op_destroy": (i32, [vp]),
+        "kron_ops_workspace_bytes": (sz, [i32, ctypes.POINTER(vp)]),
+        "kron_ops_apply": (i32, [i32, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp),
+                                 ctypes.POINTER(ctypes.c_double), ctypes.c_double, vp, vp]),
         "iga_quadrature": (i32, [i32, i32, vp, vp]),
         "iga_mixed": (i32, [i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, vp, vp, _c_int32_p, _c_int32_p]),
         "fdp_vec_dot": (i32, [vp, vp, i64, vp, vp]),
@@ -249,6 +252,7 @@ class KronOp:
         self.nin = [int(F.shape[1]) for F in terms[0]]
         self.nout = [int(F.shape[0]) for F in terms[0]]
         self._F = [_fortran(F) for T in terms for F in T]
+        self._coef = [float(x) for x in coef]
         nin = (ctypes.c_int32 * D)(*self.nin)
         nout = (ctypes.c_int32 * D)(*self.nout)
         Fp = (ctypes.c_void_p * len(self._F))(*[F.ctypes.data for F in self._F])
@@ -269,6 +273,29 @@ class KronOp:
         _check(lib.kron_op_apply(self.h, _dev(x, "x"), xbs, _dev(y, "y"), ybs, alpha, beta, batch,
                                  _dev(workspace, "workspace"), _stream(stream)))
         return y
+
+    @staticmethod
+    def _handles(ops):
+        return (ctypes.c_void_p * len(ops))(*[op.h.value for op in ops])
+
+    @staticmethod
+    def group_workspace_bytes(ops) -> int:
+        return int(lib.kron_ops_workspace_bytes(len(ops), KronOp._handles(ops)))
+
+    @staticmethod
+    def apply_group(ops, xs, ys, alphas, beta=0.0, workspace=None, stream=None):
+        """kron_ops_apply: for every distinct output Y among ys, Y = beta Y + sum alpha_i ops_i xs_i
+        (batch 1), all terms as one grouped launch per mode plus one summation per output."""
+        import torch
+        n = len(ops)
+        if workspace is None:
+            workspace = torch.empty(max(1, KronOp.group_workspace_bytes(ops) // 8),
+                                    dtype=torch.float64, device=xs[0].device)
+        X = (ctypes.c_void_p * n)(*[_dev(x, "x") for x in xs])
+        Y = (ctypes.c_void_p * n)(*[_dev(y, "y") for y in ys])
+        A = (ctypes.c_double * n)(*[float(a) for a in alphas])
+        _check(lib.kron_ops_apply(n, KronOp._handles(ops), X, Y, A, beta, _dev(workspace, "workspace"),
+                                  _stream(stream)))
 
     def close(self):
         if getattr(self, "h", None):

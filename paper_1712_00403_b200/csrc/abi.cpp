@@ -1700,3 +1700,107 @@ extern "C" fdp_status kron_op_destroy(fdp_kron h) {
   free_kron(h);
   return FDP_OK;
 }
+
+static long long kron_prod(const int* v, int D) {
+  long long p = 1;
+  for (int d = 0; d < D; ++d) p *= v[d];
+  return p;
+}
+
+extern "C" size_t kron_ops_workspace_bytes(int nops, const fdp_kron* ops) {
+  if (nops < 1 || !ops) return 0;
+  long long tot = 0;
+  for (int i = 0; i < nops; ++i) {
+    if (!ops[i]) return 0;
+    tot += (long long)ops[i]->nterms * (2 * kron_max_inter(ops[i]) + kron_prod(ops[i]->nout, ops[i]->D));
+  }
+  return (size_t)tot * sizeof(double);
+}
+
+extern "C" fdp_status kron_ops_apply(int nops, const fdp_kron* ops, const double* const* x,
+                                     double* const* y, const double* alpha, double beta,
+                                     void* workspace, void* stream) {
+  if (nops < 1 || !ops || !x || !y || !alpha) return fail(FDP_ERR_INVALID_ARG, "kron_ops_apply: bad arguments");
+  const int D = ops[0] ? ops[0]->D : 0;
+  for (int i = 0; i < nops; ++i) {
+    if (!ops[i] || ops[i]->D != D) return fail(FDP_ERR_INVALID_ARG, "kron_ops_apply: NULL or mixed-D operator");
+    if (!is_device_ptr(x[i]) || !is_device_ptr(y[i])) return fail(FDP_ERR_INVALID_ARG, "kron_ops_apply: device pointers required");
+  }
+  if (!is_device_ptr(workspace)) return fail(FDP_ERR_INVALID_ARG, "kron_ops_apply: workspace must be device memory");
+  DeviceGuard dg(ops[0]->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // per term: T1, T2 (intermediates) and its private partial
+  struct Term { const fdp_kron_s* op; int t; const double* x; double* T[2]; double* part; double scale; double* y; };
+  std::vector<Term> terms;
+  double* ws = static_cast<double*>(workspace);
+  for (int i = 0; i < nops; ++i) {
+    const fdp_kron_s* op = ops[i];
+    const long long inter = kron_max_inter(op), outn = kron_prod(op->nout, D);
+    for (int t = 0; t < op->nterms; ++t) {
+      Term tm{op, t, x[i], {ws, ws + inter}, ws + 2 * inter, alpha[i] * op->coef[t], y[i]};
+      ws += 2 * inter + outn;
+      terms.push_back(tm);
+    }
+  }
+  // one grouped stage per mode: term t's mode-d contraction (independent problems)
+  for (int d = 0; d < D; ++d) {
+    std::vector<ModeProb> probs;
+    std::vector<TileCfg> cfgs;
+    for (const Term& tm : terms) {
+      const fdp_kron_s* op = tm.op;
+      const KronFactor& kf = op->f[tm.t * D + d];
+      long long P = 1, Q = 1;
+      for (int e = 0; e < d; ++e) P *= op->nout[e];
+      for (int e = d + 1; e < D; ++e) Q *= op->nin[e];
+      const bool last = d == D - 1;
+      ModeProb p{};
+      p.X = d == 0 ? tm.x : tm.T[(d - 1) % 2];
+      p.Y = last ? tm.part : tm.T[d % 2];
+      p.W = kf.W;
+      p.P = (int)P;
+      p.n = kf.nin;
+      p.nout = kf.nout;
+      p.Q = (int)Q;
+      p.N = P * kf.nout * Q;
+      p.xbs = p.ybs = 0;
+      p.batch = 1;
+      p.ldw = kf.cfg.ldw;
+      p.n1 = p.n1v = 1;
+      p.xld = kf.nin;
+      p.yld = kf.nout;
+      p.vx = p.vy = 0;
+      p.epi = last ? EPI_AXPBY : EPI_NONE;
+      p.alpha = tm.scale;
+      p.beta = 0.0;
+      const int BM = kK1Warps * 8 * kf.cfg.MT;
+      p.tiles_m = (int)((P * Q + BM - 1) / BM);
+      p.tiles_n = kf.cfg.tiles_n;
+      p.fd_work = 0;
+      probs.push_back(p);
+      cfgs.push_back(kf.cfg);
+    }
+    FDP_CUDA(launch_stage(probs, cfgs, d == 0, s, nullptr, nullptr), "kron_ops_apply: stage");
+  }
+  // combine partials per distinct output
+  std::vector<double*> outs;
+  for (const Term& tm : terms)
+    if (std::find(outs.begin(), outs.end(), tm.y) == outs.end()) outs.push_back(tm.y);
+  for (double* yo : outs) {
+    long long n = 0;
+    std::vector<const double*> parts;
+    for (const Term& tm : terms)
+      if (tm.y == yo) {
+        parts.push_back(tm.part);
+        n = kron_prod(tm.op->nout, D);
+      }
+    double b = beta;
+    for (size_t c = 0; c < parts.size(); c += kMaxParts) {
+      PartSum ps{};
+      ps.nparts = (int)std::min<size_t>(kMaxParts, parts.size() - c);
+      for (int j = 0; j < ps.nparts; ++j) ps.parts[j] = parts[c + j];
+      FDP_CUDA(launch_partsum(ps, yo, b, n, s), "kron_ops_apply: combine");
+      b = 1.0;
+    }
+  }
+  return FDP_OK;
+}

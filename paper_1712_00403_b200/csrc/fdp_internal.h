@@ -69,7 +69,7 @@ __device__ __forceinline__ double fdp_div(double a, double b) {
 }
 #endif
 
-constexpr int kMaxGroup = 4;
+constexpr int kMaxGroup = 32;  // problems per grouped launch (kernel parameters < 32 KB)
 struct ModeGroup {
   ModeProb prob[kMaxGroup];
   int count;
@@ -128,6 +128,14 @@ cudaError_t launch_scale(const double* x, double* y, const double* s, long long 
                          long long xs, long long ys, cudaStream_t st);
 // Set the dynamic shared-memory attribute of the kernels a tile config uses (call outside capture).
 cudaError_t prepare_mode_kernels(const TileCfg& cfg);
+
+// y = beta * y + sum_i parts[i] (n elements); up to kMaxParts inputs per launch.
+constexpr int kMaxParts = 48;
+struct PartSum {
+  const double* parts[kMaxParts];
+  int nparts;
+};
+cudaError_t launch_partsum(const PartSum& ps, double* y, double beta, long long n, cudaStream_t s);
 
 // Vector kernels (vec.cu)
 cudaError_t launch_dot(const double* x, const double* y, long long n, double* result,

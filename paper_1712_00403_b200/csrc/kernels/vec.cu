@@ -55,7 +55,24 @@ __global__ void lincomb_kernel(double a, const double* x, double b, const double
   }
 }
 
+__global__ void partsum_kernel(const __grid_constant__ PartSum ps, double* __restrict__ y,
+                               double beta, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double v = beta != 0.0 ? beta * y[i] : 0.0;
+    for (int j = 0; j < ps.nparts; ++j) v += ps.parts[j][i];
+    y[i] = v;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_partsum(const PartSum& ps, double* y, double beta, long long n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 8);
+  partsum_kernel<<<blocks, 256, 0, s>>>(ps, y, beta, n);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_dot(const double* x, const double* y, long long n, double* result,
                        double* scratch, cudaStream_t s) {

@@ -92,6 +92,20 @@ class StokesOperator:
         ops = self.diag + list(self.off.values()) + self.B + self.BT
         self.ws = torch.empty(max(op.workspace_bytes(1) for op in ops) // 8 + 1, dtype=torch.float64,
                               device=f"cuda:{device}")
+        # grouped apply: every block of calA as one (ops, x-block, y-block) list -> kron_ops_apply
+        self._group = []
+        for r in range(D):
+            self._group.append((self.diag[r], r, r))
+            for s in range(D):
+                if s != r:
+                    self._group.append((self.off[(r, s)], s, r))
+            self._group.append((self.BT[r], D, r))
+        for r in range(D):
+            self._group.append((self.B[r], r, D))
+        gops = [g[0] for g in self._group]
+        self.gws = torch.empty(KronOp.group_workspace_bytes(gops) // 8 + 1, dtype=torch.float64,
+                               device=f"cuda:{device}")
+        self.grouped = True
 
     def apply(self, x, y):
         """y = calA x. The ~20 KronOp launches are captured once per (x, y) pair into a CUDA graph
@@ -115,6 +129,11 @@ class StokesOperator:
         o = self.off_idx
         D = self.D
         blk = lambda v, k: v[o[k]:o[k + 1]]
+        if self.grouped:
+            KronOp.apply_group([g[0] for g in self._group], [blk(x, g[1]) for g in self._group],
+                               [blk(y, g[2]) for g in self._group], [1.0] * len(self._group), 0.0,
+                               self.gws)
+            return y
         for r in range(D):
             yr = blk(y, r)
             self.diag[r].apply(blk(x, r), yr, 1.0, 0.0, self.ws)

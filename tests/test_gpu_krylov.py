@@ -44,6 +44,36 @@ def test_kron_op_rectangular_terms(nin, nout):
         assert rel(Y[b].cpu().numpy(), ref) < 1e-13
 
 
+def test_kron_ops_grouped_matches_single():
+    """kron_ops_apply: shared outputs accumulate, distinct outputs stay separate, beta applies once."""
+    rng = np.random.default_rng(11)
+    shapes = [((9, 70, 5), (9, 70, 5)), ((9, 70, 5), (8, 66, 5)), ((12, 7, 33), (9, 70, 5)),
+              ((9, 70, 5), (3, 4, 5))]
+    ops, xs, ys = [], [], []
+    for nin, nout in shapes:
+        nt = int(rng.integers(1, 4))
+        terms = [[rng.standard_normal((o, i)) for i, o in zip(nin, nout)] for _ in range(nt)]
+        ops.append((fdp.KronOp(terms, list(rng.standard_normal(nt))), terms))
+        xs.append(rng.standard_normal(int(np.prod(nin))))
+    y0 = rng.standard_normal(9 * 70 * 5), rng.standard_normal(8 * 66 * 5), rng.standard_normal(60)
+    out_of = [0, 1, 0, 2]
+    alphas = [0.5, -1.0, 2.0, 1.5]
+    Y = [dev(v) for v in y0]
+    fdp.KronOp.apply_group([o for o, _ in ops], [dev(x) for x in xs], [Y[k] for k in out_of], alphas,
+                           beta=-0.75)
+    for k in range(3):
+        ref = -0.75 * y0[k]
+        for i, (op, terms) in enumerate(ops):
+            if out_of[i] == k:
+                ref = ref + alphas[i] * sum(c * okron.kron_matvec(list(reversed(T)), xs[i])
+                                            for c, T in zip(np.asarray(_coef(op)), terms))
+        assert rel(Y[k].cpu().numpy(), ref) < 1e-13, k
+
+
+def _coef(op):
+    return op._coef
+
+
 @pytest.mark.parametrize("cid", [1, 2, 3])
 def test_stokes_operator_matches_oracle(cid):
     w = synth.CONFIGS[cid]
@@ -54,11 +84,13 @@ def test_stokes_operator_matches_oracle(cid):
     assert gop.n == op.n
     x = np.random.default_rng(cid).standard_normal(op.n)
     y = torch.empty(op.n, dtype=torch.float64, device="cuda")
-    gop.apply(dev(x), y)
     ref = op.matvec(x)
-    for k in range(len(op.sizes)):
-        a, b = op.off_idx[k], op.off_idx[k + 1]
-        assert rel(y[a:b].cpu().numpy(), ref[a:b]) < 1e-12, k
+    for grouped in (True, False):
+        gop.grouped = grouped
+        gop._apply_direct(dev(x), y)
+        for k in range(len(op.sizes)):
+            a, b = op.off_idx[k], op.off_idx[k + 1]
+            assert rel(y[a:b].cpu().numpy(), ref[a:b]) < 1e-12, (grouped, k)
 
 
 def test_vector_kernels():
