@@ -123,6 +123,17 @@ class StokesCube:
     def _blk(self, x, k):
         return x[self.off_idx[k]:self.off_idx[k + 1]]
 
+    def B_apply(self, u):
+        """B u = sum_r B_r u_r (velocity [u_1 | .. | u_D] -> pressure), B_r = -(x) D^QV / M^QV."""
+        yp = np.zeros(self.sizes[self.D])
+        for r in range(self.D):
+            yp -= _kron_apply(self.B[r], self._blk(u, r))
+        return yp
+
+    def BT_apply(self, pr):
+        """B^T p = [B_1^T p | .. | B_D^T p] (pressure -> velocity)."""
+        return np.concatenate([-_kron_apply([f.T.tocsr() for f in self.B[r]], pr) for r in range(self.D)])
+
     def matvec(self, x):
         D = self.D
         y = np.zeros_like(x)
