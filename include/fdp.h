@@ -205,6 +205,32 @@ size_t kron_ops_workspace_bytes(int nops, const fdp_kron* ops);
 fdp_status kron_ops_apply(int nops, const fdp_kron* ops, const double* const* x, double* const* y,
                           const double* alpha, double beta, void* workspace, void* stream);
 
+/* ---- Block-triangular and constrained preconditioners (§4; NEXT-2) ----
+ * P_T = [[P_V, B^T], [0, -P_Q]] and P_C = [[P_V, B^T], [B, B P_V^{-1} B^T - P_Q]]
+ * (P:612-618), applied as s = P^{-1} r with r, s device [u_1 | .. | u_D | p] (batch 1, must not
+ * alias). P_V, P_Q (and their P^G diagonal scalings) are the blocks of `P`
+ * (block_precond_setup); B[k] (pressure x velocity-k, i.e. nin = velocity-k extents, nout =
+ * pressure extents) and BT[k] (its transpose) are kron_op handles of the system's divergence
+ * blocks B_k, sign included. P_T: back substitution s_p = -P_Q^{-1} r_p, s_u = P_V^{-1}(r_u - B^T s_p).
+ * P_C: the paper's factorization applied right to left, two P_V^{-1} per apply.
+ * The pressure block uses the banded per-mode solves. Asynchronous on `stream`, no allocation,
+ * graph-capturable. workspace >= block_tri_workspace_bytes(...) (0 on invalid arguments). */
+enum { FDP_PREC_TRIANGULAR = 1, FDP_PREC_CONSTRAINED = 2 };
+size_t block_tri_workspace_bytes(fdp_block P, int variant, const fdp_kron* B, const fdp_kron* BT);
+fdp_status block_tri_apply(fdp_block P, int variant, const fdp_kron* B, const fdp_kron* BT,
+                           const double* r, double* s, void* workspace, void* stream);
+
+/* ---- Arnoldi helpers for GMRES (Saad & Schultz) ----
+ * V: m device vectors of length n with stride ldv >= n (V_j = V + j*ldv).
+ * fdp_vec_multidot: h[j] = V_j . w for j < m into device h; deterministic (fixed grid, fixed
+ * reduction order); workspace >= fdp_vec_multidot_workspace_bytes(m).
+ * fdp_vec_gemv: w = beta*w + alpha * sum_j h[j] V_j, h device (m <= 6144). */
+size_t fdp_vec_multidot_workspace_bytes(int m);
+fdp_status fdp_vec_multidot(const double* V, int64_t ldv, int m, const double* w, int64_t n,
+                            double* h, void* workspace, void* stream);
+fdp_status fdp_vec_gemv(const double* V, int64_t ldv, int m, const double* h, double alpha,
+                        double* w, double beta, int64_t n, void* stream);
+
 /* Mixed univariate matrix out[i, j] = int wt(x) b_test_i^(dtest)(x) b_trial_j^(dtrial)(x) dx on
  * [0,1] over n_el uniform elements with q Gauss points per element (q <= 0: deg_test+deg_trial+1
  * ... exact for unweighted products). wq: weights at the points iga_quadrature returns (n_el*q)

@@ -72,6 +72,11 @@ def _load():
         "kron_op_apply": (i32, [vp, vp, i64, vp, i64, ctypes.c_double, ctypes.c_double, i64, vp, vp]),
         "kron_op_destroy": (i32, [vp]),
         "kron_ops_workspace_bytes": (sz, [i32, ctypes.POINTER(vp)]),
+        "block_tri_workspace_bytes": (sz, [vp, i32, ctypes.POINTER(vp), ctypes.POINTER(vp)]),
+        "block_tri_apply": (i32, [vp, i32, ctypes.POINTER(vp), ctypes.POINTER(vp), vp, vp, vp, vp]),
+        "fdp_vec_multidot_workspace_bytes": (sz, [i32]),
+        "fdp_vec_multidot": (i32, [vp, i64, i32, vp, i64, vp, vp, vp]),
+        "fdp_vec_gemv": (i32, [vp, i64, i32, vp, ctypes.c_double, vp, ctypes.c_double, i64, vp]),
         "kron_ops_apply": (i32, [i32, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp),
                                  ctypes.POINTER(ctypes.c_double), ctypes.c_double, vp, vp]),
         "iga_quadrature": (i32, [i32, i32, vp, vp]),
@@ -321,6 +326,24 @@ def vec_lincomb(a, x, b, y, c, z, out, stream=None):
     return out
 
 
+def vec_multidot(V, m, w, h, workspace=None, stream=None):
+    """h[:m] = V[:m] @ w (fdp_vec_multidot; V a 2-D cuda tensor of row vectors)."""
+    import torch
+    if workspace is None:
+        workspace = torch.empty(max(1, int(lib.fdp_vec_multidot_workspace_bytes(max(m, 1))) // 8),
+                                dtype=torch.float64, device=w.device)
+    _check(lib.fdp_vec_multidot(_dev(V, "V"), V.stride(0), m, _dev(w, "w"), w.numel(), _dev(h, "h"),
+                                _dev(workspace, "workspace"), _stream(stream)))
+    return h
+
+
+def vec_gemv(V, m, h, alpha, w, beta, stream=None):
+    """w = beta w + alpha V[:m]^T h[:m] (fdp_vec_gemv)."""
+    _check(lib.fdp_vec_gemv(_dev(V, "V"), V.stride(0), m, _dev(h, "h"), alpha, _dev(w, "w"), beta,
+                            w.numel(), _stream(stream)))
+    return w
+
+
 def slab_range(n: int, nranks: int, rank: int):
     """(lo, len) of rank's share of an axis of length n (fdp_slab_range)."""
     lo, ln = ctypes.c_int64(), ctypes.c_int64()
@@ -440,6 +463,11 @@ class BlockPrecond:
                                        _stream(stream)))
         return s
 
+    def tri(self, variant: str, B, BT):
+        """The block-triangular ("T") or constrained ("C") preconditioner built on this block's
+        P_V, P_Q and the system's divergence blocks B[k], BT[k] (KronOp, sign included)."""
+        return BlockTri(self, variant, B, BT)
+
     def apply_host(self, r_host: np.ndarray, s_host: np.ndarray, batch: int = 1, stream=None):
         """End-to-end call with host buffers (H2D, apply, D2H, stream sync inside libfdp)."""
         if r_host.dtype != np.float64 or s_host.dtype != np.float64:
@@ -545,3 +573,34 @@ def build_block(d: Discretization, device: int = 0, dscale_vel=None, dscale_pres
     fds = [FD(d.Ks[k], d.Ms[k], d.coef[k], device=device) for k in range(d.D)]
     mass = KronMass(d.Mq, device=device)
     return BlockPrecond(fds, mass, dscale_vel, dscale_pres)
+
+
+FDP_PREC_TRIANGULAR = 1
+FDP_PREC_CONSTRAINED = 2
+
+
+class BlockTri:
+    """block_tri_apply: s = P_T^{-1} r or P_C^{-1} r, batch 1."""
+
+    def __init__(self, block: "BlockPrecond", variant: str, B, BT):
+        self.block = block
+        self.variant = {"T": FDP_PREC_TRIANGULAR, "C": FDP_PREC_CONSTRAINED}[variant]
+        self.B, self.BT = list(B), list(BT)
+        self._hB = KronOp._handles(self.B)
+        self._hBT = KronOp._handles(self.BT)
+        self.size = block.size
+        nb = int(lib.block_tri_workspace_bytes(block.h, self.variant, self._hB, self._hBT))
+        if nb == 0:
+            raise FdpError(1, "block_tri_workspace_bytes: " + lib.fdp_last_error().decode())
+        self._ws_bytes = nb
+
+    def workspace(self):
+        import torch
+        return torch.empty(self._ws_bytes // 8 + 1, dtype=torch.float64,
+                           device=f"cuda:{self.block.device}")
+
+    def apply(self, r, s, workspace, stream=None):
+        _check(lib.block_tri_apply(self.block.h, self.variant, self._hB, self._hBT,
+                                   _dev(r, "r", self.size), _dev(s, "s", self.size),
+                                   _dev(workspace, "workspace", self._ws_bytes // 8), _stream(stream)))
+        return s

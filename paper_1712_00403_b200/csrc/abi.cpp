@@ -1707,42 +1707,45 @@ static long long kron_prod(const int* v, int D) {
   return p;
 }
 
-extern "C" size_t kron_ops_workspace_bytes(int nops, const fdp_kron* ops) {
-  if (nops < 1 || !ops) return 0;
+// One Kronecker operator application y (+)= alpha op x, batch 1 (grouped multi-operator path).
+struct KronTask {
+  const fdp_kron_s* op;
+  const double* x;
+  double* y;
+  double alpha;
+};
+// An extra vector added (times coef) to output y in the combine pass.
+struct ExtraPart {
+  double* y;
+  const double* part;
+  double coef;
+};
+
+static long long kron_tasks_ws_elems(const std::vector<KronTask>& tasks) {
   long long tot = 0;
-  for (int i = 0; i < nops; ++i) {
-    if (!ops[i]) return 0;
-    tot += (long long)ops[i]->nterms * (2 * kron_max_inter(ops[i]) + kron_prod(ops[i]->nout, ops[i]->D));
-  }
-  return (size_t)tot * sizeof(double);
+  for (const KronTask& t : tasks)
+    tot += (long long)t.op->nterms * (2 * kron_max_inter(t.op) + kron_prod(t.op->nout, t.op->D));
+  return tot;
 }
 
-extern "C" fdp_status kron_ops_apply(int nops, const fdp_kron* ops, const double* const* x,
-                                     double* const* y, const double* alpha, double beta,
-                                     void* workspace, void* stream) {
-  if (nops < 1 || !ops || !x || !y || !alpha) return fail(FDP_ERR_INVALID_ARG, "kron_ops_apply: bad arguments");
-  const int D = ops[0] ? ops[0]->D : 0;
-  for (int i = 0; i < nops; ++i) {
-    if (!ops[i] || ops[i]->D != D) return fail(FDP_ERR_INVALID_ARG, "kron_ops_apply: NULL or mixed-D operator");
-    if (!is_device_ptr(x[i]) || !is_device_ptr(y[i])) return fail(FDP_ERR_INVALID_ARG, "kron_ops_apply: device pointers required");
-  }
-  if (!is_device_ptr(workspace)) return fail(FDP_ERR_INVALID_ARG, "kron_ops_apply: workspace must be device memory");
-  DeviceGuard dg(ops[0]->device);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // per term: T1, T2 (intermediates) and its private partial
+// For every distinct output Y: Y = beta Y + sum_{tasks into Y} alpha op x + sum_{extras into Y}
+// coef part. All terms of all tasks run as one grouped launch per mode (independent problems,
+// each writing a private partial), then one summation pass per output.
+static cudaError_t enqueue_kron_tasks(const std::vector<KronTask>& tasks, double beta,
+                                      const std::vector<ExtraPart>& extra, double* ws,
+                                      cudaStream_t s) {
+  if (tasks.empty()) return cudaSuccess;
+  const int D = tasks[0].op->D;
   struct Term { const fdp_kron_s* op; int t; const double* x; double* T[2]; double* part; double scale; double* y; };
   std::vector<Term> terms;
-  double* ws = static_cast<double*>(workspace);
-  for (int i = 0; i < nops; ++i) {
-    const fdp_kron_s* op = ops[i];
+  for (const KronTask& tk : tasks) {
+    const fdp_kron_s* op = tk.op;
     const long long inter = kron_max_inter(op), outn = kron_prod(op->nout, D);
     for (int t = 0; t < op->nterms; ++t) {
-      Term tm{op, t, x[i], {ws, ws + inter}, ws + 2 * inter, alpha[i] * op->coef[t], y[i]};
+      terms.push_back({op, t, tk.x, {ws, ws + inter}, ws + 2 * inter, tk.alpha * op->coef[t], tk.y});
       ws += 2 * inter + outn;
-      terms.push_back(tm);
     }
   }
-  // one grouped stage per mode: term t's mode-d contraction (independent problems)
   for (int d = 0; d < D; ++d) {
     std::vector<ModeProb> probs;
     std::vector<TileCfg> cfgs;
@@ -1779,28 +1782,225 @@ extern "C" fdp_status kron_ops_apply(int nops, const fdp_kron* ops, const double
       probs.push_back(p);
       cfgs.push_back(kf.cfg);
     }
-    FDP_CUDA(launch_stage(probs, cfgs, d == 0, s, nullptr, nullptr), "kron_ops_apply: stage");
+    cudaError_t e = launch_stage(probs, cfgs, d == 0, s, nullptr, nullptr);
+    if (e != cudaSuccess) return e;
   }
-  // combine partials per distinct output
-  std::vector<double*> outs;
-  for (const Term& tm : terms)
-    if (std::find(outs.begin(), outs.end(), tm.y) == outs.end()) outs.push_back(tm.y);
-  for (double* yo : outs) {
-    long long n = 0;
-    std::vector<const double*> parts;
+  std::vector<std::pair<double*, long long>> outs;
+  auto add_out = [&](double* y, long long n) {
+    for (auto& o : outs)
+      if (o.first == y) return;
+    outs.push_back({y, n});
+  };
+  for (const Term& tm : terms) add_out(tm.y, kron_prod(tm.op->nout, D));
+  for (const ExtraPart& ex : extra) add_out(ex.y, -1);
+  for (auto& o : outs) {
+    std::vector<std::pair<const double*, double>> parts;
     for (const Term& tm : terms)
-      if (tm.y == yo) {
-        parts.push_back(tm.part);
-        n = kron_prod(tm.op->nout, D);
-      }
+      if (tm.y == o.first) parts.push_back({tm.part, 1.0});
+    for (const ExtraPart& ex : extra)
+      if (ex.y == o.first) parts.push_back({ex.part, ex.coef});
     double b = beta;
     for (size_t c = 0; c < parts.size(); c += kMaxParts) {
       PartSum ps{};
       ps.nparts = (int)std::min<size_t>(kMaxParts, parts.size() - c);
-      for (int j = 0; j < ps.nparts; ++j) ps.parts[j] = parts[c + j];
-      FDP_CUDA(launch_partsum(ps, yo, b, n, s), "kron_ops_apply: combine");
+      for (int j = 0; j < ps.nparts; ++j) {
+        ps.parts[j] = parts[c + j].first;
+        ps.coef[j] = parts[c + j].second;
+      }
+      cudaError_t e = launch_partsum(ps, o.first, b, o.second, s);
+      if (e != cudaSuccess) return e;
       b = 1.0;
     }
   }
+  return cudaSuccess;
+}
+
+extern "C" size_t kron_ops_workspace_bytes(int nops, const fdp_kron* ops) {
+  if (nops < 1 || !ops) return 0;
+  std::vector<KronTask> tasks;
+  for (int i = 0; i < nops; ++i) {
+    if (!ops[i]) return 0;
+    tasks.push_back({ops[i], nullptr, nullptr, 1.0});
+  }
+  return (size_t)kron_tasks_ws_elems(tasks) * sizeof(double);
+}
+
+extern "C" fdp_status kron_ops_apply(int nops, const fdp_kron* ops, const double* const* x,
+                                     double* const* y, const double* alpha, double beta,
+                                     void* workspace, void* stream) {
+  if (nops < 1 || !ops || !x || !y || !alpha) return fail(FDP_ERR_INVALID_ARG, "kron_ops_apply: bad arguments");
+  const int D = ops[0] ? ops[0]->D : 0;
+  std::vector<KronTask> tasks;
+  for (int i = 0; i < nops; ++i) {
+    if (!ops[i] || ops[i]->D != D) return fail(FDP_ERR_INVALID_ARG, "kron_ops_apply: NULL or mixed-D operator");
+    if (!is_device_ptr(x[i]) || !is_device_ptr(y[i])) return fail(FDP_ERR_INVALID_ARG, "kron_ops_apply: device pointers required");
+    tasks.push_back({ops[i], x[i], y[i], alpha[i]});
+  }
+  if (!is_device_ptr(workspace)) return fail(FDP_ERR_INVALID_ARG, "kron_ops_apply: workspace must be device memory");
+  DeviceGuard dg(ops[0]->device);
+  FDP_CUDA(enqueue_kron_tasks(tasks, beta, {}, static_cast<double*>(workspace), static_cast<cudaStream_t>(stream)),
+           "kron_ops_apply");
+  return FDP_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+// block-triangular P_T and constrained P_C (§4)
+// ------------------------------------------------------------------------------------------------
+static long long vel_ws_elems(const fdp_block_s* h) {
+  long long v = 0;
+  for (const fdp_fd_s* f : h->vel) v += 2 * Npad(f);
+  return v;
+}
+
+// s_u = P_V^{-1} r_u on the contiguous velocity part [u_1 | .. | u_D] (batch 1); s_u may not alias r_u
+static cudaError_t enqueue_vel(const fdp_block_s* h, const double* ru, double* su, double* T,
+                               cudaStream_t st) {
+  const int D = h->D;
+  std::vector<const double*> in(D), dsc(D);
+  std::vector<double*> out(D), Tk(D);
+  long long toff = 0;
+  if (h->dv) {
+    cudaError_t e = launch_scale(ru, su, h->dv, h->nvel, 1, h->nvel, h->nvel, st);
+    if (e != cudaSuccess) return e;
+  }
+  for (int k = 0; k < D; ++k) {
+    in[k] = (h->dv ? su : ru) + h->off[k];
+    out[k] = su + h->off[k];
+    Tk[k] = T + toff;
+    toff += 2 * Npad(h->vel[k]);
+    dsc[k] = h->dv ? h->dv + h->off[k] : nullptr;
+  }
+  return enqueue_fd(h->vel, in, h->nvel, out, h->nvel, Tk, dsc, 1, st, nullptr);
+}
+
+static fdp_status check_tri_args(fdp_block h, int variant, const fdp_kron* B, const fdp_kron* BT,
+                                 const char* who) {
+  if (!h || !B || !BT) return fail(FDP_ERR_INVALID_ARG, std::string(who) + ": NULL argument");
+  if (variant != FDP_PREC_TRIANGULAR && variant != FDP_PREC_CONSTRAINED)
+    return fail(FDP_ERR_INVALID_ARG, std::string(who) + ": unknown variant");
+  const int D = h->D;
+  for (int k = 0; k < D; ++k) {
+    if (!B[k] || !BT[k] || B[k]->D != D || BT[k]->D != D)
+      return fail(FDP_ERR_INVALID_ARG, std::string(who) + ": NULL or mismatched B / B^T handle");
+    for (int d = 0; d < D; ++d)
+      if (B[k]->nin[d] != h->vel[k]->n[d] || B[k]->nout[d] != h->pres->n[d] ||
+          BT[k]->nin[d] != h->pres->n[d] || BT[k]->nout[d] != h->vel[k]->n[d])
+        return fail(FDP_ERR_SHAPE, std::string(who) + ": B_k / B_k^T extents do not match the blocks");
+  }
+  return FDP_OK;
+}
+
+static long long tri_ws_elems(const fdp_block_s* h, int variant, const fdp_kron* B, const fdp_kron* BT) {
+  std::vector<KronTask> tb, tbt;
+  for (int k = 0; k < h->D; ++k) {
+    tb.push_back({B[k], nullptr, nullptr, 1.0});
+    tbt.push_back({BT[k], nullptr, nullptr, 1.0});
+  }
+  const long long kr = std::max(kron_tasks_ws_elems(tbt), variant == FDP_PREC_CONSTRAINED ? kron_tasks_ws_elems(tb) : 0LL);
+  return vel_ws_elems(h) + kr + 2 * h->nvel + h->pres->N;
+}
+
+extern "C" size_t block_tri_workspace_bytes(fdp_block h, int variant, const fdp_kron* B,
+                                            const fdp_kron* BT) {
+  if (check_tri_args(h, variant, B, BT, "block_tri_workspace_bytes")) return 0;
+  return (size_t)tri_ws_elems(h, variant, B, BT) * sizeof(double);
+}
+
+extern "C" fdp_status block_tri_apply(fdp_block h, int variant, const fdp_kron* B, const fdp_kron* BT,
+                                      const double* r, double* s, void* workspace, void* stream) {
+  fdp_status cs = check_tri_args(h, variant, B, BT, "block_tri_apply");
+  if (cs) return cs;
+  if (!is_device_ptr(r) || !is_device_ptr(s) || !is_device_ptr(workspace))
+    return fail(FDP_ERR_INVALID_ARG, "block_tri_apply: r, s and workspace must be device memory");
+  if (r == s) return fail(FDP_ERR_INVALID_ARG, "block_tri_apply: r and s must not alias");
+  DeviceGuard dg(h->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int D = h->D;
+  const long long nv = h->nvel;
+  double* T = static_cast<double*>(workspace);        // velocity FD intermediates
+  double* K = T + vel_ws_elems(h);                    // Kronecker partials
+  std::vector<KronTask> tb, tbt;
+  for (int k = 0; k < D; ++k) {
+    tb.push_back({B[k], nullptr, nullptr, 1.0});
+    tbt.push_back({BT[k], nullptr, nullptr, 1.0});
+  }
+  const long long kr = std::max(kron_tasks_ws_elems(tbt), variant == FDP_PREC_CONSTRAINED ? kron_tasks_ws_elems(tb) : 0LL);
+  double* tu = K + kr;                                // velocity temporaries
+  double* zu = tu + nv;
+  double* tp = zu + nv;                               // pressure temporary
+  const double* ru = r;
+  const double* rp = r + nv;
+  double* su = s;
+  double* sp = s + nv;
+  auto negate = [&](const double* a, double* y, long long n) {
+    PartSum ps{};
+    ps.nparts = 1;
+    ps.parts[0] = a;
+    ps.coef[0] = -1.0;
+    return launch_partsum(ps, y, 0.0, n, st);
+  };
+  if (variant == FDP_PREC_TRIANGULAR) {
+    // [[P_V, B^T], [0, -P_Q]] s = r: t_p = P_Q^{-1} r_p, s_p = -t_p, s_u = P_V^{-1}(r_u + B^T t_p)
+    FDP_CUDA(enqueue_mass(h->pres, FDP_MASS_INVERSE, rp, tp, h->pres->N, h->dq, 1, st, nullptr), "block_tri_apply: P_Q");
+    for (int k = 0; k < D; ++k) {
+      tbt[k].x = tp;
+      tbt[k].y = tu + h->off[k];
+    }
+    std::vector<ExtraPart> ex;
+    for (int k = 0; k < D; ++k) ex.push_back({tu + h->off[k], ru + h->off[k], 1.0});
+    FDP_CUDA(enqueue_kron_tasks(tbt, 0.0, ex, K, st), "block_tri_apply: B^T");
+    FDP_CUDA(enqueue_vel(h, tu, su, T, st), "block_tri_apply: P_V");
+    FDP_CUDA(negate(tp, sp, h->pres->N), "block_tri_apply: negate");
+    return FDP_OK;
+  }
+  // P_C^{-1} = [[I, -P_V^{-1}B^T], [0, I]] diag(I, -P_Q^{-1}) [[I, 0], [-B, I]] diag(P_V^{-1}, I)
+  FDP_CUDA(enqueue_vel(h, ru, su, T, st), "block_tri_apply: P_V");                 // w_u
+  for (int k = 0; k < D; ++k) {
+    tb[k].x = su + h->off[k];
+    tb[k].y = zu;  // g_p = r_p - B w_u (zu reused as the pressure temporary g_p)
+    tb[k].alpha = -1.0;
+  }
+  FDP_CUDA(enqueue_kron_tasks(tb, 0.0, {{zu, rp, 1.0}}, K, st), "block_tri_apply: B");
+  FDP_CUDA(enqueue_mass(h->pres, FDP_MASS_INVERSE, zu, tp, h->pres->N, h->dq, 1, st, nullptr), "block_tri_apply: P_Q");
+  FDP_CUDA(negate(tp, sp, h->pres->N), "block_tri_apply: negate");                 // s_p = -t_p
+  for (int k = 0; k < D; ++k) {
+    tbt[k].x = tp;
+    tbt[k].y = tu + h->off[k];
+  }
+  FDP_CUDA(enqueue_kron_tasks(tbt, 0.0, {}, K, st), "block_tri_apply: B^T");        // B^T t_p
+  FDP_CUDA(enqueue_vel(h, tu, zu, T, st), "block_tri_apply: P_V");                 // P_V^{-1} B^T t_p
+  PartSum ps{};
+  ps.nparts = 1;
+  ps.parts[0] = zu;
+  ps.coef[0] = 1.0;
+  FDP_CUDA(launch_partsum(ps, su, 1.0, nv, st), "block_tri_apply: update");        // s_u = w_u - P_V^{-1} B^T s_p
+  return FDP_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+// Arnoldi helpers (GMRES orthogonalization, NEXT-2)
+// ------------------------------------------------------------------------------------------------
+extern "C" size_t fdp_vec_multidot_workspace_bytes(int m) {
+  return m > 0 ? multidot_scratch_elems(m) * sizeof(double) : 0;
+}
+
+extern "C" fdp_status fdp_vec_multidot(const double* V, int64_t ldv, int m, const double* w,
+                                       int64_t n, double* h, void* workspace, void* stream) {
+  if (m < 0 || n < 0 || (m > 0 && ldv < n)) return fail(FDP_ERR_SHAPE, "fdp_vec_multidot: bad extents");
+  if (m == 0) return FDP_OK;
+  if (!is_device_ptr(V) || !is_device_ptr(w) || !is_device_ptr(h) || !is_device_ptr(workspace))
+    return fail(FDP_ERR_INVALID_ARG, "fdp_vec_multidot: device pointers required");
+  FDP_CUDA(launch_multidot(V, ldv, m, w, n, h, static_cast<double*>(workspace), static_cast<cudaStream_t>(stream)),
+           "fdp_vec_multidot");
+  return FDP_OK;
+}
+
+extern "C" fdp_status fdp_vec_gemv(const double* V, int64_t ldv, int m, const double* h, double alpha,
+                                   double* w, double beta, int64_t n, void* stream) {
+  if (m < 0 || m > 6144 || n < 0 || (m > 0 && ldv < n)) return fail(FDP_ERR_SHAPE, "fdp_vec_gemv: bad extents (m <= 6144)");
+  if (n == 0) return FDP_OK;
+  if (!is_device_ptr(w) || (m > 0 && (!is_device_ptr(V) || !is_device_ptr(h))))
+    return fail(FDP_ERR_INVALID_ARG, "fdp_vec_gemv: device pointers required");
+  FDP_CUDA(launch_gemv(V, ldv, m, h, alpha, w, beta, n, static_cast<cudaStream_t>(stream)), "fdp_vec_gemv");
   return FDP_OK;
 }

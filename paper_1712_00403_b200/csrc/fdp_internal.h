@@ -129,12 +129,18 @@ cudaError_t launch_scale(const double* x, double* y, const double* s, long long 
 // Set the dynamic shared-memory attribute of the kernels a tile config uses (call outside capture).
 cudaError_t prepare_mode_kernels(const TileCfg& cfg);
 
-// y = beta * y + sum_i parts[i] (n elements); up to kMaxParts inputs per launch.
+// y = beta * y + sum_i coef[i] parts[i] (n elements); up to kMaxParts inputs per launch.
 constexpr int kMaxParts = 48;
 struct PartSum {
   const double* parts[kMaxParts];
+  double coef[kMaxParts];
   int nparts;
 };
+size_t multidot_scratch_elems(int m);
+cudaError_t launch_multidot(const double* V, long long ldv, int m, const double* w, long long n,
+                            double* h, double* scratch, cudaStream_t s);
+cudaError_t launch_gemv(const double* V, long long ldv, int m, const double* h, double alpha,
+                        double* w, double beta, long long n, cudaStream_t s);
 cudaError_t launch_partsum(const PartSum& ps, double* y, double beta, long long n, cudaStream_t s);
 
 // Vector kernels (vec.cu)

@@ -13,6 +13,12 @@ boundary so the Nitsche terms keep weight 1 (true for config 3's nu).
 MINRES is Paige & Saunders' recurrence (tolerance 1e-8, x0 = 0) with every
 vector operation in libfdp kernels (fdp_vec_dot / fdp_vec_lincomb); only the scalar recurrence
 runs on the host. Stopping rule: preconditioned residual phibar_k / phibar_0 <= tol (C-15).
+
+GMRES (NEXT-2, for the block-triangular P_T and constrained P_C) is full,
+left-preconditioned GMRES (G-1) with the Arnoldi basis on the device; the
+orthogonalization is classical Gram-Schmidt applied twice (two fdp_vec_multidot + fdp_vec_gemv
+launch pairs instead of j dependent dot/axpy pairs per step; G-2), the small Hessenberg
+least-squares problem by Givens rotations on the host.
 """
 from __future__ import annotations
 
@@ -21,7 +27,7 @@ import math
 import numpy as np
 
 from . import (FDP_IGA_INTERIOR, FDP_IGA_NITSCHE, KronOp, iga_mixed, iga_quadrature,
-               iga_univariate, vec_dot, vec_lincomb)
+               iga_univariate, vec_dot, vec_gemv, vec_lincomb, vec_multidot)
 
 
 def _spaces(D, disc, p):
@@ -215,3 +221,82 @@ def minres(apply_A, apply_P, b, tol: float = 1e-8, maxit: int = 20000):
         if phibar / beta1 <= tol:
             return x.clone(), itn, hist
     return x.clone(), maxit, hist
+
+
+_GM_BUFFERS = {}
+
+
+def gmres(apply_A, apply_P, b, tol: float = 1e-8, maxit: int = 500):
+    """GPU GMRES for A x = b with left preconditioner P: apply_A(x, y) / apply_P(r, z) write into
+    y / z. Stops when ||P^{-1}(b - A x_k)|| / ||P^{-1} b|| <= tol. Returns (x, iterations, history).
+
+    apply_A / apply_P are always called on the same two fixed buffers (so their CUDA graphs,
+    keyed by buffer addresses, are captured once)."""
+    import torch
+    n = b.numel()
+    dev = b.device
+    m = min(maxit, n)
+    key = (n, m, str(dev))
+    if key not in _GM_BUFFERS:
+        V = torch.empty((m + 1, n), dtype=torch.float64, device=dev)
+        vin = torch.empty(n, dtype=torch.float64, device=dev)
+        t = torch.empty(n, dtype=torch.float64, device=dev)
+        w = torch.empty(n, dtype=torch.float64, device=dev)
+        h = torch.empty(2 * (m + 1) + 1, dtype=torch.float64, device=dev)
+        from . import lib
+        ws = torch.empty(max(1, int(lib.fdp_vec_multidot_workspace_bytes(m + 1)) // 8),
+                         dtype=torch.float64, device=dev)
+        _GM_BUFFERS.clear()
+        _GM_BUFFERS[key] = (V, vin, t, w, h, ws)
+    V, vin, t, w, h, ws = _GM_BUFFERS[key]
+    vin.copy_(b)
+    apply_P(vin, w)
+    vec_dot(w, w, h[0:1])
+    beta = math.sqrt(float(h[0].item()))
+    if beta == 0.0:
+        return torch.zeros_like(b), 0, [0.0]
+    vec_lincomb(1.0 / beta, w, 0.0, None, 0.0, None, V[0])
+    H = np.zeros((m + 1, m))
+    cs = np.zeros(m)
+    sn = np.zeros(m)
+    g = np.zeros(m + 1)
+    g[0] = beta
+    hist = [1.0]
+    k = 0
+    h1, h2, nrm = h[:m + 1], h[m + 1:2 * m + 2], h[2 * m + 2:]
+    for j in range(m):
+        vin.copy_(V[j])
+        apply_A(vin, t)
+        apply_P(t, w)                                            # w = P^{-1} A v_j
+        vec_multidot(V, j + 1, w, h1, ws)                        # CGS, pass 1
+        vec_gemv(V, j + 1, h1, -1.0, w, 1.0)
+        vec_multidot(V, j + 1, w, h2, ws)                        # CGS, pass 2
+        vec_gemv(V, j + 1, h2, -1.0, w, 1.0)
+        vec_dot(w, w, nrm)
+        hh = h.cpu().numpy()                                     # the one host sync per step
+        H[:j + 1, j] = hh[:j + 1] + hh[m + 1:m + 2 + j]
+        H[j + 1, j] = math.sqrt(hh[2 * m + 2])
+        if H[j + 1, j] != 0.0:
+            vec_lincomb(1.0 / H[j + 1, j], w, 0.0, None, 0.0, None, V[j + 1])
+        for i in range(j):                                       # previous rotations
+            tmp = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
+            H[i + 1, j] = -sn[i] * H[i, j] + cs[i] * H[i + 1, j]
+            H[i, j] = tmp
+        den = math.hypot(H[j, j], H[j + 1, j])
+        cs[j] = H[j, j] / den
+        sn[j] = H[j + 1, j] / den
+        H[j, j] = den
+        H[j + 1, j] = 0.0
+        g[j + 1] = -sn[j] * g[j]
+        g[j] = cs[j] * g[j]
+        k = j + 1
+        hist.append(abs(g[j + 1]) / beta)
+        if abs(g[j + 1]) / beta <= tol or H[j, j] == 0.0:
+            break
+    y = np.zeros(k)
+    for i in range(k - 1, -1, -1):
+        y[i] = (g[i] - H[i, i + 1:k] @ y[i + 1:k]) / H[i, i]
+    h1[:k].copy_(torch.from_numpy(y))
+    x = torch.empty_like(b)
+    vec_gemv(V, k, h1, 1.0, x, 0.0)
+    return x, k, hist
