@@ -220,6 +220,35 @@ size_t block_tri_workspace_bytes(fdp_block P, int variant, const fdp_kron* B, co
 fdp_status block_tri_apply(fdp_block P, int variant, const fdp_kron* B, const fdp_kron* BT,
                            const double* r, double* s, void* workspace, void* stream);
 
+/* ---- Geometry-aware pencils (§6 P:1048-1059 and Appendix; NEXT-3) ----
+ * Host setup helpers (no device work). The pencils themselves are iga_mixed with weights at the
+ * quadrature points (K_d = int tau_d b' b', M_d = int mu_d b b), solved by fd_setup / fd_apply.
+ *
+ * iga_geometry_coeffs: c_out[d * nq^D + i] = c^k_dd at grid point i (i1 fastest; every direction
+ * uses the nq points x) of C_k^TH = (J^{-1} J^{-T} + D_k D_k^T) |det J|, D_k = J^{-1} e_k
+ * (eq. (Q_TH), nu = 1), for k = 0..D-1. kind FDP_GEOM_IDENTITY (D = 2, 3) or
+ * FDP_GEOM_ANNULUS (D = 3: G = ((1+eta1) cos(pi eta2/4), (1+eta1) sin(pi eta2/4), eta3), the
+ * eighth of the thick annulus of P:1264-1268). Errors: FDP_ERR_INVALID_ARG, FDP_ERR_UNSUPPORTED.
+ *
+ * iga_separable_fit: c_d (D host arrays over the nq[0] x .. x nq[D-1] grid, i1 fastest, > 0)
+ * ~ tau_d(i_d) prod_{m != d} mu_m(i_m) (Appendix), by log-domain alternating least
+ * squares (N3-2): init mu = 1, tau_d = slice geometric means; per sweep tau_1..tau_D then
+ * mu_1..mu_D by closed-form slice means; gauge geomean(mu_m) = 1; stop when the objective's
+ * relative change <= tol or after max_sweeps. tau, mu: host, concatenated per direction
+ * (sum nq doubles each); *sweeps (may be NULL) = sweeps done. FDP_ERR_INVALID_ARG on c <= 0. */
+enum { FDP_GEOM_IDENTITY = 0, FDP_GEOM_ANNULUS = 1 };
+fdp_status iga_geometry_coeffs(int kind, int D, int k, int nq, const double* x, double* c_out);
+fdp_status iga_separable_fit(int D, const int32_t* nq, const double* const* c, int max_sweeps,
+                             double tol, double* tau, double* mu, int* sweeps);
+
+/* Diagonals (host output, vec order i1 fastest), for the diagonal scalings D_V = diag(A) /
+ * diag(P^_V), D_Q = diag(Q) / diag(P_Q) of §6:
+ * fd_operator_diagonal: diag(R), R = sum_d coef_d (M_D (x) .. K_d .. (x) M_1) of the handle's pencils;
+ * kron_op_diagonal: diag(sum_t c_t F_tD (x) .. (x) F_t1) of a square operator (nin == nout),
+ * else FDP_ERR_SHAPE. */
+fdp_status fd_operator_diagonal(fdp_fd h, double* out);
+fdp_status kron_op_diagonal(fdp_kron h, double* out);
+
 /* ---- Arnoldi helpers for GMRES (Saad & Schultz) ----
  * V: m device vectors of length n with stride ldv >= n (V_j = V + j*ldv).
  * fdp_vec_multidot: h[j] = V_j . w for j < m into device h; deterministic (fixed grid, fixed

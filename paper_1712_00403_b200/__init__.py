@@ -74,6 +74,10 @@ def _load():
         "kron_ops_workspace_bytes": (sz, [i32, ctypes.POINTER(vp)]),
         "block_tri_workspace_bytes": (sz, [vp, i32, ctypes.POINTER(vp), ctypes.POINTER(vp)]),
         "block_tri_apply": (i32, [vp, i32, ctypes.POINTER(vp), ctypes.POINTER(vp), vp, vp, vp, vp]),
+        "iga_geometry_coeffs": (i32, [i32, i32, i32, i32, vp, vp]),
+        "iga_separable_fit": (i32, [i32, vp, ctypes.POINTER(vp), i32, ctypes.c_double, vp, vp, vp]),
+        "fd_operator_diagonal": (i32, [vp, vp]),
+        "kron_op_diagonal": (i32, [vp, vp]),
         "fdp_vec_multidot_workspace_bytes": (sz, [i32]),
         "fdp_vec_multidot": (i32, [vp, i64, i32, vp, i64, vp, vp, vp]),
         "fdp_vec_gemv": (i32, [vp, i64, i32, vp, ctypes.c_double, vp, ctypes.c_double, i64, vp]),
@@ -196,6 +200,12 @@ class FD:
     def workspace_bytes(self, batch: int) -> int:
         return int(lib.fd_workspace_bytes(self.h, batch))
 
+    def operator_diagonal(self):
+        """diag(sum_d coef_d (M_D (x) .. K_d .. (x) M_1)) (fd_operator_diagonal)."""
+        out = np.zeros(self.N)
+        _check(lib.fd_operator_diagonal(self.h, _ptr(out)))
+        return out
+
     def get_eigs(self, d: int):
         n = self.dims[d]
         U = np.zeros((n, n), order="F")
@@ -279,6 +289,12 @@ class KronOp:
                                  _dev(workspace, "workspace"), _stream(stream)))
         return y
 
+    def diagonal(self):
+        """diag of a square operator (kron_op_diagonal)."""
+        out = np.zeros(int(np.prod(self.nin)))
+        _check(lib.kron_op_diagonal(self.h, _ptr(out)))
+        return out
+
     @staticmethod
     def _handles(ops):
         return (ctypes.c_void_p * len(ops))(*[op.h.value for op in ops])
@@ -342,6 +358,35 @@ def vec_gemv(V, m, h, alpha, w, beta, stream=None):
     _check(lib.fdp_vec_gemv(_dev(V, "V"), V.stride(0), m, _dev(h, "h"), alpha, _dev(w, "w"), beta,
                             w.numel(), _stream(stream)))
     return w
+
+
+FDP_GEOM_IDENTITY = 0
+FDP_GEOM_ANNULUS = 1
+
+
+def iga_geometry_coeffs(kind: int, D: int, k: int, x):
+    """c^k_dd of C_k^TH at the tensor grid of the 1D points x: list of D arrays, each shaped
+    (len(x),) * D in vec order (i1 fastest) flattened (iga_geometry_coeffs)."""
+    x = _host(x)
+    nq = x.size
+    out = np.zeros(D * nq ** D)
+    _check(lib.iga_geometry_coeffs(kind, D, k, nq, _ptr(x), _ptr(out)))
+    return [out[d * nq ** D:(d + 1) * nq ** D] for d in range(D)]
+
+
+def iga_separable_fit(c, nq, max_sweeps: int = 50, tol: float = 1e-8):
+    """(tau, mu, sweeps): per-direction node values of c_d ~ tau_d prod_{m != d} mu_m."""
+    D = len(c)
+    cs = [_host(ci) for ci in c]
+    n = (ctypes.c_int32 * D)(*[int(v) for v in nq])
+    cp = (ctypes.c_void_p * D)(*[ci.ctypes.data for ci in cs])
+    tau = np.zeros(int(sum(nq)))
+    mu = np.zeros(int(sum(nq)))
+    sw = ctypes.c_int32(0)
+    _check(lib.iga_separable_fit(D, n, cp, max_sweeps, tol, _ptr(tau), _ptr(mu), ctypes.byref(sw)))
+    off = np.concatenate([[0], np.cumsum(nq)])
+    return ([tau[off[d]:off[d + 1]] for d in range(D)], [mu[off[d]:off[d + 1]] for d in range(D)],
+            sw.value)
 
 
 def slab_range(n: int, nranks: int, rank: int):

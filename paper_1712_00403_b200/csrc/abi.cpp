@@ -181,6 +181,7 @@ struct fdp_fd_s {
   int device = 0;
   TileCfg cfg[3];
   std::vector<double> U_host[3], lam_host[3];
+  std::vector<double> dK[3], dM[3];  // diagonals of the pencils (fd_operator_diagonal)
   double* Wf[3] = {nullptr, nullptr, nullptr};  // forward  W[k][a] = U[k][a]
   double* Wb[3] = {nullptr, nullptr, nullptr};  // backward W[k][a] = U[a][k]
   double* lamc[3] = {nullptr, nullptr, nullptr};  // coef[d] * lambda_d
@@ -245,6 +246,12 @@ extern "C" fdp_status fd_setup(int D, const int32_t* n, const double* const* K,
     std::string err;
     int st = gen_eig(nd, K[d], M[d], h->U_host[d].data(), h->lam_host[d].data(), &err);
     if (st) return fail((fdp_status)st, "fd_setup: " + err);
+    h->dK[d].resize(nd);
+    h->dM[d].resize(nd);
+    for (int i = 0; i < nd; ++i) {
+      h->dK[d][i] = K[d][i + (size_t)nd * i];
+      h->dM[d][i] = M[d][i + (size_t)nd * i];
+    }
     lmin += coef[d] * h->lam_host[d].front();
     lmax += coef[d] * h->lam_host[d].back();
   }
@@ -316,6 +323,33 @@ extern "C" fdp_status fd_get_eigs(fdp_fd h, int d, double* U_out, double* lambda
   if (d < 0 || d >= h->D) return fail(FDP_ERR_SHAPE, "fd_get_eigs: d out of range");
   if (U_out) std::memcpy(U_out, h->U_host[d].data(), h->U_host[d].size() * 8);
   if (lambda_out) std::memcpy(lambda_out, h->lam_host[d].data(), h->lam_host[d].size() * 8);
+  return FDP_OK;
+}
+
+// out[i] = sum_t c_t prod_d f_td[i_d] (i1 fastest) for per-direction diagonals f_td
+static void kron_diag_accumulate(int D, const int* n, const std::vector<const double*>& f, double c,
+                                 double* out) {
+  long long N = 1;
+  for (int d = 0; d < D; ++d) N *= n[d];
+  for (long long i = 0; i < N; ++i) {
+    long long t = i;
+    double v = c;
+    for (int d = 0; d < D; ++d) {
+      v *= f[d][t % n[d]];
+      t /= n[d];
+    }
+    out[i] += v;
+  }
+}
+
+extern "C" fdp_status fd_operator_diagonal(fdp_fd h, double* out) {
+  if (!h || !out) return fail(FDP_ERR_INVALID_ARG, "fd_operator_diagonal: NULL argument");
+  std::fill(out, out + h->N, 0.0);
+  for (int d = 0; d < h->D; ++d) {
+    std::vector<const double*> f(h->D);
+    for (int e = 0; e < h->D; ++e) f[e] = e == d ? h->dK[e].data() : h->dM[e].data();
+    kron_diag_accumulate(h->D, h->n, f, h->coef[d], out);
+  }
   return FDP_OK;
 }
 
@@ -1555,6 +1589,7 @@ extern "C" fdp_status fdp_vec_lincomb(double a, const double* x, double b, const
 struct KronFactor {
   int nin = 0, nout = 0;
   TileCfg cfg{};
+  std::vector<double> diag;  // F[i][i] for i < min(nin, nout) (kron_op_diagonal)
   double* W = nullptr;  // W[k][a] = F[a][k], kpad x ldw
 };
 struct fdp_kron_s {
@@ -1603,6 +1638,7 @@ extern "C" fdp_status kron_op_setup(int D, int nterms, const int32_t* nin, const
       KronFactor& kf = raw->f[t * D + d];
       kf.nin = nin[d];
       kf.nout = nout[d];
+      for (int i = 0; i < std::min(nin[d], nout[d]); ++i) kf.diag.push_back(F[i + (size_t)nout[d] * i]);
       // columns tile over nout; the small path also needs BN >= nin (W rows staged in smem)
       TileCfg c = choose_tile(std::max(nin[d], nout[d]) <= kSmallMaxN ? std::max(nin[d], nout[d]) : nout[d]);
       c.kpad = ((nin[d] + 31) / 32) * 32;
@@ -1690,6 +1726,21 @@ extern "C" fdp_status kron_op_apply(fdp_kron h, const double* x, int64_t xbs, do
       src = dst;
       sbs = dbs;
     }
+  }
+  return FDP_OK;
+}
+
+extern "C" fdp_status kron_op_diagonal(fdp_kron h, double* out) {
+  if (!h || !out) return fail(FDP_ERR_INVALID_ARG, "kron_op_diagonal: NULL argument");
+  for (int d = 0; d < h->D; ++d)
+    if (h->nin[d] != h->nout[d]) return fail(FDP_ERR_SHAPE, "kron_op_diagonal: operator is not square");
+  long long N = 1;
+  for (int d = 0; d < h->D; ++d) N *= h->nin[d];
+  std::fill(out, out + N, 0.0);
+  for (int t = 0; t < h->nterms; ++t) {
+    std::vector<const double*> f(h->D);
+    for (int d = 0; d < h->D; ++d) f[d] = h->f[t * h->D + d].diag.data();
+    kron_diag_accumulate(h->D, h->nin, f, h->coef[t], out);
   }
   return FDP_OK;
 }

@@ -44,12 +44,61 @@ def _spaces(D, disc, p):
     return V, Q
 
 
-class StokesOperator:
+class _GroupedOperator:
+    """y = calA x for a block operator given as (KronOp, input block, output block) triples:
+    applied by ONE kron_ops_apply call (all terms grouped per mode, one sum per output block),
+    captured once per (x, y) pair into a CUDA graph and replayed."""
+
+    def _finalize(self, group, sizes, device):
+        import torch
+        self.torch = torch
+        self._group = group
+        self.sizes = [int(v) for v in sizes]
+        self.off_idx = np.concatenate([[0], np.cumsum(self.sizes)]).astype(np.int64)
+        self.n = int(self.off_idx[-1])
+        ops = [g[0] for g in group]
+        self.ws = torch.empty(max(op.workspace_bytes(1) for op in ops) // 8 + 1, dtype=torch.float64,
+                              device=f"cuda:{device}")
+        self.gws = torch.empty(KronOp.group_workspace_bytes(ops) // 8 + 1, dtype=torch.float64,
+                               device=f"cuda:{device}")
+        self.grouped = True
+
+    def apply(self, x, y):
+        """y = calA x (graph-replayed; no allocation or host synchronisation inside)."""
+        torch = self.torch
+        key = (x.data_ptr(), y.data_ptr())
+        if not hasattr(self, "_graphs"):
+            self._graphs = {}
+        g = self._graphs.get(key)
+        if g is None:
+            self._apply_direct(x, y)  # warm (kernel attributes, lazy module state)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._apply_direct(x, y)
+            self._graphs[key] = g
+        g.replay()
+        return y
+
+    def _apply_direct(self, x, y):
+        o = self.off_idx
+        blk = lambda v, k: v[o[k]:o[k + 1]]
+        if self.grouped:
+            KronOp.apply_group([g[0] for g in self._group], [blk(x, g[1]) for g in self._group],
+                               [blk(y, g[2]) for g in self._group], [1.0] * len(self._group), 0.0,
+                               self.gws)
+            return y
+        seen = set()
+        for op, i, j in self._group:          # one kron_op_apply per block (reference path)
+            op.apply(blk(x, i), blk(y, j), 1.0, 1.0 if j in seen else 0.0, self.ws)
+            seen.add(j)
+        return y
+
+
+class StokesOperator(_GroupedOperator):
     """y = calA x for x = [u_1 | .. | u_D | p] (vec order, i1 fastest), on cuda:device."""
 
     def __init__(self, D: int, disc: str, p: int, n_el: int, nu_terms=None, device: int = 0):
-        import torch
-        self.torch = torch
         self.D = D
         nu_terms = nu_terms or [(1.0, None)]
         weighted = any(w is not None for _, w in nu_terms)
@@ -92,65 +141,17 @@ class StokesOperator:
             self.BT.append(KronOp([[np.asfortranarray(f.T) for f in F]], [-1.0], device))
         self.vel_dims = [self.diag[k].nin for k in range(D)]
         self.q_dims = self.B[0].nout
-        self.sizes = [int(np.prod(v)) for v in self.vel_dims] + [int(np.prod(self.q_dims))]
-        self.off_idx = np.concatenate([[0], np.cumsum(self.sizes)]).astype(np.int64)
-        self.n = int(self.off_idx[-1])
-        ops = self.diag + list(self.off.values()) + self.B + self.BT
-        self.ws = torch.empty(max(op.workspace_bytes(1) for op in ops) // 8 + 1, dtype=torch.float64,
-                              device=f"cuda:{device}")
-        # grouped apply: every block of calA as one (ops, x-block, y-block) list -> kron_ops_apply
-        self._group = []
+        group = []
         for r in range(D):
-            self._group.append((self.diag[r], r, r))
+            group.append((self.diag[r], r, r))
             for s in range(D):
                 if s != r:
-                    self._group.append((self.off[(r, s)], s, r))
-            self._group.append((self.BT[r], D, r))
+                    group.append((self.off[(r, s)], s, r))
+            group.append((self.BT[r], D, r))
         for r in range(D):
-            self._group.append((self.B[r], r, D))
-        gops = [g[0] for g in self._group]
-        self.gws = torch.empty(KronOp.group_workspace_bytes(gops) // 8 + 1, dtype=torch.float64,
-                               device=f"cuda:{device}")
-        self.grouped = True
-
-    def apply(self, x, y):
-        """y = calA x. The ~20 KronOp launches are captured once per (x, y) pair into a CUDA graph
-        and replayed (no allocation or host synchronisation inside)."""
-        torch = self.torch
-        key = (x.data_ptr(), y.data_ptr())
-        if not hasattr(self, "_graphs"):
-            self._graphs = {}
-        g = self._graphs.get(key)
-        if g is None:
-            self._apply_direct(x, y)  # warm (kernel attributes, lazy module state)
-            torch.cuda.synchronize()
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                self._apply_direct(x, y)
-            self._graphs[key] = g
-        g.replay()
-        return y
-
-    def _apply_direct(self, x, y):
-        o = self.off_idx
-        D = self.D
-        blk = lambda v, k: v[o[k]:o[k + 1]]
-        if self.grouped:
-            KronOp.apply_group([g[0] for g in self._group], [blk(x, g[1]) for g in self._group],
-                               [blk(y, g[2]) for g in self._group], [1.0] * len(self._group), 0.0,
-                               self.gws)
-            return y
-        for r in range(D):
-            yr = blk(y, r)
-            self.diag[r].apply(blk(x, r), yr, 1.0, 0.0, self.ws)
-            for s in range(D):
-                if s != r:
-                    self.off[(r, s)].apply(blk(x, s), yr, 1.0, 1.0, self.ws)
-            self.BT[r].apply(blk(x, D), yr, 1.0, 1.0, self.ws)
-        yp = blk(y, D)
-        for r in range(D):
-            self.B[r].apply(blk(x, r), yp, 1.0, 0.0 if r == 0 else 1.0, self.ws)
-        return y
+            group.append((self.B[r], r, D))
+        sizes = [int(np.prod(v)) for v in self.vel_dims] + [int(np.prod(self.q_dims))]
+        self._finalize(group, sizes, device)
 
 
 _BUFFERS = {}

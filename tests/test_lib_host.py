@@ -137,3 +137,29 @@ def test_iga_mixed_weighted_and_quadrature():
     Ao = ost._mixed(ost._space(3, 2, n_el, True), ost._space(3, 2, n_el, True), n_el, q, True, True,
                     weight=lambda t: np.sin(2 * np.pi * t))
     assert np.max(np.abs(A - Ao)) <= 1e-13 * np.max(np.abs(Ao))
+
+
+def test_geometry_coeffs_and_separable_fit_match_oracle():
+    """NEXT-3 host helpers (iga_geometry_coeffs, iga_separable_fit) vs oracle/geometry.py."""
+    from oracle import geometry as og
+    x, _ = og.quadrature_grid(3, 5)
+    for k in range(3):
+        c_o = og.sample_diagonal(og.annulus(), k, x)
+        c_l = fdp.iga_geometry_coeffs(fdp.FDP_GEOM_ANNULUS, 3, k, x)
+        for d in range(3):
+            ref = np.reshape(c_o[d], -1, order="F")
+            assert np.max(np.abs(c_l[d] - ref) / ref) < 1e-14
+        t_o, m_o, _ = og.separable_fit(c_o)
+        t_l, m_l, _ = fdp.iga_separable_fit(c_l, [x.size] * 3)
+        for a, b in zip(t_o + m_o, t_l + m_l):
+            assert np.max(np.abs(a - b) / b) < 1e-12
+        ci = fdp.iga_geometry_coeffs(fdp.FDP_GEOM_IDENTITY, 3, k, x)
+        for d in range(3):
+            assert np.all(ci[d] == (2.0 if d == k else 1.0))
+
+
+def test_separable_fit_rejects_nonpositive():
+    c = [np.ones(8), np.ones(8)]
+    c[1][3] = 0.0
+    with pytest.raises(fdp.FdpError):
+        fdp.iga_separable_fit(c, [2, 4])
