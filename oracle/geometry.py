@@ -213,6 +213,24 @@ class StokesMapped:
         y[self.off_idx[D]:] = yp
         return y
 
+    def B_apply(self, u):
+        """B u = sum_r B_r u_r (velocity -> pressure)."""
+        yp = np.zeros(self.sizes[self.D])
+        for r in range(self.D):
+            for c, F in self.B[r]:
+                yp += c * _kron_apply(F, self._blk(u, r))
+        return yp
+
+    def BT_apply(self, pr):
+        """B^T p = [B_1^T p | .. | B_D^T p]."""
+        out = []
+        for r in range(self.D):
+            acc = np.zeros(self.sizes[r])
+            for c, F in self.B[r]:
+                acc += c * _kron_apply([f.T for f in F], pr)
+            out.append(acc)
+        return np.concatenate(out)
+
     def diag_A(self, k):
         """diag(A_kk) = sum_terms c prod_m diag(F_m) (Kronecker product of diagonals, i1 fastest)."""
         out = np.zeros(self.sizes[k])

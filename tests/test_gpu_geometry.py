@@ -73,3 +73,22 @@ def test_annulus_minres_iteration_counts(p, n_el):
         counts.append(it)
     assert counts == [it_po, it_go], (counts, it_po, it_go)
     assert it_go < 0.8 * it_po
+
+
+@pytest.mark.parametrize("variant", ["T", "C"])
+def test_annulus_block_gmres_counts(variant):
+    """P_T^G- / P_C^G-GMRES on the annulus (the paper's Tables 5-6 setting): identical counts."""
+    from oracle import gmres as ogmres
+    p, n_el = 2, 8
+    op = ogeo.StokesMapped(ogeo.annulus(), p, n_el)
+    f = ostokes.project_rhs(np.random.default_rng(0).standard_normal(op.n), op.sizes[-1])
+    disc, dv, dq = ogeo.geo_discretization(op)
+    oblk = oprec.BlockPrecond(disc, dv, dq)
+    oP = (oprec.TriangularPrecond if variant == "T" else oprec.ConstrainedPrecond)(oblk, op)
+    _, it_o, _ = ogmres.gmres(op.matvec, f, oP.apply)
+    gop = ggeo.AnnulusStokesOperator(p, n_el)
+    P, _ = ggeo.geometry_block(gop)
+    tri = P.tri(variant, gop.B, gop.BT)
+    ws = tri.workspace()
+    _, it_g, _ = krylov.gmres(gop.apply, lambda r, z: tri.apply(r, z, ws), dev(f))
+    assert it_g == it_o, (variant, it_g, it_o)

@@ -192,3 +192,15 @@ def test_geometry_aware_preconditioner_reduces_minres_iterations():
     disc, dv, dq = geometry.geo_discretization(op)
     _, it_geo, _ = minres.minres(op.matvec, f, precond.BlockPrecond(disc, dv, dq).apply)
     assert it_geo < 0.8 * it_plain, (it_geo, it_plain)
+
+
+def test_mapped_b_and_bt_consistent_with_matvec():
+    op = geometry.StokesMapped(geometry.annulus(), 1, 2)
+    rng = np.random.default_rng(4)
+    nv = int(op.off_idx[-2])
+    u = rng.standard_normal(nv)
+    q = rng.standard_normal(op.sizes[-1])
+    x = np.concatenate([u, np.zeros(op.sizes[-1])])
+    assert np.allclose(op.matvec(x)[nv:], op.B_apply(u), rtol=0, atol=1e-14)
+    x = np.concatenate([np.zeros(nv), q])
+    assert np.allclose(op.matvec(x)[:nv], op.BT_apply(q), rtol=0, atol=1e-14)
