@@ -532,6 +532,7 @@ static cudaError_t launch_stage(std::vector<ModeProb>& probs_in, const std::vect
 static cudaError_t launch_pp_stage(std::vector<ModeProb>& probs1, std::vector<ModeProb>& probs2,
                                    int NT, bool kmaj1, int* sync, long long sync_cap,
                                    cudaStream_t s, int* nlaunch, Recorder* rec) {
+  if (probs1.size() > (size_t)kSmallGroup || probs2.size() != probs1.size()) return cudaErrorInvalidValue;
   ModeGroup g1{}, g2{};
   g1.count = g2.count = (int)probs1.size();
   std::vector<double> w(g1.count);
@@ -647,7 +648,7 @@ static cudaError_t enqueue_fd(const std::vector<const fdp_fd_s*>& hs,
     }
     if (hook) hook(pass, st.fwd, d, probs, cfgs);
     if (pp && (pass == 0 || pass == 3)) {
-      bool ok = probs.size() <= (size_t)kMaxGroup;
+      bool ok = probs.size() <= (size_t)kSmallGroup;
       for (const ModeProb& p : probs) ok = ok && small_ok(p);
       if (ok) {
         held = probs;

@@ -69,15 +69,31 @@ __device__ __forceinline__ double fdp_div(double a, double b) {
 }
 #endif
 
-constexpr int kMaxGroup = 32;  // problems per grouped launch (kernel parameters < 32 KB)
-struct ModeGroup {
-  ModeProb prob[kMaxGroup];
+// Problems of one grouped launch, passed by value as the kernel parameter. Kernels are compiled
+// for two capacities: kSmallGroup (the FD stages: <= 4 problems, a small parameter block keeps the
+// launch cheap) and kMaxGroup (multi-operator Kronecker stages); the host fills a ModeGroup and
+// the launcher narrows it when it fits.
+constexpr int kMaxGroup = 32;   // kernel parameters stay < 32 KB
+constexpr int kSmallGroup = 4;
+template <int G>
+struct ModeGroupT {
+  ModeProb prob[G];
   int count;
   int total_ctas;
   // diagnostics: when non-null, lane 0 of every warp records %globaltimer at kTracePhases points
   // of its first tile into trace[(blockIdx * warps + warp) * kTracePhases + phase]
   unsigned long long* trace;
 };
+using ModeGroup = ModeGroupT<kMaxGroup>;
+template <int G>
+inline ModeGroupT<G> narrow_group(const ModeGroup& g) {
+  ModeGroupT<G> o;
+  for (int i = 0; i < G; ++i) o.prob[i] = g.prob[i];
+  o.count = g.count;
+  o.total_ctas = g.total_ctas;
+  o.trace = g.trace;
+  return o;
+}
 constexpr int kTracePhases = 6;
 
 // K1 CTA: kK1Warps warps stacked along M (BM = kK1Warps * 8 * MT rows).
@@ -113,9 +129,9 @@ constexpr int kPPMaxNT = 10;  // plane pipeline keeps two W tiles in shared memo
 struct PlaneSync {
   int* cnt;
   int* done;
-  int cnt_off[kMaxGroup];
-  int rows_per_plane1[kMaxGroup];
-  int rows_per_plane2[kMaxGroup];
+  int cnt_off[kSmallGroup];
+  int rows_per_plane1[kSmallGroup];
+  int rows_per_plane2[kSmallGroup];
   int cnt_total;
 };
 cudaError_t launch_mode_pp(const ModeGroup& g1, const ModeGroup& g2, const PlaneSync& ps, int NT,

@@ -57,9 +57,9 @@ struct Smem {
   static constexpr size_t BYTES = sizeof(double) * STAGE * STAGES;
 };
 
-template <int MT, int NT, bool KMAJ>
+template <int MT, int NT, bool KMAJ, int G>
 __global__ void __launch_bounds__(THREADS)
-mode_contract_kernel(const __grid_constant__ ModeGroup grp) {
+mode_contract_kernel(const __grid_constant__ ModeGroupT<G> grp) {
   using S = Smem<MT, NT, KMAJ>;
   constexpr int BM = S::BM, BN = S::BN;
   extern __shared__ __align__(16) double smem[];
@@ -67,7 +67,7 @@ mode_contract_kernel(const __grid_constant__ ModeGroup grp) {
   // ---- which problem / tile ----
   int pi = 0;
 #pragma unroll
-  for (int i = 1; i < kMaxGroup; ++i)
+  for (int i = 1; i < G; ++i)
     if (i < grp.count && (int)blockIdx.x >= grp.prob[i].cta_begin) pi = i;
   const ModeProb& pb = grp.prob[pi];
   const int t = blockIdx.x - pb.cta_begin;
@@ -233,10 +233,18 @@ mode_contract_kernel(const __grid_constant__ ModeGroup grp) {
 template <int MT, int NT, bool KMAJ>
 cudaError_t launch_t(const ModeGroup* g, cudaStream_t s) {
   using S = Smem<MT, NT, KMAJ>;
-  if (!g)  // prepare: raise the dynamic shared-memory limit (outside any stream capture)
-    return cudaFuncSetAttribute(mode_contract_kernel<MT, NT, KMAJ>,
+  if (!g) {  // prepare: raise the dynamic shared-memory limit (outside any stream capture)
+    cudaError_t e = cudaFuncSetAttribute(mode_contract_kernel<MT, NT, KMAJ, kSmallGroup>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(mode_contract_kernel<MT, NT, KMAJ, kMaxGroup>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES);
-  mode_contract_kernel<MT, NT, KMAJ><<<g->total_ctas, THREADS, S::BYTES, s>>>(*g);
+  }
+  if (g->count <= kSmallGroup)
+    mode_contract_kernel<MT, NT, KMAJ, kSmallGroup><<<g->total_ctas, THREADS, S::BYTES, s>>>(
+        narrow_group<kSmallGroup>(*g));
+  else
+    mode_contract_kernel<MT, NT, KMAJ, kMaxGroup><<<g->total_ctas, THREADS, S::BYTES, s>>>(*g);
   return cudaGetLastError();
 }
 

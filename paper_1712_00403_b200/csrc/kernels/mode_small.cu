@@ -399,8 +399,8 @@ __device__ __forceinline__ void tile_compute_store(const ModeProb& pb, const Geo
   if (tr) tr[5] = gtimer();
 }
 
-template <int NT, bool KMAJ>
-__global__ void __launch_bounds__(STH, 1) mode_small_kernel(const __grid_constant__ ModeGroup grp) {
+template <int NT, bool KMAJ, int G>
+__global__ void __launch_bounds__(STH, 1) mode_small_kernel(const __grid_constant__ ModeGroupT<G> grp) {
   using S = SS<NT>;
   extern __shared__ __align__(16) double sm[];
   double* Ws = sm;
@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(STH, 1) mode_small_kernel(const __grid_constan
 
   int pi = 0;
 #pragma unroll
-  for (int i = 1; i < kMaxGroup; ++i)
+  for (int i = 1; i < G; ++i)
     if (i < grp.count && (int)blockIdx.x >= grp.prob[i].cta_begin) pi = i;
   const ModeProb& pb = grp.prob[pi];
   const Geo g(pb);
@@ -438,9 +438,9 @@ constexpr int SWP = 8;
 template <int NT>
 constexpr size_t bytes_prefetch() { return sizeof(double) * (SS<NT>::W_ELEMS + SWP * 2 * SS<NT>::ABUF); }
 
-template <int NT, bool KMAJ>
+template <int NT, bool KMAJ, int G>
 __global__ void __launch_bounds__(SWP * 32, 1)
-mode_small_pf_kernel(const __grid_constant__ ModeGroup grp) {
+mode_small_pf_kernel(const __grid_constant__ ModeGroupT<G> grp) {
   using S = SS<NT>;
   extern __shared__ __align__(16) double sm[];
   double* Ws = sm;
@@ -449,7 +449,7 @@ mode_small_pf_kernel(const __grid_constant__ ModeGroup grp) {
 
   int pi = 0;
 #pragma unroll
-  for (int i = 1; i < kMaxGroup; ++i)
+  for (int i = 1; i < G; ++i)
     if (i < grp.count && (int)blockIdx.x >= grp.prob[i].cta_begin) pi = i;
   const ModeProb& pb = grp.prob[pi];
   const Geo g(pb);
@@ -499,7 +499,8 @@ mode_small_pf_kernel(const __grid_constant__ ModeGroup grp) {
 // ------------------------------------------------------------------------------------------------
 template <int NT, bool KMAJ1, bool KMAJ2>
 __global__ void __launch_bounds__(STH, 1)
-mode_pp_kernel(const __grid_constant__ ModeGroup grp1, const __grid_constant__ ModeGroup grp2,
+mode_pp_kernel(const __grid_constant__ ModeGroupT<kSmallGroup> grp1,
+               const __grid_constant__ ModeGroupT<kSmallGroup> grp2,
                const __grid_constant__ PlaneSync ps) {
   using S = SS<NT>;
   extern __shared__ __align__(16) double sm[];
@@ -510,7 +511,7 @@ mode_pp_kernel(const __grid_constant__ ModeGroup grp1, const __grid_constant__ M
 
   int pi = 0;
 #pragma unroll
-  for (int i = 1; i < kMaxGroup; ++i)
+  for (int i = 1; i < kSmallGroup; ++i)
     if (i < grp1.count && (int)blockIdx.x >= grp1.prob[i].cta_begin) pi = i;
   const ModeProb& p1 = grp1.prob[pi];
   const ModeProb& p2 = grp2.prob[pi];
@@ -577,10 +578,13 @@ cudaError_t launch_s(const ModeGroup* g, cudaStream_t s) {
   // prefetching variant is opt-in (FDP_SMALL_PF=1)
   const bool pf = bytes_prefetch<NT>() <= 227 * 1024 && std::getenv("FDP_SMALL_PF") != nullptr;
   if (!g) {
-    cudaError_t e = cudaFuncSetAttribute(mode_small_kernel<NT, KMAJ>,
+    cudaError_t e = cudaFuncSetAttribute(mode_small_kernel<NT, KMAJ, kSmallGroup>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(mode_small_kernel<NT, KMAJ, kMaxGroup>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES);
     if (e != cudaSuccess || bytes_prefetch<NT>() > 227 * 1024) return e;
-    return cudaFuncSetAttribute(mode_small_pf_kernel<NT, KMAJ>,
+    return cudaFuncSetAttribute(mode_small_pf_kernel<NT, KMAJ, kSmallGroup>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes_prefetch<NT>());
   }
   cudaLaunchConfig_t cfg = {};
@@ -593,8 +597,14 @@ cudaError_t launch_s(const ModeGroup* g, cudaStream_t s) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (pf) return cudaLaunchKernelEx(&cfg, mode_small_pf_kernel<NT, KMAJ>, *g);
-  return cudaLaunchKernelEx(&cfg, mode_small_kernel<NT, KMAJ>, *g);
+  if (g->count <= kSmallGroup) {
+    const ModeGroupT<kSmallGroup> gs = narrow_group<kSmallGroup>(*g);
+    if (pf) return cudaLaunchKernelEx(&cfg, mode_small_pf_kernel<NT, KMAJ, kSmallGroup>, gs);
+    return cudaLaunchKernelEx(&cfg, mode_small_kernel<NT, KMAJ, kSmallGroup>, gs);
+  }
+  cfg.blockDim = dim3(STH);
+  cfg.dynamicSmemBytes = S::BYTES;
+  return cudaLaunchKernelEx(&cfg, mode_small_kernel<NT, KMAJ, kMaxGroup>, *g);
 }
 
 template <int NT, bool K1, bool K2>
@@ -613,7 +623,9 @@ cudaError_t launch_pp(const ModeGroup* g1, const ModeGroup* g2, const PlaneSync*
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, mode_pp_kernel<NT, K1, K2>, *g1, *g2, *ps);
+  if (g1->count > kSmallGroup) return cudaErrorInvalidValue;
+  return cudaLaunchKernelEx(&cfg, mode_pp_kernel<NT, K1, K2>, narrow_group<kSmallGroup>(*g1),
+                            narrow_group<kSmallGroup>(*g2), *ps);
 }
 
 template <bool KMAJ>
