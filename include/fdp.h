@@ -161,6 +161,11 @@ fdp_status block_precond_apply(fdp_block h, const double* r, double* s, int64_t 
  * buffers sized on first use. */
 fdp_status block_precond_apply_host(fdp_block h, const double* r_host, double* s_host,
                                     int64_t batch, void* stream);
+/* Page-locked host memory for the host-buffer path (cudaMallocHost on the current device; H2D
+ * from it runs at full PCIe rate). fdp_host_alloc returns NULL on failure (fdp_last_error says
+ * why); fdp_host_free(NULL) is a no-op. */
+void* fdp_host_alloc(size_t bytes);
+fdp_status fdp_host_free(void* p);
 fdp_status block_precond_destroy(fdp_block h);
 
 /* Number of kernel launches one block_precond_apply issues for `batch` (for accounting). */

@@ -78,6 +78,8 @@ def _load():
         "iga_separable_fit": (i32, [i32, vp, ctypes.POINTER(vp), i32, ctypes.c_double, vp, vp, vp]),
         "fd_operator_diagonal": (i32, [vp, vp]),
         "kron_op_diagonal": (i32, [vp, vp]),
+        "fdp_host_alloc": (vp, [sz]),
+        "fdp_host_free": (i32, [vp]),
         "fdp_vec_multidot_workspace_bytes": (sz, [i32]),
         "fdp_vec_multidot": (i32, [vp, i64, i32, vp, i64, vp, vp, vp]),
         "fdp_vec_gemv": (i32, [vp, i64, i32, vp, ctypes.c_double, vp, ctypes.c_double, i64, vp]),
@@ -340,6 +342,30 @@ def vec_lincomb(a, x, b, y, c, z, out, stream=None):
                                None if z is None else _dev(z, "z"), _dev(out, "out"), out.numel(),
                                _stream(stream)))
     return out
+
+
+class _PinnedBuffer:
+    def __init__(self, nbytes):
+        self.ptr = lib.fdp_host_alloc(nbytes)
+        if not self.ptr:
+            raise FdpError(6, lib.fdp_last_error().decode())
+
+    def __del__(self):
+        try:
+            lib.fdp_host_free(self.ptr)
+        except Exception:
+            pass
+
+
+def host_empty(shape, dtype=np.float64) -> np.ndarray:
+    """numpy array in page-locked host memory (fdp_host_alloc), freed with the array."""
+    dt = np.dtype(dtype)
+    n = int(np.prod(shape)) * dt.itemsize
+    buf = _PinnedBuffer(max(n, 1))
+    raw = (ctypes.c_char * max(n, 1)).from_address(buf.ptr)
+    raw._fdp_pinned = buf  # the ctypes array (the numpy base) keeps the allocation alive
+    arr = np.ctypeslib.as_array(raw)
+    return arr[:n].view(dt).reshape(shape)
 
 
 def vec_multidot(V, m, w, h, workspace=None, stream=None):

@@ -941,6 +941,13 @@ struct fdp_block_s {
   double* e2e_s = nullptr;
   void* e2e_ws = nullptr;
   int64_t e2e_batch = 0;
+  // host-buffer pipeline: copy-in / copy-out streams and per-unit events
+  cudaStream_t cin = nullptr, cout = nullptr;
+  std::vector<cudaEvent_t> ev_in, ev_done;
+  // batch-1 pipeline over pinned buffers, captured once per (r_host, s_host) and replayed
+  const double* e2e_gr = nullptr;
+  double* e2e_gs = nullptr;
+  cudaGraphExec_t e2e_graph = nullptr;
 };
 
 static void free_block(fdp_block h) {
@@ -956,6 +963,11 @@ static void free_block(fdp_block h) {
   cudaFree(h->e2e_r);
   cudaFree(h->e2e_s);
   cudaFree(h->e2e_ws);
+  for (cudaEvent_t e : h->ev_in) cudaEventDestroy(e);
+  for (cudaEvent_t e : h->ev_done) cudaEventDestroy(e);
+  if (h->e2e_graph) cudaGraphExecDestroy(h->e2e_graph);
+  if (h->cin) cudaStreamDestroy(h->cin);
+  if (h->cout) cudaStreamDestroy(h->cout);
   delete h;
 }
 
@@ -1300,11 +1312,31 @@ extern "C" fdp_status block_precond_apply(fdp_block h, const double* r, double* 
   return FDP_OK;
 }
 
+// One pipeline unit of the host-buffer path at batch 1: velocity component k (k < D) or the
+// pressure block (k == D), r -> s on stream st (T: component workspace).
+static cudaError_t enqueue_unit(fdp_block h, int k, const double* r, double* s, double* T,
+                                cudaStream_t st) {
+  if (k == h->D) {
+    return enqueue_mass(h->pres, FDP_MASS_INVERSE, r + h->off[k], s + h->off[k], h->size, h->dq, 1,
+                        st, nullptr);
+  }
+  const fdp_fd_s* f = h->vel[k];
+  const double* in = r + h->off[k];
+  const double* dsc = h->dv ? h->dv + h->off[k] : nullptr;
+  if (dsc) {
+    cudaError_t e = launch_scale(in, s + h->off[k], dsc, f->N, 1, f->N, f->N, st);
+    if (e != cudaSuccess) return e;
+    in = s + h->off[k];
+  }
+  return enqueue_fd({f}, {in}, f->N, {s + h->off[k]}, f->N, {T}, {dsc}, 1, st, nullptr);
+}
+
 extern "C" fdp_status block_precond_apply_host(fdp_block h, const double* r_host, double* s_host,
                                                int64_t batch, void* stream) {
   if (!h) return fail(FDP_ERR_INVALID_ARG, "block_precond_apply_host: NULL handle");
   if (!r_host || !s_host) return fail(FDP_ERR_INVALID_ARG, "block_precond_apply_host: NULL buffer");
   if (batch <= 0) return batch == 0 ? FDP_OK : fail(FDP_ERR_SHAPE, "block_precond_apply_host: batch < 0");
+  std::lock_guard<std::mutex> lk(h->mu);
   DeviceGuard dg(h->device);
   if (batch > h->e2e_batch) {
     cudaFree(h->e2e_r);
@@ -1319,14 +1351,127 @@ extern "C" fdp_status block_precond_apply_host(fdp_block h, const double* r_host
         (st = dalloc(reinterpret_cast<double**>(&h->e2e_ws), (size_t)block_ws_elems(h, batch))))
       return st;
     h->e2e_batch = batch;
+    if (h->e2e_graph) {  // captured against the old device buffers
+      cudaGraphExecDestroy(h->e2e_graph);
+      h->e2e_graph = nullptr;
+    }
+  }
+  if (!h->cin) {
+    FDP_CUDA(cudaStreamCreateWithFlags(&h->cin, cudaStreamNonBlocking), "apply_host: stream");
+    FDP_CUDA(cudaStreamCreateWithFlags(&h->cout, cudaStreamNonBlocking), "apply_host: stream");
+  }
+  // Pipeline units: the D + 1 blocks of one item at batch 1, whole items at batch > 1. Copies in
+  // run on cin, the applies on the caller's stream, copies out on cout, so unit j's compute
+  // overlaps unit j+1's upload and unit j-1's download (PCIe is full duplex).
+  const int units = batch == 1 ? h->D + 1 : (int)batch;
+  while ((int)h->ev_in.size() < units) {
+    cudaEvent_t a, b;
+    FDP_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming), "apply_host: event");
+    FDP_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming), "apply_host: event");
+    h->ev_in.push_back(a);
+    h->ev_done.push_back(b);
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const size_t bytes = (size_t)(batch * h->size) * sizeof(double);
-  FDP_CUDA(cudaMemcpyAsync(h->e2e_r, r_host, bytes, cudaMemcpyHostToDevice, st), "apply_host: H2D");
-  fdp_status s = block_precond_apply(h, h->e2e_r, h->e2e_s, batch, h->e2e_ws, stream);
-  if (s) return s;
-  FDP_CUDA(cudaMemcpyAsync(s_host, h->e2e_s, bytes, cudaMemcpyDeviceToHost, st), "apply_host: D2H");
-  FDP_CUDA(cudaStreamSynchronize(st), "apply_host: sync");
+  auto pinned = [](const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+  };
+  // batch 1 with page-locked buffers: replay the captured pipeline (copies, applies, events)
+  const bool use_graph = batch == 1 && pinned(r_host) && pinned(s_host) &&
+                         std::getenv("FDP_E2E_NO_GRAPH") == nullptr;
+  if (use_graph && h->e2e_graph && h->e2e_gr == r_host && h->e2e_gs == s_host) {
+    FDP_CUDA(cudaGraphLaunch(h->e2e_graph, st), "apply_host: graph launch");
+    FDP_CUDA(cudaStreamSynchronize(st), "apply_host: sync");
+    return FDP_OK;
+  }
+  cudaStream_t origin = st;
+  if (use_graph) {
+    if (h->e2e_graph) {
+      cudaGraphExecDestroy(h->e2e_graph);
+      h->e2e_graph = nullptr;
+    }
+    st = h->cap;  // capture on the handle's private stream, then launch on the caller's
+    FDP_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "apply_host: capture");
+  }
+  // batch 1: the small pressure block goes first so its solve and download hide under the
+  // velocity uploads
+  auto blk = [&](int j) { return j == 0 ? h->D : j - 1; };
+  auto span = [&](int j, long long* off, long long* len) {
+    if (batch == 1) {
+      *off = h->off[blk(j)];
+      *len = h->off[blk(j) + 1] - h->off[blk(j)];
+    } else {
+      *off = (long long)j * h->size;
+      *len = h->size;
+    }
+  };
+  // the copy-in stream must not overwrite device inputs still read by a previous call
+  FDP_CUDA(cudaEventRecord(h->ev_done[0], st), "apply_host: order");
+  FDP_CUDA(cudaStreamWaitEvent(h->cin, h->ev_done[0], 0), "apply_host: order");
+  for (int j = 0; j < units; ++j) {
+    long long off, len;
+    span(j, &off, &len);
+    FDP_CUDA(cudaMemcpyAsync(h->e2e_r + off, r_host + off, (size_t)len * sizeof(double),
+                             cudaMemcpyHostToDevice, h->cin), "apply_host: H2D");
+    FDP_CUDA(cudaEventRecord(h->ev_in[j], h->cin), "apply_host: event");
+  }
+  double* ws = static_cast<double*>(h->e2e_ws);
+  for (int j = 0; j < units; ++j) {
+    FDP_CUDA(cudaStreamWaitEvent(st, h->ev_in[j], 0), "apply_host: wait");
+    if (batch == 1) {
+      long long toff = 0;
+      for (int k = 0; k < blk(j) && k < h->D; ++k) toff += 2 * Npad(h->vel[k]);
+      FDP_CUDA(enqueue_unit(h, blk(j), h->e2e_r, h->e2e_s, ws + toff, st), "apply_host: apply");
+    } else {
+      FDP_CUDA(enqueue_block(h, h->e2e_r + (long long)j * h->size, h->e2e_s + (long long)j * h->size, 1,
+                             ws, st, nullptr), "apply_host: apply");
+    }
+    FDP_CUDA(cudaEventRecord(h->ev_done[j], st), "apply_host: event");
+    FDP_CUDA(cudaStreamWaitEvent(h->cout, h->ev_done[j], 0), "apply_host: wait");
+    long long off, len;
+    span(j, &off, &len);
+    FDP_CUDA(cudaMemcpyAsync(s_host + off, h->e2e_s + off, (size_t)len * sizeof(double),
+                             cudaMemcpyDeviceToHost, h->cout), "apply_host: D2H");
+  }
+  if (use_graph) {
+    // join the copy-out branch back into the origin stream, end the capture, launch
+    FDP_CUDA(cudaEventRecord(h->ev_in[0], h->cout), "apply_host: join");
+    FDP_CUDA(cudaStreamWaitEvent(st, h->ev_in[0], 0), "apply_host: join");
+    cudaGraph_t g = nullptr;
+    FDP_CUDA(cudaStreamEndCapture(st, &g), "apply_host: capture end");
+    cudaError_t e = cudaGraphInstantiate(&h->e2e_graph, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+      h->e2e_graph = nullptr;
+      return cuda_fail(e, "apply_host: instantiate");
+    }
+    h->e2e_gr = r_host;
+    h->e2e_gs = s_host;
+    FDP_CUDA(cudaGraphLaunch(h->e2e_graph, origin), "apply_host: graph launch");
+    FDP_CUDA(cudaStreamSynchronize(origin), "apply_host: sync");
+    return FDP_OK;
+  }
+  FDP_CUDA(cudaStreamSynchronize(h->cout), "apply_host: sync");
+  return FDP_OK;
+}
+
+extern "C" void* fdp_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  cudaError_t e = cudaMallocHost(&p, bytes ? bytes : 1);
+  if (e != cudaSuccess) {
+    cuda_fail(e, "fdp_host_alloc");
+    return nullptr;
+  }
+  return p;
+}
+
+extern "C" fdp_status fdp_host_free(void* p) {
+  if (!p) return FDP_OK;
+  FDP_CUDA(cudaFreeHost(p), "fdp_host_free");
   return FDP_OK;
 }
 

@@ -142,6 +142,28 @@ def test_graph_replay_and_host_e2e():
     assert rel(sh, ref.apply(rh)) < TOL
 
 
+@pytest.mark.parametrize("cid,batch", [(1, 1), (2, 1), (3, 1), (1, 3), (3, 2)])
+def test_host_e2e_pipeline(cid, batch):
+    """block_precond_apply_host's copy/compute pipeline (per block at batch 1, per item above)
+    with pinned (fdp.host_empty) and pageable buffers, repeated calls, vs the oracle."""
+    w, od, gd = _both(cid)
+    dv = dq = None
+    if w.variable_nu:
+        dv, dq = ospaces.nu_scalings(od, synth.viscosity)
+    P = fdp.build_block(gd, dscale_vel=dv, dscale_pres=dq)
+    ref = oprec.BlockPrecond(od, dv, dq)
+    rng = np.random.default_rng(cid + 10 * batch)
+    for pinned in (True, False):
+        for _ in range(2):
+            r = rng.standard_normal((batch, od.n_total))
+            rh = fdp.host_empty(r.shape) if pinned else np.empty_like(r)
+            rh[...] = r
+            sh = fdp.host_empty(r.shape) if pinned else np.empty_like(r)
+            P.apply_host(rh, sh, batch=batch)
+            for b in range(batch):
+                assert rel(sh[b], ref.apply(r[b])) < TOL
+
+
 def test_errors_are_reported():
     w, od, gd = _both(1)
     P = fdp.build_block(gd)
