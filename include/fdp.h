@@ -254,6 +254,25 @@ fdp_status iga_separable_fit(int D, const int32_t* nq, const double* const* c, i
 fdp_status fd_operator_diagonal(fdp_fd h, double* out);
 fdp_status kron_op_diagonal(fdp_kron h, double* out);
 
+/* ---- Device-resident MINRES (NEXT-1): the Paige-Saunders scalar recurrence on the GPU,
+ * so whole iterations can be captured in a CUDA graph with no host synchronisation ----
+ * fdp_vec_lincomb_dev: out = k[0] x + k[1] y + k[2] z, coefficients read from DEVICE memory k
+ * (3 doubles); a term with coefficient exactly 0 (or a NULL vector) is skipped, so stale
+ * vectors of a finished solve are never read into the result.
+ * fdp_minres_scalars(phase, state, hist, hist_cap, stream): one thread on `stream` updates the
+ * device `state` (>= 32 doubles):
+ *   [0] beta1 [1] beta [2] oldb [3] dbar [4] epsln [5] phibar [6] cs [7] sn [8] alfa (caller's
+ *   v.y) [9] dot (caller's r.P r) [10] itn [11] done [12] itn at convergence [13] tol (caller)
+ *   [14] error flag (P not positive definite) [16..18] k_v [19..21] k_y1 [22..24] k_y2
+ *   [25..27] k_w [28..30] k_x (lincomb_dev coefficient triples).
+ * phase 0 = init from dot = r.P r; 1 = iteration start (k_v = 1/beta, k_y1 = -beta/oldb);
+ * 2 = after alfa (k_y2 = -alfa/beta); 3 = after dot (rotation, k_w, k_x = phi, stopping test
+ * phibar/beta1 <= tol sets done and itn-at-convergence; hist[itn] = phibar/beta1 when hist != NULL
+ * and itn < hist_cap). After `done`, every coefficient that would change x is 0. */
+fdp_status fdp_vec_lincomb_dev(const double* coef, const double* x, const double* y,
+                               const double* z, double* out, int64_t n, void* stream);
+fdp_status fdp_minres_scalars(int phase, double* state, double* hist, int hist_cap, void* stream);
+
 /* ---- Arnoldi helpers for GMRES (Saad & Schultz) ----
  * V: m device vectors of length n with stride ldv >= n (V_j = V + j*ldv).
  * fdp_vec_multidot: h[j] = V_j . w for j < m into device h; deterministic (fixed grid, fixed

@@ -78,6 +78,8 @@ def _load():
         "iga_separable_fit": (i32, [i32, vp, ctypes.POINTER(vp), i32, ctypes.c_double, vp, vp, vp]),
         "fd_operator_diagonal": (i32, [vp, vp]),
         "kron_op_diagonal": (i32, [vp, vp]),
+        "fdp_vec_lincomb_dev": (i32, [vp, vp, vp, vp, vp, i64, vp]),
+        "fdp_minres_scalars": (i32, [i32, vp, vp, i32, vp]),
         "fdp_host_alloc": (vp, [sz]),
         "fdp_host_free": (i32, [vp]),
         "fdp_vec_multidot_workspace_bytes": (sz, [i32]),
@@ -342,6 +344,20 @@ def vec_lincomb(a, x, b, y, c, z, out, stream=None):
                                None if z is None else _dev(z, "z"), _dev(out, "out"), out.numel(),
                                _stream(stream)))
     return out
+
+
+def vec_lincomb_dev(k, x, y, z, out, stream=None):
+    """out = k[0] x + k[1] y + k[2] z, k a 3-element cuda tensor (zero terms skipped)."""
+    _check(lib.fdp_vec_lincomb_dev(_dev(k, "k"), _dev(x, "x"), None if y is None else _dev(y, "y"),
+                                   None if z is None else _dev(z, "z"), _dev(out, "out"), out.numel(),
+                                   _stream(stream)))
+    return out
+
+
+def minres_scalars(phase: int, state, hist=None, stream=None):
+    """fdp_minres_scalars: the MINRES scalar recurrence on the device (state layout in fdp.h)."""
+    _check(lib.fdp_minres_scalars(phase, _dev(state, "state"), None if hist is None else _dev(hist, "hist"),
+                                  0 if hist is None else hist.numel(), _stream(stream)))
 
 
 class _PinnedBuffer:

@@ -2174,6 +2174,27 @@ extern "C" fdp_status block_tri_apply(fdp_block h, int variant, const fdp_kron* 
   return FDP_OK;
 }
 
+extern "C" fdp_status fdp_vec_lincomb_dev(const double* coef, const double* x, const double* y,
+                                          const double* z, double* out, int64_t n, void* stream) {
+  if (n < 0) return fail(FDP_ERR_SHAPE, "fdp_vec_lincomb_dev: n < 0");
+  if (n == 0) return FDP_OK;
+  if (!is_device_ptr(coef) || !is_device_ptr(x) || !is_device_ptr(out) || (y && !is_device_ptr(y)) ||
+      (z && !is_device_ptr(z)))
+    return fail(FDP_ERR_INVALID_ARG, "fdp_vec_lincomb_dev: device pointers required");
+  FDP_CUDA(launch_lincomb_dev(coef, x, y, z, out, n, static_cast<cudaStream_t>(stream)), "fdp_vec_lincomb_dev");
+  return FDP_OK;
+}
+
+extern "C" fdp_status fdp_minres_scalars(int phase, double* state, double* hist, int hist_cap,
+                                         void* stream) {
+  if (phase < 0 || phase > 3 || hist_cap < 0) return fail(FDP_ERR_INVALID_ARG, "fdp_minres_scalars: bad phase");
+  if (!is_device_ptr(state) || (hist && !is_device_ptr(hist)))
+    return fail(FDP_ERR_INVALID_ARG, "fdp_minres_scalars: device pointers required");
+  FDP_CUDA(launch_minres_scalars(phase, state, hist, hist_cap, static_cast<cudaStream_t>(stream)),
+           "fdp_minres_scalars");
+  return FDP_OK;
+}
+
 // ------------------------------------------------------------------------------------------------
 // Arnoldi helpers (GMRES orthogonalization, NEXT-2)
 // ------------------------------------------------------------------------------------------------

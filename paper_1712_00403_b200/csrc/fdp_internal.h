@@ -157,6 +157,9 @@ cudaError_t launch_multidot(const double* V, long long ldv, int m, const double*
                             double* h, double* scratch, cudaStream_t s);
 cudaError_t launch_gemv(const double* V, long long ldv, int m, const double* h, double alpha,
                         double* w, double beta, long long n, cudaStream_t s);
+cudaError_t launch_lincomb_dev(const double* k, const double* x, const double* y, const double* z,
+                               double* out, long long n, cudaStream_t s);
+cudaError_t launch_minres_scalars(int phase, double* state, double* hist, int hist_cap, cudaStream_t s);
 cudaError_t launch_partsum(const PartSum& ps, double* y, double beta, long long n, cudaStream_t s);
 
 // Vector kernels (vec.cu)

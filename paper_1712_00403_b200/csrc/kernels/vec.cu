@@ -55,6 +55,103 @@ __global__ void lincomb_kernel(double a, const double* x, double b, const double
   }
 }
 
+// out = k[0] x + k[1] y + k[2] z with the coefficients read from device memory; a term whose
+// coefficient is exactly 0 is skipped (its vector is not read), as is a NULL vector
+__global__ void lincomb_dev_kernel(const double* __restrict__ k, const double* x, const double* y,
+                                   const double* z, double* out, long long n) {
+  const double a = k[0], b = y ? k[1] : 0.0, c = z ? k[2] : 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double v = a != 0.0 ? a * x[i] : 0.0;
+    if (b != 0.0) v = fma(b, y[i], v);
+    if (c != 0.0) v = fma(c, z[i], v);
+    out[i] = v;
+  }
+}
+
+// Paige-Saunders MINRES scalar recurrence on the device (one thread); state layout in fdp.h
+__global__ void minres_scalars_kernel(int phase, double* __restrict__ s, double* __restrict__ hist,
+                                      int hist_cap) {
+  enum { BETA1, BETA, OLDB, DBAR, EPSLN, PHIBAR, CS, SN, ALFA, DOT, ITN, DONE, ITN_DONE, TOL,
+         ERR, KV = 16, KY1 = 19, KY2 = 22, KW = 25, KX = 28 };
+  if (phase == 0) {  // init: DOT = r1 . P r1
+    const double d = s[DOT];
+    if (d < 0.0) s[ERR] = 1.0;
+    const double b1 = sqrt(fmax(d, 0.0));
+    s[BETA1] = b1;
+    s[BETA] = b1;
+    s[PHIBAR] = b1;
+    s[OLDB] = s[DBAR] = s[EPSLN] = 0.0;
+    s[CS] = -1.0;
+    s[SN] = 0.0;
+    s[ITN] = 0.0;
+    s[DONE] = b1 == 0.0 ? 1.0 : 0.0;
+    s[ITN_DONE] = 0.0;
+    return;
+  }
+  if (phase == 1) {  // iteration start: v = y / beta, y -= (beta / oldb) r1 (itn >= 2)
+    const double itn = s[ITN] + 1.0;
+    s[ITN] = itn;
+    const bool live = s[DONE] == 0.0;
+    s[KV] = live ? 1.0 / s[BETA] : 0.0;
+    s[KV + 1] = s[KV + 2] = 0.0;
+    s[KY1] = 1.0;
+    s[KY1 + 1] = (live && itn >= 2.0) ? -s[BETA] / s[OLDB] : 0.0;
+    s[KY1 + 2] = 0.0;
+    return;
+  }
+  if (phase == 2) {  // after alfa = v . y: y -= (alfa / beta) r2
+    const bool live = s[DONE] == 0.0;
+    s[KY2] = 1.0;
+    s[KY2 + 1] = live ? -s[ALFA] / s[BETA] : 0.0;
+    s[KY2 + 2] = 0.0;
+    return;
+  }
+  // phase 3: after DOT = r2 . P r2 -- the plane rotation, w and x coefficients, stopping test
+  const bool live = s[DONE] == 0.0;
+  if (!live) {
+    s[KW] = s[KW + 1] = s[KW + 2] = 0.0;
+    s[KX] = 1.0;
+    s[KX + 1] = s[KX + 2] = 0.0;
+    return;
+  }
+  const double d = s[DOT];
+  if (d < 0.0) s[ERR] = 1.0;
+  const double alfa = s[ALFA];
+  const double oldb = s[BETA];
+  const double beta = sqrt(fmax(d, 0.0));
+  const double cs = s[CS], sn = s[SN], dbar = s[DBAR];
+  const double oldeps = s[EPSLN];
+  const double delta = cs * dbar + sn * alfa;
+  const double gbar = sn * dbar - cs * alfa;
+  const double epsln = sn * beta;
+  const double dbar2 = -cs * beta;
+  const double gamma = fmax(hypot(gbar, beta), 2.220446049250313e-16);
+  const double cs2 = gbar / gamma, sn2 = beta / gamma;
+  const double phi = cs2 * s[PHIBAR];
+  const double phibar = sn2 * s[PHIBAR];
+  s[OLDB] = oldb;
+  s[BETA] = beta;
+  s[EPSLN] = epsln;
+  s[DBAR] = dbar2;
+  s[CS] = cs2;
+  s[SN] = sn2;
+  s[PHIBAR] = phibar;
+  s[KW] = 1.0 / gamma;
+  s[KW + 1] = -oldeps / gamma;
+  s[KW + 2] = -delta / gamma;
+  s[KX] = 1.0;
+  s[KX + 1] = phi;
+  s[KX + 2] = 0.0;
+  const int itn = (int)s[ITN];
+  const double rel = phibar / s[BETA1];
+  if (hist && itn < hist_cap) hist[itn] = rel;
+  if (rel <= s[TOL]) {
+    s[DONE] = 1.0;
+    s[ITN_DONE] = itn;
+  }
+}
+
 __global__ void partsum_kernel(const __grid_constant__ PartSum ps, double* __restrict__ y,
                                double beta, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -167,6 +264,19 @@ cudaError_t launch_dot(const double* x, const double* y, long long n, double* re
 }
 
 int dot_scratch_doubles() { return kDotBlocks; }
+
+cudaError_t launch_lincomb_dev(const double* k, const double* x, const double* y, const double* z,
+                               double* out, long long n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 8);
+  lincomb_dev_kernel<<<blocks, 256, 0, s>>>(k, x, y, z, out, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_minres_scalars(int phase, double* state, double* hist, int hist_cap, cudaStream_t s) {
+  minres_scalars_kernel<<<1, 1, 0, s>>>(phase, state, hist, hist_cap);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_lincomb(double a, const double* x, double b, const double* y, double c,
                            const double* z, double* out, long long n, cudaStream_t s) {

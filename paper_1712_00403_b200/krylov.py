@@ -27,7 +27,8 @@ import math
 import numpy as np
 
 from . import (FDP_IGA_INTERIOR, FDP_IGA_NITSCHE, KronOp, iga_mixed, iga_quadrature,
-               iga_univariate, vec_dot, vec_gemv, vec_lincomb, vec_multidot)
+               iga_univariate, minres_scalars, vec_dot, vec_gemv, vec_lincomb, vec_lincomb_dev,
+               vec_multidot)
 
 
 def _spaces(D, disc, p):
@@ -222,6 +223,95 @@ def minres(apply_A, apply_P, b, tol: float = 1e-8, maxit: int = 20000):
         if phibar / beta1 <= tol:
             return x.clone(), itn, hist
     return x.clone(), maxit, hist
+
+
+_DEV_MINRES = {}
+
+
+def minres_device(apply_A, apply_P, b, tol: float = 1e-8, maxit: int = 20000, unroll: int = 6):
+    """MINRES with the scalar recurrence on the GPU (fdp_minres_scalars): `unroll` whole
+    iterations (operator, preconditioner, dots, recurrence, vector updates) are captured into one
+    CUDA graph and replayed; the host reads the `done` flag once per replay. The same arithmetic
+    and stopping rule as ``minres``; iterations after convergence leave x untouched (their
+    coefficients are 0), so the result and the reported count are exactly those of the
+    converged step. apply_A / apply_P must be capturable (direct launches, no inner graph
+    replay). unroll is a multiple of 6 so the r (period 2) and w (period 3) buffer rotations of
+    the recurrence return to the captured roles. Returns (x, iterations, history)."""
+    import torch
+    assert unroll % 6 == 0
+    n = b.numel()
+    dev = b.device
+    # bound methods are new objects on every attribute access: key them by (instance, function)
+    fid = lambda f: (id(getattr(f, "__self__", f)), getattr(getattr(f, "__func__", f), "__qualname__", ""))
+    key = (n, str(dev), unroll, fid(apply_A), fid(apply_P))
+    ent = _DEV_MINRES.get(key)
+    if ent is None:
+        _DEV_MINRES.clear()
+        vecs = [torch.zeros(n, dtype=torch.float64, device=dev) for _ in range(8)]
+        state = torch.zeros(32, dtype=torch.float64, device=dev)
+        hist = torch.zeros(maxit + 1, dtype=torch.float64, device=dev)
+        ent = {"vecs": vecs, "state": state, "hist": hist, "graph": None}
+        _DEV_MINRES[key] = ent
+    x, r1, r2, y, v, w, w1, w2 = ent["vecs"]
+    state, hist = ent["state"], ent["hist"]
+    if hist.numel() < maxit + 1:
+        hist = ent["hist"] = torch.zeros(maxit + 1, dtype=torch.float64, device=dev)
+        ent["graph"] = None
+    for t in (x, w, w1, w2):
+        t.zero_()
+    r1.copy_(b)
+    r2.copy_(b)
+    apply_P(r1, y)
+    state.zero_()
+    state[13] = tol
+    vec_dot(r1, y, state[9:10])
+    minres_scalars(0, state)
+    kv, ky1, ky2, kw, kx = (state[16:19], state[19:22], state[22:25], state[25:28], state[28:31])
+
+    def iterations():
+        R1, R2, W, W1, W2 = r1, r2, w, w1, w2
+        for _ in range(unroll):
+            minres_scalars(1, state)
+            vec_lincomb_dev(kv, y, None, None, v)           # v = y / beta
+            apply_A(v, y)                                   # y = A v
+            vec_lincomb_dev(ky1, y, R1, None, y)            # y -= (beta/oldb) r1
+            vec_dot(v, y, state[8:9])                       # alfa
+            minres_scalars(2, state)
+            vec_lincomb_dev(ky2, y, R2, None, y)            # y -= (alfa/beta) r2
+            R1, R2 = R2, R1
+            R2.copy_(y)
+            apply_P(R2, y)
+            vec_dot(R2, y, state[9:10])                     # beta^2
+            minres_scalars(3, state, hist)
+            W1, W2, W = W2, W, W1
+            vec_lincomb_dev(kw, v, W1, W2, W)               # w = (v - oldeps w1 - delta w2) / gamma
+            vec_lincomb_dev(kx, x, W, None, x)              # x += phi w
+
+    if ent["graph"] is None:
+        s = torch.cuda.Stream(device=dev)
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        # warm-up outside capture would advance the recurrence: snapshot and restore the state
+        snap = [t.clone() for t in (x, r1, r2, y, v, w, w1, w2, state)]
+        with torch.cuda.stream(s):
+            iterations()
+        torch.cuda.current_stream().wait_stream(s)
+        for t, c in zip((x, r1, r2, y, v, w, w1, w2, state), snap):
+            t.copy_(c)
+        with torch.cuda.graph(g):
+            iterations()
+        ent["graph"] = g
+    g = ent["graph"]
+    while True:
+        g.replay()
+        st = state[10:13].tolist()   # itn, done, itn_done (the one host read per replay)
+        if st[1] != 0.0 or st[0] >= maxit:
+            break
+    if state[14].item() != 0.0:
+        raise ValueError("preconditioner is not positive definite")
+    its = int(st[2]) if st[1] != 0.0 else maxit
+    h = [1.0] + hist[1:its + 1].tolist()
+    return x.clone(), its, h
 
 
 _GM_BUFFERS = {}

@@ -54,8 +54,17 @@ for cid in cids:
     b.record()
     torch.cuda.synchronize()
     pc = a.elapsed_time(b) / 10
+    # device-resident recurrence (6 iterations per graph replay)
+    ap = lambda r, z: P.apply(r, z, workspace=ws)
+    krylov.minres_device(gop._apply_direct, ap, fd_)
+    torch.cuda.synchronize()
+    a.record()
+    xd, its_d, _ = krylov.minres_device(gop._apply_direct, ap, fd_)
+    b.record()
+    torch.cuda.synchronize()
     line = {"config": cid, "dofs": gop.n, "iterations": its, "gpu_solve_ms": ms, "true_rel_residual": res,
-            "matvec_ms": mv, "precond_ms": pc, "setup_s": setup}
+            "matvec_ms": mv, "precond_ms": pc, "setup_s": setup,
+            "device_resident_iterations": its_d, "device_resident_solve_ms": a.elapsed_time(b)}
     if oracle:
         from oracle import minres as om, precond as op_, spaces as os_, stokes as ost
         odisc = os_.build(w.dim, w.disc, w.p, w.n_el)

@@ -128,3 +128,31 @@ def test_gpu_minres_iteration_counts(cid):
     n = min(len(h_o), len(h_g))
     assert max(abs(a - b) / a for a, b in zip(h_o[:n], h_g[:n])) < 1e-6
     assert rel(x_g.cpu().numpy(), x_o) < 1e-6
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3])
+def test_gpu_minres_device_resident(cid):
+    """minres_device (scalar recurrence on the GPU, 6 iterations per graph replay): the oracle's
+    iteration count, its residual history, and the host-driven GPU MINRES's solution."""
+    w = synth.CONFIGS[cid]
+    nu_o = ostokes.config3_nu_terms(w.dim) if w.variable_nu else None
+    nu_g = synth.viscosity_separable(w.dim) if w.variable_nu else None
+    op = ostokes.StokesCube(w.dim, w.disc, w.p, w.n_el, nu_terms=nu_o)
+    od = ospaces.build(w.dim, w.disc, w.p, w.n_el)
+    gd = fdp.discretization(w.dim, w.disc, w.p, w.n_el)
+    dv = dq = None
+    if w.variable_nu:
+        dv, dq = ospaces.nu_scalings(od, synth.viscosity)
+    f = ostokes.project_rhs(synth.rhs(w.seed, op.n, 1)[0], op.sizes[-1])
+    x_o, it_o, h_o = ominres.minres(op.matvec, f, oprec.BlockPrecond(od, dv, dq).apply)
+    gop = krylov.StokesOperator(w.dim, w.disc, w.p, w.n_el, nu_terms=nu_g)
+    P = fdp.build_block(gd, dscale_vel=dv, dscale_pres=dq)
+    ws = P.workspace(1)
+    ap = lambda r, z: P.apply(r, z, workspace=ws)
+    for _ in range(2):  # second call replays the captured graph
+        x_g, it_g, h_g = krylov.minres_device(gop._apply_direct, ap, dev(f))
+        assert it_g == it_o, (cid, it_g, it_o)
+        assert max(abs(a - b) / a for a, b in zip(h_o, h_g)) < 1e-6
+        assert rel(x_g.cpu().numpy(), x_o) < 1e-6
+    x_h, it_h, _ = krylov.minres(gop.apply, ap, dev(f))
+    assert it_h == it_g and rel(x_g.cpu().numpy(), x_h.cpu().numpy()) < 1e-10
