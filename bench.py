@@ -64,7 +64,8 @@ def workload_config(cid, w, n_total, batch_total, gpus, flush):
         "preconditioner": "P_D^G (D_V=nu, D_Q=1/nu at dofs)" if w.variable_nu else "P_D",
         "dofs_per_rhs": n_total,
         "global_batch": batch_total,
-        "parallelism": ("slab-a2a" if cid == 5 and gpus > 1 else "batch-shard" if cid == 4 else "replicas") + f"x{gpus}",
+        "parallelism": (("slab-" + os.environ.get("FDP_SLAB_EXCHANGE", "peer")) if cid == 5 and gpus > 1
+                        else "batch-shard" if cid == 4 else "replicas") + f"x{gpus}",
         "l2": flush,
         "rhs": f"numpy default_rng(seed={w.seed}).standard_normal, FP64",
     }
@@ -209,9 +210,29 @@ def main():
 
     # config 5 at N > 1: slab decomposition with NCCL all-to-all exchanges (strong scaling)
     slab = cid == 5 and world > 1
+    exchange = None
     if slab:
         from paper_1712_00403_b200 import dist as fdist
-        SB = fdist.SlabBlockPrecond(P)
+        # default: exchanges fused into the contraction epilogues (peer stores over NVLink,
+        # DESIGN.md §9); FDP_SLAB_EXCHANGE=nccl selects the NCCL all-to-all baseline
+        exchange = os.environ.get("FDP_SLAB_EXCHANGE", "peer")
+        SB = None
+        if exchange == "peer":
+            try:
+                SB = fdist.PeerSlabBlockPrecond(P)
+                ok = 1.0
+            except Exception as e:  # no CUDA IPC / peer access between the ranks' GPUs
+                print(f"peer-store exchange unavailable ({e}); using NCCL all-to-all", file=sys.stderr)
+                ok = 0.0
+            flag = torch.tensor([ok], device=f"cuda:{dev}")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)  # every rank takes the same path
+            if flag.item() < 1.0:
+                if SB is not None:
+                    SB.close()
+                SB = None
+                exchange = "nccl"
+        if SB is None:
+            SB = fdist.SlabBlockPrecond(P)
     # batch per rank: config 4 shards its 8 RHS across ranks; others replicate one RHS stream
     if slab:
         items = [0]
@@ -369,7 +390,7 @@ def main():
     roof_kind = "per-launch CUDA events of K1 inside the apply graph"
     if slab:
         # K1 algorithmic flops of one full apply / G per rank over the whole step time
-        # (a lower bound: includes packing and the two NCCL all-to-all exchanges)
+        # (a lower bound: includes the two exchanges)
         fl = sum(4.0 * float(np.prod(d)) * sum(d) for d in gd.comp_dims)
         achieved = fl / world / (dev_ms_max / args.steps * 1e-3) / 1e12
         per_kind[0] = tot_ms = 1.0
@@ -419,7 +440,7 @@ def main():
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "apply/s",
                 "h2d_bytes_per_step": int(r_host.nbytes), "d2h_bytes_per_step": int(r_host.nbytes),
-                "api": ("pinned H2D + SlabBlockPrecond.apply (NCCL all-to-all) + D2H + sync" if slab
+                "api": (f"pinned H2D + slab apply ({exchange} exchange) + D2H + sync" if slab
                         else "block_precond_apply_host (pinned host buffers, H2D+apply+D2H+sync)")},
         "gpu_launches": launches * args.steps,
         "clocks": clocks,

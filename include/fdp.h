@@ -225,6 +225,42 @@ size_t block_tri_workspace_bytes(fdp_block P, int variant, const fdp_kron* B, co
 fdp_status block_tri_apply(fdp_block P, int variant, const fdp_kron* B, const fdp_kron* BT,
                            const double* r, double* s, void* workspace, void* stream);
 
+/* ---- Peer-store slab exchange (SURVEY.md §8(e) "fused variant") ----
+ * Same phases and slab partition as fd_apply_slab / kron_mass_apply_slab, but each exchange is
+ * fused into the contraction before it: the kernel's epilogue stores every element directly into
+ * the destination rank's buffer (peer memory mapped with fdp_peer_open, P2P over NVLink), so there
+ * is no pack / unpack pass and no separate collective. `peers`: DEVICE array of nranks pointers.
+ *  phase 0: in = this rank's z-slab (n1, n2, nz) [pre-scaled by dscale]; modes 1-2; element
+ *           (i1, i2, i3) lands in peers[h] = the y-slab buffer (n1, ny_h, n3) of the rank h owning
+ *           i2, at (i1, i2 - y0_h, z0 + i3).
+ *  phase 1: in = this rank's y-slab buffer (filled by every rank's phase 0); the mode-3 triple
+ *           (Lambda^{-1} included); element (i1, i2, i3) lands in peers[g] = the z-slab buffer
+ *           (n1, n2, nz_g) of the rank g owning i3, at (i1, y0 + i2, i3 - z0_g).
+ *  phase 2: in = this rank's z-slab buffer (filled by every rank's phase 1); modes 2-1 backward
+ *           [post-scaled by dscale] -> out (n1, n2, nz).
+ * Between phases every rank must pass fdp_peer_barrier. workspace: fd_slab_workspace_bytes /
+ * kron_mass_slab_workspace_bytes. out unused in phases 0-1, peers unused in phase 2. */
+fdp_status fd_apply_slab_peer(fdp_fd h, int phase, int nranks, int rank, const double* in,
+                              double* out, double* const* peers, const double* dscale,
+                              void* workspace, void* stream);
+fdp_status kron_mass_apply_slab_peer(fdp_mass h, int phase, int nranks, int rank,
+                                     const double* in, double* out, double* const* peers,
+                                     const double* dscale, void* workspace, void* stream);
+/* Cross-rank barrier on `stream` (one warp): increments *counter (device, this rank's epoch),
+ * release-stores it (system scope, after a system fence that orders this rank's earlier peer
+ * stores) into flags[o][rank] for every rank o, then acquire-spins until flags[rank][0..nranks-1]
+ * all reach it. flags: DEVICE array of nranks pointers to each rank's nranks-slot uint64 flag
+ * array (zero-initialised, mapped with fdp_peer_open). nranks <= 32. Graph-capturable. */
+fdp_status fdp_peer_barrier(unsigned long long* const* flags, unsigned long long* counter,
+                            int nranks, int rank, void* stream);
+/* Device buffers shareable with peer processes over CUDA IPC: fdp_peer_alloc (cudaMalloc,
+ * zeroed) returns the pointer and a 64-byte handle; another process maps it with fdp_peer_open
+ * (lazy peer access) and unmaps with fdp_peer_close; the owner frees with fdp_peer_free. */
+fdp_status fdp_peer_alloc(size_t bytes, int device, void** dev_ptr, void* ipc_handle);
+fdp_status fdp_peer_open(const void* ipc_handle, int device, void** dev_ptr);
+fdp_status fdp_peer_close(void* dev_ptr);
+fdp_status fdp_peer_free(void* dev_ptr);
+
 /* ---- Geometry-aware pencils (§6 P:1048-1059 and Appendix; NEXT-3) ----
  * Host setup helpers (no device work). The pencils themselves are iga_mixed with weights at the
  * quadrature points (K_d = int tau_d b' b', M_d = int mu_d b b), solved by fd_setup / fd_apply.

@@ -93,6 +93,13 @@ def _load():
         "fdp_vec_lincomb": (i32, [ctypes.c_double, vp, ctypes.c_double, vp, ctypes.c_double, vp, vp, i64, vp]),
         "fd_slab_workspace_bytes": (sz, [vp, i32, i32]),
         "fd_apply_slab": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, vp]),
+        "fd_apply_slab_peer": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp]),
+        "kron_mass_apply_slab_peer": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp]),
+        "fdp_peer_barrier": (i32, [vp, vp, i32, i32, vp]),
+        "fdp_peer_alloc": (i32, [sz, i32, ctypes.POINTER(vp), vp]),
+        "fdp_peer_open": (i32, [vp, i32, ctypes.POINTER(vp)]),
+        "fdp_peer_close": (i32, [vp]),
+        "fdp_peer_free": (i32, [vp]),
         "kron_mass_slab_workspace_bytes": (sz, [vp, i32, i32]),
         "kron_mass_apply_slab": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, vp]),
         "block_precond_profile_read": (i32, [vp, i32, vp, vp, vp, vp]),
@@ -451,6 +458,86 @@ def kron_mass_apply_slab(h, phase: int, nranks: int, rank: int, x_in, x_out, dsc
                                     None if dscale is None else _dev(dscale, "dscale"),
                                     None if workspace is None else _dev(workspace, "workspace"),
                                     _stream(stream)))
+
+
+def fd_apply_slab_peer(h, phase: int, nranks: int, rank: int, x_in, x_out, peers, dscale, workspace,
+                       stream=None):
+    """libfdp peer-store slab phase (exchange fused into the epilogue); see include/fdp.h.
+    peers: int64 cuda tensor of nranks device addresses (or None in phase 2)."""
+    _check(lib.fd_apply_slab_peer(h.h, phase, nranks, rank, _dev(x_in, "in"),
+                                  None if x_out is None else _dev(x_out, "out"),
+                                  None if peers is None else peers.data_ptr(),
+                                  None if dscale is None else _dev(dscale, "dscale"),
+                                  _dev(workspace, "workspace"), _stream(stream)))
+
+
+def kron_mass_apply_slab_peer(h, phase: int, nranks: int, rank: int, x_in, x_out, peers, dscale,
+                              workspace, stream=None):
+    _check(lib.kron_mass_apply_slab_peer(h.h, phase, nranks, rank, _dev(x_in, "in"),
+                                         None if x_out is None else _dev(x_out, "out"),
+                                         None if peers is None else peers.data_ptr(),
+                                         None if dscale is None else _dev(dscale, "dscale"),
+                                         None if workspace is None else _dev(workspace, "workspace"),
+                                         _stream(stream)))
+
+
+def peer_barrier(flag_ptrs, counter, nranks: int, rank: int, stream=None):
+    """fdp_peer_barrier: flag_ptrs int64 cuda tensor of nranks flag-array addresses."""
+    _check(lib.fdp_peer_barrier(flag_ptrs.data_ptr(), counter.data_ptr(), nranks, rank, _stream(stream)))
+
+
+class PeerBuffer:
+    """A device buffer shareable over CUDA IPC (fdp_peer_alloc); .handle is 64 bytes."""
+
+    def __init__(self, nbytes: int, device: int = 0):
+        p = ctypes.c_void_p()
+        hbuf = ctypes.create_string_buffer(64)
+        _check(lib.fdp_peer_alloc(nbytes, device, ctypes.byref(p), hbuf))
+        self.ptr = p.value
+        self.handle = hbuf.raw
+        self.nbytes = nbytes
+        self.device = device
+
+    def tensor(self, n: int, dtype=None):
+        """Zero-copy float64 (or given dtype) cuda tensor view of the first n elements."""
+        import torch
+        dt = torch.float64 if dtype is None else dtype
+        return _tensor_from_ptr(self.ptr, n, dt, self.device)
+
+    def close(self):
+        if getattr(self, "ptr", None):
+            lib.fdp_peer_free(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def peer_open(handle: bytes, device: int = 0) -> int:
+    p = ctypes.c_void_p()
+    _check(lib.fdp_peer_open(ctypes.create_string_buffer(handle, 64), device, ctypes.byref(p)))
+    return p.value
+
+
+def peer_close(ptr: int):
+    _check(lib.fdp_peer_close(ptr))
+
+
+def _tensor_from_ptr(ptr: int, n: int, dtype, device: int):
+    """A torch cuda tensor aliasing n elements at a device address (no ownership)."""
+    import torch
+
+    class _CAI:
+        def __init__(self):
+            typestr = {torch.float64: "<f8", torch.int64: "<i8", torch.uint64: "<u8"}[dtype]
+            self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
+                                             "version": 3, "strides": None}
+
+    with torch.cuda.device(device):
+        return torch.as_tensor(_CAI(), device=f"cuda:{device}")
 
 
 class KronMass:

@@ -1612,6 +1612,184 @@ extern "C" fdp_status fd_apply_slab(fdp_fd h, int phase, int nranks, int rank, c
   return FDP_OK;
 }
 
+// ---- peer-store slab exchange: the exchanges are fused into the epilogues of
+// the contraction that precedes them; data crosses NVLink as the kernels' own stores ----
+static void set_scatter(ModeProb& p, double* const* peers, int G, int na, int n1, int qoff, int a0,
+                        int a1, int q0, int q1) {
+  p.peers = peers;
+  p.sc_G = G;
+  p.sc_na = na;
+  p.sc_n1 = n1;
+  p.sc_qoff = qoff;
+  p.sc_a0 = a0;
+  p.sc_a1 = a1;
+  p.sc_q0 = q0;
+  p.sc_q1 = q1;
+}
+
+extern "C" fdp_status fd_apply_slab_peer(fdp_fd h, int phase, int nranks, int rank, const double* in,
+                                         double* out, double* const* peers, const double* dscale,
+                                         void* workspace, void* stream) {
+  if (!h) return fail(FDP_ERR_INVALID_ARG, "fd_apply_slab_peer: NULL handle");
+  if (h->D != 3) return fail(FDP_ERR_UNSUPPORTED, "fd_apply_slab_peer: D must be 3");
+  if (nranks < 1 || nranks > 32 || rank < 0 || rank >= nranks || phase < 0 || phase > 2)
+    return fail(FDP_ERR_INVALID_ARG, "fd_apply_slab_peer: bad phase / rank");
+  const long long n1 = h->n[0], n2 = h->n[1], n3 = h->n[2];
+  long long z0, nz, y0, ny;
+  part_range(n3, nranks, rank, &z0, &nz);
+  part_range(n2, nranks, rank, &y0, &ny);
+  if ((phase == 1 ? ny : nz) == 0) return FDP_OK;
+  if (!is_device_ptr(in) || !is_device_ptr(workspace) || (phase == 2 && !is_device_ptr(out)) ||
+      (phase < 2 && !is_device_ptr(peers)) || (dscale && !is_device_ptr(dscale)))
+    return fail(FDP_ERR_INVALID_ARG, "fd_apply_slab_peer: device pointers required");
+  DeviceGuard dg(h->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double* T1 = static_cast<double*>(workspace);
+  double* T2 = T1 + n1 * n2 * nz;
+  if (phase == 0) {
+    // modes 1, 2 on the z-slab; mode 2 stores element (i1, i2, i3) straight into the y-slab
+    // buffer (n1, ny_h, n3) of the rank h owning i2, at (i1, i2 - y0_h, z0 + i3)
+    const double* src = in;
+    if (dscale) {
+      FDP_CUDA(launch_scale(in, T2, dscale, n1 * n2 * nz, 1, 0, 0, s), "fd_apply_slab_peer: prescale");
+      src = T2;
+    }
+    FDP_CUDA(run1(slab_prob(h, 0, true, src, T1, 1, n2 * nz, EPI_NONE, nullptr, nullptr), h->cfg[0], true, s),
+             "fd_apply_slab_peer: mode 1");
+    ModeProb p = slab_prob(h, 1, true, T1, nullptr, n1, nz, EPI_NONE, nullptr, nullptr);
+    set_scatter(p, peers, nranks, (int)n2, (int)n1, (int)z0, 1, 0, 0, 1);
+    FDP_CUDA(run1(p, h->cfg[1], false, s), "fd_apply_slab_peer: mode 2 + exchange");
+  } else if (phase == 1) {
+    // the mode-3 triple on the y-slab; the last contraction stores element (i1, i2, i3) straight
+    // into the z-slab buffer (n1, n2, nz_g) of the rank g owning i3, at (i1, y0 + i2, i3 - z0_g)
+    const double* lam1 = h->lamc[1] + y0;
+    const bool fuse = std::getenv("FDP_NO_FUSE") == nullptr && std::getenv("FDP_NO_SMALL") == nullptr &&
+                      n3 <= kSmallMaxN && h->cfg[2].tiles_n == 1;
+    if (fuse) {
+      ModeProb p = slab_prob(h, 2, true, in, nullptr, n1 * ny, 1, EPI_FUSED, nullptr, lam1);
+      set_scatter(p, peers, nranks, (int)n3, (int)n1, (int)y0, (int)n2, 0, 1, 0);
+      FDP_CUDA(run1(p, h->cfg[2], false, s), "fd_apply_slab_peer: fused mode 3 + exchange");
+    } else {
+      FDP_CUDA(run1(slab_prob(h, 2, true, in, T1, n1 * ny, 1, EPI_LAMBDA, nullptr, lam1), h->cfg[2], false, s),
+               "fd_apply_slab_peer: mode 3 fwd");
+      ModeProb p = slab_prob(h, 2, false, T1, nullptr, n1 * ny, 1, EPI_NONE, nullptr, nullptr);
+      set_scatter(p, peers, nranks, (int)n3, (int)n1, (int)y0, (int)n2, 0, 1, 0);
+      FDP_CUDA(run1(p, h->cfg[2], false, s), "fd_apply_slab_peer: mode 3 bwd + exchange");
+    }
+  } else {
+    FDP_CUDA(run1(slab_prob(h, 1, false, in, T2, n1, nz, EPI_NONE, nullptr, nullptr), h->cfg[1], false, s),
+             "fd_apply_slab_peer: mode 2 bwd");
+    FDP_CUDA(run1(slab_prob(h, 0, false, T2, out, 1, n2 * nz, dscale ? EPI_SCALE : EPI_NONE, dscale, nullptr),
+                  h->cfg[0], true, s),
+             "fd_apply_slab_peer: mode 1 bwd");
+  }
+  return FDP_OK;
+}
+
+extern "C" fdp_status kron_mass_apply_slab_peer(fdp_mass h, int phase, int nranks, int rank,
+                                                const double* in, double* out, double* const* peers,
+                                                const double* dscale, void* workspace, void* stream) {
+  if (!h) return fail(FDP_ERR_INVALID_ARG, "kron_mass_apply_slab_peer: NULL handle");
+  if (h->D != 3) return fail(FDP_ERR_UNSUPPORTED, "kron_mass_apply_slab_peer: D must be 3");
+  if (nranks < 1 || nranks > 32 || rank < 0 || rank >= nranks || phase < 0 || phase > 2)
+    return fail(FDP_ERR_INVALID_ARG, "kron_mass_apply_slab_peer: bad phase / rank");
+  const long long n1 = h->n[0], n2 = h->n[1], n3 = h->n[2];
+  long long z0, nz, y0, ny;
+  part_range(n3, nranks, rank, &z0, &nz);
+  part_range(n2, nranks, rank, &y0, &ny);
+  if ((phase == 1 ? ny : nz) == 0) return FDP_OK;
+  if (!is_device_ptr(in) || (phase < 2 && (!is_device_ptr(workspace) || !is_device_ptr(peers))) ||
+      (phase == 2 && !is_device_ptr(out)) || (dscale && !is_device_ptr(dscale)))
+    return fail(FDP_ERR_INVALID_ARG, "kron_mass_apply_slab_peer: device pointers required");
+  DeviceGuard dg(h->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto mode = [&](int d, const double* src, double* dst, long long P, long long Q, const double* pre) {
+    MassMode m{};
+    m.in = src;
+    m.out = dst;
+    m.Lb = h->Lb[d];
+    m.invd = h->invd[d];
+    m.Mb = h->Mb[d];
+    m.pre = pre;
+    m.N = P * h->n[d] * Q;
+    m.bs = 0;
+    m.P = (int)P;
+    m.n = h->n[d];
+    m.Q = (int)Q;
+    m.batch = 1;
+    m.band = h->band[d];
+    return launch_mass_mode(m, s);
+  };
+  double* T = static_cast<double*>(workspace);
+  if (phase == 0) {
+    FDP_CUDA(mode(0, in, T, 1, n2 * nz, dscale), "kron_mass_apply_slab_peer: mode 1");
+    FDP_CUDA(mode(1, T, T, n1, nz, nullptr), "kron_mass_apply_slab_peer: mode 2");
+    ScatterDesc sd{peers, nranks, (int)n2, (int)n1, (int)z0, 1, 0, 0, 1};
+    FDP_CUDA(launch_slab_scatter(T, sd, (int)nz, 0, s), "kron_mass_apply_slab_peer: exchange");
+  } else if (phase == 1) {
+    FDP_CUDA(mode(2, in, T, n1 * ny, 1, nullptr), "kron_mass_apply_slab_peer: mode 3");
+    ScatterDesc sd{peers, nranks, (int)n3, (int)n1, (int)y0, (int)n2, 0, 1, 0};
+    FDP_CUDA(launch_slab_scatter(T, sd, (int)ny, 1, s), "kron_mass_apply_slab_peer: exchange");
+  } else if (dscale) {
+    FDP_CUDA(launch_scale(in, out, dscale, n1 * n2 * nz, 1, 0, 0, s), "kron_mass_apply_slab_peer: postscale");
+  } else if (in != out) {
+    FDP_CUDA(cudaMemcpyAsync(out, in, (size_t)(n1 * n2 * nz) * sizeof(double), cudaMemcpyDeviceToDevice, s),
+             "kron_mass_apply_slab_peer: copy");
+  }
+  return FDP_OK;
+}
+
+extern "C" fdp_status fdp_peer_barrier(unsigned long long* const* flags, unsigned long long* counter,
+                                       int nranks, int rank, void* stream) {
+  if (nranks < 1 || nranks > 32 || rank < 0 || rank >= nranks)
+    return fail(FDP_ERR_INVALID_ARG, "fdp_peer_barrier: bad rank");
+  if (!is_device_ptr(flags) || !is_device_ptr(counter))
+    return fail(FDP_ERR_INVALID_ARG, "fdp_peer_barrier: device pointers required");
+  FDP_CUDA(launch_peer_barrier(flags, counter, nranks, rank, static_cast<cudaStream_t>(stream)),
+           "fdp_peer_barrier");
+  return FDP_OK;
+}
+
+extern "C" fdp_status fdp_peer_alloc(size_t bytes, int device, void** dev_ptr, void* ipc_handle) {
+  if (!dev_ptr || !ipc_handle) return fail(FDP_ERR_INVALID_ARG, "fdp_peer_alloc: NULL argument");
+  *dev_ptr = nullptr;
+  DeviceGuard dg(device);
+  void* p = nullptr;
+  FDP_CUDA(cudaMalloc(&p, bytes ? bytes : 8), "fdp_peer_alloc: cudaMalloc");
+  cudaError_t e = cudaMemset(p, 0, bytes ? bytes : 8);
+  cudaIpcMemHandle_t hd;
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&hd, p);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    return cuda_fail(e, "fdp_peer_alloc: IPC handle");
+  }
+  std::memcpy(ipc_handle, &hd, sizeof(hd));
+  *dev_ptr = p;
+  return FDP_OK;
+}
+
+extern "C" fdp_status fdp_peer_open(const void* ipc_handle, int device, void** dev_ptr) {
+  if (!ipc_handle || !dev_ptr) return fail(FDP_ERR_INVALID_ARG, "fdp_peer_open: NULL argument");
+  *dev_ptr = nullptr;
+  DeviceGuard dg(device);
+  cudaIpcMemHandle_t hd;
+  std::memcpy(&hd, ipc_handle, sizeof(hd));
+  FDP_CUDA(cudaIpcOpenMemHandle(dev_ptr, hd, cudaIpcMemLazyEnablePeerAccess), "fdp_peer_open");
+  return FDP_OK;
+}
+
+extern "C" fdp_status fdp_peer_close(void* dev_ptr) {
+  if (!dev_ptr) return FDP_OK;
+  FDP_CUDA(cudaIpcCloseMemHandle(dev_ptr), "fdp_peer_close");
+  return FDP_OK;
+}
+
+extern "C" fdp_status fdp_peer_free(void* dev_ptr) {
+  if (!dev_ptr) return FDP_OK;
+  FDP_CUDA(cudaFree(dev_ptr), "fdp_peer_free");
+  return FDP_OK;
+}
+
 extern "C" size_t kron_mass_slab_workspace_bytes(fdp_mass h, int nranks, int rank) {
   if (!h || h->D != 3 || nranks < 1 || rank < 0 || rank >= nranks) return 0;
   long long z0, nz;

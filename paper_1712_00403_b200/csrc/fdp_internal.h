@@ -53,7 +53,28 @@ struct ModeProb {
   int cta_begin;          // first CTA of this problem in the grouped grid
   int fd_work;            // host-side accounting only: 1 = FD contraction, 0 = dense P_Q pass
   int ctas;               // small-n kernel: CTAs assigned to this problem
+  // Peer-store scatter (slab exchange fused into the epilogue): when peers != NULL,
+  // output element (GEMM row m, column a) of a batch-1, non-KMAJ problem is stored at
+  // peers[o] + r + sc_n1 * ((a - lo_o) * (sc_a0 + sc_a1 * len_o) + (q + sc_qoff) * (sc_q0 + sc_q1 * len_o))
+  // with r = m % sc_n1, q = m / sc_n1, and [lo_o, lo_o + len_o) the share of rank o that owns a
+  // under the even split of sc_na over sc_G ranks (first sc_na % sc_G ranks one extra).
+  double* const* peers;
+  int sc_G, sc_na, sc_n1, sc_qoff, sc_a0, sc_a1, sc_q0, sc_q1;
 };
+
+#ifdef __CUDACC__
+__device__ __forceinline__ double* scatter_ptr(const ModeProb& pb, long long m, int a) {
+  const int G = pb.sc_G, na = pb.sc_na;
+  const int q = na / G, rem = na % G;
+  const int o = (q == 0 || a < rem * (q + 1)) ? a / (q + 1) : rem + (a - rem * (q + 1)) / q;
+  const int lo = o * q + (o < rem ? o : rem);
+  const int len = q + (o < rem ? 1 : 0);
+  const long long r = m % pb.sc_n1, qq = m / pb.sc_n1;
+  return pb.peers[o] + r +
+         (long long)pb.sc_n1 * ((long long)(a - lo) * (pb.sc_a0 + pb.sc_a1 * len) +
+                                (qq + pb.sc_qoff) * (pb.sc_q0 + pb.sc_q1 * len));
+}
+#endif
 
 // Quotient a / b for the Lambda^{-1} epilogues (b = Lambda > 0, normal): hardware reciprocal
 // approximation (~2^-23), one Newton step (~2^-46) and one Markstein correction of the quotient
@@ -174,6 +195,20 @@ int iga_mixed_build(int deg_t, int alpha_t, int flags_t, int deg_r, int alpha_r,
 int iga_quadrature_build(int n_el, int q, double* x, double* w);
 
 // Slab pack (dir 0: z-slab -> piece buffer) / unpack (dir 1, optional scale on the z-slab).
+// Peer scatter-copy (pressure blocks of the peer-store slab exchange): src is the local tensor
+// with the split axis `a` (extent na) and the other axis `q` (extent nq), i1 fastest; a_outer = 0:
+// src (n1, na, nq), a_outer = 1: src (n1, nq, na). Destinations as ModeProb's scatter fields.
+struct ScatterDesc {
+  double* const* peers;
+  int G, na, n1, qoff, a0, a1, q0, q1;
+};
+cudaError_t launch_slab_scatter(const double* src, const ScatterDesc& sd, int nq, int a_outer,
+                                cudaStream_t s);
+// Cross-GPU barrier over peer flags (one warp): bumps the caller's epoch counter, release-stores
+// it into slot `rank` of every rank's flag array (flags[o], device pointers, mapped via IPC) and
+// acquire-spins until all G slots of its own array reach it (system-scope fences).
+cudaError_t launch_peer_barrier(unsigned long long* const* flags, unsigned long long* counter,
+                                int G, int rank, cudaStream_t s);
 cudaError_t launch_slab_copy(const double* src, double* dst, int n1, int n2, int nz, int G, int dir,
                              const double* scale, cudaStream_t s);
 

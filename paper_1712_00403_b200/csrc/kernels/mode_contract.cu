@@ -219,7 +219,7 @@ mode_contract_kernel(const __grid_constant__ ModeGroupT<G> grp) {
         const int a = n0 + 8 * j + 2 * fc + h;
         if (a < ncols) {
           double v = acc[i][j][h];
-          double* yp = Y + row_off + (long long)P * a;
+          double* yp = pb.peers ? scatter_ptr(pb, m, a) : Y + row_off + (long long)P * a;
           if (epi == EPI_LAMBDA) v = pad_row ? 0.0 : fdp_div(v, lrow + pb.lamcol[a]);
           else if (epi == EPI_SCALE) v = v * pb.scale[sidx + (long long)P * a];
           else if (epi == EPI_AXPBY) v = pb.alpha * v + (pb.beta != 0.0 ? pb.beta * *yp : 0.0);

@@ -362,7 +362,17 @@ __device__ __forceinline__ void tile_compute_store(const ModeProb& pb, const Geo
     __syncwarp();
     return;
   }
-  if (pb.vy && KMAJ) {
+  if (pb.peers) {  // peer-store scatter of the slab exchange (scalar stores)
+    if (mv) {
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int a = 8 * j + 2 * fc + h;
+          if (a < g.nout) *scatter_ptr(pb, m, a) = acc[j][h];
+        }
+    }
+  } else if (pb.vy && KMAJ) {
     // (a, a+1) adjacent in a row of an even-stride tensor
     if (mv) {
 #pragma unroll

@@ -45,7 +45,77 @@ __global__ void slab_copy_kernel(const double* __restrict__ src, double* __restr
   }
 }
 
+__global__ void slab_scatter_kernel(const double* __restrict__ src, const ScatterDesc sd, int nq,
+                                    int a_outer) {
+  const long long total = (long long)sd.n1 * sd.na * nq;
+  const int G = sd.G, na = sd.na;
+  const int qd = na / G, rem = na % G;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i1 = (int)(e % sd.n1);
+    const long long t = e / sd.n1;
+    int a, q;
+    if (a_outer) {
+      q = (int)(t % nq);
+      a = (int)(t / nq);
+    } else {
+      a = (int)(t % na);
+      q = (int)(t / na);
+    }
+    const int o = (qd == 0 || a < rem * (qd + 1)) ? a / (qd + 1) : rem + (a - rem * (qd + 1)) / qd;
+    const int lo = o * qd + (o < rem ? o : rem);
+    const int len = qd + (o < rem ? 1 : 0);
+    sd.peers[o][i1 + (long long)sd.n1 * ((long long)(a - lo) * (sd.a0 + sd.a1 * len) +
+                                         (long long)(q + sd.qoff) * (sd.q0 + sd.q1 * len))] = src[e];
+  }
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void peer_barrier_kernel(unsigned long long* const* flags, unsigned long long* counter,
+                                    int G, int rank) {
+  const int lane = threadIdx.x;
+  unsigned long long epoch = 0;
+  if (lane == 0) {
+    epoch = *counter + 1;
+    *counter = epoch;
+  }
+  epoch = __shfl_sync(0xffffffffu, epoch, 0);
+  __threadfence_system();  // this rank's earlier peer stores (previous kernels) before the signal
+  if (lane < G) st_release_sys(flags[lane] + rank, epoch);
+  if (lane < G) {
+    const unsigned long long* mine = flags[rank] + lane;
+    while (ld_acquire_sys(mine) < epoch) {
+    }
+  }
+  __syncwarp();
+  __threadfence_system();
+}
+
 }  // namespace
+
+cudaError_t launch_slab_scatter(const double* src, const ScatterDesc& sd, int nq, int a_outer,
+                                cudaStream_t s) {
+  const long long total = (long long)sd.n1 * sd.na * nq;
+  if (total == 0) return cudaSuccess;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+  slab_scatter_kernel<<<blocks, 256, 0, s>>>(src, sd, nq, a_outer);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_peer_barrier(unsigned long long* const* flags, unsigned long long* counter,
+                                int G, int rank, cudaStream_t s) {
+  if (G < 1 || G > 32) return cudaErrorInvalidValue;
+  peer_barrier_kernel<<<1, 32, 0, s>>>(flags, counter, G, rank);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_slab_copy(const double* src, double* dst, int n1, int n2, int nz, int G, int dir,
                              const double* scale, cudaStream_t s) {

@@ -151,3 +151,16 @@ def test_batch_shard_config4():
         shards = [fdist.batch_shard(8, world, r) for r in range(world)]
         assert sorted(sum(shards, [])) == list(range(8))
         assert len(set(len(s) for s in shards)) == 1
+
+
+def _handles(rank, world):
+    hs = [bytes([rank, i]) * 32 for i in range(3)]  # stand-ins for 64-byte IPC handles
+    allh = fdist.exchange_handles(hs)
+    return all(allh[r][i] == bytes([r, i]) * 32 for r in range(world) for i in range(3))
+
+
+def test_peer_handle_exchange_gloo():
+    """The host plumbing of the peer-store exchange: every rank gets every rank's handles in rank
+    order (world size 2, gloo)."""
+    res = _run(_handles)
+    assert res == {0: True, 1: True}

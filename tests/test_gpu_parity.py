@@ -321,3 +321,77 @@ def test_slab_block_precond_nccl_single_rank():
     finally:
         if created:
             tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("G", [1, 2, 3, 5, 8])
+@pytest.mark.parametrize("case", [(3, "RT", 2, 6), (3, "TH", 2, 5)])
+@pytest.mark.parametrize("env", [{}, {"FDP_NO_SMALL": "1"}])
+def test_slab_peer_store_emulated(G, case, env, monkeypatch):
+    """Peer-store slab exchange (epilogue scatter into the owners' buffers) for G
+    virtual ranks on one device (buffers poisoned with NaN: every element must be written
+    exactly where the next phase reads it); small and big contraction paths."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    from paper_1712_00403_b200 import dist as fdist
+    D, disc, p, n_el = case
+    od = ospaces.build(D, disc, p, n_el)
+    gd = fdp.discretization(D, disc, p, n_el)
+    P = fdp.build_block(gd)
+    r = np.random.default_rng(G).standard_normal(od.n_total)
+    s = fdist.emulate_slab_apply_peer(P, dev(r), G).cpu().numpy()
+    ref = oprec.BlockPrecond(od).apply(r)
+    assert np.all(np.isfinite(s))
+    assert rel(s, ref) < TOL
+
+
+def test_slab_peer_store_config3_size():
+    from paper_1712_00403_b200 import dist as fdist
+    w, od, gd = _both(3)
+    P = fdp.build_block(gd)
+    r = synth.rhs(w.seed, od.n_total, 1)[0]
+    s = fdist.emulate_slab_apply_peer(P, dev(r), 8).cpu().numpy()
+    assert rel(s, oprec.BlockPrecond(od).apply(r)) < TOL
+
+
+def test_peer_slab_block_precond_single_rank():
+    """PeerSlabBlockPrecond through a real process group of one rank: IPC-allocated buffers,
+    the peer-store phases and the system-scope barrier kernel (signalling itself), applied
+    repeatedly (epoch counter) and captured in a CUDA graph."""
+    import os
+    import socket
+    import torch.distributed as tdist
+    from paper_1712_00403_b200 import dist as fdist
+    s0 = socket.socket()
+    s0.bind(("127.0.0.1", 0))
+    port = s0.getsockname()[1]
+    s0.close()
+    os.environ.update({"MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
+    created = False
+    if not tdist.is_initialized():
+        tdist.init_process_group("gloo", rank=0, world_size=1)
+        created = True
+    try:
+        w, od, gd = _both(3)
+        P = fdp.build_block(gd)
+        SB = fdist.PeerSlabBlockPrecond(P)
+        ref = oprec.BlockPrecond(od)
+        rng = np.random.default_rng(5)
+        for _ in range(3):
+            r = rng.standard_normal(od.n_total)
+            rt = dev(r)
+            st = torch.empty_like(rt)
+            SB.apply(rt, st)
+            assert rel(st.cpu().numpy(), ref.apply(r)) < TOL
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            SB.apply(rt, st)
+        r = rng.standard_normal(od.n_total)
+        rt.copy_(dev(r))
+        for _ in range(2):
+            g.replay()
+        torch.cuda.synchronize()
+        assert rel(st.cpu().numpy(), ref.apply(r)) < TOL
+        SB.close()
+    finally:
+        if created:
+            tdist.destroy_process_group()
