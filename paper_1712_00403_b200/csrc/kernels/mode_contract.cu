@@ -57,7 +57,7 @@ struct Smem {
   static constexpr size_t BYTES = sizeof(double) * STAGE * STAGES;
 };
 
-template <int MT, int NT, bool KMAJ, int G>
+template <int MT, int NT, bool KMAJ, int G, bool SC = false>
 __global__ void __launch_bounds__(THREADS)
 mode_contract_kernel(const __grid_constant__ ModeGroupT<G> grp) {
   using S = Smem<MT, NT, KMAJ>;
@@ -219,7 +219,9 @@ mode_contract_kernel(const __grid_constant__ ModeGroupT<G> grp) {
         const int a = n0 + 8 * j + 2 * fc + h;
         if (a < ncols) {
           double v = acc[i][j][h];
-          double* yp = pb.peers ? scatter_ptr(pb, m, a) : Y + row_off + (long long)P * a;
+          // SC (compile-time): peer-store scatter of the slab exchange; other launches keep the
+          // plain addressing (the scatter branch cost 5% on config 4 when always compiled in)
+          double* yp = SC ? scatter_ptr(pb, m, a) : Y + row_off + (long long)P * a;
           if (epi == EPI_LAMBDA) v = pad_row ? 0.0 : fdp_div(v, lrow + pb.lamcol[a]);
           else if (epi == EPI_SCALE) v = v * pb.scale[sidx + (long long)P * a];
           else if (epi == EPI_AXPBY) v = pb.alpha * v + (pb.beta != 0.0 ? pb.beta * *yp : 0.0);
@@ -236,11 +238,20 @@ cudaError_t launch_t(const ModeGroup* g, cudaStream_t s) {
   if (!g) {  // prepare: raise the dynamic shared-memory limit (outside any stream capture)
     cudaError_t e = cudaFuncSetAttribute(mode_contract_kernel<MT, NT, KMAJ, kSmallGroup>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES);
+    if (e == cudaSuccess && !KMAJ)
+      e = cudaFuncSetAttribute(mode_contract_kernel<MT, NT, false, kSmallGroup, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES);
     if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(mode_contract_kernel<MT, NT, KMAJ, kMaxGroup>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES);
   }
-  if (g->count <= kSmallGroup)
+  bool sc = false;
+  for (int i = 0; i < g->count; ++i) sc = sc || g->prob[i].peers != nullptr;
+  if (sc) {  // peer-store problems: batch 1, non-KMAJ, launched one at a time (run1)
+    if (KMAJ || g->count > kSmallGroup) return cudaErrorInvalidValue;
+    mode_contract_kernel<MT, NT, false, kSmallGroup, true><<<g->total_ctas, THREADS, S::BYTES, s>>>(
+        narrow_group<kSmallGroup>(*g));
+  } else if (g->count <= kSmallGroup)
     mode_contract_kernel<MT, NT, KMAJ, kSmallGroup><<<g->total_ctas, THREADS, S::BYTES, s>>>(
         narrow_group<kSmallGroup>(*g));
   else

@@ -117,7 +117,7 @@ __device__ __forceinline__ double ldx(const double* p) {
   return COHERENT ? __ldcg(p) : __ldg(p);
 }
 
-template <int NT, bool KMAJ>
+template <int NT, bool KMAJ, bool SC = false>
 __device__ __forceinline__ void tile_compute_store(const ModeProb& pb, const Geo& g,
                                                    const double* Ws, double* A, long long t,
                                                    int lane, unsigned long long* tr);
@@ -166,7 +166,7 @@ __device__ __forceinline__ void load_panel_async(const ModeProb& pb, const Geo& 
 
 // One 8-row tile: panel load (LDG -> STS, zero fill beyond n / M), DMMAs, epilogue.
 // COHERENT: the input was written earlier in the same launch (plane pipeline): L2-coherent loads.
-template <int NT, bool KMAJ, bool COHERENT>
+template <int NT, bool KMAJ, bool COHERENT, bool SC = false>
 __device__ __forceinline__ void do_tile(const ModeProb& pb, const Geo& g, const double* Ws,
                                         double* A, long long t, int lane,
                                         unsigned long long* tr) {
@@ -267,10 +267,10 @@ __device__ __forceinline__ void do_tile(const ModeProb& pb, const Geo& g, const 
   }
   __syncwarp();
   if (tr) tr[3] = gtimer();
-  tile_compute_store<NT, KMAJ>(pb, g, Ws, A, t, lane, tr);
+  tile_compute_store<NT, KMAJ, SC>(pb, g, Ws, A, t, lane, tr);
 }
 
-template <int NT, bool KMAJ>
+template <int NT, bool KMAJ, bool SC>
 __device__ __forceinline__ void tile_compute_store(const ModeProb& pb, const Geo& g,
                                                    const double* Ws, double* A, long long t,
                                                    int lane, unsigned long long* tr) {
@@ -362,7 +362,7 @@ __device__ __forceinline__ void tile_compute_store(const ModeProb& pb, const Geo
     __syncwarp();
     return;
   }
-  if (pb.peers) {  // peer-store scatter of the slab exchange (scalar stores)
+  if (SC) {  // peer-store scatter of the slab exchange (scalar stores)
     if (mv) {
 #pragma unroll
       for (int j = 0; j < NT; ++j)
@@ -409,7 +409,7 @@ __device__ __forceinline__ void tile_compute_store(const ModeProb& pb, const Geo
   if (tr) tr[5] = gtimer();
 }
 
-template <int NT, bool KMAJ, int G>
+template <int NT, bool KMAJ, int G, bool SC = false>
 __global__ void __launch_bounds__(STH, 1) mode_small_kernel(const __grid_constant__ ModeGroupT<G> grp) {
   using S = SS<NT>;
   extern __shared__ __align__(16) double sm[];
@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(STH, 1) mode_small_kernel(const __grid_constan
   const int gw = (blockIdx.x - pb.cta_begin) + pb.ctas * warp;
   const int nw = pb.ctas * SW;
   for (long long t = gw; t < pb.tiles_m; t += nw)
-    do_tile<NT, KMAJ, false>(pb, g, Ws, A, t, lane, (trace && lane == 0 && t == gw) ? trace : nullptr);
+    do_tile<NT, KMAJ, false, SC>(pb, g, Ws, A, t, lane, (trace && lane == 0 && t == gw) ? trace : nullptr);
 }
 
 // Prefetching variant: SWP = 8 warps per CTA, two panels per warp; the next tile's panel streams
@@ -593,6 +593,9 @@ cudaError_t launch_s(const ModeGroup* g, cudaStream_t s) {
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(mode_small_kernel<NT, KMAJ, kMaxGroup>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES);
+    if (e == cudaSuccess && !KMAJ)
+      e = cudaFuncSetAttribute(mode_small_kernel<NT, false, kSmallGroup, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES);
     if (e != cudaSuccess || bytes_prefetch<NT>() > 227 * 1024) return e;
     return cudaFuncSetAttribute(mode_small_pf_kernel<NT, KMAJ, kSmallGroup>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes_prefetch<NT>());
@@ -607,6 +610,15 @@ cudaError_t launch_s(const ModeGroup* g, cudaStream_t s) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  bool sc = false;
+  for (int i = 0; i < g->count; ++i) sc = sc || g->prob[i].peers != nullptr;
+  if (sc) {  // peer-store problems (slab exchange): non-KMAJ, single-buffered kernel
+    if (KMAJ || g->count > kSmallGroup) return cudaErrorInvalidValue;
+    cfg.blockDim = dim3(STH);
+    cfg.dynamicSmemBytes = S::BYTES;
+    return cudaLaunchKernelEx(&cfg, mode_small_kernel<NT, false, kSmallGroup, true>,
+                              narrow_group<kSmallGroup>(*g));
+  }
   if (g->count <= kSmallGroup) {
     const ModeGroupT<kSmallGroup> gs = narrow_group<kSmallGroup>(*g);
     if (pf) return cudaLaunchKernelEx(&cfg, mode_small_pf_kernel<NT, KMAJ, kSmallGroup>, gs);
