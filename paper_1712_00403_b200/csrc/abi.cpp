@@ -342,6 +342,22 @@ static void kron_diag_accumulate(int D, const int* n, const std::vector<const do
   }
 }
 
+extern "C" fdp_status iga_geometry_coeffs(int kind, int D, int k, int nq, const double* x,
+                                          double* c_out) {
+  const fdp_status st = geometry_coeffs_impl(kind, D, k, nq, x, c_out);
+  if (st == FDP_ERR_UNSUPPORTED) return fail(st, "iga_geometry_coeffs: the annulus map is 3D only");
+  if (st) return fail(st, "iga_geometry_coeffs: bad kind, k, nq or NULL pointer");
+  return FDP_OK;
+}
+
+extern "C" fdp_status iga_separable_fit(int D, const int32_t* nq, const double* const* c,
+                                        int max_sweeps, double tol, double* tau, double* mu,
+                                        int* sweeps) {
+  const fdp_status st = separable_fit_impl(D, nq, c, max_sweeps, tol, tau, mu, sweeps);
+  if (st) return fail(st, "iga_separable_fit: bad arguments or a sample <= 0 (logs undefined)");
+  return FDP_OK;
+}
+
 extern "C" fdp_status fd_operator_diagonal(fdp_fd h, double* out) {
   if (!h || !out) return fail(FDP_ERR_INVALID_ARG, "fd_operator_diagonal: NULL argument");
   std::fill(out, out + h->N, 0.0);

@@ -183,6 +183,11 @@ cudaError_t launch_lincomb_dev(const double* k, const double* x, const double* y
 cudaError_t launch_minres_scalars(int phase, double* state, double* hist, int hist_cap, cudaStream_t s);
 cudaError_t launch_partsum(const PartSum& ps, double* y, double beta, long long n, cudaStream_t s);
 
+// Geometry-aware setup (host_geo.cpp), wrapped by the C ABI in abi.cpp
+fdp_status geometry_coeffs_impl(int kind, int D, int k, int nq, const double* x, double* c_out);
+fdp_status separable_fit_impl(int D, const int32_t* nq, const double* const* c, int max_sweeps,
+                              double tol, double* tau, double* mu, int* sweeps);
+
 // Vector kernels (vec.cu)
 cudaError_t launch_dot(const double* x, const double* y, long long n, double* result,
                        double* scratch, cudaStream_t s);

@@ -10,7 +10,7 @@
 #include <cstring>
 #include <vector>
 
-#include "../../include/fdp.h"
+#include "fdp_internal.h"
 
 namespace {
 
@@ -47,8 +47,10 @@ double inverse3(const double J[3][3], double Ji[3][3]) {
 
 }  // namespace
 
-extern "C" fdp_status iga_geometry_coeffs(int kind, int D, int k, int nq, const double* x,
-                                          double* c_out) {
+namespace fdp {
+
+// Implementations behind the C ABI wrappers in abi.cpp (which set fdp_last_error).
+fdp_status geometry_coeffs_impl(int kind, int D, int k, int nq, const double* x, double* c_out) {
   if (kind != FDP_GEOM_IDENTITY && kind != FDP_GEOM_ANNULUS) return FDP_ERR_INVALID_ARG;
   if (D != 3 && !(D == 2 && kind == FDP_GEOM_IDENTITY)) return FDP_ERR_UNSUPPORTED;
   if (k < 0 || k >= D || nq < 1 || !x || !c_out) return FDP_ERR_INVALID_ARG;
@@ -75,9 +77,8 @@ extern "C" fdp_status iga_geometry_coeffs(int kind, int D, int k, int nq, const 
   return FDP_OK;
 }
 
-extern "C" fdp_status iga_separable_fit(int D, const int32_t* nq, const double* const* c,
-                                        int max_sweeps, double tol, double* tau, double* mu,
-                                        int* sweeps) {
+fdp_status separable_fit_impl(int D, const int32_t* nq, const double* const* c, int max_sweeps,
+                              double tol, double* tau, double* mu, int* sweeps) {
   if (D < 2 || D > 3 || !nq || !c || !tau || !mu || max_sweeps < 0) return FDP_ERR_INVALID_ARG;
   long long NQ = 1;
   int off[4] = {0, 0, 0, 0};
@@ -165,3 +166,5 @@ extern "C" fdp_status iga_separable_fit(int D, const int32_t* nq, const double* 
   if (sweeps) *sweeps = sw;
   return FDP_OK;
 }
+
+}  // namespace fdp
