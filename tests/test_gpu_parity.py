@@ -395,3 +395,30 @@ def test_peer_slab_block_precond_single_rank():
     finally:
         if created:
             tdist.destroy_process_group()
+
+
+@pytest.mark.slow
+def test_config5_full_size_residual():
+    """Config 5 (548 M dofs) at full size in the bench launch configuration: a single output of
+    an FD solve needs the whole solve, so the check is the property that holds at any size —
+    the Sylvester residual ||R_k x_k - b_k|| / ||b_k|| of every velocity block (R_k applied by the
+    oracle's Kronecker matvec with the oracle's own pencils) and ||P_Q x_p - b_p|| / ||b_p||
+    of the pressure block. Bound: eps * kappa(R) ~ 1e-16 * 1e7 (SURVEY App. A spectra)."""
+    from oracle import kron as okron
+    w, od, gd = _both(5)
+    b = synth.rhs(w.seed, od.n_total, 1)[0]
+    P = fdp.build_block(gd)
+    x = P.apply(dev(b)).cpu().numpy()
+    o = od.offsets()
+    for k, c in enumerate(od.comps):
+        xk, bk = x[o[k]:o[k + 1]], b[o[k]:o[k + 1]]
+        Rx = np.zeros_like(bk)
+        for d in range(3):
+            F = [c.Ks[e] if e == d else c.Ms[e] for e in range(3)]
+            Rx += c.coef[d] * okron.kron_matvec(list(reversed(F)), xk)
+        res = np.linalg.norm(Rx - bk) / np.linalg.norm(bk)
+        assert res < 1e-9, (k, res)
+        del Rx
+    xp, bp = x[o[3]:], b[o[3]:]
+    Mx = okron.kron_matvec(list(reversed(od.Mq)), xp)
+    assert np.linalg.norm(Mx - bp) / np.linalg.norm(bp) < 1e-12
