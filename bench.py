@@ -163,7 +163,7 @@ def run_reference(args, w, cid):
     line = {
         "impl": "reference", "metric": "preconditioner_applications_per_s", "value": value,
         "unit": "apply/s", "n_gpus": args.gpus, "steps": steps, "warmup": warm,
-        "ms_per_step": 1e3 * dt / steps, "higher_is_better": True, "scaling": "replicas",
+        "ms_per_step": 1e3 * dt / steps, "higher_is_better": True, "scaling": "strong" if cid in (4, 5) else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "dof_per_s": value * od.n_total,
         "config": workload_config(cid, w, od.n_total, 1, 1, "n/a (CPU)"),
