@@ -959,7 +959,9 @@ struct fdp_block_s {
   int64_t e2e_batch = 0;
   // host-buffer pipeline: copy-in / copy-out streams and per-unit events
   cudaStream_t cin = nullptr, cout = nullptr;
+  cudaStream_t cs[3] = {nullptr, nullptr, nullptr};  // per-component compute streams (batch 1)
   std::vector<cudaEvent_t> ev_in, ev_done;
+  cudaEvent_t ev_start = nullptr;
   // batch-1 pipeline over pinned buffers, captured once per (r_host, s_host) and replayed
   const double* e2e_gr = nullptr;
   double* e2e_gs = nullptr;
@@ -982,6 +984,9 @@ static void free_block(fdp_block h) {
   for (cudaEvent_t e : h->ev_in) cudaEventDestroy(e);
   for (cudaEvent_t e : h->ev_done) cudaEventDestroy(e);
   if (h->e2e_graph) cudaGraphExecDestroy(h->e2e_graph);
+  for (cudaStream_t c : h->cs)
+    if (c) cudaStreamDestroy(c);
+  if (h->ev_start) cudaEventDestroy(h->ev_start);
   if (h->cin) cudaStreamDestroy(h->cin);
   if (h->cout) cudaStreamDestroy(h->cout);
   delete h;
@@ -1333,8 +1338,50 @@ extern "C" fdp_status block_precond_apply(fdp_block h, const double* r, double* 
 static cudaError_t enqueue_unit(fdp_block h, int k, const double* r, double* s, double* T,
                                 cudaStream_t st) {
   if (k == h->D) {
-    return enqueue_mass(h->pres, FDP_MASS_INVERSE, r + h->off[k], s + h->off[k], h->size, h->dq, 1,
-                        st, nullptr);
+    const double* rq = r + h->off[k];
+    double* sq = s + h->off[k];
+    if (!h->pres_dense)  // banded per-mode solves
+      return enqueue_mass(h->pres, FDP_MASS_INVERSE, rq, sq, h->size, h->dq, 1, st, nullptr);
+    // dense per-mode inverses (C-9): three small-path passes rq -> T -> T' -> sq, with the
+    // D_Q^{-1/2} scalings as a pre-scale and the last pass's epilogue
+    const long long nq = h->pres->N;
+    double* T1 = T;
+    double* T2 = T + nq;
+    const double* dq = h->dall ? h->dall + h->off[k] : nullptr;
+    if (dq) {
+      cudaError_t e = launch_scale(rq, T2, dq, nq, 1, nq, nq, st);
+      if (e != cudaSuccess) return e;
+      rq = T2;
+    }
+    const TileCfg& vc = h->vel[0]->cfg[0];
+    for (int d = 0; d < h->D; ++d) {
+      long long P = 1, Q = 1;
+      for (int e = 0; e < d; ++e) P *= h->pres->n[e];
+      for (int e = d + 1; e < h->D; ++e) Q *= h->pres->n[e];
+      const bool last = d == h->D - 1;
+      ModeProb p{};
+      p.X = d == 0 ? rq : (d % 2 == 1 ? T1 : T2);
+      p.Y = last ? sq : (d % 2 == 0 ? T1 : T2);
+      p.W = h->Wq[d];
+      p.N = nq;
+      p.P = (int)P;
+      p.n = p.nout = h->pres->n[d];
+      p.Q = (int)Q;
+      p.batch = 1;
+      p.ldw = h->q_ldw[d];
+      p.n1 = p.n1v = h->pres->n[0];
+      p.xld = p.yld = h->pres->n[0];
+      p.epi = (last && dq) ? EPI_SCALE : EPI_NONE;
+      p.scale = (last && dq) ? dq : nullptr;
+      const int BM = kK1Warps * 8 * vc.MT;
+      p.tiles_m = (int)((P * Q + BM - 1) / BM);
+      p.tiles_n = h->q_tiles_n[d];
+      std::vector<ModeProb> probs{p};
+      std::vector<TileCfg> cfgs{h->vel[0]->cfg[d]};
+      cudaError_t e = launch_stage(probs, cfgs, d == 0, st, nullptr, nullptr);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
   }
   const fdp_fd_s* f = h->vel[k];
   const double* in = r + h->off[k];
@@ -1375,10 +1422,15 @@ extern "C" fdp_status block_precond_apply_host(fdp_block h, const double* r_host
   if (!h->cin) {
     FDP_CUDA(cudaStreamCreateWithFlags(&h->cin, cudaStreamNonBlocking), "apply_host: stream");
     FDP_CUDA(cudaStreamCreateWithFlags(&h->cout, cudaStreamNonBlocking), "apply_host: stream");
+    for (int k = 0; k < h->D; ++k)
+      FDP_CUDA(cudaStreamCreateWithFlags(&h->cs[k], cudaStreamNonBlocking), "apply_host: stream");
+    FDP_CUDA(cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming), "apply_host: event");
   }
   // Pipeline units: the D + 1 blocks of one item at batch 1, whole items at batch > 1. Copies in
   // run on cin, the applies on the caller's stream, copies out on cout, so unit j's compute
   // overlaps unit j+1's upload and unit j-1's download (PCIe is full duplex).
+  // batch 1: D + 1 units (velocity components in order, then the pressure block), batch > 1:
+  // the items
   const int units = batch == 1 ? h->D + 1 : (int)batch;
   while ((int)h->ev_in.size() < units) {
     cudaEvent_t a, b;
@@ -1413,13 +1465,13 @@ extern "C" fdp_status block_precond_apply_host(fdp_block h, const double* r_host
     st = h->cap;  // capture on the handle's private stream, then launch on the caller's
     FDP_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "apply_host: capture");
   }
-  // batch 1: the small pressure block goes first so its solve and download hide under the
-  // velocity uploads
-  auto blk = [&](int j) { return j == 0 ? h->D : j - 1; };
+  // batch 1: velocity components in order on the caller's stream (each apply uses every SM),
+  // the pressure block last, solved on its own stream (measured: pressure first or merged with
+  // the last component's copies is slower)
   auto span = [&](int j, long long* off, long long* len) {
     if (batch == 1) {
-      *off = h->off[blk(j)];
-      *len = h->off[blk(j) + 1] - h->off[blk(j)];
+      *off = h->off[j];
+      *len = h->off[j + 1] - h->off[j];
     } else {
       *off = (long long)j * h->size;
       *len = h->size;
@@ -1437,16 +1489,18 @@ extern "C" fdp_status block_precond_apply_host(fdp_block h, const double* r_host
   }
   double* ws = static_cast<double*>(h->e2e_ws);
   for (int j = 0; j < units; ++j) {
-    FDP_CUDA(cudaStreamWaitEvent(st, h->ev_in[j], 0), "apply_host: wait");
+    cudaStream_t us = (batch == 1 && j == h->D) ? h->cs[0] : st;
+    FDP_CUDA(cudaStreamWaitEvent(us, h->ev_in[j], 0), "apply_host: wait");
     if (batch == 1) {
       long long toff = 0;
-      for (int k = 0; k < blk(j) && k < h->D; ++k) toff += 2 * Npad(h->vel[k]);
-      FDP_CUDA(enqueue_unit(h, blk(j), h->e2e_r, h->e2e_s, ws + toff, st), "apply_host: apply");
+      for (int k = 0; k < j; ++k) toff += 2 * Npad(h->vel[k]);
+      FDP_CUDA(enqueue_unit(h, j, h->e2e_r, h->e2e_s, ws + toff, us), "apply_host: apply");
     } else {
       FDP_CUDA(enqueue_block(h, h->e2e_r + (long long)j * h->size, h->e2e_s + (long long)j * h->size, 1,
                              ws, st, nullptr), "apply_host: apply");
     }
-    FDP_CUDA(cudaEventRecord(h->ev_done[j], st), "apply_host: event");
+    FDP_CUDA(cudaEventRecord(h->ev_done[j], us), "apply_host: event");
+    if (us != st) FDP_CUDA(cudaStreamWaitEvent(st, h->ev_done[j], 0), "apply_host: join");
     FDP_CUDA(cudaStreamWaitEvent(h->cout, h->ev_done[j], 0), "apply_host: wait");
     long long off, len;
     span(j, &off, &len);
