@@ -261,6 +261,31 @@ fdp_status fdp_peer_open(const void* ipc_handle, int device, void** dev_ptr);
 fdp_status fdp_peer_close(void* dev_ptr);
 fdp_status fdp_peer_free(void* dev_ptr);
 
+/* ---- Sharded block apply (SURVEY.md §8(b) multi-GPU row, §8(e) config 5) ----
+ * A communicator for one block preconditioner P (D = 3) over nranks processes (one GPU each):
+ *   1. fdp_comm_create: allocates this rank's exchange buffers (per block a y-slab and a z-slab,
+ *      plus an nranks-slot barrier flag array) and writes its blob of CUDA IPC handles
+ *      (fdp_comm_blob_bytes(P, nranks) bytes, host memory owned by the caller);
+ *   2. the caller all-gathers the blobs (e.g. torch.distributed; rank-major, host);
+ *   3. fdp_comm_connect maps every peer's buffers (P2P over NVLink / NVSwitch).
+ * block_precond_apply_sharded then applies P_D^{-1} (or (P_D^G)^{-1}: the block's D scalings,
+ * sliced to the rank's slab) to this rank's slabs: r, s device, block_precond_sharded_size
+ * doubles laid out [u_1 z-slab | .. | u_D z-slab | p z-slab] (z-slab of block b: planes
+ * fdp_slab_range(n3_b, nranks, rank) of the block in vec order). All blocks' phases run with
+ * the exchanges fused into the epilogues (fd_apply_slab_peer, kron_mass_apply_slab_peer) and
+ * an fdp_peer_barrier after each phase; no host synchronisation, graph-capturable. Every rank
+ * must make the same calls in the same order. The communicator is not thread- or stream-safe.
+ * workspace: device, >= block_precond_sharded_workspace_bytes. */
+typedef struct fdp_comm_s* fdp_comm;
+size_t fdp_comm_blob_bytes(fdp_block P, int nranks);
+fdp_status fdp_comm_create(fdp_block P, int nranks, int rank, fdp_comm* out, void* blob);
+fdp_status fdp_comm_connect(fdp_comm c, const void* all_blobs);
+int64_t block_precond_sharded_size(fdp_block P, int nranks, int rank);
+size_t block_precond_sharded_workspace_bytes(fdp_block P, fdp_comm c);
+fdp_status block_precond_apply_sharded(fdp_block P, fdp_comm c, const double* r, double* s,
+                                       void* workspace, void* stream);
+fdp_status fdp_comm_destroy(fdp_comm c);
+
 /* ---- Geometry-aware pencils (§6 P:1048-1059 and Appendix; NEXT-3) ----
  * Host setup helpers (no device work). The pencils themselves are iga_mixed with weights at the
  * quadrature points (K_d = int tau_d b' b', M_d = int mu_d b b), solved by fd_setup / fd_apply.

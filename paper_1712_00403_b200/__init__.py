@@ -96,6 +96,13 @@ def _load():
         "fd_apply_slab_peer": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp]),
         "kron_mass_apply_slab_peer": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp]),
         "fdp_peer_barrier": (i32, [vp, vp, i32, i32, vp]),
+        "fdp_comm_blob_bytes": (sz, [vp, i32]),
+        "fdp_comm_create": (i32, [vp, i32, i32, ctypes.POINTER(vp), vp]),
+        "fdp_comm_connect": (i32, [vp, vp]),
+        "block_precond_sharded_size": (i64, [vp, i32, i32]),
+        "block_precond_sharded_workspace_bytes": (sz, [vp, vp]),
+        "block_precond_apply_sharded": (i32, [vp, vp, vp, vp, vp, vp]),
+        "fdp_comm_destroy": (i32, [vp]),
         "fdp_peer_alloc": (i32, [sz, i32, ctypes.POINTER(vp), vp]),
         "fdp_peer_open": (i32, [vp, i32, ctypes.POINTER(vp)]),
         "fdp_peer_close": (i32, [vp]),

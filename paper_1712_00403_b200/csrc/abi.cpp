@@ -1860,6 +1860,196 @@ extern "C" fdp_status fdp_peer_free(void* dev_ptr) {
   return FDP_OK;
 }
 
+// ---- C-level communicator for the sharded block apply (SURVEY.md §8(b) "multi-GPU") ----
+// Every rank owns, per block of the preconditioner, a y-slab receive buffer (exchange 1) and a
+// z-slab return buffer (exchange 2), plus an nranks-slot barrier flag array; their CUDA IPC
+// handles form the rank's blob, which the caller all-gathers (torch.distributed is plumbing).
+struct fdp_comm_s {
+  int nranks = 0, rank = 0, device = 0, nblocks = 0;
+  std::vector<void*> own;             // y-slab, z-slab per block, then flags (device)
+  std::vector<void*> opened;          // peer mappings to close
+  double** peers_y = nullptr;         // device: [block][rank] pointer tables
+  double** peers_z = nullptr;
+  unsigned long long** flag_ptrs = nullptr;  // device: [rank]
+  unsigned long long* counter = nullptr;
+  bool connected = false;
+};
+
+static void free_comm(fdp_comm c) {
+  if (!c) return;
+  for (void* p : c->opened) cudaIpcCloseMemHandle(p);
+  for (void* p : c->own) cudaFree(p);
+  cudaFree(c->peers_y);
+  cudaFree(c->peers_z);
+  cudaFree(c->flag_ptrs);
+  cudaFree(c->counter);
+  delete c;
+}
+
+static void block_dims(const fdp_block_s* P, int b, long long* n1, long long* n2, long long* n3) {
+  const int* n = b < P->D ? P->vel[b]->n : P->pres->n;
+  *n1 = n[0];
+  *n2 = n[1];
+  *n3 = n[2];
+}
+
+extern "C" size_t fdp_comm_blob_bytes(fdp_block P, int nranks) {
+  if (!P || P->D != 3 || nranks < 1) return 0;
+  return (size_t)(2 * (P->D + 1) + 1) * sizeof(cudaIpcMemHandle_t);
+}
+
+extern "C" fdp_status fdp_comm_create(fdp_block P, int nranks, int rank, fdp_comm* out, void* blob) {
+  if (!out || !blob) return fail(FDP_ERR_INVALID_ARG, "fdp_comm_create: NULL argument");
+  *out = nullptr;
+  if (!P) return fail(FDP_ERR_INVALID_ARG, "fdp_comm_create: NULL block");
+  if (P->D != 3) return fail(FDP_ERR_UNSUPPORTED, "fdp_comm_create: D must be 3");
+  if (nranks < 1 || nranks > 32 || rank < 0 || rank >= nranks)
+    return fail(FDP_ERR_INVALID_ARG, "fdp_comm_create: bad rank");
+  DeviceGuard dg(P->device);
+  std::unique_ptr<fdp_comm_s> c(new (std::nothrow) fdp_comm_s);
+  if (!c) return fail(FDP_ERR_OOM, "fdp_comm_create: host allocation");
+  c->nranks = nranks;
+  c->rank = rank;
+  c->device = P->device;
+  c->nblocks = P->D + 1;
+  fdp_comm raw = c.release();
+  auto alloc = [&](size_t bytes) -> fdp_status {
+    void* p = nullptr;
+    cudaIpcMemHandle_t hd;
+    fdp_status st = fdp_peer_alloc(bytes, raw->device, &p, &hd);
+    if (st) return st;
+    std::memcpy(static_cast<char*>(blob) + raw->own.size() * sizeof(hd), &hd, sizeof(hd));
+    raw->own.push_back(p);
+    return FDP_OK;
+  };
+  fdp_status st = FDP_OK;
+  for (int b = 0; b < raw->nblocks && !st; ++b) {
+    long long n1, n2, n3, y0, ny, z0, nz;
+    block_dims(P, b, &n1, &n2, &n3);
+    part_range(n2, nranks, rank, &y0, &ny);
+    part_range(n3, nranks, rank, &z0, &nz);
+    st = alloc((size_t)std::max(1LL, n1 * ny * n3) * sizeof(double));
+    if (!st) st = alloc((size_t)std::max(1LL, n1 * n2 * nz) * sizeof(double));
+  }
+  if (!st) st = alloc((size_t)nranks * sizeof(unsigned long long));
+  if (!st) st = dalloc(&raw->counter, 1);
+  if (!st) {
+    cudaError_t e = cudaMemset(raw->counter, 0, sizeof(unsigned long long));
+    if (e != cudaSuccess) st = cuda_fail(e, "fdp_comm_create: counter");
+  }
+  if (st) {
+    free_comm(raw);
+    return st;
+  }
+  *out = raw;
+  return FDP_OK;
+}
+
+extern "C" fdp_status fdp_comm_connect(fdp_comm c, const void* all_blobs) {
+  if (!c || !all_blobs) return fail(FDP_ERR_INVALID_ARG, "fdp_comm_connect: NULL argument");
+  if (c->connected) return fail(FDP_ERR_INVALID_ARG, "fdp_comm_connect: already connected");
+  DeviceGuard dg(c->device);
+  const int G = c->nranks, nb = c->nblocks, per = 2 * nb + 1;
+  std::vector<double*> py((size_t)nb * G), pz((size_t)nb * G);
+  std::vector<unsigned long long*> pf(G);
+  for (int r = 0; r < G; ++r) {
+    for (int i = 0; i < per; ++i) {
+      void* p = c->own[i];
+      if (r != c->rank) {  // map the peer's buffer (P2P over NVLink)
+        const char* hp = static_cast<const char*>(all_blobs) + ((size_t)r * per + i) * sizeof(cudaIpcMemHandle_t);
+        fdp_status st = fdp_peer_open(hp, c->device, &p);
+        if (st) return st;
+        c->opened.push_back(p);
+      }
+      if (i < 2 * nb) {
+        const int b = i / 2;
+        (i % 2 == 0 ? py : pz)[(size_t)b * G + r] = static_cast<double*>(p);
+      } else {
+        pf[r] = static_cast<unsigned long long*>(p);
+      }
+    }
+  }
+  fdp_status st;
+  if ((st = dalloc(&c->peers_y, py.size())) || (st = dalloc(&c->peers_z, pz.size())) ||
+      (st = dalloc(&c->flag_ptrs, pf.size())))
+    return st;
+  FDP_CUDA(cudaMemcpy(c->peers_y, py.data(), py.size() * sizeof(double*), cudaMemcpyHostToDevice), "fdp_comm_connect");
+  FDP_CUDA(cudaMemcpy(c->peers_z, pz.data(), pz.size() * sizeof(double*), cudaMemcpyHostToDevice), "fdp_comm_connect");
+  FDP_CUDA(cudaMemcpy(c->flag_ptrs, pf.data(), pf.size() * sizeof(void*), cudaMemcpyHostToDevice), "fdp_comm_connect");
+  c->connected = true;
+  return FDP_OK;
+}
+
+extern "C" int64_t block_precond_sharded_size(fdp_block P, int nranks, int rank) {
+  if (!P || P->D != 3 || nranks < 1 || rank < 0 || rank >= nranks) return 0;
+  long long tot = 0;
+  for (int b = 0; b <= P->D; ++b) {
+    long long n1, n2, n3, z0, nz;
+    block_dims(P, b, &n1, &n2, &n3);
+    part_range(n3, nranks, rank, &z0, &nz);
+    tot += n1 * n2 * nz;
+  }
+  return tot;
+}
+
+extern "C" size_t block_precond_sharded_workspace_bytes(fdp_block P, fdp_comm c) {
+  if (!P || !c || P->D != 3) return 0;
+  size_t m = 0;
+  for (int k = 0; k < P->D; ++k)
+    m = std::max(m, fd_slab_workspace_bytes(const_cast<fdp_fd>(P->vel[k]), c->nranks, c->rank));
+  m = std::max(m, kron_mass_slab_workspace_bytes(const_cast<fdp_mass>(P->pres), c->nranks, c->rank));
+  return m;
+}
+
+extern "C" fdp_status block_precond_apply_sharded(fdp_block P, fdp_comm c, const double* r, double* s,
+                                                  void* workspace, void* stream) {
+  if (!P || !c) return fail(FDP_ERR_INVALID_ARG, "block_precond_apply_sharded: NULL handle");
+  if (!c->connected) return fail(FDP_ERR_INVALID_ARG, "block_precond_apply_sharded: comm not connected");
+  if (!is_device_ptr(r) || !is_device_ptr(s) || !is_device_ptr(workspace))
+    return fail(FDP_ERR_INVALID_ARG, "block_precond_apply_sharded: device pointers required");
+  DeviceGuard dg(P->device);
+  const int G = c->nranks, g = c->rank, D = P->D;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // local layout [u_1 z-slab | .. | u_D z-slab | p z-slab]; D^{-1/2} slices of the P^G scalings
+  std::vector<long long> loff(D + 2, 0), goff(D + 1, 0);
+  for (int b = 0; b <= D; ++b) {
+    long long n1, n2, n3, z0, nz;
+    block_dims(P, b, &n1, &n2, &n3);
+    part_range(n3, G, g, &z0, &nz);
+    loff[b + 1] = loff[b] + n1 * n2 * nz;
+    goff[b] = n1 * n2 * z0;
+  }
+  auto dsc = [&](int b) -> const double* {
+    if (b < D) return P->dv ? P->dv + P->off[b] + goff[b] : nullptr;
+    return P->dq ? P->dq + goff[b] : nullptr;
+  };
+  const int nb = c->nblocks;
+  for (int phase = 0; phase < 3; ++phase) {
+    for (int b = 0; b < nb; ++b) {
+      double* const* peers = phase == 0 ? c->peers_y + (size_t)b * G : c->peers_z + (size_t)b * G;
+      const double* in = phase == 0 ? r + loff[b] : static_cast<const double*>(c->own[2 * b + (phase == 1 ? 0 : 1)]);
+      double* out = phase == 2 ? s + loff[b] : nullptr;
+      const double* ds = phase == 1 ? nullptr : dsc(b);
+      fdp_status e = b < D ? fd_apply_slab_peer(const_cast<fdp_fd>(P->vel[b]), phase, G, g, in, out,
+                                                phase == 2 ? nullptr : peers, ds, workspace, stream)
+                           : kron_mass_apply_slab_peer(const_cast<fdp_mass>(P->pres), phase, G, g, in, out,
+                                                       phase == 2 ? nullptr : peers, ds, workspace, stream);
+      if (e) return e;
+    }
+    // exchanges complete on every rank before the next phase reads (and, after phase 2, before
+    // the next apply's phase 0 overwrites y-slabs)
+    FDP_CUDA(launch_peer_barrier(c->flag_ptrs, c->counter, G, g, st), "block_precond_apply_sharded: barrier");
+  }
+  return FDP_OK;
+}
+
+extern "C" fdp_status fdp_comm_destroy(fdp_comm c) {
+  if (!c) return FDP_OK;
+  DeviceGuard dg(c->device);
+  free_comm(c);
+  return FDP_OK;
+}
+
 extern "C" size_t kron_mass_slab_workspace_bytes(fdp_mass h, int nranks, int rank) {
   if (!h || h->D != 3 || nranks < 1 || rank < 0 || rank >= nranks) return 0;
   long long z0, nz;

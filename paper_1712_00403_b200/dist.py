@@ -200,17 +200,21 @@ def exchange_handles(local: list, group=None) -> list:
 
 
 class PeerSlabBlockPrecond:
-    """P_D^{-1} slab-decomposed over a process group with the peer-store exchange: every rank
-    owns, per block, a y-slab receive buffer and a z-slab return buffer allocated with
-    fdp_peer_alloc and mapped into every peer (CUDA IPC); phase 0's mode-2 epilogue and phase 1's
-    last mode-3 epilogue store straight into the owners' buffers over NVLink, and fdp_peer_barrier
-    separates the phases. No pack / unpack kernels, no NCCL call in the apply. Local layout as
+    """P_D^{-1} slab-decomposed over a process group with the peer-store exchange, through
+    libfdp's communicator (fdp_comm_create / fdp_comm_connect / block_precond_apply_sharded):
+    every rank owns, per block, a y-slab receive buffer and a z-slab return buffer mapped into
+    every peer (CUDA IPC); phase 0's mode-2 epilogue and phase 1's last mode-3 epilogue store
+    straight into the owners' buffers over NVLink, and a system-scope barrier kernel separates the
+    phases. No pack / unpack kernels, no NCCL call in the apply. This class only moves the IPC
+    handle blobs between ranks (torch.distributed all_gather_object). Local layout as
     SlabBlockPrecond: [u_1 z-slab | ... | u_D z-slab | p z-slab]. D = 3 only."""
 
     def __init__(self, block, group=None):
+        import ctypes
+
         import torch
         import torch.distributed as dist
-        from . import PeerBuffer, lib, peer_open
+        from . import _check, lib
 
         self.torch = torch
         self.G = G = dist.get_world_size(group)
@@ -218,75 +222,37 @@ class PeerSlabBlockPrecond:
         self.block = block
         self.fds = block.fds
         self.mass = block.mass
-        dev = block.device
-        self.device = dev
         self.plans = [BlockPlan(tuple(f.dims), G, g) for f in self.fds]
         self.plans.append(BlockPlan(tuple(self.mass.dims), G, g))
         self.local_sizes = [p.zslab_size for p in self.plans]
         self.local_off = np.concatenate([[0], np.cumsum(self.local_sizes)]).astype(np.int64)
         self.local_n = int(self.local_off[-1])
-        # own peer buffers: per block a y-slab (receive of exchange 1) and a z-slab (receive of
-        # exchange 2), plus the G-slot barrier flag array
-        self.ybuf = [PeerBuffer(max(p.yslab_size, 1) * 8, dev) for p in self.plans]
-        self.zbuf = [PeerBuffer(max(p.zslab_size, 1) * 8, dev) for p in self.plans]
-        self.flags = PeerBuffer(G * 8, dev)
-        local = [b.handle for b in self.ybuf] + [b.handle for b in self.zbuf] + [self.flags.handle]
-        allh = exchange_handles(local, group)
-        self._opened = []
-        nb = len(self.plans)
-
-        def addr(r, i, own):
-            if r == g:
-                return own.ptr
-            p = peer_open(allh[r][i], dev)
-            self._opened.append(p)
-            return p
-
-        d = f"cuda:{dev}"
-        self.peers_y = [torch.tensor([addr(r, k, self.ybuf[k]) for r in range(G)], dtype=torch.int64, device=d)
-                        for k in range(nb)]
-        self.peers_z = [torch.tensor([addr(r, nb + k, self.zbuf[k]) for r in range(G)], dtype=torch.int64,
-                                     device=d) for k in range(nb)]
-        self.flag_ptrs = torch.tensor([addr(r, 2 * nb, self.flags) for r in range(G)], dtype=torch.int64, device=d)
-        self.counter = torch.zeros(1, dtype=torch.int64, device=d)
-        wsb = [lib.fd_slab_workspace_bytes(f.h, G, g) for f in self.fds]
-        wsb.append(lib.kron_mass_slab_workspace_bytes(self.mass.h, G, g))
-        self.ws = torch.empty(max(wsb) // 8 + 1, dtype=torch.float64, device=d)
-        self.yv = [b.tensor(max(p.yslab_size, 1)) for b, p in zip(self.ybuf, self.plans)]
-        self.zv = [b.tensor(max(p.zslab_size, 1)) for b, p in zip(self.zbuf, self.plans)]
+        assert self.local_n == int(lib.block_precond_sharded_size(block.h, G, g))
+        nb = int(lib.fdp_comm_blob_bytes(block.h, G))
+        blob = ctypes.create_string_buffer(nb)
+        c = ctypes.c_void_p()
+        _check(lib.fdp_comm_create(block.h, G, g, ctypes.byref(c), blob))
+        self.comm = c
+        blobs = [None] * G
+        dist.all_gather_object(blobs, blob.raw, group=group)
+        allb = ctypes.create_string_buffer(b"".join(blobs), nb * G)
+        _check(lib.fdp_comm_connect(c, allb))
+        wsb = int(lib.block_precond_sharded_workspace_bytes(block.h, c))
+        self.ws = torch.empty(wsb // 8 + 1, dtype=torch.float64, device=f"cuda:{block.device}")
         dist.barrier(group)
 
-    def apply(self, r, s, dscale_vel=None, dscale_pres=None, stream=None):
-        from . import fd_apply_slab_peer, kron_mass_apply_slab_peer, peer_barrier
-        G, g = self.G, self.g
-        o = self.local_off
-        nk = len(self.fds)
-        for k, f in enumerate(self.fds):
-            fd_apply_slab_peer(f, 0, G, g, r[o[k]:o[k + 1]], None, self.peers_y[k], None, self.ws, stream)
-        kron_mass_apply_slab_peer(self.mass, 0, G, g, r[o[nk]:o[nk + 1]], None, self.peers_y[nk], None,
-                                  self.ws, stream)
-        peer_barrier(self.flag_ptrs, self.counter, G, g, stream)
-        for k, f in enumerate(self.fds):
-            fd_apply_slab_peer(f, 1, G, g, self.yv[k], None, self.peers_z[k], None, self.ws, stream)
-        kron_mass_apply_slab_peer(self.mass, 1, G, g, self.yv[nk], None, self.peers_z[nk], None, self.ws,
-                                  stream)
-        peer_barrier(self.flag_ptrs, self.counter, G, g, stream)
-        for k, f in enumerate(self.fds):
-            fd_apply_slab_peer(f, 2, G, g, self.zv[k], s[o[k]:o[k + 1]], None, None, self.ws, stream)
-        kron_mass_apply_slab_peer(self.mass, 2, G, g, self.zv[nk], s[o[nk]:o[nk + 1]], None, None, None,
-                                  stream)
-        # the next apply's phase 0 overwrites peers' y-slabs: every rank must be done reading them
-        peer_barrier(self.flag_ptrs, self.counter, G, g, stream)
+    def apply(self, r, s, stream=None):
+        from . import _check, _dev, _stream, lib
+        _check(lib.block_precond_apply_sharded(self.block.h, self.comm, _dev(r, "r", self.local_n),
+                                               _dev(s, "s", self.local_n), _dev(self.ws, "workspace"),
+                                               _stream(stream)))
         return s
 
     def close(self):
-        from . import peer_close
-        for p in getattr(self, "_opened", []):
-            try:
-                peer_close(p)
-            except Exception:
-                pass
-        self._opened = []
+        from . import lib
+        if getattr(self, "comm", None):
+            lib.fdp_comm_destroy(self.comm)
+            self.comm = None
 
 
 def emulate_slab_apply_peer(block, r_full, G: int):

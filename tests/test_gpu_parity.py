@@ -392,6 +392,15 @@ def test_peer_slab_block_precond_single_rank():
         torch.cuda.synchronize()
         assert rel(st.cpu().numpy(), ref.apply(r)) < TOL
         SB.close()
+        # P_D^G: the block's D scalings, sliced to the slab, inside block_precond_apply_sharded
+        dv, dq = ospaces.nu_scalings(od, synth.viscosity)
+        PG = fdp.build_block(gd, dscale_vel=dv, dscale_pres=dq)
+        SG = fdist.PeerSlabBlockPrecond(PG)
+        r = rng.standard_normal(od.n_total)
+        rt = dev(r)
+        SG.apply(rt, st)
+        assert rel(st.cpu().numpy(), oprec.BlockPrecond(od, dv, dq).apply(r)) < TOL
+        SG.close()
     finally:
         if created:
             tdist.destroy_process_group()
