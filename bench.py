@@ -143,6 +143,12 @@ def run_reference(args, w, cid):
     rank, world, _ = dist_env()
     if rank != 0:
         return
+    # rank 0 runs alone: give the oracle every host core (torchrun sets OMP_NUM_THREADS=1)
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(limits=os.cpu_count() or 1)
+    except Exception:
+        pass
     # each step = one oracle application to one RHS (bounded: the whole run stays within minutes)
     steps, warm = args.steps, args.warmup
     from oracle import precond, spaces
@@ -191,8 +197,15 @@ def main():
 
     rank, world, local = dist_env()
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        # FDP_BENCH_SHARED_GPU=1 (host-logic check only): every rank on cuda:0 with gloo
+        # collectives, for exercising the multi-rank code path on a one-GPU box; not a measurement
+        if os.environ.get("FDP_BENCH_SHARED_GPU"):
+            local = 0
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
