@@ -13,7 +13,7 @@ import torch
 from paper_1712_00403_b200 import geometry as ggeo
 from paper_1712_00403_b200 import krylov
 
-cases = [(int(a), int(b)) for a, b in (c.split("x") for c in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["2x8", "3x16", "3x32"]))]
+cases = [(int(a), int(b)) for a, b in (c.split("x") for c in (sys.argv[1].split(",") if len(sys.argv) > 1 and "x" in sys.argv[1] else ["2x8", "3x16", "3x32"]))]
 for p, n_el in cases:
     t0 = time.perf_counter()
     gop = ggeo.AnnulusStokesOperator(p, n_el)
@@ -41,3 +41,27 @@ for p, n_el in cases:
                           "dofs": gop.n, "precond": name, "iterations": its,
                           "gpu_solve_ms": a.elapsed_time(b), "true_rel_residual": res,
                           "setup_s": t_setup, "operator_setup_s": t_op}))
+
+
+# P_T^G / P_C^G GMRES on the annulus (the paper's Tables 5-6 setting)
+if "--gmres" in sys.argv:
+    for p, n_el in cases:
+        gop = ggeo.AnnulusStokesOperator(p, n_el)
+        f = np.random.default_rng(0).standard_normal(gop.n)
+        f[-gop.sizes[-1]:] -= f[-gop.sizes[-1]:].mean()
+        fd_ = torch.from_numpy(f).cuda()
+        P, _ = ggeo.geometry_block(gop)
+        for variant in ("T", "C"):
+            tri = P.tri(variant, gop.B, gop.BT)
+            ws = tri.workspace()
+            ap = lambda r, z: tri.apply(r, z, ws)
+            krylov.gmres(gop.apply, ap, fd_)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            x, its, _ = krylov.gmres(gop.apply, ap, fd_)
+            b.record()
+            torch.cuda.synchronize()
+            print(json.dumps({"geometry": "eighth_annulus", "disc": "TH", "p": p, "n_el": n_el,
+                              "dofs": gop.n, "precond": f"P_{variant}^G", "solver": "GMRES",
+                              "iterations": its, "gpu_solve_ms": a.elapsed_time(b)}))
