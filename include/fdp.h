@@ -334,6 +334,33 @@ fdp_status fdp_vec_lincomb_dev(const double* coef, const double* x, const double
                                const double* z, double* out, int64_t n, void* stream);
 fdp_status fdp_minres_scalars(int phase, double* state, double* hist, int hist_cap, void* stream);
 
+/* ---- Device-resident GMRES (NEXT-2): indices and counts read from device memory, so whole
+ * Arnoldi steps can be captured in one CUDA graph ----
+ * fdp_vec_copy_indexed: out = V_{*idx}; fdp_vec_store_indexed: V_{*idx} = (*coef) w, skipped
+ * when *coef == 0; fdp_vec_multidot_dev / fdp_vec_gemv_dev: as fdp_vec_multidot / fdp_vec_gemv
+ * over m = min(*m, m_max) vectors (grids sized for m_max; workspace as for m_max).
+ * fdp_gmres_scalars(phase, istate, dstate, H, ldh, h1, h2, hist, m_max): one thread.
+ *   istate (int[5]): [0] j (next column) [1] done [2] iterations at convergence [3] j + 1 (the
+ *     multidot count) [4] index of the next basis vector;
+ *   dstate (double[8 + 3 (m_max + 1)]): [0] beta = ||P^{-1} b|| [1] tol (caller) [2] coefficient
+ *     of the next basis vector [3] ||w||^2 (caller) [4] ||P^{-1} b||^2 (caller), then cs, sn, g;
+ *   H: column-major (ldh >= m_max + 1), column j = the Arnoldi coefficients h1 + h2 (classical
+ *     Gram-Schmidt, two passes) and ||w||, rotated into R by the stored Givens rotations;
+ *   phase 0 = init, 1 = one step (no-op after done); stopping rule |g_{j+1}| / beta <= tol. */
+fdp_status fdp_vec_copy_indexed(const double* V, int64_t ldv, const int* idx, double* out,
+                                int64_t n, void* stream);
+fdp_status fdp_vec_store_indexed(double* V, int64_t ldv, const int* idx, const double* w,
+                                 const double* coef, int64_t n, void* stream);
+fdp_status fdp_vec_multidot_dev(const double* V, int64_t ldv, const int* m, int m_max,
+                                const double* w, int64_t n, double* h, void* workspace,
+                                void* stream);
+fdp_status fdp_vec_gemv_dev(const double* V, int64_t ldv, const int* m, int m_max,
+                            const double* h, double alpha, double* w, double beta, int64_t n,
+                            void* stream);
+fdp_status fdp_gmres_scalars(int phase, int* istate, double* dstate, double* H, int ldh,
+                             const double* h1, const double* h2, double* hist, int m_max,
+                             void* stream);
+
 /* ---- Arnoldi helpers for GMRES (Saad & Schultz) ----
  * V: m device vectors of length n with stride ldv >= n (V_j = V + j*ldv).
  * fdp_vec_multidot: h[j] = V_j . w for j < m into device h; deterministic (fixed grid, fixed

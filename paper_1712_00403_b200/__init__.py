@@ -80,6 +80,11 @@ def _load():
         "kron_op_diagonal": (i32, [vp, vp]),
         "fdp_vec_lincomb_dev": (i32, [vp, vp, vp, vp, vp, i64, vp]),
         "fdp_minres_scalars": (i32, [i32, vp, vp, i32, vp]),
+        "fdp_vec_copy_indexed": (i32, [vp, i64, vp, vp, i64, vp]),
+        "fdp_vec_store_indexed": (i32, [vp, i64, vp, vp, vp, i64, vp]),
+        "fdp_vec_multidot_dev": (i32, [vp, i64, vp, i32, vp, i64, vp, vp, vp]),
+        "fdp_vec_gemv_dev": (i32, [vp, i64, vp, i32, vp, ctypes.c_double, vp, ctypes.c_double, i64, vp]),
+        "fdp_gmres_scalars": (i32, [i32, vp, vp, vp, i32, vp, vp, vp, i32, vp]),
         "fdp_host_alloc": (vp, [sz]),
         "fdp_host_free": (i32, [vp]),
         "fdp_vec_multidot_workspace_bytes": (sz, [i32]),

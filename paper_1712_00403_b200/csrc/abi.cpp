@@ -2633,6 +2633,61 @@ extern "C" fdp_status fdp_minres_scalars(int phase, double* state, double* hist,
   return FDP_OK;
 }
 
+extern "C" fdp_status fdp_vec_copy_indexed(const double* V, int64_t ldv, const int* idx, double* out,
+                                           int64_t n, void* stream) {
+  if (n < 0 || ldv < n) return fail(FDP_ERR_SHAPE, "fdp_vec_copy_indexed: bad extents");
+  if (!is_device_ptr(V) || !is_device_ptr(idx) || !is_device_ptr(out))
+    return fail(FDP_ERR_INVALID_ARG, "fdp_vec_copy_indexed: device pointers required");
+  FDP_CUDA(launch_copy_indexed(V, ldv, idx, out, n, static_cast<cudaStream_t>(stream)), "fdp_vec_copy_indexed");
+  return FDP_OK;
+}
+
+extern "C" fdp_status fdp_vec_store_indexed(double* V, int64_t ldv, const int* idx, const double* w,
+                                            const double* coef, int64_t n, void* stream) {
+  if (n < 0 || ldv < n) return fail(FDP_ERR_SHAPE, "fdp_vec_store_indexed: bad extents");
+  if (!is_device_ptr(V) || !is_device_ptr(idx) || !is_device_ptr(w) || !is_device_ptr(coef))
+    return fail(FDP_ERR_INVALID_ARG, "fdp_vec_store_indexed: device pointers required");
+  FDP_CUDA(launch_store_indexed(V, ldv, idx, w, coef, n, static_cast<cudaStream_t>(stream)), "fdp_vec_store_indexed");
+  return FDP_OK;
+}
+
+extern "C" fdp_status fdp_vec_multidot_dev(const double* V, int64_t ldv, const int* m, int m_max,
+                                           const double* w, int64_t n, double* h, void* workspace,
+                                           void* stream) {
+  if (m_max < 0 || n < 0 || (m_max > 0 && ldv < n)) return fail(FDP_ERR_SHAPE, "fdp_vec_multidot_dev: bad extents");
+  if (m_max == 0) return FDP_OK;
+  if (!is_device_ptr(V) || !is_device_ptr(m) || !is_device_ptr(w) || !is_device_ptr(h) || !is_device_ptr(workspace))
+    return fail(FDP_ERR_INVALID_ARG, "fdp_vec_multidot_dev: device pointers required");
+  FDP_CUDA(launch_multidot_dev(V, ldv, m, m_max, w, n, h, static_cast<double*>(workspace),
+                               static_cast<cudaStream_t>(stream)), "fdp_vec_multidot_dev");
+  return FDP_OK;
+}
+
+extern "C" fdp_status fdp_vec_gemv_dev(const double* V, int64_t ldv, const int* m, int m_max,
+                                       const double* h, double alpha, double* w, double beta,
+                                       int64_t n, void* stream) {
+  if (m_max < 0 || m_max > 6144 || n < 0 || ldv < n) return fail(FDP_ERR_SHAPE, "fdp_vec_gemv_dev: bad extents");
+  if (n == 0) return FDP_OK;
+  if (!is_device_ptr(V) || !is_device_ptr(m) || !is_device_ptr(h) || !is_device_ptr(w))
+    return fail(FDP_ERR_INVALID_ARG, "fdp_vec_gemv_dev: device pointers required");
+  FDP_CUDA(launch_gemv_dev(V, ldv, m, m_max, h, alpha, w, beta, n, static_cast<cudaStream_t>(stream)),
+           "fdp_vec_gemv_dev");
+  return FDP_OK;
+}
+
+extern "C" fdp_status fdp_gmres_scalars(int phase, int* istate, double* dstate, double* H, int ldh,
+                                        const double* h1, const double* h2, double* hist, int m_max,
+                                        void* stream) {
+  if ((phase != 0 && phase != 1) || m_max < 1 || ldh < m_max + 1)
+    return fail(FDP_ERR_INVALID_ARG, "fdp_gmres_scalars: bad phase or extents");
+  if (!is_device_ptr(istate) || !is_device_ptr(dstate) || !is_device_ptr(H) || !is_device_ptr(h1) ||
+      !is_device_ptr(h2) || (hist && !is_device_ptr(hist)))
+    return fail(FDP_ERR_INVALID_ARG, "fdp_gmres_scalars: device pointers required");
+  FDP_CUDA(launch_gmres_scalars(phase, istate, dstate, H, ldh, h1, h2, hist, m_max,
+                                static_cast<cudaStream_t>(stream)), "fdp_gmres_scalars");
+  return FDP_OK;
+}
+
 // ------------------------------------------------------------------------------------------------
 // Arnoldi helpers (GMRES orthogonalization, NEXT-2)
 // ------------------------------------------------------------------------------------------------

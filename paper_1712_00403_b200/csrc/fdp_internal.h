@@ -178,6 +178,19 @@ cudaError_t launch_multidot(const double* V, long long ldv, int m, const double*
                             double* h, double* scratch, cudaStream_t s);
 cudaError_t launch_gemv(const double* V, long long ldv, int m, const double* h, double alpha,
                         double* w, double beta, long long n, cudaStream_t s);
+cudaError_t launch_copy_indexed(const double* V, long long ldv, const int* idx, double* out,
+                                long long n, cudaStream_t s);
+cudaError_t launch_store_indexed(double* V, long long ldv, const int* idx, const double* w,
+                                 const double* coef, long long n, cudaStream_t s);
+cudaError_t launch_multidot_dev(const double* V, long long ldv, const int* m_ptr, int m_max,
+                                const double* w, long long n, double* h, double* scratch,
+                                cudaStream_t s);
+cudaError_t launch_gemv_dev(const double* V, long long ldv, const int* m_ptr, int m_max,
+                            const double* h, double alpha, double* w, double beta, long long n,
+                            cudaStream_t s);
+cudaError_t launch_gmres_scalars(int phase, int* is, double* ds, double* H, int ldh,
+                                 const double* h1, const double* h2, double* hist, int m_max,
+                                 cudaStream_t s);
 cudaError_t launch_lincomb_dev(const double* k, const double* x, const double* y, const double* z,
                                double* out, long long n, cudaStream_t s);
 cudaError_t launch_minres_scalars(int phase, double* state, double* hist, int hist_cap, cudaStream_t s);

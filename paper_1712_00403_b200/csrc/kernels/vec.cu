@@ -228,7 +228,190 @@ __global__ void gemv_kernel(const double* __restrict__ V, long long ldv, int m,
   }
 }
 
+// ---- device-indexed Arnoldi helpers (GPU-resident GMRES): counts and indices read from device
+// memory so that whole iterations can be captured in one CUDA graph ----
+__global__ void copy_indexed_kernel(const double* __restrict__ V, long long ldv, const int* idx,
+                                    double* __restrict__ out, long long n) {
+  const long long base = (long long)(*idx) * ldv;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = V[base + i];
+}
+
+__global__ void store_indexed_kernel(double* __restrict__ V, long long ldv, const int* idx,
+                                     const double* __restrict__ w, const double* coef, long long n) {
+  const double c = *coef;
+  if (c == 0.0) return;
+  const long long base = (long long)(*idx) * ldv;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    V[base + i] = c * w[i];
+}
+
+__global__ void multidot_partial_dev_kernel(const double* __restrict__ V, long long ldv,
+                                            const int* m_ptr, int m_max,
+                                            const double* __restrict__ w, long long n,
+                                            double* __restrict__ partial) {
+  const int m = min(*m_ptr, m_max);
+  const int j0 = blockIdx.y * kMdVec;
+  if (j0 >= m) return;
+  __shared__ double sh[kDotThreads / 32][kMdVec];
+  const int nv = min(kMdVec, m - j0);
+  double s[kMdVec];
+#pragma unroll
+  for (int j = 0; j < kMdVec; ++j) s[j] = 0.0;
+  for (long long i = blockIdx.x * (long long)kDotThreads + threadIdx.x; i < n;
+       i += (long long)gridDim.x * kDotThreads) {
+    const double wi = w[i];
+#pragma unroll
+    for (int j = 0; j < kMdVec; ++j)
+      if (j < nv) s[j] = fma(V[(j0 + j) * ldv + i], wi, s[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < kMdVec; ++j) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s[j] += __shfl_down_sync(0xffffffffu, s[j], o);
+  }
+  if ((threadIdx.x & 31) == 0)
+#pragma unroll
+    for (int j = 0; j < kMdVec; ++j) sh[threadIdx.x >> 5][j] = s[j];
+  __syncthreads();
+  if (threadIdx.x < nv) {
+    double t = 0.0;
+    for (int q = 0; q < kDotThreads / 32; ++q) t += sh[q][threadIdx.x];
+    partial[(long long)(j0 + threadIdx.x) * kDotBlocks + blockIdx.x] = t;
+  }
+}
+
+__global__ void multidot_final_dev_kernel(const double* __restrict__ partial, const int* m_ptr,
+                                          int m_max, double* __restrict__ h) {
+  if ((int)blockIdx.x >= min(*m_ptr, m_max)) return;
+  __shared__ double sh[kDotThreads / 32];
+  const double* p = partial + (long long)blockIdx.x * kDotBlocks;
+  double v = 0.0;
+  for (int i = threadIdx.x; i < kDotBlocks; i += kDotThreads) v += p[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int q = 0; q < kDotThreads / 32; ++q) t += sh[q];
+    h[blockIdx.x] = t;
+  }
+}
+
+__global__ void gemv_dev_kernel(const double* __restrict__ V, long long ldv, const int* m_ptr,
+                                int m_max, const double* __restrict__ h, double alpha,
+                                double* __restrict__ w, double beta, long long n) {
+  extern __shared__ double hs[];
+  const int m = min(*m_ptr, m_max);
+  for (int j = threadIdx.x; j < m; j += blockDim.x) hs[j] = h[j];
+  __syncthreads();
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < m; ++j) s = fma(hs[j], V[j * ldv + i], s);
+    w[i] = beta != 0.0 ? fma(alpha, s, beta * w[i]) : alpha * s;
+  }
+}
+
+// GMRES least-squares bookkeeping on the device (one thread), Saad & Schultz with Givens
+// rotations; layouts in fdp.h.
+__global__ void gmres_scalars_kernel(int phase, int* __restrict__ is, double* __restrict__ ds,
+                                     double* __restrict__ H, int ldh, const double* __restrict__ h1,
+                                     const double* __restrict__ h2, double* __restrict__ hist,
+                                     int m_max) {
+  enum { J, DONE, KFIN, MCNT, STORE };
+  enum { BETA, TOL, COEF, NRM2, DOT };
+  double* cs = ds + 8;
+  double* sn = cs + m_max + 1;
+  double* g = sn + m_max + 1;
+  if (phase == 0) {  // init from DOT = ||P^{-1} b||^2
+    const double beta = sqrt(fmax(ds[DOT], 0.0));
+    ds[BETA] = beta;
+    for (int i = 0; i <= m_max; ++i) g[i] = 0.0;
+    g[0] = beta;
+    is[J] = 0;
+    is[DONE] = beta == 0.0 ? 1 : 0;
+    is[KFIN] = 0;
+    is[MCNT] = 1;
+    is[STORE] = 0;
+    ds[COEF] = beta == 0.0 ? 0.0 : 1.0 / beta;
+    if (hist) hist[0] = 1.0;
+    return;
+  }
+  if (is[DONE]) {
+    ds[COEF] = 0.0;
+    return;
+  }
+  const int j = is[J];
+  double* col = H + (long long)j * ldh;
+  for (int i = 0; i <= j; ++i) col[i] = h1[i] + h2[i];
+  const double hn = sqrt(fmax(ds[NRM2], 0.0));
+  col[j + 1] = hn;
+  ds[COEF] = hn != 0.0 ? 1.0 / hn : 0.0;
+  is[STORE] = j + 1;
+  for (int i = 0; i < j; ++i) {
+    const double t = cs[i] * col[i] + sn[i] * col[i + 1];
+    col[i + 1] = -sn[i] * col[i] + cs[i] * col[i + 1];
+    col[i] = t;
+  }
+  const double den = hypot(col[j], col[j + 1]);
+  cs[j] = col[j] / den;
+  sn[j] = col[j + 1] / den;
+  col[j] = den;
+  col[j + 1] = 0.0;
+  g[j + 1] = -sn[j] * g[j];
+  g[j] = cs[j] * g[j];
+  const double res = fabs(g[j + 1]) / ds[BETA];
+  if (hist) hist[j + 1] = res;
+  is[J] = j + 1;
+  is[MCNT] = j + 2;
+  if (res <= ds[TOL] || den == 0.0 || j + 1 >= m_max) {
+    is[DONE] = 1;
+    is[KFIN] = j + 1;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_copy_indexed(const double* V, long long ldv, const int* idx, double* out,
+                                long long n, cudaStream_t s) {
+  const int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 8);
+  copy_indexed_kernel<<<std::max(blocks, 1), 256, 0, s>>>(V, ldv, idx, out, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_store_indexed(double* V, long long ldv, const int* idx, const double* w,
+                                 const double* coef, long long n, cudaStream_t s) {
+  const int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 8);
+  store_indexed_kernel<<<std::max(blocks, 1), 256, 0, s>>>(V, ldv, idx, w, coef, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_multidot_dev(const double* V, long long ldv, const int* m_ptr, int m_max,
+                                const double* w, long long n, double* h, double* scratch,
+                                cudaStream_t s) {
+  if (m_max <= 0) return cudaSuccess;
+  dim3 grid(kDotBlocks, (m_max + kMdVec - 1) / kMdVec);
+  multidot_partial_dev_kernel<<<grid, kDotThreads, 0, s>>>(V, ldv, m_ptr, m_max, w, n, scratch);
+  multidot_final_dev_kernel<<<m_max, kDotThreads, 0, s>>>(scratch, m_ptr, m_max, h);
+  return cudaGetLastError();
+}
+cudaError_t launch_gemv_dev(const double* V, long long ldv, const int* m_ptr, int m_max,
+                            const double* h, double alpha, double* w, double beta, long long n,
+                            cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const int blocks = (int)std::min<long long>((n + 255) / 256, 148LL * 8);
+  gemv_dev_kernel<<<blocks, 256, (size_t)std::max(m_max, 1) * sizeof(double), s>>>(V, ldv, m_ptr, m_max, h,
+                                                                                   alpha, w, beta, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_gmres_scalars(int phase, int* is, double* ds, double* H, int ldh,
+                                 const double* h1, const double* h2, double* hist, int m_max,
+                                 cudaStream_t s) {
+  gmres_scalars_kernel<<<1, 1, 0, s>>>(phase, is, ds, H, ldh, h1, h2, hist, m_max);
+  return cudaGetLastError();
+}
 
 size_t multidot_scratch_elems(int m) { return (size_t)m * kDotBlocks; }
 

@@ -391,3 +391,103 @@ def gmres(apply_A, apply_P, b, tol: float = 1e-8, maxit: int = 500):
     x = torch.empty_like(b)
     vec_gemv(V, k, h1, 1.0, x, 0.0)
     return x, k, hist
+
+
+_DEV_GMRES = {}
+
+
+def gmres_device(apply_A, apply_P, b, tol: float = 1e-8, maxit: int = 500, unroll: int = 4):
+    """GMRES with the Arnoldi bookkeeping on the GPU (fdp_gmres_scalars; basis indices and counts
+    read from device memory by fdp_vec_copy_indexed / _store_indexed / _multidot_dev /
+    _gemv_dev): `unroll` whole steps are one CUDA graph, the host reads the `done` flag once per
+    replay. Same arithmetic and stopping rule as ``gmres`` (classical Gram-Schmidt twice, Givens
+    rotations); steps after convergence change nothing. apply_A / apply_P must be capturable
+    (direct launches). Returns (x, iterations, history)."""
+    import ctypes
+
+    import torch
+    from . import _check, lib
+    n = b.numel()
+    dev = b.device
+    m = min(maxit, n)
+    fid = lambda f: (id(getattr(f, "__self__", f)), getattr(getattr(f, "__func__", f), "__qualname__", ""))
+    key = (n, m, str(dev), unroll, fid(apply_A), fid(apply_P))
+    ent = _DEV_GMRES.get(key)
+    st = lambda: torch.cuda.current_stream().cuda_stream
+    if ent is None:
+        _DEV_GMRES.clear()
+        f64 = dict(dtype=torch.float64, device=dev)
+        ent = {
+            "V": torch.empty((m + 1, n), **f64), "vin": torch.empty(n, **f64), "t": torch.empty(n, **f64),
+            "w": torch.empty(n, **f64), "h1": torch.zeros(m + 1, **f64), "h2": torch.zeros(m + 1, **f64),
+            "H": torch.zeros((m, m + 1), **f64), "hist": torch.zeros(m + 1, **f64),
+            "ds": torch.zeros(8 + 3 * (m + 1), **f64),
+            "is": torch.zeros(5, dtype=torch.int32, device=dev),
+            "scr": torch.empty(max(1, int(lib.fdp_vec_multidot_workspace_bytes(m + 1)) // 8), **f64),
+            "graph": None,
+        }
+        _DEV_GMRES[key] = ent
+    V, vin, t, w = ent["V"], ent["vin"], ent["t"], ent["w"]
+    h1, h2, H, hist, ds, is_, scr = ent["h1"], ent["h2"], ent["H"], ent["hist"], ent["ds"], ent["is"], ent["scr"]
+    P = lambda x: ctypes.c_void_p(x.data_ptr())
+    ldv = V.stride(0)
+
+    def scalars(phase):
+        _check(lib.fdp_gmres_scalars(phase, P(is_), P(ds), P(H), m + 1, P(h1), P(h2), P(hist), m, st()))
+
+    def store():  # V[istate[4]] = dstate[2] * w
+        _check(lib.fdp_vec_store_indexed(P(V), ldv, ctypes.c_void_p(is_.data_ptr() + 16), P(w),
+                                         ctypes.c_void_p(ds.data_ptr() + 16), n, st()))
+
+    def steps():
+        for _ in range(unroll):
+            _check(lib.fdp_vec_copy_indexed(P(V), ldv, P(is_), P(vin), n, st()))
+            apply_A(vin, t)
+            apply_P(t, w)                                              # w = P^{-1} A v_j
+            mc = ctypes.c_void_p(is_.data_ptr() + 12)                  # j + 1
+            for h in (h1, h2):                                         # classical GS, twice
+                _check(lib.fdp_vec_multidot_dev(P(V), ldv, mc, m + 1, P(w), n, P(h), P(scr), st()))
+                _check(lib.fdp_vec_gemv_dev(P(V), ldv, mc, m + 1, P(h), -1.0, P(w), 1.0, n, st()))
+            vec_dot(w, w, ds[3:4])
+            scalars(1)
+            store()
+
+    vin.copy_(b)
+    apply_P(vin, w)
+    ds.zero_()
+    ds[1] = tol
+    vec_dot(w, w, ds[4:5])
+    scalars(0)
+    store()
+    if ent["graph"] is None:
+        # warm-up outside capture would advance the iteration: snapshot and restore
+        snap = [x.clone() for x in (V[0], is_, ds, H, hist)]
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            steps()
+        torch.cuda.current_stream().wait_stream(side)
+        for x, c in zip((V[0], is_, ds, H, hist), snap):
+            x.copy_(c)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            steps()
+        ent["graph"] = g
+    g = ent["graph"]
+    while True:
+        g.replay()
+        iv = is_.tolist()                                              # the one host read per replay
+        if iv[1] or iv[0] >= m:
+            break
+    k = iv[2] if iv[1] else m
+    if k == 0:
+        return torch.zeros_like(b), 0, [0.0]
+    R = H[:k, :k].cpu().numpy().T                                      # R[i, j] = H column j, row i
+    gv = ds[8 + 2 * (m + 1): 8 + 2 * (m + 1) + k].cpu().numpy()
+    y = np.zeros(k)
+    for i in range(k - 1, -1, -1):
+        y[i] = (gv[i] - R[i, i + 1:k] @ y[i + 1:k]) / R[i, i]
+    h1[:k].copy_(torch.from_numpy(y))
+    x = torch.empty_like(b)
+    vec_gemv(V, k, h1, 1.0, x, 0.0)
+    return x, k, [1.0] + hist[1:k + 1].tolist()

@@ -63,6 +63,16 @@ for cid in cids:
             papply(r_buf, z_buf)
         b.record()
         torch.cuda.synchronize()
+        pms = a.elapsed_time(b) / 20
+        # device-resident Arnoldi bookkeeping (4 steps per graph replay)
+        apd = lambda r, z: tri.apply(r, z, ws)
+        krylov.gmres_device(gop._apply_direct, apd, fd_)
+        torch.cuda.synchronize()
+        a.record()
+        xd, its_d, _ = krylov.gmres_device(gop._apply_direct, apd, fd_)
+        b.record()
+        torch.cuda.synchronize()
         print(json.dumps({"config": cid, "variant": variant, "dofs": gop.n, "iterations": its,
-                          "gpu_solve_ms": ms, "true_rel_residual": res,
-                          "precond_ms": a.elapsed_time(b) / 20}))
+                          "gpu_solve_ms": ms, "true_rel_residual": res, "precond_ms": pms,
+                          "device_resident_iterations": its_d,
+                          "device_resident_solve_ms": a.elapsed_time(b)}))

@@ -100,3 +100,24 @@ def test_gpu_gmres_iteration_counts(cid, variant):
     xg[-nq:] -= xg[-nq:].mean()
     x_o[-nq:] -= x_o[-nq:].mean()
     assert rel(xg, x_o) < 1e-6
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3])
+@pytest.mark.parametrize("variant", ["T", "C"])
+def test_gpu_gmres_device_resident(cid, variant):
+    """gmres_device (Arnoldi bookkeeping on the GPU, 4 steps per graph replay): the oracle's
+    iteration count and history, and the host-driven GPU GMRES's solution."""
+    w, op, oblk, gop, P = _setup(cid)
+    oP = (oprec.TriangularPrecond if variant == "T" else oprec.ConstrainedPrecond)(oblk, op)
+    f = ostokes.project_rhs(synth.rhs(w.seed, op.n, 1)[0], op.sizes[-1])
+    _, it_o, h_o = ogmres.gmres(op.matvec, f, oP.apply)
+    tri = P.tri(variant, gop.B, gop.BT)
+    ws = tri.workspace()
+    ap = lambda r, z: tri.apply(r, z, ws)
+    for _ in range(2):
+        x_d, it_d, h_d = krylov.gmres_device(gop._apply_direct, ap, dev(f))
+        assert it_d == it_o, (cid, variant, it_d, it_o)
+        assert max(abs(a - b) / a for a, b in zip(h_o, h_d)) < 1e-6
+    x_h, it_h, _ = krylov.gmres(gop.apply, ap, dev(f))
+    assert it_h == it_d
+    assert rel(x_d.cpu().numpy(), x_h.cpu().numpy()) < 1e-9
