@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <memory>
 #include <mutex>
 #include <new>
@@ -27,6 +28,20 @@ static fdp_status fail(fdp_status s, const std::string& msg) {
   g_last_error = msg;
   return s;
 }
+// No C++ exception crosses the C ABI: every entry point catches and reports (mostly
+// std::bad_alloc from host-side containers). Called from inside a catch handler.
+static fdp_status abi_exception(const char* fn) {
+  try {
+    throw;
+  } catch (const std::bad_alloc&) {
+    return fail(FDP_ERR_OOM, std::string(fn) + ": host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(FDP_ERR_INVALID_ARG, std::string(fn) + ": " + e.what());
+  } catch (...) {
+    return fail(FDP_ERR_INVALID_ARG, std::string(fn) + ": unexpected exception");
+  }
+}
+
 static fdp_status cuda_fail(cudaError_t e, const char* where) {
   cudaGetLastError();  // clear sticky-free errors
   return fail(FDP_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
@@ -140,34 +155,46 @@ struct Recorder {
 // ------------------------------------------------------------------------------------------------
 extern "C" fdp_status iga_univariate(int deg, int alpha, int n_el, int flags, double c_pen, int q,
                                      double* K, double* M, int32_t* n_out) {
-  if (!n_out) return fail(FDP_ERR_INVALID_ARG, "iga_univariate: n_out is NULL");
-  std::string err;
-  int n = 0;
-  int st = iga_build(deg, alpha, n_el, flags, c_pen, q, K, M, &n, &err);
-  if (st) return fail((fdp_status)st, err);
-  *n_out = n;
-  return FDP_OK;
+  try {
+    if (!n_out) return fail(FDP_ERR_INVALID_ARG, "iga_univariate: n_out is NULL");
+    std::string err;
+    int n = 0;
+    int st = iga_build(deg, alpha, n_el, flags, c_pen, q, K, M, &n, &err);
+    if (st) return fail((fdp_status)st, err);
+    *n_out = n;
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
 }
 
 extern "C" fdp_status iga_greville(int deg, int alpha, int n_el, int flags, double* g,
                                    int32_t* n_out) {
-  if (!n_out) return fail(FDP_ERR_INVALID_ARG, "iga_greville: n_out is NULL");
-  std::string err;
-  int n = 0;
-  int st = iga_greville_build(deg, alpha, n_el, flags, g, &n, &err);
-  if (st) return fail((fdp_status)st, err);
-  *n_out = n;
-  return FDP_OK;
+  try {
+    if (!n_out) return fail(FDP_ERR_INVALID_ARG, "iga_greville: n_out is NULL");
+    std::string err;
+    int n = 0;
+    int st = iga_greville_build(deg, alpha, n_el, flags, g, &n, &err);
+    if (st) return fail((fdp_status)st, err);
+    *n_out = n;
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
 }
 
 extern "C" fdp_status fdp_gen_eig(int n, const double* K, const double* M, double* U,
                                   double* lambda) {
-  if (n < 1) return fail(FDP_ERR_SHAPE, "fdp_gen_eig: n < 1");
-  if (!K || !M || !U || !lambda) return fail(FDP_ERR_INVALID_ARG, "fdp_gen_eig: NULL argument");
-  std::string err;
-  int st = gen_eig(n, K, M, U, lambda, &err);
-  if (st) return fail((fdp_status)st, "fdp_gen_eig: " + err);
-  return FDP_OK;
+  try {
+    if (n < 1) return fail(FDP_ERR_SHAPE, "fdp_gen_eig: n < 1");
+    if (!K || !M || !U || !lambda) return fail(FDP_ERR_INVALID_ARG, "fdp_gen_eig: NULL argument");
+    std::string err;
+    int st = gen_eig(n, K, M, U, lambda, &err);
+    if (st) return fail((fdp_status)st, "fdp_gen_eig: " + err);
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -212,118 +239,126 @@ static void free_fd(fdp_fd h) {
 extern "C" fdp_status fd_setup(int D, const int32_t* n, const double* const* K,
                                const double* const* M, const double* coef, int device,
                                int64_t max_batch, fdp_fd* out) {
-  if (!out) return fail(FDP_ERR_INVALID_ARG, "fd_setup: out is NULL");
-  *out = nullptr;
-  if (D < 2 || D > 3) return fail(FDP_ERR_UNSUPPORTED, "fd_setup: D must be 2 or 3");
-  if (!n || !K || !M || !coef) return fail(FDP_ERR_INVALID_ARG, "fd_setup: NULL argument");
-  if (max_batch < 0) return fail(FDP_ERR_SHAPE, "fd_setup: max_batch < 0");
-  long long N = 1;
-  for (int d = 0; d < D; ++d) {
-    if (n[d] < 1 || n[d] > 2048) return fail(FDP_ERR_SHAPE, "fd_setup: n[d] must be in [1, 2048]");
-    if (!K[d] || !M[d]) return fail(FDP_ERR_INVALID_ARG, "fd_setup: NULL K[d] or M[d]");
-    if (!(coef[d] > 0.0)) return fail(FDP_ERR_INVALID_ARG, "fd_setup: coef[d] must be > 0");
-    if (!symmetric(n[d], K[d]) || !symmetric(n[d], M[d]))
-      return fail(FDP_ERR_NOT_SPD, "fd_setup: K[d] or M[d] not symmetric");
-    N *= n[d];
-  }
-  if (is_device_ptr(K[0]) || is_device_ptr(M[0]))
-    return fail(FDP_ERR_INVALID_ARG, "fd_setup: K and M must be host arrays");
-  std::unique_ptr<fdp_fd_s> h(new (std::nothrow) fdp_fd_s);
-  if (!h) return fail(FDP_ERR_OOM, "fd_setup: host allocation");
-  h->D = D;
-  h->N = N;
-  h->device = device;
-  for (int d = 0; d < D; ++d) {
-    h->n[d] = n[d];
-    h->coef[d] = coef[d];
-  }
-  // Algorithm 1 step 1: generalized eigendecompositions on the host.
-  double lmin = 0.0, lmax = 0.0;
-  for (int d = 0; d < D; ++d) {
-    const int nd = n[d];
-    h->U_host[d].resize((size_t)nd * nd);
-    h->lam_host[d].resize(nd);
-    std::string err;
-    int st = gen_eig(nd, K[d], M[d], h->U_host[d].data(), h->lam_host[d].data(), &err);
-    if (st) return fail((fdp_status)st, "fd_setup: " + err);
-    h->dK[d].resize(nd);
-    h->dM[d].resize(nd);
-    for (int i = 0; i < nd; ++i) {
-      h->dK[d][i] = K[d][i + (size_t)nd * i];
-      h->dM[d][i] = M[d][i + (size_t)nd * i];
+  try {
+    if (!out) return fail(FDP_ERR_INVALID_ARG, "fd_setup: out is NULL");
+    *out = nullptr;
+    if (D < 2 || D > 3) return fail(FDP_ERR_UNSUPPORTED, "fd_setup: D must be 2 or 3");
+    if (!n || !K || !M || !coef) return fail(FDP_ERR_INVALID_ARG, "fd_setup: NULL argument");
+    if (max_batch < 0) return fail(FDP_ERR_SHAPE, "fd_setup: max_batch < 0");
+    long long N = 1;
+    for (int d = 0; d < D; ++d) {
+      if (n[d] < 1 || n[d] > 2048) return fail(FDP_ERR_SHAPE, "fd_setup: n[d] must be in [1, 2048]");
+      if (!K[d] || !M[d]) return fail(FDP_ERR_INVALID_ARG, "fd_setup: NULL K[d] or M[d]");
+      if (!(coef[d] > 0.0)) return fail(FDP_ERR_INVALID_ARG, "fd_setup: coef[d] must be > 0");
+      if (!symmetric(n[d], K[d]) || !symmetric(n[d], M[d]))
+        return fail(FDP_ERR_NOT_SPD, "fd_setup: K[d] or M[d] not symmetric");
+      N *= n[d];
     }
-    lmin += coef[d] * h->lam_host[d].front();
-    lmax += coef[d] * h->lam_host[d].back();
-  }
-  if (!(lmin > 1e-12 * lmax))
-    return fail(FDP_ERR_SINGULAR, "fd_setup: Kronecker-sum spectrum not positive (min Lambda <= 1e-12 max Lambda)");
-
-  DeviceGuard dg(device);
-  if (!dg.ok) return fail(FDP_ERR_CUDA, "fd_setup: cannot select device");
-  fdp_fd raw = h.release();
-  for (int d = 0; d < D; ++d) {
-    const int nd = n[d];
-    TileCfg c = choose_tile(nd);
-    raw->cfg[d] = c;
-    const int wrows = std::max(c.kpad, c.ldw);  // the fused small kernel reads W^T rows < ldw
-    std::vector<double> wf((size_t)wrows * c.ldw, 0.0), wb((size_t)wrows * c.ldw, 0.0);
-    const std::vector<double>& U = raw->U_host[d];  // column-major: U[i + n*j]
-    for (int k = 0; k < nd; ++k)
-      for (int a = 0; a < nd; ++a) {
-        wf[(size_t)k * c.ldw + a] = U[k + (size_t)nd * a];  // W[k][a] = U[k][a]
-        wb[(size_t)k * c.ldw + a] = U[a + (size_t)nd * k];  // W[k][a] = U[a][k]
+    if (is_device_ptr(K[0]) || is_device_ptr(M[0]))
+      return fail(FDP_ERR_INVALID_ARG, "fd_setup: K and M must be host arrays");
+    std::unique_ptr<fdp_fd_s> h(new (std::nothrow) fdp_fd_s);
+    if (!h) return fail(FDP_ERR_OOM, "fd_setup: host allocation");
+    h->D = D;
+    h->N = N;
+    h->device = device;
+    for (int d = 0; d < D; ++d) {
+      h->n[d] = n[d];
+      h->coef[d] = coef[d];
+    }
+    // Algorithm 1 step 1: generalized eigendecompositions on the host.
+    double lmin = 0.0, lmax = 0.0;
+    for (int d = 0; d < D; ++d) {
+      const int nd = n[d];
+      h->U_host[d].resize((size_t)nd * nd);
+      h->lam_host[d].resize(nd);
+      std::string err;
+      int st = gen_eig(nd, K[d], M[d], h->U_host[d].data(), h->lam_host[d].data(), &err);
+      if (st) return fail((fdp_status)st, "fd_setup: " + err);
+      h->dK[d].resize(nd);
+      h->dM[d].resize(nd);
+      for (int i = 0; i < nd; ++i) {
+        h->dK[d][i] = K[d][i + (size_t)nd * i];
+        h->dM[d][i] = M[d][i + (size_t)nd * i];
       }
-    std::vector<double> lc(nd);
-    for (int i = 0; i < nd; ++i) lc[i] = coef[d] * raw->lam_host[d][i];
-    fdp_status st;
-    if ((st = dalloc(&raw->Wf[d], wf.size())) || (st = dalloc(&raw->Wb[d], wb.size())) ||
-        (st = dalloc(&raw->lamc[d], lc.size()))) {
-      free_fd(raw);
-      return st;
+      lmin += coef[d] * h->lam_host[d].front();
+      lmax += coef[d] * h->lam_host[d].back();
     }
-    cudaError_t e;
-    if ((e = cudaMemcpy(raw->Wf[d], wf.data(), wf.size() * 8, cudaMemcpyHostToDevice)) ||
-        (e = cudaMemcpy(raw->Wb[d], wb.data(), wb.size() * 8, cudaMemcpyHostToDevice)) ||
-        (e = cudaMemcpy(raw->lamc[d], lc.data(), lc.size() * 8, cudaMemcpyHostToDevice)) ||
-        (e = prepare_mode_kernels(c)) || (e = prepare_mode_small(c.NT))) {
-      free_fd(raw);
-      return cuda_fail(e, "fd_setup: upload");
+    if (!(lmin > 1e-12 * lmax))
+      return fail(FDP_ERR_SINGULAR, "fd_setup: Kronecker-sum spectrum not positive (min Lambda <= 1e-12 max Lambda)");
+
+    DeviceGuard dg(device);
+    if (!dg.ok) return fail(FDP_ERR_CUDA, "fd_setup: cannot select device");
+    fdp_fd raw = h.release();
+    for (int d = 0; d < D; ++d) {
+      const int nd = n[d];
+      TileCfg c = choose_tile(nd);
+      raw->cfg[d] = c;
+      const int wrows = std::max(c.kpad, c.ldw);  // the fused small kernel reads W^T rows < ldw
+      std::vector<double> wf((size_t)wrows * c.ldw, 0.0), wb((size_t)wrows * c.ldw, 0.0);
+      const std::vector<double>& U = raw->U_host[d];  // column-major: U[i + n*j]
+      for (int k = 0; k < nd; ++k)
+        for (int a = 0; a < nd; ++a) {
+          wf[(size_t)k * c.ldw + a] = U[k + (size_t)nd * a];  // W[k][a] = U[k][a]
+          wb[(size_t)k * c.ldw + a] = U[a + (size_t)nd * k];  // W[k][a] = U[a][k]
+        }
+      std::vector<double> lc(nd);
+      for (int i = 0; i < nd; ++i) lc[i] = coef[d] * raw->lam_host[d][i];
+      fdp_status st;
+      if ((st = dalloc(&raw->Wf[d], wf.size())) || (st = dalloc(&raw->Wb[d], wb.size())) ||
+          (st = dalloc(&raw->lamc[d], lc.size()))) {
+        free_fd(raw);
+        return st;
+      }
+      cudaError_t e;
+      if ((e = cudaMemcpy(raw->Wf[d], wf.data(), wf.size() * 8, cudaMemcpyHostToDevice)) ||
+          (e = cudaMemcpy(raw->Wb[d], wb.data(), wb.size() * 8, cudaMemcpyHostToDevice)) ||
+          (e = cudaMemcpy(raw->lamc[d], lc.data(), lc.size() * 8, cudaMemcpyHostToDevice)) ||
+          (e = prepare_mode_kernels(c)) || (e = prepare_mode_small(c.NT))) {
+        free_fd(raw);
+        return cuda_fail(e, "fd_setup: upload");
+      }
     }
+    {
+      const int64_t sb = std::max<int64_t>(1, max_batch);
+      const long long cap = 2 * ((long long)raw->n[2] * sb + 1);
+      fdp_status st = dalloc(&raw->sync, (size_t)cap);
+      if (st) {
+        free_fd(raw);
+        return st;
+      }
+      cudaError_t e = cudaMemset(raw->sync, 0, cap * sizeof(int));
+      if (e != cudaSuccess) {
+        free_fd(raw);
+        return cuda_fail(e, "fd_setup: sync init");
+      }
+      raw->sync_cap = cap;
+      raw->sync_batch = sb;
+    }
+    if (max_batch > 0) {
+      fdp_status st = dalloc(&raw->ws, (size_t)(2 * max_batch * Npad(raw)));
+      if (st) {
+        free_fd(raw);
+        return st;
+      }
+      raw->ws_batch = max_batch;
+    }
+    *out = raw;
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
   }
-  {
-    const int64_t sb = std::max<int64_t>(1, max_batch);
-    const long long cap = 2 * ((long long)raw->n[2] * sb + 1);
-    fdp_status st = dalloc(&raw->sync, (size_t)cap);
-    if (st) {
-      free_fd(raw);
-      return st;
-    }
-    cudaError_t e = cudaMemset(raw->sync, 0, cap * sizeof(int));
-    if (e != cudaSuccess) {
-      free_fd(raw);
-      return cuda_fail(e, "fd_setup: sync init");
-    }
-    raw->sync_cap = cap;
-    raw->sync_batch = sb;
-  }
-  if (max_batch > 0) {
-    fdp_status st = dalloc(&raw->ws, (size_t)(2 * max_batch * Npad(raw)));
-    if (st) {
-      free_fd(raw);
-      return st;
-    }
-    raw->ws_batch = max_batch;
-  }
-  *out = raw;
-  return FDP_OK;
 }
 
 extern "C" fdp_status fd_get_eigs(fdp_fd h, int d, double* U_out, double* lambda_out) {
-  if (!h) return fail(FDP_ERR_INVALID_ARG, "fd_get_eigs: NULL handle");
-  if (d < 0 || d >= h->D) return fail(FDP_ERR_SHAPE, "fd_get_eigs: d out of range");
-  if (U_out) std::memcpy(U_out, h->U_host[d].data(), h->U_host[d].size() * 8);
-  if (lambda_out) std::memcpy(lambda_out, h->lam_host[d].data(), h->lam_host[d].size() * 8);
-  return FDP_OK;
+  try {
+    if (!h) return fail(FDP_ERR_INVALID_ARG, "fd_get_eigs: NULL handle");
+    if (d < 0 || d >= h->D) return fail(FDP_ERR_SHAPE, "fd_get_eigs: d out of range");
+    if (U_out) std::memcpy(U_out, h->U_host[d].data(), h->U_host[d].size() * 8);
+    if (lambda_out) std::memcpy(lambda_out, h->lam_host[d].data(), h->lam_host[d].size() * 8);
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
 }
 
 // out[i] = sum_t c_t prod_d f_td[i_d] (i1 fastest) for per-direction diagonals f_td
@@ -344,34 +379,50 @@ static void kron_diag_accumulate(int D, const int* n, const std::vector<const do
 
 extern "C" fdp_status iga_geometry_coeffs(int kind, int D, int k, int nq, const double* x,
                                           double* c_out) {
-  const fdp_status st = geometry_coeffs_impl(kind, D, k, nq, x, c_out);
-  if (st == FDP_ERR_UNSUPPORTED) return fail(st, "iga_geometry_coeffs: the annulus map is 3D only");
-  if (st) return fail(st, "iga_geometry_coeffs: bad kind, k, nq or NULL pointer");
-  return FDP_OK;
+  try {
+    const fdp_status st = geometry_coeffs_impl(kind, D, k, nq, x, c_out);
+    if (st == FDP_ERR_UNSUPPORTED) return fail(st, "iga_geometry_coeffs: the annulus map is 3D only");
+    if (st) return fail(st, "iga_geometry_coeffs: bad kind, k, nq or NULL pointer");
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
 }
 
 extern "C" fdp_status iga_separable_fit(int D, const int32_t* nq, const double* const* c,
                                         int max_sweeps, double tol, double* tau, double* mu,
                                         int* sweeps) {
-  const fdp_status st = separable_fit_impl(D, nq, c, max_sweeps, tol, tau, mu, sweeps);
-  if (st) return fail(st, "iga_separable_fit: bad arguments or a sample <= 0 (logs undefined)");
-  return FDP_OK;
+  try {
+    const fdp_status st = separable_fit_impl(D, nq, c, max_sweeps, tol, tau, mu, sweeps);
+    if (st) return fail(st, "iga_separable_fit: bad arguments or a sample <= 0 (logs undefined)");
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
 }
 
 extern "C" fdp_status fd_operator_diagonal(fdp_fd h, double* out) {
-  if (!h || !out) return fail(FDP_ERR_INVALID_ARG, "fd_operator_diagonal: NULL argument");
-  std::fill(out, out + h->N, 0.0);
-  for (int d = 0; d < h->D; ++d) {
-    std::vector<const double*> f(h->D);
-    for (int e = 0; e < h->D; ++e) f[e] = e == d ? h->dK[e].data() : h->dM[e].data();
-    kron_diag_accumulate(h->D, h->n, f, h->coef[d], out);
+  try {
+    if (!h || !out) return fail(FDP_ERR_INVALID_ARG, "fd_operator_diagonal: NULL argument");
+    std::fill(out, out + h->N, 0.0);
+    for (int d = 0; d < h->D; ++d) {
+      std::vector<const double*> f(h->D);
+      for (int e = 0; e < h->D; ++e) f[e] = e == d ? h->dK[e].data() : h->dM[e].data();
+      kron_diag_accumulate(h->D, h->n, f, h->coef[d], out);
+    }
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
   }
-  return FDP_OK;
 }
 
 extern "C" int64_t fd_size(fdp_fd h) { return h ? h->N : 0; }
 extern "C" size_t fd_workspace_bytes(fdp_fd h, int64_t batch) {
-  return h && batch > 0 ? (size_t)(2 * batch * Npad(h)) * sizeof(double) : 0;
+  try {
+    return h && batch > 0 ? (size_t)(2 * batch * Npad(h)) * sizeof(double) : 0;
+  } catch (...) {
+    return 0;
+  }
 }
 
 // One FD problem inside a grouped stage: mode d (0-based), direction fwd/bwd. xld / yld: fiber
@@ -700,39 +751,47 @@ static cudaError_t enqueue_fd(const std::vector<const fdp_fd_s*>& hs,
 
 extern "C" fdp_status fd_apply(fdp_fd h, const double* b, double* x, const double* dscale,
                                int64_t batch, void* workspace, void* stream) {
-  if (!h) return fail(FDP_ERR_INVALID_ARG, "fd_apply: NULL handle");
-  if (batch < 0) return fail(FDP_ERR_SHAPE, "fd_apply: batch < 0");
-  if (batch == 0) return FDP_OK;
-  if (!is_device_ptr(b) || !is_device_ptr(x))
-    return fail(FDP_ERR_INVALID_ARG, "fd_apply: b and x must be device pointers");
-  if (dscale && !is_device_ptr(dscale))
-    return fail(FDP_ERR_INVALID_ARG, "fd_apply: dscale must be a device pointer");
-  double* T = static_cast<double*>(workspace);
-  if (!T) {
-    if (batch > h->ws_batch) return fail(FDP_ERR_SHAPE, "fd_apply: batch exceeds handle max_batch and no workspace given");
-    T = h->ws;
-  } else if (!is_device_ptr(T)) {
-    return fail(FDP_ERR_INVALID_ARG, "fd_apply: workspace must be device memory");
+  try {
+    if (!h) return fail(FDP_ERR_INVALID_ARG, "fd_apply: NULL handle");
+    if (batch < 0) return fail(FDP_ERR_SHAPE, "fd_apply: batch < 0");
+    if (batch == 0) return FDP_OK;
+    if (!is_device_ptr(b) || !is_device_ptr(x))
+      return fail(FDP_ERR_INVALID_ARG, "fd_apply: b and x must be device pointers");
+    if (dscale && !is_device_ptr(dscale))
+      return fail(FDP_ERR_INVALID_ARG, "fd_apply: dscale must be a device pointer");
+    double* T = static_cast<double*>(workspace);
+    if (!T) {
+      if (batch > h->ws_batch) return fail(FDP_ERR_SHAPE, "fd_apply: batch exceeds handle max_batch and no workspace given");
+      T = h->ws;
+    } else if (!is_device_ptr(T)) {
+      return fail(FDP_ERR_INVALID_ARG, "fd_apply: workspace must be device memory");
+    }
+    DeviceGuard dg(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const double* src = b;
+    if (dscale) {  // x <- D^{-1/2} b, then the transforms read x
+      FDP_CUDA(launch_scale(b, x, dscale, h->N, batch, h->N, h->N, s), "fd_apply: prescale");
+      src = x;
+    }
+    const bool sy = batch <= h->sync_batch;
+    FDP_CUDA(enqueue_fd({h}, {src}, h->N, {x}, h->N, {T}, {dscale}, batch, s, nullptr, nullptr,
+                        nullptr, sy ? h->sync : nullptr, sy ? h->sync_cap : 0),
+             "fd_apply");
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
   }
-  DeviceGuard dg(h->device);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const double* src = b;
-  if (dscale) {  // x <- D^{-1/2} b, then the transforms read x
-    FDP_CUDA(launch_scale(b, x, dscale, h->N, batch, h->N, h->N, s), "fd_apply: prescale");
-    src = x;
-  }
-  const bool sy = batch <= h->sync_batch;
-  FDP_CUDA(enqueue_fd({h}, {src}, h->N, {x}, h->N, {T}, {dscale}, batch, s, nullptr, nullptr,
-                      nullptr, sy ? h->sync : nullptr, sy ? h->sync_cap : 0),
-           "fd_apply");
-  return FDP_OK;
 }
 
 extern "C" fdp_status fd_destroy(fdp_fd h) {
-  if (!h) return FDP_OK;
-  DeviceGuard dg(h->device);
-  free_fd(h);
-  return FDP_OK;
+  try {
+    if (!h) return FDP_OK;
+    DeviceGuard dg(h->device);
+    free_fd(h);
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -762,54 +821,58 @@ static void free_mass(fdp_mass h) {
 
 extern "C" fdp_status kron_mass_setup(int D, const int32_t* n, const double* const* M, int device,
                                       fdp_mass* out) {
-  if (!out) return fail(FDP_ERR_INVALID_ARG, "kron_mass_setup: out is NULL");
-  *out = nullptr;
-  if (D < 2 || D > 3) return fail(FDP_ERR_UNSUPPORTED, "kron_mass_setup: D must be 2 or 3");
-  if (!n || !M) return fail(FDP_ERR_INVALID_ARG, "kron_mass_setup: NULL argument");
-  std::unique_ptr<fdp_mass_s> h(new (std::nothrow) fdp_mass_s);
-  if (!h) return fail(FDP_ERR_OOM, "kron_mass_setup: host allocation");
-  h->D = D;
-  h->device = device;
-  h->N = 1;
-  std::vector<double> Lb[3], invd[3], Mb[3];
-  for (int d = 0; d < D; ++d) {
-    if (n[d] < 1 || n[d] > 1 << 20) return fail(FDP_ERR_SHAPE, "kron_mass_setup: n[d] out of range");
-    if (!M[d]) return fail(FDP_ERR_INVALID_ARG, "kron_mass_setup: NULL M[d]");
-    if (!symmetric(n[d], M[d])) return fail(FDP_ERR_NOT_SPD, "kron_mass_setup: M[d] not symmetric");
-    h->n[d] = n[d];
-    h->N *= n[d];
-    const int b = detect_bandwidth(n[d], M[d]);
-    if (b > 15) return fail(FDP_ERR_UNSUPPORTED, "kron_mass_setup: half bandwidth > 15");
-    h->band[d] = b;
-    std::string err;
-    int st = band_cholesky(n[d], b, M[d], &Lb[d], &invd[d], &err);
-    if (st) return fail((fdp_status)st, "kron_mass_setup: " + err);
-    Mb[d].assign((size_t)n[d] * (2 * b + 1), 0.0);
-    for (int i = 0; i < n[d]; ++i)
-      for (int j = std::max(0, i - b); j <= std::min(n[d] - 1, i + b); ++j)
-        Mb[d][(size_t)i * (2 * b + 1) + (j - i + b)] = M[d][i + (size_t)n[d] * j];
-  }
-  DeviceGuard dg(device);
-  if (!dg.ok) return fail(FDP_ERR_CUDA, "kron_mass_setup: cannot select device");
-  fdp_mass raw = h.release();
-  for (int d = 0; d < D; ++d) raw->Lb_host[d] = Lb[d];
-  for (int d = 0; d < D; ++d) {
-    fdp_status st;
-    if ((st = dalloc(&raw->Lb[d], Lb[d].size())) || (st = dalloc(&raw->invd[d], invd[d].size())) ||
-        (st = dalloc(&raw->Mb[d], Mb[d].size()))) {
-      free_mass(raw);
-      return st;
+  try {
+    if (!out) return fail(FDP_ERR_INVALID_ARG, "kron_mass_setup: out is NULL");
+    *out = nullptr;
+    if (D < 2 || D > 3) return fail(FDP_ERR_UNSUPPORTED, "kron_mass_setup: D must be 2 or 3");
+    if (!n || !M) return fail(FDP_ERR_INVALID_ARG, "kron_mass_setup: NULL argument");
+    std::unique_ptr<fdp_mass_s> h(new (std::nothrow) fdp_mass_s);
+    if (!h) return fail(FDP_ERR_OOM, "kron_mass_setup: host allocation");
+    h->D = D;
+    h->device = device;
+    h->N = 1;
+    std::vector<double> Lb[3], invd[3], Mb[3];
+    for (int d = 0; d < D; ++d) {
+      if (n[d] < 1 || n[d] > 1 << 20) return fail(FDP_ERR_SHAPE, "kron_mass_setup: n[d] out of range");
+      if (!M[d]) return fail(FDP_ERR_INVALID_ARG, "kron_mass_setup: NULL M[d]");
+      if (!symmetric(n[d], M[d])) return fail(FDP_ERR_NOT_SPD, "kron_mass_setup: M[d] not symmetric");
+      h->n[d] = n[d];
+      h->N *= n[d];
+      const int b = detect_bandwidth(n[d], M[d]);
+      if (b > 15) return fail(FDP_ERR_UNSUPPORTED, "kron_mass_setup: half bandwidth > 15");
+      h->band[d] = b;
+      std::string err;
+      int st = band_cholesky(n[d], b, M[d], &Lb[d], &invd[d], &err);
+      if (st) return fail((fdp_status)st, "kron_mass_setup: " + err);
+      Mb[d].assign((size_t)n[d] * (2 * b + 1), 0.0);
+      for (int i = 0; i < n[d]; ++i)
+        for (int j = std::max(0, i - b); j <= std::min(n[d] - 1, i + b); ++j)
+          Mb[d][(size_t)i * (2 * b + 1) + (j - i + b)] = M[d][i + (size_t)n[d] * j];
     }
-    cudaError_t e;
-    if ((e = cudaMemcpy(raw->Lb[d], Lb[d].data(), Lb[d].size() * 8, cudaMemcpyHostToDevice)) ||
-        (e = cudaMemcpy(raw->invd[d], invd[d].data(), invd[d].size() * 8, cudaMemcpyHostToDevice)) ||
-        (e = cudaMemcpy(raw->Mb[d], Mb[d].data(), Mb[d].size() * 8, cudaMemcpyHostToDevice))) {
-      free_mass(raw);
-      return cuda_fail(e, "kron_mass_setup: upload");
+    DeviceGuard dg(device);
+    if (!dg.ok) return fail(FDP_ERR_CUDA, "kron_mass_setup: cannot select device");
+    fdp_mass raw = h.release();
+    for (int d = 0; d < D; ++d) raw->Lb_host[d] = Lb[d];
+    for (int d = 0; d < D; ++d) {
+      fdp_status st;
+      if ((st = dalloc(&raw->Lb[d], Lb[d].size())) || (st = dalloc(&raw->invd[d], invd[d].size())) ||
+          (st = dalloc(&raw->Mb[d], Mb[d].size()))) {
+        free_mass(raw);
+        return st;
+      }
+      cudaError_t e;
+      if ((e = cudaMemcpy(raw->Lb[d], Lb[d].data(), Lb[d].size() * 8, cudaMemcpyHostToDevice)) ||
+          (e = cudaMemcpy(raw->invd[d], invd[d].data(), invd[d].size() * 8, cudaMemcpyHostToDevice)) ||
+          (e = cudaMemcpy(raw->Mb[d], Mb[d].data(), Mb[d].size() * 8, cudaMemcpyHostToDevice))) {
+        free_mass(raw);
+        return cuda_fail(e, "kron_mass_setup: upload");
+      }
     }
+    *out = raw;
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
   }
-  *out = raw;
-  return FDP_OK;
 }
 
 extern "C" int64_t kron_mass_size(fdp_mass h) { return h ? h->N : 0; }
@@ -853,63 +916,71 @@ static cudaError_t enqueue_mass(const fdp_mass_s* h, int mode, const double* in,
 
 extern "C" fdp_status kron_mass_apply(fdp_mass h, int mode, const double* b, double* x,
                                       const double* dscale, int64_t batch, void* stream) {
-  if (!h) return fail(FDP_ERR_INVALID_ARG, "kron_mass_apply: NULL handle");
-  if (mode != FDP_MASS_INVERSE && mode != FDP_MASS_FORWARD)
-    return fail(FDP_ERR_INVALID_ARG, "kron_mass_apply: bad mode");
-  if (batch < 0) return fail(FDP_ERR_SHAPE, "kron_mass_apply: batch < 0");
-  if (batch == 0) return FDP_OK;
-  if (!is_device_ptr(b) || !is_device_ptr(x))
-    return fail(FDP_ERR_INVALID_ARG, "kron_mass_apply: b and x must be device pointers");
-  if (mode == FDP_MASS_FORWARD) {
-    if (dscale) return fail(FDP_ERR_INVALID_ARG, "kron_mass_apply: FORWARD takes no dscale");
-    if (b == x) return fail(FDP_ERR_INVALID_ARG, "kron_mass_apply: FORWARD cannot run in place");
-  }
-  if (dscale && !is_device_ptr(dscale))
-    return fail(FDP_ERR_INVALID_ARG, "kron_mass_apply: dscale must be a device pointer");
-  DeviceGuard dg(h->device);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (mode == FDP_MASS_FORWARD) {
-    // out-of-place stencil per mode: b -> x (d=0), x -> tmp (d=1), tmp -> x (d=2) ...
-    double* tmp = nullptr;
-    FDP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tmp), (size_t)(h->N * batch) * 8, s),
-             "kron_mass_apply: temporary");
-    const double* src = b;
-    for (int d = 0; d < h->D; ++d) {
-      double* dst = ((h->D - d) % 2 == 1) ? x : tmp;
-      MassMode m{};
-      long long P = 1, Q = 1;
-      for (int e = 0; e < d; ++e) P *= h->n[e];
-      for (int e = d + 1; e < h->D; ++e) Q *= h->n[e];
-      m.in = src;
-      m.out = dst;
-      m.Mb = h->Mb[d];
-      m.N = h->N;
-      m.bs = h->N;
-      m.P = (int)P;
-      m.n = h->n[d];
-      m.Q = (int)Q;
-      m.batch = (int)batch;
-      m.band = h->band[d];
-      m.forward = 1;
-      cudaError_t e = launch_mass_mode(m, s);
-      if (e != cudaSuccess) {
-        cudaFreeAsync(tmp, s);
-        return cuda_fail(e, "kron_mass_apply");
-      }
-      src = dst;
+  try {
+    if (!h) return fail(FDP_ERR_INVALID_ARG, "kron_mass_apply: NULL handle");
+    if (mode != FDP_MASS_INVERSE && mode != FDP_MASS_FORWARD)
+      return fail(FDP_ERR_INVALID_ARG, "kron_mass_apply: bad mode");
+    if (batch < 0) return fail(FDP_ERR_SHAPE, "kron_mass_apply: batch < 0");
+    if (batch == 0) return FDP_OK;
+    if (!is_device_ptr(b) || !is_device_ptr(x))
+      return fail(FDP_ERR_INVALID_ARG, "kron_mass_apply: b and x must be device pointers");
+    if (mode == FDP_MASS_FORWARD) {
+      if (dscale) return fail(FDP_ERR_INVALID_ARG, "kron_mass_apply: FORWARD takes no dscale");
+      if (b == x) return fail(FDP_ERR_INVALID_ARG, "kron_mass_apply: FORWARD cannot run in place");
     }
-    FDP_CUDA(cudaFreeAsync(tmp, s), "kron_mass_apply: free");
+    if (dscale && !is_device_ptr(dscale))
+      return fail(FDP_ERR_INVALID_ARG, "kron_mass_apply: dscale must be a device pointer");
+    DeviceGuard dg(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (mode == FDP_MASS_FORWARD) {
+      // out-of-place stencil per mode: b -> x (d=0), x -> tmp (d=1), tmp -> x (d=2) ...
+      double* tmp = nullptr;
+      FDP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tmp), (size_t)(h->N * batch) * 8, s),
+               "kron_mass_apply: temporary");
+      const double* src = b;
+      for (int d = 0; d < h->D; ++d) {
+        double* dst = ((h->D - d) % 2 == 1) ? x : tmp;
+        MassMode m{};
+        long long P = 1, Q = 1;
+        for (int e = 0; e < d; ++e) P *= h->n[e];
+        for (int e = d + 1; e < h->D; ++e) Q *= h->n[e];
+        m.in = src;
+        m.out = dst;
+        m.Mb = h->Mb[d];
+        m.N = h->N;
+        m.bs = h->N;
+        m.P = (int)P;
+        m.n = h->n[d];
+        m.Q = (int)Q;
+        m.batch = (int)batch;
+        m.band = h->band[d];
+        m.forward = 1;
+        cudaError_t e = launch_mass_mode(m, s);
+        if (e != cudaSuccess) {
+          cudaFreeAsync(tmp, s);
+          return cuda_fail(e, "kron_mass_apply");
+        }
+        src = dst;
+      }
+      FDP_CUDA(cudaFreeAsync(tmp, s), "kron_mass_apply: free");
+      return FDP_OK;
+    }
+    FDP_CUDA(enqueue_mass(h, mode, b, x, h->N, dscale, batch, s, nullptr), "kron_mass_apply");
     return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
   }
-  FDP_CUDA(enqueue_mass(h, mode, b, x, h->N, dscale, batch, s, nullptr), "kron_mass_apply");
-  return FDP_OK;
 }
 
 extern "C" fdp_status kron_mass_destroy(fdp_mass h) {
-  if (!h) return FDP_OK;
-  DeviceGuard dg(h->device);
-  free_mass(h);
-  return FDP_OK;
+  try {
+    if (!h) return FDP_OK;
+    DeviceGuard dg(h->device);
+    free_mass(h);
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -995,99 +1066,103 @@ static void free_block(fdp_block h) {
 extern "C" fdp_status block_precond_setup(int D, const fdp_fd* vel, fdp_mass pres,
                                           const double* dscale_vel, const double* dscale_pres,
                                           fdp_block* out) {
-  if (!out) return fail(FDP_ERR_INVALID_ARG, "block_precond_setup: out is NULL");
-  *out = nullptr;
-  if (D < 2 || D > 3) return fail(FDP_ERR_UNSUPPORTED, "block_precond_setup: D must be 2 or 3");
-  if (!vel || !pres) return fail(FDP_ERR_INVALID_ARG, "block_precond_setup: NULL handle");
-  std::unique_ptr<fdp_block_s> h(new (std::nothrow) fdp_block_s);
-  if (!h) return fail(FDP_ERR_OOM, "block_precond_setup: host allocation");
-  h->D = D;
-  h->device = pres->device;
-  h->pres = pres;
-  long long o = 0;
-  for (int k = 0; k < D; ++k) {
-    if (!vel[k]) return fail(FDP_ERR_INVALID_ARG, "block_precond_setup: NULL velocity handle");
-    if (vel[k]->D != D) return fail(FDP_ERR_SHAPE, "block_precond_setup: velocity handle dimension != D");
-    if (vel[k]->device != h->device) return fail(FDP_ERR_INVALID_ARG, "block_precond_setup: handles on different devices");
-    h->vel.push_back(vel[k]);
+  try {
+    if (!out) return fail(FDP_ERR_INVALID_ARG, "block_precond_setup: out is NULL");
+    *out = nullptr;
+    if (D < 2 || D > 3) return fail(FDP_ERR_UNSUPPORTED, "block_precond_setup: D must be 2 or 3");
+    if (!vel || !pres) return fail(FDP_ERR_INVALID_ARG, "block_precond_setup: NULL handle");
+    std::unique_ptr<fdp_block_s> h(new (std::nothrow) fdp_block_s);
+    if (!h) return fail(FDP_ERR_OOM, "block_precond_setup: host allocation");
+    h->D = D;
+    h->device = pres->device;
+    h->pres = pres;
+    long long o = 0;
+    for (int k = 0; k < D; ++k) {
+      if (!vel[k]) return fail(FDP_ERR_INVALID_ARG, "block_precond_setup: NULL velocity handle");
+      if (vel[k]->D != D) return fail(FDP_ERR_SHAPE, "block_precond_setup: velocity handle dimension != D");
+      if (vel[k]->device != h->device) return fail(FDP_ERR_INVALID_ARG, "block_precond_setup: handles on different devices");
+      h->vel.push_back(vel[k]);
+      h->off.push_back(o);
+      o += vel[k]->N;
+    }
+    if (pres->D != D) return fail(FDP_ERR_SHAPE, "block_precond_setup: pressure handle dimension != D");
+    h->nvel = o;
     h->off.push_back(o);
-    o += vel[k]->N;
-  }
-  if (pres->D != D) return fail(FDP_ERR_SHAPE, "block_precond_setup: pressure handle dimension != D");
-  h->nvel = o;
-  h->off.push_back(o);
-  o += pres->N;
-  h->off.push_back(o);
-  h->size = o;
-  if ((dscale_vel && is_device_ptr(dscale_vel)) || (dscale_pres && is_device_ptr(dscale_pres)))
-    return fail(FDP_ERR_INVALID_ARG, "block_precond_setup: dscale vectors must be host arrays");
-  DeviceGuard dg(h->device);
-  fdp_block raw = h.release();
-  auto upload_isqrt = [&](const double* src, long long n, double** dst) -> fdp_status {
-    std::vector<double> v(n);
-    for (long long i = 0; i < n; ++i) {
-      if (!(src[i] > 0.0)) return fail(FDP_ERR_INVALID_ARG, "block_precond_setup: dscale entries must be > 0");
-      v[i] = 1.0 / std::sqrt(src[i]);
+    o += pres->N;
+    h->off.push_back(o);
+    h->size = o;
+    if ((dscale_vel && is_device_ptr(dscale_vel)) || (dscale_pres && is_device_ptr(dscale_pres)))
+      return fail(FDP_ERR_INVALID_ARG, "block_precond_setup: dscale vectors must be host arrays");
+    DeviceGuard dg(h->device);
+    fdp_block raw = h.release();
+    auto upload_isqrt = [&](const double* src, long long n, double** dst) -> fdp_status {
+      std::vector<double> v(n);
+      for (long long i = 0; i < n; ++i) {
+        if (!(src[i] > 0.0)) return fail(FDP_ERR_INVALID_ARG, "block_precond_setup: dscale entries must be > 0");
+        v[i] = 1.0 / std::sqrt(src[i]);
+      }
+      fdp_status st = dalloc(dst, (size_t)n);
+      if (st) return st;
+      cudaError_t e = cudaMemcpy(*dst, v.data(), n * 8, cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) return cuda_fail(e, "block_precond_setup: upload");
+      return FDP_OK;
+    };
+    fdp_status st = FDP_OK;
+    if (dscale_vel) st = upload_isqrt(dscale_vel, raw->nvel, &raw->dv);
+    if (!st && dscale_pres) st = upload_isqrt(dscale_pres, pres->N, &raw->dq);
+    // P_Q by dense per-mode inverses when every factor is small (2 n flops/entry/mode beat the
+    // banded recurrences' latency and ride in the velocity launches); banded otherwise.
+    const char* env = std::getenv("FDP_PRESSURE");
+    bool dense = true;
+    for (int d = 0; d < D; ++d) dense = dense && pres->n[d] <= 160;
+    if (env && std::string(env) == "banded") dense = false;
+    if (env && std::string(env) == "dense") dense = true;
+    for (int d = 0; d < D && dense; ++d)
+      for (int k = 1; k < D; ++k) dense = dense && raw->vel[k]->cfg[d].NT == raw->vel[0]->cfg[d].NT;
+    if (!st && dense) {
+      raw->pres_dense = true;
+      for (int d = 0; d < D && !st; ++d) {
+        const int nq = pres->n[d];
+        const TileCfg& vc = raw->vel[0]->cfg[d];
+        const int BN = 8 * vc.NT;
+        raw->q_tiles_n[d] = (nq + BN - 1) / BN;
+        raw->q_ldw[d] = raw->q_tiles_n[d] * BN;
+        const int kpad = ((nq + 15) / 16) * 16;
+        std::vector<double> X;
+        spd_inverse_from_band(nq, pres->band[d], pres->Lb_host[d], &X);
+        std::vector<double> w((size_t)kpad * raw->q_ldw[d], 0.0);
+        for (int k = 0; k < nq; ++k)
+          for (int a = 0; a < nq; ++a) w[(size_t)k * raw->q_ldw[d] + a] = X[a + (size_t)nq * k];
+        st = dalloc(&raw->Wq[d], w.size());
+        if (!st) {
+          cudaError_t e = cudaMemcpy(raw->Wq[d], w.data(), w.size() * 8, cudaMemcpyHostToDevice);
+          if (e != cudaSuccess) st = cuda_fail(e, "block_precond_setup: upload");
+        }
+      }
+      if (!st && (dscale_vel || dscale_pres)) {
+        std::vector<double> v(raw->size, 1.0);
+        for (long long i = 0; i < raw->nvel && dscale_vel; ++i) v[i] = 1.0 / std::sqrt(dscale_vel[i]);
+        for (long long i = 0; i < pres->N && dscale_pres; ++i) v[raw->nvel + i] = 1.0 / std::sqrt(dscale_pres[i]);
+        st = dalloc(&raw->dall, v.size());
+        if (!st) {
+          cudaError_t e = cudaMemcpy(raw->dall, v.data(), v.size() * 8, cudaMemcpyHostToDevice);
+          if (e != cudaSuccess) st = cuda_fail(e, "block_precond_setup: upload");
+        }
+      }
     }
-    fdp_status st = dalloc(dst, (size_t)n);
-    if (st) return st;
-    cudaError_t e = cudaMemcpy(*dst, v.data(), n * 8, cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) return cuda_fail(e, "block_precond_setup: upload");
+    if (!st) {
+      cudaError_t e = cudaStreamCreateWithFlags(&raw->cap, cudaStreamNonBlocking);
+      if (e != cudaSuccess) st = cuda_fail(e, "block_precond_setup: stream");
+    }
+    if (st) {
+      free_block(raw);
+      return st;
+    }
+    *out = raw;
     return FDP_OK;
-  };
-  fdp_status st = FDP_OK;
-  if (dscale_vel) st = upload_isqrt(dscale_vel, raw->nvel, &raw->dv);
-  if (!st && dscale_pres) st = upload_isqrt(dscale_pres, pres->N, &raw->dq);
-  // P_Q by dense per-mode inverses when every factor is small (2 n flops/entry/mode beat the
-  // banded recurrences' latency and ride in the velocity launches); banded otherwise.
-  const char* env = std::getenv("FDP_PRESSURE");
-  bool dense = true;
-  for (int d = 0; d < D; ++d) dense = dense && pres->n[d] <= 160;
-  if (env && std::string(env) == "banded") dense = false;
-  if (env && std::string(env) == "dense") dense = true;
-  for (int d = 0; d < D && dense; ++d)
-    for (int k = 1; k < D; ++k) dense = dense && raw->vel[k]->cfg[d].NT == raw->vel[0]->cfg[d].NT;
-  if (!st && dense) {
-    raw->pres_dense = true;
-    for (int d = 0; d < D && !st; ++d) {
-      const int nq = pres->n[d];
-      const TileCfg& vc = raw->vel[0]->cfg[d];
-      const int BN = 8 * vc.NT;
-      raw->q_tiles_n[d] = (nq + BN - 1) / BN;
-      raw->q_ldw[d] = raw->q_tiles_n[d] * BN;
-      const int kpad = ((nq + 15) / 16) * 16;
-      std::vector<double> X;
-      spd_inverse_from_band(nq, pres->band[d], pres->Lb_host[d], &X);
-      std::vector<double> w((size_t)kpad * raw->q_ldw[d], 0.0);
-      for (int k = 0; k < nq; ++k)
-        for (int a = 0; a < nq; ++a) w[(size_t)k * raw->q_ldw[d] + a] = X[a + (size_t)nq * k];
-      st = dalloc(&raw->Wq[d], w.size());
-      if (!st) {
-        cudaError_t e = cudaMemcpy(raw->Wq[d], w.data(), w.size() * 8, cudaMemcpyHostToDevice);
-        if (e != cudaSuccess) st = cuda_fail(e, "block_precond_setup: upload");
-      }
-    }
-    if (!st && (dscale_vel || dscale_pres)) {
-      std::vector<double> v(raw->size, 1.0);
-      for (long long i = 0; i < raw->nvel && dscale_vel; ++i) v[i] = 1.0 / std::sqrt(dscale_vel[i]);
-      for (long long i = 0; i < pres->N && dscale_pres; ++i) v[raw->nvel + i] = 1.0 / std::sqrt(dscale_pres[i]);
-      st = dalloc(&raw->dall, v.size());
-      if (!st) {
-        cudaError_t e = cudaMemcpy(raw->dall, v.data(), v.size() * 8, cudaMemcpyHostToDevice);
-        if (e != cudaSuccess) st = cuda_fail(e, "block_precond_setup: upload");
-      }
-    }
+  } catch (...) {
+    return abi_exception(__func__);
   }
-  if (!st) {
-    cudaError_t e = cudaStreamCreateWithFlags(&raw->cap, cudaStreamNonBlocking);
-    if (e != cudaSuccess) st = cuda_fail(e, "block_precond_setup: stream");
-  }
-  if (st) {
-    free_block(raw);
-    return st;
-  }
-  *out = raw;
-  return FDP_OK;
 }
 
 extern "C" int64_t block_precond_size(fdp_block h) { return h ? h->size : 0; }
@@ -1097,7 +1172,11 @@ static long long block_ws_elems(const fdp_block_s* h, int64_t batch) {
   return batch * (v + (h->pres_dense ? 2 * h->pres->N : 0));
 }
 extern "C" size_t block_precond_workspace_bytes(fdp_block h, int64_t batch) {
-  return h && batch > 0 ? (size_t)block_ws_elems(h, batch) * sizeof(double) : 0;
+  try {
+    return h && batch > 0 ? (size_t)block_ws_elems(h, batch) * sizeof(double) : 0;
+  } catch (...) {
+    return 0;
+  }
 }
 
 static cudaError_t enqueue_block(fdp_block h, const double* r, double* s, int64_t batch, double* ws,
@@ -1199,138 +1278,154 @@ static cudaError_t enqueue_block(fdp_block h, const double* r, double* s, int64_
 }
 
 extern "C" fdp_status block_precond_profile(fdp_block h, int enable) {
-  if (!h) return fail(FDP_ERR_INVALID_ARG, "block_precond_profile: NULL handle");
-  std::lock_guard<std::mutex> lk(h->mu);
-  DeviceGuard dg(h->device);
-  if (enable && h->ev.empty()) {
-    h->ev.resize(64);
-    for (auto& e : h->ev) FDP_CUDA(cudaEventCreate(&e), "block_precond_profile: event");
+  try {
+    if (!h) return fail(FDP_ERR_INVALID_ARG, "block_precond_profile: NULL handle");
+    std::lock_guard<std::mutex> lk(h->mu);
+    DeviceGuard dg(h->device);
+    if (enable && h->ev.empty()) {
+      h->ev.resize(64);
+      for (auto& e : h->ev) FDP_CUDA(cudaEventCreate(&e), "block_precond_profile: event");
+    }
+    if ((enable != 0) != h->prof) {
+      h->prof = enable != 0;
+      for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);  // re-capture with / without events
+      h->graphs.clear();
+    }
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
   }
-  if ((enable != 0) != h->prof) {
-    h->prof = enable != 0;
-    for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);  // re-capture with / without events
-    h->graphs.clear();
-  }
-  return FDP_OK;
 }
 
 extern "C" int block_precond_profile_read(fdp_block h, int max, int32_t* kind, float* ms,
                                           double* flops, double* bytes) {
-  if (!h || !h->prof) return -1;
-  std::lock_guard<std::mutex> lk(h->mu);
-  DeviceGuard dg(h->device);
-  const int n = (int)h->info.size();
-  for (int i = 0; i < n && i < max; ++i) {
-    if (kind) kind[i] = h->info[i].kind;
-    if (flops) flops[i] = h->info[i].flops;
-    if (bytes) bytes[i] = h->info[i].bytes;
-    if (ms) {
-      float t = 0.f;
-      if (cudaEventElapsedTime(&t, h->ev[i], h->ev[i + 1]) != cudaSuccess) {
-        cudaGetLastError();
-        return -1;
+  try {
+    if (!h || !h->prof) return -1;
+    std::lock_guard<std::mutex> lk(h->mu);
+    DeviceGuard dg(h->device);
+    const int n = (int)h->info.size();
+    for (int i = 0; i < n && i < max; ++i) {
+      if (kind) kind[i] = h->info[i].kind;
+      if (flops) flops[i] = h->info[i].flops;
+      if (bytes) bytes[i] = h->info[i].bytes;
+      if (ms) {
+        float t = 0.f;
+        if (cudaEventElapsedTime(&t, h->ev[i], h->ev[i + 1]) != cudaSuccess) {
+          cudaGetLastError();
+          return -1;
+        }
+        ms[i] = t;
       }
-      ms[i] = t;
     }
+    return n;
+  } catch (...) {
+    return -1;
   }
-  return n;
 }
 
 extern "C" int fdp_block_launch_count(fdp_block h, int64_t batch) {
-  if (!h || batch <= 0) return 0;
-  int n = 0;
-  int D = h->D;
-  n += h->dv ? 1 : 0;
-  for (int d = 0; d < D; ++d) {
-    // components with equal tile config share a launch
-    std::vector<int> nts;
-    for (int k = 0; k < D; ++k) nts.push_back(h->vel[k]->cfg[d].NT);
-    std::sort(nts.begin(), nts.end());
-    int groups = (int)(std::unique(nts.begin(), nts.end()) - nts.begin());
-    n += 2 * groups;
+  try {
+    if (!h || batch <= 0) return 0;
+    int n = 0;
+    int D = h->D;
+    n += h->dv ? 1 : 0;
+    for (int d = 0; d < D; ++d) {
+      // components with equal tile config share a launch
+      std::vector<int> nts;
+      for (int k = 0; k < D; ++k) nts.push_back(h->vel[k]->cfg[d].NT);
+      std::sort(nts.begin(), nts.end());
+      int groups = (int)(std::unique(nts.begin(), nts.end()) - nts.begin());
+      n += 2 * groups;
+    }
+    bool fuse = std::getenv("FDP_NO_FUSE") == nullptr && std::getenv("FDP_NO_SMALL") == nullptr;
+    for (int k = 0; k < D; ++k)
+      for (int d = 0; d < D; ++d) fuse = fuse && h->vel[k]->n[d] <= kSmallMaxN && h->vel[k]->cfg[d].tiles_n == 1;
+    if (fuse) n -= 1;
+    bool pp = fuse && D == 3 && std::getenv("FDP_PP") != nullptr;
+    for (int k = 0; k < D; ++k)
+      for (int d = 0; d < 2; ++d)
+        pp = pp && h->vel[k]->cfg[d].NT <= kPPMaxNT && h->vel[k]->cfg[d].NT == h->vel[0]->cfg[0].NT;
+    if (pp) n -= 2;
+    if (!h->pres_dense) n += h->pres->D;
+    else if (h->dall) n += h->dv ? 0 : 1;
+    return n;
+  } catch (...) {
+    return -1;
   }
-  bool fuse = std::getenv("FDP_NO_FUSE") == nullptr && std::getenv("FDP_NO_SMALL") == nullptr;
-  for (int k = 0; k < D; ++k)
-    for (int d = 0; d < D; ++d) fuse = fuse && h->vel[k]->n[d] <= kSmallMaxN && h->vel[k]->cfg[d].tiles_n == 1;
-  if (fuse) n -= 1;
-  bool pp = fuse && D == 3 && std::getenv("FDP_PP") != nullptr;
-  for (int k = 0; k < D; ++k)
-    for (int d = 0; d < 2; ++d)
-      pp = pp && h->vel[k]->cfg[d].NT <= kPPMaxNT && h->vel[k]->cfg[d].NT == h->vel[0]->cfg[0].NT;
-  if (pp) n -= 2;
-  if (!h->pres_dense) n += h->pres->D;
-  else if (h->dall) n += h->dv ? 0 : 1;
-  return n;
 }
 
 extern "C" fdp_status block_precond_apply(fdp_block h, const double* r, double* s, int64_t batch,
                                           void* workspace, void* stream) {
-  if (!h) return fail(FDP_ERR_INVALID_ARG, "block_precond_apply: NULL handle");
-  if (batch < 0) return fail(FDP_ERR_SHAPE, "block_precond_apply: batch < 0");
-  if (batch == 0) return FDP_OK;
-  std::lock_guard<std::mutex> lk(h->mu);
-  fdp_block_s::GraphEntry* hit = nullptr;
-  for (auto& g : h->graphs)
-    if (g.r == r && g.s == s && g.ws == workspace && g.batch == batch) hit = &g;
-  const bool same = hit != nullptr;
-  if (!same) {
-    if (!is_device_ptr(r) || !is_device_ptr(s))
-      return fail(FDP_ERR_INVALID_ARG, "block_precond_apply: r and s must be device pointers");
-    if (!workspace || !is_device_ptr(workspace))
-      return fail(FDP_ERR_INVALID_ARG, "block_precond_apply: workspace must be device memory");
-  }
-  DeviceGuard dg(h->device);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  FDP_CUDA(cudaStreamIsCapturing(st, &cs), "block_precond_apply: capture query");
-  if (!same && cs != cudaStreamCaptureStatusActive) {
-    const long long need =
-        2 * pp_sync_ints(h->vel, batch, h->pres_dense && h->D == 3 ? h->pres->n[2] : 0);
-    if (h->sync_cap < need) {
-      FDP_CUDA(cudaStreamSynchronize(st), "block_precond_apply: sync before realloc");
-      cudaFree(h->sync);
-      h->sync = nullptr;
-      h->sync_cap = 0;
-      fdp_status s2 = dalloc(&h->sync, (size_t)need);
-      if (s2) return s2;
-      FDP_CUDA(cudaMemset(h->sync, 0, need * sizeof(int)), "block_precond_apply: sync init");
-      h->sync_cap = need;
+  try {
+    if (!h) return fail(FDP_ERR_INVALID_ARG, "block_precond_apply: NULL handle");
+    if (batch < 0) return fail(FDP_ERR_SHAPE, "block_precond_apply: batch < 0");
+    if (batch == 0) return FDP_OK;
+    std::lock_guard<std::mutex> lk(h->mu);
+    fdp_block_s::GraphEntry* hit = nullptr;
+    for (auto& g : h->graphs)
+      if (g.r == r && g.s == s && g.ws == workspace && g.batch == batch) hit = &g;
+    const bool same = hit != nullptr;
+    if (!same) {
+      if (!is_device_ptr(r) || !is_device_ptr(s))
+        return fail(FDP_ERR_INVALID_ARG, "block_precond_apply: r and s must be device pointers");
+      if (!workspace || !is_device_ptr(workspace))
+        return fail(FDP_ERR_INVALID_ARG, "block_precond_apply: workspace must be device memory");
     }
-  }
-  if (cs == cudaStreamCaptureStatusActive) {
-    FDP_CUDA(enqueue_block(h, r, s, batch, static_cast<double*>(workspace), st, nullptr),
-             "block_precond_apply");
+    DeviceGuard dg(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    FDP_CUDA(cudaStreamIsCapturing(st, &cs), "block_precond_apply: capture query");
+    if (!same && cs != cudaStreamCaptureStatusActive) {
+      const long long need =
+          2 * pp_sync_ints(h->vel, batch, h->pres_dense && h->D == 3 ? h->pres->n[2] : 0);
+      if (h->sync_cap < need) {
+        FDP_CUDA(cudaStreamSynchronize(st), "block_precond_apply: sync before realloc");
+        cudaFree(h->sync);
+        h->sync = nullptr;
+        h->sync_cap = 0;
+        fdp_status s2 = dalloc(&h->sync, (size_t)need);
+        if (s2) return s2;
+        FDP_CUDA(cudaMemset(h->sync, 0, need * sizeof(int)), "block_precond_apply: sync init");
+        h->sync_cap = need;
+      }
+    }
+    if (cs == cudaStreamCaptureStatusActive) {
+      FDP_CUDA(enqueue_block(h, r, s, batch, static_cast<double*>(workspace), st, nullptr),
+               "block_precond_apply");
+      return FDP_OK;
+    }
+    if (!same) {
+      constexpr size_t kMaxGraphs = 4;
+      if (h->graphs.size() >= kMaxGraphs) {  // evict the least recently used
+        size_t lru = 0;
+        for (size_t i = 1; i < h->graphs.size(); ++i)
+          if (h->graphs[i].used < h->graphs[lru].used) lru = i;
+        FDP_CUDA(cudaStreamSynchronize(st), "block_precond_apply: evict sync");
+        cudaGraphExecDestroy(h->graphs[lru].exec);
+        h->graphs.erase(h->graphs.begin() + lru);
+      }
+      cudaGraph_t g = nullptr;
+      FDP_CUDA(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal), "capture begin");
+      cudaError_t e = enqueue_block(h, r, s, batch, static_cast<double*>(workspace), h->cap, nullptr);
+      cudaError_t e2 = cudaStreamEndCapture(h->cap, &g);
+      if (e != cudaSuccess) {
+        if (g) cudaGraphDestroy(g);
+        return cuda_fail(e, "block_precond_apply: enqueue");
+      }
+      if (e2 != cudaSuccess) return cuda_fail(e2, "block_precond_apply: capture end");
+      cudaGraphExec_t ex = nullptr;
+      e = cudaGraphInstantiate(&ex, g, 0);
+      cudaGraphDestroy(g);
+      if (e != cudaSuccess) return cuda_fail(e, "block_precond_apply: instantiate");
+      h->graphs.push_back({r, s, workspace, batch, ex, 0});
+      hit = &h->graphs.back();
+    }
+    hit->used = ++h->tick;
+    FDP_CUDA(cudaGraphLaunch(hit->exec, st), "block_precond_apply: graph launch");
     return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
   }
-  if (!same) {
-    constexpr size_t kMaxGraphs = 4;
-    if (h->graphs.size() >= kMaxGraphs) {  // evict the least recently used
-      size_t lru = 0;
-      for (size_t i = 1; i < h->graphs.size(); ++i)
-        if (h->graphs[i].used < h->graphs[lru].used) lru = i;
-      FDP_CUDA(cudaStreamSynchronize(st), "block_precond_apply: evict sync");
-      cudaGraphExecDestroy(h->graphs[lru].exec);
-      h->graphs.erase(h->graphs.begin() + lru);
-    }
-    cudaGraph_t g = nullptr;
-    FDP_CUDA(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal), "capture begin");
-    cudaError_t e = enqueue_block(h, r, s, batch, static_cast<double*>(workspace), h->cap, nullptr);
-    cudaError_t e2 = cudaStreamEndCapture(h->cap, &g);
-    if (e != cudaSuccess) {
-      if (g) cudaGraphDestroy(g);
-      return cuda_fail(e, "block_precond_apply: enqueue");
-    }
-    if (e2 != cudaSuccess) return cuda_fail(e2, "block_precond_apply: capture end");
-    cudaGraphExec_t ex = nullptr;
-    e = cudaGraphInstantiate(&ex, g, 0);
-    cudaGraphDestroy(g);
-    if (e != cudaSuccess) return cuda_fail(e, "block_precond_apply: instantiate");
-    h->graphs.push_back({r, s, workspace, batch, ex, 0});
-    hit = &h->graphs.back();
-  }
-  hit->used = ++h->tick;
-  FDP_CUDA(cudaGraphLaunch(hit->exec, st), "block_precond_apply: graph launch");
-  return FDP_OK;
 }
 
 // One pipeline unit of the host-buffer path at batch 1: velocity component k (k < D) or the
@@ -1396,170 +1491,190 @@ static cudaError_t enqueue_unit(fdp_block h, int k, const double* r, double* s, 
 
 extern "C" fdp_status block_precond_apply_host(fdp_block h, const double* r_host, double* s_host,
                                                int64_t batch, void* stream) {
-  if (!h) return fail(FDP_ERR_INVALID_ARG, "block_precond_apply_host: NULL handle");
-  if (!r_host || !s_host) return fail(FDP_ERR_INVALID_ARG, "block_precond_apply_host: NULL buffer");
-  if (batch <= 0) return batch == 0 ? FDP_OK : fail(FDP_ERR_SHAPE, "block_precond_apply_host: batch < 0");
-  std::lock_guard<std::mutex> lk(h->mu);
-  DeviceGuard dg(h->device);
-  if (batch > h->e2e_batch) {
-    cudaFree(h->e2e_r);
-    cudaFree(h->e2e_s);
-    cudaFree(h->e2e_ws);
-    h->e2e_r = h->e2e_s = nullptr;
-    h->e2e_ws = nullptr;
-    h->e2e_batch = 0;
-    fdp_status st;
-    if ((st = dalloc(&h->e2e_r, (size_t)(batch * h->size))) ||
-        (st = dalloc(&h->e2e_s, (size_t)(batch * h->size))) ||
-        (st = dalloc(reinterpret_cast<double**>(&h->e2e_ws), (size_t)block_ws_elems(h, batch))))
-      return st;
-    h->e2e_batch = batch;
-    if (h->e2e_graph) {  // captured against the old device buffers
-      cudaGraphExecDestroy(h->e2e_graph);
-      h->e2e_graph = nullptr;
+  try {
+    if (!h) return fail(FDP_ERR_INVALID_ARG, "block_precond_apply_host: NULL handle");
+    if (!r_host || !s_host) return fail(FDP_ERR_INVALID_ARG, "block_precond_apply_host: NULL buffer");
+    if (batch <= 0) return batch == 0 ? FDP_OK : fail(FDP_ERR_SHAPE, "block_precond_apply_host: batch < 0");
+    std::lock_guard<std::mutex> lk(h->mu);
+    DeviceGuard dg(h->device);
+    if (batch > h->e2e_batch) {
+      cudaFree(h->e2e_r);
+      cudaFree(h->e2e_s);
+      cudaFree(h->e2e_ws);
+      h->e2e_r = h->e2e_s = nullptr;
+      h->e2e_ws = nullptr;
+      h->e2e_batch = 0;
+      fdp_status st;
+      if ((st = dalloc(&h->e2e_r, (size_t)(batch * h->size))) ||
+          (st = dalloc(&h->e2e_s, (size_t)(batch * h->size))) ||
+          (st = dalloc(reinterpret_cast<double**>(&h->e2e_ws), (size_t)block_ws_elems(h, batch))))
+        return st;
+      h->e2e_batch = batch;
+      if (h->e2e_graph) {  // captured against the old device buffers
+        cudaGraphExecDestroy(h->e2e_graph);
+        h->e2e_graph = nullptr;
+      }
     }
-  }
-  if (!h->cin) {
-    FDP_CUDA(cudaStreamCreateWithFlags(&h->cin, cudaStreamNonBlocking), "apply_host: stream");
-    FDP_CUDA(cudaStreamCreateWithFlags(&h->cout, cudaStreamNonBlocking), "apply_host: stream");
-    for (int k = 0; k < h->D; ++k)
-      FDP_CUDA(cudaStreamCreateWithFlags(&h->cs[k], cudaStreamNonBlocking), "apply_host: stream");
-    FDP_CUDA(cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming), "apply_host: event");
-  }
-  // Pipeline units: the D + 1 blocks of one item at batch 1, whole items at batch > 1. Copies in
-  // run on cin, the applies on the caller's stream, copies out on cout, so unit j's compute
-  // overlaps unit j+1's upload and unit j-1's download (PCIe is full duplex).
-  // batch 1: D + 1 units (velocity components in order, then the pressure block), batch > 1:
-  // the items
-  const int units = batch == 1 ? h->D + 1 : (int)batch;
-  while ((int)h->ev_in.size() < units) {
-    cudaEvent_t a, b;
-    FDP_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming), "apply_host: event");
-    FDP_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming), "apply_host: event");
-    h->ev_in.push_back(a);
-    h->ev_done.push_back(b);
-  }
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  auto pinned = [](const void* p) {
-    cudaPointerAttributes a{};
-    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-      cudaGetLastError();
-      return false;
+    if (!h->cin) {
+      FDP_CUDA(cudaStreamCreateWithFlags(&h->cin, cudaStreamNonBlocking), "apply_host: stream");
+      FDP_CUDA(cudaStreamCreateWithFlags(&h->cout, cudaStreamNonBlocking), "apply_host: stream");
+      for (int k = 0; k < h->D; ++k)
+        FDP_CUDA(cudaStreamCreateWithFlags(&h->cs[k], cudaStreamNonBlocking), "apply_host: stream");
+      FDP_CUDA(cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming), "apply_host: event");
     }
-    return a.type == cudaMemoryTypeHost;
-  };
-  // batch 1 with page-locked buffers: replay the captured pipeline (copies, applies, events)
-  const bool use_graph = batch == 1 && pinned(r_host) && pinned(s_host) &&
-                         std::getenv("FDP_E2E_NO_GRAPH") == nullptr;
-  if (use_graph && h->e2e_graph && h->e2e_gr == r_host && h->e2e_gs == s_host) {
-    FDP_CUDA(cudaGraphLaunch(h->e2e_graph, st), "apply_host: graph launch");
-    FDP_CUDA(cudaStreamSynchronize(st), "apply_host: sync");
+    // Pipeline units: the D + 1 blocks of one item at batch 1, whole items at batch > 1. Copies in
+    // run on cin, the applies on the caller's stream, copies out on cout, so unit j's compute
+    // overlaps unit j+1's upload and unit j-1's download (PCIe is full duplex).
+    // batch 1: D + 1 units (velocity components in order, then the pressure block), batch > 1:
+    // the items
+    const int units = batch == 1 ? h->D + 1 : (int)batch;
+    while ((int)h->ev_in.size() < units) {
+      cudaEvent_t a, b;
+      FDP_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming), "apply_host: event");
+      FDP_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming), "apply_host: event");
+      h->ev_in.push_back(a);
+      h->ev_done.push_back(b);
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    auto pinned = [](const void* p) {
+      cudaPointerAttributes a{};
+      if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+      }
+      return a.type == cudaMemoryTypeHost;
+    };
+    // batch 1 with page-locked buffers: replay the captured pipeline (copies, applies, events)
+    const bool use_graph = batch == 1 && pinned(r_host) && pinned(s_host) &&
+                           std::getenv("FDP_E2E_NO_GRAPH") == nullptr;
+    if (use_graph && h->e2e_graph && h->e2e_gr == r_host && h->e2e_gs == s_host) {
+      FDP_CUDA(cudaGraphLaunch(h->e2e_graph, st), "apply_host: graph launch");
+      FDP_CUDA(cudaStreamSynchronize(st), "apply_host: sync");
+      return FDP_OK;
+    }
+    cudaStream_t origin = st;
+    if (use_graph) {
+      if (h->e2e_graph) {
+        cudaGraphExecDestroy(h->e2e_graph);
+        h->e2e_graph = nullptr;
+      }
+      st = h->cap;  // capture on the handle's private stream, then launch on the caller's
+      FDP_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "apply_host: capture");
+    }
+    // batch 1: velocity components in order on the caller's stream (each apply uses every SM),
+    // the pressure block last, solved on its own stream (measured: pressure first or merged with
+    // the last component's copies is slower)
+    auto span = [&](int j, long long* off, long long* len) {
+      if (batch == 1) {
+        *off = h->off[j];
+        *len = h->off[j + 1] - h->off[j];
+      } else {
+        *off = (long long)j * h->size;
+        *len = h->size;
+      }
+    };
+    // the copy-in stream must not overwrite device inputs still read by a previous call
+    FDP_CUDA(cudaEventRecord(h->ev_done[0], st), "apply_host: order");
+    FDP_CUDA(cudaStreamWaitEvent(h->cin, h->ev_done[0], 0), "apply_host: order");
+    for (int j = 0; j < units; ++j) {
+      long long off, len;
+      span(j, &off, &len);
+      FDP_CUDA(cudaMemcpyAsync(h->e2e_r + off, r_host + off, (size_t)len * sizeof(double),
+                               cudaMemcpyHostToDevice, h->cin), "apply_host: H2D");
+      FDP_CUDA(cudaEventRecord(h->ev_in[j], h->cin), "apply_host: event");
+    }
+    double* ws = static_cast<double*>(h->e2e_ws);
+    for (int j = 0; j < units; ++j) {
+      cudaStream_t us = (batch == 1 && j == h->D) ? h->cs[0] : st;
+      FDP_CUDA(cudaStreamWaitEvent(us, h->ev_in[j], 0), "apply_host: wait");
+      if (batch == 1) {
+        long long toff = 0;
+        for (int k = 0; k < j; ++k) toff += 2 * Npad(h->vel[k]);
+        FDP_CUDA(enqueue_unit(h, j, h->e2e_r, h->e2e_s, ws + toff, us), "apply_host: apply");
+      } else {
+        FDP_CUDA(enqueue_block(h, h->e2e_r + (long long)j * h->size, h->e2e_s + (long long)j * h->size, 1,
+                               ws, st, nullptr), "apply_host: apply");
+      }
+      FDP_CUDA(cudaEventRecord(h->ev_done[j], us), "apply_host: event");
+      if (us != st) FDP_CUDA(cudaStreamWaitEvent(st, h->ev_done[j], 0), "apply_host: join");
+      FDP_CUDA(cudaStreamWaitEvent(h->cout, h->ev_done[j], 0), "apply_host: wait");
+      long long off, len;
+      span(j, &off, &len);
+      FDP_CUDA(cudaMemcpyAsync(s_host + off, h->e2e_s + off, (size_t)len * sizeof(double),
+                               cudaMemcpyDeviceToHost, h->cout), "apply_host: D2H");
+    }
+    if (use_graph) {
+      // join the copy-out branch back into the origin stream, end the capture, launch
+      FDP_CUDA(cudaEventRecord(h->ev_in[0], h->cout), "apply_host: join");
+      FDP_CUDA(cudaStreamWaitEvent(st, h->ev_in[0], 0), "apply_host: join");
+      cudaGraph_t g = nullptr;
+      FDP_CUDA(cudaStreamEndCapture(st, &g), "apply_host: capture end");
+      cudaError_t e = cudaGraphInstantiate(&h->e2e_graph, g, 0);
+      cudaGraphDestroy(g);
+      if (e != cudaSuccess) {
+        h->e2e_graph = nullptr;
+        return cuda_fail(e, "apply_host: instantiate");
+      }
+      h->e2e_gr = r_host;
+      h->e2e_gs = s_host;
+      FDP_CUDA(cudaGraphLaunch(h->e2e_graph, origin), "apply_host: graph launch");
+      FDP_CUDA(cudaStreamSynchronize(origin), "apply_host: sync");
+      return FDP_OK;
+    }
+    FDP_CUDA(cudaStreamSynchronize(h->cout), "apply_host: sync");
     return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
   }
-  cudaStream_t origin = st;
-  if (use_graph) {
-    if (h->e2e_graph) {
-      cudaGraphExecDestroy(h->e2e_graph);
-      h->e2e_graph = nullptr;
-    }
-    st = h->cap;  // capture on the handle's private stream, then launch on the caller's
-    FDP_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "apply_host: capture");
-  }
-  // batch 1: velocity components in order on the caller's stream (each apply uses every SM),
-  // the pressure block last, solved on its own stream (measured: pressure first or merged with
-  // the last component's copies is slower)
-  auto span = [&](int j, long long* off, long long* len) {
-    if (batch == 1) {
-      *off = h->off[j];
-      *len = h->off[j + 1] - h->off[j];
-    } else {
-      *off = (long long)j * h->size;
-      *len = h->size;
-    }
-  };
-  // the copy-in stream must not overwrite device inputs still read by a previous call
-  FDP_CUDA(cudaEventRecord(h->ev_done[0], st), "apply_host: order");
-  FDP_CUDA(cudaStreamWaitEvent(h->cin, h->ev_done[0], 0), "apply_host: order");
-  for (int j = 0; j < units; ++j) {
-    long long off, len;
-    span(j, &off, &len);
-    FDP_CUDA(cudaMemcpyAsync(h->e2e_r + off, r_host + off, (size_t)len * sizeof(double),
-                             cudaMemcpyHostToDevice, h->cin), "apply_host: H2D");
-    FDP_CUDA(cudaEventRecord(h->ev_in[j], h->cin), "apply_host: event");
-  }
-  double* ws = static_cast<double*>(h->e2e_ws);
-  for (int j = 0; j < units; ++j) {
-    cudaStream_t us = (batch == 1 && j == h->D) ? h->cs[0] : st;
-    FDP_CUDA(cudaStreamWaitEvent(us, h->ev_in[j], 0), "apply_host: wait");
-    if (batch == 1) {
-      long long toff = 0;
-      for (int k = 0; k < j; ++k) toff += 2 * Npad(h->vel[k]);
-      FDP_CUDA(enqueue_unit(h, j, h->e2e_r, h->e2e_s, ws + toff, us), "apply_host: apply");
-    } else {
-      FDP_CUDA(enqueue_block(h, h->e2e_r + (long long)j * h->size, h->e2e_s + (long long)j * h->size, 1,
-                             ws, st, nullptr), "apply_host: apply");
-    }
-    FDP_CUDA(cudaEventRecord(h->ev_done[j], us), "apply_host: event");
-    if (us != st) FDP_CUDA(cudaStreamWaitEvent(st, h->ev_done[j], 0), "apply_host: join");
-    FDP_CUDA(cudaStreamWaitEvent(h->cout, h->ev_done[j], 0), "apply_host: wait");
-    long long off, len;
-    span(j, &off, &len);
-    FDP_CUDA(cudaMemcpyAsync(s_host + off, h->e2e_s + off, (size_t)len * sizeof(double),
-                             cudaMemcpyDeviceToHost, h->cout), "apply_host: D2H");
-  }
-  if (use_graph) {
-    // join the copy-out branch back into the origin stream, end the capture, launch
-    FDP_CUDA(cudaEventRecord(h->ev_in[0], h->cout), "apply_host: join");
-    FDP_CUDA(cudaStreamWaitEvent(st, h->ev_in[0], 0), "apply_host: join");
-    cudaGraph_t g = nullptr;
-    FDP_CUDA(cudaStreamEndCapture(st, &g), "apply_host: capture end");
-    cudaError_t e = cudaGraphInstantiate(&h->e2e_graph, g, 0);
-    cudaGraphDestroy(g);
-    if (e != cudaSuccess) {
-      h->e2e_graph = nullptr;
-      return cuda_fail(e, "apply_host: instantiate");
-    }
-    h->e2e_gr = r_host;
-    h->e2e_gs = s_host;
-    FDP_CUDA(cudaGraphLaunch(h->e2e_graph, origin), "apply_host: graph launch");
-    FDP_CUDA(cudaStreamSynchronize(origin), "apply_host: sync");
-    return FDP_OK;
-  }
-  FDP_CUDA(cudaStreamSynchronize(h->cout), "apply_host: sync");
-  return FDP_OK;
 }
 
 extern "C" void* fdp_host_alloc(size_t bytes) {
-  void* p = nullptr;
-  cudaError_t e = cudaMallocHost(&p, bytes ? bytes : 1);
-  if (e != cudaSuccess) {
-    cuda_fail(e, "fdp_host_alloc");
+  try {
+    void* p = nullptr;
+    cudaError_t e = cudaMallocHost(&p, bytes ? bytes : 1);
+    if (e != cudaSuccess) {
+      cuda_fail(e, "fdp_host_alloc");
+      return nullptr;
+    }
+    return p;
+  } catch (...) {
     return nullptr;
   }
-  return p;
 }
 
 extern "C" fdp_status fdp_host_free(void* p) {
-  if (!p) return FDP_OK;
-  FDP_CUDA(cudaFreeHost(p), "fdp_host_free");
-  return FDP_OK;
+  try {
+    if (!p) return FDP_OK;
+    FDP_CUDA(cudaFreeHost(p), "fdp_host_free");
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
 }
 
 extern "C" fdp_status block_precond_destroy(fdp_block h) {
-  if (!h) return FDP_OK;
-  DeviceGuard dg(h->device);
-  free_block(h);
-  return FDP_OK;
+  try {
+    if (!h) return FDP_OK;
+    DeviceGuard dg(h->device);
+    free_block(h);
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
 }
 
 // Diagnostics only (not part of include/fdp.h): route per-warp phase timestamps of subsequent
 // small-path launches into a device buffer of `cap` uint64 (NULL disables). Invalidates nothing:
 // callers must use fresh buffers / handles so graphs are re-captured.
 extern "C" int fdp_debug_trace(unsigned long long* dev_buf, size_t cap) {
-  g_trace = dev_buf;
-  g_trace_cap = dev_buf ? cap : 0;
-  g_trace_used = 0;
-  return 0;
+  try {
+    g_trace = dev_buf;
+    g_trace_cap = dev_buf ? cap : 0;
+    g_trace_used = 0;
+    return 0;
+  } catch (...) {
+    return -1;
+  }
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -1572,22 +1687,30 @@ static void part_range(long long n, int G, int r, long long* lo, long long* len)
 }
 
 extern "C" fdp_status fdp_slab_range(int64_t n, int nranks, int rank, int64_t* lo, int64_t* len) {
-  if (nranks < 1 || rank < 0 || rank >= nranks || n < 0 || !lo || !len)
-    return fail(FDP_ERR_INVALID_ARG, "fdp_slab_range: bad arguments");
-  long long a, b;
-  part_range(n, nranks, rank, &a, &b);
-  *lo = a;
-  *len = b;
-  return FDP_OK;
+  try {
+    if (nranks < 1 || rank < 0 || rank >= nranks || n < 0 || !lo || !len)
+      return fail(FDP_ERR_INVALID_ARG, "fdp_slab_range: bad arguments");
+    long long a, b;
+    part_range(n, nranks, rank, &a, &b);
+    *lo = a;
+    *len = b;
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
 }
 
 extern "C" size_t fd_slab_workspace_bytes(fdp_fd h, int nranks, int rank) {
-  if (!h || h->D != 3 || nranks < 1 || rank < 0 || rank >= nranks) return 0;
-  long long z0, nz, y0, ny;
-  part_range(h->n[2], nranks, rank, &z0, &nz);
-  part_range(h->n[1], nranks, rank, &y0, &ny);
-  const long long zs = (long long)h->n[0] * h->n[1] * nz, ys = (long long)h->n[0] * ny * h->n[2];
-  return (size_t)std::max(2 * zs, ys) * sizeof(double);
+  try {
+    if (!h || h->D != 3 || nranks < 1 || rank < 0 || rank >= nranks) return 0;
+    long long z0, nz, y0, ny;
+    part_range(h->n[2], nranks, rank, &z0, &nz);
+    part_range(h->n[1], nranks, rank, &y0, &ny);
+    const long long zs = (long long)h->n[0] * h->n[1] * nz, ys = (long long)h->n[0] * ny * h->n[2];
+    return (size_t)std::max(2 * zs, ys) * sizeof(double);
+  } catch (...) {
+    return 0;
+  }
 }
 
 // Mode contraction of a (P, n, Q) view with the handle's direction-d matrices (batch 1).
@@ -1631,55 +1754,59 @@ static cudaError_t run1(ModeProb p, const TileCfg& c, bool kmaj, cudaStream_t s)
 extern "C" fdp_status fd_apply_slab(fdp_fd h, int phase, int nranks, int rank, const double* in,
                                     double* out, const double* dscale, void* workspace,
                                     void* stream) {
-  if (!h) return fail(FDP_ERR_INVALID_ARG, "fd_apply_slab: NULL handle");
-  if (h->D != 3) return fail(FDP_ERR_UNSUPPORTED, "fd_apply_slab: D must be 3");
-  if (nranks < 1 || rank < 0 || rank >= nranks || phase < 0 || phase > 2)
-    return fail(FDP_ERR_INVALID_ARG, "fd_apply_slab: bad phase / rank");
-  const long long n1 = h->n[0], n2 = h->n[1], n3 = h->n[2];
-  long long z0, nz, y0, ny;
-  part_range(n3, nranks, rank, &z0, &nz);
-  part_range(n2, nranks, rank, &y0, &ny);
-  if ((phase == 1 ? ny : nz) == 0) return FDP_OK;  // this rank owns nothing of that axis
-  if (!is_device_ptr(in) || !is_device_ptr(out) || !is_device_ptr(workspace) ||
-      (dscale && !is_device_ptr(dscale)))
-    return fail(FDP_ERR_INVALID_ARG, "fd_apply_slab: device pointers required");
-  DeviceGuard dg(h->device);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  double* T1 = static_cast<double*>(workspace);
-  double* T2 = T1 + n1 * n2 * nz;
-  if (phase == 0) {
-    const double* src = in;
-    if (dscale) {
-      FDP_CUDA(launch_scale(in, T2, dscale, n1 * n2 * nz, 1, 0, 0, s), "fd_apply_slab: prescale");
-      src = T2;
-    }
-    FDP_CUDA(run1(slab_prob(h, 0, true, src, T1, 1, n2 * nz, EPI_NONE, nullptr, nullptr), h->cfg[0], true, s),
-             "fd_apply_slab: mode 1");
-    FDP_CUDA(run1(slab_prob(h, 1, true, T1, T2, n1, nz, EPI_NONE, nullptr, nullptr), h->cfg[1], false, s),
-             "fd_apply_slab: mode 2");
-    FDP_CUDA(launch_slab_copy(T2, out, (int)n1, (int)n2, (int)nz, nranks, 0, nullptr, s), "fd_apply_slab: pack");
-  } else if (phase == 1) {
-    const double* lam1 = h->lamc[1] + y0;
-    const bool fuse = std::getenv("FDP_NO_FUSE") == nullptr && std::getenv("FDP_NO_SMALL") == nullptr &&
-                      n3 <= kSmallMaxN && h->cfg[2].tiles_n == 1;
-    if (fuse) {  // in place: each 8-row tile is read whole before it is written
-      FDP_CUDA(run1(slab_prob(h, 2, true, in, out, n1 * ny, 1, EPI_FUSED, nullptr, lam1), h->cfg[2], false, s),
-               "fd_apply_slab: fused mode 3");
+  try {
+    if (!h) return fail(FDP_ERR_INVALID_ARG, "fd_apply_slab: NULL handle");
+    if (h->D != 3) return fail(FDP_ERR_UNSUPPORTED, "fd_apply_slab: D must be 3");
+    if (nranks < 1 || rank < 0 || rank >= nranks || phase < 0 || phase > 2)
+      return fail(FDP_ERR_INVALID_ARG, "fd_apply_slab: bad phase / rank");
+    const long long n1 = h->n[0], n2 = h->n[1], n3 = h->n[2];
+    long long z0, nz, y0, ny;
+    part_range(n3, nranks, rank, &z0, &nz);
+    part_range(n2, nranks, rank, &y0, &ny);
+    if ((phase == 1 ? ny : nz) == 0) return FDP_OK;  // this rank owns nothing of that axis
+    if (!is_device_ptr(in) || !is_device_ptr(out) || !is_device_ptr(workspace) ||
+        (dscale && !is_device_ptr(dscale)))
+      return fail(FDP_ERR_INVALID_ARG, "fd_apply_slab: device pointers required");
+    DeviceGuard dg(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    double* T1 = static_cast<double*>(workspace);
+    double* T2 = T1 + n1 * n2 * nz;
+    if (phase == 0) {
+      const double* src = in;
+      if (dscale) {
+        FDP_CUDA(launch_scale(in, T2, dscale, n1 * n2 * nz, 1, 0, 0, s), "fd_apply_slab: prescale");
+        src = T2;
+      }
+      FDP_CUDA(run1(slab_prob(h, 0, true, src, T1, 1, n2 * nz, EPI_NONE, nullptr, nullptr), h->cfg[0], true, s),
+               "fd_apply_slab: mode 1");
+      FDP_CUDA(run1(slab_prob(h, 1, true, T1, T2, n1, nz, EPI_NONE, nullptr, nullptr), h->cfg[1], false, s),
+               "fd_apply_slab: mode 2");
+      FDP_CUDA(launch_slab_copy(T2, out, (int)n1, (int)n2, (int)nz, nranks, 0, nullptr, s), "fd_apply_slab: pack");
+    } else if (phase == 1) {
+      const double* lam1 = h->lamc[1] + y0;
+      const bool fuse = std::getenv("FDP_NO_FUSE") == nullptr && std::getenv("FDP_NO_SMALL") == nullptr &&
+                        n3 <= kSmallMaxN && h->cfg[2].tiles_n == 1;
+      if (fuse) {  // in place: each 8-row tile is read whole before it is written
+        FDP_CUDA(run1(slab_prob(h, 2, true, in, out, n1 * ny, 1, EPI_FUSED, nullptr, lam1), h->cfg[2], false, s),
+                 "fd_apply_slab: fused mode 3");
+      } else {
+        FDP_CUDA(run1(slab_prob(h, 2, true, in, T1, n1 * ny, 1, EPI_LAMBDA, nullptr, lam1), h->cfg[2], false, s),
+                 "fd_apply_slab: mode 3 fwd");
+        FDP_CUDA(run1(slab_prob(h, 2, false, T1, out, n1 * ny, 1, EPI_NONE, nullptr, nullptr), h->cfg[2], false, s),
+                 "fd_apply_slab: mode 3 bwd");
+      }
     } else {
-      FDP_CUDA(run1(slab_prob(h, 2, true, in, T1, n1 * ny, 1, EPI_LAMBDA, nullptr, lam1), h->cfg[2], false, s),
-               "fd_apply_slab: mode 3 fwd");
-      FDP_CUDA(run1(slab_prob(h, 2, false, T1, out, n1 * ny, 1, EPI_NONE, nullptr, nullptr), h->cfg[2], false, s),
-               "fd_apply_slab: mode 3 bwd");
+      FDP_CUDA(launch_slab_copy(in, T1, (int)n1, (int)n2, (int)nz, nranks, 1, nullptr, s), "fd_apply_slab: unpack");
+      FDP_CUDA(run1(slab_prob(h, 1, false, T1, T2, n1, nz, EPI_NONE, nullptr, nullptr), h->cfg[1], false, s),
+               "fd_apply_slab: mode 2 bwd");
+      FDP_CUDA(run1(slab_prob(h, 0, false, T2, out, 1, n2 * nz, dscale ? EPI_SCALE : EPI_NONE, dscale, nullptr),
+                    h->cfg[0], true, s),
+               "fd_apply_slab: mode 1 bwd");
     }
-  } else {
-    FDP_CUDA(launch_slab_copy(in, T1, (int)n1, (int)n2, (int)nz, nranks, 1, nullptr, s), "fd_apply_slab: unpack");
-    FDP_CUDA(run1(slab_prob(h, 1, false, T1, T2, n1, nz, EPI_NONE, nullptr, nullptr), h->cfg[1], false, s),
-             "fd_apply_slab: mode 2 bwd");
-    FDP_CUDA(run1(slab_prob(h, 0, false, T2, out, 1, n2 * nz, dscale ? EPI_SCALE : EPI_NONE, dscale, nullptr),
-                  h->cfg[0], true, s),
-             "fd_apply_slab: mode 1 bwd");
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
   }
-  return FDP_OK;
 }
 
 // ---- peer-store slab exchange: the exchanges are fused into the epilogues of
@@ -1700,164 +1827,192 @@ static void set_scatter(ModeProb& p, double* const* peers, int G, int na, int n1
 extern "C" fdp_status fd_apply_slab_peer(fdp_fd h, int phase, int nranks, int rank, const double* in,
                                          double* out, double* const* peers, const double* dscale,
                                          void* workspace, void* stream) {
-  if (!h) return fail(FDP_ERR_INVALID_ARG, "fd_apply_slab_peer: NULL handle");
-  if (h->D != 3) return fail(FDP_ERR_UNSUPPORTED, "fd_apply_slab_peer: D must be 3");
-  if (nranks < 1 || nranks > 32 || rank < 0 || rank >= nranks || phase < 0 || phase > 2)
-    return fail(FDP_ERR_INVALID_ARG, "fd_apply_slab_peer: bad phase / rank");
-  const long long n1 = h->n[0], n2 = h->n[1], n3 = h->n[2];
-  long long z0, nz, y0, ny;
-  part_range(n3, nranks, rank, &z0, &nz);
-  part_range(n2, nranks, rank, &y0, &ny);
-  if ((phase == 1 ? ny : nz) == 0) return FDP_OK;
-  if (!is_device_ptr(in) || !is_device_ptr(workspace) || (phase == 2 && !is_device_ptr(out)) ||
-      (phase < 2 && !is_device_ptr(peers)) || (dscale && !is_device_ptr(dscale)))
-    return fail(FDP_ERR_INVALID_ARG, "fd_apply_slab_peer: device pointers required");
-  DeviceGuard dg(h->device);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  double* T1 = static_cast<double*>(workspace);
-  double* T2 = T1 + n1 * n2 * nz;
-  if (phase == 0) {
-    // modes 1, 2 on the z-slab; mode 2 stores element (i1, i2, i3) straight into the y-slab
-    // buffer (n1, ny_h, n3) of the rank h owning i2, at (i1, i2 - y0_h, z0 + i3)
-    const double* src = in;
-    if (dscale) {
-      FDP_CUDA(launch_scale(in, T2, dscale, n1 * n2 * nz, 1, 0, 0, s), "fd_apply_slab_peer: prescale");
-      src = T2;
-    }
-    FDP_CUDA(run1(slab_prob(h, 0, true, src, T1, 1, n2 * nz, EPI_NONE, nullptr, nullptr), h->cfg[0], true, s),
-             "fd_apply_slab_peer: mode 1");
-    ModeProb p = slab_prob(h, 1, true, T1, nullptr, n1, nz, EPI_NONE, nullptr, nullptr);
-    set_scatter(p, peers, nranks, (int)n2, (int)n1, (int)z0, 1, 0, 0, 1);
-    FDP_CUDA(run1(p, h->cfg[1], false, s), "fd_apply_slab_peer: mode 2 + exchange");
-  } else if (phase == 1) {
-    // the mode-3 triple on the y-slab; the last contraction stores element (i1, i2, i3) straight
-    // into the z-slab buffer (n1, n2, nz_g) of the rank g owning i3, at (i1, y0 + i2, i3 - z0_g)
-    const double* lam1 = h->lamc[1] + y0;
-    const bool fuse = std::getenv("FDP_NO_FUSE") == nullptr && std::getenv("FDP_NO_SMALL") == nullptr &&
-                      n3 <= kSmallMaxN && h->cfg[2].tiles_n == 1;
-    if (fuse) {
-      ModeProb p = slab_prob(h, 2, true, in, nullptr, n1 * ny, 1, EPI_FUSED, nullptr, lam1);
-      set_scatter(p, peers, nranks, (int)n3, (int)n1, (int)y0, (int)n2, 0, 1, 0);
-      FDP_CUDA(run1(p, h->cfg[2], false, s), "fd_apply_slab_peer: fused mode 3 + exchange");
+  try {
+    if (!h) return fail(FDP_ERR_INVALID_ARG, "fd_apply_slab_peer: NULL handle");
+    if (h->D != 3) return fail(FDP_ERR_UNSUPPORTED, "fd_apply_slab_peer: D must be 3");
+    if (nranks < 1 || nranks > 32 || rank < 0 || rank >= nranks || phase < 0 || phase > 2)
+      return fail(FDP_ERR_INVALID_ARG, "fd_apply_slab_peer: bad phase / rank");
+    const long long n1 = h->n[0], n2 = h->n[1], n3 = h->n[2];
+    long long z0, nz, y0, ny;
+    part_range(n3, nranks, rank, &z0, &nz);
+    part_range(n2, nranks, rank, &y0, &ny);
+    if ((phase == 1 ? ny : nz) == 0) return FDP_OK;
+    if (!is_device_ptr(in) || !is_device_ptr(workspace) || (phase == 2 && !is_device_ptr(out)) ||
+        (phase < 2 && !is_device_ptr(peers)) || (dscale && !is_device_ptr(dscale)))
+      return fail(FDP_ERR_INVALID_ARG, "fd_apply_slab_peer: device pointers required");
+    DeviceGuard dg(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    double* T1 = static_cast<double*>(workspace);
+    double* T2 = T1 + n1 * n2 * nz;
+    if (phase == 0) {
+      // modes 1, 2 on the z-slab; mode 2 stores element (i1, i2, i3) straight into the y-slab
+      // buffer (n1, ny_h, n3) of the rank h owning i2, at (i1, i2 - y0_h, z0 + i3)
+      const double* src = in;
+      if (dscale) {
+        FDP_CUDA(launch_scale(in, T2, dscale, n1 * n2 * nz, 1, 0, 0, s), "fd_apply_slab_peer: prescale");
+        src = T2;
+      }
+      FDP_CUDA(run1(slab_prob(h, 0, true, src, T1, 1, n2 * nz, EPI_NONE, nullptr, nullptr), h->cfg[0], true, s),
+               "fd_apply_slab_peer: mode 1");
+      ModeProb p = slab_prob(h, 1, true, T1, nullptr, n1, nz, EPI_NONE, nullptr, nullptr);
+      set_scatter(p, peers, nranks, (int)n2, (int)n1, (int)z0, 1, 0, 0, 1);
+      FDP_CUDA(run1(p, h->cfg[1], false, s), "fd_apply_slab_peer: mode 2 + exchange");
+    } else if (phase == 1) {
+      // the mode-3 triple on the y-slab; the last contraction stores element (i1, i2, i3) straight
+      // into the z-slab buffer (n1, n2, nz_g) of the rank g owning i3, at (i1, y0 + i2, i3 - z0_g)
+      const double* lam1 = h->lamc[1] + y0;
+      const bool fuse = std::getenv("FDP_NO_FUSE") == nullptr && std::getenv("FDP_NO_SMALL") == nullptr &&
+                        n3 <= kSmallMaxN && h->cfg[2].tiles_n == 1;
+      if (fuse) {
+        ModeProb p = slab_prob(h, 2, true, in, nullptr, n1 * ny, 1, EPI_FUSED, nullptr, lam1);
+        set_scatter(p, peers, nranks, (int)n3, (int)n1, (int)y0, (int)n2, 0, 1, 0);
+        FDP_CUDA(run1(p, h->cfg[2], false, s), "fd_apply_slab_peer: fused mode 3 + exchange");
+      } else {
+        FDP_CUDA(run1(slab_prob(h, 2, true, in, T1, n1 * ny, 1, EPI_LAMBDA, nullptr, lam1), h->cfg[2], false, s),
+                 "fd_apply_slab_peer: mode 3 fwd");
+        ModeProb p = slab_prob(h, 2, false, T1, nullptr, n1 * ny, 1, EPI_NONE, nullptr, nullptr);
+        set_scatter(p, peers, nranks, (int)n3, (int)n1, (int)y0, (int)n2, 0, 1, 0);
+        FDP_CUDA(run1(p, h->cfg[2], false, s), "fd_apply_slab_peer: mode 3 bwd + exchange");
+      }
     } else {
-      FDP_CUDA(run1(slab_prob(h, 2, true, in, T1, n1 * ny, 1, EPI_LAMBDA, nullptr, lam1), h->cfg[2], false, s),
-               "fd_apply_slab_peer: mode 3 fwd");
-      ModeProb p = slab_prob(h, 2, false, T1, nullptr, n1 * ny, 1, EPI_NONE, nullptr, nullptr);
-      set_scatter(p, peers, nranks, (int)n3, (int)n1, (int)y0, (int)n2, 0, 1, 0);
-      FDP_CUDA(run1(p, h->cfg[2], false, s), "fd_apply_slab_peer: mode 3 bwd + exchange");
+      FDP_CUDA(run1(slab_prob(h, 1, false, in, T2, n1, nz, EPI_NONE, nullptr, nullptr), h->cfg[1], false, s),
+               "fd_apply_slab_peer: mode 2 bwd");
+      FDP_CUDA(run1(slab_prob(h, 0, false, T2, out, 1, n2 * nz, dscale ? EPI_SCALE : EPI_NONE, dscale, nullptr),
+                    h->cfg[0], true, s),
+               "fd_apply_slab_peer: mode 1 bwd");
     }
-  } else {
-    FDP_CUDA(run1(slab_prob(h, 1, false, in, T2, n1, nz, EPI_NONE, nullptr, nullptr), h->cfg[1], false, s),
-             "fd_apply_slab_peer: mode 2 bwd");
-    FDP_CUDA(run1(slab_prob(h, 0, false, T2, out, 1, n2 * nz, dscale ? EPI_SCALE : EPI_NONE, dscale, nullptr),
-                  h->cfg[0], true, s),
-             "fd_apply_slab_peer: mode 1 bwd");
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
   }
-  return FDP_OK;
 }
 
 extern "C" fdp_status kron_mass_apply_slab_peer(fdp_mass h, int phase, int nranks, int rank,
                                                 const double* in, double* out, double* const* peers,
                                                 const double* dscale, void* workspace, void* stream) {
-  if (!h) return fail(FDP_ERR_INVALID_ARG, "kron_mass_apply_slab_peer: NULL handle");
-  if (h->D != 3) return fail(FDP_ERR_UNSUPPORTED, "kron_mass_apply_slab_peer: D must be 3");
-  if (nranks < 1 || nranks > 32 || rank < 0 || rank >= nranks || phase < 0 || phase > 2)
-    return fail(FDP_ERR_INVALID_ARG, "kron_mass_apply_slab_peer: bad phase / rank");
-  const long long n1 = h->n[0], n2 = h->n[1], n3 = h->n[2];
-  long long z0, nz, y0, ny;
-  part_range(n3, nranks, rank, &z0, &nz);
-  part_range(n2, nranks, rank, &y0, &ny);
-  if ((phase == 1 ? ny : nz) == 0) return FDP_OK;
-  if (!is_device_ptr(in) || (phase < 2 && (!is_device_ptr(workspace) || !is_device_ptr(peers))) ||
-      (phase == 2 && !is_device_ptr(out)) || (dscale && !is_device_ptr(dscale)))
-    return fail(FDP_ERR_INVALID_ARG, "kron_mass_apply_slab_peer: device pointers required");
-  DeviceGuard dg(h->device);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  auto mode = [&](int d, const double* src, double* dst, long long P, long long Q, const double* pre) {
-    MassMode m{};
-    m.in = src;
-    m.out = dst;
-    m.Lb = h->Lb[d];
-    m.invd = h->invd[d];
-    m.Mb = h->Mb[d];
-    m.pre = pre;
-    m.N = P * h->n[d] * Q;
-    m.bs = 0;
-    m.P = (int)P;
-    m.n = h->n[d];
-    m.Q = (int)Q;
-    m.batch = 1;
-    m.band = h->band[d];
-    return launch_mass_mode(m, s);
-  };
-  double* T = static_cast<double*>(workspace);
-  if (phase == 0) {
-    FDP_CUDA(mode(0, in, T, 1, n2 * nz, dscale), "kron_mass_apply_slab_peer: mode 1");
-    FDP_CUDA(mode(1, T, T, n1, nz, nullptr), "kron_mass_apply_slab_peer: mode 2");
-    ScatterDesc sd{peers, nranks, (int)n2, (int)n1, (int)z0, 1, 0, 0, 1};
-    FDP_CUDA(launch_slab_scatter(T, sd, (int)nz, 0, s), "kron_mass_apply_slab_peer: exchange");
-  } else if (phase == 1) {
-    FDP_CUDA(mode(2, in, T, n1 * ny, 1, nullptr), "kron_mass_apply_slab_peer: mode 3");
-    ScatterDesc sd{peers, nranks, (int)n3, (int)n1, (int)y0, (int)n2, 0, 1, 0};
-    FDP_CUDA(launch_slab_scatter(T, sd, (int)ny, 1, s), "kron_mass_apply_slab_peer: exchange");
-  } else if (dscale) {
-    FDP_CUDA(launch_scale(in, out, dscale, n1 * n2 * nz, 1, 0, 0, s), "kron_mass_apply_slab_peer: postscale");
-  } else if (in != out) {
-    FDP_CUDA(cudaMemcpyAsync(out, in, (size_t)(n1 * n2 * nz) * sizeof(double), cudaMemcpyDeviceToDevice, s),
-             "kron_mass_apply_slab_peer: copy");
+  try {
+    if (!h) return fail(FDP_ERR_INVALID_ARG, "kron_mass_apply_slab_peer: NULL handle");
+    if (h->D != 3) return fail(FDP_ERR_UNSUPPORTED, "kron_mass_apply_slab_peer: D must be 3");
+    if (nranks < 1 || nranks > 32 || rank < 0 || rank >= nranks || phase < 0 || phase > 2)
+      return fail(FDP_ERR_INVALID_ARG, "kron_mass_apply_slab_peer: bad phase / rank");
+    const long long n1 = h->n[0], n2 = h->n[1], n3 = h->n[2];
+    long long z0, nz, y0, ny;
+    part_range(n3, nranks, rank, &z0, &nz);
+    part_range(n2, nranks, rank, &y0, &ny);
+    if ((phase == 1 ? ny : nz) == 0) return FDP_OK;
+    if (!is_device_ptr(in) || (phase < 2 && (!is_device_ptr(workspace) || !is_device_ptr(peers))) ||
+        (phase == 2 && !is_device_ptr(out)) || (dscale && !is_device_ptr(dscale)))
+      return fail(FDP_ERR_INVALID_ARG, "kron_mass_apply_slab_peer: device pointers required");
+    DeviceGuard dg(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    auto mode = [&](int d, const double* src, double* dst, long long P, long long Q, const double* pre) {
+      MassMode m{};
+      m.in = src;
+      m.out = dst;
+      m.Lb = h->Lb[d];
+      m.invd = h->invd[d];
+      m.Mb = h->Mb[d];
+      m.pre = pre;
+      m.N = P * h->n[d] * Q;
+      m.bs = 0;
+      m.P = (int)P;
+      m.n = h->n[d];
+      m.Q = (int)Q;
+      m.batch = 1;
+      m.band = h->band[d];
+      return launch_mass_mode(m, s);
+    };
+    double* T = static_cast<double*>(workspace);
+    if (phase == 0) {
+      FDP_CUDA(mode(0, in, T, 1, n2 * nz, dscale), "kron_mass_apply_slab_peer: mode 1");
+      FDP_CUDA(mode(1, T, T, n1, nz, nullptr), "kron_mass_apply_slab_peer: mode 2");
+      ScatterDesc sd{peers, nranks, (int)n2, (int)n1, (int)z0, 1, 0, 0, 1};
+      FDP_CUDA(launch_slab_scatter(T, sd, (int)nz, 0, s), "kron_mass_apply_slab_peer: exchange");
+    } else if (phase == 1) {
+      FDP_CUDA(mode(2, in, T, n1 * ny, 1, nullptr), "kron_mass_apply_slab_peer: mode 3");
+      ScatterDesc sd{peers, nranks, (int)n3, (int)n1, (int)y0, (int)n2, 0, 1, 0};
+      FDP_CUDA(launch_slab_scatter(T, sd, (int)ny, 1, s), "kron_mass_apply_slab_peer: exchange");
+    } else if (dscale) {
+      FDP_CUDA(launch_scale(in, out, dscale, n1 * n2 * nz, 1, 0, 0, s), "kron_mass_apply_slab_peer: postscale");
+    } else if (in != out) {
+      FDP_CUDA(cudaMemcpyAsync(out, in, (size_t)(n1 * n2 * nz) * sizeof(double), cudaMemcpyDeviceToDevice, s),
+               "kron_mass_apply_slab_peer: copy");
+    }
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
   }
-  return FDP_OK;
 }
 
 extern "C" fdp_status fdp_peer_barrier(unsigned long long* const* flags, unsigned long long* counter,
                                        int nranks, int rank, void* stream) {
-  if (nranks < 1 || nranks > 32 || rank < 0 || rank >= nranks)
-    return fail(FDP_ERR_INVALID_ARG, "fdp_peer_barrier: bad rank");
-  if (!is_device_ptr(flags) || !is_device_ptr(counter))
-    return fail(FDP_ERR_INVALID_ARG, "fdp_peer_barrier: device pointers required");
-  FDP_CUDA(launch_peer_barrier(flags, counter, nranks, rank, static_cast<cudaStream_t>(stream)),
-           "fdp_peer_barrier");
-  return FDP_OK;
+  try {
+    if (nranks < 1 || nranks > 32 || rank < 0 || rank >= nranks)
+      return fail(FDP_ERR_INVALID_ARG, "fdp_peer_barrier: bad rank");
+    if (!is_device_ptr(flags) || !is_device_ptr(counter))
+      return fail(FDP_ERR_INVALID_ARG, "fdp_peer_barrier: device pointers required");
+    FDP_CUDA(launch_peer_barrier(flags, counter, nranks, rank, static_cast<cudaStream_t>(stream)),
+             "fdp_peer_barrier");
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
 }
 
 extern "C" fdp_status fdp_peer_alloc(size_t bytes, int device, void** dev_ptr, void* ipc_handle) {
-  if (!dev_ptr || !ipc_handle) return fail(FDP_ERR_INVALID_ARG, "fdp_peer_alloc: NULL argument");
-  *dev_ptr = nullptr;
-  DeviceGuard dg(device);
-  void* p = nullptr;
-  FDP_CUDA(cudaMalloc(&p, bytes ? bytes : 8), "fdp_peer_alloc: cudaMalloc");
-  cudaError_t e = cudaMemset(p, 0, bytes ? bytes : 8);
-  cudaIpcMemHandle_t hd;
-  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&hd, p);
-  if (e != cudaSuccess) {
-    cudaFree(p);
-    return cuda_fail(e, "fdp_peer_alloc: IPC handle");
+  try {
+    if (!dev_ptr || !ipc_handle) return fail(FDP_ERR_INVALID_ARG, "fdp_peer_alloc: NULL argument");
+    *dev_ptr = nullptr;
+    DeviceGuard dg(device);
+    void* p = nullptr;
+    FDP_CUDA(cudaMalloc(&p, bytes ? bytes : 8), "fdp_peer_alloc: cudaMalloc");
+    cudaError_t e = cudaMemset(p, 0, bytes ? bytes : 8);
+    cudaIpcMemHandle_t hd;
+    if (e == cudaSuccess) e = cudaIpcGetMemHandle(&hd, p);
+    if (e != cudaSuccess) {
+      cudaFree(p);
+      return cuda_fail(e, "fdp_peer_alloc: IPC handle");
+    }
+    std::memcpy(ipc_handle, &hd, sizeof(hd));
+    *dev_ptr = p;
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
   }
-  std::memcpy(ipc_handle, &hd, sizeof(hd));
-  *dev_ptr = p;
-  return FDP_OK;
 }
 
 extern "C" fdp_status fdp_peer_open(const void* ipc_handle, int device, void** dev_ptr) {
-  if (!ipc_handle || !dev_ptr) return fail(FDP_ERR_INVALID_ARG, "fdp_peer_open: NULL argument");
-  *dev_ptr = nullptr;
-  DeviceGuard dg(device);
-  cudaIpcMemHandle_t hd;
-  std::memcpy(&hd, ipc_handle, sizeof(hd));
-  FDP_CUDA(cudaIpcOpenMemHandle(dev_ptr, hd, cudaIpcMemLazyEnablePeerAccess), "fdp_peer_open");
-  return FDP_OK;
+  try {
+    if (!ipc_handle || !dev_ptr) return fail(FDP_ERR_INVALID_ARG, "fdp_peer_open: NULL argument");
+    *dev_ptr = nullptr;
+    DeviceGuard dg(device);
+    cudaIpcMemHandle_t hd;
+    std::memcpy(&hd, ipc_handle, sizeof(hd));
+    FDP_CUDA(cudaIpcOpenMemHandle(dev_ptr, hd, cudaIpcMemLazyEnablePeerAccess), "fdp_peer_open");
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
 }
 
 extern "C" fdp_status fdp_peer_close(void* dev_ptr) {
-  if (!dev_ptr) return FDP_OK;
-  FDP_CUDA(cudaIpcCloseMemHandle(dev_ptr), "fdp_peer_close");
-  return FDP_OK;
+  try {
+    if (!dev_ptr) return FDP_OK;
+    FDP_CUDA(cudaIpcCloseMemHandle(dev_ptr), "fdp_peer_close");
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
 }
 
 extern "C" fdp_status fdp_peer_free(void* dev_ptr) {
-  if (!dev_ptr) return FDP_OK;
-  FDP_CUDA(cudaFree(dev_ptr), "fdp_peer_free");
-  return FDP_OK;
+  try {
+    if (!dev_ptr) return FDP_OK;
+    FDP_CUDA(cudaFree(dev_ptr), "fdp_peer_free");
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
 }
 
 // ---- C-level communicator for the sharded block apply (SURVEY.md §8(b) "multi-GPU") ----
@@ -1894,240 +2049,284 @@ static void block_dims(const fdp_block_s* P, int b, long long* n1, long long* n2
 }
 
 extern "C" size_t fdp_comm_blob_bytes(fdp_block P, int nranks) {
-  if (!P || P->D != 3 || nranks < 1) return 0;
-  return (size_t)(2 * (P->D + 1) + 1) * sizeof(cudaIpcMemHandle_t);
+  try {
+    if (!P || P->D != 3 || nranks < 1) return 0;
+    return (size_t)(2 * (P->D + 1) + 1) * sizeof(cudaIpcMemHandle_t);
+  } catch (...) {
+    return 0;
+  }
 }
 
 extern "C" fdp_status fdp_comm_create(fdp_block P, int nranks, int rank, fdp_comm* out, void* blob) {
-  if (!out || !blob) return fail(FDP_ERR_INVALID_ARG, "fdp_comm_create: NULL argument");
-  *out = nullptr;
-  if (!P) return fail(FDP_ERR_INVALID_ARG, "fdp_comm_create: NULL block");
-  if (P->D != 3) return fail(FDP_ERR_UNSUPPORTED, "fdp_comm_create: D must be 3");
-  if (nranks < 1 || nranks > 32 || rank < 0 || rank >= nranks)
-    return fail(FDP_ERR_INVALID_ARG, "fdp_comm_create: bad rank");
-  DeviceGuard dg(P->device);
-  std::unique_ptr<fdp_comm_s> c(new (std::nothrow) fdp_comm_s);
-  if (!c) return fail(FDP_ERR_OOM, "fdp_comm_create: host allocation");
-  c->nranks = nranks;
-  c->rank = rank;
-  c->device = P->device;
-  c->nblocks = P->D + 1;
-  fdp_comm raw = c.release();
-  auto alloc = [&](size_t bytes) -> fdp_status {
-    void* p = nullptr;
-    cudaIpcMemHandle_t hd;
-    fdp_status st = fdp_peer_alloc(bytes, raw->device, &p, &hd);
-    if (st) return st;
-    std::memcpy(static_cast<char*>(blob) + raw->own.size() * sizeof(hd), &hd, sizeof(hd));
-    raw->own.push_back(p);
+  try {
+    if (!out || !blob) return fail(FDP_ERR_INVALID_ARG, "fdp_comm_create: NULL argument");
+    *out = nullptr;
+    if (!P) return fail(FDP_ERR_INVALID_ARG, "fdp_comm_create: NULL block");
+    if (P->D != 3) return fail(FDP_ERR_UNSUPPORTED, "fdp_comm_create: D must be 3");
+    if (nranks < 1 || nranks > 32 || rank < 0 || rank >= nranks)
+      return fail(FDP_ERR_INVALID_ARG, "fdp_comm_create: bad rank");
+    DeviceGuard dg(P->device);
+    std::unique_ptr<fdp_comm_s> c(new (std::nothrow) fdp_comm_s);
+    if (!c) return fail(FDP_ERR_OOM, "fdp_comm_create: host allocation");
+    c->nranks = nranks;
+    c->rank = rank;
+    c->device = P->device;
+    c->nblocks = P->D + 1;
+    fdp_comm raw = c.release();
+    auto alloc = [&](size_t bytes) -> fdp_status {
+      void* p = nullptr;
+      cudaIpcMemHandle_t hd;
+      fdp_status st = fdp_peer_alloc(bytes, raw->device, &p, &hd);
+      if (st) return st;
+      std::memcpy(static_cast<char*>(blob) + raw->own.size() * sizeof(hd), &hd, sizeof(hd));
+      raw->own.push_back(p);
+      return FDP_OK;
+    };
+    fdp_status st = FDP_OK;
+    for (int b = 0; b < raw->nblocks && !st; ++b) {
+      long long n1, n2, n3, y0, ny, z0, nz;
+      block_dims(P, b, &n1, &n2, &n3);
+      part_range(n2, nranks, rank, &y0, &ny);
+      part_range(n3, nranks, rank, &z0, &nz);
+      st = alloc((size_t)std::max(1LL, n1 * ny * n3) * sizeof(double));
+      if (!st) st = alloc((size_t)std::max(1LL, n1 * n2 * nz) * sizeof(double));
+    }
+    if (!st) st = alloc((size_t)nranks * sizeof(unsigned long long));
+    if (!st) st = dalloc(&raw->counter, 1);
+    if (!st) {
+      cudaError_t e = cudaMemset(raw->counter, 0, sizeof(unsigned long long));
+      if (e != cudaSuccess) st = cuda_fail(e, "fdp_comm_create: counter");
+    }
+    if (st) {
+      free_comm(raw);
+      return st;
+    }
+    *out = raw;
     return FDP_OK;
-  };
-  fdp_status st = FDP_OK;
-  for (int b = 0; b < raw->nblocks && !st; ++b) {
-    long long n1, n2, n3, y0, ny, z0, nz;
-    block_dims(P, b, &n1, &n2, &n3);
-    part_range(n2, nranks, rank, &y0, &ny);
-    part_range(n3, nranks, rank, &z0, &nz);
-    st = alloc((size_t)std::max(1LL, n1 * ny * n3) * sizeof(double));
-    if (!st) st = alloc((size_t)std::max(1LL, n1 * n2 * nz) * sizeof(double));
+  } catch (...) {
+    return abi_exception(__func__);
   }
-  if (!st) st = alloc((size_t)nranks * sizeof(unsigned long long));
-  if (!st) st = dalloc(&raw->counter, 1);
-  if (!st) {
-    cudaError_t e = cudaMemset(raw->counter, 0, sizeof(unsigned long long));
-    if (e != cudaSuccess) st = cuda_fail(e, "fdp_comm_create: counter");
-  }
-  if (st) {
-    free_comm(raw);
-    return st;
-  }
-  *out = raw;
-  return FDP_OK;
 }
 
 extern "C" fdp_status fdp_comm_connect(fdp_comm c, const void* all_blobs) {
-  if (!c || !all_blobs) return fail(FDP_ERR_INVALID_ARG, "fdp_comm_connect: NULL argument");
-  if (c->connected) return fail(FDP_ERR_INVALID_ARG, "fdp_comm_connect: already connected");
-  DeviceGuard dg(c->device);
-  const int G = c->nranks, nb = c->nblocks, per = 2 * nb + 1;
-  std::vector<double*> py((size_t)nb * G), pz((size_t)nb * G);
-  std::vector<unsigned long long*> pf(G);
-  for (int r = 0; r < G; ++r) {
-    for (int i = 0; i < per; ++i) {
-      void* p = c->own[i];
-      if (r != c->rank) {  // map the peer's buffer (P2P over NVLink)
-        const char* hp = static_cast<const char*>(all_blobs) + ((size_t)r * per + i) * sizeof(cudaIpcMemHandle_t);
-        fdp_status st = fdp_peer_open(hp, c->device, &p);
-        if (st) return st;
-        c->opened.push_back(p);
-      }
-      if (i < 2 * nb) {
-        const int b = i / 2;
-        (i % 2 == 0 ? py : pz)[(size_t)b * G + r] = static_cast<double*>(p);
-      } else {
-        pf[r] = static_cast<unsigned long long*>(p);
+  try {
+    if (!c || !all_blobs) return fail(FDP_ERR_INVALID_ARG, "fdp_comm_connect: NULL argument");
+    if (c->connected) return fail(FDP_ERR_INVALID_ARG, "fdp_comm_connect: already connected");
+    DeviceGuard dg(c->device);
+    const int G = c->nranks, nb = c->nblocks, per = 2 * nb + 1;
+    std::vector<double*> py((size_t)nb * G), pz((size_t)nb * G);
+    std::vector<unsigned long long*> pf(G);
+    for (int r = 0; r < G; ++r) {
+      for (int i = 0; i < per; ++i) {
+        void* p = c->own[i];
+        if (r != c->rank) {  // map the peer's buffer (P2P over NVLink)
+          const char* hp = static_cast<const char*>(all_blobs) + ((size_t)r * per + i) * sizeof(cudaIpcMemHandle_t);
+          fdp_status st = fdp_peer_open(hp, c->device, &p);
+          if (st) return st;
+          c->opened.push_back(p);
+        }
+        if (i < 2 * nb) {
+          const int b = i / 2;
+          (i % 2 == 0 ? py : pz)[(size_t)b * G + r] = static_cast<double*>(p);
+        } else {
+          pf[r] = static_cast<unsigned long long*>(p);
+        }
       }
     }
+    fdp_status st;
+    if ((st = dalloc(&c->peers_y, py.size())) || (st = dalloc(&c->peers_z, pz.size())) ||
+        (st = dalloc(&c->flag_ptrs, pf.size())))
+      return st;
+    FDP_CUDA(cudaMemcpy(c->peers_y, py.data(), py.size() * sizeof(double*), cudaMemcpyHostToDevice), "fdp_comm_connect");
+    FDP_CUDA(cudaMemcpy(c->peers_z, pz.data(), pz.size() * sizeof(double*), cudaMemcpyHostToDevice), "fdp_comm_connect");
+    FDP_CUDA(cudaMemcpy(c->flag_ptrs, pf.data(), pf.size() * sizeof(void*), cudaMemcpyHostToDevice), "fdp_comm_connect");
+    c->connected = true;
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
   }
-  fdp_status st;
-  if ((st = dalloc(&c->peers_y, py.size())) || (st = dalloc(&c->peers_z, pz.size())) ||
-      (st = dalloc(&c->flag_ptrs, pf.size())))
-    return st;
-  FDP_CUDA(cudaMemcpy(c->peers_y, py.data(), py.size() * sizeof(double*), cudaMemcpyHostToDevice), "fdp_comm_connect");
-  FDP_CUDA(cudaMemcpy(c->peers_z, pz.data(), pz.size() * sizeof(double*), cudaMemcpyHostToDevice), "fdp_comm_connect");
-  FDP_CUDA(cudaMemcpy(c->flag_ptrs, pf.data(), pf.size() * sizeof(void*), cudaMemcpyHostToDevice), "fdp_comm_connect");
-  c->connected = true;
-  return FDP_OK;
 }
 
 extern "C" int64_t block_precond_sharded_size(fdp_block P, int nranks, int rank) {
-  if (!P || P->D != 3 || nranks < 1 || rank < 0 || rank >= nranks) return 0;
-  long long tot = 0;
-  for (int b = 0; b <= P->D; ++b) {
-    long long n1, n2, n3, z0, nz;
-    block_dims(P, b, &n1, &n2, &n3);
-    part_range(n3, nranks, rank, &z0, &nz);
-    tot += n1 * n2 * nz;
+  try {
+    if (!P || P->D != 3 || nranks < 1 || rank < 0 || rank >= nranks) return 0;
+    long long tot = 0;
+    for (int b = 0; b <= P->D; ++b) {
+      long long n1, n2, n3, z0, nz;
+      block_dims(P, b, &n1, &n2, &n3);
+      part_range(n3, nranks, rank, &z0, &nz);
+      tot += n1 * n2 * nz;
+    }
+    return tot;
+  } catch (...) {
+    return 0;
   }
-  return tot;
 }
 
 extern "C" size_t block_precond_sharded_workspace_bytes(fdp_block P, fdp_comm c) {
-  if (!P || !c || P->D != 3) return 0;
-  size_t m = 0;
-  for (int k = 0; k < P->D; ++k)
-    m = std::max(m, fd_slab_workspace_bytes(const_cast<fdp_fd>(P->vel[k]), c->nranks, c->rank));
-  m = std::max(m, kron_mass_slab_workspace_bytes(const_cast<fdp_mass>(P->pres), c->nranks, c->rank));
-  return m;
+  try {
+    if (!P || !c || P->D != 3) return 0;
+    size_t m = 0;
+    for (int k = 0; k < P->D; ++k)
+      m = std::max(m, fd_slab_workspace_bytes(const_cast<fdp_fd>(P->vel[k]), c->nranks, c->rank));
+    m = std::max(m, kron_mass_slab_workspace_bytes(const_cast<fdp_mass>(P->pres), c->nranks, c->rank));
+    return m;
+  } catch (...) {
+    return 0;
+  }
 }
 
 extern "C" fdp_status block_precond_apply_sharded(fdp_block P, fdp_comm c, const double* r, double* s,
                                                   void* workspace, void* stream) {
-  if (!P || !c) return fail(FDP_ERR_INVALID_ARG, "block_precond_apply_sharded: NULL handle");
-  if (!c->connected) return fail(FDP_ERR_INVALID_ARG, "block_precond_apply_sharded: comm not connected");
-  if (!is_device_ptr(r) || !is_device_ptr(s) || !is_device_ptr(workspace))
-    return fail(FDP_ERR_INVALID_ARG, "block_precond_apply_sharded: device pointers required");
-  DeviceGuard dg(P->device);
-  const int G = c->nranks, g = c->rank, D = P->D;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  // local layout [u_1 z-slab | .. | u_D z-slab | p z-slab]; D^{-1/2} slices of the P^G scalings
-  std::vector<long long> loff(D + 2, 0), goff(D + 1, 0);
-  for (int b = 0; b <= D; ++b) {
-    long long n1, n2, n3, z0, nz;
-    block_dims(P, b, &n1, &n2, &n3);
-    part_range(n3, G, g, &z0, &nz);
-    loff[b + 1] = loff[b] + n1 * n2 * nz;
-    goff[b] = n1 * n2 * z0;
-  }
-  auto dsc = [&](int b) -> const double* {
-    if (b < D) return P->dv ? P->dv + P->off[b] + goff[b] : nullptr;
-    return P->dq ? P->dq + goff[b] : nullptr;
-  };
-  const int nb = c->nblocks;
-  for (int phase = 0; phase < 3; ++phase) {
-    for (int b = 0; b < nb; ++b) {
-      double* const* peers = phase == 0 ? c->peers_y + (size_t)b * G : c->peers_z + (size_t)b * G;
-      const double* in = phase == 0 ? r + loff[b] : static_cast<const double*>(c->own[2 * b + (phase == 1 ? 0 : 1)]);
-      double* out = phase == 2 ? s + loff[b] : nullptr;
-      const double* ds = phase == 1 ? nullptr : dsc(b);
-      fdp_status e = b < D ? fd_apply_slab_peer(const_cast<fdp_fd>(P->vel[b]), phase, G, g, in, out,
-                                                phase == 2 ? nullptr : peers, ds, workspace, stream)
-                           : kron_mass_apply_slab_peer(const_cast<fdp_mass>(P->pres), phase, G, g, in, out,
-                                                       phase == 2 ? nullptr : peers, ds, workspace, stream);
-      if (e) return e;
+  try {
+    if (!P || !c) return fail(FDP_ERR_INVALID_ARG, "block_precond_apply_sharded: NULL handle");
+    if (!c->connected) return fail(FDP_ERR_INVALID_ARG, "block_precond_apply_sharded: comm not connected");
+    if (!is_device_ptr(r) || !is_device_ptr(s) || !is_device_ptr(workspace))
+      return fail(FDP_ERR_INVALID_ARG, "block_precond_apply_sharded: device pointers required");
+    DeviceGuard dg(P->device);
+    const int G = c->nranks, g = c->rank, D = P->D;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // local layout [u_1 z-slab | .. | u_D z-slab | p z-slab]; D^{-1/2} slices of the P^G scalings
+    std::vector<long long> loff(D + 2, 0), goff(D + 1, 0);
+    for (int b = 0; b <= D; ++b) {
+      long long n1, n2, n3, z0, nz;
+      block_dims(P, b, &n1, &n2, &n3);
+      part_range(n3, G, g, &z0, &nz);
+      loff[b + 1] = loff[b] + n1 * n2 * nz;
+      goff[b] = n1 * n2 * z0;
     }
-    // exchanges complete on every rank before the next phase reads (and, after phase 2, before
-    // the next apply's phase 0 overwrites y-slabs)
-    FDP_CUDA(launch_peer_barrier(c->flag_ptrs, c->counter, G, g, st), "block_precond_apply_sharded: barrier");
+    auto dsc = [&](int b) -> const double* {
+      if (b < D) return P->dv ? P->dv + P->off[b] + goff[b] : nullptr;
+      return P->dq ? P->dq + goff[b] : nullptr;
+    };
+    const int nb = c->nblocks;
+    for (int phase = 0; phase < 3; ++phase) {
+      for (int b = 0; b < nb; ++b) {
+        double* const* peers = phase == 0 ? c->peers_y + (size_t)b * G : c->peers_z + (size_t)b * G;
+        const double* in = phase == 0 ? r + loff[b] : static_cast<const double*>(c->own[2 * b + (phase == 1 ? 0 : 1)]);
+        double* out = phase == 2 ? s + loff[b] : nullptr;
+        const double* ds = phase == 1 ? nullptr : dsc(b);
+        fdp_status e = b < D ? fd_apply_slab_peer(const_cast<fdp_fd>(P->vel[b]), phase, G, g, in, out,
+                                                  phase == 2 ? nullptr : peers, ds, workspace, stream)
+                             : kron_mass_apply_slab_peer(const_cast<fdp_mass>(P->pres), phase, G, g, in, out,
+                                                         phase == 2 ? nullptr : peers, ds, workspace, stream);
+        if (e) return e;
+      }
+      // exchanges complete on every rank before the next phase reads (and, after phase 2, before
+      // the next apply's phase 0 overwrites y-slabs)
+      FDP_CUDA(launch_peer_barrier(c->flag_ptrs, c->counter, G, g, st), "block_precond_apply_sharded: barrier");
+    }
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
   }
-  return FDP_OK;
 }
 
 extern "C" fdp_status fdp_comm_destroy(fdp_comm c) {
-  if (!c) return FDP_OK;
-  DeviceGuard dg(c->device);
-  free_comm(c);
-  return FDP_OK;
+  try {
+    if (!c) return FDP_OK;
+    DeviceGuard dg(c->device);
+    free_comm(c);
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
 }
 
 extern "C" size_t kron_mass_slab_workspace_bytes(fdp_mass h, int nranks, int rank) {
-  if (!h || h->D != 3 || nranks < 1 || rank < 0 || rank >= nranks) return 0;
-  long long z0, nz;
-  part_range(h->n[2], nranks, rank, &z0, &nz);
-  return (size_t)((long long)h->n[0] * h->n[1] * nz) * sizeof(double);
+  try {
+    if (!h || h->D != 3 || nranks < 1 || rank < 0 || rank >= nranks) return 0;
+    long long z0, nz;
+    part_range(h->n[2], nranks, rank, &z0, &nz);
+    return (size_t)((long long)h->n[0] * h->n[1] * nz) * sizeof(double);
+  } catch (...) {
+    return 0;
+  }
 }
 
 extern "C" fdp_status kron_mass_apply_slab(fdp_mass h, int phase, int nranks, int rank,
                                            const double* in, double* out, const double* dscale,
                                            void* workspace, void* stream) {
-  if (!h) return fail(FDP_ERR_INVALID_ARG, "kron_mass_apply_slab: NULL handle");
-  if (h->D != 3) return fail(FDP_ERR_UNSUPPORTED, "kron_mass_apply_slab: D must be 3");
-  if (nranks < 1 || rank < 0 || rank >= nranks || phase < 0 || phase > 2)
-    return fail(FDP_ERR_INVALID_ARG, "kron_mass_apply_slab: bad phase / rank");
-  const long long n1 = h->n[0], n2 = h->n[1], n3 = h->n[2];
-  long long z0, nz, y0, ny;
-  part_range(n3, nranks, rank, &z0, &nz);
-  part_range(n2, nranks, rank, &y0, &ny);
-  if ((phase == 1 ? ny : nz) == 0) return FDP_OK;
-  if (!is_device_ptr(in) || !is_device_ptr(out) || (phase == 0 && !is_device_ptr(workspace)) ||
-      (dscale && !is_device_ptr(dscale)))
-    return fail(FDP_ERR_INVALID_ARG, "kron_mass_apply_slab: device pointers required");
-  DeviceGuard dg(h->device);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  auto mode = [&](int d, const double* src, double* dst, long long P, long long Q, const double* pre) {
-    MassMode m{};
-    m.in = src;
-    m.out = dst;
-    m.Lb = h->Lb[d];
-    m.invd = h->invd[d];
-    m.Mb = h->Mb[d];
-    m.pre = pre;
-    m.N = P * h->n[d] * Q;
-    m.bs = 0;
-    m.P = (int)P;
-    m.n = h->n[d];
-    m.Q = (int)Q;
-    m.batch = 1;
-    m.band = h->band[d];
-    return launch_mass_mode(m, s);
-  };
-  double* T = static_cast<double*>(workspace);
-  if (phase == 0) {
-    FDP_CUDA(mode(0, in, T, 1, n2 * nz, dscale), "kron_mass_apply_slab: mode 1");
-    FDP_CUDA(mode(1, T, T, n1, nz, nullptr), "kron_mass_apply_slab: mode 2");
-    FDP_CUDA(launch_slab_copy(T, out, (int)n1, (int)n2, (int)nz, nranks, 0, nullptr, s),
-             "kron_mass_apply_slab: pack");
-  } else if (phase == 1) {
-    FDP_CUDA(mode(2, in, out, n1 * ny, 1, nullptr), "kron_mass_apply_slab: mode 3");
-  } else {
-    FDP_CUDA(launch_slab_copy(in, out, (int)n1, (int)n2, (int)nz, nranks, 1, dscale, s),
-             "kron_mass_apply_slab: unpack");
+  try {
+    if (!h) return fail(FDP_ERR_INVALID_ARG, "kron_mass_apply_slab: NULL handle");
+    if (h->D != 3) return fail(FDP_ERR_UNSUPPORTED, "kron_mass_apply_slab: D must be 3");
+    if (nranks < 1 || rank < 0 || rank >= nranks || phase < 0 || phase > 2)
+      return fail(FDP_ERR_INVALID_ARG, "kron_mass_apply_slab: bad phase / rank");
+    const long long n1 = h->n[0], n2 = h->n[1], n3 = h->n[2];
+    long long z0, nz, y0, ny;
+    part_range(n3, nranks, rank, &z0, &nz);
+    part_range(n2, nranks, rank, &y0, &ny);
+    if ((phase == 1 ? ny : nz) == 0) return FDP_OK;
+    if (!is_device_ptr(in) || !is_device_ptr(out) || (phase == 0 && !is_device_ptr(workspace)) ||
+        (dscale && !is_device_ptr(dscale)))
+      return fail(FDP_ERR_INVALID_ARG, "kron_mass_apply_slab: device pointers required");
+    DeviceGuard dg(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    auto mode = [&](int d, const double* src, double* dst, long long P, long long Q, const double* pre) {
+      MassMode m{};
+      m.in = src;
+      m.out = dst;
+      m.Lb = h->Lb[d];
+      m.invd = h->invd[d];
+      m.Mb = h->Mb[d];
+      m.pre = pre;
+      m.N = P * h->n[d] * Q;
+      m.bs = 0;
+      m.P = (int)P;
+      m.n = h->n[d];
+      m.Q = (int)Q;
+      m.batch = 1;
+      m.band = h->band[d];
+      return launch_mass_mode(m, s);
+    };
+    double* T = static_cast<double*>(workspace);
+    if (phase == 0) {
+      FDP_CUDA(mode(0, in, T, 1, n2 * nz, dscale), "kron_mass_apply_slab: mode 1");
+      FDP_CUDA(mode(1, T, T, n1, nz, nullptr), "kron_mass_apply_slab: mode 2");
+      FDP_CUDA(launch_slab_copy(T, out, (int)n1, (int)n2, (int)nz, nranks, 0, nullptr, s),
+               "kron_mass_apply_slab: pack");
+    } else if (phase == 1) {
+      FDP_CUDA(mode(2, in, out, n1 * ny, 1, nullptr), "kron_mass_apply_slab: mode 3");
+    } else {
+      FDP_CUDA(launch_slab_copy(in, out, (int)n1, (int)n2, (int)nz, nranks, 1, dscale, s),
+               "kron_mass_apply_slab: unpack");
+    }
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
   }
-  return FDP_OK;
 }
 
 // ------------------------------------------------------------------------------------------------
 // host helpers: quadrature points and mixed univariate matrices
 // ------------------------------------------------------------------------------------------------
 extern "C" fdp_status iga_quadrature(int n_el, int q, double* x, double* w) {
-  if (n_el < 1 || q < 1) return fail(FDP_ERR_SHAPE, "iga_quadrature: n_el, q >= 1");
-  iga_quadrature_build(n_el, q, x, w);
-  return FDP_OK;
+  try {
+    if (n_el < 1 || q < 1) return fail(FDP_ERR_SHAPE, "iga_quadrature: n_el, q >= 1");
+    iga_quadrature_build(n_el, q, x, w);
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
 }
 
 extern "C" fdp_status iga_mixed(int deg_test, int alpha_test, int flags_test, int deg_trial,
                                 int alpha_trial, int flags_trial, int n_el, int dtest, int dtrial,
                                 int q, const double* wq, double* out, int32_t* n_test,
                                 int32_t* n_trial) {
-  if (!n_test || !n_trial) return fail(FDP_ERR_INVALID_ARG, "iga_mixed: NULL size outputs");
-  std::string err;
-  int a = 0, b = 0;
-  int st = iga_mixed_build(deg_test, alpha_test, flags_test, deg_trial, alpha_trial, flags_trial,
-                           n_el, dtest, dtrial, q, wq, out, &a, &b, &err);
-  if (st) return fail((fdp_status)st, err);
-  *n_test = a;
-  *n_trial = b;
-  return FDP_OK;
+  try {
+    if (!n_test || !n_trial) return fail(FDP_ERR_INVALID_ARG, "iga_mixed: NULL size outputs");
+    std::string err;
+    int a = 0, b = 0;
+    int st = iga_mixed_build(deg_test, alpha_test, flags_test, deg_trial, alpha_trial, flags_trial,
+                             n_el, dtest, dtrial, q, wq, out, &a, &b, &err);
+    if (st) return fail((fdp_status)st, err);
+    *n_test = a;
+    *n_trial = b;
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -2145,26 +2344,34 @@ static double* dot_scratch(int dev) {
 
 extern "C" fdp_status fdp_vec_dot(const double* x, const double* y, int64_t n, double* result,
                                   void* stream) {
-  if (n < 0) return fail(FDP_ERR_SHAPE, "fdp_vec_dot: n < 0");
-  if (!is_device_ptr(result) || (n > 0 && (!is_device_ptr(x) || !is_device_ptr(y))))
-    return fail(FDP_ERR_INVALID_ARG, "fdp_vec_dot: device pointers required");
-  int dev = 0;
-  cudaGetDevice(&dev);
-  double* sc = dot_scratch(dev);
-  if (!sc) return fail(FDP_ERR_OOM, "fdp_vec_dot: scratch");
-  FDP_CUDA(launch_dot(x, y, n, result, sc, static_cast<cudaStream_t>(stream)), "fdp_vec_dot");
-  return FDP_OK;
+  try {
+    if (n < 0) return fail(FDP_ERR_SHAPE, "fdp_vec_dot: n < 0");
+    if (!is_device_ptr(result) || (n > 0 && (!is_device_ptr(x) || !is_device_ptr(y))))
+      return fail(FDP_ERR_INVALID_ARG, "fdp_vec_dot: device pointers required");
+    int dev = 0;
+    cudaGetDevice(&dev);
+    double* sc = dot_scratch(dev);
+    if (!sc) return fail(FDP_ERR_OOM, "fdp_vec_dot: scratch");
+    FDP_CUDA(launch_dot(x, y, n, result, sc, static_cast<cudaStream_t>(stream)), "fdp_vec_dot");
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
 }
 
 extern "C" fdp_status fdp_vec_lincomb(double a, const double* x, double b, const double* y,
                                       double c, const double* z, double* out, int64_t n,
                                       void* stream) {
-  if (n < 0) return fail(FDP_ERR_SHAPE, "fdp_vec_lincomb: n < 0");
-  if (n == 0) return FDP_OK;
-  if (!is_device_ptr(x) || !is_device_ptr(out) || (y && !is_device_ptr(y)) || (z && !is_device_ptr(z)))
-    return fail(FDP_ERR_INVALID_ARG, "fdp_vec_lincomb: device pointers required");
-  FDP_CUDA(launch_lincomb(a, x, b, y, c, z, out, n, static_cast<cudaStream_t>(stream)), "fdp_vec_lincomb");
-  return FDP_OK;
+  try {
+    if (n < 0) return fail(FDP_ERR_SHAPE, "fdp_vec_lincomb: n < 0");
+    if (n == 0) return FDP_OK;
+    if (!is_device_ptr(x) || !is_device_ptr(out) || (y && !is_device_ptr(y)) || (z && !is_device_ptr(z)))
+      return fail(FDP_ERR_INVALID_ARG, "fdp_vec_lincomb: device pointers required");
+    FDP_CUDA(launch_lincomb(a, x, b, y, c, z, out, n, static_cast<cudaStream_t>(stream)), "fdp_vec_lincomb");
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -2192,56 +2399,60 @@ static void free_kron(fdp_kron h) {
 extern "C" fdp_status kron_op_setup(int D, int nterms, const int32_t* nin, const int32_t* nout,
                                     const double* const* factors, const double* coef, int device,
                                     fdp_kron* out) {
-  if (!out) return fail(FDP_ERR_INVALID_ARG, "kron_op_setup: out is NULL");
-  *out = nullptr;
-  if (D < 2 || D > 3) return fail(FDP_ERR_UNSUPPORTED, "kron_op_setup: D must be 2 or 3");
-  if (nterms < 1 || !nin || !nout || !factors || !coef)
-    return fail(FDP_ERR_INVALID_ARG, "kron_op_setup: bad arguments");
-  std::unique_ptr<fdp_kron_s> h(new (std::nothrow) fdp_kron_s);
-  if (!h) return fail(FDP_ERR_OOM, "kron_op_setup: host allocation");
-  h->D = D;
-  h->nterms = nterms;
-  h->device = device;
-  for (int d = 0; d < D; ++d) {
-    if (nin[d] < 1 || nin[d] > 2048 || nout[d] < 1 || nout[d] > 2048)
-      return fail(FDP_ERR_SHAPE, "kron_op_setup: extents must be in [1, 2048]");
-    h->nin[d] = nin[d];
-    h->nout[d] = nout[d];
-  }
-  h->coef.assign(coef, coef + nterms);
-  DeviceGuard dg(device);
-  fdp_kron raw = h.release();
-  raw->f.resize((size_t)nterms * D);
-  for (int t = 0; t < nterms; ++t)
+  try {
+    if (!out) return fail(FDP_ERR_INVALID_ARG, "kron_op_setup: out is NULL");
+    *out = nullptr;
+    if (D < 2 || D > 3) return fail(FDP_ERR_UNSUPPORTED, "kron_op_setup: D must be 2 or 3");
+    if (nterms < 1 || !nin || !nout || !factors || !coef)
+      return fail(FDP_ERR_INVALID_ARG, "kron_op_setup: bad arguments");
+    std::unique_ptr<fdp_kron_s> h(new (std::nothrow) fdp_kron_s);
+    if (!h) return fail(FDP_ERR_OOM, "kron_op_setup: host allocation");
+    h->D = D;
+    h->nterms = nterms;
+    h->device = device;
     for (int d = 0; d < D; ++d) {
-      const double* F = factors[t * D + d];
-      if (!F) {
-        free_kron(raw);
-        return fail(FDP_ERR_INVALID_ARG, "kron_op_setup: NULL factor");
-      }
-      KronFactor& kf = raw->f[t * D + d];
-      kf.nin = nin[d];
-      kf.nout = nout[d];
-      for (int i = 0; i < std::min(nin[d], nout[d]); ++i) kf.diag.push_back(F[i + (size_t)nout[d] * i]);
-      // columns tile over nout; the small path also needs BN >= nin (W rows staged in smem)
-      TileCfg c = choose_tile(std::max(nin[d], nout[d]) <= kSmallMaxN ? std::max(nin[d], nout[d]) : nout[d]);
-      c.kpad = ((nin[d] + 31) / 32) * 32;
-      kf.cfg = c;
-      const int rows = std::max(c.kpad, c.ldw);
-      std::vector<double> w((size_t)rows * c.ldw, 0.0);
-      for (int k = 0; k < nin[d]; ++k)
-        for (int a = 0; a < nout[d]; ++a) w[(size_t)k * c.ldw + a] = F[a + (size_t)nout[d] * k];
-      fdp_status st = dalloc(&kf.W, w.size());
-      cudaError_t e = st ? cudaSuccess : cudaMemcpy(kf.W, w.data(), w.size() * 8, cudaMemcpyHostToDevice);
-      if (!st && e == cudaSuccess) e = prepare_mode_kernels(c);
-      if (!st && e == cudaSuccess) e = prepare_mode_small(c.NT);
-      if (st || e != cudaSuccess) {
-        free_kron(raw);
-        return st ? st : cuda_fail(e, "kron_op_setup: upload");
-      }
+      if (nin[d] < 1 || nin[d] > 2048 || nout[d] < 1 || nout[d] > 2048)
+        return fail(FDP_ERR_SHAPE, "kron_op_setup: extents must be in [1, 2048]");
+      h->nin[d] = nin[d];
+      h->nout[d] = nout[d];
     }
-  *out = raw;
-  return FDP_OK;
+    h->coef.assign(coef, coef + nterms);
+    DeviceGuard dg(device);
+    fdp_kron raw = h.release();
+    raw->f.resize((size_t)nterms * D);
+    for (int t = 0; t < nterms; ++t)
+      for (int d = 0; d < D; ++d) {
+        const double* F = factors[t * D + d];
+        if (!F) {
+          free_kron(raw);
+          return fail(FDP_ERR_INVALID_ARG, "kron_op_setup: NULL factor");
+        }
+        KronFactor& kf = raw->f[t * D + d];
+        kf.nin = nin[d];
+        kf.nout = nout[d];
+        for (int i = 0; i < std::min(nin[d], nout[d]); ++i) kf.diag.push_back(F[i + (size_t)nout[d] * i]);
+        // columns tile over nout; the small path also needs BN >= nin (W rows staged in smem)
+        TileCfg c = choose_tile(std::max(nin[d], nout[d]) <= kSmallMaxN ? std::max(nin[d], nout[d]) : nout[d]);
+        c.kpad = ((nin[d] + 31) / 32) * 32;
+        kf.cfg = c;
+        const int rows = std::max(c.kpad, c.ldw);
+        std::vector<double> w((size_t)rows * c.ldw, 0.0);
+        for (int k = 0; k < nin[d]; ++k)
+          for (int a = 0; a < nout[d]; ++a) w[(size_t)k * c.ldw + a] = F[a + (size_t)nout[d] * k];
+        fdp_status st = dalloc(&kf.W, w.size());
+        cudaError_t e = st ? cudaSuccess : cudaMemcpy(kf.W, w.data(), w.size() * 8, cudaMemcpyHostToDevice);
+        if (!st && e == cudaSuccess) e = prepare_mode_kernels(c);
+        if (!st && e == cudaSuccess) e = prepare_mode_small(c.NT);
+        if (st || e != cudaSuccess) {
+          free_kron(raw);
+          return st ? st : cuda_fail(e, "kron_op_setup: upload");
+        }
+      }
+    *out = raw;
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
 }
 
 static long long kron_max_inter(const fdp_kron_s* h) {
@@ -2255,85 +2466,101 @@ static long long kron_max_inter(const fdp_kron_s* h) {
 }
 
 extern "C" size_t kron_op_workspace_bytes(fdp_kron h, int64_t batch) {
-  return h && batch > 0 ? (size_t)(2 * kron_max_inter(h) * batch) * sizeof(double) : 0;
+  try {
+    return h && batch > 0 ? (size_t)(2 * kron_max_inter(h) * batch) * sizeof(double) : 0;
+  } catch (...) {
+    return 0;
+  }
 }
 
 extern "C" fdp_status kron_op_apply(fdp_kron h, const double* x, int64_t xbs, double* y,
                                     int64_t ybs, double alpha, double beta, int64_t batch,
                                     void* workspace, void* stream) {
-  if (!h) return fail(FDP_ERR_INVALID_ARG, "kron_op_apply: NULL handle");
-  if (batch < 0) return fail(FDP_ERR_SHAPE, "kron_op_apply: batch < 0");
-  if (batch == 0) return FDP_OK;
-  if (!is_device_ptr(x) || !is_device_ptr(y) || !is_device_ptr(workspace))
-    return fail(FDP_ERR_INVALID_ARG, "kron_op_apply: device pointers required");
-  DeviceGuard dg(h->device);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int D = h->D;
-  const long long inter = kron_max_inter(h);
-  double* buf[2] = {static_cast<double*>(workspace), static_cast<double*>(workspace) + inter * batch};
-  for (int t = 0; t < h->nterms; ++t) {
-    const double* src = x;
-    long long sbs = xbs;
-    for (int d = 0; d < D; ++d) {
-      const KronFactor& kf = h->f[t * D + d];
-      long long P = 1, Q = 1;
-      for (int e = 0; e < d; ++e) P *= h->nout[e];
-      for (int e = d + 1; e < D; ++e) Q *= h->nin[e];
-      const bool last = d == D - 1;
-      double* dst = last ? y : buf[d % 2];
-      const long long dbs = last ? ybs : P * kf.nout * Q;
-      ModeProb p{};
-      p.X = src;
-      p.Y = dst;
-      p.W = kf.W;
-      p.P = (int)P;
-      p.n = kf.nin;
-      p.nout = kf.nout;
-      p.Q = (int)Q;
-      p.N = P * kf.nout * Q;
-      p.xbs = sbs;
-      p.ybs = dbs;
-      p.batch = (int)batch;
-      p.ldw = kf.cfg.ldw;
-      p.n1 = p.n1v = 1;
-      p.xld = kf.nin;
-      p.yld = kf.nout;
-      p.vx = p.vy = 0;
-      p.epi = last ? EPI_AXPBY : EPI_NONE;
-      p.alpha = alpha * h->coef[t];
-      p.beta = t == 0 ? beta : 1.0;
-      const int BM = kK1Warps * 8 * kf.cfg.MT;
-      p.tiles_m = (int)((P * Q * batch + BM - 1) / BM);
-      p.tiles_n = kf.cfg.tiles_n;
-      p.fd_work = 0;
-      FDP_CUDA(run1(p, kf.cfg, d == 0, s), "kron_op_apply");
-      src = dst;
-      sbs = dbs;
+  try {
+    if (!h) return fail(FDP_ERR_INVALID_ARG, "kron_op_apply: NULL handle");
+    if (batch < 0) return fail(FDP_ERR_SHAPE, "kron_op_apply: batch < 0");
+    if (batch == 0) return FDP_OK;
+    if (!is_device_ptr(x) || !is_device_ptr(y) || !is_device_ptr(workspace))
+      return fail(FDP_ERR_INVALID_ARG, "kron_op_apply: device pointers required");
+    DeviceGuard dg(h->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int D = h->D;
+    const long long inter = kron_max_inter(h);
+    double* buf[2] = {static_cast<double*>(workspace), static_cast<double*>(workspace) + inter * batch};
+    for (int t = 0; t < h->nterms; ++t) {
+      const double* src = x;
+      long long sbs = xbs;
+      for (int d = 0; d < D; ++d) {
+        const KronFactor& kf = h->f[t * D + d];
+        long long P = 1, Q = 1;
+        for (int e = 0; e < d; ++e) P *= h->nout[e];
+        for (int e = d + 1; e < D; ++e) Q *= h->nin[e];
+        const bool last = d == D - 1;
+        double* dst = last ? y : buf[d % 2];
+        const long long dbs = last ? ybs : P * kf.nout * Q;
+        ModeProb p{};
+        p.X = src;
+        p.Y = dst;
+        p.W = kf.W;
+        p.P = (int)P;
+        p.n = kf.nin;
+        p.nout = kf.nout;
+        p.Q = (int)Q;
+        p.N = P * kf.nout * Q;
+        p.xbs = sbs;
+        p.ybs = dbs;
+        p.batch = (int)batch;
+        p.ldw = kf.cfg.ldw;
+        p.n1 = p.n1v = 1;
+        p.xld = kf.nin;
+        p.yld = kf.nout;
+        p.vx = p.vy = 0;
+        p.epi = last ? EPI_AXPBY : EPI_NONE;
+        p.alpha = alpha * h->coef[t];
+        p.beta = t == 0 ? beta : 1.0;
+        const int BM = kK1Warps * 8 * kf.cfg.MT;
+        p.tiles_m = (int)((P * Q * batch + BM - 1) / BM);
+        p.tiles_n = kf.cfg.tiles_n;
+        p.fd_work = 0;
+        FDP_CUDA(run1(p, kf.cfg, d == 0, s), "kron_op_apply");
+        src = dst;
+        sbs = dbs;
+      }
     }
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
   }
-  return FDP_OK;
 }
 
 extern "C" fdp_status kron_op_diagonal(fdp_kron h, double* out) {
-  if (!h || !out) return fail(FDP_ERR_INVALID_ARG, "kron_op_diagonal: NULL argument");
-  for (int d = 0; d < h->D; ++d)
-    if (h->nin[d] != h->nout[d]) return fail(FDP_ERR_SHAPE, "kron_op_diagonal: operator is not square");
-  long long N = 1;
-  for (int d = 0; d < h->D; ++d) N *= h->nin[d];
-  std::fill(out, out + N, 0.0);
-  for (int t = 0; t < h->nterms; ++t) {
-    std::vector<const double*> f(h->D);
-    for (int d = 0; d < h->D; ++d) f[d] = h->f[t * h->D + d].diag.data();
-    kron_diag_accumulate(h->D, h->nin, f, h->coef[t], out);
+  try {
+    if (!h || !out) return fail(FDP_ERR_INVALID_ARG, "kron_op_diagonal: NULL argument");
+    for (int d = 0; d < h->D; ++d)
+      if (h->nin[d] != h->nout[d]) return fail(FDP_ERR_SHAPE, "kron_op_diagonal: operator is not square");
+    long long N = 1;
+    for (int d = 0; d < h->D; ++d) N *= h->nin[d];
+    std::fill(out, out + N, 0.0);
+    for (int t = 0; t < h->nterms; ++t) {
+      std::vector<const double*> f(h->D);
+      for (int d = 0; d < h->D; ++d) f[d] = h->f[t * h->D + d].diag.data();
+      kron_diag_accumulate(h->D, h->nin, f, h->coef[t], out);
+    }
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
   }
-  return FDP_OK;
 }
 
 extern "C" fdp_status kron_op_destroy(fdp_kron h) {
-  if (!h) return FDP_OK;
-  DeviceGuard dg(h->device);
-  free_kron(h);
-  return FDP_OK;
+  try {
+    if (!h) return FDP_OK;
+    DeviceGuard dg(h->device);
+    free_kron(h);
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
 }
 
 static long long kron_prod(const int* v, int D) {
@@ -2451,31 +2678,39 @@ static cudaError_t enqueue_kron_tasks(const std::vector<KronTask>& tasks, double
 }
 
 extern "C" size_t kron_ops_workspace_bytes(int nops, const fdp_kron* ops) {
-  if (nops < 1 || !ops) return 0;
-  std::vector<KronTask> tasks;
-  for (int i = 0; i < nops; ++i) {
-    if (!ops[i]) return 0;
-    tasks.push_back({ops[i], nullptr, nullptr, 1.0});
+  try {
+    if (nops < 1 || !ops) return 0;
+    std::vector<KronTask> tasks;
+    for (int i = 0; i < nops; ++i) {
+      if (!ops[i]) return 0;
+      tasks.push_back({ops[i], nullptr, nullptr, 1.0});
+    }
+    return (size_t)kron_tasks_ws_elems(tasks) * sizeof(double);
+  } catch (...) {
+    return 0;
   }
-  return (size_t)kron_tasks_ws_elems(tasks) * sizeof(double);
 }
 
 extern "C" fdp_status kron_ops_apply(int nops, const fdp_kron* ops, const double* const* x,
                                      double* const* y, const double* alpha, double beta,
                                      void* workspace, void* stream) {
-  if (nops < 1 || !ops || !x || !y || !alpha) return fail(FDP_ERR_INVALID_ARG, "kron_ops_apply: bad arguments");
-  const int D = ops[0] ? ops[0]->D : 0;
-  std::vector<KronTask> tasks;
-  for (int i = 0; i < nops; ++i) {
-    if (!ops[i] || ops[i]->D != D) return fail(FDP_ERR_INVALID_ARG, "kron_ops_apply: NULL or mixed-D operator");
-    if (!is_device_ptr(x[i]) || !is_device_ptr(y[i])) return fail(FDP_ERR_INVALID_ARG, "kron_ops_apply: device pointers required");
-    tasks.push_back({ops[i], x[i], y[i], alpha[i]});
+  try {
+    if (nops < 1 || !ops || !x || !y || !alpha) return fail(FDP_ERR_INVALID_ARG, "kron_ops_apply: bad arguments");
+    const int D = ops[0] ? ops[0]->D : 0;
+    std::vector<KronTask> tasks;
+    for (int i = 0; i < nops; ++i) {
+      if (!ops[i] || ops[i]->D != D) return fail(FDP_ERR_INVALID_ARG, "kron_ops_apply: NULL or mixed-D operator");
+      if (!is_device_ptr(x[i]) || !is_device_ptr(y[i])) return fail(FDP_ERR_INVALID_ARG, "kron_ops_apply: device pointers required");
+      tasks.push_back({ops[i], x[i], y[i], alpha[i]});
+    }
+    if (!is_device_ptr(workspace)) return fail(FDP_ERR_INVALID_ARG, "kron_ops_apply: workspace must be device memory");
+    DeviceGuard dg(ops[0]->device);
+    FDP_CUDA(enqueue_kron_tasks(tasks, beta, {}, static_cast<double*>(workspace), static_cast<cudaStream_t>(stream)),
+             "kron_ops_apply");
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
   }
-  if (!is_device_ptr(workspace)) return fail(FDP_ERR_INVALID_ARG, "kron_ops_apply: workspace must be device memory");
-  DeviceGuard dg(ops[0]->device);
-  FDP_CUDA(enqueue_kron_tasks(tasks, beta, {}, static_cast<double*>(workspace), static_cast<cudaStream_t>(stream)),
-           "kron_ops_apply");
-  return FDP_OK;
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -2537,181 +2772,229 @@ static long long tri_ws_elems(const fdp_block_s* h, int variant, const fdp_kron*
 
 extern "C" size_t block_tri_workspace_bytes(fdp_block h, int variant, const fdp_kron* B,
                                             const fdp_kron* BT) {
-  if (check_tri_args(h, variant, B, BT, "block_tri_workspace_bytes")) return 0;
-  return (size_t)tri_ws_elems(h, variant, B, BT) * sizeof(double);
+  try {
+    if (check_tri_args(h, variant, B, BT, "block_tri_workspace_bytes")) return 0;
+    return (size_t)tri_ws_elems(h, variant, B, BT) * sizeof(double);
+  } catch (...) {
+    return 0;
+  }
 }
 
 extern "C" fdp_status block_tri_apply(fdp_block h, int variant, const fdp_kron* B, const fdp_kron* BT,
                                       const double* r, double* s, void* workspace, void* stream) {
-  fdp_status cs = check_tri_args(h, variant, B, BT, "block_tri_apply");
-  if (cs) return cs;
-  if (!is_device_ptr(r) || !is_device_ptr(s) || !is_device_ptr(workspace))
-    return fail(FDP_ERR_INVALID_ARG, "block_tri_apply: r, s and workspace must be device memory");
-  if (r == s) return fail(FDP_ERR_INVALID_ARG, "block_tri_apply: r and s must not alias");
-  DeviceGuard dg(h->device);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int D = h->D;
-  const long long nv = h->nvel;
-  double* T = static_cast<double*>(workspace);        // velocity FD intermediates
-  double* K = T + vel_ws_elems(h);                    // Kronecker partials
-  std::vector<KronTask> tb, tbt;
-  for (int k = 0; k < D; ++k) {
-    tb.push_back({B[k], nullptr, nullptr, 1.0});
-    tbt.push_back({BT[k], nullptr, nullptr, 1.0});
-  }
-  const long long kr = std::max(kron_tasks_ws_elems(tbt), variant == FDP_PREC_CONSTRAINED ? kron_tasks_ws_elems(tb) : 0LL);
-  double* tu = K + kr;                                // velocity temporaries
-  double* zu = tu + nv;
-  double* tp = zu + nv;                               // pressure temporary
-  const double* ru = r;
-  const double* rp = r + nv;
-  double* su = s;
-  double* sp = s + nv;
-  auto negate = [&](const double* a, double* y, long long n) {
-    PartSum ps{};
-    ps.nparts = 1;
-    ps.parts[0] = a;
-    ps.coef[0] = -1.0;
-    return launch_partsum(ps, y, 0.0, n, st);
-  };
-  if (variant == FDP_PREC_TRIANGULAR) {
-    // [[P_V, B^T], [0, -P_Q]] s = r: t_p = P_Q^{-1} r_p, s_p = -t_p, s_u = P_V^{-1}(r_u + B^T t_p)
-    FDP_CUDA(enqueue_mass(h->pres, FDP_MASS_INVERSE, rp, tp, h->pres->N, h->dq, 1, st, nullptr), "block_tri_apply: P_Q");
+  try {
+    fdp_status cs = check_tri_args(h, variant, B, BT, "block_tri_apply");
+    if (cs) return cs;
+    if (!is_device_ptr(r) || !is_device_ptr(s) || !is_device_ptr(workspace))
+      return fail(FDP_ERR_INVALID_ARG, "block_tri_apply: r, s and workspace must be device memory");
+    if (r == s) return fail(FDP_ERR_INVALID_ARG, "block_tri_apply: r and s must not alias");
+    DeviceGuard dg(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int D = h->D;
+    const long long nv = h->nvel;
+    double* T = static_cast<double*>(workspace);        // velocity FD intermediates
+    double* K = T + vel_ws_elems(h);                    // Kronecker partials
+    std::vector<KronTask> tb, tbt;
+    for (int k = 0; k < D; ++k) {
+      tb.push_back({B[k], nullptr, nullptr, 1.0});
+      tbt.push_back({BT[k], nullptr, nullptr, 1.0});
+    }
+    const long long kr = std::max(kron_tasks_ws_elems(tbt), variant == FDP_PREC_CONSTRAINED ? kron_tasks_ws_elems(tb) : 0LL);
+    double* tu = K + kr;                                // velocity temporaries
+    double* zu = tu + nv;
+    double* tp = zu + nv;                               // pressure temporary
+    const double* ru = r;
+    const double* rp = r + nv;
+    double* su = s;
+    double* sp = s + nv;
+    auto negate = [&](const double* a, double* y, long long n) {
+      PartSum ps{};
+      ps.nparts = 1;
+      ps.parts[0] = a;
+      ps.coef[0] = -1.0;
+      return launch_partsum(ps, y, 0.0, n, st);
+    };
+    if (variant == FDP_PREC_TRIANGULAR) {
+      // [[P_V, B^T], [0, -P_Q]] s = r: t_p = P_Q^{-1} r_p, s_p = -t_p, s_u = P_V^{-1}(r_u + B^T t_p)
+      FDP_CUDA(enqueue_mass(h->pres, FDP_MASS_INVERSE, rp, tp, h->pres->N, h->dq, 1, st, nullptr), "block_tri_apply: P_Q");
+      for (int k = 0; k < D; ++k) {
+        tbt[k].x = tp;
+        tbt[k].y = tu + h->off[k];
+      }
+      std::vector<ExtraPart> ex;
+      for (int k = 0; k < D; ++k) ex.push_back({tu + h->off[k], ru + h->off[k], 1.0});
+      FDP_CUDA(enqueue_kron_tasks(tbt, 0.0, ex, K, st), "block_tri_apply: B^T");
+      FDP_CUDA(enqueue_vel(h, tu, su, T, st), "block_tri_apply: P_V");
+      FDP_CUDA(negate(tp, sp, h->pres->N), "block_tri_apply: negate");
+      return FDP_OK;
+    }
+    // P_C^{-1} = [[I, -P_V^{-1}B^T], [0, I]] diag(I, -P_Q^{-1}) [[I, 0], [-B, I]] diag(P_V^{-1}, I)
+    FDP_CUDA(enqueue_vel(h, ru, su, T, st), "block_tri_apply: P_V");                 // w_u
+    for (int k = 0; k < D; ++k) {
+      tb[k].x = su + h->off[k];
+      tb[k].y = zu;  // g_p = r_p - B w_u (zu reused as the pressure temporary g_p)
+      tb[k].alpha = -1.0;
+    }
+    FDP_CUDA(enqueue_kron_tasks(tb, 0.0, {{zu, rp, 1.0}}, K, st), "block_tri_apply: B");
+    FDP_CUDA(enqueue_mass(h->pres, FDP_MASS_INVERSE, zu, tp, h->pres->N, h->dq, 1, st, nullptr), "block_tri_apply: P_Q");
+    FDP_CUDA(negate(tp, sp, h->pres->N), "block_tri_apply: negate");                 // s_p = -t_p
     for (int k = 0; k < D; ++k) {
       tbt[k].x = tp;
       tbt[k].y = tu + h->off[k];
     }
-    std::vector<ExtraPart> ex;
-    for (int k = 0; k < D; ++k) ex.push_back({tu + h->off[k], ru + h->off[k], 1.0});
-    FDP_CUDA(enqueue_kron_tasks(tbt, 0.0, ex, K, st), "block_tri_apply: B^T");
-    FDP_CUDA(enqueue_vel(h, tu, su, T, st), "block_tri_apply: P_V");
-    FDP_CUDA(negate(tp, sp, h->pres->N), "block_tri_apply: negate");
+    FDP_CUDA(enqueue_kron_tasks(tbt, 0.0, {}, K, st), "block_tri_apply: B^T");        // B^T t_p
+    FDP_CUDA(enqueue_vel(h, tu, zu, T, st), "block_tri_apply: P_V");                 // P_V^{-1} B^T t_p
+    PartSum ps{};
+    ps.nparts = 1;
+    ps.parts[0] = zu;
+    ps.coef[0] = 1.0;
+    FDP_CUDA(launch_partsum(ps, su, 1.0, nv, st), "block_tri_apply: update");        // s_u = w_u - P_V^{-1} B^T s_p
     return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
   }
-  // P_C^{-1} = [[I, -P_V^{-1}B^T], [0, I]] diag(I, -P_Q^{-1}) [[I, 0], [-B, I]] diag(P_V^{-1}, I)
-  FDP_CUDA(enqueue_vel(h, ru, su, T, st), "block_tri_apply: P_V");                 // w_u
-  for (int k = 0; k < D; ++k) {
-    tb[k].x = su + h->off[k];
-    tb[k].y = zu;  // g_p = r_p - B w_u (zu reused as the pressure temporary g_p)
-    tb[k].alpha = -1.0;
-  }
-  FDP_CUDA(enqueue_kron_tasks(tb, 0.0, {{zu, rp, 1.0}}, K, st), "block_tri_apply: B");
-  FDP_CUDA(enqueue_mass(h->pres, FDP_MASS_INVERSE, zu, tp, h->pres->N, h->dq, 1, st, nullptr), "block_tri_apply: P_Q");
-  FDP_CUDA(negate(tp, sp, h->pres->N), "block_tri_apply: negate");                 // s_p = -t_p
-  for (int k = 0; k < D; ++k) {
-    tbt[k].x = tp;
-    tbt[k].y = tu + h->off[k];
-  }
-  FDP_CUDA(enqueue_kron_tasks(tbt, 0.0, {}, K, st), "block_tri_apply: B^T");        // B^T t_p
-  FDP_CUDA(enqueue_vel(h, tu, zu, T, st), "block_tri_apply: P_V");                 // P_V^{-1} B^T t_p
-  PartSum ps{};
-  ps.nparts = 1;
-  ps.parts[0] = zu;
-  ps.coef[0] = 1.0;
-  FDP_CUDA(launch_partsum(ps, su, 1.0, nv, st), "block_tri_apply: update");        // s_u = w_u - P_V^{-1} B^T s_p
-  return FDP_OK;
 }
 
 extern "C" fdp_status fdp_vec_lincomb_dev(const double* coef, const double* x, const double* y,
                                           const double* z, double* out, int64_t n, void* stream) {
-  if (n < 0) return fail(FDP_ERR_SHAPE, "fdp_vec_lincomb_dev: n < 0");
-  if (n == 0) return FDP_OK;
-  if (!is_device_ptr(coef) || !is_device_ptr(x) || !is_device_ptr(out) || (y && !is_device_ptr(y)) ||
-      (z && !is_device_ptr(z)))
-    return fail(FDP_ERR_INVALID_ARG, "fdp_vec_lincomb_dev: device pointers required");
-  FDP_CUDA(launch_lincomb_dev(coef, x, y, z, out, n, static_cast<cudaStream_t>(stream)), "fdp_vec_lincomb_dev");
-  return FDP_OK;
+  try {
+    if (n < 0) return fail(FDP_ERR_SHAPE, "fdp_vec_lincomb_dev: n < 0");
+    if (n == 0) return FDP_OK;
+    if (!is_device_ptr(coef) || !is_device_ptr(x) || !is_device_ptr(out) || (y && !is_device_ptr(y)) ||
+        (z && !is_device_ptr(z)))
+      return fail(FDP_ERR_INVALID_ARG, "fdp_vec_lincomb_dev: device pointers required");
+    FDP_CUDA(launch_lincomb_dev(coef, x, y, z, out, n, static_cast<cudaStream_t>(stream)), "fdp_vec_lincomb_dev");
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
 }
 
 extern "C" fdp_status fdp_minres_scalars(int phase, double* state, double* hist, int hist_cap,
                                          void* stream) {
-  if (phase < 0 || phase > 3 || hist_cap < 0) return fail(FDP_ERR_INVALID_ARG, "fdp_minres_scalars: bad phase");
-  if (!is_device_ptr(state) || (hist && !is_device_ptr(hist)))
-    return fail(FDP_ERR_INVALID_ARG, "fdp_minres_scalars: device pointers required");
-  FDP_CUDA(launch_minres_scalars(phase, state, hist, hist_cap, static_cast<cudaStream_t>(stream)),
-           "fdp_minres_scalars");
-  return FDP_OK;
+  try {
+    if (phase < 0 || phase > 3 || hist_cap < 0) return fail(FDP_ERR_INVALID_ARG, "fdp_minres_scalars: bad phase");
+    if (!is_device_ptr(state) || (hist && !is_device_ptr(hist)))
+      return fail(FDP_ERR_INVALID_ARG, "fdp_minres_scalars: device pointers required");
+    FDP_CUDA(launch_minres_scalars(phase, state, hist, hist_cap, static_cast<cudaStream_t>(stream)),
+             "fdp_minres_scalars");
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
 }
 
 extern "C" fdp_status fdp_vec_copy_indexed(const double* V, int64_t ldv, const int* idx, double* out,
                                            int64_t n, void* stream) {
-  if (n < 0 || ldv < n) return fail(FDP_ERR_SHAPE, "fdp_vec_copy_indexed: bad extents");
-  if (!is_device_ptr(V) || !is_device_ptr(idx) || !is_device_ptr(out))
-    return fail(FDP_ERR_INVALID_ARG, "fdp_vec_copy_indexed: device pointers required");
-  FDP_CUDA(launch_copy_indexed(V, ldv, idx, out, n, static_cast<cudaStream_t>(stream)), "fdp_vec_copy_indexed");
-  return FDP_OK;
+  try {
+    if (n < 0 || ldv < n) return fail(FDP_ERR_SHAPE, "fdp_vec_copy_indexed: bad extents");
+    if (!is_device_ptr(V) || !is_device_ptr(idx) || !is_device_ptr(out))
+      return fail(FDP_ERR_INVALID_ARG, "fdp_vec_copy_indexed: device pointers required");
+    FDP_CUDA(launch_copy_indexed(V, ldv, idx, out, n, static_cast<cudaStream_t>(stream)), "fdp_vec_copy_indexed");
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
 }
 
 extern "C" fdp_status fdp_vec_store_indexed(double* V, int64_t ldv, const int* idx, const double* w,
                                             const double* coef, int64_t n, void* stream) {
-  if (n < 0 || ldv < n) return fail(FDP_ERR_SHAPE, "fdp_vec_store_indexed: bad extents");
-  if (!is_device_ptr(V) || !is_device_ptr(idx) || !is_device_ptr(w) || !is_device_ptr(coef))
-    return fail(FDP_ERR_INVALID_ARG, "fdp_vec_store_indexed: device pointers required");
-  FDP_CUDA(launch_store_indexed(V, ldv, idx, w, coef, n, static_cast<cudaStream_t>(stream)), "fdp_vec_store_indexed");
-  return FDP_OK;
+  try {
+    if (n < 0 || ldv < n) return fail(FDP_ERR_SHAPE, "fdp_vec_store_indexed: bad extents");
+    if (!is_device_ptr(V) || !is_device_ptr(idx) || !is_device_ptr(w) || !is_device_ptr(coef))
+      return fail(FDP_ERR_INVALID_ARG, "fdp_vec_store_indexed: device pointers required");
+    FDP_CUDA(launch_store_indexed(V, ldv, idx, w, coef, n, static_cast<cudaStream_t>(stream)), "fdp_vec_store_indexed");
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
 }
 
 extern "C" fdp_status fdp_vec_multidot_dev(const double* V, int64_t ldv, const int* m, int m_max,
                                            const double* w, int64_t n, double* h, void* workspace,
                                            void* stream) {
-  if (m_max < 0 || n < 0 || (m_max > 0 && ldv < n)) return fail(FDP_ERR_SHAPE, "fdp_vec_multidot_dev: bad extents");
-  if (m_max == 0) return FDP_OK;
-  if (!is_device_ptr(V) || !is_device_ptr(m) || !is_device_ptr(w) || !is_device_ptr(h) || !is_device_ptr(workspace))
-    return fail(FDP_ERR_INVALID_ARG, "fdp_vec_multidot_dev: device pointers required");
-  FDP_CUDA(launch_multidot_dev(V, ldv, m, m_max, w, n, h, static_cast<double*>(workspace),
-                               static_cast<cudaStream_t>(stream)), "fdp_vec_multidot_dev");
-  return FDP_OK;
+  try {
+    if (m_max < 0 || n < 0 || (m_max > 0 && ldv < n)) return fail(FDP_ERR_SHAPE, "fdp_vec_multidot_dev: bad extents");
+    if (m_max == 0) return FDP_OK;
+    if (!is_device_ptr(V) || !is_device_ptr(m) || !is_device_ptr(w) || !is_device_ptr(h) || !is_device_ptr(workspace))
+      return fail(FDP_ERR_INVALID_ARG, "fdp_vec_multidot_dev: device pointers required");
+    FDP_CUDA(launch_multidot_dev(V, ldv, m, m_max, w, n, h, static_cast<double*>(workspace),
+                                 static_cast<cudaStream_t>(stream)), "fdp_vec_multidot_dev");
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
 }
 
 extern "C" fdp_status fdp_vec_gemv_dev(const double* V, int64_t ldv, const int* m, int m_max,
                                        const double* h, double alpha, double* w, double beta,
                                        int64_t n, void* stream) {
-  if (m_max < 0 || m_max > 6144 || n < 0 || ldv < n) return fail(FDP_ERR_SHAPE, "fdp_vec_gemv_dev: bad extents");
-  if (n == 0) return FDP_OK;
-  if (!is_device_ptr(V) || !is_device_ptr(m) || !is_device_ptr(h) || !is_device_ptr(w))
-    return fail(FDP_ERR_INVALID_ARG, "fdp_vec_gemv_dev: device pointers required");
-  FDP_CUDA(launch_gemv_dev(V, ldv, m, m_max, h, alpha, w, beta, n, static_cast<cudaStream_t>(stream)),
-           "fdp_vec_gemv_dev");
-  return FDP_OK;
+  try {
+    if (m_max < 0 || m_max > 6144 || n < 0 || ldv < n) return fail(FDP_ERR_SHAPE, "fdp_vec_gemv_dev: bad extents");
+    if (n == 0) return FDP_OK;
+    if (!is_device_ptr(V) || !is_device_ptr(m) || !is_device_ptr(h) || !is_device_ptr(w))
+      return fail(FDP_ERR_INVALID_ARG, "fdp_vec_gemv_dev: device pointers required");
+    FDP_CUDA(launch_gemv_dev(V, ldv, m, m_max, h, alpha, w, beta, n, static_cast<cudaStream_t>(stream)),
+             "fdp_vec_gemv_dev");
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
 }
 
 extern "C" fdp_status fdp_gmres_scalars(int phase, int* istate, double* dstate, double* H, int ldh,
                                         const double* h1, const double* h2, double* hist, int m_max,
                                         void* stream) {
-  if ((phase != 0 && phase != 1) || m_max < 1 || ldh < m_max + 1)
-    return fail(FDP_ERR_INVALID_ARG, "fdp_gmres_scalars: bad phase or extents");
-  if (!is_device_ptr(istate) || !is_device_ptr(dstate) || !is_device_ptr(H) || !is_device_ptr(h1) ||
-      !is_device_ptr(h2) || (hist && !is_device_ptr(hist)))
-    return fail(FDP_ERR_INVALID_ARG, "fdp_gmres_scalars: device pointers required");
-  FDP_CUDA(launch_gmres_scalars(phase, istate, dstate, H, ldh, h1, h2, hist, m_max,
-                                static_cast<cudaStream_t>(stream)), "fdp_gmres_scalars");
-  return FDP_OK;
+  try {
+    if ((phase != 0 && phase != 1) || m_max < 1 || ldh < m_max + 1)
+      return fail(FDP_ERR_INVALID_ARG, "fdp_gmres_scalars: bad phase or extents");
+    if (!is_device_ptr(istate) || !is_device_ptr(dstate) || !is_device_ptr(H) || !is_device_ptr(h1) ||
+        !is_device_ptr(h2) || (hist && !is_device_ptr(hist)))
+      return fail(FDP_ERR_INVALID_ARG, "fdp_gmres_scalars: device pointers required");
+    FDP_CUDA(launch_gmres_scalars(phase, istate, dstate, H, ldh, h1, h2, hist, m_max,
+                                  static_cast<cudaStream_t>(stream)), "fdp_gmres_scalars");
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
 }
 
 // ------------------------------------------------------------------------------------------------
 // Arnoldi helpers (GMRES orthogonalization, NEXT-2)
 // ------------------------------------------------------------------------------------------------
 extern "C" size_t fdp_vec_multidot_workspace_bytes(int m) {
-  return m > 0 ? multidot_scratch_elems(m) * sizeof(double) : 0;
+  try {
+    return m > 0 ? multidot_scratch_elems(m) * sizeof(double) : 0;
+  } catch (...) {
+    return 0;
+  }
 }
 
 extern "C" fdp_status fdp_vec_multidot(const double* V, int64_t ldv, int m, const double* w,
                                        int64_t n, double* h, void* workspace, void* stream) {
-  if (m < 0 || n < 0 || (m > 0 && ldv < n)) return fail(FDP_ERR_SHAPE, "fdp_vec_multidot: bad extents");
-  if (m == 0) return FDP_OK;
-  if (!is_device_ptr(V) || !is_device_ptr(w) || !is_device_ptr(h) || !is_device_ptr(workspace))
-    return fail(FDP_ERR_INVALID_ARG, "fdp_vec_multidot: device pointers required");
-  FDP_CUDA(launch_multidot(V, ldv, m, w, n, h, static_cast<double*>(workspace), static_cast<cudaStream_t>(stream)),
-           "fdp_vec_multidot");
-  return FDP_OK;
+  try {
+    if (m < 0 || n < 0 || (m > 0 && ldv < n)) return fail(FDP_ERR_SHAPE, "fdp_vec_multidot: bad extents");
+    if (m == 0) return FDP_OK;
+    if (!is_device_ptr(V) || !is_device_ptr(w) || !is_device_ptr(h) || !is_device_ptr(workspace))
+      return fail(FDP_ERR_INVALID_ARG, "fdp_vec_multidot: device pointers required");
+    FDP_CUDA(launch_multidot(V, ldv, m, w, n, h, static_cast<double*>(workspace), static_cast<cudaStream_t>(stream)),
+             "fdp_vec_multidot");
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
 }
 
 extern "C" fdp_status fdp_vec_gemv(const double* V, int64_t ldv, int m, const double* h, double alpha,
                                    double* w, double beta, int64_t n, void* stream) {
-  if (m < 0 || m > 6144 || n < 0 || (m > 0 && ldv < n)) return fail(FDP_ERR_SHAPE, "fdp_vec_gemv: bad extents (m <= 6144)");
-  if (n == 0) return FDP_OK;
-  if (!is_device_ptr(w) || (m > 0 && (!is_device_ptr(V) || !is_device_ptr(h))))
-    return fail(FDP_ERR_INVALID_ARG, "fdp_vec_gemv: device pointers required");
-  FDP_CUDA(launch_gemv(V, ldv, m, h, alpha, w, beta, n, static_cast<cudaStream_t>(stream)), "fdp_vec_gemv");
-  return FDP_OK;
+  try {
+    if (m < 0 || m > 6144 || n < 0 || (m > 0 && ldv < n)) return fail(FDP_ERR_SHAPE, "fdp_vec_gemv: bad extents (m <= 6144)");
+    if (n == 0) return FDP_OK;
+    if (!is_device_ptr(w) || (m > 0 && (!is_device_ptr(V) || !is_device_ptr(h))))
+      return fail(FDP_ERR_INVALID_ARG, "fdp_vec_gemv: device pointers required");
+    FDP_CUDA(launch_gemv(V, ldv, m, h, alpha, w, beta, n, static_cast<cudaStream_t>(stream)), "fdp_vec_gemv");
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
 }

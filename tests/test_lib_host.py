@@ -163,3 +163,21 @@ def test_separable_fit_rejects_nonpositive():
     c[1][3] = 0.0
     with pytest.raises(fdp.FdpError):
         fdp.iga_separable_fit(c, [2, 4])
+
+
+def test_header_is_plain_c99(tmp_path):
+    """include/fdp.h is a C99 header: it compiles as C with -pedantic, and a C
+    program can call the host-only entry points through it."""
+    src = tmp_path / "t.c"
+    src.write_text('#include "fdp.h"\n#include <stdio.h>\nint main(void) {\n'
+                   '  int32_t n = 0;\n  fdp_status s = iga_univariate(2, 1, 4, 0, 0.0, 0, NULL, NULL, &n);\n'
+                   '  printf("%d %d %s\\n", (int)s, (int)n, fdp_version());\n  return s != FDP_OK;\n}\n')
+    inc = os.path.join(ROOT, "include")
+    libdir = os.path.dirname(fdp.LIB_PATH)
+    exe = tmp_path / "t"
+    r = subprocess.run(["gcc", "-std=c99", "-pedantic", "-Wall", "-Werror", "-I", inc, str(src), "-o", str(exe),
+                        "-L", libdir, "-lfdp", f"-Wl,-rpath,{libdir}"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr
+    assert out.stdout.split()[1] == "6"   # m = n_el (p - alpha) + alpha + 1 = 4 + 1 + 1
