@@ -493,65 +493,6 @@ def kron_mass_apply_slab_peer(h, phase: int, nranks: int, rank: int, x_in, x_out
                                          _stream(stream)))
 
 
-def peer_barrier(flag_ptrs, counter, nranks: int, rank: int, stream=None):
-    """fdp_peer_barrier: flag_ptrs int64 cuda tensor of nranks flag-array addresses."""
-    _check(lib.fdp_peer_barrier(flag_ptrs.data_ptr(), counter.data_ptr(), nranks, rank, _stream(stream)))
-
-
-class PeerBuffer:
-    """A device buffer shareable over CUDA IPC (fdp_peer_alloc); .handle is 64 bytes."""
-
-    def __init__(self, nbytes: int, device: int = 0):
-        p = ctypes.c_void_p()
-        hbuf = ctypes.create_string_buffer(64)
-        _check(lib.fdp_peer_alloc(nbytes, device, ctypes.byref(p), hbuf))
-        self.ptr = p.value
-        self.handle = hbuf.raw
-        self.nbytes = nbytes
-        self.device = device
-
-    def tensor(self, n: int, dtype=None):
-        """Zero-copy float64 (or given dtype) cuda tensor view of the first n elements."""
-        import torch
-        dt = torch.float64 if dtype is None else dtype
-        return _tensor_from_ptr(self.ptr, n, dt, self.device)
-
-    def close(self):
-        if getattr(self, "ptr", None):
-            lib.fdp_peer_free(self.ptr)
-            self.ptr = None
-
-    def __del__(self):
-        try:
-            self.close()
-        except Exception:
-            pass
-
-
-def peer_open(handle: bytes, device: int = 0) -> int:
-    p = ctypes.c_void_p()
-    _check(lib.fdp_peer_open(ctypes.create_string_buffer(handle, 64), device, ctypes.byref(p)))
-    return p.value
-
-
-def peer_close(ptr: int):
-    _check(lib.fdp_peer_close(ptr))
-
-
-def _tensor_from_ptr(ptr: int, n: int, dtype, device: int):
-    """A torch cuda tensor aliasing n elements at a device address (no ownership)."""
-    import torch
-
-    class _CAI:
-        def __init__(self):
-            typestr = {torch.float64: "<f8", torch.int64: "<i8", torch.uint64: "<u8"}[dtype]
-            self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
-                                             "version": 3, "strides": None}
-
-    with torch.cuda.device(device):
-        return torch.as_tensor(_CAI(), device=f"cuda:{device}")
-
-
 class KronMass:
     """kron_mass_setup / kron_mass_apply: P_Q = M_D (x) .. (x) M_1 and its inverse."""
 

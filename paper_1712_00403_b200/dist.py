@@ -189,13 +189,12 @@ def emulate_slab_apply(block, r_full, G: int):
 # ------------------------------------------------------------------------------------------------
 # Peer-store exchange: the exchanges fused into the contraction epilogues
 # ------------------------------------------------------------------------------------------------
-def exchange_handles(local: list, group=None) -> list:
-    """All ranks' lists of 64-byte IPC handles, indexed [rank][i] (torch.distributed
-    all_gather_object: host-side plumbing only)."""
+def allgather_bytes(blob: bytes, group=None) -> list:
+    """Every rank's byte string, in rank order (torch.distributed all_gather_object: host-side
+    plumbing for the IPC handle blobs of the peer-store exchange)."""
     import torch.distributed as dist
-    G = dist.get_world_size(group)
-    out = [None] * G
-    dist.all_gather_object(out, [bytes(h) for h in local], group=group)
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, bytes(blob), group=group)
     return out
 
 
@@ -233,8 +232,7 @@ class PeerSlabBlockPrecond:
         c = ctypes.c_void_p()
         _check(lib.fdp_comm_create(block.h, G, g, ctypes.byref(c), blob))
         self.comm = c
-        blobs = [None] * G
-        dist.all_gather_object(blobs, blob.raw, group=group)
+        blobs = allgather_bytes(blob.raw, group)
         allb = ctypes.create_string_buffer(b"".join(blobs), nb * G)
         _check(lib.fdp_comm_connect(c, allb))
         wsb = int(lib.block_precond_sharded_workspace_bytes(block.h, c))

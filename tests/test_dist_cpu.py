@@ -154,13 +154,13 @@ def test_batch_shard_config4():
 
 
 def _handles(rank, world):
-    hs = [bytes([rank, i]) * 32 for i in range(3)]  # stand-ins for 64-byte IPC handles
-    allh = fdist.exchange_handles(hs)
-    return all(allh[r][i] == bytes([r, i]) * 32 for r in range(world) for i in range(3))
+    blob = bytes([rank, 7]) * 160  # stand-in for a rank's blob of 64-byte IPC handles
+    allb = fdist.allgather_bytes(blob)
+    return all(allb[r] == bytes([r, 7]) * 160 for r in range(world))
 
 
 def test_peer_handle_exchange_gloo():
-    """The host plumbing of the peer-store exchange: every rank gets every rank's handles in rank
-    order (world size 2, gloo)."""
+    """The host plumbing of the peer-store exchange (PeerSlabBlockPrecond): every rank gets every
+    rank's IPC handle blob, in rank order (world size 2, gloo)."""
     res = _run(_handles)
     assert res == {0: True, 1: True}
