@@ -1,0 +1,82 @@
+// C ABI: host-only spline helpers (univariate K/M, Greville points, generalized eigenproblem,
+// quadrature and mixed weighted matrices).
+#include "abi_impl.h"
+
+// ------------------------------------------------------------------------------------------------
+// host helpers
+// ------------------------------------------------------------------------------------------------
+extern "C" fdp_status iga_univariate(int deg, int alpha, int n_el, int flags, double c_pen, int q,
+                                     double* K, double* M, int32_t* n_out) {
+  try {
+    if (!n_out) return fail(FDP_ERR_INVALID_ARG, "iga_univariate: n_out is NULL");
+    std::string err;
+    int n = 0;
+    int st = iga_build(deg, alpha, n_el, flags, c_pen, q, K, M, &n, &err);
+    if (st) return fail((fdp_status)st, err);
+    *n_out = n;
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
+}
+
+extern "C" fdp_status iga_greville(int deg, int alpha, int n_el, int flags, double* g,
+                                   int32_t* n_out) {
+  try {
+    if (!n_out) return fail(FDP_ERR_INVALID_ARG, "iga_greville: n_out is NULL");
+    std::string err;
+    int n = 0;
+    int st = iga_greville_build(deg, alpha, n_el, flags, g, &n, &err);
+    if (st) return fail((fdp_status)st, err);
+    *n_out = n;
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
+}
+
+extern "C" fdp_status fdp_gen_eig(int n, const double* K, const double* M, double* U,
+                                  double* lambda) {
+  try {
+    if (n < 1) return fail(FDP_ERR_SHAPE, "fdp_gen_eig: n < 1");
+    if (!K || !M || !U || !lambda) return fail(FDP_ERR_INVALID_ARG, "fdp_gen_eig: NULL argument");
+    std::string err;
+    int st = gen_eig(n, K, M, U, lambda, &err);
+    if (st) return fail((fdp_status)st, "fdp_gen_eig: " + err);
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// host helpers: quadrature points and mixed univariate matrices
+// ------------------------------------------------------------------------------------------------
+extern "C" fdp_status iga_quadrature(int n_el, int q, double* x, double* w) {
+  try {
+    if (n_el < 1 || q < 1) return fail(FDP_ERR_SHAPE, "iga_quadrature: n_el, q >= 1");
+    iga_quadrature_build(n_el, q, x, w);
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
+}
+
+extern "C" fdp_status iga_mixed(int deg_test, int alpha_test, int flags_test, int deg_trial,
+                                int alpha_trial, int flags_trial, int n_el, int dtest, int dtrial,
+                                int q, const double* wq, double* out, int32_t* n_test,
+                                int32_t* n_trial) {
+  try {
+    if (!n_test || !n_trial) return fail(FDP_ERR_INVALID_ARG, "iga_mixed: NULL size outputs");
+    std::string err;
+    int a = 0, b = 0;
+    int st = iga_mixed_build(deg_test, alpha_test, flags_test, deg_trial, alpha_trial, flags_trial,
+                             n_el, dtest, dtrial, q, wq, out, &a, &b, &err);
+    if (st) return fail((fdp_status)st, err);
+    *n_test = a;
+    *n_trial = b;
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
+}

@@ -1,0 +1,264 @@
+// Internal header of the C ABI implementation (abi_*.cpp): shared helpers, error reporting,
+// handle structs and the launch orchestration entry points used across the ABI files.
+#pragma once
+#include <algorithm>
+#include <functional>
+#include <cmath>
+#include <cstdio>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "fdp_internal.h"
+
+
+// ------------------------------------------------------------------------------------------------
+// errors
+// ------------------------------------------------------------------------------------------------
+inline thread_local std::string g_last_error;
+
+inline fdp_status fail(fdp_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+// No C++ exception crosses the C ABI: every entry point catches and reports (mostly
+// std::bad_alloc from host-side containers). Called from inside a catch handler.
+inline fdp_status abi_exception(const char* fn) {
+  try {
+    throw;
+  } catch (const std::bad_alloc&) {
+    return fail(FDP_ERR_OOM, std::string(fn) + ": host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(FDP_ERR_INVALID_ARG, std::string(fn) + ": " + e.what());
+  } catch (...) {
+    return fail(FDP_ERR_INVALID_ARG, std::string(fn) + ": unexpected exception");
+  }
+}
+
+inline fdp_status cuda_fail(cudaError_t e, const char* where) {
+  cudaGetLastError();  // clear sticky-free errors
+  return fail(FDP_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define FDP_CUDA(call, where)                                  \
+  do {                                                         \
+    cudaError_t e_ = (call);                                   \
+    if (e_ != cudaSuccess) return cuda_fail(e_, where);        \
+  } while (0)
+
+// A pointer is acceptable as a device operand if the runtime knows it as device or managed memory.
+inline bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+inline int num_sms() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess &&
+      cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+    return n;
+  cudaGetLastError();
+  return 148;
+}
+
+struct DeviceGuard {  // select the handle's device for the duration of a call, then restore
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) { cudaGetLastError(); prev = -1; }
+    if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    int cur;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+template <class T>
+inline fdp_status dalloc(T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) return FDP_OK;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(FDP_ERR_OOM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  }
+  return FDP_OK;
+}
+
+inline bool symmetric(int n, const double* A) {
+  double mx = 0.0;
+  for (size_t i = 0; i < (size_t)n * n; ++i) mx = std::max(mx, std::fabs(A[i]));
+  for (int j = 0; j < n; ++j)
+    for (int i = j + 1; i < n; ++i)
+      if (std::fabs(A[i + (size_t)n * j] - A[j + (size_t)n * i]) > 1e-12 * mx) return false;
+  return true;
+}
+
+// ------------------------------------------------------------------------------------------------
+// per-launch profiling (events recorded on the launching stream, optionally into a graph)
+// ------------------------------------------------------------------------------------------------
+struct LaunchInfo {
+  int kind;      // 0 K1 mode contraction, 1 K2 scaling, 2 K3 mass
+  double flops;  // algorithmic
+  double bytes;  // algorithmic DRAM bytes
+};
+struct Recorder {
+  std::vector<cudaEvent_t>* ev = nullptr;
+  std::vector<LaunchInfo>* info = nullptr;
+  cudaStream_t s = nullptr;
+  cudaError_t before(int kind, double flops, double bytes) {
+    if (!ev) return cudaSuccess;
+    size_t i = info->size();
+    if (i >= ev->size()) return cudaErrorInvalidValue;
+    info->push_back({kind, flops, bytes});
+    return cudaEventRecordWithFlags((*ev)[i], s, cudaEventRecordExternal);
+  }
+  cudaError_t finish() {
+    if (!ev) return cudaSuccess;
+    size_t i = info->size();
+    if (i >= ev->size()) return cudaErrorInvalidValue;
+    return cudaEventRecordWithFlags((*ev)[i], s, cudaEventRecordExternal);
+  }
+};
+
+using namespace fdp;
+
+// ------------------------------------------------------------------------------------------------
+// handle structs
+// ------------------------------------------------------------------------------------------------
+struct fdp_fd_s {
+  int D = 0;
+  int n[3] = {1, 1, 1};
+  long long N = 0;
+  double coef[3] = {0, 0, 0};
+  int device = 0;
+  TileCfg cfg[3];
+  std::vector<double> U_host[3], lam_host[3];
+  std::vector<double> dK[3], dM[3];  // diagonals of the pencils (fd_operator_diagonal)
+  double* Wf[3] = {nullptr, nullptr, nullptr};  // forward  W[k][a] = U[k][a]
+  double* Wb[3] = {nullptr, nullptr, nullptr};  // backward W[k][a] = U[a][k]
+  double* lamc[3] = {nullptr, nullptr, nullptr};  // coef[d] * lambda_d
+  double* ws = nullptr;
+  int64_t ws_batch = 0;
+  int* sync = nullptr;        // plane-pipeline counters (zeroed, self-resetting)
+  long long sync_cap = 0;
+  int64_t sync_batch = 0;
+};
+
+// Intermediate tensors between passes use an even leading dimension n1p (16-byte aligned rows
+// and row pairs for vector memory operations); the C-ABI input/output stay unpadded.
+static int n1pad(const fdp_fd_s* h) { return h->n[0] + (h->n[0] & 1); }
+static long long Npad(const fdp_fd_s* h) { return h->N / h->n[0] * n1pad(h); }
+
+struct fdp_mass_s {
+  int D = 0;
+  int n[3] = {1, 1, 1};
+  int band[3] = {0, 0, 0};
+  long long N = 0;
+  int device = 0;
+  double* Lb[3] = {nullptr, nullptr, nullptr};
+  double* invd[3] = {nullptr, nullptr, nullptr};
+  double* Mb[3] = {nullptr, nullptr, nullptr};
+  std::vector<double> Lb_host[3];
+};
+
+struct fdp_block_s {
+  int D = 0;
+  int device = 0;
+  std::vector<const fdp_fd_s*> vel;
+  const fdp_mass_s* pres = nullptr;
+  std::vector<long long> off;  // offsets of u_1..u_D, p within one item; off[D+1] = size
+  long long size = 0;
+  long long nvel = 0;
+  double* dv = nullptr;        // D_V^{-1/2} (sum N_k) or NULL
+  double* dq = nullptr;        // D_Q^{-1/2} (n_Q) or NULL
+  double* dall = nullptr;      // [D_V^{-1/2} | D_Q^{-1/2}] (ones where absent), dense-P_Q path
+  // dense-inverse P_Q path: M_d^{-1} padded to the velocity tile config of mode d, so the
+  // pressure passes join the velocity launches of stages 0..D-1 (C-9)
+  bool pres_dense = false;
+  double* Wq[3] = {nullptr, nullptr, nullptr};
+  int q_tiles_n[3] = {0, 0, 0};
+  int q_ldw[3] = {0, 0, 0};
+  cudaStream_t cap = nullptr;  // private capture stream
+  // graph cache
+  std::mutex mu;
+  struct GraphEntry {
+    const double* r;
+    double* s;
+    void* ws;
+    int64_t batch;
+    cudaGraphExec_t exec;
+    unsigned long long used;
+  };
+  std::vector<GraphEntry> graphs;  // small LRU cache keyed by (r, s, workspace, batch)
+  unsigned long long tick = 0;
+  // plane-pipeline counters (zeroed at allocation, self-resetting)
+  int* sync = nullptr;
+  long long sync_cap = 0;
+  // profiling
+  bool prof = false;
+  std::vector<cudaEvent_t> ev;
+  std::vector<LaunchInfo> info;
+  // host e2e buffers
+  double* e2e_r = nullptr;
+  double* e2e_s = nullptr;
+  void* e2e_ws = nullptr;
+  int64_t e2e_batch = 0;
+  // host-buffer pipeline: copy-in / copy-out streams and per-unit events
+  cudaStream_t cin = nullptr, cout = nullptr;
+  cudaStream_t cs[3] = {nullptr, nullptr, nullptr};  // per-component compute streams (batch 1)
+  std::vector<cudaEvent_t> ev_in, ev_done;
+  cudaEvent_t ev_start = nullptr;
+  // batch-1 pipeline over pinned buffers, captured once per (r_host, s_host) and replayed
+  const double* e2e_gr = nullptr;
+  double* e2e_gs = nullptr;
+  cudaGraphExec_t e2e_graph = nullptr;
+};
+
+struct KronFactor {
+  int nin = 0, nout = 0;
+  TileCfg cfg{};
+  std::vector<double> diag;  // F[i][i] for i < min(nin, nout) (kron_op_diagonal)
+  double* W = nullptr;  // W[k][a] = F[a][k], kpad x ldw
+};
+
+struct fdp_kron_s {
+  int D = 0, nterms = 0, device = 0;
+  int nin[3] = {1, 1, 1}, nout[3] = {1, 1, 1};
+  std::vector<double> coef;
+  std::vector<KronFactor> f;  // nterms * D
+};
+
+// ------------------------------------------------------------------------------------------------
+// launch orchestration shared by the ABI files (abi_fd.cpp)
+// ------------------------------------------------------------------------------------------------
+using StageHook = std::function<void(int pass, bool fwd, int d, std::vector<ModeProb>&,
+                                     std::vector<TileCfg>&)>;
+cudaError_t launch_stage(std::vector<ModeProb>& probs_in, const std::vector<TileCfg>& cfgs_in,
+                         bool kmaj, cudaStream_t s, int* nlaunch, Recorder* rec);
+long long pp_sync_ints(const std::vector<const fdp_fd_s*>& hs, int64_t batch, int extra_n3);
+cudaError_t enqueue_fd(const std::vector<const fdp_fd_s*>& hs,
+                       const std::vector<const double*>& in, long long ibs,
+                       const std::vector<double*>& out, long long obs,
+                       const std::vector<double*>& T,
+                       const std::vector<const double*>& dscale, int64_t batch,
+                       cudaStream_t s, int* nlaunch, Recorder* rec = nullptr,
+                       const StageHook& hook = nullptr, int* sync = nullptr,
+                       long long sync_cap = 0);
+cudaError_t enqueue_mass(const fdp_mass_s* h, int mode, const double* in, double* out,
+                         long long bs, const double* dscale, int64_t batch, cudaStream_t s,
+                         int* nlaunch, Recorder* rec = nullptr);
+void kron_diag_accumulate(int D, const int* n, const std::vector<const double*>& f, double c,
+                          double* out);
+cudaError_t run1(ModeProb p, const TileCfg& c, bool kmaj, cudaStream_t s);
