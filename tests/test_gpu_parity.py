@@ -431,3 +431,20 @@ def test_config5_full_size_residual():
     xp, bp = x[o[3]:], b[o[3]:]
     Mx = okron.kron_matvec(list(reversed(od.Mq)), xp)
     assert np.linalg.norm(Mx - bp) / np.linalg.norm(bp) < 1e-12
+
+
+def test_empty_batches_are_noops():
+    """batch = 0 (empty input) is a successful no-op for every apply entry point."""
+    import ctypes
+    w, od, gd = _both(1)
+    P = fdp.build_block(gd)
+    x = torch.full((od.n_total,), 7.0, dtype=torch.float64, device="cuda")
+    ws = P.workspace(1)
+    lib = fdp.lib
+    assert lib.block_precond_apply(P.h, x.data_ptr(), x.data_ptr(), 0, ws.data_ptr(), None) == 0
+    f = P.fds[0]
+    assert lib.fd_apply(f.h, x.data_ptr(), x.data_ptr(), None, 0, ws.data_ptr(), None) == 0
+    assert lib.kron_mass_apply(P.mass.h, 0, x.data_ptr(), x.data_ptr(), None, 0, None) == 0
+    assert lib.block_precond_apply_host(P.h, ctypes.c_void_p(1), ctypes.c_void_p(1), 0, None) == 0
+    torch.cuda.synchronize()
+    assert torch.all(x == 7.0)

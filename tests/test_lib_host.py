@@ -181,3 +181,33 @@ def test_header_is_plain_c99(tmp_path):
     out = subprocess.run([str(exe)], capture_output=True, text=True)
     assert out.returncode == 0, out.stderr
     assert out.stdout.split()[1] == "6"   # m = n_el (p - alpha) + alpha + 1 = 4 + 1 + 1
+
+
+def test_setup_validation_paths_without_gpu():
+    """Argument checks that run before any device work: extents above the 2048 limit, non-positive
+    coefficients, non-symmetric pencils, block / Kronecker / communicator misuse, slab ranks."""
+    h = ctypes.c_void_p()
+    K = np.eye(3)
+    Kp = (ctypes.c_void_p * 3)(*[K.ctypes.data] * 3)
+    c = (ctypes.c_double * 3)(1, 1, 1)
+    big = (ctypes.c_int32 * 3)(2049, 3, 3)
+    assert fdp.lib.fd_setup(3, big, Kp, Kp, c, 0, 0, ctypes.byref(h)) == 2           # SHAPE
+    n3 = (ctypes.c_int32 * 3)(3, 3, 3)
+    c0 = (ctypes.c_double * 3)(1, 0, 1)
+    assert fdp.lib.fd_setup(3, n3, Kp, Kp, c0, 0, 0, ctypes.byref(h)) == 1           # coef <= 0
+    A = np.array([[2.0, 1.0, 0.0], [0.0, 2.0, 0.0], [0.0, 0.0, 2.0]], order="F")
+    Ap = (ctypes.c_void_p * 3)(*[A.ctypes.data] * 3)
+    assert fdp.lib.fd_setup(3, n3, Ap, Kp, c, 0, 0, ctypes.byref(h)) == 3            # NOT_SPD (asym.)
+    assert fdp.lib.fd_setup(3, n3, Kp, Kp, c, 0, -1, ctypes.byref(h)) == 2           # max_batch < 0
+    assert fdp.lib.block_precond_setup(3, None, None, None, None, ctypes.byref(h)) == 1
+    assert fdp.lib.block_precond_setup(4, None, None, None, None, ctypes.byref(h)) == 8
+    assert fdp.lib.kron_op_setup(2, 0, n3, n3, Kp, c, 0, ctypes.byref(h)) == 1        # no terms
+    assert fdp.lib.kron_op_setup(2, 1, big, n3, Kp, c, 0, ctypes.byref(h)) == 2       # extent
+    assert fdp.lib.fdp_comm_create(None, 2, 0, ctypes.byref(h), ctypes.create_string_buffer(8)) == 1
+    lo, ln = ctypes.c_int64(), ctypes.c_int64()
+    assert fdp.lib.fdp_slab_range(10, 3, 3, ctypes.byref(lo), ctypes.byref(ln)) == 1  # rank >= G
+    assert fdp.lib.fdp_slab_range(10, 3, 2, ctypes.byref(lo), ctypes.byref(ln)) == 0
+    assert (lo.value, ln.value) == (7, 3)
+    assert fdp.lib.fd_destroy(None) == 0 and fdp.lib.block_precond_destroy(None) == 0
+    assert fdp.lib.fdp_comm_destroy(None) == 0 and fdp.lib.kron_op_destroy(None) == 0
+    assert fdp.lib.fdp_last_error()  # a message was recorded
