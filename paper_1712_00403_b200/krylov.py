@@ -257,15 +257,18 @@ def minres_device(apply_A, apply_P, b, tol: float = 1e-8, maxit: int = 20000, un
     if hist.numel() < maxit + 1:
         hist = ent["hist"] = torch.zeros(maxit + 1, dtype=torch.float64, device=dev)
         ent["graph"] = None
-    for t in (x, w, w1, w2):
-        t.zero_()
-    r1.copy_(b)
-    r2.copy_(b)
-    apply_P(r1, y)
-    state.zero_()
-    state[13] = tol
-    vec_dot(r1, y, state[9:10])
-    minres_scalars(0, state)
+    def init():
+        for t in (x, w, w1, w2):
+            t.zero_()
+        r1.copy_(b)
+        r2.copy_(b)
+        apply_P(r1, y)
+        state.zero_()
+        state[13] = tol
+        vec_dot(r1, y, state[9:10])
+        minres_scalars(0, state)
+
+    init()
     kv, ky1, ky2, kw, kx = (state[16:19], state[19:22], state[22:25], state[25:28], state[28:31])
 
     def iterations():
@@ -291,16 +294,13 @@ def minres_device(apply_A, apply_P, b, tol: float = 1e-8, maxit: int = 20000, un
         s = torch.cuda.Stream(device=dev)
         s.wait_stream(torch.cuda.current_stream())
         g = torch.cuda.CUDAGraph()
-        # warm-up outside capture would advance the recurrence: snapshot and restore the state
-        snap = [t.clone() for t in (x, r1, r2, y, v, w, w1, w2, state)]
-        with torch.cuda.stream(s):
+        with torch.cuda.stream(s):  # warm-up (advances the recurrence: re-initialised below)
             iterations()
         torch.cuda.current_stream().wait_stream(s)
-        for t, c in zip((x, r1, r2, y, v, w, w1, w2, state), snap):
-            t.copy_(c)
         with torch.cuda.graph(g):
             iterations()
         ent["graph"] = g
+        init()
     g = ent["graph"]
     while True:
         g.replay()
@@ -452,27 +452,27 @@ def gmres_device(apply_A, apply_P, b, tol: float = 1e-8, maxit: int = 500, unrol
             scalars(1)
             store()
 
-    vin.copy_(b)
-    apply_P(vin, w)
-    ds.zero_()
-    ds[1] = tol
-    vec_dot(w, w, ds[4:5])
-    scalars(0)
-    store()
+    def init():
+        vin.copy_(b)
+        apply_P(vin, w)
+        ds.zero_()
+        ds[1] = tol
+        vec_dot(w, w, ds[4:5])
+        scalars(0)
+        store()
+
+    init()
     if ent["graph"] is None:
-        # warm-up outside capture would advance the iteration: snapshot and restore
-        snap = [x.clone() for x in (V[0], is_, ds, H, hist)]
         side = torch.cuda.Stream(device=dev)
         side.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(side):
+        with torch.cuda.stream(side):  # warm-up (advances the iteration: re-initialised below)
             steps()
         torch.cuda.current_stream().wait_stream(side)
-        for x, c in zip((V[0], is_, ds, H, hist), snap):
-            x.copy_(c)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             steps()
         ent["graph"] = g
+        init()
     g = ent["graph"]
     while True:
         g.replay()

@@ -54,7 +54,9 @@ for cid in cids:
     b.record()
     torch.cuda.synchronize()
     pc = a.elapsed_time(b) / 10
-    # device-resident recurrence (6 iterations per graph replay)
+    # device-resident recurrence (6 iterations per graph replay); free the host-driven buffers
+    krylov._BUFFERS.clear()
+    torch.cuda.empty_cache()
     ap = lambda r, z: P.apply(r, z, workspace=ws)
     krylov.minres_device(gop._apply_direct, ap, fd_)
     torch.cuda.synchronize()
