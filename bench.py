@@ -71,6 +71,35 @@ def workload_config(cid, w, n_total, batch_total, gpus, flush):
     }
 
 
+def nvml_sampler(stop, out, dev):
+    """Fast NVML polling (~1 kHz) so that even a millisecond-scale timed region gets samples;
+    each sample is (host time, SM MHz, max SM MHz, reason flags as 'Active' / 'Not Active')."""
+    import pynvml
+    pynvml.nvmlInit()
+    try:
+        h = pynvml.nvmlDeviceGetHandleByIndex(dev)
+        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        bits = [getattr(pynvml, "nvmlClocksThrottleReasonHwSlowdown", 0x8),
+                getattr(pynvml, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40),
+                getattr(pynvml, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20),
+                getattr(pynvml, "nvmlClocksThrottleReasonSwPowerCap", 0x4)]
+        while not stop.is_set():
+            sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+            rs = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+            flags = ["Active" if rs & b else "Not Active" for b in bits]
+            out.append((time.perf_counter(), [str(sm), str(mx), str(rs)] + flags))
+            stop.wait(0.001)
+    finally:
+        pynvml.nvmlShutdown()
+
+
+def clock_sampler(stop, out, dev):
+    try:
+        nvml_sampler(stop, out, dev)
+    except Exception:
+        nvsmi_sampler(stop, out, dev)
+
+
 def nvsmi_sampler(stop, out, dev):
     q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -81,13 +110,19 @@ def nvsmi_sampler(stop, out, dev):
                                 "--format=csv,noheader,nounits"], capture_output=True, text=True,
                                timeout=5)
             if r.returncode == 0 and r.stdout.strip():
-                out.append([x.strip() for x in r.stdout.strip().split(",")])
+                out.append((time.perf_counter(), [x.strip() for x in r.stdout.strip().split(",")]))
         except Exception:
             pass
         stop.wait(0.2)
 
 
-def summarize_clocks(samples):
+def summarize_clocks(samples, t0=None, t1=None):
+    """Median SM clock and the throttle reasons seen, from the samples taken inside the timed
+    region [t0, t1] (host clock); the nearest samples around it if none fell inside."""
+    inside = [s for t, s in samples if t0 is None or t0 <= t <= t1]
+    if not inside and samples:
+        inside = [min(samples, key=lambda ts: abs(ts[0] - (t0 or 0.0)))[1]]
+    samples = inside
     if not samples:
         return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
     sm = [float(s[0]) for s in samples if s[0].replace(".", "").isdigit()]
@@ -305,7 +340,7 @@ def main():
     # ---- timed region (device events per step; L2 flushed between steps when resident) ----
     stop = threading.Event()
     samples = []
-    th = threading.Thread(target=nvsmi_sampler, args=(stop, samples, dev), daemon=True)
+    th = threading.Thread(target=clock_sampler, args=(stop, samples, dev), daemon=True)
     th.start()
     time.sleep(0.3)
     if world > 1:
@@ -423,7 +458,7 @@ def main():
         launches = 3 * 7 + 5
         roof_kind = "K1 flops / step time per rank (includes exchanges; lower bound)"
     
-    clocks = summarize_clocks(samples)
+    clocks = summarize_clocks(samples, wall0, wall0 + wall)
     cpu = None
     if not args.no_cpu_baseline:
         os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
