@@ -37,6 +37,8 @@ def _rand_spd(n, rng, shift):
     ((150, 67), (2.0, 1.0), 4),             # 2D, two column tiles in mode 1
     ((1, 7, 3), (1.0, 1.0, 1.0), 2),        # degenerate extent 1
     ((96, 96, 2), (0.5, 1.5, 3.0), 1),
+    ((2048, 3, 2), (1.0, 2.0, 1.0), 1),     # largest extent fd_setup accepts (22 column tiles)
+    ((2, 2048), (1.0, 3.0), 2),
 ])
 def test_fd_apply_random_pencils(dims, coef, batch):
     rng = np.random.default_rng(sum(dims) + batch)
