@@ -378,6 +378,13 @@ fdp_status fdp_vec_gemv(const double* V, int64_t ldv, int m, const double* h, do
  * or NULL for wt = 1. flags as iga_univariate (FDP_IGA_INTERIOR per space). out: host,
  * column-major n_test x n_trial. */
 fdp_status iga_quadrature(int n_el, int q, double* x, double* w);
+/* Diagonal-of-mass factor: out[i + n*g] = w_g b_i(x_g)^2 at the n_el*q element Gauss points of
+ * iga_quadrature (column-major n x (n_el q), host), so that for a weight f sampled at the points
+ * int f b_i^2 = sum_g out[i, g] f(x_g); tensor products of these factors give diagonals of
+ * weighted multivariate mass matrices (the D_Q = diag(Q) / diag(P_Q) scaling of P:1039 with
+ * Q = int nu^{-1} rho_i rho_j). out NULL: only *n_out. flags: FDP_IGA_INTERIOR. */
+fdp_status iga_mass_diag_factor(int deg, int alpha, int n_el, int flags, int q, double* out,
+                                int32_t* n_out);
 fdp_status iga_mixed(int deg_test, int alpha_test, int flags_test, int deg_trial, int alpha_trial,
                      int flags_trial, int n_el, int dtest, int dtrial, int q, const double* wq,
                      double* out, int32_t* n_test, int32_t* n_trial);

@@ -169,3 +169,41 @@ def config3_nu_terms(D: int = 3):
     """nu(x) = 1 + 0.5 prod_d sin(2 pi x_d) (synth.viscosity) as two separable terms."""
     s = lambda x: np.sin(2 * np.pi * x)
     return [(1.0, None), (0.5, [s] * D)]
+
+
+def _kron_diag(diags):
+    """diag(F_D (x) .. (x) F_1) from per-direction diagonals [d_1, .., d_D], vec order (i1 fastest)."""
+    out = np.ones(1)
+    for dg in diags:
+        out = np.kron(dg, out)
+    return out
+
+
+def nu_scalings_paper(disc, op: StokesCube, nu, q: int):
+    """Config 3 under the paper's definition of the P^G scalings (SURVEY.md C-6, second row;
+    PAPER.md §6): [D_V]_ii = [A_kk]_ii / [P_V,k]_ii with A_kk the nu-weighted
+    velocity block of ``op`` (built with the separable nu terms), and [D_Q]_ii = [Q]_ii / [P_Q]_ii
+    with Q = int nu^{-1} rho_i rho_j (identity map). diag(A_kk) is the Kronecker product
+    of the factors' diagonals summed over the terms; diag(Q) is the q-point element Gauss rule in
+    every direction applied to nu^{-1} rho_i^2 on the tensor grid (nu^{-1} is not separable), as
+    three tensor contractions; nu is the callable nu(x, y, z) (C-6b)."""
+    D = disc.D
+    dv = []
+    for k, c in enumerate(disc.comps):
+        dA = np.zeros(c.size)
+        for cf, F in op.diag[k]:
+            dA += cf * _kron_diag([np.asarray(f.diagonal()).ravel() for f in F])
+        dP = np.zeros(c.size)
+        for d in range(D):
+            dP += c.coef[d] * _kron_diag([np.diag(c.Ks[e]) if e == d else np.diag(c.Ms[e]) for e in range(D)])
+        dv.append(dA / dP)
+    xi = splines.open_uniform_knots(disc.p, disc.p - 1, disc.n_el)
+    x, w = splines.element_quadrature(np.linspace(0, 1, disc.n_el + 1), q)
+    E = w[:, None] * splines.basis(xi, disc.p, x) ** 2        # (points, n_q): w_g b_i(x_g)^2
+    G = np.meshgrid(*([x] * D), indexing="ij")
+    T = 1.0 / nu(*G)                                            # nu^{-1} on the grid, [g1, .., gD]
+    for d in range(D):                                          # contract g_d against E
+        T = np.moveaxis(np.tensordot(E, T, axes=([0], [d])), 0, d)
+    dQ = np.reshape(T, -1, order="F")
+    dPq = _kron_diag([np.diag(M) for M in disc.Mq])
+    return np.concatenate(dv), dQ / dPq

@@ -80,3 +80,18 @@ extern "C" fdp_status iga_mixed(int deg_test, int alpha_test, int flags_test, in
     return abi_exception(__func__);
   }
 }
+
+extern "C" fdp_status iga_mass_diag_factor(int deg, int alpha, int n_el, int flags, int q, double* out,
+                                           int32_t* n_out) {
+  try {
+    if (!n_out) return fail(FDP_ERR_INVALID_ARG, "iga_mass_diag_factor: n_out is NULL");
+    std::string err;
+    int n = 0;
+    const int st = iga_mass_diag_factor_build(deg, alpha, n_el, flags, q, out, &n, &err);
+    if (st) return fail((fdp_status)st, "iga_mass_diag_factor: " + err);
+    *n_out = n;
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
+}

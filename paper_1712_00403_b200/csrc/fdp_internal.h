@@ -210,6 +210,8 @@ cudaError_t launch_lincomb(double a, const double* x, double b, const double* y,
 int iga_mixed_build(int deg_t, int alpha_t, int flags_t, int deg_r, int alpha_r, int flags_r,
                     int n_el, int dtest, int dtrial, int q, const double* wq, double* out,
                     int* n_test, int* n_trial, std::string* err);
+int iga_mass_diag_factor_build(int deg, int alpha, int n_el, int flags, int q, double* out,
+                               int* n_out, std::string* err);
 int iga_quadrature_build(int n_el, int q, double* x, double* w);
 
 // Slab pack (dir 0: z-slab -> piece buffer) / unpack (dir 1, optional scale on the z-slab).

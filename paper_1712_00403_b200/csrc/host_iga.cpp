@@ -201,6 +201,43 @@ int iga_quadrature_build(int n_el, int q, double* x, double* w) {
 
 // out[i, j] = int wt b_test_i^(dtest) b_trial_j^(dtrial) over the uniform mesh (both spaces live
 // on the same n_el elements; each element has exactly one non-empty span in each knot vector).
+int iga_mass_diag_factor_build(int deg, int alpha, int n_el, int flags, int q, double* out,
+                               int* n_out, std::string* err) {
+  int n = 0;
+  int st = iga_build(deg, alpha, n_el, flags & FDP_IGA_INTERIOR, 0.0, 0, nullptr, nullptr, &n, err);
+  if (st) return st;
+  *n_out = n;
+  if (!out) return FDP_OK;
+  if (q < 1) {
+    if (err) *err = "q must be >= 1";
+    return FDP_ERR_SHAPE;
+  }
+  const std::vector<double> xi = knot_vector(deg, alpha, n_el);
+  const int m = (int)xi.size() - deg - 1;
+  const int off = (flags & FDP_IGA_INTERIOR) ? 1 : 0;
+  std::vector<double> gx, gw;
+  gauss_rule(q, &gx, &gw);
+  std::vector<double> N(deg + 1), dN(deg + 1);
+  const long long npts = (long long)n_el * q;
+  for (long long i = 0; i < (long long)n * npts; ++i) out[i] = 0.0;
+  for (int e = 0; e < n_el; ++e) {
+    const double a = (double)e / n_el, b = (double)(e + 1) / n_el;
+    const double mid = 0.5 * (a + b);
+    const int s = find_span(xi, deg, m, mid);
+    for (int g = 0; g < q; ++g) {
+      const double u = mid + 0.5 * (b - a) * gx[g];
+      const double wt = 0.5 * (b - a) * gw[g];
+      span_basis(xi, deg, s, u, N.data(), dN.data());
+      for (int r = 0; r <= deg; ++r) {
+        const int i = s - deg + r - off;  // basis index within the (restricted) space
+        if (i < 0 || i >= n) continue;
+        out[i + (size_t)n * (e * q + g)] = wt * N[r] * N[r];
+      }
+    }
+  }
+  return FDP_OK;
+}
+
 int iga_mixed_build(int deg_t, int alpha_t, int flags_t, int deg_r, int alpha_r, int flags_r,
                     int n_el, int dtest, int dtrial, int q, const double* wq, double* out,
                     int* n_test, int* n_trial, std::string* err) {

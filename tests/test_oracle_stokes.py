@@ -140,3 +140,45 @@ def test_minres_finite_termination_spd():
     x, its, _ = minres.minres(lambda v: A @ v, b, lambda r: r, tol=1e-13)
     assert its <= 12
     assert np.allclose(A @ x, b, atol=1e-10)
+
+
+def test_paper_scalings_constant_viscosity_closed_form():
+    """nu == c (constant): A_kk = c P_V,k and Q = P_Q / c, so D_V == c and D_Q == 1/c."""
+    d = spaces.build(3, "RT", 2, 3)
+    c = 1.7
+    op = stokes.StokesCube(3, "RT", 2, 3, nu_terms=[(c, None)])
+    dv, dq = stokes.nu_scalings_paper(d, op, lambda x, y, z: c + 0.0 * x, q=6)
+    assert np.max(np.abs(dv - c)) < 1e-12 * c
+    assert np.max(np.abs(dq - 1.0 / c)) < 1e-12
+
+
+def test_paper_pressure_diagonal_brute_force():
+    """diag(Q), Q = int nu^{-1} rho_i rho_j, by three tensor contractions = the diagonal of the
+    densely assembled 3D quadrature (tiny grid, config 3's viscosity)."""
+    import synth
+    p, n_el, q = 2, 2, 6
+    d = spaces.build(3, "RT", p, n_el)
+    op = stokes.StokesCube(3, "RT", p, n_el)
+    _, dq = stokes.nu_scalings_paper(d, op, synth.viscosity, q)
+    spQ = [asm._space(p, p - 1, n_el, False)] * 3
+    X, W = asm._grid([n_el] * 3, q)
+    BQ, _, _ = asm._trivariate(spQ, X)
+    wn = W / synth.viscosity(X[:, 0], X[:, 1], X[:, 2])
+    diagQ = np.einsum("q,qi->i", wn, BQ ** 2)
+    PQ = np.kron(d.Mq[2], np.kron(d.Mq[1], d.Mq[0]))
+    assert np.max(np.abs(dq * np.diag(PQ) - diagQ)) < 1e-13 * np.max(diagQ)
+
+
+def test_paper_velocity_scaling_is_operator_diagonal_ratio():
+    """D_V diag(P_V,k) = diag(A_kk) of the densely applied nu-weighted operator (tiny RT grid)."""
+    p, n_el = 1, 2
+    d = spaces.build(3, "RT", p, n_el)
+    op = stokes.StokesCube(3, "RT", p, n_el, nu_terms=stokes.config3_nu_terms(3))
+    import synth
+    dv, _ = stokes.nu_scalings_paper(d, op, synth.viscosity, q=6)
+    A = _dense(op)
+    o = op.off_idx
+    for k, c in enumerate(d.comps):
+        R = fd.assemble_R(c.Ks, c.Ms, c.coef)
+        blk = np.diag(A[o[k]:o[k + 1], o[k]:o[k + 1]])
+        assert np.max(np.abs(dv[o[k]:o[k + 1]] * np.diag(R) - blk)) < 1e-12 * np.max(np.abs(blk))
