@@ -78,6 +78,7 @@ def _load():
         "iga_separable_fit": (i32, [i32, vp, ctypes.POINTER(vp), i32, ctypes.c_double, vp, vp, vp]),
         "fd_operator_diagonal": (i32, [vp, vp]),
         "kron_op_diagonal": (i32, [vp, vp]),
+        "iga_mass_diag_factor": (i32, [i32, i32, i32, i32, i32, vp, ctypes.POINTER(ctypes.c_int32)]),
         "fdp_vec_lincomb_dev": (i32, [vp, vp, vp, vp, vp, i64, vp]),
         "fdp_minres_scalars": (i32, [i32, vp, vp, i32, vp]),
         "fdp_vec_copy_indexed": (i32, [vp, i64, vp, vp, i64, vp]),
@@ -268,6 +269,17 @@ def iga_quadrature(n_el: int, q: int):
     w = np.zeros(n_el * q)
     _check(lib.iga_quadrature(n_el, q, _ptr(x), _ptr(w)))
     return x, w
+
+
+def iga_mass_diag_factor(space, n_el: int, q: int):
+    """(n x n_el q) host matrix of w_g b_i(x_g)^2 at libfdp's element Gauss points;
+    space = (deg, alpha, flags)."""
+    deg, alpha, flags = space
+    n = ctypes.c_int32(0)
+    _check(lib.iga_mass_diag_factor(deg, alpha, n_el, flags, q, None, ctypes.byref(n)))
+    out = np.zeros((n.value, n_el * q), order="F")
+    _check(lib.iga_mass_diag_factor(deg, alpha, n_el, flags, q, _ptr(out), ctypes.byref(n)))
+    return out
 
 
 def iga_mixed(test, trial, n_el: int, dtest: int = 0, dtrial: int = 0, q: int = 0, wq=None):

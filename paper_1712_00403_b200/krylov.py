@@ -26,9 +26,9 @@ import math
 
 import numpy as np
 
-from . import (FDP_IGA_INTERIOR, FDP_IGA_NITSCHE, KronOp, iga_mixed, iga_quadrature,
-               iga_univariate, minres_scalars, vec_dot, vec_gemv, vec_lincomb, vec_lincomb_dev,
-               vec_multidot)
+from . import (FDP_IGA_INTERIOR, FDP_IGA_NITSCHE, KronOp, iga_mass_diag_factor, iga_mixed,
+               iga_quadrature, iga_univariate, minres_scalars, vec_dot, vec_gemv, vec_lincomb,
+               vec_lincomb_dev, vec_multidot)
 
 
 def _spaces(D, disc, p):
@@ -223,6 +223,32 @@ def minres(apply_A, apply_P, b, tol: float = 1e-8, maxit: int = 20000):
         if phibar / beta1 <= tol:
             return x.clone(), itn, hist
     return x.clone(), maxit, hist
+
+
+def nu_scalings_paper(gd, op: "StokesOperator", nu, q: int, device: int = 0):
+    """Config 3's P^G scalings under the paper's definition (§6, DESIGN.md
+    C-6b): D_V = diag(A_kk) / diag(P_V,k) with A_kk the nu-weighted velocity block of ``op``
+    (kron_op_diagonal) and P_V,k the plain pencils; D_Q = diag(Q) / diag(P_Q) with
+    Q = int nu^{-1} rho_i rho_j: libfdp's diagonal-of-mass factors contracted with
+    nu^{-1} sampled on the q-point element Gauss grid by a KronOp on the GPU. Returns host arrays
+    (D_V over all components, D_Q)."""
+    import torch
+    D = gd.D
+    dv = []
+    for k in range(D):
+        dA = op.diag[k].diagonal()
+        terms = [[gd.Ks[k][e] if e == d else gd.Ms[k][e] for e in range(D)] for d in range(D)]
+        dP = KronOp(terms, gd.coef[k], device).diagonal()
+        dv.append(dA / dP)
+    F = iga_mass_diag_factor((gd.p, gd.p - 1, 0), gd.n_el, q)        # (n_q, points)
+    xq, _ = iga_quadrature(gd.n_el, q)
+    G = np.meshgrid(*([xq] * D), indexing="ij")
+    w = torch.from_numpy(np.reshape(1.0 / nu(*G), -1, order="F")).to(f"cuda:{device}")
+    Kq = KronOp([[F] * D], [1.0], device)
+    dQ = torch.empty(int(np.prod(Kq.nout)), dtype=torch.float64, device=w.device)
+    Kq.apply(w, dQ)
+    dPq = KronOp([list(gd.Mq)], [1.0], device).diagonal()
+    return np.concatenate(dv), dQ.cpu().numpy() / dPq
 
 
 _DEV_MINRES = {}

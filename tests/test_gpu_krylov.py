@@ -156,3 +156,29 @@ def test_gpu_minres_device_resident(cid):
         assert rel(x_g.cpu().numpy(), x_o) < 1e-6
     x_h, it_h, _ = krylov.minres(gop.apply, ap, dev(f))
     assert it_h == it_g and rel(x_g.cpu().numpy(), x_h.cpu().numpy()) < 1e-10
+
+
+def test_config3_paper_scalings_and_minres():
+    """Config 3 with the paper's definition of the P^G scalings (C-6b): D_V, D_Q from
+    libfdp vs the oracle, the resulting P_D^G apply, and identical MINRES counts."""
+    w = synth.CONFIGS[3]
+    q = w.p + 7
+    nu_o = ostokes.config3_nu_terms(w.dim)
+    op = ostokes.StokesCube(w.dim, w.disc, w.p, w.n_el, nu_terms=nu_o)
+    od = ospaces.build(w.dim, w.disc, w.p, w.n_el)
+    dv_o, dq_o = ostokes.nu_scalings_paper(od, op, synth.viscosity, q)
+    gop = krylov.StokesOperator(w.dim, w.disc, w.p, w.n_el, nu_terms=synth.viscosity_separable(w.dim))
+    gd = fdp.discretization(w.dim, w.disc, w.p, w.n_el)
+    dv_g, dq_g = krylov.nu_scalings_paper(gd, gop, synth.viscosity, q)
+    assert rel(dv_g, dv_o) < 1e-12 and rel(dq_g, dq_o) < 1e-12
+    P = fdp.build_block(gd, dscale_vel=dv_g, dscale_pres=dq_g)
+    oP = oprec.BlockPrecond(od, dv_o, dq_o)
+    r = synth.rhs(w.seed, op.n, 1)[0]
+    assert rel(P.apply(dev(r)).cpu().numpy(), oP.apply(r)) < 1e-9
+    f = ostokes.project_rhs(r, op.sizes[-1])
+    _, it_o, _ = ominres.minres(op.matvec, f, oP.apply)
+    ws = P.workspace(1)
+    _, it_g, _ = krylov.minres(gop.apply, lambda a, z: P.apply(a, z, workspace=ws), dev(f))
+    assert it_g == it_o, (it_g, it_o)
+    with open("gpurun_out/minres_counts.jsonl" if __import__("os").path.isdir("gpurun_out") else "/dev/null", "a") as fh:
+        fh.write('{"config": 3, "scalings": "paper (diag ratios)", "iterations": %d}\n' % it_g)

@@ -211,3 +211,17 @@ def test_setup_validation_paths_without_gpu():
     assert fdp.lib.fd_destroy(None) == 0 and fdp.lib.block_precond_destroy(None) == 0
     assert fdp.lib.fdp_comm_destroy(None) == 0 and fdp.lib.kron_op_destroy(None) == 0
     assert fdp.lib.fdp_last_error()  # a message was recorded
+
+
+def test_mass_diag_factor_matches_oracle():
+    """iga_mass_diag_factor: w_g b_i(x_g)^2 at the element Gauss points; its row sums are the
+    diagonal of the unweighted mass matrix."""
+    from oracle import splines
+    for deg, alpha, n_el, q in [(2, 1, 4, 3), (4, 3, 6, 7), (3, 1, 5, 5)]:
+        F = fdp.iga_mass_diag_factor((deg, alpha, 0), n_el, q)
+        xi = splines.open_uniform_knots(deg, alpha, n_el)
+        x, w = splines.element_quadrature(np.linspace(0, 1, n_el + 1), q)
+        ref = (w[:, None] * splines.basis(xi, deg, x) ** 2).T
+        assert np.max(np.abs(F - ref)) < 1e-14
+        _, M = univariate.stiffness_mass(deg, alpha, n_el)
+        assert np.max(np.abs(F.sum(axis=1) - np.diag(M))) < 1e-14
