@@ -140,6 +140,16 @@ def summarize_clocks(samples, t0=None, t1=None):
 # ----------------------------------------------------------------------------------------------
 # CPU oracle timing (cpu_baseline and --impl reference)
 # ----------------------------------------------------------------------------------------------
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip() + f" x {os.cpu_count()} threads"
+    except Exception:
+        pass
+    return None
+
+
 def oracle_threads():
     try:
         from threadpoolctl import threadpool_info
@@ -464,7 +474,18 @@ def main():
         os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
         v, nd, n, t, setup_o, _ = oracle_sample(w, args.cpu_seconds)
         cpu = {"value": v, "unit": "apply/s", "cores": oracle_threads(), "kind": "oracle",
-               "sample": f"{n} oracle applications (numpy/scipy FP64) to one RHS of {w.name} in {t:.1f} s; setup {setup_o:.2f} s excluded"}
+               "sample": f"{n} oracle applications (numpy/scipy FP64) to one RHS of {w.name} in {t:.1f} s; setup {setup_o:.2f} s excluded",
+               "cpu_model": cpu_model()}
+        if cid in (1, 2, 3):
+            # also one thread, the paper's protocol
+            try:
+                from threadpoolctl import threadpool_limits
+                with threadpool_limits(limits=1):
+                    v1, _, n1, t1, _, _ = oracle_sample(w, min(args.cpu_seconds, 8.0))
+                cpu["one_thread"] = {"value": v1, "unit": "apply/s", "cores": 1,
+                                     "sample": f"{n1} oracle applications in {t1:.1f} s"}
+            except Exception as e:  # pragma: no cover - threadpoolctl missing
+                cpu["one_thread"] = {"unavailable": str(e)}
     line = {
         "metric": "preconditioner_applications_per_s",
         "value": value,
