@@ -40,6 +40,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--rt-reading", default="paper", choices=["paper", "literal"],
+                    help="RT own-direction regularity: the paper's alpha+1 (default) or configs 3/5's "
+                         "literal 'C^3' wording, alpha (SURVEY.md C-3; a secondary row)")
     ap.add_argument("--impl", default="fdp", choices=["fdp", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the oracle sample")
@@ -56,9 +59,17 @@ def dist_env():
 # ----------------------------------------------------------------------------------------------
 # workload description (counts only; no method arithmetic beyond sizes)
 # ----------------------------------------------------------------------------------------------
+_RT_LITERAL = False
+
+
+def RT_OWN_ALPHA(w):
+    """RT own-direction regularity for --rt-reading literal, else the paper's."""
+    return (w.p - 1) if (_RT_LITERAL and w.disc == "RT") else None
+
+
 def workload_config(cid, w, n_total, batch_total, gpus, flush):
     return {
-        "workload": w.name,
+        "workload": w.name + ("_literal_c3" if (_RT_LITERAL and w.disc == "RT") else ""),
         "config_index": cid,
         "discretization": f"{w.dim}D {w.disc} pressure p={w.p}, velocity p={w.p + 1}, alpha=p-1, {w.n_el}^{w.dim} elements",
         "preconditioner": "P_D^G (D_V=nu, D_Q=1/nu at dofs)" if w.variable_nu else "P_D",
@@ -164,7 +175,7 @@ def oracle_sample(w, budget_s, max_steps=None):
     for about budget_s seconds. Returns (applies/s, dofs/apply, n_calls, seconds, setup_s)."""
     from oracle import precond, spaces
     t0 = time.perf_counter()
-    od = spaces.build(w.dim, w.disc, w.p, w.n_el)
+    od = spaces.build(w.dim, w.disc, w.p, w.n_el, rt_own_alpha=RT_OWN_ALPHA(w))
     dv = dq = None
     if w.variable_nu:
         dv, dq = spaces.nu_scalings(od, synth.viscosity)
@@ -197,7 +208,7 @@ def run_reference(args, w, cid):
     # each step = one oracle application to one RHS (bounded: the whole run stays within minutes)
     steps, warm = args.steps, args.warmup
     from oracle import precond, spaces
-    od = spaces.build(w.dim, w.disc, w.p, w.n_el)
+    od = spaces.build(w.dim, w.disc, w.p, w.n_el, rt_own_alpha=RT_OWN_ALPHA(w))
     dv = dq = None
     if w.variable_nu:
         dv, dq = spaces.nu_scalings(od, synth.viscosity)
@@ -242,7 +253,9 @@ def run_reference(args, w, cid):
 # GPU arm
 # ----------------------------------------------------------------------------------------------
 def main():
+    global _RT_LITERAL
     args = parse()
+    _RT_LITERAL = args.rt_reading == "literal"
     cid = args.config
     w = synth.CONFIGS[cid]
     if args.impl == "reference":
@@ -271,7 +284,7 @@ def main():
 
     # ---- setup (excluded from timing) ----
     t0 = time.perf_counter()
-    gd = fdp.discretization(w.dim, w.disc, w.p, w.n_el)
+    gd = fdp.discretization(w.dim, w.disc, w.p, w.n_el, rt_own_alpha=RT_OWN_ALPHA(w))
     dv = dq = None
     if w.variable_nu:
         dv, dq = fdp.nu_scalings(gd, synth.viscosity)

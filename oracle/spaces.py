@@ -57,10 +57,12 @@ def _grev(deg, alpha, n_el, interior):
     return g[1:-1] if interior else g
 
 
-def build(D: int, disc: str, p: int, n_el: int) -> Discretization:
+def build(D: int, disc: str, p: int, n_el: int, rt_own_alpha: int | None = None) -> Discretization:
     """alpha = p - 1, p = pressure degree; TH velocity S^{p+1}_alpha restricted
     to interior functions in every direction (P:265-276); RT component k: S^{p+1}_{alpha+1}
-    interior in direction k, S^p_alpha full elsewhere with Nitsche."""
+    interior in direction k, S^p_alpha full elsewhere with Nitsche.
+    rt_own_alpha: regularity of the RT own direction (default alpha + 1 = p, the paper;
+    p - 1 is config 3's literal "C^3" wording)."""
     alpha = p - 1
     comps = []
     if disc == "TH":
@@ -69,9 +71,9 @@ def build(D: int, disc: str, p: int, n_el: int) -> Discretization:
         for k in range(D):
             comps.append(Component([K] * D, [M] * D, [1.0 + (d == k) for d in range(D)], [g] * D))
     elif disc == "RT":
-        Kn, Mn = univariate.rt_normal_pencil(p, n_el)
+        Kn, Mn = univariate.rt_normal_pencil(p, n_el, rt_own_alpha)
         Kt, Mt = univariate.rt_tangential_pencil(p, n_el)
-        gn = _grev(p + 1, alpha + 1, n_el, True)
+        gn = _grev(p + 1, alpha + 1 if rt_own_alpha is None else rt_own_alpha, n_el, True)
         gt = _grev(p, alpha, n_el, False)
         for k in range(D):
             comps.append(Component([Kn if d == k else Kt for d in range(D)],

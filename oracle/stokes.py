@@ -59,7 +59,9 @@ class StokesCube:
     (None = constant 1). Config 3's nu = 1 + 0.5 sin(2 pi x) sin(2 pi y) sin(2 pi z) is two
     terms; it equals 1 on the boundary of the cube, so the Nitsche terms keep weight 1."""
 
-    def __init__(self, D: int, disc: str, p: int, n_el: int, nu_terms=None):
+    def __init__(self, D: int, disc: str, p: int, n_el: int, nu_terms=None, rt_own_alpha=None):
+        """rt_own_alpha: regularity of the RT own direction (default alpha + 1; p - 1 is
+        config 3's literal "C^3" wording)."""
         self.D = D
         alpha = p - 1
         nu_terms = nu_terms or [(1.0, None)]
@@ -71,7 +73,7 @@ class StokesCube:
         if disc == "TH":
             V = [[_space(p + 1, alpha, n_el, True)] * D for _ in range(D)]
         elif disc == "RT":
-            N = _space(p + 1, alpha + 1, n_el, True)
+            N = _space(p + 1, alpha + 1 if rt_own_alpha is None else rt_own_alpha, n_el, True)
             T = _space(p, alpha, n_el, False)
             V = [[N if d == k else T for d in range(D)] for k in range(D)]
         else:

@@ -57,9 +57,10 @@ def th_velocity_pencil(p: int, n_el: int):
     return interior(K), interior(M)
 
 
-def rt_normal_pencil(p: int, n_el: int):
-    """(K_k^RT, M_k^RT): degree p+1, regularity alpha+1 = p, interior."""
-    K, M = stiffness_mass(p + 1, p, n_el)
+def rt_normal_pencil(p: int, n_el: int, alpha_own: int | None = None):
+    """(K_k^RT, M_k^RT): degree p+1, regularity alpha+1 = p, interior. alpha_own
+    overrides the regularity (SURVEY.md C-3's literal reading of config 3: p - 1)."""
+    K, M = stiffness_mass(p + 1, p if alpha_own is None else alpha_own, n_el)
     return interior(K), interior(M)
 
 

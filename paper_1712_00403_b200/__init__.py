@@ -662,7 +662,7 @@ class Discretization:
         return int(sum(self.sizes))
 
 
-def discretization(D: int, disc: str, p: int, n_el: int) -> Discretization:
+def discretization(D: int, disc: str, p: int, n_el: int, rt_own_alpha: int | None = None) -> Discretization:
     """Pencils of P_V,k and P_Q with alpha = p-1, C_pen = 5p.
 
     TH: velocity degree p+1 interior in every direction, c_d = 1 + [d = k].
@@ -679,9 +679,10 @@ def discretization(D: int, disc: str, p: int, n_el: int) -> Discretization:
             out.coef.append([1.0 + (d == k) for d in range(D)])
             out.grev.append([g] * D)
     elif disc == "RT":
-        Kn, Mn = iga_univariate(p + 1, a + 1, n_el, FDP_IGA_INTERIOR)
+        ao = a + 1 if rt_own_alpha is None else rt_own_alpha
+        Kn, Mn = iga_univariate(p + 1, ao, n_el, FDP_IGA_INTERIOR)
         Kt, Mt = iga_univariate(p, a, n_el, FDP_IGA_NITSCHE, 5.0 * p)
-        gn = iga_greville(p + 1, a + 1, n_el, FDP_IGA_INTERIOR)
+        gn = iga_greville(p + 1, ao, n_el, FDP_IGA_INTERIOR)
         gt = iga_greville(p, a, n_el)
         for k in range(D):
             out.Ks.append([Kn if d == k else Kt for d in range(D)])

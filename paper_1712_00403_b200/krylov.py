@@ -31,13 +31,13 @@ from . import (FDP_IGA_INTERIOR, FDP_IGA_NITSCHE, KronOp, iga_mass_diag_factor, 
                vec_lincomb_dev, vec_multidot)
 
 
-def _spaces(D, disc, p):
+def _spaces(D, disc, p, rt_own_alpha=None):
     a = p - 1
     Q = (p, a, 0)
     if disc == "TH":
         V = [[(p + 1, a, FDP_IGA_INTERIOR)] * D for _ in range(D)]
     elif disc == "RT":
-        N = (p + 1, a + 1, FDP_IGA_INTERIOR)
+        N = (p + 1, a + 1 if rt_own_alpha is None else rt_own_alpha, FDP_IGA_INTERIOR)
         T = (p, a, 0)
         V = [[N if d == k else T for d in range(D)] for k in range(D)]
     else:
@@ -99,12 +99,15 @@ class _GroupedOperator:
 class StokesOperator(_GroupedOperator):
     """y = calA x for x = [u_1 | .. | u_D | p] (vec order, i1 fastest), on cuda:device."""
 
-    def __init__(self, D: int, disc: str, p: int, n_el: int, nu_terms=None, device: int = 0):
+    def __init__(self, D: int, disc: str, p: int, n_el: int, nu_terms=None, device: int = 0,
+                 rt_own_alpha=None):
+        # rt_own_alpha: RT own-direction regularity (default p, the paper; p - 1 = config 3's
+        # literal "C^3" wording, DESIGN.md C-3)
         self.D = D
         nu_terms = nu_terms or [(1.0, None)]
         weighted = any(w is not None for _, w in nu_terms)
         q = p + 3 + (4 if weighted else 0)
-        V, Qs = _spaces(D, disc, p)
+        V, Qs = _spaces(D, disc, p, rt_own_alpha)
         xq, _ = iga_quadrature(n_el, q)
         mixed = lambda t, r, dt=0, dr=0, w=None: iga_mixed(t, r, n_el, dt, dr, q, None if w is None else w(xq))
         cp = 5.0 * p

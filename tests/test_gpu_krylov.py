@@ -182,3 +182,27 @@ def test_config3_paper_scalings_and_minres():
     assert it_g == it_o, (it_g, it_o)
     with open("gpurun_out/minres_counts.jsonl" if __import__("os").path.isdir("gpurun_out") else "/dev/null", "a") as fh:
         fh.write('{"config": 3, "scalings": "paper (diag ratios)", "iterations": %d}\n' % it_g)
+
+
+def test_config3_literal_c3_minres():
+    """Config 3 under the literal 'C^3' own-direction reading (C-3, secondary row):
+    operator, P_D^G and MINRES all on the alpha_own = p - 1 spaces; identical counts."""
+    w = synth.CONFIGS[3]
+    a = w.p - 1
+    op = ostokes.StokesCube(w.dim, w.disc, w.p, w.n_el, nu_terms=ostokes.config3_nu_terms(w.dim),
+                            rt_own_alpha=a)
+    od = ospaces.build(w.dim, w.disc, w.p, w.n_el, rt_own_alpha=a)
+    gd = fdp.discretization(w.dim, w.disc, w.p, w.n_el, rt_own_alpha=a)
+    assert op.vel_dims == [c.dims for c in od.comps] and gd.comp_dims == op.vel_dims
+    dv, dq = ospaces.nu_scalings(od, synth.viscosity)
+    f = ostokes.project_rhs(synth.rhs(w.seed, op.n, 1)[0], op.sizes[-1])
+    _, it_o, h_o = ominres.minres(op.matvec, f, oprec.BlockPrecond(od, dv, dq).apply)
+    gop = krylov.StokesOperator(w.dim, w.disc, w.p, w.n_el, nu_terms=synth.viscosity_separable(w.dim),
+                                rt_own_alpha=a)
+    P = fdp.build_block(gd, dscale_vel=dv, dscale_pres=dq)
+    ws = P.workspace(1)
+    _, it_g, h_g = krylov.minres(gop.apply, lambda r, z: P.apply(r, z, workspace=ws), dev(f))
+    assert it_g == it_o, (it_g, it_o)
+    assert max(abs(x - y) / x for x, y in zip(h_o, h_g)) < 1e-6
+    with open("gpurun_out/minres_counts.jsonl" if __import__("os").path.isdir("gpurun_out") else "/dev/null", "a") as fh:
+        fh.write('{"config": 3, "reading": "literal C^3 own direction", "iterations": %d}\n' % it_g)

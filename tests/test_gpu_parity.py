@@ -450,3 +450,24 @@ def test_empty_batches_are_noops():
     assert lib.block_precond_apply_host(P.h, ctypes.c_void_p(1), ctypes.c_void_p(1), 0, None) == 0
     torch.cuda.synchronize()
     assert torch.all(x == 7.0)
+
+
+def test_config3_literal_c3_reading():
+    """SURVEY.md C-3's secondary row: config 3 with the literal 'C^3' regularity in the RT own
+    direction (130 x 68 x 68 per component at 64^3: the own-direction mode leaves the small
+    path), P_D^G with the Greville scalings, against the oracle built the same way."""
+    w = synth.CONFIGS[3]
+    od = ospaces.build(w.dim, w.disc, w.p, w.n_el, rt_own_alpha=w.p - 1)
+    gd = fdp.discretization(w.dim, w.disc, w.p, w.n_el, rt_own_alpha=w.p - 1)
+    assert gd.comp_dims == [c.dims for c in od.comps] and gd.q_dims == od.q_dims
+    assert gd.comp_dims[0] == [130, 68, 68] and od.n_total == 2117792
+    dv, dq = ospaces.nu_scalings(od, synth.viscosity)
+    gdv, gdq = fdp.nu_scalings(gd, synth.viscosity)
+    assert np.max(np.abs(gdv - dv)) < 1e-14 and np.max(np.abs(gdq - dq)) < 1e-14
+    P = fdp.build_block(gd, dscale_vel=dv, dscale_pres=dq)
+    r = synth.rhs(w.seed, od.n_total, 1)
+    s = P.apply(dev(r), batch=1).cpu().numpy()
+    ref = oprec.BlockPrecond(od, dv, dq).apply(r)
+    o = od.offsets()
+    for k in range(len(o) - 1):
+        assert rel(s[0, o[k]:o[k + 1]], ref[0, o[k]:o[k + 1]]) < TOL, k

@@ -84,12 +84,15 @@ def test_th_block_equals_kronecker_sum(k):
     assert np.max(np.abs(A - R)) < 1e-13 * np.max(np.abs(R))
 
 
-@pytest.mark.parametrize("k", [0, 1, 2])
-def test_rt_block_equals_kronecker_sum_with_nitsche(k):
+@pytest.mark.parametrize("k,own", [(0, None), (1, None), (2, None), (0, 1), (2, 1)])
+def test_rt_block_equals_kronecker_sum_with_nitsche(k, own):
+    # own = RT own-direction regularity: None = alpha + 1 = p, 1 = p - 1 (config 3's
+    # literal "C^3" wording)
     p, n_el = 2, 2
     cpen = univariate.c_pen(p)
     h = 1.0 / n_el
-    sp = [_space(p + 1, p, n_el, True) if d == k else _space(p, p - 1, n_el, False) for d in range(3)]
+    sp = [_space(p + 1, p if own is None else own, n_el, True) if d == k else _space(p, p - 1, n_el, False)
+          for d in range(3)]
     X, W = _grid([n_el] * 3, p + 3)
     _, G, n = _trivariate(sp, X)
     A = _a_hat(G, W, k)
@@ -119,7 +122,7 @@ def test_rt_block_equals_kronecker_sum_with_nitsche(k):
                 wv = np.outer(Bf[q], Bf[q])  # w_i . v_j = B_i B_j (both along e_k)
                 cons = np.outer(Sn @ ek, Bf[q])  # ((grad^s w_i) n) . v_j
                 A += wts[q] * 2.0 * (cpen / h * wv - cons - cons.T)
-    Kn, Mn = univariate.rt_normal_pencil(p, n_el)
+    Kn, Mn = univariate.rt_normal_pencil(p, n_el, own)
     Kt, Mt = univariate.rt_tangential_pencil(p, n_el)
     Ks = [Kn if d == k else Kt for d in range(3)]
     Ms = [Mn if d == k else Mt for d in range(3)]

@@ -34,12 +34,13 @@ def test_operator_symmetric_and_null_space(disc, p, n_el):
     assert np.all(A[op.off_idx[3]:, op.off_idx[3]:] == 0.0)
 
 
-@pytest.mark.parametrize("disc,p,n_el", [("TH", 1, 2), ("RT", 2, 2), ("TH", 2, 1)])
-def test_diagonal_blocks_equal_pv(disc, p, n_el):
-    # A_kk = P_V,k on the identity map
-    op = stokes.StokesCube(3, disc, p, n_el)
+@pytest.mark.parametrize("disc,p,n_el,own", [("TH", 1, 2, None), ("RT", 2, 2, None), ("TH", 2, 1, None),
+                                              ("RT", 2, 2, 1)])
+def test_diagonal_blocks_equal_pv(disc, p, n_el, own):
+    # A_kk = P_V,k on the identity map; own = 1: the literal C-3 reading
+    op = stokes.StokesCube(3, disc, p, n_el, rt_own_alpha=own)
     A = _dense(op)
-    d = spaces.build(3, disc, p, n_el)
+    d = spaces.build(3, disc, p, n_el, rt_own_alpha=own)
     o = op.off_idx
     for k, c in enumerate(d.comps):
         R = fd.assemble_R(c.Ks, c.Ms, c.coef)
