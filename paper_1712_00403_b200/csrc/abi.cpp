@@ -24,12 +24,105 @@ extern "C" const char* fdp_version(void) { return "fdp 0.1 sm_100a"; }
 // ------------------------------------------------------------------------------------------------
 
 
+// ------------------------------------------------------------------------------------------------
+// Even-odd folding (DESIGN.md §5 "folded transforms"). J = index reversal. A persymmetric pencil
+// (J K J = K, J M J = M: every pencil of the cube configurations, open uniform knots with the
+// same boundary treatment at both ends) is block-diagonalised by the orthogonal
+//   Q = [q^E_0 .. q^E_{ne-1} | q^O_0 .. q^O_{no-1}],  q^E_k = (e_k + e_{n-1-k}) / sqrt2 (k < no),
+//   q^E_h = e_h (odd n, h = no),  q^O_k = (e_k - e_{n-1-k}) / sqrt2,
+// so K U = M U Lambda splits into the ne x ne and no x no pencils Q_E^T (K, M) Q_E and
+// Q_O^T (K, M) Q_O (P:990-996 on each block), U = Q diag(V_E, V_O), U^T M U = I unchanged.
+// ------------------------------------------------------------------------------------------------
+bool persymmetric(int n, const double* A, double rtol) {
+  double mx = 0.0, dev = 0.0;
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i) {
+      const double a = A[i + (size_t)n * j];
+      mx = std::max(mx, std::fabs(a));
+      dev = std::max(dev, std::fabs(a - A[(n - 1 - i) + (size_t)n * (n - 1 - j)]));
+    }
+  return dev <= rtol * mx;
+}
+
+// Q_X^T A Q_X (X = E: sign +1, X = O: sign -1), column-major m x m
+static std::vector<double> fold_block(int n, const double* A, int sign) {
+  const int no = n / 2, m = sign > 0 ? (n + 1) / 2 : no;
+  const double r2 = std::sqrt(0.5);
+  auto a = [&](int i, int j) { return A[i + (size_t)n * j]; };
+  std::vector<double> B((size_t)m * m);
+  for (int j = 0; j < m; ++j)
+    for (int i = 0; i < m; ++i) {
+      const bool mi = i == no, mj = j == no;  // middle of an odd n (E only)
+      double v;
+      if (mi && mj) v = a(no, no);
+      else if (mi) v = r2 * (a(no, j) + a(no, n - 1 - j));
+      else if (mj) v = r2 * (a(i, no) + a(n - 1 - i, no));
+      else
+        v = 0.5 * (a(i, j) + sign * a(i, n - 1 - j) + sign * a(n - 1 - i, j) + a(n - 1 - i, n - 1 - j));
+      B[i + (size_t)m * j] = v;
+    }
+  return B;
+}
+
+void fold_sym_matrix(int n, const double* A, int foldh, int ldw, std::vector<double>* w) {
+  // y = A x: e_c = sum_k W_E[k][c] s_k, o_c = sum_k W_O[k][c] d_k, y_c = e_c + o_c,
+  // y_{n-1-c} = e_c - o_c with W_E[k][c] = (A[c][k] + A[c][n-1-k]) / 2 (the middle row k = h:
+  // A[c][h] / 2, since s_h = 2 x_h), W_O[k][c] = (A[c][k] - A[c][n-1-k]) / 2.
+  const int ne = (n + 1) / 2, no = n / 2;
+  w->assign((size_t)2 * foldh * ldw, 0.0);
+  auto a = [&](int i, int j) { return A[i + (size_t)n * j]; };
+  for (int k = 0; k < ne; ++k)
+    for (int c = 0; c < ne; ++c)
+      (*w)[(size_t)k * ldw + c] = k == no ? 0.5 * a(c, k) : 0.5 * (a(c, k) + a(c, n - 1 - k));
+  for (int k = 0; k < no; ++k)
+    for (int c = 0; c < no; ++c)
+      (*w)[(size_t)(foldh + k) * ldw + c] = 0.5 * (a(c, k) - a(c, n - 1 - k));
+}
+
+// Folded eigen-data of a persymmetric pencil: forward / backward matrices in the folded layout and
+// coef * [lambda_E | lambda_O].
+static int fold_eig(int n, const double* K, const double* M, double coef, int foldh, int ldw,
+                    std::vector<double>* wf, std::vector<double>* wb, std::vector<double>* lam,
+                    std::string* err) {
+  const int ne = (n + 1) / 2, no = n / 2;
+  const double r2 = std::sqrt(0.5);
+  std::vector<double> KE = fold_block(n, K, 1), ME = fold_block(n, M, 1);
+  std::vector<double> KO = fold_block(n, K, -1), MO = fold_block(n, M, -1);
+  std::vector<double> VE((size_t)ne * ne), VO((size_t)no * no), lE(ne), lO(no);
+  int st = gen_eig(ne, KE.data(), ME.data(), VE.data(), lE.data(), err);
+  if (!st && no > 0) st = gen_eig(no, KO.data(), MO.data(), VO.data(), lO.data(), err);
+  if (st) return st;
+  wf->assign((size_t)2 * foldh * ldw, 0.0);
+  wb->assign((size_t)2 * foldh * ldw, 0.0);
+  // forward W_E[k][a] = V_E[k][a] / sqrt2 (k < no), V_E[h][a] / 2 (middle: s_h = 2 x_h);
+  // backward W_E[a][c] = V_E[c][a] / sqrt2 (c < no), V_E[h][a] (middle)
+  for (int k = 0; k < ne; ++k)
+    for (int a = 0; a < ne; ++a) {
+      const double v = VE[k + (size_t)ne * a];
+      (*wf)[(size_t)k * ldw + a] = k == no ? 0.5 * v : r2 * v;
+      (*wb)[(size_t)a * ldw + k] = k == no ? v : r2 * v;
+    }
+  for (int k = 0; k < no; ++k)
+    for (int a = 0; a < no; ++a) {
+      const double v = r2 * VO[k + (size_t)no * a];
+      (*wf)[(size_t)(foldh + k) * ldw + a] = v;
+      (*wb)[(size_t)(foldh + a) * ldw + k] = v;
+    }
+  lam->resize(n);
+  for (int a = 0; a < ne; ++a) (*lam)[a] = coef * lE[a];
+  for (int a = 0; a < no; ++a) (*lam)[ne + a] = coef * lO[a];
+  return 0;
+}
+
 static void free_fd(fdp_fd h) {
   if (!h) return;
   for (int d = 0; d < 3; ++d) {
     cudaFree(h->Wf[d]);
     cudaFree(h->Wb[d]);
     cudaFree(h->lamc[d]);
+    cudaFree(h->WfF[d]);
+    cudaFree(h->WbF[d]);
+    cudaFree(h->lamcF[d]);
   }
   cudaFree(h->ws);
   cudaFree(h->sync);
@@ -108,6 +201,51 @@ extern "C" fdp_status fd_setup(int D, const int32_t* n, const double* const* K,
           (st = dalloc(&raw->lamc[d], lc.size()))) {
         free_fd(raw);
         return st;
+      }
+      // folded copy (small-path extents with a persymmetric pencil; FDP_NO_FOLD=1 disables)
+      const bool can_fold = std::getenv("FDP_NO_FOLD") == nullptr &&
+                            std::getenv("FDP_NO_SMALL") == nullptr && nd >= 8 && nd <= kSmallMaxN &&
+                            c.tiles_n == 1 && persymmetric(nd, K[d], 1e-12) &&
+                            persymmetric(nd, M[d], 1e-12);
+      std::vector<double> lcf = lc;
+      if (can_fold) {
+        const int nt = fold_nt(nd);
+        const int foldh = 4 * nt, ldwf = 4 * nt;  // KPF rows / 8 * NTE columns of the kernel
+        std::vector<double> wff, wbf;
+        std::string err;
+        const int fst = fold_eig(nd, K[d], M[d], coef[d], foldh, ldwf, &wff, &wbf, &lcf, &err);
+        if (fst) {
+          free_fd(raw);
+          return fail((fdp_status)fst, "fd_setup (folded): " + err);
+        }
+        raw->fold[d] = 1;
+        raw->fold_nt[d] = nt;
+        raw->foldh[d] = foldh;
+        raw->ldwF[d] = ldwf;
+        fdp_status fs;
+        if ((fs = dalloc(&raw->WfF[d], wff.size())) || (fs = dalloc(&raw->WbF[d], wbf.size()))) {
+          free_fd(raw);
+          return fs;
+        }
+        cudaError_t e;
+        if ((e = cudaMemcpy(raw->WfF[d], wff.data(), wff.size() * 8, cudaMemcpyHostToDevice)) ||
+            (e = cudaMemcpy(raw->WbF[d], wbf.data(), wbf.size() * 8, cudaMemcpyHostToDevice)) ||
+            (e = prepare_mode_small(nt))) {
+          free_fd(raw);
+          return cuda_fail(e, "fd_setup: folded upload");
+        }
+      }
+      {
+        fdp_status fs = dalloc(&raw->lamcF[d], lcf.size());
+        if (fs) {
+          free_fd(raw);
+          return fs;
+        }
+        cudaError_t e = cudaMemcpy(raw->lamcF[d], lcf.data(), lcf.size() * 8, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+          free_fd(raw);
+          return cuda_fail(e, "fd_setup: upload");
+        }
       }
       cudaError_t e;
       if ((e = cudaMemcpy(raw->Wf[d], wf.data(), wf.size() * 8, cudaMemcpyHostToDevice)) ||
@@ -262,10 +400,16 @@ static ModeProb make_mode_prob(const fdp_fd_s* h, int d, bool fwd, const double*
   if (std::getenv("FDP_NO_VEC")) p.vx = p.vy = 0;
   p.epi = epi;
   p.scale = scale;
-  if (epi == EPI_LAMBDA || epi == EPI_FUSED) {
-    p.lam0 = h->lamc[0];
-    p.lam1 = h->D == 3 ? h->lamc[1] : nullptr;
-    p.lamcol = h->lamc[h->D - 1];
+  if (epi == EPI_LAMBDA || epi == EPI_FUSED) {  // spectral order of the (possibly folded) modes
+    p.lam0 = h->lamcF[0];
+    p.lam1 = h->D == 3 ? h->lamcF[1] : nullptr;
+    p.lamcol = h->lamcF[h->D - 1];
+  }
+  if (h->fold[d]) {
+    p.fold = epi == EPI_FUSED ? FOLD_FUSED : (fwd ? FOLD_FWD : FOLD_BWD);
+    p.W = fwd ? h->WfF[d] : h->WbF[d];
+    p.ldw = h->ldwF[d];
+    p.foldh = h->foldh[d];
   }
   const int BM = kK1Warps * 8 * h->cfg[d].MT;
   const long long M = P * Q * batch;
@@ -344,7 +488,9 @@ cudaError_t launch_stage(std::vector<ModeProb>& probs_in, const std::vector<Tile
     g.count = 0;
     int ctas = 0;
     for (size_t j = i; j < probs.size() && g.count < kMaxGroup; ++j) {
-      if (done[j] || cfgs[j].NT != cfgs[i].NT || cfgs[j].MT != cfgs[i].MT) continue;
+      if (done[j] || cfgs[j].NT != cfgs[i].NT || cfgs[j].MT != cfgs[i].MT ||
+          (probs[j].fold != FOLD_NONE) != (probs[i].fold != FOLD_NONE))
+        continue;
       ModeProb p = probs[j];
       p.cta_begin = ctas;
       ctas += p.tiles_m * p.tiles_n;
@@ -361,12 +507,13 @@ cudaError_t launch_stage(std::vector<ModeProb>& probs_in, const std::vector<Tile
         ModeProb& p = g.prob[j];
         const long long M = (long long)p.P * p.Q * p.batch;
         p.tiles_m = (int)((M + 7) / 8);
-        w[j] = (double)p.tiles_m * ((p.n + 3) / 4) * (p.epi == EPI_FUSED ? 2 : 1);
+        const int kn = p.fold ? (p.n + 1) / 2 : p.n;  // folded: about half the k4 steps
+        w[j] = (double)p.tiles_m * ((kn + 3) / 4) * (p.epi == EPI_FUSED ? 2 : 1);
       }
       alloc_small_ctas(g, w);
     } else {
-      for (int j = 0; j < g.count; ++j)
-        if (g.prob[j].epi == EPI_FUSED) return cudaErrorInvalidValue;  // fused needs small path
+      for (int j = 0; j < g.count; ++j)  // fused and folded passes need the small path
+        if (g.prob[j].epi == EPI_FUSED || g.prob[j].fold) return cudaErrorInvalidValue;
     }
     if (rec) {
       double fl = 0.0, by = 0.0;
@@ -483,7 +630,8 @@ cudaError_t enqueue_fd(const std::vector<const fdp_fd_s*>& hs,
   bool pp = fuse && D == 3 && sync != nullptr && std::getenv("FDP_PP") != nullptr;
   for (size_t k = 0; k < K; ++k)
     for (int d = 0; d < 2; ++d)
-      pp = pp && hs[k]->cfg[d].NT <= kPPMaxNT && hs[k]->cfg[d].NT == hs[0]->cfg[0].NT;
+      pp = pp && hs[k]->cfg[d].NT <= kPPMaxNT && hs[k]->cfg[d].NT == hs[0]->cfg[0].NT &&
+           !hs[k]->fold[d];
   std::vector<ModeProb> held;  // phase-1 problems waiting for their phase-2 partners
   for (int pass = 0; pass < npass; ++pass) {
     const Stage& st = stages[pass];
@@ -508,7 +656,9 @@ cudaError_t enqueue_fd(const std::vector<const fdp_fd_s*>& hs,
       else if (st.fwd && d == D - 1) epi = EPI_LAMBDA;
       if (!st.fwd && d == 0 && dscale[k]) { epi = EPI_SCALE; sc = dscale[k]; }
       probs.push_back(make_mode_prob(hs[k], d, st.fwd, src, sbs, dst, dbs, batch, epi, sc, xld, yld));
-      cfgs.push_back(hs[k]->cfg[d]);
+      TileCfg c = hs[k]->cfg[d];
+      if (hs[k]->fold[d]) c.NT = hs[k]->fold_nt[d];
+      cfgs.push_back(c);
     }
     if (hook) hook(pass, st.fwd, d, probs, cfgs);
     if (pp && (pass == 0 || pass == 3)) {

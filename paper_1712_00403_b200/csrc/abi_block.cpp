@@ -97,9 +97,24 @@ extern "C" fdp_status block_precond_setup(int D, const fdp_fd* vel, fdp_mass pre
         const int kpad = ((nq + 15) / 16) * 16;
         std::vector<double> X;
         spd_inverse_from_band(nq, pres->band[d], pres->Lb_host[d], &X);
-        std::vector<double> w((size_t)kpad * raw->q_ldw[d], 0.0);
-        for (int k = 0; k < nq; ++k)
-          for (int a = 0; a < nq; ++a) w[(size_t)k * raw->q_ldw[d] + a] = X[a + (size_t)nq * k];
+        // the velocity launch of stage d is folded: a centrosymmetric M_d^{-1} joins it as a
+        // FOLD_SYM pass (about half the DMMAs); otherwise its own dense launch
+        bool vfold = true;
+        for (int k = 0; k < D; ++k)
+          vfold = vfold && raw->vel[k]->fold[d] && raw->vel[k]->fold_nt[d] == raw->vel[0]->fold_nt[d];
+        std::vector<double> w;
+        if (vfold && nq >= 8 && fold_nt(nq) <= raw->vel[0]->fold_nt[d] && persymmetric(nq, X.data(), 1e-10)) {
+          const int nt = raw->vel[0]->fold_nt[d];
+          raw->q_fold[d] = 1;
+          raw->q_foldh[d] = 4 * nt;
+          raw->q_ldw[d] = 4 * nt;
+          raw->q_tiles_n[d] = 1;
+          fold_sym_matrix(nq, X.data(), 4 * nt, 4 * nt, &w);
+        } else {
+          w.assign((size_t)kpad * raw->q_ldw[d], 0.0);
+          for (int k = 0; k < nq; ++k)
+            for (int a = 0; a < nq; ++a) w[(size_t)k * raw->q_ldw[d] + a] = X[a + (size_t)nq * k];
+        }
         st = dalloc(&raw->Wq[d], w.size());
         if (!st) {
           cudaError_t e = cudaMemcpy(raw->Wq[d], w.data(), w.size() * 8, cudaMemcpyHostToDevice);
@@ -225,8 +240,14 @@ static cudaError_t enqueue_block(fdp_block h, const double* r, double* s, int64_
       p.tiles_m = (int)((P * Q * batch + BM - 1) / BM);
       p.tiles_n = h->q_tiles_n[d];
       p.fd_work = 0;
+      TileCfg qc = h->vel[0]->cfg[d];
+      if (h->q_fold[d]) {
+        p.fold = FOLD_SYM;
+        p.foldh = h->q_foldh[d];
+        qc.NT = h->vel[0]->fold_nt[d];
+      }
       probs.push_back(p);
-      cfgs.push_back(cfgs[0]);
+      cfgs.push_back(qc);
       (void)pass;
     };
   }
@@ -438,8 +459,14 @@ static cudaError_t enqueue_unit(fdp_block h, int k, const double* r, double* s, 
       const int BM = kK1Warps * 8 * vc.MT;
       p.tiles_m = (int)((P * Q + BM - 1) / BM);
       p.tiles_n = h->q_tiles_n[d];
+      TileCfg qc = h->vel[0]->cfg[d];
+      if (h->q_fold[d]) {
+        p.fold = FOLD_SYM;
+        p.foldh = h->q_foldh[d];
+        qc.NT = h->vel[0]->fold_nt[d];
+      }
       std::vector<ModeProb> probs{p};
-      std::vector<TileCfg> cfgs{h->vel[0]->cfg[d]};
+      std::vector<TileCfg> cfgs{qc};
       cudaError_t e = launch_stage(probs, cfgs, d == 0, st, nullptr, nullptr);
       if (e != cudaSuccess) return e;
     }

@@ -149,6 +149,17 @@ struct fdp_fd_s {
   double* Wf[3] = {nullptr, nullptr, nullptr};  // forward  W[k][a] = U[k][a]
   double* Wb[3] = {nullptr, nullptr, nullptr};  // backward W[k][a] = U[a][k]
   double* lamc[3] = {nullptr, nullptr, nullptr};  // coef[d] * lambda_d
+  // even-odd folded transforms: modes with a persymmetric pencil and a small-path
+  // extent. WfF / WbF: blocks E (rows [0, foldh)) and O (rows [foldh, 2 foldh)), ldwF columns;
+  // lamcF: coef[d] * lambda_d in the folded spectral order [E | O] (= lamc for unfolded modes).
+  // The dense Wf / Wb / lamc stay for the slab-sharded paths.
+  int fold[3] = {0, 0, 0};
+  int fold_nt[3] = {0, 0, 0};  // small-kernel NT of a folded mode: 2 * ceil(ceil(n/2) / 8)
+  int foldh[3] = {0, 0, 0};
+  int ldwF[3] = {0, 0, 0};
+  double* WfF[3] = {nullptr, nullptr, nullptr};
+  double* WbF[3] = {nullptr, nullptr, nullptr};
+  double* lamcF[3] = {nullptr, nullptr, nullptr};
   double* ws = nullptr;
   int64_t ws_batch = 0;
   int* sync = nullptr;        // plane-pipeline counters (zeroed, self-resetting)
@@ -190,6 +201,8 @@ struct fdp_block_s {
   double* Wq[3] = {nullptr, nullptr, nullptr};
   int q_tiles_n[3] = {0, 0, 0};
   int q_ldw[3] = {0, 0, 0};
+  int q_fold[3] = {0, 0, 0};   // M_d^{-1} is centrosymmetric: folded (FOLD_SYM) pass, Wq = E | O
+  int q_foldh[3] = {0, 0, 0};
   cudaStream_t cap = nullptr;  // private capture stream
   // graph cache
   std::mutex mu;
@@ -243,6 +256,12 @@ struct fdp_kron_s {
 // ------------------------------------------------------------------------------------------------
 // launch orchestration shared by the ABI files (abi_fd.cpp)
 // ------------------------------------------------------------------------------------------------
+// Even-odd folding helpers (abi.cpp). fold_nt: the small-kernel NT of a folded extent n.
+bool persymmetric(int n, const double* A, double rtol);
+inline int fold_nt(int n) { return 2 * (((n + 1) / 2 + 7) / 8); }
+// Centrosymmetric A (n x n, column-major): folded single-pass matrix (FOLD_SYM) in the global
+// layout of the folded kernels: rows [0, foldh) = E block, [foldh, 2 foldh) = O block, ldw cols.
+void fold_sym_matrix(int n, const double* A, int foldh, int ldw, std::vector<double>* w);
 using StageHook = std::function<void(int pass, bool fwd, int d, std::vector<ModeProb>&,
                                      std::vector<TileCfg>&)>;
 cudaError_t launch_stage(std::vector<ModeProb>& probs_in, const std::vector<TileCfg>& cfgs_in,

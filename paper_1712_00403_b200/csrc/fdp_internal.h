@@ -21,6 +21,9 @@ namespace fdp {
 //   backward transform (x_d U_d)  : W[k][a] = U_d[a][k]
 // Flattened GEMM rows m = p + P*q; "KMAJ" (P == 1, mode 1) rows are contiguous along k.
 // ---------------------------------------------------------------------------------------------
+// FOLD_SYM: y = A x for a centrosymmetric A (J A J = A) in one folded pass (dense P_Q^{-1} modes)
+enum Fold : int { FOLD_NONE = 0, FOLD_FWD = 1, FOLD_BWD = 2, FOLD_FUSED = 3, FOLD_SYM = 4 };
+
 enum Epilogue : int {
   EPI_NONE = 0,
   EPI_LAMBDA = 1,  // divide by Lambda[i] = lamrow(p) + lamcol[a]   (Algorithm 1 step 3)
@@ -53,6 +56,12 @@ struct ModeProb {
   int cta_begin;          // first CTA of this problem in the grouped grid
   int fd_work;            // host-side accounting only: 1 = FD contraction, 0 = dense P_Q pass
   int ctas;               // small-n kernel: CTAs assigned to this problem
+  // Even-odd folding of a persymmetric mode (DESIGN.md §5 "folded transforms"): 0 = dense W,
+  // FOLD_FWD / FOLD_BWD / FOLD_FUSED = the folded forward, backward or fused (forward, Lambda,
+  // backward) transform. W then holds two blocks, E (rows [0, foldh)) and O (rows [foldh, 2 foldh)),
+  // and the mode's spectral index runs over [E (ceil(n/2)) | O (floor(n/2))].
+  int fold;
+  int foldh;
   // Peer-store scatter (slab exchange fused into the epilogue): when peers != NULL,
   // output element (GEMM row m, column a) of a batch-1, non-KMAJ problem is stored at
   // peers[o] + r + sc_n1 * ((a - lo_o) * (sc_a0 + sc_a1 * len_o) + (q + sc_qoff) * (sc_q0 + sc_q1 * len_o))
@@ -157,6 +166,8 @@ struct PlaneSync {
 };
 cudaError_t launch_mode_pp(const ModeGroup& g1, const ModeGroup& g2, const PlaneSync& ps, int NT,
                            bool kmaj1, cudaStream_t s);
+// Folded problems (prob.fold != 0, every problem of the group) take the even-odd kernel; NT is
+// then 2 * ceil(ceil(n/2) / 8) (even).
 cudaError_t launch_mode_small(const ModeGroup& g, int NT, bool kmaj, cudaStream_t s);
 cudaError_t prepare_mode_small(int NT);
 

@@ -60,6 +60,10 @@ struct SS {
   static constexpr int W_ELEMS = KP * SB;
   static constexpr size_t BYTES = sizeof(double) * (W_ELEMS + SW * ABUF);
   static constexpr size_t BYTES_PP = sizeof(double) * (2 * W_ELEMS + SW * ABUF);
+  // folded W (NT = 2 * NTE): blocks E and O of KPF rows x 8*NTE columns, row stride SBF
+  static constexpr int KPF = 4 * NT;
+  static constexpr int SBF = ((KPF + 15) / 16) * 16 + 4;
+  static_assert(2 * KPF * SBF <= W_ELEMS, "folded W must fit the dense W footprint");
 };
 
 // Load W (rows 0..rows-1, cols 0..BN-1 of the padded global matrix) into shared memory.
@@ -73,6 +77,20 @@ __device__ __forceinline__ void load_w(double* Ws, const ModeProb& pb, int tid) 
   for (int c = tid; c < chunks; c += STH) {
     const int r = c / (S::BN / 2), cc = (c % (S::BN / 2)) * 2;
     cp_async16g(&Ws[r * S::SB + cc], pb.W + (size_t)r * pb.ldw + cc);
+  }
+  commit();
+}
+
+// Folded W: block E = global rows [0, KPF), block O = global rows [foldh, foldh + KPF), columns
+// [0, 8*NTE) of each.
+template <int NT>
+__device__ __forceinline__ void load_w_fold(double* Ws, const ModeProb& pb, int tid) {
+  using S = SS<NT>;
+  constexpr int CPR = S::KPF / 2;  // 16-byte chunks per row (8*NTE doubles)
+  for (int c = tid; c < 2 * S::KPF * CPR; c += STH) {
+    const int r = c / CPR, cc = (c % CPR) * 2;
+    const int gr = r < S::KPF ? r : pb.foldh + (r - S::KPF);
+    cp_async16g(&Ws[r * S::SBF + cc], pb.W + (size_t)gr * pb.ldw + cc);
   }
   commit();
 }
@@ -121,6 +139,10 @@ template <int NT, bool KMAJ, bool SC = false>
 __device__ __forceinline__ void tile_compute_store(const ModeProb& pb, const Geo& g,
                                                    const double* Ws, double* A, long long t,
                                                    int lane, unsigned long long* tr);
+template <int NT, bool KMAJ>
+__device__ __forceinline__ void tile_compute_store_fold(const ModeProb& pb, const Geo& g,
+                                                        const double* Ws, double* A, long long t,
+                                                        int lane);
 
 // Asynchronous panel load (8-byte cp.async with zero fill beyond n / M) into A ([8][SA]); one
 // commit group.
@@ -166,7 +188,7 @@ __device__ __forceinline__ void load_panel_async(const ModeProb& pb, const Geo& 
 
 // One 8-row tile: panel load (LDG -> STS, zero fill beyond n / M), DMMAs, epilogue.
 // COHERENT: the input was written earlier in the same launch (plane pipeline): L2-coherent loads.
-template <int NT, bool KMAJ, bool COHERENT, bool SC = false>
+template <int NT, bool KMAJ, bool COHERENT, bool SC = false, bool FOLD = false>
 __device__ __forceinline__ void do_tile(const ModeProb& pb, const Geo& g, const double* Ws,
                                         double* A, long long t, int lane,
                                         unsigned long long* tr) {
@@ -267,7 +289,10 @@ __device__ __forceinline__ void do_tile(const ModeProb& pb, const Geo& g, const 
   }
   __syncwarp();
   if (tr) tr[3] = gtimer();
-  tile_compute_store<NT, KMAJ, SC>(pb, g, Ws, A, t, lane, tr);
+  if constexpr (FOLD)
+    tile_compute_store_fold<NT, KMAJ>(pb, g, Ws, A, t, lane);
+  else
+    tile_compute_store<NT, KMAJ, SC>(pb, g, Ws, A, t, lane, tr);
 }
 
 template <int NT, bool KMAJ, bool SC>
@@ -409,7 +434,227 @@ __device__ __forceinline__ void tile_compute_store(const ModeProb& pb, const Geo
   if (tr) tr[5] = gtimer();
 }
 
-template <int NT, bool KMAJ, int G, bool SC = false>
+
+// Even-odd folded transform of one 8-row tile (pb.fold != 0). For a persymmetric
+// pencil (J K J = K, J M J = M, J the index reversal) the eigenvectors split into ne = ceil(n/2)
+// symmetric and no = floor(n/2) antisymmetric ones, so with s_k = x_k + x_{n-1-k} (k < ne) and
+// d_k = x_k - x_{n-1-k} (k < no):
+//   forward   y_E = W_E^T s,  y_O = W_O^T d                       (spectral order [E | O])
+//   backward  e = W_E y_E, o = W_O y_O;  x_k = e_k + o_k,  x_{n-1-k} = e_k - o_k
+// -- the same x as the dense m-mode product of P:389-398 (Algorithm 1 steps 2 and 4)
+// in about half the DMMAs. W_E / W_O carry the 1/sqrt(2) normalisation (the middle row of an odd
+// n: 1/2 in the forward matrix, 1 in the backward one). FOLD_FUSED (small D-th mode): forward,
+// division by Lambda and backward in one pass, the backward reading the forward W
+// transposed; its middle output (odd n) is doubled to undo the forward's 1/2. FOLD_SYM: y = A x
+// for a centrosymmetric A (the dense M_d^{-1} passes of P_Q): e = W_E^T s,
+// o = W_O^T d and the backward's output butterfly.
+template <int NT, bool KMAJ>
+__device__ __forceinline__ void tile_compute_store_fold(const ModeProb& pb, const Geo& g,
+                                                        const double* Ws, double* A, long long t,
+                                                        int lane) {
+  using S = SS<NT>;
+  constexpr int NTE = NT / 2;
+  constexpr int SBF = S::SBF;
+  const double* WO = Ws + S::KPF * SBF;
+  const int n = g.n, ne = (n + 1) >> 1, no = n >> 1;
+  const bool full_o = ((no + 7) >> 3) == NTE;  // else the last O tile is empty
+  const int m0 = (int)(t * 8);
+  const int fr = lane >> 2, fc = lane & 3;
+  double* Ar = A + fr * S::SA;
+  const int mode = pb.fold;
+  double ae[NTE][2], ao[NTE][2];
+#pragma unroll
+  for (int j = 0; j < NTE; ++j) ae[j][0] = ae[j][1] = ao[j][0] = ao[j][1] = 0.0;
+
+  if (mode != FOLD_BWD) {
+    const int k4n = (ne + 3) >> 2;
+    for (int k4 = 0; k4 < k4n; ++k4) {
+      const int k = 4 * k4 + fc;
+      const double x0 = Ar[k], x1 = Ar[n - 1 - k];  // k <= ne + 2 < n (n >= 8)
+      const double sv = x0 + x1, dv = x0 - x1;
+      double be[NTE], bo[NTE];
+#pragma unroll
+      for (int j = 0; j < NTE; ++j) {
+        be[j] = Ws[k * SBF + 8 * j + fr];
+        bo[j] = WO[k * SBF + 8 * j + fr];
+      }
+#pragma unroll
+      for (int j = 0; j < NTE; ++j) dmma(ae[j], sv, be[j]);
+#pragma unroll
+      for (int j = 0; j < NTE; ++j)
+        if (j < NTE - 1 || full_o) dmma(ao[j], dv, bo[j]);
+    }
+  }
+
+  const int m = m0 + fr;
+  const bool mv = (long long)m < g.M;
+  int sidx = 0, item = 0;
+  double lrow = 0.0;
+  bool pad_row = false;
+  if (mv) {
+    row_index<KMAJ>(g, m, sidx, item, pb.yld, g.Pno);
+    if (!KMAJ && (mode == FOLD_FUSED || pb.epi == EPI_LAMBDA)) {
+      const int mi = m - item * g.Mi;
+      const int p = mi - (int)((unsigned)mi / (unsigned)g.P) * g.P;
+      const unsigned i2 = (unsigned)p / (unsigned)pb.n1;
+      const int i1 = p - (int)i2 * pb.n1;
+      pad_row = i1 >= pb.n1v;
+      if (!pad_row) lrow = pb.lam1 ? pb.lam0[i1] + pb.lam1[i2] : pb.lam0[p];
+    }
+  }
+
+  if (mode == FOLD_FUSED) {
+    // spectral panel [E | O] <- y / Lambda (positions >= n keep the load's zero fill)
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < NTE; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int a = 8 * j + 2 * fc + h;
+        const bool ok = mv && !pad_row;
+        if (a < ne) Ar[a] = ok ? fdp_div(ae[j][h], lrow + pb.lamcol[a]) : 0.0;
+        if (a < no) Ar[ne + a] = ok ? fdp_div(ao[j][h], lrow + pb.lamcol[ne + a]) : 0.0;
+      }
+    __syncwarp();
+  }
+
+  if (mode == FOLD_FWD) {
+    // spectral outputs: E column a -> a, O column a -> ne + a
+    double* __restrict__ Y = pb.Y + pb.ybs * (long long)item + sidx;
+    const int ncols = KMAJ ? pb.yld : n;  // KMAJ: the row's pad columns get their zeros
+    const bool lam = pb.epi == EPI_LAMBDA;
+#pragma unroll
+    for (int j = 0; j < NTE; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int a = 8 * j + 2 * fc + h;
+        if (lam) {
+          ae[j][h] = (pad_row || a >= ne) ? 0.0 : fdp_div(ae[j][h], lrow + pb.lamcol[a]);
+          ao[j][h] = (pad_row || a >= no) ? 0.0 : fdp_div(ao[j][h], lrow + pb.lamcol[ne + a]);
+        }
+      }
+    if (!KMAJ && pb.vy) {
+      // rows (p, p+1), p even, adjacent: pair up with the partner lane (fr ^ 1)
+      const bool odd = fr & 1;
+      double* base = odd ? Y - 1 : Y;
+#pragma unroll
+      for (int j = 0; j < NTE; ++j) {
+        const int c = 8 * j + 2 * fc + (odd ? 1 : 0);
+        const double se = odd ? ae[j][0] : ae[j][1];
+        const double ge = __shfl_xor_sync(0xffffffffu, se, 4);
+        const double so = odd ? ao[j][0] : ao[j][1];
+        const double go = __shfl_xor_sync(0xffffffffu, so, 4);
+        if (mv && c < ne)
+          *reinterpret_cast<double2*>(base + (long long)g.P * c) =
+              odd ? make_double2(ge, ae[j][1]) : make_double2(ae[j][0], ge);
+        if (mv && c < no)
+          *reinterpret_cast<double2*>(base + (long long)g.P * (ne + c)) =
+              odd ? make_double2(go, ao[j][1]) : make_double2(ao[j][0], go);
+      }
+    } else if (mv) {
+      const long long cs = KMAJ ? 1 : g.P;
+#pragma unroll
+      for (int j = 0; j < NTE; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int a = 8 * j + 2 * fc + h;
+          if (a < ne) Y[cs * a] = ae[j][h];
+          if (ne + a < ncols && (a < no || KMAJ)) Y[cs * (ne + a)] = ao[j][h];
+        }
+    }
+    __syncwarp();
+    return;
+  }
+
+  // backward: e over the E part of the spectral panel, o over the O part (FOLD_SYM: e and o are
+  // the forward-style products already in ae / ao)
+  const bool tr = mode == FOLD_FUSED;  // the forward W read transposed
+  if (mode != FOLD_SYM) {
+#pragma unroll
+    for (int j = 0; j < NTE; ++j) ae[j][0] = ae[j][1] = ao[j][0] = ao[j][1] = 0.0;
+  {
+    const int k4n = (ne + 3) >> 2;
+    for (int k4 = 0; k4 < k4n; ++k4) {
+      const int k = 4 * k4 + fc;
+      const double a = Ar[k];
+      double b[NTE];
+#pragma unroll
+      for (int j = 0; j < NTE; ++j) b[j] = tr ? Ws[(8 * j + fr) * SBF + k] : Ws[k * SBF + 8 * j + fr];
+#pragma unroll
+      for (int j = 0; j < NTE; ++j) dmma(ae[j], a, b[j]);
+    }
+  }
+  {
+    const int k4n = (no + 3) >> 2;
+    for (int k4 = 0; k4 < k4n; ++k4) {
+      const int k = 4 * k4 + fc;
+      const double a = Ar[ne + k];  // <= n + 2: inside the zeroed panel row
+      double b[NTE];
+#pragma unroll
+      for (int j = 0; j < NTE; ++j) b[j] = tr ? WO[(8 * j + fr) * SBF + k] : WO[k * SBF + 8 * j + fr];
+#pragma unroll
+      for (int j = 0; j < NTE; ++j)
+        if (j < NTE - 1 || full_o) dmma(ao[j], a, b[j]);
+    }
+  }
+  }
+  // x_c = e_c + o_c, x_{n-1-c} = e_c - o_c (c < ne; the middle of an odd n is written twice with
+  // the same value)
+  const bool scale = pb.epi == EPI_SCALE;
+  const bool mid2 = tr && (n & 1);
+  double xd[NTE][2], xm[NTE][2];
+#pragma unroll
+  for (int j = 0; j < NTE; ++j)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = 8 * j + 2 * fc + h;
+      double e = ae[j][h];
+      if (mid2 && c == no) e *= 2.0;
+      double v0 = e + ao[j][h], v1 = e - ao[j][h];
+      if (scale && mv && c < ne) {
+        v0 *= pb.scale[sidx + (long long)g.P * c];
+        v1 *= pb.scale[sidx + (long long)g.P * (n - 1 - c)];
+      }
+      xd[j][h] = v0;
+      xm[j][h] = v1;
+    }
+  double* __restrict__ Y = pb.Y + pb.ybs * (long long)item + sidx;
+  if (!KMAJ && pb.vy) {
+    const bool odd = fr & 1;
+    double* base = odd ? Y - 1 : Y;
+#pragma unroll
+    for (int j = 0; j < NTE; ++j) {
+      const int c = 8 * j + 2 * fc + (odd ? 1 : 0);
+      const double sd = odd ? xd[j][0] : xd[j][1];
+      const double gd = __shfl_xor_sync(0xffffffffu, sd, 4);
+      const double sm_ = odd ? xm[j][0] : xm[j][1];
+      const double gm = __shfl_xor_sync(0xffffffffu, sm_, 4);
+      if (mv && c < ne) {
+        *reinterpret_cast<double2*>(base + (long long)g.P * c) =
+            odd ? make_double2(gd, xd[j][1]) : make_double2(xd[j][0], gd);
+        *reinterpret_cast<double2*>(base + (long long)g.P * (n - 1 - c)) =
+            odd ? make_double2(gm, xm[j][1]) : make_double2(xm[j][0], gm);
+      }
+    }
+  } else if (mv) {
+    const long long cs = KMAJ ? 1 : g.P;
+#pragma unroll
+    for (int j = 0; j < NTE; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = 8 * j + 2 * fc + h;
+        if (c < ne) {
+          Y[cs * c] = xd[j][h];
+          Y[cs * (n - 1 - c)] = xm[j][h];
+        }
+      }
+    if (KMAJ && fc == 0)
+      for (int c = n; c < pb.yld; ++c) Y[c] = 0.0;  // zero pad column of a padded row
+  }
+  __syncwarp();
+}
+
+template <int NT, bool KMAJ, int G, bool SC = false, bool FOLD = false>
 __global__ void __launch_bounds__(STH, 1) mode_small_kernel(const __grid_constant__ ModeGroupT<G> grp) {
   using S = SS<NT>;
   extern __shared__ __align__(16) double sm[];
@@ -426,7 +671,13 @@ __global__ void __launch_bounds__(STH, 1) mode_small_kernel(const __grid_constan
 
   unsigned long long* trace = grp.trace ? grp.trace + ((size_t)blockIdx.x * SW + warp) * kTracePhases : nullptr;
   if (trace && lane == 0) trace[0] = gtimer();
-  load_w<NT>(Ws, pb, tid);  // independent of the previous kernel
+  // independent of the previous kernel
+  if constexpr (FOLD) {
+    load_w_fold<NT>(Ws, pb, tid);
+    for (int i = lane; i < S::ABUF; i += 32) A[i] = 0.0;  // panel pad columns read as zeros
+  } else {
+    load_w<NT>(Ws, pb, tid);
+  }
   // PDL: everything below may read what the previous kernel wrote.
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
@@ -439,7 +690,7 @@ __global__ void __launch_bounds__(STH, 1) mode_small_kernel(const __grid_constan
   const int gw = (blockIdx.x - pb.cta_begin) + pb.ctas * warp;
   const int nw = pb.ctas * SW;
   for (long long t = gw; t < pb.tiles_m; t += nw)
-    do_tile<NT, KMAJ, false, SC>(pb, g, Ws, A, t, lane, (trace && lane == 0 && t == gw) ? trace : nullptr);
+    do_tile<NT, KMAJ, false, SC, FOLD>(pb, g, Ws, A, t, lane, (trace && lane == 0 && t == gw) ? trace : nullptr);
 }
 
 // Prefetching variant: SWP = 8 warps per CTA, two panels per warp; the next tile's panel streams
@@ -596,6 +847,10 @@ cudaError_t launch_s(const ModeGroup* g, cudaStream_t s) {
     if (e == cudaSuccess && !KMAJ)
       e = cudaFuncSetAttribute(mode_small_kernel<NT, false, kSmallGroup, true>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES);
+    if constexpr (NT % 2 == 0)
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(mode_small_kernel<NT, KMAJ, kSmallGroup, false, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES);
     if (e != cudaSuccess || bytes_prefetch<NT>() > 227 * 1024) return e;
     return cudaFuncSetAttribute(mode_small_pf_kernel<NT, KMAJ, kSmallGroup>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes_prefetch<NT>());
@@ -612,6 +867,15 @@ cudaError_t launch_s(const ModeGroup* g, cudaStream_t s) {
   cfg.numAttrs = 1;
   bool sc = false;
   for (int i = 0; i < g->count; ++i) sc = sc || g->prob[i].peers != nullptr;
+  if (g->prob[0].fold != FOLD_NONE) {  // even-odd folded group (host-checked: all problems)
+    if (sc || NT % 2 || g->count > kSmallGroup) return cudaErrorInvalidValue;
+    cfg.blockDim = dim3(STH);
+    cfg.dynamicSmemBytes = S::BYTES;
+    if constexpr (NT % 2 == 0)
+      return cudaLaunchKernelEx(&cfg, mode_small_kernel<NT, KMAJ, kSmallGroup, false, true>,
+                                narrow_group<kSmallGroup>(*g));
+    return cudaErrorInvalidValue;
+  }
   if (sc) {  // peer-store problems (slab exchange): non-KMAJ, single-buffered kernel
     if (KMAJ || g->count > kSmallGroup) return cudaErrorInvalidValue;
     cfg.blockDim = dim3(STH);

@@ -53,6 +53,45 @@ def test_fd_apply_random_pencils(dims, coef, batch):
         assert rel(x[i], ref.apply(b[i])) < TOL
 
 
+def _rand_persym_spd(n, rng, shift):
+    A = _rand_spd(n, rng, shift)
+    return 0.5 * (A + A[::-1, ::-1])  # J A J = A: the even-odd folded path takes it
+
+
+@pytest.mark.parametrize("dims,coef,batch,dscale", [
+    ((37, 70, 19), (2.0, 1.0, 1.0), 2, False),   # all folded, fused middle pass, odd/even extents
+    ((8, 9, 96), (1.0, 2.0, 1.0), 1, True),      # smallest / largest folded extents, P^G scaling
+    ((150, 67, 40), (1.0, 1.0, 2.0), 1, False),  # mode 1 dense (> 96): Lambda on a folded forward
+    ((65, 65, 65), (2.0, 1.0, 1.0), 1, True),    # config 2's velocity extent
+    ((33, 64), (1.0, 2.0), 3, False),            # 2D
+    ((7, 12, 20), (1.0, 1.0, 1.0), 1, False),    # 7 < 8 stays dense next to folded modes
+])
+def test_fd_apply_folded_persymmetric(dims, coef, batch, dscale):
+    """Even-odd folded transforms on random persymmetric SPD pencils: the folded
+    apply against the oracle's dense FD (Algorithm 1) and against the library's own dense path
+    (FDP_NO_FOLD=1)."""
+    import os
+    rng = np.random.default_rng(sum(dims) + 7 * batch)
+    Ks = [_rand_persym_spd(n, rng, 1.0) for n in dims]
+    Ms = [_rand_persym_spd(n, rng, 2.0) for n in dims]
+    N = int(np.prod(dims))
+    b = rng.standard_normal((batch, N))
+    dsc = rng.uniform(0.5, 1.5, N) if dscale else None
+    S = fdp.FD(Ks, Ms, coef)
+    kw = {"dscale": dev(1.0 / np.sqrt(dsc))} if dscale else {}
+    x = S.apply(dev(b), batch=batch, **kw).cpu().numpy()
+    os.environ["FDP_NO_FOLD"] = "1"
+    try:
+        x_dense = fdp.FD(Ks, Ms, coef).apply(dev(b), batch=batch, **kw).cpu().numpy()
+    finally:
+        del os.environ["FDP_NO_FOLD"]
+    ref = ofd.FDSolver(Ks, Ms, coef)
+    for i in range(batch):
+        r = ofd.scaled_apply(ref, b[i], dsc) if dscale else ref.apply(b[i])
+        assert rel(x[i], r) < TOL
+        assert rel(x[i], x_dense[i]) < 1e-12
+
+
 def test_fd_apply_dscale_and_inplace():
     d = ospaces.build(3, "RT", 2, 6)
     c = d.comps[1]
