@@ -230,7 +230,7 @@ extern "C" fdp_status fd_setup(int D, const int32_t* n, const double* const* K,
         cudaError_t e;
         if ((e = cudaMemcpy(raw->WfF[d], wff.data(), wff.size() * 8, cudaMemcpyHostToDevice)) ||
             (e = cudaMemcpy(raw->WbF[d], wbf.data(), wbf.size() * 8, cudaMemcpyHostToDevice)) ||
-            (e = prepare_mode_small(nt))) {
+            (e = prepare_mode_small(nt)) || (e = prepare_mode_plane(nt, 227 * 1024))) {
           free_fd(raw);
           return cuda_fail(e, "fd_setup: folded upload");
         }
@@ -602,15 +602,185 @@ long long pp_sync_ints(const std::vector<const fdp_fd_s*>& hs, int64_t batch, in
 // in[k], out[k] with batch strides ibs/obs; T[k] workspace with stride N_k. dscale[k] may be NULL.
 // Pre-scaling (if any) must already have been applied by the caller (into out[k]) and `in` point
 // at it.
+// Plane path: D = 3 and every mode of every component folded with one kernel NT
+// for modes 2 and 3; returns that NT, or 0 when the path does not apply.
+static int plane_nt(const std::vector<const fdp_fd_s*>& hs, const PresPlane* pq) {
+  if (std::getenv("FDP_NO_PLANE") || std::getenv("FDP_NO_FUSE") || std::getenv("FDP_NO_SMALL"))
+    return 0;
+  if (hs.empty() || hs.size() + (pq ? 1 : 0) > (size_t)kPlaneMax || hs[0]->D != 3) return 0;
+  const int nt = hs[0]->fold_nt[1];
+  for (const fdp_fd_s* h : hs) {
+    if (!h->fold[0] || !h->fold[1] || !h->fold[2]) return 0;
+    if (h->fold_nt[1] != nt || h->fold_nt[2] != nt || h->fold_nt[0] != hs[0]->fold_nt[0]) return 0;
+  }
+  if (pq && !(pq->q_fold[0] && pq->q_fold[1] && pq->q_fold[2])) return 0;
+  return nt;
+}
+
+static cudaError_t enqueue_fd_plane(const std::vector<const fdp_fd_s*>& hs,
+                                    const std::vector<const double*>& in, long long ibs,
+                                    const std::vector<double*>& out, long long obs,
+                                    const std::vector<double*>& T,
+                                    const std::vector<const double*>& dscale, int64_t batch,
+                                    int nt, cudaStream_t s, int* nlaunch, Recorder* rec,
+                                    const PresPlane* pq) {
+  const size_t K = hs.size();
+  // L1: mode-1 forward, plane-major output (velocity into T[k], pressure M_1^{-1} into Tq)
+  {
+    std::vector<ModeProb> probs;
+    std::vector<TileCfg> cfgs;
+    for (size_t k = 0; k < K; ++k) {
+      const fdp_fd_s* h = hs[k];
+      ModeProb p = make_mode_prob(h, 0, true, in[k], ibs, T[k], Npad(h), batch, EPI_NONE, nullptr,
+                                  h->n[0], h->n[0]);
+      p.tio = TIO_OUT_T;
+      p.vy = 0;
+      probs.push_back(p);
+      TileCfg c = h->cfg[0];
+      c.NT = h->fold_nt[0];
+      cfgs.push_back(c);
+    }
+    if (pq) {
+      ModeProb p{};
+      p.X = pq->rq;
+      p.xbs = pq->rbs;
+      p.Y = pq->Tq;
+      p.ybs = pq->tqbs;
+      p.W = pq->Wq[0];
+      p.ldw = pq->q_ldw[0];
+      p.foldh = pq->q_foldh[0];
+      p.fold = FOLD_SYM;
+      p.tio = TIO_OUT_T;
+      p.N = (long long)pq->n[0] * pq->n[1] * pq->n[2];
+      p.P = 1;
+      p.n = p.nout = pq->n[0];
+      p.Q = pq->n[1] * pq->n[2];
+      p.batch = (int)batch;
+      p.n1 = p.n1v = pq->n[0];
+      p.xld = p.yld = pq->n[0];
+      p.tiles_n = 1;
+      probs.push_back(p);
+      cfgs.push_back(cfgs[0]);
+    }
+    cudaError_t e = launch_stage(probs, cfgs, true, s, nlaunch, rec);
+    if (e != cudaSuccess) return e;
+  }
+  // L2: the planes
+  {
+    PlaneGroup g{};
+    int sp = 4, rows = 8, begin = 0;
+    double fl = 0.0, by = 0.0;
+    for (size_t k = 0; k < K; ++k) {
+      const fdp_fd_s* h = hs[k];
+      PlaneProb& q = g.prob[g.count++];
+      q.T = T[k];
+      q.tbs = Npad(h);
+      q.W2 = h->WfF[1];
+      q.W3 = h->WfF[2];
+      q.ldw2 = h->ldwF[1];
+      q.foldh2 = h->foldh[1];
+      q.ldw3 = h->ldwF[2];
+      q.foldh3 = h->foldh[2];
+      q.lam1 = h->lamcF[0];
+      q.lam2 = h->lamcF[1];
+      q.lam3 = h->lamcF[2];
+      q.n1 = h->n[0];
+      q.n2 = h->n[1];
+      q.n3 = h->n[2];
+      q.batch = (int)batch;
+      q.sp = plane_stride(q.n2);
+      q.kind = 0;
+      q.plane_begin = begin;
+      begin += q.n1 * (int)batch;
+      sp = std::max(sp, q.sp);
+      rows = std::max(rows, q.n3);  // full tiles and leftover rows never read past row n3
+      fl += 2.0 * h->N * batch * (2.0 * h->n[1] + 2.0 * h->n[2]);
+      by += 16.0 * h->N * batch;
+    }
+    if (pq) {
+      PlaneProb& q = g.prob[g.count++];
+      q.T = pq->Tq;
+      q.tbs = pq->tqbs;
+      q.W2 = pq->Wq[1];
+      q.W3 = pq->Wq[2];
+      q.ldw2 = pq->q_ldw[1];
+      q.foldh2 = pq->q_foldh[1];
+      q.ldw3 = pq->q_ldw[2];
+      q.foldh3 = pq->q_foldh[2];
+      q.n1 = pq->n[0];
+      q.n2 = pq->n[1];
+      q.n3 = pq->n[2];
+      q.batch = (int)batch;
+      q.sp = plane_stride(q.n2);
+      q.kind = 1;
+      q.Y = pq->out;
+      q.ybs = pq->obs;
+      q.scale = pq->scale;
+      q.plane_begin = begin;
+      begin += q.n1 * (int)batch;
+      sp = std::max(sp, q.sp);
+      rows = std::max(rows, q.n3);
+      by += 16.0 * pq->n[0] * pq->n[1] * pq->n[2] * batch;
+    }
+    g.total = begin;
+    g.dmma_tail = std::getenv("FDP_PLANE_DMMA_TAIL") != nullptr;
+    if (g.dmma_tail) rows = ((rows + 7) / 8) * 8 + 8;  // the ragged tile reads rows < round8 + 8
+    const size_t smem = plane_smem_bytes(nt, sp, rows);
+    if (smem > 227 * 1024) return cudaErrorInvalidValue;
+    const int per_sm = smem <= 112 * 1024 ? 2 : 1;
+    g.grid = std::min(g.total, per_sm * num_sms());
+    if (rec) {
+      cudaError_t e0 = rec->before(0, fl, by);
+      if (e0 != cudaSuccess) return e0;
+    }
+    g.trace = nullptr;
+    if (g_trace) {
+      const size_t need = (size_t)g.grid * 8;
+      if (g_trace_used + need <= g_trace_cap) {
+        g.trace = g_trace + g_trace_used;
+        g_trace_used += need;
+      }
+    }
+    cudaError_t e = launch_mode_plane(g, nt, smem, s);
+    if (e != cudaSuccess) return e;
+    if (nlaunch) ++*nlaunch;
+  }
+  // L3: mode-1 backward reading the plane-major tensor (P = n2 n3, Q = 1), natural-layout output
+  {
+    std::vector<ModeProb> probs;
+    std::vector<TileCfg> cfgs;
+    for (size_t k = 0; k < K; ++k) {
+      const fdp_fd_s* h = hs[k];
+      const bool sc = dscale[k] != nullptr;
+      ModeProb p = make_mode_prob(h, 0, false, T[k], Npad(h), out[k], obs, batch,
+                                  sc ? EPI_SCALE : EPI_NONE, dscale[k], h->n[0], h->n[0]);
+      p.P = h->n[1] * h->n[2];
+      p.Q = 1;
+      p.vx = p.vy = 0;
+      p.tio = TIO_OUT_K;
+      probs.push_back(p);
+      TileCfg c = h->cfg[0];
+      c.NT = h->fold_nt[0];
+      cfgs.push_back(c);
+    }
+    cudaError_t e = launch_stage(probs, cfgs, false, s, nlaunch, rec);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 cudaError_t enqueue_fd(const std::vector<const fdp_fd_s*>& hs,
                               const std::vector<const double*>& in, long long ibs,
                               const std::vector<double*>& out, long long obs,
                               const std::vector<double*>& T,
                               const std::vector<const double*>& dscale, int64_t batch,
                               cudaStream_t s, int* nlaunch, Recorder* rec, const StageHook& hook, int* sync,
-                              long long sync_cap) {
+                              long long sync_cap, const PresPlane* pq) {
   const int D = hs[0]->D;
   const size_t K = hs.size();
+  if (const int nt = plane_nt(hs, pq); nt > 0 && (pq || !hook) &&
+                                       (long long)hs[0]->N * batch < (1LL << 31))
+    return enqueue_fd_plane(hs, in, ibs, out, obs, T, dscale, batch, nt, s, nlaunch, rec, pq);
   // Stage list: forward d = 0..D-1, backward d = D-1..0. When every mode of every component is
   // small (single column tile, n <= 96) the mode-D forward / Lambda / mode-D backward triple is
   // one fused pass. Destinations alternate so that the last pass lands in `out`.

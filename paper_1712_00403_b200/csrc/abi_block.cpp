@@ -253,8 +253,24 @@ static cudaError_t enqueue_block(fdp_block h, const double* r, double* s, int64_
   }
   const long long need = 2 * pp_sync_ints(h->vel, batch, h->pres_dense && D == 3 ? h->pres->n[2] : 0);
   const bool sy = h->sync && h->sync_cap >= need;
+  PresPlane pq{};
+  const bool pplane = h->pres_dense && D == 3;
+  if (pplane) {
+    pq.n = h->pres->n;
+    pq.rq = rq;
+    pq.rbs = sz;
+    pq.Tq = Tq1;
+    pq.tqbs = nq;
+    pq.out = s + h->off[D];
+    pq.obs = sz;
+    pq.scale = h->dall ? h->dall + h->off[D] : nullptr;
+    pq.Wq = h->Wq;
+    pq.q_ldw = h->q_ldw;
+    pq.q_foldh = h->q_foldh;
+    pq.q_fold = h->q_fold;
+  }
   cudaError_t e = enqueue_fd(h->vel, in, sz, out, sz, T, dsc, batch, st, nlaunch, rec, hook,
-                             sy ? h->sync : nullptr, sy ? need : 0);
+                             sy ? h->sync : nullptr, sy ? need : 0, pplane ? &pq : nullptr);
   if (e != cudaSuccess) return e;
   if (!h->pres_dense) {
     // pressure block by banded per-mode solves: r_p -> s_p

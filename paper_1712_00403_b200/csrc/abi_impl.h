@@ -267,6 +267,23 @@ using StageHook = std::function<void(int pass, bool fwd, int d, std::vector<Mode
 cudaError_t launch_stage(std::vector<ModeProb>& probs_in, const std::vector<TileCfg>& cfgs_in,
                          bool kmaj, cudaStream_t s, int* nlaunch, Recorder* rec);
 long long pp_sync_ints(const std::vector<const fdp_fd_s*>& hs, int64_t batch, int extra_n3);
+// Dense P_Q riding in the plane path (D = 3, every M_d^{-1} folded): mode 1 (FOLD_SYM, plane-major
+// output into Tq) joins the velocity mode-1 forward launch, modes 2 and 3 are planes of kind 1
+// in the plane launch, which stores s_p (optionally scaled) at out.
+struct PresPlane {
+  const int* n;                   // pressure extents n[0..2]
+  const double* rq;
+  long long rbs;
+  double* Tq;
+  long long tqbs;
+  double* out;
+  long long obs;
+  const double* scale;
+  double* const* Wq;
+  const int* q_ldw;
+  const int* q_foldh;
+  const int* q_fold;
+};
 cudaError_t enqueue_fd(const std::vector<const fdp_fd_s*>& hs,
                        const std::vector<const double*>& in, long long ibs,
                        const std::vector<double*>& out, long long obs,
@@ -274,7 +291,7 @@ cudaError_t enqueue_fd(const std::vector<const fdp_fd_s*>& hs,
                        const std::vector<const double*>& dscale, int64_t batch,
                        cudaStream_t s, int* nlaunch, Recorder* rec = nullptr,
                        const StageHook& hook = nullptr, int* sync = nullptr,
-                       long long sync_cap = 0);
+                       long long sync_cap = 0, const PresPlane* pq = nullptr);
 cudaError_t enqueue_mass(const fdp_mass_s* h, int mode, const double* in, double* out,
                          long long bs, const double* dscale, int64_t batch, cudaStream_t s,
                          int* nlaunch, Recorder* rec = nullptr);

@@ -24,6 +24,8 @@ namespace fdp {
 // FOLD_SYM: y = A x for a centrosymmetric A (J A J = A) in one folded pass (dense P_Q^{-1} modes)
 enum Fold : int { FOLD_NONE = 0, FOLD_FWD = 1, FOLD_BWD = 2, FOLD_FUSED = 3, FOLD_SYM = 4 };
 
+enum TransIO : int { TIO_NONE = 0, TIO_OUT_T = 1, TIO_OUT_K = 2 };
+
 enum Epilogue : int {
   EPI_NONE = 0,
   EPI_LAMBDA = 1,  // divide by Lambda[i] = lamrow(p) + lamcol[a]   (Algorithm 1 step 3)
@@ -62,6 +64,11 @@ struct ModeProb {
   // and the mode's spectral index runs over [E (ceil(n/2)) | O (floor(n/2))].
   int fold;
   int foldh;
+  // Transposed I/O of the plane path (folded problems only): TIO_OUT_T (KMAJ
+  // kernel): output row m, column a at Y[item * ybs + mi + Mi * a] (the plane-major layout, mi the
+  // row within its item, Mi = P * Q rows per item); TIO_OUT_K (non-KMAJ kernel reading a
+  // plane-major tensor as P = Mi, Q = 1): output at Y[item * ybs + yld * mi + a].
+  int tio;
   // Peer-store scatter (slab exchange fused into the epilogue): when peers != NULL,
   // output element (GEMM row m, column a) of a batch-1, non-KMAJ problem is stored at
   // peers[o] + r + sc_n1 * ((a - lo_o) * (sc_a0 + sc_a1 * len_o) + (q + sc_qoff) * (sc_q0 + sc_q1 * len_o))
@@ -169,6 +176,43 @@ cudaError_t launch_mode_pp(const ModeGroup& g1, const ModeGroup& g2, const Plane
 // Folded problems (prob.fold != 0, every problem of the group) take the even-odd kernel; NT is
 // then 2 * ceil(ceil(n/2) / 8) (even).
 cudaError_t launch_mode_small(const ModeGroup& g, int NT, bool kmaj, cudaStream_t s);
+
+// Plane kernel (D = 3, kernels/mode_plane.cu): per plane a1 of a plane-major tensor (written by a
+// TIO_OUT_T mode-1 pass), the folded mode-2 forward, mode-3 forward / Lambda^{-1} / backward and
+// mode-2 backward in shared memory (kind 0, in place), or the FOLD_SYM mode-2 and mode-3 passes
+// of P_Q with the result stored in the natural layout (kind 1).
+struct PlaneProb {
+  double* T;              // plane-major tensor: item b, plane a1 at T + b * tbs + a1 * n2 * n3
+  long long tbs;
+  const double* W2;       // folded forward (kind 0) or FOLD_SYM (kind 1) matrices, global layout
+  const double* W3;
+  int ldw2, foldh2, ldw3, foldh3;
+  const double* lam1;     // kind 0: coef-scaled eigenvalues, folded spectral order
+  const double* lam2;
+  const double* lam3;
+  int n1, n2, n3, batch;
+  int sp;                 // shared-memory row stride of the plane
+  int kind;
+  double* Y;              // kind 1: output (natural layout), batch stride ybs, optional scale
+  long long ybs;
+  const double* scale;
+  int plane_begin;        // first plane of this problem in the grouped grid
+};
+constexpr int kPlaneMax = 8;
+struct PlaneGroup {
+  PlaneProb prob[kPlaneMax];
+  int count;
+  int total;              // planes over all problems
+  int grid;               // CTAs (persistent over planes)
+  // diagnostics: thread 0 of every CTA records %globaltimer at 8 points of its first plane into
+  // trace[blockIdx * 8 + point] when non-null
+  unsigned long long* trace;
+  int dmma_tail;          // experiment (FDP_PLANE_DMMA_TAIL=1): ragged last tile on the DMMA pipe
+};
+size_t plane_smem_bytes(int NT, int sp, int rows);
+int plane_stride(int n2);
+cudaError_t launch_mode_plane(const PlaneGroup& g, int NT, size_t smem, cudaStream_t s);
+cudaError_t prepare_mode_plane(int NT, size_t smem);
 cudaError_t prepare_mode_small(int NT);
 
 // y[b*ys + i] = x[b*xs + i] * s[i], i < N  (P^G pre-scaling), over `batch` items.

@@ -142,7 +142,7 @@ __device__ __forceinline__ void tile_compute_store(const ModeProb& pb, const Geo
 template <int NT, bool KMAJ>
 __device__ __forceinline__ void tile_compute_store_fold(const ModeProb& pb, const Geo& g,
                                                         const double* Ws, double* A, long long t,
-                                                        int lane);
+                                                        int lane, unsigned long long* tr);
 
 // Asynchronous panel load (8-byte cp.async with zero fill beyond n / M) into A ([8][SA]); one
 // commit group.
@@ -290,7 +290,7 @@ __device__ __forceinline__ void do_tile(const ModeProb& pb, const Geo& g, const 
   __syncwarp();
   if (tr) tr[3] = gtimer();
   if constexpr (FOLD)
-    tile_compute_store_fold<NT, KMAJ>(pb, g, Ws, A, t, lane);
+    tile_compute_store_fold<NT, KMAJ>(pb, g, Ws, A, t, lane, tr);
   else
     tile_compute_store<NT, KMAJ, SC>(pb, g, Ws, A, t, lane, tr);
 }
@@ -451,7 +451,7 @@ __device__ __forceinline__ void tile_compute_store(const ModeProb& pb, const Geo
 template <int NT, bool KMAJ>
 __device__ __forceinline__ void tile_compute_store_fold(const ModeProb& pb, const Geo& g,
                                                         const double* Ws, double* A, long long t,
-                                                        int lane) {
+                                                        int lane, unsigned long long* tr) {
   using S = SS<NT>;
   constexpr int NTE = NT / 2;
   constexpr int SBF = S::SBF;
@@ -518,10 +518,21 @@ __device__ __forceinline__ void tile_compute_store_fold(const ModeProb& pb, cons
     __syncwarp();
   }
 
+  // output addressing: row base sidx, column stride cs; kout = rows are contiguous in the output
+  long long cs = KMAJ ? 1 : g.P;
+  bool kout = KMAJ;
+  if (pb.tio != TIO_NONE && mv) {
+    const int mi = m - item * g.Mi;
+    if (pb.tio == TIO_OUT_T) { sidx = mi; cs = g.Mi; kout = false; }
+    else { sidx = pb.yld * mi; cs = 1; kout = true; }
+  }
+  const bool vrow = !KMAJ && pb.vy && pb.tio == TIO_NONE;  // 16-byte row-pair stores
+
   if (mode == FOLD_FWD) {
+    if (tr) tr[4] = gtimer();
     // spectral outputs: E column a -> a, O column a -> ne + a
     double* __restrict__ Y = pb.Y + pb.ybs * (long long)item + sidx;
-    const int ncols = KMAJ ? pb.yld : n;  // KMAJ: the row's pad columns get their zeros
+    const int ncols = kout ? pb.yld : n;  // row-major rows: their pad columns get their zeros
     const bool lam = pb.epi == EPI_LAMBDA;
 #pragma unroll
     for (int j = 0; j < NTE; ++j)
@@ -533,7 +544,7 @@ __device__ __forceinline__ void tile_compute_store_fold(const ModeProb& pb, cons
           ao[j][h] = (pad_row || a >= no) ? 0.0 : fdp_div(ao[j][h], lrow + pb.lamcol[ne + a]);
         }
       }
-    if (!KMAJ && pb.vy) {
+    if (vrow) {
       // rows (p, p+1), p even, adjacent: pair up with the partner lane (fr ^ 1)
       const bool odd = fr & 1;
       double* base = odd ? Y - 1 : Y;
@@ -552,23 +563,23 @@ __device__ __forceinline__ void tile_compute_store_fold(const ModeProb& pb, cons
               odd ? make_double2(go, ao[j][1]) : make_double2(ao[j][0], go);
       }
     } else if (mv) {
-      const long long cs = KMAJ ? 1 : g.P;
 #pragma unroll
       for (int j = 0; j < NTE; ++j)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int a = 8 * j + 2 * fc + h;
           if (a < ne) Y[cs * a] = ae[j][h];
-          if (ne + a < ncols && (a < no || KMAJ)) Y[cs * (ne + a)] = ao[j][h];
+          if (ne + a < ncols && (a < no || kout)) Y[cs * (ne + a)] = ao[j][h];
         }
     }
     __syncwarp();
+    if (tr) tr[5] = gtimer();
     return;
   }
 
   // backward: e over the E part of the spectral panel, o over the O part (FOLD_SYM: e and o are
   // the forward-style products already in ae / ao)
-  const bool tr = mode == FOLD_FUSED;  // the forward W read transposed
+  const bool trw = mode == FOLD_FUSED;  // the forward W read transposed
   if (mode != FOLD_SYM) {
 #pragma unroll
     for (int j = 0; j < NTE; ++j) ae[j][0] = ae[j][1] = ao[j][0] = ao[j][1] = 0.0;
@@ -579,7 +590,7 @@ __device__ __forceinline__ void tile_compute_store_fold(const ModeProb& pb, cons
       const double a = Ar[k];
       double b[NTE];
 #pragma unroll
-      for (int j = 0; j < NTE; ++j) b[j] = tr ? Ws[(8 * j + fr) * SBF + k] : Ws[k * SBF + 8 * j + fr];
+      for (int j = 0; j < NTE; ++j) b[j] = trw ? Ws[(8 * j + fr) * SBF + k] : Ws[k * SBF + 8 * j + fr];
 #pragma unroll
       for (int j = 0; j < NTE; ++j) dmma(ae[j], a, b[j]);
     }
@@ -591,17 +602,18 @@ __device__ __forceinline__ void tile_compute_store_fold(const ModeProb& pb, cons
       const double a = Ar[ne + k];  // <= n + 2: inside the zeroed panel row
       double b[NTE];
 #pragma unroll
-      for (int j = 0; j < NTE; ++j) b[j] = tr ? WO[(8 * j + fr) * SBF + k] : WO[k * SBF + 8 * j + fr];
+      for (int j = 0; j < NTE; ++j) b[j] = trw ? WO[(8 * j + fr) * SBF + k] : WO[k * SBF + 8 * j + fr];
 #pragma unroll
       for (int j = 0; j < NTE; ++j)
         if (j < NTE - 1 || full_o) dmma(ao[j], a, b[j]);
     }
   }
   }
+  if (tr) tr[4] = gtimer();
   // x_c = e_c + o_c, x_{n-1-c} = e_c - o_c (c < ne; the middle of an odd n is written twice with
   // the same value)
   const bool scale = pb.epi == EPI_SCALE;
-  const bool mid2 = tr && (n & 1);
+  const bool mid2 = trw && (n & 1);
   double xd[NTE][2], xm[NTE][2];
 #pragma unroll
   for (int j = 0; j < NTE; ++j)
@@ -612,14 +624,14 @@ __device__ __forceinline__ void tile_compute_store_fold(const ModeProb& pb, cons
       if (mid2 && c == no) e *= 2.0;
       double v0 = e + ao[j][h], v1 = e - ao[j][h];
       if (scale && mv && c < ne) {
-        v0 *= pb.scale[sidx + (long long)g.P * c];
-        v1 *= pb.scale[sidx + (long long)g.P * (n - 1 - c)];
+        v0 *= pb.scale[sidx + cs * c];
+        v1 *= pb.scale[sidx + cs * (n - 1 - c)];
       }
       xd[j][h] = v0;
       xm[j][h] = v1;
     }
   double* __restrict__ Y = pb.Y + pb.ybs * (long long)item + sidx;
-  if (!KMAJ && pb.vy) {
+  if (vrow) {
     const bool odd = fr & 1;
     double* base = odd ? Y - 1 : Y;
 #pragma unroll
@@ -637,7 +649,6 @@ __device__ __forceinline__ void tile_compute_store_fold(const ModeProb& pb, cons
       }
     }
   } else if (mv) {
-    const long long cs = KMAJ ? 1 : g.P;
 #pragma unroll
     for (int j = 0; j < NTE; ++j)
 #pragma unroll
@@ -648,10 +659,11 @@ __device__ __forceinline__ void tile_compute_store_fold(const ModeProb& pb, cons
           Y[cs * (n - 1 - c)] = xm[j][h];
         }
       }
-    if (KMAJ && fc == 0)
+    if (kout && fc == 0)
       for (int c = n; c < pb.yld; ++c) Y[c] = 0.0;  // zero pad column of a padded row
   }
   __syncwarp();
+  if (tr) tr[5] = gtimer();
 }
 
 template <int NT, bool KMAJ, int G, bool SC = false, bool FOLD = false>

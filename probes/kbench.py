@@ -48,9 +48,12 @@ if __name__ == "__main__":
     cid = int(sys.argv[1]) if len(sys.argv) > 1 else 2
     batches = [int(x) for x in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["1", "4"])]
     variants = [{}, {"FDP_NO_FUSE": "1"}, {"FDP_NO_SMALL": "1"}]
+    if len(sys.argv) > 3:
+        variants = json.loads(sys.argv[3])
     for var in variants:
-        for k in ("FDP_NO_FUSE", "FDP_NO_SMALL", "FDP_PRESSURE"):
-            os.environ.pop(k, None)
+        for k in list(os.environ):
+            if k.startswith("FDP_"):
+                os.environ.pop(k, None)
         os.environ.update(var)
         for bt in batches:
             ms, prof, nl = run(cid, bt)

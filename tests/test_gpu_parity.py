@@ -243,7 +243,8 @@ def test_block_precond_config4_full_size_bench_launch():
 
 
 @pytest.mark.parametrize("env", [{"FDP_NO_SMALL": "1"}, {"FDP_NO_FUSE": "1"}, {"FDP_PRESSURE": "banded"},
-                                 {"FDP_PRESSURE": "dense"}, {"FDP_PP": "1"}, {"FDP_SMALL_PF": "1"}, {}])
+                                 {"FDP_PRESSURE": "dense"}, {"FDP_PP": "1"}, {"FDP_SMALL_PF": "1"},
+                                 {"FDP_NO_FOLD": "1"}, {"FDP_NO_PLANE": "1"}, {}])
 @pytest.mark.parametrize("cfg_id", [1, 2, 3])
 def test_block_precond_kernel_paths(cfg_id, env, monkeypatch):
     """Every kernel path (big/small K1, fused middle, banded/dense P_Q) against the oracle."""
