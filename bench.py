@@ -462,6 +462,10 @@ def main():
                 k3_ms += ms
                 k3_by += by
     achieved = (k1_fl / (k1_ms * 1e-3)) / 1e12 if k1_ms > 0 else None
+    # the dense FD's work (4 N_k sum_d n_d per component and RHS) at the same
+    # K1 time: what the even-odd folding saves shows as dense_equiv > achieved
+    dense_fl = sum(4.0 * float(np.prod(d)) * sum(d) for d in gd.comp_dims) * batch_total / world
+    dense_equiv = (dense_fl * len(prof_runs) / (k1_ms * 1e-3)) / 1e12 if k1_ms > 0 else None
     # DRAM traffic per K1 launch from the committed ncu --set full capture of this config
     traffic = traffic_src = None
     ncu_json = os.path.join(ROOT, "profiles", f"r01_ncu_cfg{cid}.json")
@@ -523,11 +527,18 @@ def main():
                                   else "working set > L2"),
         "roofline": {
             "bound": "tensor",
-            "kernel": "K1 mode_contract (FP64 mma.sync m8n8k4 -> DMMA)",
+            "kernel": "K1 family: the FD transform launches (mode_small / mode_plane / "
+                      "mode_contract; FP64 mma.sync m8n8k4 -> DMMA)",
             "achieved": achieved,
             "peak": fp64_peak,
             "unit": "TFLOP/s",
             "frac": (achieved / fp64_peak) if achieved else None,
+            "flops_counted": "as executed: 2 R (ne^2 + no^2) per folded m-mode product, 2 R n^2 "
+                             "per dense one (DESIGN.md §8)",
+            "dense_fd_equiv": {"achieved": dense_equiv,
+                               "frac": (dense_equiv / fp64_peak) if dense_equiv else None,
+                               "flops_per_apply": dense_fl / max(1, batch_total / world),
+                               "source": "SURVEY.md §8(d) D-4 dense FD flops over the same K1 time"},
             "traffic": traffic,
             "traffic_source": traffic_src,
             "peak_source": "measured all-SM DMMA register loop, profiles/r01_fp64_peaks.json (MEASURED_PEAKS.json has no FP64 entry)",

@@ -82,8 +82,8 @@ void fold_sym_matrix(int n, const double* A, int foldh, int ldw, std::vector<dou
 // Folded eigen-data of a persymmetric pencil: forward / backward matrices in the folded layout and
 // coef * [lambda_E | lambda_O].
 static int fold_eig(int n, const double* K, const double* M, double coef, int foldh, int ldw,
-                    std::vector<double>* wf, std::vector<double>* wb, std::vector<double>* lam,
-                    std::string* err) {
+                    int ldwb, std::vector<double>* wf, std::vector<double>* wb,
+                    std::vector<double>* lam, std::string* err) {
   const int ne = (n + 1) / 2, no = n / 2;
   const double r2 = std::sqrt(0.5);
   std::vector<double> KE = fold_block(n, K, 1), ME = fold_block(n, M, 1);
@@ -93,20 +93,20 @@ static int fold_eig(int n, const double* K, const double* M, double coef, int fo
   if (!st && no > 0) st = gen_eig(no, KO.data(), MO.data(), VO.data(), lO.data(), err);
   if (st) return st;
   wf->assign((size_t)2 * foldh * ldw, 0.0);
-  wb->assign((size_t)2 * foldh * ldw, 0.0);
+  wb->assign((size_t)2 * foldh * ldwb, 0.0);
   // forward W_E[k][a] = V_E[k][a] / sqrt2 (k < no), V_E[h][a] / 2 (middle: s_h = 2 x_h);
   // backward W_E[a][c] = V_E[c][a] / sqrt2 (c < no), V_E[h][a] (middle)
   for (int k = 0; k < ne; ++k)
     for (int a = 0; a < ne; ++a) {
       const double v = VE[k + (size_t)ne * a];
       (*wf)[(size_t)k * ldw + a] = k == no ? 0.5 * v : r2 * v;
-      (*wb)[(size_t)a * ldw + k] = k == no ? v : r2 * v;
+      (*wb)[(size_t)a * ldwb + k] = k == no ? v : r2 * v;
     }
   for (int k = 0; k < no; ++k)
     for (int a = 0; a < no; ++a) {
       const double v = r2 * VO[k + (size_t)no * a];
       (*wf)[(size_t)(foldh + k) * ldw + a] = v;
-      (*wb)[(size_t)(foldh + a) * ldw + k] = v;
+      (*wb)[(size_t)(foldh + a) * ldwb + k] = v;
     }
   lam->resize(n);
   for (int a = 0; a < ne; ++a) (*lam)[a] = coef * lE[a];
@@ -202,26 +202,51 @@ extern "C" fdp_status fd_setup(int D, const int32_t* n, const double* const* K,
         free_fd(raw);
         return st;
       }
-      // folded copy (small-path extents with a persymmetric pencil; FDP_NO_FOLD=1 disables)
-      const bool can_fold = std::getenv("FDP_NO_FOLD") == nullptr &&
-                            std::getenv("FDP_NO_SMALL") == nullptr && nd >= 8 && nd <= kSmallMaxN &&
-                            c.tiles_n == 1 && persymmetric(nd, K[d], 1e-12) &&
-                            persymmetric(nd, M[d], 1e-12);
+      // folded copy for a persymmetric pencil (FDP_NO_FOLD=1 disables): small-path extents use
+      // the small kernels (fold 1), larger ones the folded K1 kernels (fold 2)
+      const bool persym = std::getenv("FDP_NO_FOLD") == nullptr && nd >= 8 &&
+                          persymmetric(nd, K[d], 1e-12) && persymmetric(nd, M[d], 1e-12);
+      const bool small_fold = persym && std::getenv("FDP_NO_SMALL") == nullptr &&
+                              nd <= kSmallMaxN && c.tiles_n == 1;
+      const bool k1_fold = persym && !small_fold && nd > kSmallMaxN;
       std::vector<double> lcf = lc;
-      if (can_fold) {
-        const int nt = fold_nt(nd);
-        const int foldh = 4 * nt, ldwf = 4 * nt;  // KPF rows / 8 * NTE columns of the kernel
+      if (small_fold || k1_fold) {
+        int nt = 0, foldh, ldwf, ldwb;
+        if (small_fold) {
+          nt = fold_nt(nd);
+          foldh = ldwf = ldwb = 4 * nt;  // KPF rows / 8 * NTE columns of the kernel
+        } else {
+          const int ne = (nd + 1) / 2, no = nd / 2;
+          TileCfg cf{}, cb{};
+          const int n8e = (ne + 7) / 8, n8o = (no + 7) / 8;
+          cf.MT = cb.MT = 2;
+          cf.NT = (n8e + (n8e + 11) / 12 - 1) / ((n8e + 11) / 12);   // <= 12 n8-tiles per column tile
+          const int te = (n8e + cf.NT - 1) / cf.NT, to = (n8o + cf.NT - 1) / cf.NT;
+          cf.tiles_n = te + to;
+          cf.ldw = std::max(te, to) * 8 * cf.NT;
+          cb.NT = (n8e + (n8e + 5) / 6 - 1) / ((n8e + 5) / 6);       // <= 6: two accumulator sets
+          cb.tiles_n = (n8e + cb.NT - 1) / cb.NT;
+          cb.ldw = cb.tiles_n * 8 * cb.NT;
+          cf.kpad = cb.kpad = c.kpad;
+          raw->cfgFf[d] = cf;
+          raw->cfgFb[d] = cb;
+          raw->tiles_ne[d] = te;
+          foldh = ((ne + 31) / 32) * 32;
+          ldwf = cf.ldw;
+          ldwb = cb.ldw;
+        }
         std::vector<double> wff, wbf;
         std::string err;
-        const int fst = fold_eig(nd, K[d], M[d], coef[d], foldh, ldwf, &wff, &wbf, &lcf, &err);
+        const int fst = fold_eig(nd, K[d], M[d], coef[d], foldh, ldwf, ldwb, &wff, &wbf, &lcf, &err);
         if (fst) {
           free_fd(raw);
           return fail((fdp_status)fst, "fd_setup (folded): " + err);
         }
-        raw->fold[d] = 1;
+        raw->fold[d] = small_fold ? 1 : 2;
         raw->fold_nt[d] = nt;
         raw->foldh[d] = foldh;
         raw->ldwF[d] = ldwf;
+        raw->ldwFb[d] = ldwb;
         fdp_status fs;
         if ((fs = dalloc(&raw->WfF[d], wff.size())) || (fs = dalloc(&raw->WbF[d], wbf.size()))) {
           free_fd(raw);
@@ -230,7 +255,8 @@ extern "C" fdp_status fd_setup(int D, const int32_t* n, const double* const* K,
         cudaError_t e;
         if ((e = cudaMemcpy(raw->WfF[d], wff.data(), wff.size() * 8, cudaMemcpyHostToDevice)) ||
             (e = cudaMemcpy(raw->WbF[d], wbf.data(), wbf.size() * 8, cudaMemcpyHostToDevice)) ||
-            (e = prepare_mode_small(nt)) || (e = prepare_mode_plane(nt, 227 * 1024))) {
+            (e = small_fold ? prepare_mode_small(nt) : prepare_mode_kernels(raw->cfgFf[d])) ||
+            (e = small_fold ? prepare_mode_plane(nt, 227 * 1024) : prepare_mode_kernels(raw->cfgFb[d]))) {
           free_fd(raw);
           return cuda_fail(e, "fd_setup: folded upload");
         }
@@ -405,17 +431,22 @@ static ModeProb make_mode_prob(const fdp_fd_s* h, int d, bool fwd, const double*
     p.lam1 = h->D == 3 ? h->lamcF[1] : nullptr;
     p.lamcol = h->lamcF[h->D - 1];
   }
-  if (h->fold[d]) {
-    p.fold = epi == EPI_FUSED ? FOLD_FUSED : (fwd ? FOLD_FWD : FOLD_BWD);
-    p.W = fwd ? h->WfF[d] : h->WbF[d];
-    p.ldw = h->ldwF[d];
-    p.foldh = h->foldh[d];
-  }
   const int BM = kK1Warps * 8 * h->cfg[d].MT;
   const long long M = P * Q * batch;
   p.tiles_m = (int)((M + BM - 1) / BM);
   p.tiles_n = h->cfg[d].tiles_n;
   p.fd_work = 1;
+  if (h->fold[d]) {
+    p.fold = epi == EPI_FUSED ? FOLD_FUSED : (fwd ? FOLD_FWD : FOLD_BWD);
+    p.W = fwd ? h->WfF[d] : h->WbF[d];
+    p.ldw = fwd ? h->ldwF[d] : h->ldwFb[d];
+    p.foldh = h->foldh[d];
+    if (h->fold[d] == 2) {
+      p.fold_k1 = 1;
+      p.tiles_n = fwd ? h->cfgFf[d].tiles_n : h->cfgFb[d].tiles_n;
+      p.tiles_ne = h->tiles_ne[d];
+    }
+  }
   return p;
 }
 
@@ -458,9 +489,14 @@ static bool small_ok(const ModeProb& p) {
 }
 
 static double recorded_flops(const ModeProb& p) {
-  const double elems = (double)p.P * p.Q * p.batch * p.n;
-  // dense-inverse pressure passes ride along but are not FD work: count their bytes only
-  return p.fd_work ? (p.epi == EPI_FUSED ? 4.0 : 2.0) * elems * p.n : 0.0;
+  // algorithmic FLOPs of the transform as executed: dense 2 R n^2 per m-mode product (R = rows),
+  // folded 2 R (ne^2 + no^2); dense-inverse pressure passes ride along but are
+  // not FD work: their bytes only
+  if (!p.fd_work) return 0.0;
+  const double rows = (double)p.P * p.Q * p.batch;
+  const double ne = (p.n + 1) / 2, no = p.n / 2;
+  const double per = p.fold ? 2.0 * rows * (ne * ne + no * no) : 2.0 * rows * p.n * p.n;
+  return (p.epi == EPI_FUSED ? 2.0 : 1.0) * per;
 }
 static double recorded_bytes(const ModeProb& p) {
   const double elems = (double)p.P * p.Q * p.batch * p.n;
@@ -489,7 +525,8 @@ cudaError_t launch_stage(std::vector<ModeProb>& probs_in, const std::vector<Tile
     int ctas = 0;
     for (size_t j = i; j < probs.size() && g.count < kMaxGroup; ++j) {
       if (done[j] || cfgs[j].NT != cfgs[i].NT || cfgs[j].MT != cfgs[i].MT ||
-          (probs[j].fold != FOLD_NONE) != (probs[i].fold != FOLD_NONE))
+          (probs[j].fold != FOLD_NONE) != (probs[i].fold != FOLD_NONE) ||
+          probs[j].fold_k1 != probs[i].fold_k1 || (probs[i].fold_k1 && g.count >= kSmallGroup))
         continue;
       ModeProb p = probs[j];
       p.cta_begin = ctas;
@@ -512,8 +549,9 @@ cudaError_t launch_stage(std::vector<ModeProb>& probs_in, const std::vector<Tile
       }
       alloc_small_ctas(g, w);
     } else {
-      for (int j = 0; j < g.count; ++j)  // fused and folded passes need the small path
-        if (g.prob[j].epi == EPI_FUSED || g.prob[j].fold) return cudaErrorInvalidValue;
+      for (int j = 0; j < g.count; ++j)  // fused and small-fold passes need the small path
+        if (g.prob[j].epi == EPI_FUSED || (g.prob[j].fold && !g.prob[j].fold_k1))
+          return cudaErrorInvalidValue;
     }
     if (rec) {
       double fl = 0.0, by = 0.0;
@@ -610,7 +648,7 @@ static int plane_nt(const std::vector<const fdp_fd_s*>& hs, const PresPlane* pq)
   if (hs.empty() || hs.size() + (pq ? 1 : 0) > (size_t)kPlaneMax || hs[0]->D != 3) return 0;
   const int nt = hs[0]->fold_nt[1];
   for (const fdp_fd_s* h : hs) {
-    if (!h->fold[0] || !h->fold[1] || !h->fold[2]) return 0;
+    if (h->fold[0] != 1 || h->fold[1] != 1 || h->fold[2] != 1) return 0;
     if (h->fold_nt[1] != nt || h->fold_nt[2] != nt || h->fold_nt[0] != hs[0]->fold_nt[0]) return 0;
   }
   if (pq && !(pq->q_fold[0] && pq->q_fold[1] && pq->q_fold[2])) return 0;
@@ -694,7 +732,10 @@ static cudaError_t enqueue_fd_plane(const std::vector<const fdp_fd_s*>& hs,
       begin += q.n1 * (int)batch;
       sp = std::max(sp, q.sp);
       rows = std::max(rows, q.n3);  // full tiles and leftover rows never read past row n3
-      fl += 2.0 * h->N * batch * (2.0 * h->n[1] + 2.0 * h->n[2]);
+      for (int d = 1; d < 3; ++d) {  // forward + backward folded transforms of modes 2 and 3
+        const double ne = (h->n[d] + 1) / 2, no = h->n[d] / 2;
+        fl += 2.0 * 2.0 * (double)(h->N / h->n[d]) * batch * (ne * ne + no * no);
+      }
       by += 16.0 * h->N * batch;
     }
     if (pq) {
@@ -827,7 +868,8 @@ cudaError_t enqueue_fd(const std::vector<const fdp_fd_s*>& hs,
       if (!st.fwd && d == 0 && dscale[k]) { epi = EPI_SCALE; sc = dscale[k]; }
       probs.push_back(make_mode_prob(hs[k], d, st.fwd, src, sbs, dst, dbs, batch, epi, sc, xld, yld));
       TileCfg c = hs[k]->cfg[d];
-      if (hs[k]->fold[d]) c.NT = hs[k]->fold_nt[d];
+      if (hs[k]->fold[d] == 1) c.NT = hs[k]->fold_nt[d];
+      if (hs[k]->fold[d] == 2) c = st.fwd ? hs[k]->cfgFf[d] : hs[k]->cfgFb[d];
       cfgs.push_back(c);
     }
     if (hook) hook(pass, st.fwd, d, probs, cfgs);

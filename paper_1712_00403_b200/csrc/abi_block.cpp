@@ -101,7 +101,7 @@ extern "C" fdp_status block_precond_setup(int D, const fdp_fd* vel, fdp_mass pre
         // FOLD_SYM pass (about half the DMMAs); otherwise its own dense launch
         bool vfold = true;
         for (int k = 0; k < D; ++k)
-          vfold = vfold && raw->vel[k]->fold[d] && raw->vel[k]->fold_nt[d] == raw->vel[0]->fold_nt[d];
+          vfold = vfold && raw->vel[k]->fold[d] == 1 && raw->vel[k]->fold_nt[d] == raw->vel[0]->fold_nt[d];
         std::vector<double> w;
         if (vfold && nq >= 8 && fold_nt(nq) <= raw->vel[0]->fold_nt[d] && persymmetric(nq, X.data(), 1e-10)) {
           const int nt = raw->vel[0]->fold_nt[d];

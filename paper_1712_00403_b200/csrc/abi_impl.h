@@ -156,7 +156,11 @@ struct fdp_fd_s {
   int fold[3] = {0, 0, 0};
   int fold_nt[3] = {0, 0, 0};  // small-kernel NT of a folded mode: 2 * ceil(ceil(n/2) / 8)
   int foldh[3] = {0, 0, 0};
-  int ldwF[3] = {0, 0, 0};
+  int ldwF[3] = {0, 0, 0};     // forward matrix columns (small-path fold: both matrices)
+  int ldwFb[3] = {0, 0, 0};    // backward matrix columns
+  // fold[d] == 2: K1-path fold (n > 96), tile configs of the forward / backward transforms
+  TileCfg cfgFf[3], cfgFb[3];
+  int tiles_ne[3] = {0, 0, 0};
   double* WfF[3] = {nullptr, nullptr, nullptr};
   double* WbF[3] = {nullptr, nullptr, nullptr};
   double* lamcF[3] = {nullptr, nullptr, nullptr};

@@ -64,6 +64,8 @@ struct ModeProb {
   // and the mode's spectral index runs over [E (ceil(n/2)) | O (floor(n/2))].
   int fold;
   int foldh;
+  int fold_k1;            // folded problem of the K1 kernel (n > 96): 1; small-path fold: 0
+  int tiles_ne;           // K1 FOLD_FWD: column tiles of the E block (the rest are O tiles)
   // Transposed I/O of the plane path (folded problems only): TIO_OUT_T (KMAJ
   // kernel): output row m, column a at Y[item * ybs + mi + Mi * a] (the plane-major layout, mi the
   // row within its item, Mi = P * Q rows per item); TIO_OUT_K (non-KMAJ kernel reading a

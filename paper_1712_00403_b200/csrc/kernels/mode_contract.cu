@@ -237,6 +237,245 @@ mode_contract_kernel(const __grid_constant__ ModeGroupT<G> grp) {
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// K1f: the even-odd folded transform (mode_small.cu tile_compute_store_fold has the
+// algebra) on the K1 tiling, for extents n > 96.
+//   FOLD = FOLD_FWD: a CTA's column tile lies in the E block (tn < tiles_ne: spectral columns
+//     [0, ne), operand s_k = x_k + x_{n-1-k}) or the O block (columns ne + [0, no), operand
+//     d_k = x_k - x_{n-1-k}); each pipeline stage holds the direct A tile (k0 .. k0+BK-1) and the
+//     mirrored one (n-k0-BK .. n-k0-1), combined at the fragment load. K = ne or no: about half
+//     the dense DMMAs. Optional EPI_LAMBDA (spectral order [E | O]).
+//   FOLD = FOLD_BWD: a CTA owns spatial columns c in [n0, n0 + BN) of [0, ne) and accumulates
+//     e = W_E y_E over the E half of the spectral row and o = W_O y_O over the O half in two
+//     register sets, then writes x_c = e + o and x_{n-1-c} = e - o (optional EPI_SCALE).
+// ---------------------------------------------------------------------------------------------
+template <int MT, int NT, bool KMAJ, int FOLD>
+struct SmemF {
+  using B = Smem<MT, NT, KMAJ>;
+  static constexpr int A_ELEMS = B::A_ELEMS * (FOLD == FOLD_FWD ? 2 : 1);
+  static constexpr int STAGE = A_ELEMS + B::B_ELEMS;
+  static constexpr size_t BYTES = sizeof(double) * STAGE * STAGES;
+};
+
+template <int MT, int NT, bool KMAJ, int FOLD>
+__global__ void __launch_bounds__(THREADS, FDP_K1_MINB)
+mode_contract_fold_kernel(const __grid_constant__ ModeGroupT<kSmallGroup> grp) {
+  using S = Smem<MT, NT, KMAJ>;
+  using SF = SmemF<MT, NT, KMAJ, FOLD>;
+  constexpr int BM = S::BM, BN = S::BN;
+  extern __shared__ __align__(16) double smem[];
+
+  int pi = 0;
+#pragma unroll
+  for (int i = 1; i < kSmallGroup; ++i)
+    if (i < grp.count && (int)blockIdx.x >= grp.prob[i].cta_begin) pi = i;
+  const ModeProb& pb = grp.prob[pi];
+  const int t = blockIdx.x - pb.cta_begin;
+  const int tn = t % pb.tiles_n;
+  const int tm = t / pb.tiles_n;
+  const long long m0 = (long long)tm * BM;
+  const long long M = (long long)pb.P * pb.Q * pb.batch;
+  const int P = pb.P, n = pb.n, ldw = pb.ldw, nout = pb.nout;
+  const int ne = (n + 1) >> 1, no = n >> 1;
+  const long long Pn = (long long)P * n, Pno = (long long)P * nout;
+  const double* __restrict__ X = pb.X;
+  const double* __restrict__ W = pb.W;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  // FOLD_FWD: E or O column tile
+  const bool isE = FOLD != FOLD_FWD || tn < pb.tiles_ne;
+  const int n0 = (FOLD == FOLD_FWD && !isE ? tn - pb.tiles_ne : tn) * BN;
+
+  constexpr int RSTEP = THREADS / BK;
+  constexpr int A_ROWS_PER_THREAD = KMAJ ? BM / RSTEP : 1;
+  long long a_off[A_ROWS_PER_THREAD];
+  bool a_ok[A_ROWS_PER_THREAD];
+  const int Qn = pb.Q;
+  if (KMAJ) {
+#pragma unroll
+    for (int j = 0; j < A_ROWS_PER_THREAD; ++j) {
+      long long m = m0 + tid / BK + RSTEP * j;
+      a_ok[j] = m < M;
+      a_off[j] = a_ok[j] ? (long long)pb.xld * (m % Qn) + pb.xbs * (m / Qn) : 0;
+    }
+  } else {
+    long long m = m0 + tid % BM;
+    a_ok[0] = m < M;
+    if (a_ok[0]) {
+      const long long p = m % P, r = m / P;
+      a_off[0] = p + Pn * (r % Qn) + pb.xbs * (r / Qn);
+    } else {
+      a_off[0] = 0;
+    }
+  }
+
+  // A tile of columns kb .. kb+BK-1 (zero outside [0, n)) into As
+  auto load_a = [&](double* As, int kb) {
+    if (KMAJ) {
+      const int k = tid % BK;
+      const int kk = kb + k;
+      const bool kv = kk >= 0 && kk < n;
+#pragma unroll
+      for (int j = 0; j < A_ROWS_PER_THREAD; ++j) {
+        const int mr = tid / BK + RSTEP * j;
+        const bool v = a_ok[j] && kv;
+        cp_async8(&As[mr * S::SA + k], X + (v ? a_off[j] + kk : 0), v);
+      }
+    } else {
+      constexpr int KSTEP = THREADS / BM;
+      const int mr = tid % BM;
+#pragma unroll
+      for (int k = tid / BM; k < BK; k += KSTEP) {
+        const int kk = kb + k;
+        const bool v = a_ok[0] && kk >= 0 && kk < n;
+        cp_async8(&As[k * S::SA + mr], X + (v ? a_off[0] + (long long)P * kk : 0), v);
+      }
+    }
+  };
+  // one stage: A (direct; FOLD_FWD also the mirror block) and the W rows wrow0 + k0 ..
+  auto load_stage = [&](int stage, int k0, int aoff, int wrow0) {
+    double* As = smem + stage * SF::STAGE;
+    double* Bs = As + SF::A_ELEMS;
+    load_a(As, aoff + k0);
+    if (FOLD == FOLD_FWD) load_a(As + S::A_ELEMS, n - k0 - BK);
+    constexpr int CHUNKS = BK * BN / 2;
+#pragma unroll
+    for (int c = tid; c < CHUNKS; c += THREADS) {
+      const int kr = c / (BN / 2), cc = (c % (BN / 2)) * 2;
+      cp_async16(&Bs[kr * S::SB + cc], W + (size_t)(wrow0 + k0 + kr) * ldw + n0 + cc);
+    }
+  };
+
+  const int fr = lane >> 2, fc = lane & 3;
+  const int wm = warp * 8 * MT;
+  double acc[MT][NT][2], acc2[FOLD == FOLD_BWD ? MT : 1][FOLD == FOLD_BWD ? NT : 1][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  if constexpr (FOLD == FOLD_BWD) {
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) acc2[i][j][0] = acc2[i][j][1] = 0.0;
+  }
+
+  // K loop over K columns of the operand starting at aoff, W rows from wrow0, into accumulator c
+  auto kloop = [&](double (&c)[MT][NT][2], int K, int aoff, int wrow0, double sgn) {
+    const int KT = (K + BK - 1) / BK;
+#pragma unroll
+    for (int st = 0; st < STAGES - 1; ++st) {
+      if (st < KT) load_stage(st, st * BK, aoff, wrow0);
+      cp_async_commit();
+    }
+    for (int kt = 0; kt < KT; ++kt) {
+      cp_async_wait<STAGES - 2>();
+      __syncthreads();
+      {
+        const int nk = kt + STAGES - 1;
+        if (nk < KT) load_stage(nk % STAGES, nk * BK, aoff, wrow0);
+        cp_async_commit();
+      }
+      const double* As = smem + (kt % STAGES) * SF::STAGE;
+      const double* As2 = As + S::A_ELEMS;
+      const double* Bs = As + SF::A_ELEMS;
+      const int kvalid = min(BK, K - kt * BK);
+#pragma unroll
+      for (int k4 = 0; k4 < BK; k4 += 4) {
+        if (k4 < kvalid) {
+          double a[MT], b[NT];
+#pragma unroll
+          for (int i = 0; i < MT; ++i) {
+            const int mr = wm + 8 * i + fr;
+            const int kk = k4 + fc;
+            a[i] = KMAJ ? As[mr * S::SA + kk] : As[kk * S::SA + mr];
+            if (FOLD == FOLD_FWD) {
+              const int km = BK - 1 - kk;  // mirror block holds n-k0-BK .. n-k0-1
+              a[i] += sgn * (KMAJ ? As2[mr * S::SA + km] : As2[km * S::SA + mr]);
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < NT; ++j) b[j] = Bs[(k4 + fc) * S::SB + 8 * j + fr];
+#pragma unroll
+          for (int i = 0; i < MT; ++i)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) dmma(c[i][j], a[i], b[j]);
+        }
+      }
+    }
+    cp_async_wait<0>();
+    __syncthreads();  // the next phase refills the ring
+  };
+
+  if constexpr (FOLD == FOLD_FWD) {
+    kloop(acc, isE ? ne : no, 0, isE ? 0 : pb.foldh, isE ? 1.0 : -1.0);
+  } else {
+    kloop(acc, ne, 0, 0, 0.0);              // e over the E half of the spectral row
+    kloop(acc2, no, ne, pb.foldh, 0.0);     // o over the O half
+  }
+
+  // ---- epilogue ----
+  const int epi = pb.epi;
+  double* __restrict__ Y = pb.Y;
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    const long long m = m0 + wm + 8 * i + fr;
+    if (m >= M) continue;
+    long long row_off, sidx;
+    double lrow = 0.0;
+    bool pad_row = false;
+    if (KMAJ) {
+      sidx = (long long)pb.yld * (m % Qn);
+      row_off = sidx + pb.ybs * (m / Qn);
+    } else {
+      const long long p = m % P, r = m / P;
+      sidx = p + Pno * (r % Qn);
+      row_off = sidx + pb.ybs * (r / Qn);
+      if (epi == EPI_LAMBDA) {
+        const int i1 = (int)(p % pb.n1);
+        pad_row = i1 >= pb.n1v;
+        if (!pad_row) lrow = pb.lam1 ? pb.lam0[i1] + pb.lam1[p / pb.n1] : pb.lam0[p];
+      }
+    }
+    const long long cs = KMAJ ? 1 : P;
+    if constexpr (FOLD == FOLD_FWD) {
+      const int ncols = KMAJ ? pb.yld : nout;  // KMAJ rows: their pad columns get their zeros
+      const int coff = isE ? 0 : ne, cval = isE ? ne : no;
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int a = n0 + 8 * j + 2 * fc + h;
+          const int oc = coff + a;
+          if (oc < ncols && (a < cval || (KMAJ && !isE))) {
+            double v = a < cval ? acc[i][j][h] : 0.0;
+            if (epi == EPI_LAMBDA) v = (pad_row || a >= cval) ? 0.0 : fdp_div(v, lrow + pb.lamcol[oc]);
+            Y[row_off + cs * oc] = v;
+          }
+        }
+    } else {
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = n0 + 8 * j + 2 * fc + h;
+          if (c < ne) {
+            double v0 = acc[i][j][0 + h] + acc2[i][j][h];
+            double v1 = acc[i][j][h] - acc2[i][j][h];
+            if (epi == EPI_SCALE) {
+              v0 *= pb.scale[sidx + cs * c];
+              v1 *= pb.scale[sidx + cs * (n - 1 - c)];
+            }
+            Y[row_off + cs * c] = v0;
+            Y[row_off + cs * (n - 1 - c)] = v1;
+          }
+        }
+      if (KMAJ && n0 == 0 && fc == 0)
+        for (int c = n; c < pb.yld; ++c) Y[row_off + c] = 0.0;  // zero pad column of a padded row
+    }
+  }
+}
+
 template <int MT, int NT, bool KMAJ>
 cudaError_t launch_t(const ModeGroup* g, cudaStream_t s) {
   using S = Smem<MT, NT, KMAJ>;
@@ -247,8 +486,28 @@ cudaError_t launch_t(const ModeGroup* g, cudaStream_t s) {
       e = cudaFuncSetAttribute(mode_contract_kernel<MT, NT, false, kSmallGroup, true>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES);
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(mode_contract_kernel<MT, NT, KMAJ, kMaxGroup>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES);
+    e = cudaFuncSetAttribute(mode_contract_kernel<MT, NT, KMAJ, kMaxGroup>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(mode_contract_fold_kernel<MT, NT, KMAJ, FOLD_FWD>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)SmemF<MT, NT, KMAJ, FOLD_FWD>::BYTES);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(mode_contract_fold_kernel<MT, NT, KMAJ, FOLD_BWD>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)SmemF<MT, NT, KMAJ, FOLD_BWD>::BYTES);
+    return e;
+  }
+  if (g->prob[0].fold != FOLD_NONE) {  // folded K1 group (host-checked: all problems, one kind)
+    const int f = g->prob[0].fold;
+    if (g->count > kSmallGroup || (f != FOLD_FWD && f != FOLD_BWD)) return cudaErrorInvalidValue;
+    if (f == FOLD_FWD)
+      mode_contract_fold_kernel<MT, NT, KMAJ, FOLD_FWD>
+          <<<g->total_ctas, THREADS, SmemF<MT, NT, KMAJ, FOLD_FWD>::BYTES, s>>>(narrow_group<kSmallGroup>(*g));
+    else
+      mode_contract_fold_kernel<MT, NT, KMAJ, FOLD_BWD>
+          <<<g->total_ctas, THREADS, SmemF<MT, NT, KMAJ, FOLD_BWD>::BYTES, s>>>(narrow_group<kSmallGroup>(*g));
+    return cudaGetLastError();
   }
   bool sc = false;
   for (int i = 0; i < g->count; ++i) sc = sc || g->prob[i].peers != nullptr;

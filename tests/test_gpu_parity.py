@@ -65,6 +65,9 @@ def _rand_persym_spd(n, rng, shift):
     ((65, 65, 65), (2.0, 1.0, 1.0), 1, True),    # config 2's velocity extent
     ((33, 64), (1.0, 2.0), 3, False),            # 2D
     ((7, 12, 20), (1.0, 1.0, 1.0), 1, False),    # 7 < 8 stays dense next to folded modes
+    ((259, 20, 9), (2.0, 1.0, 1.0), 2, True),    # K1 folded mode 1 (KMAJ), odd n, P^G scaling
+    ((12, 258, 97), (1.0, 2.0, 1.0), 1, False),  # K1 folded modes 2 and 3, Lambda on the K1 fold
+    ((300, 2), (1.0, 3.0), 2, False),            # 2D, K1 folded even extent
 ])
 def test_fd_apply_folded_persymmetric(dims, coef, batch, dscale):
     """Even-odd folded transforms on random persymmetric SPD pencils: the folded
