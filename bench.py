@@ -237,9 +237,9 @@ def run_reference(args, w, cid):
         # BASELINE.md §2.1 holds the paper's own per-apply time at config 2's size (P_D, 866,750
         # dofs: 9.94 s / 166 applications = 59.9 ms on one Haswell-E thread):
         # context from another machine, not a target
-        "vs_baseline": (value / (166 / 9.94)) if (cid == 2 and not slab) else None,
+        "vs_baseline": (value / (166 / 9.94)) if cid == 2 else None,
         "vs_baseline_source": ("BASELINE.md §2.1: 59.9 ms per P_D apply at config 2's size (paper, "
-                               "MATLAB, one Haswell-E thread)") if (cid == 2 and not slab) else None, "dtype": "f64", "data": "synthetic",
+                               "MATLAB, one Haswell-E thread)") if cid == 2 else None, "dtype": "f64", "data": "synthetic",
         "dof_per_s": value * od.n_total,
         "config": workload_config(cid, w, od.n_total, 1, 1, "n/a (CPU)"),
         "cpu_baseline": {"value": value, "unit": "apply/s", "cores": cores, "kind": "oracle",
@@ -347,6 +347,13 @@ def main():
     flush_buf = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev) if flush else None
     stream = torch.cuda.current_stream()
 
+    def flush_l2():
+        # write a buffer 4x the L2, then read it back: the timed step starts on an L2 full of
+        # clean lines (a write-only flush leaves ~126 MB of dirty lines whose write-back would
+        # compete with the step's own traffic and made config-2 timings vary by 15%)
+        flush_buf.zero_()
+        torch.sum(flush_buf, dtype=torch.int64)
+
     def step():
         if slab:
             SB.apply(r[0], s[0], stream=stream)
@@ -356,7 +363,7 @@ def main():
     # ---- warmup ----
     for _ in range(max(args.warmup, 3)):
         if flush:
-            flush_buf.zero_()
+            flush_l2()
         step()
     torch.cuda.synchronize()
 
@@ -374,7 +381,7 @@ def main():
     wall0 = time.perf_counter()
     for i in range(args.steps):
         if flush:
-            flush_buf.zero_()
+            flush_l2()
         ev[i][0].record(stream)
         step()
         ev[i][1].record(stream)
@@ -391,7 +398,7 @@ def main():
         P.profile(True)
         for i in range(max(3, min(args.steps, 20))):
             if flush:
-                flush_buf.zero_()
+                flush_l2()
             step()
             torch.cuda.synchronize()
             if i >= 1:
@@ -523,7 +530,7 @@ def main():
         "data": "synthetic",
         "dof_per_s": value * n_total,
         "config": workload_config(cid, w, n_total, batch_total, world,
-                                  "flushed (512 MB write) before every timed step" if flush
+                                  "flushed before every timed step (512 MB written, then read back)" if flush
                                   else "working set > L2"),
         "roofline": {
             "bound": "tensor",

@@ -68,8 +68,13 @@ def launches(path):
         name = r[ki].split("(")[0].replace("void ", "")
         agg.setdefault(name, []).append(float(r[vi].replace(",", "")) / 1e3)
     tot = sum(sum(v) for v in agg.values())
+    # share of the step: over libfdp's own kernels only (the bench's L2-flush fills run between
+    # steps, outside the timed step)
+    tot_fdp = sum(sum(v) for k, v in agg.items() if k.startswith("fdp::")) or tot
     return {k: {"launches": len(v), "total_us": round(sum(v), 1), "mean_us": round(sum(v) / len(v), 2),
-                "share": round(sum(v) / tot, 4)} for k, v in agg.items()}
+                "share": round(sum(v) / tot, 4),
+                "share_of_step": round(sum(v) / tot_fdp, 4) if k.startswith("fdp::") else None}
+            for k, v in agg.items()}
 
 
 def main():
@@ -89,9 +94,11 @@ def main():
     lines = [f"# {a.tag}", ""]
     if "launch_list" in out:
         lines += ["## Launch list (ncu gpu__time_duration.sum, cold-cache, serialised)", "",
-                  "| kernel | launches | total us | mean us | share |", "|---|---|---|---|---|"]
+                  "| kernel | launches | total us | mean us | share (all) | share of step (libfdp kernels) |",
+                  "|---|---|---|---|---|---|"]
         for k, v in out["launch_list"].items():
-            lines.append(f"| {k} | {v['launches']} | {v['total_us']} | {v['mean_us']} | {v['share']:.3f} |")
+            sos = "-" if v["share_of_step"] is None else f"{v['share_of_step']:.3f}"
+            lines.append(f"| {k} | {v['launches']} | {v['total_us']} | {v['mean_us']} | {v['share']:.3f} | {sos} |")
         lines.append("")
     if "kernels" in out:
         lines += ["## Full-set captures", "",
