@@ -10,6 +10,8 @@
 // STAGES-deep cp.async ring in shared memory. Each warp owns MT x NT DMMA accumulators (FP64
 // registers). Shared-memory strides are == 4 (mod 16) doubles so the 8x4 / 4x8 fragment loads
 // are bank-conflict free.
+#include <cstdlib>
+
 #include "../fdp_internal.h"
 
 namespace fdp {
@@ -27,6 +29,11 @@ namespace {
 #define FDP_K1_MINB 4
 #endif
 constexpr int BK = FDP_K1_BK;
+// folded forward: two A tiles per stage; K chunks of 8 keep 4 CTAs (16 warps) per SM
+#ifndef FDP_K1F_BK
+#define FDP_K1F_BK 8
+#endif
+constexpr int kFoldBK = FDP_K1F_BK;
 constexpr int STAGES = FDP_K1_STAGES;
 constexpr int WARPS = kK1Warps;
 constexpr int THREADS = WARPS * 32;
@@ -249,19 +256,24 @@ mode_contract_kernel(const __grid_constant__ ModeGroupT<G> grp) {
 //     e = W_E y_E over the E half of the spectral row and o = W_O y_O over the O half in two
 //     register sets, then writes x_c = e + o and x_{n-1-c} = e - o (optional EPI_SCALE).
 // ---------------------------------------------------------------------------------------------
-template <int MT, int NT, bool KMAJ, int FOLD>
+template <int MT, int NT, bool KMAJ, int FOLD, int BKF>
 struct SmemF {
-  using B = Smem<MT, NT, KMAJ>;
-  static constexpr int A_ELEMS = B::A_ELEMS * (FOLD == FOLD_FWD ? 2 : 1);
-  static constexpr int STAGE = A_ELEMS + B::B_ELEMS;
+  static constexpr int BM = WARPS * 8 * MT;
+  static constexpr int BN = 8 * NT;
+  static constexpr int SA = KMAJ ? (BKF + 4) : (BM + 4);
+  static constexpr int A1 = KMAJ ? BM * SA : BKF * SA;       // one A tile
+  static constexpr int A_ELEMS = A1 * (FOLD == FOLD_FWD ? 2 : 1);
+  static constexpr int SB = ((BN + 15) / 16) * 16 + 4;
+  static constexpr int B_ELEMS = BKF * SB;
+  static constexpr int STAGE = A_ELEMS + B_ELEMS;
   static constexpr size_t BYTES = sizeof(double) * STAGE * STAGES;
 };
 
-template <int MT, int NT, bool KMAJ, int FOLD>
+template <int MT, int NT, bool KMAJ, int FOLD, int BKF>
 __global__ void __launch_bounds__(THREADS, FDP_K1_MINB)
 mode_contract_fold_kernel(const __grid_constant__ ModeGroupT<kSmallGroup> grp) {
-  using S = Smem<MT, NT, KMAJ>;
-  using SF = SmemF<MT, NT, KMAJ, FOLD>;
+  using S = SmemF<MT, NT, KMAJ, FOLD, BKF>;
+  using SF = S;
   constexpr int BM = S::BM, BN = S::BN;
   extern __shared__ __align__(16) double smem[];
 
@@ -286,7 +298,7 @@ mode_contract_fold_kernel(const __grid_constant__ ModeGroupT<kSmallGroup> grp) {
   const bool isE = FOLD != FOLD_FWD || tn < pb.tiles_ne;
   const int n0 = (FOLD == FOLD_FWD && !isE ? tn - pb.tiles_ne : tn) * BN;
 
-  constexpr int RSTEP = THREADS / BK;
+  constexpr int RSTEP = THREADS / BKF;
   constexpr int A_ROWS_PER_THREAD = KMAJ ? BM / RSTEP : 1;
   long long a_off[A_ROWS_PER_THREAD];
   bool a_ok[A_ROWS_PER_THREAD];
@@ -294,7 +306,7 @@ mode_contract_fold_kernel(const __grid_constant__ ModeGroupT<kSmallGroup> grp) {
   if (KMAJ) {
 #pragma unroll
     for (int j = 0; j < A_ROWS_PER_THREAD; ++j) {
-      long long m = m0 + tid / BK + RSTEP * j;
+      long long m = m0 + tid / BKF + RSTEP * j;
       a_ok[j] = m < M;
       a_off[j] = a_ok[j] ? (long long)pb.xld * (m % Qn) + pb.xbs * (m / Qn) : 0;
     }
@@ -309,15 +321,15 @@ mode_contract_fold_kernel(const __grid_constant__ ModeGroupT<kSmallGroup> grp) {
     }
   }
 
-  // A tile of columns kb .. kb+BK-1 (zero outside [0, n)) into As
+  // A tile of columns kb .. kb+BKF-1 (zero outside [0, n)) into As
   auto load_a = [&](double* As, int kb) {
     if (KMAJ) {
-      const int k = tid % BK;
+      const int k = tid % BKF;
       const int kk = kb + k;
       const bool kv = kk >= 0 && kk < n;
 #pragma unroll
       for (int j = 0; j < A_ROWS_PER_THREAD; ++j) {
-        const int mr = tid / BK + RSTEP * j;
+        const int mr = tid / BKF + RSTEP * j;
         const bool v = a_ok[j] && kv;
         cp_async8(&As[mr * S::SA + k], X + (v ? a_off[j] + kk : 0), v);
       }
@@ -325,7 +337,7 @@ mode_contract_fold_kernel(const __grid_constant__ ModeGroupT<kSmallGroup> grp) {
       constexpr int KSTEP = THREADS / BM;
       const int mr = tid % BM;
 #pragma unroll
-      for (int k = tid / BM; k < BK; k += KSTEP) {
+      for (int k = tid / BM; k < BKF; k += KSTEP) {
         const int kk = kb + k;
         const bool v = a_ok[0] && kk >= 0 && kk < n;
         cp_async8(&As[k * S::SA + mr], X + (v ? a_off[0] + (long long)P * kk : 0), v);
@@ -337,8 +349,8 @@ mode_contract_fold_kernel(const __grid_constant__ ModeGroupT<kSmallGroup> grp) {
     double* As = smem + stage * SF::STAGE;
     double* Bs = As + SF::A_ELEMS;
     load_a(As, aoff + k0);
-    if (FOLD == FOLD_FWD) load_a(As + S::A_ELEMS, n - k0 - BK);
-    constexpr int CHUNKS = BK * BN / 2;
+    if (FOLD == FOLD_FWD) load_a(As + S::A1, n - k0 - BKF);
+    constexpr int CHUNKS = BKF * BN / 2;
 #pragma unroll
     for (int c = tid; c < CHUNKS; c += THREADS) {
       const int kr = c / (BN / 2), cc = (c % (BN / 2)) * 2;
@@ -362,10 +374,10 @@ mode_contract_fold_kernel(const __grid_constant__ ModeGroupT<kSmallGroup> grp) {
 
   // K loop over K columns of the operand starting at aoff, W rows from wrow0, into accumulator c
   auto kloop = [&](double (&c)[MT][NT][2], int K, int aoff, int wrow0, double sgn) {
-    const int KT = (K + BK - 1) / BK;
+    const int KT = (K + BKF - 1) / BKF;
 #pragma unroll
     for (int st = 0; st < STAGES - 1; ++st) {
-      if (st < KT) load_stage(st, st * BK, aoff, wrow0);
+      if (st < KT) load_stage(st, st * BKF, aoff, wrow0);
       cp_async_commit();
     }
     for (int kt = 0; kt < KT; ++kt) {
@@ -373,15 +385,15 @@ mode_contract_fold_kernel(const __grid_constant__ ModeGroupT<kSmallGroup> grp) {
       __syncthreads();
       {
         const int nk = kt + STAGES - 1;
-        if (nk < KT) load_stage(nk % STAGES, nk * BK, aoff, wrow0);
+        if (nk < KT) load_stage(nk % STAGES, nk * BKF, aoff, wrow0);
         cp_async_commit();
       }
       const double* As = smem + (kt % STAGES) * SF::STAGE;
-      const double* As2 = As + S::A_ELEMS;
+      const double* As2 = As + S::A1;
       const double* Bs = As + SF::A_ELEMS;
-      const int kvalid = min(BK, K - kt * BK);
+      const int kvalid = min(BKF, K - kt * BKF);
 #pragma unroll
-      for (int k4 = 0; k4 < BK; k4 += 4) {
+      for (int k4 = 0; k4 < BKF; k4 += 4) {
         if (k4 < kvalid) {
           double a[MT], b[NT];
 #pragma unroll
@@ -390,7 +402,7 @@ mode_contract_fold_kernel(const __grid_constant__ ModeGroupT<kSmallGroup> grp) {
             const int kk = k4 + fc;
             a[i] = KMAJ ? As[mr * S::SA + kk] : As[kk * S::SA + mr];
             if (FOLD == FOLD_FWD) {
-              const int km = BK - 1 - kk;  // mirror block holds n-k0-BK .. n-k0-1
+              const int km = BKF - 1 - kk;  // mirror block holds n-k0-BKF .. n-k0-1
               a[i] += sgn * (KMAJ ? As2[mr * S::SA + km] : As2[km * S::SA + mr]);
             }
           }
@@ -489,24 +501,32 @@ cudaError_t launch_t(const ModeGroup* g, cudaStream_t s) {
     e = cudaFuncSetAttribute(mode_contract_kernel<MT, NT, KMAJ, kMaxGroup>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(mode_contract_fold_kernel<MT, NT, KMAJ, FOLD_FWD>,
+      e = cudaFuncSetAttribute(mode_contract_fold_kernel<MT, NT, KMAJ, FOLD_FWD, kFoldBK>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)SmemF<MT, NT, KMAJ, FOLD_FWD>::BYTES);
+                               (int)SmemF<MT, NT, KMAJ, FOLD_FWD, kFoldBK>::BYTES);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(mode_contract_fold_kernel<MT, NT, KMAJ, FOLD_BWD>,
+      e = cudaFuncSetAttribute(mode_contract_fold_kernel<MT, NT, KMAJ, FOLD_FWD, BK>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)SmemF<MT, NT, KMAJ, FOLD_BWD>::BYTES);
+                               (int)SmemF<MT, NT, KMAJ, FOLD_FWD, BK>::BYTES);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(mode_contract_fold_kernel<MT, NT, KMAJ, FOLD_BWD, BK>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)SmemF<MT, NT, KMAJ, FOLD_BWD, BK>::BYTES);
     return e;
   }
   if (g->prob[0].fold != FOLD_NONE) {  // folded K1 group (host-checked: all problems, one kind)
     const int f = g->prob[0].fold;
     if (g->count > kSmallGroup || (f != FOLD_FWD && f != FOLD_BWD)) return cudaErrorInvalidValue;
-    if (f == FOLD_FWD)
-      mode_contract_fold_kernel<MT, NT, KMAJ, FOLD_FWD>
-          <<<g->total_ctas, THREADS, SmemF<MT, NT, KMAJ, FOLD_FWD>::BYTES, s>>>(narrow_group<kSmallGroup>(*g));
+    const bool bk16 = std::getenv("FDP_K1F_BK16") != nullptr;  // experiment switch
+    if (f == FOLD_FWD && !bk16)
+      mode_contract_fold_kernel<MT, NT, KMAJ, FOLD_FWD, kFoldBK>
+          <<<g->total_ctas, THREADS, SmemF<MT, NT, KMAJ, FOLD_FWD, kFoldBK>::BYTES, s>>>(narrow_group<kSmallGroup>(*g));
+    else if (f == FOLD_FWD)
+      mode_contract_fold_kernel<MT, NT, KMAJ, FOLD_FWD, BK>
+          <<<g->total_ctas, THREADS, SmemF<MT, NT, KMAJ, FOLD_FWD, BK>::BYTES, s>>>(narrow_group<kSmallGroup>(*g));
     else
-      mode_contract_fold_kernel<MT, NT, KMAJ, FOLD_BWD>
-          <<<g->total_ctas, THREADS, SmemF<MT, NT, KMAJ, FOLD_BWD>::BYTES, s>>>(narrow_group<kSmallGroup>(*g));
+      mode_contract_fold_kernel<MT, NT, KMAJ, FOLD_BWD, BK>
+          <<<g->total_ctas, THREADS, SmemF<MT, NT, KMAJ, FOLD_BWD, BK>::BYTES, s>>>(narrow_group<kSmallGroup>(*g));
     return cudaGetLastError();
   }
   bool sc = false;
