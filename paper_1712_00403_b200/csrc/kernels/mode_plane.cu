@@ -278,11 +278,21 @@ __global__ void __launch_bounds__(PTH, 2) mode_plane_kernel(const __grid_constan
   double* W2 = sm;
   double* W3 = sm + S::WB;
   double* Sc = sm + 2 * S::WB;        // per-warp scratch rows of the leftover-row path (96 each)
-  double* Pl = Sc + PW * 96;
+  double* Lm = Sc + PW * 96;          // lambda_1 | lambda_2 | lambda_3 of the current problem
+  double* Pl = Lm + 3 * 96;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int CPR = S::KPF / 2;  // 16-byte chunks per W row (8 NTE doubles)
 
+  // the eigenvalues next to W (a cold-L2 apply otherwise pays an HBM round trip per warp in the
+  // Lambda epilogue)
+  auto load_lam = [&](const PlaneProb& pb) {
+    if (pb.kind != 0) return;
+    for (int i = tid; i < pb.n1; i += PTH) cp_async8(&Lm[i], pb.lam1 + i);
+    for (int i = tid; i < pb.n2; i += PTH) cp_async8(&Lm[96 + i], pb.lam2 + i);
+    for (int i = tid; i < pb.n3; i += PTH) cp_async8(&Lm[192 + i], pb.lam3 + i);
+  };
   auto load_w = [&](const PlaneProb& pb) {
+    load_lam(pb);
     for (int c = tid; c < 2 * S::KPF * CPR; c += PTH) {
       const int rr = c / CPR, cc = (c % CPR) * 2;
       const int g2 = rr < S::KPF ? rr : pb.foldh2 + (rr - S::KPF);
@@ -339,8 +349,8 @@ __global__ void __launch_bounds__(PTH, 2) mode_plane_kernel(const __grid_constan
     __syncthreads();
     if (tr) tr[3] = gtimer();
     // mode 3 on the a2 columns (FD: forward, Lambda, backward)
-    const double lb = fd ? pb.lam1[a1] : 0.0;
-    plane_step<NT>(Pl, 1, sp, n2, n3, W3, fd ? PT_FUSED : PT_SYM, lb, pb.lam2, pb.lam3, Sc, warp, lane, grp.dmma_tail);
+    const double lb = fd ? Lm[a1] : 0.0;
+    plane_step<NT>(Pl, 1, sp, n2, n3, W3, fd ? PT_FUSED : PT_SYM, lb, Lm + 96, Lm + 192, Sc, warp, lane, grp.dmma_tail);
     __syncthreads();
     if (tr) tr[4] = gtimer();
     if (fd) {  // mode-2 backward on the i3 rows
@@ -364,7 +374,9 @@ __global__ void __launch_bounds__(PTH, 2) mode_plane_kernel(const __grid_constan
     __syncthreads();  // the plane buffer is refilled next
     if (tr) {
       tr[6] = gtimer();
-      tr[7] = ((unsigned long long)pb.kind << 32) | (unsigned)gp;
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      tr[7] = ((unsigned long long)pb.kind << 32) | ((unsigned long long)smid << 16) | (unsigned)gp;
     }
   }
   wait_all();
@@ -404,7 +416,7 @@ cudaError_t dispatch_p(const PlaneGroup* g, int NT, size_t smem, cudaStream_t s)
 
 size_t plane_smem_bytes(int NT, int sp, int rows) {
   const int KPF = 4 * NT, SBF = ((KPF + 15) / 16) * 16 + 4;
-  return sizeof(double) * ((size_t)2 * 2 * KPF * SBF + PW * 96 + (size_t)sp * rows);
+  return sizeof(double) * ((size_t)2 * 2 * KPF * SBF + PW * 96 + 3 * 96 + (size_t)sp * rows);
 }
 
 int plane_stride(int n2) {

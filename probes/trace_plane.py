@@ -13,6 +13,7 @@ import paper_1712_00403_b200 as fdp
 import synth
 
 cid = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+cold = "cold" in sys.argv  # flush L2 (512 MB written + read back) before the traced apply
 w = synth.CONFIGS[cid]
 gd = fdp.discretization(w.dim, w.disc, w.p, w.n_el)
 P = fdp.build_block(gd)
@@ -29,6 +30,10 @@ fdp.lib.fdp_debug_trace(buf.data_ptr(), cap)
 s2 = torch.empty_like(r)
 P.apply(r, s2, batch=1, workspace=ws)
 torch.cuda.synchronize()
+if cold:
+    fb = torch.empty(512 << 20 >> 2, dtype=torch.int32, device="cuda")
+    fb.zero_()
+    torch.sum(fb, dtype=torch.int64)
 P.apply(r, s2, batch=1, workspace=ws)
 torch.cuda.synchronize()
 fdp.lib.fdp_debug_trace(None, 0)
@@ -39,7 +44,7 @@ a0 = t[:small].reshape(-1, 6)
 a0 = a0[a0[:, 0] > 0]
 t0 = a0[:, 0].min()
 print(f"L1 start 0, first-tile end max {(a0[a0[:,5]>0,5].max()-t0)/1e3:.2f} us")
-grid = int(sys.argv[2]) if len(sys.argv) > 2 else min(2 * nsm, 10**9)
+grid = 2 * nsm
 # plane launch: grid * 8 entries; find grid by scanning for the next small chunk
 p = t[small:small + 8 * 2 * nsm].reshape(-1, 8)
 valid = p[:, 0] > 0
@@ -47,6 +52,18 @@ p = p[valid]
 names = ["start", "W+pdl", "plane load", "mode-2 fwd", "mode-3 fused", "mode-2 bwd", "store"]
 print(f"L2 CTAs {len(p)}: start {(p[:,0].min()-t0)/1e3:.2f} .. {(p[:,0].max()-t0)/1e3:.2f} us, end max {(p[:,6].max()-t0)/1e3:.2f} us")
 kind = p[:, 7] >> 32
+smid = (p[:, 7] >> 16) & 0xFFFF
+import collections
+cnt = collections.Counter(smid.tolist())
+per = collections.Counter(cnt.values())
+print("  CTAs per SM:", dict(sorted(per.items())), " SMs used:", len(cnt))
+two = [sm for sm, c in cnt.items() if c == 2]
+one = [sm for sm, c in cnt.items() if c == 1]
+for label, sms in (("SMs with 2 CTAs", two), ("SMs with 1 CTA", one)):
+    sel = np.isin(smid, sms) & (kind == 0)
+    if sel.any():
+        print(f"  {label}: kind-0 end med {np.median((p[sel,6]-t0)/1e3):.2f} max {((p[sel,6]-t0)/1e3).max():.2f} us,"
+              f" start med {np.median((p[sel,0]-t0)/1e3):.2f}")
 for kd in (0, 1):
     q = p[kind == kd]
     if not len(q):

@@ -29,7 +29,11 @@ fdp.lib.fdp_debug_trace(buf.data_ptr(), cap)
 s2 = torch.empty_like(r)  # new pointer -> re-capture with trace
 P.apply(r, s2, batch=batch, workspace=ws)
 torch.cuda.synchronize()
-P.apply(r, s2, batch=batch, workspace=ws)  # replay (trace overwritten, warm)
+if "cold" in sys.argv:  # flush L2 (512 MB written + read back) before the traced apply
+    fb = torch.empty(512 << 20 >> 2, dtype=torch.int32, device="cuda")
+    fb.zero_()
+    torch.sum(fb, dtype=torch.int64)
+P.apply(r, s2, batch=batch, workspace=ws)  # replay (trace overwritten)
 torch.cuda.synchronize()
 fdp.lib.fdp_debug_trace(None, 0)
 t = buf.cpu().numpy().astype(np.int64)
