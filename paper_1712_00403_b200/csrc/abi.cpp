@@ -765,6 +765,10 @@ static cudaError_t enqueue_fd_plane(const std::vector<const fdp_fd_s*>& hs,
     }
     g.total = begin;
     g.dmma_tail = std::getenv("FDP_PLANE_DMMA_TAIL") != nullptr;
+    {
+      const char* mt = std::getenv("FDP_PLANE_MT");
+      g.mt2 = !(mt && std::string(mt) == "1");
+    }
     if (g.dmma_tail) rows = ((rows + 7) / 8) * 8 + 8;  // the ragged tile reads rows < round8 + 8
     const size_t smem = plane_smem_bytes(nt, sp, rows);
     if (smem > 227 * 1024) return cudaErrorInvalidValue;

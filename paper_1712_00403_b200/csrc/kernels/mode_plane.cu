@@ -65,30 +65,44 @@ enum PlaneStep : int { PT_FWD = 0, PT_FUSED = 1, PT_BWDT = 2, PT_SYM = 3 };
 //   PT_FUSED: PT_FWD, / (lrow + lamcol[a]), then the backward transform with W read transposed
 //   PT_BWDT:  backward transform, W read transposed    -> spatial along k
 //   PT_SYM:   e = W_E^T s, o = W_O^T d, output butterfly (y = A x, A centrosymmetric)
-template <int NT>
+template <int NT, int MT>
 __device__ __forceinline__ void plane_tile(double* Pl, int rs, int ks, int r0, int nrows, int n,
                                            const double* W, int step, double lbase,
                                            const double* lrowv, const double* lamcol, int lane) {
+  // MT row tiles of 8 per warp share every B fragment (MT = 2: half the B loads per DMMA and two
+  // independent accumulator chains per fragment)
   using S = PS<NT>;
   constexpr int NTE = S::NTE, SBF = S::SBF;
   const double* WO = W + S::KPF * SBF;
   const int ne = (n + 1) >> 1, no = n >> 1;
   const bool full_o = ((no + 7) >> 3) == NTE;
   const int fr = lane >> 2, fc = lane & 3;
-  const int r = r0 + fr;
-  const bool rv = r < nrows;
-  double* Ar = Pl + (long long)r * rs;
-  double ae[NTE][2], ao[NTE][2];
+  double* Ar[MT];
+  bool rv[MT];
 #pragma unroll
-  for (int j = 0; j < NTE; ++j) ae[j][0] = ae[j][1] = ao[j][0] = ao[j][1] = 0.0;
+  for (int i = 0; i < MT; ++i) {
+    const int r = r0 + 8 * i + fr;
+    rv[i] = r < nrows;
+    Ar[i] = Pl + (long long)r * rs;
+  }
+  double ae[MT][NTE][2], ao[MT][NTE][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NTE; ++j) ae[i][j][0] = ae[i][j][1] = ao[i][j][0] = ao[i][j][1] = 0.0;
 
   if (step != PT_BWDT) {
     const int k4n = (ne + 3) >> 2;
 #pragma unroll 2
     for (int k4 = 0; k4 < k4n; ++k4) {
       const int k = 4 * k4 + fc;
-      const double x0 = Ar[k * ks], x1 = Ar[(n - 1 - k) * ks];
-      const double sv = x0 + x1, dv = x0 - x1;
+      double sv[MT], dv[MT];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const double x0 = Ar[i][k * ks], x1 = Ar[i][(n - 1 - k) * ks];
+        sv[i] = x0 + x1;
+        dv[i] = x0 - x1;
+      }
       double be[NTE], bo[NTE];
 #pragma unroll
       for (int j = 0; j < NTE; ++j) {
@@ -96,23 +110,30 @@ __device__ __forceinline__ void plane_tile(double* Pl, int rs, int ks, int r0, i
         bo[j] = WO[k * SBF + 8 * j + fr];
       }
 #pragma unroll
-      for (int j = 0; j < NTE; ++j) dmma(ae[j], sv, be[j]);
+      for (int j = 0; j < NTE; ++j)
+#pragma unroll
+        for (int i = 0; i < MT; ++i) dmma(ae[i][j], sv[i], be[j]);
 #pragma unroll
       for (int j = 0; j < NTE; ++j)
-        if (j < NTE - 1 || full_o) dmma(ao[j], dv, bo[j]);
+        if (j < NTE - 1 || full_o)
+#pragma unroll
+          for (int i = 0; i < MT; ++i) dmma(ao[i][j], dv[i], bo[j]);
     }
     __syncwarp();
     if (step == PT_FWD || step == PT_FUSED) {
-      const double lrow = step == PT_FUSED && rv ? lbase + lrowv[r] : 0.0;
 #pragma unroll
-      for (int j = 0; j < NTE; ++j)
+      for (int i = 0; i < MT; ++i) {
+        if (!rv[i]) continue;
+        const double lrow = step == PT_FUSED ? lbase + lrowv[r0 + 8 * i + fr] : 0.0;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int a = 8 * j + 2 * fc + h;
-          if (!rv) continue;
-          if (a < ne) Ar[a * ks] = step == PT_FUSED ? fdp_div(ae[j][h], lrow + lamcol[a]) : ae[j][h];
-          if (a < no) Ar[(ne + a) * ks] = step == PT_FUSED ? fdp_div(ao[j][h], lrow + lamcol[ne + a]) : ao[j][h];
-        }
+        for (int j = 0; j < NTE; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int a = 8 * j + 2 * fc + h;
+            if (a < ne) Ar[i][a * ks] = step == PT_FUSED ? fdp_div(ae[i][j][h], lrow + lamcol[a]) : ae[i][j][h];
+            if (a < no) Ar[i][(ne + a) * ks] = step == PT_FUSED ? fdp_div(ao[i][j][h], lrow + lamcol[ne + a]) : ao[i][j][h];
+          }
+      }
       __syncwarp();
       if (step == PT_FWD) return;
     }
@@ -120,18 +141,24 @@ __device__ __forceinline__ void plane_tile(double* Pl, int rs, int ks, int r0, i
   if (step != PT_SYM) {
     // backward from the spectral row: e over [0, ne), o over [ne, n); W_f read transposed
 #pragma unroll
-    for (int j = 0; j < NTE; ++j) ae[j][0] = ae[j][1] = ao[j][0] = ao[j][1] = 0.0;
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < NTE; ++j) ae[i][j][0] = ae[i][j][1] = ao[i][j][0] = ao[i][j][1] = 0.0;
     {
       const int k4n = (ne + 3) >> 2;
 #pragma unroll 2
       for (int k4 = 0; k4 < k4n; ++k4) {
         const int k = 4 * k4 + fc;
-        const double a = k < n ? Ar[k * ks] : 0.0;
+        double a[MT];
+#pragma unroll
+        for (int i = 0; i < MT; ++i) a[i] = k < n ? Ar[i][k * ks] : 0.0;
         double b[NTE];
 #pragma unroll
         for (int j = 0; j < NTE; ++j) b[j] = W[(8 * j + fr) * SBF + k];
 #pragma unroll
-        for (int j = 0; j < NTE; ++j) dmma(ae[j], a, b[j]);
+        for (int j = 0; j < NTE; ++j)
+#pragma unroll
+          for (int i = 0; i < MT; ++i) dmma(ae[i][j], a[i], b[j]);
       }
     }
     {
@@ -139,13 +166,17 @@ __device__ __forceinline__ void plane_tile(double* Pl, int rs, int ks, int r0, i
 #pragma unroll 2
       for (int k4 = 0; k4 < k4n; ++k4) {
         const int k = 4 * k4 + fc;
-        const double a = ne + k < n ? Ar[(ne + k) * ks] : 0.0;
+        double a[MT];
+#pragma unroll
+        for (int i = 0; i < MT; ++i) a[i] = ne + k < n ? Ar[i][(ne + k) * ks] : 0.0;
         double b[NTE];
 #pragma unroll
         for (int j = 0; j < NTE; ++j) b[j] = WO[(8 * j + fr) * SBF + k];
 #pragma unroll
         for (int j = 0; j < NTE; ++j)
-          if (j < NTE - 1 || full_o) dmma(ao[j], a, b[j]);
+          if (j < NTE - 1 || full_o)
+#pragma unroll
+            for (int i = 0; i < MT; ++i) dmma(ao[i][j], a[i], b[j]);
       }
     }
     __syncwarp();
@@ -153,16 +184,18 @@ __device__ __forceinline__ void plane_tile(double* Pl, int rs, int ks, int r0, i
   // x_c = e_c + o_c, x_{n-1-c} = e_c - o_c; the transposed forward matrix halves the middle row
   // of an odd n (undone here)
   const bool mid2 = step != PT_SYM && (n & 1);
-  if (rv) {
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    if (!rv[i]) continue;
 #pragma unroll
     for (int j = 0; j < NTE; ++j)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int c = 8 * j + 2 * fc + h;
         if (c < ne) {
-          const double e = (mid2 && c == no) ? 2.0 * ae[j][h] : ae[j][h];
-          Ar[c * ks] = e + ao[j][h];
-          Ar[(n - 1 - c) * ks] = e - ao[j][h];
+          const double e = (mid2 && c == no) ? 2.0 * ae[i][j][h] : ae[i][j][h];
+          Ar[i][c * ks] = e + ao[i][j][h];
+          Ar[i][(n - 1 - c) * ks] = e - ao[i][j][h];
         }
       }
   }
@@ -258,16 +291,27 @@ template <int NT>
 __device__ __forceinline__ void plane_step(double* Pl, int rs, int ks, int nrows, int n,
                                            const double* W, int step, double lbase,
                                            const double* lrowv, const double* lamcol,
-                                           double* scratch, int warp, int lane, bool dtail) {
+                                           double* scratch, int warp, int lane, bool dtail,
+                                           bool mt2) {
   if (dtail) {
     for (int t = warp; 8 * t < nrows; t += PW)
-      plane_tile<NT>(Pl, rs, ks, 8 * t, nrows, n, W, step, lbase, lrowv, lamcol, lane);
+      plane_tile<NT, 1>(Pl, rs, ks, 8 * t, nrows, n, W, step, lbase, lrowv, lamcol, lane);
     return;
   }
-  const int full = nrows >> 3;
-  for (int t = warp; t < full; t += PW)
-    plane_tile<NT>(Pl, rs, ks, 8 * t, nrows, n, W, step, lbase, lrowv, lamcol, lane);
-  for (int r = 8 * full + ((warp + PW - full % PW) % PW); r < nrows; r += PW)
+  int full = nrows >> 3;
+  if (mt2) {  // 16-row tiles (and one 8-row tile when the count of full 8-row tiles is odd)
+    const int f16 = full >> 1;
+    for (int t = warp; t < f16; t += PW)
+      plane_tile<NT, 2>(Pl, rs, ks, 16 * t, nrows, n, W, step, lbase, lrowv, lamcol, lane);
+    if ((full & 1) && warp == PW - 1)
+      plane_tile<NT, 1>(Pl, rs, ks, 16 * f16, nrows, n, W, step, lbase, lrowv, lamcol, lane);
+  } else {
+    for (int t = warp; t < full; t += PW)
+      plane_tile<NT, 1>(Pl, rs, ks, 8 * t, nrows, n, W, step, lbase, lrowv, lamcol, lane);
+  }
+  // leftover rows to the warps without a tile (or with the fewest)
+  const int first = mt2 ? (full >> 1) % PW : full % PW;
+  for (int r = 8 * full + ((warp + PW - first) % PW); r < nrows; r += PW)
     plane_row<NT>(Pl, rs, ks, r, n, W, step, lbase, lrowv, lamcol, scratch + warp * 96, lane);
 }
 
@@ -345,16 +389,16 @@ __global__ void __launch_bounds__(PTH, 2) mode_plane_kernel(const __grid_constan
 
     const bool fd = pb.kind == 0;
     // mode 2 on the i3 rows
-    plane_step<NT>(Pl, sp, 1, n3, n2, W2, fd ? PT_FWD : PT_SYM, 0.0, nullptr, nullptr, Sc, warp, lane, grp.dmma_tail);
+    plane_step<NT>(Pl, sp, 1, n3, n2, W2, fd ? PT_FWD : PT_SYM, 0.0, nullptr, nullptr, Sc, warp, lane, grp.dmma_tail, grp.mt2);
     __syncthreads();
     if (tr) tr[3] = gtimer();
     // mode 3 on the a2 columns (FD: forward, Lambda, backward)
     const double lb = fd ? Lm[a1] : 0.0;
-    plane_step<NT>(Pl, 1, sp, n2, n3, W3, fd ? PT_FUSED : PT_SYM, lb, Lm + 96, Lm + 192, Sc, warp, lane, grp.dmma_tail);
+    plane_step<NT>(Pl, 1, sp, n2, n3, W3, fd ? PT_FUSED : PT_SYM, lb, Lm + 96, Lm + 192, Sc, warp, lane, grp.dmma_tail, grp.mt2);
     __syncthreads();
     if (tr) tr[4] = gtimer();
     if (fd) {  // mode-2 backward on the i3 rows
-      plane_step<NT>(Pl, sp, 1, n3, n2, W2, PT_BWDT, 0.0, nullptr, nullptr, Sc, warp, lane, grp.dmma_tail);
+      plane_step<NT>(Pl, sp, 1, n3, n2, W2, PT_BWDT, 0.0, nullptr, nullptr, Sc, warp, lane, grp.dmma_tail, grp.mt2);
       __syncthreads();
       if (tr) tr[5] = gtimer();
       double* dst = pb.T + pb.tbs * (long long)b + (long long)a1 * Mi;  // in place
