@@ -93,22 +93,36 @@ __device__ __forceinline__ void plane_tile(double* Pl, int rs, int ks, int r0, i
 
   if (step != PT_BWDT) {
     const int k4n = (ne + 3) >> 2;
+    // running pointers: x_k and x_{n-1-k} of each row, the k-th rows of W_E / W_O
+    const double* px0[MT];
+    const double* px1[MT];
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      px0[i] = Ar[i] + fc * ks;
+      px1[i] = Ar[i] + (n - 1 - fc) * ks;
+    }
+    const double* pwe = W + fc * SBF + fr;
+    const double* pwo = WO + fc * SBF + fr;
+    const int kstep = 4 * ks;
 #pragma unroll 2
     for (int k4 = 0; k4 < k4n; ++k4) {
-      const int k = 4 * k4 + fc;
       double sv[MT], dv[MT];
 #pragma unroll
       for (int i = 0; i < MT; ++i) {
-        const double x0 = Ar[i][k * ks], x1 = Ar[i][(n - 1 - k) * ks];
+        const double x0 = *px0[i], x1 = *px1[i];
+        px0[i] += kstep;
+        px1[i] -= kstep;
         sv[i] = x0 + x1;
         dv[i] = x0 - x1;
       }
       double be[NTE], bo[NTE];
 #pragma unroll
       for (int j = 0; j < NTE; ++j) {
-        be[j] = W[k * SBF + 8 * j + fr];
-        bo[j] = WO[k * SBF + 8 * j + fr];
+        be[j] = pwe[8 * j];
+        bo[j] = pwo[8 * j];
       }
+      pwe += 4 * SBF;
+      pwo += 4 * SBF;
 #pragma unroll
       for (int j = 0; j < NTE; ++j)
 #pragma unroll
