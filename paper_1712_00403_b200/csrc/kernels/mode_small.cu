@@ -83,11 +83,11 @@ __device__ __forceinline__ void load_w(double* Ws, const ModeProb& pb, int tid) 
 
 // Folded W: block E = global rows [0, KPF), block O = global rows [foldh, foldh + KPF), columns
 // [0, 8*NTE) of each.
-template <int NT>
+template <int NT, int NTHREADS = STH>
 __device__ __forceinline__ void load_w_fold(double* Ws, const ModeProb& pb, int tid) {
   using S = SS<NT>;
   constexpr int CPR = S::KPF / 2;  // 16-byte chunks per row (8*NTE doubles)
-  for (int c = tid; c < 2 * S::KPF * CPR; c += STH) {
+  for (int c = tid; c < 2 * S::KPF * CPR; c += NTHREADS) {
     const int r = c / CPR, cc = (c % CPR) * 2;
     const int gr = r < S::KPF ? r : pb.foldh + (r - S::KPF);
     cp_async16g(&Ws[r * S::SBF + cc], pb.W + (size_t)gr * pb.ldw + cc);
@@ -139,7 +139,7 @@ template <int NT, bool KMAJ, bool SC = false>
 __device__ __forceinline__ void tile_compute_store(const ModeProb& pb, const Geo& g,
                                                    const double* Ws, double* A, long long t,
                                                    int lane, unsigned long long* tr);
-template <int NT, bool KMAJ>
+template <int NT, bool KMAJ, int MT = 1>
 __device__ __forceinline__ void tile_compute_store_fold(const ModeProb& pb, const Geo& g,
                                                         const double* Ws, double* A, long long t,
                                                         int lane, unsigned long long* tr);
@@ -188,10 +188,10 @@ __device__ __forceinline__ void load_panel_async(const ModeProb& pb, const Geo& 
 
 // One 8-row tile: panel load (LDG -> STS, zero fill beyond n / M), DMMAs, epilogue.
 // COHERENT: the input was written earlier in the same launch (plane pipeline): L2-coherent loads.
-template <int NT, bool KMAJ, bool COHERENT, bool SC = false, bool FOLD = false>
-__device__ __forceinline__ void do_tile(const ModeProb& pb, const Geo& g, const double* Ws,
-                                        double* A, long long t, int lane,
-                                        unsigned long long* tr) {
+// Rows 8t .. 8t+7 of the tile's panel into A ([8][SA]; LDG -> STS, zero fill beyond n / M).
+template <int NT, bool KMAJ, bool COHERENT>
+__device__ __forceinline__ void load_tile_rows(const ModeProb& pb, const Geo& g, double* A,
+                                               long long t, int lane) {
   using S = SS<NT>;
   const double* __restrict__ X = pb.X;
   const int m0 = (int)(t * 8);
@@ -287,6 +287,13 @@ __device__ __forceinline__ void do_tile(const ModeProb& pb, const Geo& g, const 
       if (k < g.kpad) A[r * S::SA + k] = v[j];
     }
   }
+}
+
+template <int NT, bool KMAJ, bool COHERENT, bool SC = false, bool FOLD = false>
+__device__ __forceinline__ void do_tile(const ModeProb& pb, const Geo& g, const double* Ws,
+                                        double* A, long long t, int lane,
+                                        unsigned long long* tr) {
+  load_tile_rows<NT, KMAJ, COHERENT>(pb, g, A, t, lane);
   __syncwarp();
   if (tr) tr[3] = gtimer();
   if constexpr (FOLD)
@@ -448,30 +455,39 @@ __device__ __forceinline__ void tile_compute_store(const ModeProb& pb, const Geo
 // transposed; its middle output (odd n) is doubled to undo the forward's 1/2. FOLD_SYM: y = A x
 // for a centrosymmetric A (the dense M_d^{-1} passes of P_Q): e = W_E^T s,
 // o = W_O^T d and the backward's output butterfly.
-template <int NT, bool KMAJ>
+template <int NT, bool KMAJ, int MT>
 __device__ __forceinline__ void tile_compute_store_fold(const ModeProb& pb, const Geo& g,
                                                         const double* Ws, double* A, long long t,
                                                         int lane, unsigned long long* tr) {
+  // MT 8-row DMMA tiles per warp (rows 8 MT t .. 8 MT t + 8 MT - 1 of the panel A) share every B
+  // fragment
   using S = SS<NT>;
   constexpr int NTE = NT / 2;
   constexpr int SBF = S::SBF;
   const double* WO = Ws + S::KPF * SBF;
   const int n = g.n, ne = (n + 1) >> 1, no = n >> 1;
   const bool full_o = ((no + 7) >> 3) == NTE;  // else the last O tile is empty
-  const int m0 = (int)(t * 8);
+  const int m0 = (int)(t * 8 * MT);
   const int fr = lane >> 2, fc = lane & 3;
-  double* Ar = A + fr * S::SA;
   const int mode = pb.fold;
-  double ae[NTE][2], ao[NTE][2];
+  double ae[MT][NTE][2], ao[MT][NTE][2];
 #pragma unroll
-  for (int j = 0; j < NTE; ++j) ae[j][0] = ae[j][1] = ao[j][0] = ao[j][1] = 0.0;
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NTE; ++j) ae[i][j][0] = ae[i][j][1] = ao[i][j][0] = ao[i][j][1] = 0.0;
 
   if (mode != FOLD_BWD) {
     const int k4n = (ne + 3) >> 2;
     for (int k4 = 0; k4 < k4n; ++k4) {
       const int k = 4 * k4 + fc;
-      const double x0 = Ar[k], x1 = Ar[n - 1 - k];  // k <= ne + 2 < n (n >= 8)
-      const double sv = x0 + x1, dv = x0 - x1;
+      double sv[MT], dv[MT];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const double* Ar = A + (8 * i + fr) * S::SA;
+        const double x0 = Ar[k], x1 = Ar[n - 1 - k];  // k <= ne + 2 < n (n >= 8)
+        sv[i] = x0 + x1;
+        dv[i] = x0 - x1;
+      }
       double be[NTE], bo[NTE];
 #pragma unroll
       for (int j = 0; j < NTE; ++j) {
@@ -479,98 +495,117 @@ __device__ __forceinline__ void tile_compute_store_fold(const ModeProb& pb, cons
         bo[j] = WO[k * SBF + 8 * j + fr];
       }
 #pragma unroll
-      for (int j = 0; j < NTE; ++j) dmma(ae[j], sv, be[j]);
+      for (int j = 0; j < NTE; ++j)
+#pragma unroll
+        for (int i = 0; i < MT; ++i) dmma(ae[i][j], sv[i], be[j]);
 #pragma unroll
       for (int j = 0; j < NTE; ++j)
-        if (j < NTE - 1 || full_o) dmma(ao[j], dv, bo[j]);
+        if (j < NTE - 1 || full_o)
+#pragma unroll
+          for (int i = 0; i < MT; ++i) dmma(ao[i][j], dv[i], bo[j]);
     }
   }
 
-  const int m = m0 + fr;
-  const bool mv = (long long)m < g.M;
-  int sidx = 0, item = 0;
-  double lrow = 0.0;
-  bool pad_row = false;
-  if (mv) {
-    row_index<KMAJ>(g, m, sidx, item, pb.yld, g.Pno);
-    if (!KMAJ && (mode == FOLD_FUSED || pb.epi == EPI_LAMBDA)) {
-      const int mi = m - item * g.Mi;
-      const int p = mi - (int)((unsigned)mi / (unsigned)g.P) * g.P;
-      const unsigned i2 = (unsigned)p / (unsigned)pb.n1;
-      const int i1 = p - (int)i2 * pb.n1;
-      pad_row = i1 >= pb.n1v;
-      if (!pad_row) lrow = pb.lam1 ? pb.lam0[i1] + pb.lam1[i2] : pb.lam0[p];
+  // per row group i: row bookkeeping, then (FUSED) the spectral panel or (FWD) the stores
+  int sidx[MT], item[MT];
+  bool mv[MT], pad_row[MT];
+  double lrow[MT];
+  long long cs = KMAJ ? 1 : g.P;
+  bool kout = KMAJ;
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    const int m = m0 + 8 * i + fr;
+    mv[i] = (long long)m < g.M;
+    sidx[i] = item[i] = 0;
+    lrow[i] = 0.0;
+    pad_row[i] = false;
+    if (mv[i]) {
+      row_index<KMAJ>(g, m, sidx[i], item[i], pb.yld, g.Pno);
+      if (!KMAJ && (mode == FOLD_FUSED || pb.epi == EPI_LAMBDA)) {
+        const int mi = m - item[i] * g.Mi;
+        const int p = mi - (int)((unsigned)mi / (unsigned)g.P) * g.P;
+        const unsigned i2 = (unsigned)p / (unsigned)pb.n1;
+        const int i1 = p - (int)i2 * pb.n1;
+        pad_row[i] = i1 >= pb.n1v;
+        if (!pad_row[i]) lrow[i] = pb.lam1 ? pb.lam0[i1] + pb.lam1[i2] : pb.lam0[p];
+      }
+      // output addressing: row base sidx, column stride cs; kout = rows contiguous in the output
+      if (pb.tio != TIO_NONE) {
+        const int mi = m - item[i] * g.Mi;
+        if (pb.tio == TIO_OUT_T) { sidx[i] = mi; cs = g.Mi; kout = false; }
+        else { sidx[i] = pb.yld * mi; cs = 1; kout = true; }
+      }
     }
   }
+  if (pb.tio == TIO_OUT_T) { cs = g.Mi; kout = false; }
+  else if (pb.tio == TIO_OUT_K) { cs = 1; kout = true; }
+  const bool vrow = !KMAJ && pb.vy && pb.tio == TIO_NONE;  // 16-byte row-pair stores
 
   if (mode == FOLD_FUSED) {
     // spectral panel [E | O] <- y / Lambda (positions >= n keep the load's zero fill)
     __syncwarp();
 #pragma unroll
-    for (int j = 0; j < NTE; ++j)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int a = 8 * j + 2 * fc + h;
-        const bool ok = mv && !pad_row;
-        if (a < ne) Ar[a] = ok ? fdp_div(ae[j][h], lrow + pb.lamcol[a]) : 0.0;
-        if (a < no) Ar[ne + a] = ok ? fdp_div(ao[j][h], lrow + pb.lamcol[ne + a]) : 0.0;
-      }
-    __syncwarp();
-  }
-
-  // output addressing: row base sidx, column stride cs; kout = rows are contiguous in the output
-  long long cs = KMAJ ? 1 : g.P;
-  bool kout = KMAJ;
-  if (pb.tio != TIO_NONE && mv) {
-    const int mi = m - item * g.Mi;
-    if (pb.tio == TIO_OUT_T) { sidx = mi; cs = g.Mi; kout = false; }
-    else { sidx = pb.yld * mi; cs = 1; kout = true; }
-  }
-  const bool vrow = !KMAJ && pb.vy && pb.tio == TIO_NONE;  // 16-byte row-pair stores
-
-  if (mode == FOLD_FWD) {
-    if (tr) tr[4] = gtimer();
-    // spectral outputs: E column a -> a, O column a -> ne + a
-    double* __restrict__ Y = pb.Y + pb.ybs * (long long)item + sidx;
-    const int ncols = kout ? pb.yld : n;  // row-major rows: their pad columns get their zeros
-    const bool lam = pb.epi == EPI_LAMBDA;
-#pragma unroll
-    for (int j = 0; j < NTE; ++j)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int a = 8 * j + 2 * fc + h;
-        if (lam) {
-          ae[j][h] = (pad_row || a >= ne) ? 0.0 : fdp_div(ae[j][h], lrow + pb.lamcol[a]);
-          ao[j][h] = (pad_row || a >= no) ? 0.0 : fdp_div(ao[j][h], lrow + pb.lamcol[ne + a]);
-        }
-      }
-    if (vrow) {
-      // rows (p, p+1), p even, adjacent: pair up with the partner lane (fr ^ 1)
-      const bool odd = fr & 1;
-      double* base = odd ? Y - 1 : Y;
-#pragma unroll
-      for (int j = 0; j < NTE; ++j) {
-        const int c = 8 * j + 2 * fc + (odd ? 1 : 0);
-        const double se = odd ? ae[j][0] : ae[j][1];
-        const double ge = __shfl_xor_sync(0xffffffffu, se, 4);
-        const double so = odd ? ao[j][0] : ao[j][1];
-        const double go = __shfl_xor_sync(0xffffffffu, so, 4);
-        if (mv && c < ne)
-          *reinterpret_cast<double2*>(base + (long long)g.P * c) =
-              odd ? make_double2(ge, ae[j][1]) : make_double2(ae[j][0], ge);
-        if (mv && c < no)
-          *reinterpret_cast<double2*>(base + (long long)g.P * (ne + c)) =
-              odd ? make_double2(go, ao[j][1]) : make_double2(ao[j][0], go);
-      }
-    } else if (mv) {
+    for (int i = 0; i < MT; ++i) {
+      double* Ar = A + (8 * i + fr) * S::SA;
+      const bool ok = mv[i] && !pad_row[i];
 #pragma unroll
       for (int j = 0; j < NTE; ++j)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int a = 8 * j + 2 * fc + h;
-          if (a < ne) Y[cs * a] = ae[j][h];
-          if (ne + a < ncols && (a < no || kout)) Y[cs * (ne + a)] = ao[j][h];
+          if (a < ne) Ar[a] = ok ? fdp_div(ae[i][j][h], lrow[i] + pb.lamcol[a]) : 0.0;
+          if (a < no) Ar[ne + a] = ok ? fdp_div(ao[i][j][h], lrow[i] + pb.lamcol[ne + a]) : 0.0;
         }
+    }
+    __syncwarp();
+  }
+
+  if (mode == FOLD_FWD) {
+    if (tr) tr[4] = gtimer();
+    const int ncols = kout ? pb.yld : n;  // row-major rows: their pad columns get their zeros
+    const bool lam = pb.epi == EPI_LAMBDA;
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      // spectral outputs: E column a -> a, O column a -> ne + a
+      double* __restrict__ Y = pb.Y + pb.ybs * (long long)item[i] + sidx[i];
+      if (lam) {
+#pragma unroll
+        for (int j = 0; j < NTE; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int a = 8 * j + 2 * fc + h;
+            ae[i][j][h] = (pad_row[i] || a >= ne) ? 0.0 : fdp_div(ae[i][j][h], lrow[i] + pb.lamcol[a]);
+            ao[i][j][h] = (pad_row[i] || a >= no) ? 0.0 : fdp_div(ao[i][j][h], lrow[i] + pb.lamcol[ne + a]);
+          }
+      }
+      if (vrow) {
+        // rows (p, p+1), p even, adjacent: pair up with the partner lane (fr ^ 1)
+        const bool odd = fr & 1;
+        double* base = odd ? Y - 1 : Y;
+#pragma unroll
+        for (int j = 0; j < NTE; ++j) {
+          const int c = 8 * j + 2 * fc + (odd ? 1 : 0);
+          const double se = odd ? ae[i][j][0] : ae[i][j][1];
+          const double ge = __shfl_xor_sync(0xffffffffu, se, 4);
+          const double so = odd ? ao[i][j][0] : ao[i][j][1];
+          const double go = __shfl_xor_sync(0xffffffffu, so, 4);
+          if (mv[i] && c < ne)
+            *reinterpret_cast<double2*>(base + (long long)g.P * c) =
+                odd ? make_double2(ge, ae[i][j][1]) : make_double2(ae[i][j][0], ge);
+          if (mv[i] && c < no)
+            *reinterpret_cast<double2*>(base + (long long)g.P * (ne + c)) =
+                odd ? make_double2(go, ao[i][j][1]) : make_double2(ao[i][j][0], go);
+        }
+      } else if (mv[i]) {
+#pragma unroll
+        for (int j = 0; j < NTE; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int a = 8 * j + 2 * fc + h;
+            if (a < ne) Y[cs * a] = ae[i][j][h];
+            if (ne + a < ncols && (a < no || kout)) Y[cs * (ne + a)] = ao[i][j][h];
+          }
+      }
     }
     __syncwarp();
     if (tr) tr[5] = gtimer();
@@ -582,85 +617,98 @@ __device__ __forceinline__ void tile_compute_store_fold(const ModeProb& pb, cons
   const bool trw = mode == FOLD_FUSED;  // the forward W read transposed
   if (mode != FOLD_SYM) {
 #pragma unroll
-    for (int j = 0; j < NTE; ++j) ae[j][0] = ae[j][1] = ao[j][0] = ao[j][1] = 0.0;
-  {
-    const int k4n = (ne + 3) >> 2;
-    for (int k4 = 0; k4 < k4n; ++k4) {
-      const int k = 4 * k4 + fc;
-      const double a = Ar[k];
-      double b[NTE];
+    for (int i = 0; i < MT; ++i)
 #pragma unroll
-      for (int j = 0; j < NTE; ++j) b[j] = trw ? Ws[(8 * j + fr) * SBF + k] : Ws[k * SBF + 8 * j + fr];
+      for (int j = 0; j < NTE; ++j) ae[i][j][0] = ae[i][j][1] = ao[i][j][0] = ao[i][j][1] = 0.0;
+    {
+      const int k4n = (ne + 3) >> 2;
+      for (int k4 = 0; k4 < k4n; ++k4) {
+        const int k = 4 * k4 + fc;
+        double a[MT];
 #pragma unroll
-      for (int j = 0; j < NTE; ++j) dmma(ae[j], a, b[j]);
+        for (int i = 0; i < MT; ++i) a[i] = A[(8 * i + fr) * S::SA + k];
+        double b[NTE];
+#pragma unroll
+        for (int j = 0; j < NTE; ++j) b[j] = trw ? Ws[(8 * j + fr) * SBF + k] : Ws[k * SBF + 8 * j + fr];
+#pragma unroll
+        for (int j = 0; j < NTE; ++j)
+#pragma unroll
+          for (int i = 0; i < MT; ++i) dmma(ae[i][j], a[i], b[j]);
+      }
     }
-  }
-  {
-    const int k4n = (no + 3) >> 2;
-    for (int k4 = 0; k4 < k4n; ++k4) {
-      const int k = 4 * k4 + fc;
-      const double a = Ar[ne + k];  // <= n + 2: inside the zeroed panel row
-      double b[NTE];
+    {
+      const int k4n = (no + 3) >> 2;
+      for (int k4 = 0; k4 < k4n; ++k4) {
+        const int k = 4 * k4 + fc;
+        double a[MT];
 #pragma unroll
-      for (int j = 0; j < NTE; ++j) b[j] = trw ? WO[(8 * j + fr) * SBF + k] : WO[k * SBF + 8 * j + fr];
+        for (int i = 0; i < MT; ++i) a[i] = A[(8 * i + fr) * S::SA + ne + k];  // <= n + 2: zeroed pad
+        double b[NTE];
 #pragma unroll
-      for (int j = 0; j < NTE; ++j)
-        if (j < NTE - 1 || full_o) dmma(ao[j], a, b[j]);
+        for (int j = 0; j < NTE; ++j) b[j] = trw ? WO[(8 * j + fr) * SBF + k] : WO[k * SBF + 8 * j + fr];
+#pragma unroll
+        for (int j = 0; j < NTE; ++j)
+          if (j < NTE - 1 || full_o)
+#pragma unroll
+            for (int i = 0; i < MT; ++i) dmma(ao[i][j], a[i], b[j]);
+      }
     }
-  }
   }
   if (tr) tr[4] = gtimer();
   // x_c = e_c + o_c, x_{n-1-c} = e_c - o_c (c < ne; the middle of an odd n is written twice with
   // the same value)
   const bool scale = pb.epi == EPI_SCALE;
   const bool mid2 = trw && (n & 1);
-  double xd[NTE][2], xm[NTE][2];
 #pragma unroll
-  for (int j = 0; j < NTE; ++j)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int c = 8 * j + 2 * fc + h;
-      double e = ae[j][h];
-      if (mid2 && c == no) e *= 2.0;
-      double v0 = e + ao[j][h], v1 = e - ao[j][h];
-      if (scale && mv && c < ne) {
-        v0 *= pb.scale[sidx + cs * c];
-        v1 *= pb.scale[sidx + cs * (n - 1 - c)];
-      }
-      xd[j][h] = v0;
-      xm[j][h] = v1;
-    }
-  double* __restrict__ Y = pb.Y + pb.ybs * (long long)item + sidx;
-  if (vrow) {
-    const bool odd = fr & 1;
-    double* base = odd ? Y - 1 : Y;
-#pragma unroll
-    for (int j = 0; j < NTE; ++j) {
-      const int c = 8 * j + 2 * fc + (odd ? 1 : 0);
-      const double sd = odd ? xd[j][0] : xd[j][1];
-      const double gd = __shfl_xor_sync(0xffffffffu, sd, 4);
-      const double sm_ = odd ? xm[j][0] : xm[j][1];
-      const double gm = __shfl_xor_sync(0xffffffffu, sm_, 4);
-      if (mv && c < ne) {
-        *reinterpret_cast<double2*>(base + (long long)g.P * c) =
-            odd ? make_double2(gd, xd[j][1]) : make_double2(xd[j][0], gd);
-        *reinterpret_cast<double2*>(base + (long long)g.P * (n - 1 - c)) =
-            odd ? make_double2(gm, xm[j][1]) : make_double2(xm[j][0], gm);
-      }
-    }
-  } else if (mv) {
+  for (int i = 0; i < MT; ++i) {
+    double xd[NTE][2], xm[NTE][2];
 #pragma unroll
     for (int j = 0; j < NTE; ++j)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int c = 8 * j + 2 * fc + h;
-        if (c < ne) {
-          Y[cs * c] = xd[j][h];
-          Y[cs * (n - 1 - c)] = xm[j][h];
+        double e = ae[i][j][h];
+        if (mid2 && c == no) e *= 2.0;
+        double v0 = e + ao[i][j][h], v1 = e - ao[i][j][h];
+        if (scale && mv[i] && c < ne) {
+          v0 *= pb.scale[sidx[i] + cs * c];
+          v1 *= pb.scale[sidx[i] + cs * (n - 1 - c)];
+        }
+        xd[j][h] = v0;
+        xm[j][h] = v1;
+      }
+    double* __restrict__ Y = pb.Y + pb.ybs * (long long)item[i] + sidx[i];
+    if (vrow) {
+      const bool odd = fr & 1;
+      double* base = odd ? Y - 1 : Y;
+#pragma unroll
+      for (int j = 0; j < NTE; ++j) {
+        const int c = 8 * j + 2 * fc + (odd ? 1 : 0);
+        const double sd = odd ? xd[j][0] : xd[j][1];
+        const double gd = __shfl_xor_sync(0xffffffffu, sd, 4);
+        const double sm_ = odd ? xm[j][0] : xm[j][1];
+        const double gm = __shfl_xor_sync(0xffffffffu, sm_, 4);
+        if (mv[i] && c < ne) {
+          *reinterpret_cast<double2*>(base + (long long)g.P * c) =
+              odd ? make_double2(gd, xd[j][1]) : make_double2(xd[j][0], gd);
+          *reinterpret_cast<double2*>(base + (long long)g.P * (n - 1 - c)) =
+              odd ? make_double2(gm, xm[j][1]) : make_double2(xm[j][0], gm);
         }
       }
-    if (kout && fc == 0)
-      for (int c = n; c < pb.yld; ++c) Y[c] = 0.0;  // zero pad column of a padded row
+    } else if (mv[i]) {
+#pragma unroll
+      for (int j = 0; j < NTE; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = 8 * j + 2 * fc + h;
+          if (c < ne) {
+            Y[cs * c] = xd[j][h];
+            Y[cs * (n - 1 - c)] = xm[j][h];
+          }
+        }
+      if (kout && fc == 0)
+        for (int c = n; c < pb.yld; ++c) Y[c] = 0.0;  // zero pad column of a padded row
+    }
   }
   __syncwarp();
   if (tr) tr[5] = gtimer();
@@ -703,6 +751,41 @@ __global__ void __launch_bounds__(STH, 1) mode_small_kernel(const __grid_constan
   const int nw = pb.ctas * SW;
   for (long long t = gw; t < pb.tiles_m; t += nw)
     do_tile<NT, KMAJ, false, SC, FOLD>(pb, g, Ws, A, t, lane, (trace && lane == 0 && t == gw) ? trace : nullptr);
+}
+
+// Folded transforms with 16-row warp tiles: two 8-row DMMA tiles share every B fragment (half the
+// shared-memory B loads per DMMA, two independent accumulator chains); 8 warps per CTA so the
+// panels fit the same shared memory as 16 warps of 8-row panels.
+constexpr int SW2 = 8;
+template <int NT, bool KMAJ>
+__global__ void __launch_bounds__(SW2 * 32, 1)
+mode_small_fold2_kernel(const __grid_constant__ ModeGroupT<kSmallGroup> grp) {
+  using S = SS<NT>;
+  extern __shared__ __align__(16) double sm[];
+  double* Ws = sm;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* A = sm + S::W_ELEMS + warp * 2 * S::ABUF;  // this warp's 16-row panel ([16][SA])
+  int pi = 0;
+#pragma unroll
+  for (int i = 1; i < kSmallGroup; ++i)
+    if (i < grp.count && (int)blockIdx.x >= grp.prob[i].cta_begin) pi = i;
+  const ModeProb& pb = grp.prob[pi];
+  const Geo g(pb);
+  load_w_fold<NT, SW2 * 32>(Ws, pb, tid);  // independent of the previous kernel
+  for (int i = lane; i < 2 * S::ABUF; i += 32) A[i] = 0.0;  // panel pad columns read as zeros
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  wait_group<0>();
+  __syncthreads();
+  const int gw = (blockIdx.x - pb.cta_begin) + pb.ctas * warp;
+  const int nw = pb.ctas * SW2;
+  const long long tiles16 = (pb.tiles_m + 1) / 2;
+  for (long long u = gw; u < tiles16; u += nw) {
+    load_tile_rows<NT, KMAJ, false>(pb, g, A, 2 * u, lane);
+    load_tile_rows<NT, KMAJ, false>(pb, g, A + 8 * S::SA, 2 * u + 1, lane);  // zero past M
+    __syncwarp();
+    tile_compute_store_fold<NT, KMAJ, 2>(pb, g, Ws, A, u, lane, nullptr);
+  }
 }
 
 // Prefetching variant: SWP = 8 warps per CTA, two panels per warp; the next tile's panel streams
@@ -859,10 +942,14 @@ cudaError_t launch_s(const ModeGroup* g, cudaStream_t s) {
     if (e == cudaSuccess && !KMAJ)
       e = cudaFuncSetAttribute(mode_small_kernel<NT, false, kSmallGroup, true>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES);
-    if constexpr (NT % 2 == 0)
+    if constexpr (NT % 2 == 0) {
       if (e == cudaSuccess)
         e = cudaFuncSetAttribute(mode_small_kernel<NT, KMAJ, kSmallGroup, false, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(mode_small_fold2_kernel<NT, KMAJ>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES);
+    }
     if (e != cudaSuccess || bytes_prefetch<NT>() > 227 * 1024) return e;
     return cudaFuncSetAttribute(mode_small_pf_kernel<NT, KMAJ, kSmallGroup>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes_prefetch<NT>());
@@ -883,9 +970,19 @@ cudaError_t launch_s(const ModeGroup* g, cudaStream_t s) {
     if (sc || NT % 2 || g->count > kSmallGroup) return cudaErrorInvalidValue;
     cfg.blockDim = dim3(STH);
     cfg.dynamicSmemBytes = S::BYTES;
-    if constexpr (NT % 2 == 0)
+    // 16-row warp tiles are opt-in (FDP_SMALL_MT=2): with about one 8-row tile per warp at batch
+    // 1 they halve the busy warps and measured slower (config 2 54.8 vs 49.4 us, config 1 16.6
+    // vs 12.5 us), unlike in the plane kernel
+    const char* mt = std::getenv("FDP_SMALL_MT");
+    const bool mt2 = mt && mt[0] == '2' && g->trace == nullptr;
+    if constexpr (NT % 2 == 0) {
+      if (mt2) {
+        cfg.blockDim = dim3(SW2 * 32);
+        return cudaLaunchKernelEx(&cfg, mode_small_fold2_kernel<NT, KMAJ>, narrow_group<kSmallGroup>(*g));
+      }
       return cudaLaunchKernelEx(&cfg, mode_small_kernel<NT, KMAJ, kSmallGroup, false, true>,
                                 narrow_group<kSmallGroup>(*g));
+    }
     return cudaErrorInvalidValue;
   }
   if (sc) {  // peer-store problems (slab exchange): non-KMAJ, single-buffered kernel
