@@ -764,12 +764,6 @@ static cudaError_t enqueue_fd_plane(const std::vector<const fdp_fd_s*>& hs,
       by += 16.0 * pq->n[0] * pq->n[1] * pq->n[2] * batch;
     }
     g.total = begin;
-    g.dmma_tail = std::getenv("FDP_PLANE_DMMA_TAIL") != nullptr;
-    {
-      const char* mt = std::getenv("FDP_PLANE_MT");
-      g.mt2 = !(mt && std::string(mt) == "1");
-    }
-    if (g.dmma_tail) rows = ((rows + 7) / 8) * 8 + 8;  // the ragged tile reads rows < round8 + 8
     const size_t smem = plane_smem_bytes(nt, sp, rows);
     if (smem > 227 * 1024) return cudaErrorInvalidValue;
     const int per_sm = smem <= 112 * 1024 ? 2 : 1;

@@ -209,8 +209,6 @@ struct PlaneGroup {
   // diagnostics: thread 0 of every CTA records %globaltimer at 8 points of its first plane into
   // trace[blockIdx * 8 + point] when non-null
   unsigned long long* trace;
-  int dmma_tail;          // experiment (FDP_PLANE_DMMA_TAIL=1): ragged last tile on the DMMA pipe
-  int mt2;                // 16-row warp tiles (FDP_PLANE_MT=1 selects 8-row tiles)
 };
 size_t plane_smem_bytes(int NT, int sp, int rows);
 int plane_stride(int n2);

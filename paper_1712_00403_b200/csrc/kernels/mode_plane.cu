@@ -66,7 +66,7 @@ enum PlaneStep : int { PT_FWD = 0, PT_FUSED = 1, PT_BWDT = 2, PT_SYM = 3 };
 //   PT_BWDT:  backward transform, W read transposed    -> spatial along k
 //   PT_SYM:   e = W_E^T s, o = W_O^T d, output butterfly (y = A x, A centrosymmetric)
 template <int NT, int MT>
-__device__ __forceinline__ void plane_tile(double* Pl, int rs, int ks, int r0, int nrows, int n,
+__device__ __noinline__ void plane_tile(double* Pl, int rs, int ks, int r0, int nrows, int n,
                                            const double* W, int step, double lbase,
                                            const double* lrowv, const double* lamcol, int lane) {
   // MT row tiles of 8 per warp share every B fragment (MT = 2: half the B loads per DMMA and two
@@ -235,7 +235,7 @@ __device__ __forceinline__ double dot4(const double* w, int wstride, const doubl
 }
 
 template <int NT>
-__device__ __forceinline__ void plane_row(double* Pl, int rs, int ks, int r, int n, const double* W,
+__device__ __noinline__ void plane_row(double* Pl, int rs, int ks, int r, int n, const double* W,
                                           int step, double lbase, const double* lrowv,
                                           const double* lamcol, double* scratch, int lane) {
   using S = PS<NT>;
@@ -305,26 +305,14 @@ template <int NT>
 __device__ __forceinline__ void plane_step(double* Pl, int rs, int ks, int nrows, int n,
                                            const double* W, int step, double lbase,
                                            const double* lrowv, const double* lamcol,
-                                           double* scratch, int warp, int lane, bool dtail,
-                                           bool mt2) {
-  if (dtail) {
-    for (int t = warp; 8 * t < nrows; t += PW)
-      plane_tile<NT, 1>(Pl, rs, ks, 8 * t, nrows, n, W, step, lbase, lrowv, lamcol, lane);
-    return;
-  }
-  int full = nrows >> 3;
-  if (mt2) {  // 16-row tiles (and one 8-row tile when the count of full 8-row tiles is odd)
-    const int f16 = full >> 1;
-    for (int t = warp; t < f16; t += PW)
-      plane_tile<NT, 2>(Pl, rs, ks, 16 * t, nrows, n, W, step, lbase, lrowv, lamcol, lane);
-    if ((full & 1) && warp == PW - 1)
-      plane_tile<NT, 1>(Pl, rs, ks, 16 * f16, nrows, n, W, step, lbase, lrowv, lamcol, lane);
-  } else {
-    for (int t = warp; t < full; t += PW)
-      plane_tile<NT, 1>(Pl, rs, ks, 8 * t, nrows, n, W, step, lbase, lrowv, lamcol, lane);
-  }
-  // leftover rows to the warps without a tile (or with the fewest)
-  const int first = mt2 ? (full >> 1) % PW : full % PW;
+                                           double* scratch, int warp, int lane) {
+  // 16-row tiles over the full 8-row tiles (an odd last one masked to its 8 rows), the leftover
+  // rows (nrows % 8) on the FMA pipe by the warps without a tile
+  const int full = nrows >> 3;
+  const int t16 = (full + 1) >> 1;
+  for (int t = warp; t < t16; t += PW)
+    plane_tile<NT, 2>(Pl, rs, ks, 16 * t, 8 * full, n, W, step, lbase, lrowv, lamcol, lane);
+  const int first = t16 % PW;
   for (int r = 8 * full + ((warp + PW - first) % PW); r < nrows; r += PW)
     plane_row<NT>(Pl, rs, ks, r, n, W, step, lbase, lrowv, lamcol, scratch + warp * 96, lane);
 }
@@ -403,16 +391,16 @@ __global__ void __launch_bounds__(PTH, 2) mode_plane_kernel(const __grid_constan
 
     const bool fd = pb.kind == 0;
     // mode 2 on the i3 rows
-    plane_step<NT>(Pl, sp, 1, n3, n2, W2, fd ? PT_FWD : PT_SYM, 0.0, nullptr, nullptr, Sc, warp, lane, grp.dmma_tail, grp.mt2);
+    plane_step<NT>(Pl, sp, 1, n3, n2, W2, fd ? PT_FWD : PT_SYM, 0.0, nullptr, nullptr, Sc, warp, lane);
     __syncthreads();
     if (tr) tr[3] = gtimer();
     // mode 3 on the a2 columns (FD: forward, Lambda, backward)
     const double lb = fd ? Lm[a1] : 0.0;
-    plane_step<NT>(Pl, 1, sp, n2, n3, W3, fd ? PT_FUSED : PT_SYM, lb, Lm + 96, Lm + 192, Sc, warp, lane, grp.dmma_tail, grp.mt2);
+    plane_step<NT>(Pl, 1, sp, n2, n3, W3, fd ? PT_FUSED : PT_SYM, lb, Lm + 96, Lm + 192, Sc, warp, lane);
     __syncthreads();
     if (tr) tr[4] = gtimer();
     if (fd) {  // mode-2 backward on the i3 rows
-      plane_step<NT>(Pl, sp, 1, n3, n2, W2, PT_BWDT, 0.0, nullptr, nullptr, Sc, warp, lane, grp.dmma_tail, grp.mt2);
+      plane_step<NT>(Pl, sp, 1, n3, n2, W2, PT_BWDT, 0.0, nullptr, nullptr, Sc, warp, lane);
       __syncthreads();
       if (tr) tr[5] = gtimer();
       double* dst = pb.T + pb.tbs * (long long)b + (long long)a1 * Mi;  // in place
