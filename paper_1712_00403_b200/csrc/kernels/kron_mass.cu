@@ -10,7 +10,7 @@
 namespace fdp {
 namespace {
 
-template <int BAND>
+template <int BAND, int U>
 __global__ void mass_solve_kernel(const MassMode mm) {
   const long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long nf = (long long)mm.P * mm.Q * mm.batch;
@@ -24,39 +24,177 @@ __global__ void mass_solve_kernel(const MassMode mm) {
   const double* __restrict__ Lb = mm.Lb;
   const double* __restrict__ invd = mm.invd;
 
+  // The recurrences are sequential in i but their loads are not: each sweep reads U fiber values
+  // ahead (U independent loads in flight per thread instead of one; with one, the HBM latency
+  // capped modes >= 2 at about half the copy bandwidth: config 5 1.30 -> 1.10 ms per mode).
+  // Mode 1 (P == 1) takes mass_solve_mode1_kernel: read-ahead on its uncoalesced fibers only
+  // thrashed L1 (3.1 vs 2.0 ms); the transposed tiles bring it to 1.6 ms.
   // forward substitution L y = x  (y written to out)
   double ring[BAND > 0 ? BAND : 1];  // ring[0] = y_{i-1}, ring[1] = y_{i-2}, ...
 #pragma unroll
   for (int j = 0; j < BAND; ++j) ring[j] = 0.0;
-  for (int i = 0; i < n; ++i) {
-    const long long idx = base + (long long)P * i;
-    double v = in[idx];
-    if (mm.pre) v *= mm.pre[sbase + (long long)P * i];
-    const double* Li = Lb + (size_t)i * (BAND + 1);
+  for (int i0 = 0; i0 < n; i0 += U) {
+    double xv[U];
 #pragma unroll
-    for (int j = 1; j <= BAND; ++j) v -= Li[BAND - j] * ring[j - 1];
-    v *= invd[i];
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u;
+      xv[u] = i < n ? in[base + (long long)P * i] : 0.0;
+      if (mm.pre && i < n) xv[u] *= mm.pre[sbase + (long long)P * i];
+    }
 #pragma unroll
-    for (int j = BAND - 1; j > 0; --j) ring[j] = ring[j - 1];
-    if (BAND > 0) ring[0] = v;
-    out[idx] = v;
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u;
+      if (i < n) {
+        double v = xv[u];
+        const double* Li = Lb + (size_t)i * (BAND + 1);
+#pragma unroll
+        for (int j = 1; j <= BAND; ++j) v -= Li[BAND - j] * ring[j - 1];
+        v *= invd[i];
+#pragma unroll
+        for (int j = BAND - 1; j > 0; --j) ring[j] = ring[j - 1];
+        if (BAND > 0) ring[0] = v;
+        out[base + (long long)P * i] = v;
+      }
+    }
   }
   // back substitution L^T z = y:  z_i = (y_i - sum_j L[i+j][i] z_{i+j}) / L[i][i]
 #pragma unroll
   for (int j = 0; j < BAND; ++j) ring[j] = 0.0;
-  for (int i = n - 1; i >= 0; --i) {
-    const long long idx = base + (long long)P * i;
-    double v = out[idx];
+  for (int i0 = n - 1; i0 >= 0; i0 -= U) {
+    double yv[U];
 #pragma unroll
-    for (int j = 1; j <= BAND; ++j) {
-      if (i + j < n) v -= Lb[(size_t)(i + j) * (BAND + 1) + (BAND - j)] * ring[j - 1];
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 - u;
+      yv[u] = i >= 0 ? out[base + (long long)P * i] : 0.0;
     }
-    v *= invd[i];
 #pragma unroll
-    for (int j = BAND - 1; j > 0; --j) ring[j] = ring[j - 1];
-    if (BAND > 0) ring[0] = v;
-    if (mm.post) v *= mm.post[sbase + (long long)P * i];
-    out[idx] = v;
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 - u;
+      if (i >= 0) {
+        double v = yv[u];
+#pragma unroll
+        for (int j = 1; j <= BAND; ++j) {
+          if (i + j < n) v -= Lb[(size_t)(i + j) * (BAND + 1) + (BAND - j)] * ring[j - 1];
+        }
+        v *= invd[i];
+#pragma unroll
+        for (int j = BAND - 1; j > 0; --j) ring[j] = ring[j - 1];
+        if (BAND > 0) ring[0] = v;
+        if (mm.post) v *= mm.post[sbase + (long long)P * i];
+        out[base + (long long)P * i] = v;
+      }
+    }
+  }
+}
+
+// Mode 1 (P == 1: each fiber contiguous): one warp per 32 consecutive fibers, chunks of 32
+// elements staged through a padded shared-memory tile so that every global access is a coalesced
+// 256-byte row segment, the recurrence of lane l running down row l of the tile (stride 33:
+// conflict-free). Same arithmetic, same order as mass_solve_kernel.
+constexpr int kM1Warps = 4;
+template <int BAND>
+__global__ void __launch_bounds__(kM1Warps * 32)
+mass_solve_mode1_kernel(const MassMode mm) {
+  __shared__ double tile[kM1Warps][32][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const long long nf = (long long)mm.Q * mm.batch;
+  const long long f0 = ((long long)blockIdx.x * kM1Warps + w) * 32;
+  if (f0 >= nf) return;
+  const int n = mm.n;
+  double (*T)[33] = tile[w];
+  // lane r holds fiber f0 + r's element-0 offsets (global, and within its batch item), shared
+  // with the warp by shuffles
+  long long my_g = 0, my_s = 0;
+  const bool my_ok = f0 + lane < nf;
+  if (my_ok) {
+    const long long f = f0 + lane, q = f % mm.Q, b = f / mm.Q;
+    my_s = (long long)n * q;
+    my_g = my_s + mm.bs * b;
+  }
+  const double* __restrict__ Lb = mm.Lb;
+  const double* __restrict__ invd = mm.invd;
+  double ring[BAND > 0 ? BAND : 1];
+#pragma unroll
+  for (int j = 0; j < BAND; ++j) ring[j] = 0.0;
+  // forward substitution L y = x, y -> out
+  for (int k0 = 0; k0 < n; k0 += 32) {
+    const int k = k0 + lane;
+    double v[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {  // 32 independent coalesced row segments in flight
+      const long long g = __shfl_sync(0xffffffffu, my_g, r);
+      const long long sb = __shfl_sync(0xffffffffu, my_s, r);
+      const bool ok = __shfl_sync(0xffffffffu, my_ok, r) && k < n;
+      v[r] = ok ? mm.in[g + k] : 0.0;
+      if (ok && mm.pre) v[r] *= mm.pre[sb + k];
+    }
+#pragma unroll
+    for (int r = 0; r < 32; ++r) T[r][lane] = v[r];
+    __syncwarp();
+    const int kend = min(32, n - k0);
+    for (int kk = 0; kk < kend; ++kk) {
+      const int i = k0 + kk;
+      double x = T[lane][kk];
+      const double* Li = Lb + (size_t)i * (BAND + 1);
+#pragma unroll
+      for (int j = 1; j <= BAND; ++j) x -= Li[BAND - j] * ring[j - 1];
+      x *= invd[i];
+#pragma unroll
+      for (int j = BAND - 1; j > 0; --j) ring[j] = ring[j - 1];
+      if (BAND > 0) ring[0] = x;
+      T[lane][kk] = x;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      const long long g = __shfl_sync(0xffffffffu, my_g, r);
+      const bool ok = __shfl_sync(0xffffffffu, my_ok, r) && k < n;
+      if (ok) mm.out[g + k] = T[r][lane];
+    }
+    __syncwarp();
+  }
+  // back substitution L^T z = y over the chunks in reverse
+#pragma unroll
+  for (int j = 0; j < BAND; ++j) ring[j] = 0.0;
+  for (int k0 = ((n - 1) / 32) * 32; k0 >= 0; k0 -= 32) {
+    const int k = k0 + lane;
+    double v[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      const long long g = __shfl_sync(0xffffffffu, my_g, r);
+      const bool ok = __shfl_sync(0xffffffffu, my_ok, r) && k < n;
+      v[r] = ok ? mm.out[g + k] : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < 32; ++r) T[r][lane] = v[r];
+    __syncwarp();
+    const int kend = min(32, n - k0);
+    for (int kk = kend - 1; kk >= 0; --kk) {
+      const int i = k0 + kk;
+      double x = T[lane][kk];
+#pragma unroll
+      for (int j = 1; j <= BAND; ++j) {
+        if (i + j < n) x -= Lb[(size_t)(i + j) * (BAND + 1) + (BAND - j)] * ring[j - 1];
+      }
+      x *= invd[i];
+#pragma unroll
+      for (int j = BAND - 1; j > 0; --j) ring[j] = ring[j - 1];
+      if (BAND > 0) ring[0] = x;
+      T[lane][kk] = x;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      const long long g = __shfl_sync(0xffffffffu, my_g, r);
+      const long long sb = __shfl_sync(0xffffffffu, my_s, r);
+      const bool ok = __shfl_sync(0xffffffffu, my_ok, r) && k < n;
+      if (ok) {
+        double x = T[r][lane];
+        if (mm.post) x *= mm.post[sb + k];
+        mm.out[g + k] = x;
+      }
+    }
+    __syncwarp();
   }
 }
 
@@ -87,7 +225,11 @@ cudaError_t launch_b(const MassMode& m, cudaStream_t s) {
   const long long blocks = (nf + threads - 1) / threads;
   if (blocks == 0) return cudaSuccess;
   if (m.forward) mass_forward_kernel<BAND><<<(unsigned)blocks, threads, 0, s>>>(m);
-  else mass_solve_kernel<BAND><<<(unsigned)blocks, threads, 0, s>>>(m);
+  else if (m.P == 1) {
+    const long long warps = (nf + 31) / 32;
+    mass_solve_mode1_kernel<BAND><<<(unsigned)((warps + kM1Warps - 1) / kM1Warps), kM1Warps * 32, 0, s>>>(m);
+  }
+  else mass_solve_kernel<BAND, 8><<<(unsigned)blocks, threads, 0, s>>>(m);
   return cudaGetLastError();
 }
 
