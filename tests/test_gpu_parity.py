@@ -68,6 +68,8 @@ def _rand_persym_spd(n, rng, shift):
     ((259, 20, 9), (2.0, 1.0, 1.0), 2, True),    # K1 folded mode 1 (KMAJ), odd n, P^G scaling
     ((12, 258, 97), (1.0, 2.0, 1.0), 1, False),  # K1 folded modes 2 and 3, Lambda on the K1 fold
     ((300, 2), (1.0, 3.0), 2, False),            # 2D, K1 folded even extent
+    ((40, 66, 71), (1.0, 1.0, 2.0), 3, True),    # plane path, n2 != n3 (one kernel NT), batch 3
+    ((9, 57, 64), (2.0, 1.0, 1.0), 1, False),    # plane path, leftover rows in both plane steps
 ])
 def test_fd_apply_folded_persymmetric(dims, coef, batch, dscale):
     """Even-odd folded transforms on random persymmetric SPD pencils: the folded
