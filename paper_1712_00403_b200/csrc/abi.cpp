@@ -208,7 +208,10 @@ extern "C" fdp_status fd_setup(int D, const int32_t* n, const double* const* K,
                           persymmetric(nd, K[d], 1e-12) && persymmetric(nd, M[d], 1e-12);
       const bool small_fold = persym && std::getenv("FDP_NO_SMALL") == nullptr &&
                               nd <= kSmallMaxN && c.tiles_n == 1;
-      const bool k1_fold = persym && !small_fold && nd > kSmallMaxN;
+      // (FDP_NO_SMALL=1 routes every extent through K1, so the folded K1 kernels also take the
+      // small extents then)
+      const bool k1_fold = persym && !small_fold &&
+                           (nd > kSmallMaxN || std::getenv("FDP_NO_SMALL") != nullptr);
       std::vector<double> lcf = lc;
       if (small_fold || k1_fold) {
         int nt = 0, foldh, ldwf, ldwb;

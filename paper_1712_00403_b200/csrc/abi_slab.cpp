@@ -38,10 +38,29 @@ extern "C" size_t fd_slab_workspace_bytes(fdp_fd h, int nranks, int rank) {
   }
 }
 
+// Even-odd folding in the slab phases: a mode is folded in every pass of a
+// slab apply or in none (its spectral order must agree between the forward pass, the eigenvalue
+// vector and the backward pass). The peer-store variant scatters from the folded K1 kernels
+// (n > 96) but not from the small-path ones, so there modes 2 and 3 fold only on the K1 path.
+static bool slab_fold(const fdp_fd_s* h, int d, bool peer) {
+  return h->fold[d] == 2 || (h->fold[d] == 1 && (!peer || d == 0));
+}
+static const double* slab_lam(const fdp_fd_s* h, int d, bool peer) {
+  return slab_fold(h, d, peer) ? h->lamcF[d] : h->lamc[d];
+}
+static TileCfg slab_cfg(const fdp_fd_s* h, int d, bool fwd, bool peer) {
+  TileCfg c = h->cfg[d];
+  if (slab_fold(h, d, peer)) {
+    if (h->fold[d] == 1) c.NT = h->fold_nt[d];
+    else c = fwd ? h->cfgFf[d] : h->cfgFb[d];
+  }
+  return c;
+}
+
 // Mode contraction of a (P, n, Q) view with the handle's direction-d matrices (batch 1).
 static ModeProb slab_prob(const fdp_fd_s* h, int d, bool fwd, const double* X, double* Y,
                           long long P, long long Q, int epi, const double* scale,
-                          const double* lam1) {
+                          const double* lam1, bool peer = false) {
   ModeProb p{};
   p.X = X;
   p.Y = Y;
@@ -59,14 +78,25 @@ static ModeProb slab_prob(const fdp_fd_s* h, int d, bool fwd, const double* X, d
   p.epi = epi;
   p.scale = scale;
   if (epi == EPI_LAMBDA || epi == EPI_FUSED) {
-    p.lam0 = h->lamc[0];
+    p.lam0 = slab_lam(h, 0, peer);
     p.lam1 = lam1;
-    p.lamcol = h->lamc[2];
+    p.lamcol = slab_lam(h, 2, peer);
   }
   const int BM = kK1Warps * 8 * h->cfg[d].MT;
   p.tiles_m = (int)((P * Q + BM - 1) / BM);
   p.tiles_n = h->cfg[d].tiles_n;
   p.fd_work = 1;
+  if (slab_fold(h, d, peer)) {
+    p.fold = epi == EPI_FUSED ? FOLD_FUSED : (fwd ? FOLD_FWD : FOLD_BWD);
+    p.W = fwd ? h->WfF[d] : h->WbF[d];
+    p.ldw = fwd ? h->ldwF[d] : h->ldwFb[d];
+    p.foldh = h->foldh[d];
+    if (h->fold[d] == 2) {
+      p.fold_k1 = 1;
+      p.tiles_n = fwd ? h->cfgFf[d].tiles_n : h->cfgFb[d].tiles_n;
+      p.tiles_ne = h->tiles_ne[d];
+    }
+  }
   return p;
 }
 
@@ -97,30 +127,30 @@ extern "C" fdp_status fd_apply_slab(fdp_fd h, int phase, int nranks, int rank, c
         FDP_CUDA(launch_scale(in, T2, dscale, n1 * n2 * nz, 1, 0, 0, s), "fd_apply_slab: prescale");
         src = T2;
       }
-      FDP_CUDA(run1(slab_prob(h, 0, true, src, T1, 1, n2 * nz, EPI_NONE, nullptr, nullptr), h->cfg[0], true, s),
+      FDP_CUDA(run1(slab_prob(h, 0, true, src, T1, 1, n2 * nz, EPI_NONE, nullptr, nullptr, false), slab_cfg(h, 0, true, false), true, s),
                "fd_apply_slab: mode 1");
-      FDP_CUDA(run1(slab_prob(h, 1, true, T1, T2, n1, nz, EPI_NONE, nullptr, nullptr), h->cfg[1], false, s),
+      FDP_CUDA(run1(slab_prob(h, 1, true, T1, T2, n1, nz, EPI_NONE, nullptr, nullptr, false), slab_cfg(h, 1, true, false), false, s),
                "fd_apply_slab: mode 2");
       FDP_CUDA(launch_slab_copy(T2, out, (int)n1, (int)n2, (int)nz, nranks, 0, nullptr, s), "fd_apply_slab: pack");
     } else if (phase == 1) {
-      const double* lam1 = h->lamc[1] + y0;
+      const double* lam1 = slab_lam(h, 1, false) + y0;
       const bool fuse = std::getenv("FDP_NO_FUSE") == nullptr && std::getenv("FDP_NO_SMALL") == nullptr &&
                         n3 <= kSmallMaxN && h->cfg[2].tiles_n == 1;
       if (fuse) {  // in place: each 8-row tile is read whole before it is written
-        FDP_CUDA(run1(slab_prob(h, 2, true, in, out, n1 * ny, 1, EPI_FUSED, nullptr, lam1), h->cfg[2], false, s),
+        FDP_CUDA(run1(slab_prob(h, 2, true, in, out, n1 * ny, 1, EPI_FUSED, nullptr, lam1, false), slab_cfg(h, 2, true, false), false, s),
                  "fd_apply_slab: fused mode 3");
       } else {
-        FDP_CUDA(run1(slab_prob(h, 2, true, in, T1, n1 * ny, 1, EPI_LAMBDA, nullptr, lam1), h->cfg[2], false, s),
+        FDP_CUDA(run1(slab_prob(h, 2, true, in, T1, n1 * ny, 1, EPI_LAMBDA, nullptr, lam1, false), slab_cfg(h, 2, true, false), false, s),
                  "fd_apply_slab: mode 3 fwd");
-        FDP_CUDA(run1(slab_prob(h, 2, false, T1, out, n1 * ny, 1, EPI_NONE, nullptr, nullptr), h->cfg[2], false, s),
+        FDP_CUDA(run1(slab_prob(h, 2, false, T1, out, n1 * ny, 1, EPI_NONE, nullptr, nullptr, false), slab_cfg(h, 2, false, false), false, s),
                  "fd_apply_slab: mode 3 bwd");
       }
     } else {
       FDP_CUDA(launch_slab_copy(in, T1, (int)n1, (int)n2, (int)nz, nranks, 1, nullptr, s), "fd_apply_slab: unpack");
-      FDP_CUDA(run1(slab_prob(h, 1, false, T1, T2, n1, nz, EPI_NONE, nullptr, nullptr), h->cfg[1], false, s),
+      FDP_CUDA(run1(slab_prob(h, 1, false, T1, T2, n1, nz, EPI_NONE, nullptr, nullptr, false), slab_cfg(h, 1, false, false), false, s),
                "fd_apply_slab: mode 2 bwd");
-      FDP_CUDA(run1(slab_prob(h, 0, false, T2, out, 1, n2 * nz, dscale ? EPI_SCALE : EPI_NONE, dscale, nullptr),
-                    h->cfg[0], true, s),
+      FDP_CUDA(run1(slab_prob(h, 0, false, T2, out, 1, n2 * nz, dscale ? EPI_SCALE : EPI_NONE, dscale, nullptr, false),
+                    slab_cfg(h, 0, false, false), true, s),
                "fd_apply_slab: mode 1 bwd");
     }
     return FDP_OK;
@@ -172,33 +202,33 @@ extern "C" fdp_status fd_apply_slab_peer(fdp_fd h, int phase, int nranks, int ra
         FDP_CUDA(launch_scale(in, T2, dscale, n1 * n2 * nz, 1, 0, 0, s), "fd_apply_slab_peer: prescale");
         src = T2;
       }
-      FDP_CUDA(run1(slab_prob(h, 0, true, src, T1, 1, n2 * nz, EPI_NONE, nullptr, nullptr), h->cfg[0], true, s),
+      FDP_CUDA(run1(slab_prob(h, 0, true, src, T1, 1, n2 * nz, EPI_NONE, nullptr, nullptr, true), slab_cfg(h, 0, true, true), true, s),
                "fd_apply_slab_peer: mode 1");
-      ModeProb p = slab_prob(h, 1, true, T1, nullptr, n1, nz, EPI_NONE, nullptr, nullptr);
+      ModeProb p = slab_prob(h, 1, true, T1, nullptr, n1, nz, EPI_NONE, nullptr, nullptr, true);
       set_scatter(p, peers, nranks, (int)n2, (int)n1, (int)z0, 1, 0, 0, 1);
-      FDP_CUDA(run1(p, h->cfg[1], false, s), "fd_apply_slab_peer: mode 2 + exchange");
+      FDP_CUDA(run1(p, slab_cfg(h, 1, true, true), false, s), "fd_apply_slab_peer: mode 2 + exchange");
     } else if (phase == 1) {
       // the mode-3 triple on the y-slab; the last contraction stores element (i1, i2, i3) straight
       // into the z-slab buffer (n1, n2, nz_g) of the rank g owning i3, at (i1, y0 + i2, i3 - z0_g)
-      const double* lam1 = h->lamc[1] + y0;
+      const double* lam1 = slab_lam(h, 1, true) + y0;
       const bool fuse = std::getenv("FDP_NO_FUSE") == nullptr && std::getenv("FDP_NO_SMALL") == nullptr &&
                         n3 <= kSmallMaxN && h->cfg[2].tiles_n == 1;
       if (fuse) {
-        ModeProb p = slab_prob(h, 2, true, in, nullptr, n1 * ny, 1, EPI_FUSED, nullptr, lam1);
+        ModeProb p = slab_prob(h, 2, true, in, nullptr, n1 * ny, 1, EPI_FUSED, nullptr, lam1, true);
         set_scatter(p, peers, nranks, (int)n3, (int)n1, (int)y0, (int)n2, 0, 1, 0);
-        FDP_CUDA(run1(p, h->cfg[2], false, s), "fd_apply_slab_peer: fused mode 3 + exchange");
+        FDP_CUDA(run1(p, slab_cfg(h, 2, true, true), false, s), "fd_apply_slab_peer: fused mode 3 + exchange");
       } else {
-        FDP_CUDA(run1(slab_prob(h, 2, true, in, T1, n1 * ny, 1, EPI_LAMBDA, nullptr, lam1), h->cfg[2], false, s),
+        FDP_CUDA(run1(slab_prob(h, 2, true, in, T1, n1 * ny, 1, EPI_LAMBDA, nullptr, lam1, true), slab_cfg(h, 2, true, true), false, s),
                  "fd_apply_slab_peer: mode 3 fwd");
-        ModeProb p = slab_prob(h, 2, false, T1, nullptr, n1 * ny, 1, EPI_NONE, nullptr, nullptr);
+        ModeProb p = slab_prob(h, 2, false, T1, nullptr, n1 * ny, 1, EPI_NONE, nullptr, nullptr, true);
         set_scatter(p, peers, nranks, (int)n3, (int)n1, (int)y0, (int)n2, 0, 1, 0);
-        FDP_CUDA(run1(p, h->cfg[2], false, s), "fd_apply_slab_peer: mode 3 bwd + exchange");
+        FDP_CUDA(run1(p, slab_cfg(h, 2, false, true), false, s), "fd_apply_slab_peer: mode 3 bwd + exchange");
       }
     } else {
-      FDP_CUDA(run1(slab_prob(h, 1, false, in, T2, n1, nz, EPI_NONE, nullptr, nullptr), h->cfg[1], false, s),
+      FDP_CUDA(run1(slab_prob(h, 1, false, in, T2, n1, nz, EPI_NONE, nullptr, nullptr, true), slab_cfg(h, 1, false, true), false, s),
                "fd_apply_slab_peer: mode 2 bwd");
-      FDP_CUDA(run1(slab_prob(h, 0, false, T2, out, 1, n2 * nz, dscale ? EPI_SCALE : EPI_NONE, dscale, nullptr),
-                    h->cfg[0], true, s),
+      FDP_CUDA(run1(slab_prob(h, 0, false, T2, out, 1, n2 * nz, dscale ? EPI_SCALE : EPI_NONE, dscale, nullptr, true),
+                    slab_cfg(h, 0, false, true), true, s),
                "fd_apply_slab_peer: mode 1 bwd");
     }
     return FDP_OK;

@@ -269,7 +269,7 @@ struct SmemF {
   static constexpr size_t BYTES = sizeof(double) * STAGE * STAGES;
 };
 
-template <int MT, int NT, bool KMAJ, int FOLD, int BKF>
+template <int MT, int NT, bool KMAJ, int FOLD, int BKF, bool SC = false>
 __global__ void __launch_bounds__(THREADS, FDP_K1_MINB)
 mode_contract_fold_kernel(const __grid_constant__ ModeGroupT<kSmallGroup> grp) {
   using S = SmemF<MT, NT, KMAJ, FOLD, BKF>;
@@ -462,7 +462,9 @@ mode_contract_fold_kernel(const __grid_constant__ ModeGroupT<kSmallGroup> grp) {
           if (oc < ncols && (a < cval || (KMAJ && !isE))) {
             double v = a < cval ? acc[i][j][h] : 0.0;
             if (epi == EPI_LAMBDA) v = (pad_row || a >= cval) ? 0.0 : fdp_div(v, lrow + pb.lamcol[oc]);
-            Y[row_off + cs * oc] = v;
+            // SC: peer-store scatter of the slab exchange
+            if (SC) *scatter_ptr(pb, m, oc) = v;
+            else Y[row_off + cs * oc] = v;
           }
         }
     } else {
@@ -478,11 +480,16 @@ mode_contract_fold_kernel(const __grid_constant__ ModeGroupT<kSmallGroup> grp) {
               v0 *= pb.scale[sidx + cs * c];
               v1 *= pb.scale[sidx + cs * (n - 1 - c)];
             }
-            Y[row_off + cs * c] = v0;
-            Y[row_off + cs * (n - 1 - c)] = v1;
+            if (SC) {
+              *scatter_ptr(pb, m, c) = v0;
+              *scatter_ptr(pb, m, n - 1 - c) = v1;
+            } else {
+              Y[row_off + cs * c] = v0;
+              Y[row_off + cs * (n - 1 - c)] = v1;
+            }
           }
         }
-      if (KMAJ && n0 == 0 && fc == 0)
+      if (KMAJ && !SC && n0 == 0 && fc == 0)
         for (int c = n; c < pb.yld; ++c) Y[row_off + c] = 0.0;  // zero pad column of a padded row
     }
   }
@@ -512,12 +519,32 @@ cudaError_t launch_t(const ModeGroup* g, cudaStream_t s) {
       e = cudaFuncSetAttribute(mode_contract_fold_kernel<MT, NT, KMAJ, FOLD_BWD, BK>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)SmemF<MT, NT, KMAJ, FOLD_BWD, BK>::BYTES);
+    if (!KMAJ && e == cudaSuccess)
+      e = cudaFuncSetAttribute(mode_contract_fold_kernel<MT, NT, false, FOLD_FWD, kFoldBK, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)SmemF<MT, NT, false, FOLD_FWD, kFoldBK>::BYTES);
+    if (!KMAJ && e == cudaSuccess)
+      e = cudaFuncSetAttribute(mode_contract_fold_kernel<MT, NT, false, FOLD_BWD, BK, true>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)SmemF<MT, NT, false, FOLD_BWD, BK>::BYTES);
     return e;
   }
   if (g->prob[0].fold != FOLD_NONE) {  // folded K1 group (host-checked: all problems, one kind)
     const int f = g->prob[0].fold;
     if (g->count > kSmallGroup || (f != FOLD_FWD && f != FOLD_BWD)) return cudaErrorInvalidValue;
     const bool bk16 = std::getenv("FDP_K1F_BK16") != nullptr;  // experiment switch
+    bool scf = false;
+    for (int i = 0; i < g->count; ++i) scf = scf || g->prob[i].peers != nullptr;
+    if (scf) {  // peer-store problems: non-KMAJ, batch 1
+      if (KMAJ) return cudaErrorInvalidValue;
+      if (f == FOLD_FWD)
+        mode_contract_fold_kernel<MT, NT, false, FOLD_FWD, kFoldBK, true>
+            <<<g->total_ctas, THREADS, SmemF<MT, NT, false, FOLD_FWD, kFoldBK>::BYTES, s>>>(narrow_group<kSmallGroup>(*g));
+      else
+        mode_contract_fold_kernel<MT, NT, false, FOLD_BWD, BK, true>
+            <<<g->total_ctas, THREADS, SmemF<MT, NT, false, FOLD_BWD, BK>::BYTES, s>>>(narrow_group<kSmallGroup>(*g));
+      return cudaGetLastError();
+    }
     if (f == FOLD_FWD && !bk16)
       mode_contract_fold_kernel<MT, NT, KMAJ, FOLD_FWD, kFoldBK>
           <<<g->total_ctas, THREADS, SmemF<MT, NT, KMAJ, FOLD_FWD, kFoldBK>::BYTES, s>>>(narrow_group<kSmallGroup>(*g));
