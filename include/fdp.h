@@ -168,7 +168,10 @@ void* fdp_host_alloc(size_t bytes);
 fdp_status fdp_host_free(void* p);
 fdp_status block_precond_destroy(fdp_block h);
 
-/* Number of kernel launches one block_precond_apply issues for `batch` (for accounting). */
+/* Number of kernel launches one block_precond_apply issues for `batch` (for accounting): exact
+ * (the kernel nodes of the CUDA graph captured for an apply of that batch size) once such an apply
+ * has run on the handle, else a static estimate of the pass structure. Returns 0 for a NULL
+ * handle or batch <= 0, -1 on an internal error. */
 int fdp_block_launch_count(fdp_block h, int64_t batch);
 
 /* Per-launch timing of block_precond_apply (roofline diagnostics). With enable != 0 every later

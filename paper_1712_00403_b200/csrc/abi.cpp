@@ -658,13 +658,19 @@ static int plane_nt(const std::vector<const fdp_fd_s*>& hs, const PresPlane* pq)
   return nt;
 }
 
+bool plane_path(const std::vector<const fdp_fd_s*>& hs, const PresPlane* pq, int64_t batch) {
+  return plane_nt(hs, pq) > 0 && (long long)hs[0]->N * batch < (1LL << 31);
+}
+
+// fuse_prescale: the inputs are not yet scaled by D^{-1/2} (dscale[k] / pq->pre): the mode-1
+// pass scales while it loads (P^G pre-scaling; saves the separate streaming launch)
 static cudaError_t enqueue_fd_plane(const std::vector<const fdp_fd_s*>& hs,
                                     const std::vector<const double*>& in, long long ibs,
                                     const std::vector<double*>& out, long long obs,
                                     const std::vector<double*>& T,
                                     const std::vector<const double*>& dscale, int64_t batch,
                                     int nt, cudaStream_t s, int* nlaunch, Recorder* rec,
-                                    const PresPlane* pq) {
+                                    const PresPlane* pq, bool fuse_prescale) {
   const size_t K = hs.size();
   // L1: mode-1 forward, plane-major output (velocity into T[k], pressure M_1^{-1} into Tq)
   {
@@ -676,6 +682,7 @@ static cudaError_t enqueue_fd_plane(const std::vector<const fdp_fd_s*>& hs,
                                   h->n[0], h->n[0]);
       p.tio = TIO_OUT_T;
       p.vy = 0;
+      if (fuse_prescale) p.pre = dscale[k];
       probs.push_back(p);
       TileCfg c = h->cfg[0];
       c.NT = h->fold_nt[0];
@@ -700,6 +707,7 @@ static cudaError_t enqueue_fd_plane(const std::vector<const fdp_fd_s*>& hs,
       p.n1 = p.n1v = pq->n[0];
       p.xld = p.yld = pq->n[0];
       p.tiles_n = 1;
+      if (fuse_prescale) p.pre = pq->pre;
       probs.push_back(p);
       cfgs.push_back(cfgs[0]);
     }
@@ -817,12 +825,13 @@ cudaError_t enqueue_fd(const std::vector<const fdp_fd_s*>& hs,
                               const std::vector<double*>& T,
                               const std::vector<const double*>& dscale, int64_t batch,
                               cudaStream_t s, int* nlaunch, Recorder* rec, const StageHook& hook, int* sync,
-                              long long sync_cap, const PresPlane* pq) {
+                              long long sync_cap, const PresPlane* pq, bool fuse_prescale) {
   const int D = hs[0]->D;
   const size_t K = hs.size();
-  if (const int nt = plane_nt(hs, pq); nt > 0 && (pq || !hook) &&
-                                       (long long)hs[0]->N * batch < (1LL << 31))
-    return enqueue_fd_plane(hs, in, ibs, out, obs, T, dscale, batch, nt, s, nlaunch, rec, pq);
+  if ((pq || !hook) && plane_path(hs, pq, batch))
+    return enqueue_fd_plane(hs, in, ibs, out, obs, T, dscale, batch, plane_nt(hs, pq), s, nlaunch,
+                            rec, pq, fuse_prescale);
+  if (fuse_prescale) return cudaErrorInvalidValue;  // callers check plane_path first
   // Stage list: forward d = 0..D-1, backward d = D-1..0. When every mode of every component is
   // small (single column tile, n <= 96) the mode-D forward / Lambda / mode-D backward triple is
   // one fused pass. Destinations alternate so that the last pass lands in `out`.
@@ -929,13 +938,15 @@ extern "C" fdp_status fd_apply(fdp_fd h, const double* b, double* x, const doubl
     DeviceGuard dg(h->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const double* src = b;
-    if (dscale) {  // x <- D^{-1/2} b, then the transforms read x
+    // plane path: the mode-1 pass applies D^{-1/2} while loading; otherwise a streaming launch
+    const bool fuse = dscale && plane_path({h}, nullptr, batch);
+    if (dscale && !fuse) {  // x <- D^{-1/2} b, then the transforms read x
       FDP_CUDA(launch_scale(b, x, dscale, h->N, batch, h->N, h->N, s), "fd_apply: prescale");
       src = x;
     }
     const bool sy = batch <= h->sync_batch;
     FDP_CUDA(enqueue_fd({h}, {src}, h->N, {x}, h->N, {T}, {dscale}, batch, s, nullptr, nullptr,
-                        nullptr, sy ? h->sync : nullptr, sy ? h->sync_cap : 0),
+                        nullptr, sy ? h->sync : nullptr, sy ? h->sync_cap : 0, nullptr, fuse),
              "fd_apply");
     return FDP_OK;
   } catch (...) {

@@ -188,7 +188,24 @@ static cudaError_t enqueue_block(fdp_block h, const double* r, double* s, int64_
   double* Tq1 = ws + toff;
   double* Tq2 = Tq1 + nq * batch;
   const double* rq = r + h->off[D];
-  if (h->pres_dense && h->dall) {
+  // plane path with P^G: the D^{-1/2} pre-scaling rides in the mode-1 pass's loads
+  PresPlane pq{};
+  const bool pplane = h->pres_dense && D == 3;
+  if (pplane) {
+    pq.n = h->pres->n;
+    pq.Tq = Tq1;
+    pq.tqbs = nq;
+    pq.out = s + h->off[D];
+    pq.obs = sz;
+    pq.scale = h->dall ? h->dall + h->off[D] : nullptr;
+    pq.Wq = h->Wq;
+    pq.q_ldw = h->q_ldw;
+    pq.q_foldh = h->q_foldh;
+    pq.q_fold = h->q_fold;
+  }
+  const bool fuse_pre = pplane && h->dall && plane_path(h->vel, &pq, batch);
+  if (fuse_pre) pq.pre = h->dall + h->off[D];
+  if (h->pres_dense && h->dall && !fuse_pre) {
     // s <- [D_V^{-1/2} | D_Q^{-1/2}] o r over the whole item (one streaming launch)
     if (rec) {
       cudaError_t e0 = rec->before(1, (double)sz * batch, 16.0 * sz * batch + 8.0 * sz);
@@ -199,7 +216,7 @@ static cudaError_t enqueue_block(fdp_block h, const double* r, double* s, int64_
     if (nlaunch) ++*nlaunch;
     for (int k = 0; k < D; ++k) in[k] = s + h->off[k];
     rq = s + h->off[D];
-  } else if (h->dv) {
+  } else if (h->dv && !fuse_pre) {
     // s_vel <- D_V^{-1/2} r_vel (one streaming launch over all velocity components)
     if (rec) {
       cudaError_t e0 = rec->before(1, (double)h->nvel * batch, 16.0 * h->nvel * batch + 8.0 * h->nvel);
@@ -253,24 +270,12 @@ static cudaError_t enqueue_block(fdp_block h, const double* r, double* s, int64_
   }
   const long long need = 2 * pp_sync_ints(h->vel, batch, h->pres_dense && D == 3 ? h->pres->n[2] : 0);
   const bool sy = h->sync && h->sync_cap >= need;
-  PresPlane pq{};
-  const bool pplane = h->pres_dense && D == 3;
   if (pplane) {
-    pq.n = h->pres->n;
     pq.rq = rq;
     pq.rbs = sz;
-    pq.Tq = Tq1;
-    pq.tqbs = nq;
-    pq.out = s + h->off[D];
-    pq.obs = sz;
-    pq.scale = h->dall ? h->dall + h->off[D] : nullptr;
-    pq.Wq = h->Wq;
-    pq.q_ldw = h->q_ldw;
-    pq.q_foldh = h->q_foldh;
-    pq.q_fold = h->q_fold;
   }
   cudaError_t e = enqueue_fd(h->vel, in, sz, out, sz, T, dsc, batch, st, nlaunch, rec, hook,
-                             sy ? h->sync : nullptr, sy ? need : 0, pplane ? &pq : nullptr);
+                             sy ? h->sync : nullptr, sy ? need : 0, pplane ? &pq : nullptr, fuse_pre);
   if (e != cudaSuccess) return e;
   if (!h->pres_dense) {
     // pressure block by banded per-mode solves: r_p -> s_p
@@ -330,6 +335,12 @@ extern "C" int block_precond_profile_read(fdp_block h, int max, int32_t* kind, f
 extern "C" int fdp_block_launch_count(fdp_block h, int64_t batch) {
   try {
     if (!h || batch <= 0) return 0;
+    {  // exact: the kernel nodes of a captured apply of this batch size
+      std::lock_guard<std::mutex> lk(h->mu);
+      for (const auto& lc : h->launch_counts)
+        if (lc.first == batch && lc.second > 0) return lc.second;
+    }
+    // no apply of this batch captured yet: the static estimate of the pass structure
     int n = 0;
     int D = h->D;
     n += h->dv ? 1 : 0;
@@ -417,11 +428,28 @@ extern "C" fdp_status block_precond_apply(fdp_block h, const double* r, double* 
         return cuda_fail(e, "block_precond_apply: enqueue");
       }
       if (e2 != cudaSuccess) return cuda_fail(e2, "block_precond_apply: capture end");
+      int kernels = 0;  // the launches one apply makes, counted from the captured graph
+      {
+        size_t nn = 0;
+        if (cudaGraphGetNodes(g, nullptr, &nn) == cudaSuccess && nn > 0) {
+          std::vector<cudaGraphNode_t> nodes(nn);
+          if (cudaGraphGetNodes(g, nodes.data(), &nn) == cudaSuccess)
+            for (size_t i = 0; i < nn; ++i) {
+              cudaGraphNodeType t;
+              if (cudaGraphNodeGetType(nodes[i], &t) == cudaSuccess && t == cudaGraphNodeTypeKernel)
+                ++kernels;
+            }
+        }
+      }
       cudaGraphExec_t ex = nullptr;
       e = cudaGraphInstantiate(&ex, g, 0);
       cudaGraphDestroy(g);
       if (e != cudaSuccess) return cuda_fail(e, "block_precond_apply: instantiate");
-      h->graphs.push_back({r, s, workspace, batch, ex, 0});
+      h->graphs.push_back({r, s, workspace, batch, ex, 0, kernels});
+      bool known = false;
+      for (auto& lc : h->launch_counts)
+        if (lc.first == batch) { lc.second = kernels; known = true; }
+      if (!known) h->launch_counts.push_back({batch, kernels});
       hit = &h->graphs.back();
     }
     hit->used = ++h->tick;

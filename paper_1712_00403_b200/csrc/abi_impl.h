@@ -217,8 +217,10 @@ struct fdp_block_s {
     int64_t batch;
     cudaGraphExec_t exec;
     unsigned long long used;
+    int kernels;  // kernel nodes of the captured apply (fdp_block_launch_count)
   };
   std::vector<GraphEntry> graphs;  // small LRU cache keyed by (r, s, workspace, batch)
+  std::vector<std::pair<int64_t, int>> launch_counts;  // (batch, kernels) of captured applies
   unsigned long long tick = 0;
   // plane-pipeline counters (zeroed at allocation, self-resetting)
   int* sync = nullptr;
@@ -287,7 +289,11 @@ struct PresPlane {
   const int* q_ldw;
   const int* q_foldh;
   const int* q_fold;
+  const double* pre;              // D_Q^{-1/2} fused into the mode-1 pass (when the block's
+                                  // pre-scaling launch is skipped), else NULL
 };
+// True when enqueue_fd will take the plane path for these handles (and pressure).
+bool plane_path(const std::vector<const fdp_fd_s*>& hs, const PresPlane* pq, int64_t batch);
 cudaError_t enqueue_fd(const std::vector<const fdp_fd_s*>& hs,
                        const std::vector<const double*>& in, long long ibs,
                        const std::vector<double*>& out, long long obs,
@@ -295,7 +301,8 @@ cudaError_t enqueue_fd(const std::vector<const fdp_fd_s*>& hs,
                        const std::vector<const double*>& dscale, int64_t batch,
                        cudaStream_t s, int* nlaunch, Recorder* rec = nullptr,
                        const StageHook& hook = nullptr, int* sync = nullptr,
-                       long long sync_cap = 0, const PresPlane* pq = nullptr);
+                       long long sync_cap = 0, const PresPlane* pq = nullptr,
+                       bool fuse_prescale = false);
 cudaError_t enqueue_mass(const fdp_mass_s* h, int mode, const double* in, double* out,
                          long long bs, const double* dscale, int64_t batch, cudaStream_t s,
                          int* nlaunch, Recorder* rec = nullptr);

@@ -199,11 +199,14 @@ __device__ __forceinline__ void load_tile_rows(const ModeProb& pb, const Geo& g,
     int mi, b0;
     row_index<true>(g, m0, mi, b0, 1, 0);  // fiber index of the tile's first row
     const double* src[8];
+    const double* pre[8];
     bool rv[8];
+    const bool scaled = pb.pre != nullptr;
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       rv[r] = (long long)m0 + r < g.M;
       src[r] = X + ((long long)pb.xld * mi + pb.xbs * b0);
+      pre[r] = scaled ? pb.pre + (long long)pb.xld * mi : nullptr;
       if (++mi == g.Mi) { mi = 0; ++b0; }
     }
     if (pb.vx) {
@@ -218,6 +221,15 @@ __device__ __forceinline__ void load_tile_rows(const ModeProb& pb, const Geo& g,
           v[c][r] = (rv[r] && k < g.n) ? (COHERENT ? __ldcg(reinterpret_cast<const double2*>(src[r] + k))
                                                  : __ldg(reinterpret_cast<const double2*>(src[r] + k)))
                                       : make_double2(0.0, 0.0);
+        if (scaled) {
+#pragma unroll
+          for (int r = 0; r < 8; ++r)
+            if (rv[r] && k < g.n) {
+              const double2 w = __ldg(reinterpret_cast<const double2*>(pre[r] + k));
+              v[c][r].x *= w.x;
+              v[c][r].y *= (k + 1 < g.n) ? w.y : 0.0;  // the pad column stays 0
+            }
+        }
       }
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
@@ -234,6 +246,11 @@ __device__ __forceinline__ void load_tile_rows(const ModeProb& pb, const Geo& g,
         const int k = 32 * c + lane;
 #pragma unroll
         for (int r = 0; r < 8; ++r) v[c][r] = (c < g.nch && rv[r] && k < g.n) ? ldx<COHERENT>(src[r] + k) : 0.0;
+        if (scaled) {
+#pragma unroll
+          for (int r = 0; r < 8; ++r)
+            if (c < g.nch && rv[r] && k < g.n) v[c][r] *= __ldg(pre[r] + k);
+        }
       }
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
