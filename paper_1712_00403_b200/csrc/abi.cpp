@@ -775,6 +775,10 @@ static cudaError_t enqueue_fd_plane(const std::vector<const fdp_fd_s*>& hs,
       by += 16.0 * pq->n[0] * pq->n[1] * pq->n[2] * batch;
     }
     g.total = begin;
+    {  // E / O warp pairs: opt-in (measured slower: config 2 53.8 vs 50.3 us, config 3 64.5 vs 59.4)
+      const char* eo = std::getenv("FDP_PLANE_EO");
+      g.eo = eo && eo[0] == '1';
+    }
     const size_t smem = plane_smem_bytes(nt, sp, rows);
     if (smem > 227 * 1024) return cudaErrorInvalidValue;
     const int per_sm = smem <= 112 * 1024 ? 2 : 1;

@@ -212,6 +212,7 @@ struct PlaneGroup {
   // diagnostics: thread 0 of every CTA records %globaltimer at 8 points of its first plane into
   // trace[blockIdx * 8 + point] when non-null
   unsigned long long* trace;
+  int eo;                 // 16-row tiles split over E / O warp pairs (opt-in, FDP_PLANE_EO=1)
 };
 size_t plane_smem_bytes(int NT, int sp, int rows);
 int plane_stride(int n2);
