@@ -250,6 +250,10 @@ struct KronFactor {
   TileCfg cfg{};
   std::vector<double> diag;  // F[i][i] for i < min(nin, nout) (kron_op_diagonal)
   double* W = nullptr;  // W[k][a] = F[a][k], kpad x ldw
+  // banded copy (bw > 0): row a's nonzeros F[a][lo[a] .. lo[a] + bw) (K4, kernels/kron_band.cu)
+  int bw = 0;
+  int* lo = nullptr;
+  double* Wb = nullptr;
 };
 
 struct fdp_kron_s {

@@ -8,8 +8,69 @@
 
 static void free_kron(fdp_kron h) {
   if (!h) return;
-  for (auto& k : h->f) cudaFree(k.W);
+  for (auto& k : h->f) {
+    cudaFree(k.W);
+    cudaFree(k.lo);
+    cudaFree(k.Wb);
+  }
   delete h;
+}
+
+// Banded copy of a factor (column-major nout x nin): per output row the contiguous range that
+// holds its nonzeros, widened to the widest row (bw) and shifted to stay inside [0, nin). Used
+// for large extents (the dense contraction's 2 n_in flops per output exceed the band's by n/bw);
+// FDP_KRON_BAND=0 / 1 disables / forces it.
+static fdp_status kron_band_setup(KronFactor& kf, const double* F) {
+  const char* env = std::getenv("FDP_KRON_BAND");
+  if (env && env[0] == '0') return FDP_OK;
+  const int nin = kf.nin, nout = kf.nout;
+  std::vector<int> lo(nout, 0);
+  int bw = 0;
+  for (int a = 0; a < nout; ++a) {
+    int l = -1, h = -1;
+    for (int k = 0; k < nin; ++k)
+      if (F[a + (size_t)nout * k] != 0.0) {
+        if (l < 0) l = k;
+        h = k;
+      }
+    lo[a] = l < 0 ? 0 : l;
+    bw = std::max(bw, l < 0 ? 1 : h - l + 1);
+  }
+  const bool force = env && env[0] == '1';
+  if (!(bw <= 32 && (force || (nin >= 128 && 4 * bw <= nin)))) return FDP_OK;
+  std::vector<double> wb((size_t)nout * bw, 0.0);
+  for (int a = 0; a < nout; ++a) {
+    lo[a] = std::min(lo[a], nin - bw);
+    for (int j = 0; j < bw; ++j) wb[(size_t)a * bw + j] = F[a + (size_t)nout * (lo[a] + j)];
+  }
+  fdp_status st;
+  if ((st = dalloc(&kf.Wb, wb.size()))) return st;
+  int* dlo = nullptr;
+  if (cudaMalloc(&dlo, (size_t)nout * sizeof(int)) != cudaSuccess) return fail(FDP_ERR_OOM, "kron_op_setup: band");
+  kf.lo = dlo;
+  cudaError_t e = cudaMemcpy(kf.Wb, wb.data(), wb.size() * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(kf.lo, lo.data(), lo.size() * sizeof(int), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(e, "kron_op_setup: band upload");
+  kf.bw = bw;
+  return FDP_OK;
+}
+
+// Launch the banded problems of a stage, grouped kBandMax per launch.
+static cudaError_t launch_band_probs(std::vector<BandProb>& bp, cudaStream_t s) {
+  for (size_t i = 0; i < bp.size(); i += kBandMax) {
+    BandGroup g{};
+    g.count = (int)std::min<size_t>(kBandMax, bp.size() - i);
+    int blk = 0;
+    for (int j = 0; j < g.count; ++j) {
+      g.prob[j] = bp[i + j];
+      g.prob[j].blk_begin = blk;
+      blk += kron_band_blocks((long long)g.prob[j].P * g.prob[j].nout * g.prob[j].Q);
+    }
+    g.total_blocks = blk;
+    cudaError_t e = launch_kron_band(g, s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 extern "C" fdp_status kron_op_setup(int D, int nterms, const int32_t* nin, const int32_t* nout,
@@ -63,6 +124,10 @@ extern "C" fdp_status kron_op_setup(int D, int nterms, const int32_t* nin, const
           free_kron(raw);
           return st ? st : cuda_fail(e, "kron_op_setup: upload");
         }
+        if ((st = kron_band_setup(kf, F))) {
+          free_kron(raw);
+          return st;
+        }
       }
     *out = raw;
     return FDP_OK;
@@ -114,6 +179,25 @@ extern "C" fdp_status kron_op_apply(fdp_kron h, const double* x, int64_t xbs, do
         const bool last = d == D - 1;
         double* dst = last ? y : buf[d % 2];
         const long long dbs = last ? ybs : P * kf.nout * Q;
+        if (kf.bw > 0 && batch == 1) {
+          std::vector<BandProb> bp(1);
+          BandProb& b = bp[0];
+          b.X = src;
+          b.Y = dst;
+          b.Wb = kf.Wb;
+          b.lo = kf.lo;
+          b.bw = kf.bw;
+          b.P = (int)P;
+          b.nin = kf.nin;
+          b.nout = kf.nout;
+          b.Q = (int)Q;
+          b.alpha = last ? alpha * h->coef[t] : 1.0;
+          b.beta = last ? (t == 0 ? beta : 1.0) : 0.0;
+          FDP_CUDA(launch_band_probs(bp, s), "kron_op_apply: band");
+          src = dst;
+          sbs = dbs;
+          continue;
+        }
         ModeProb p{};
         p.X = src;
         p.Y = dst;
@@ -227,6 +311,7 @@ static cudaError_t enqueue_kron_tasks(const std::vector<KronTask>& tasks, double
   for (int d = 0; d < D; ++d) {
     std::vector<ModeProb> probs;
     std::vector<TileCfg> cfgs;
+    std::vector<BandProb> bands;
     for (const Term& tm : terms) {
       const fdp_kron_s* op = tm.op;
       const KronFactor& kf = op->f[tm.t * D + d];
@@ -234,6 +319,22 @@ static cudaError_t enqueue_kron_tasks(const std::vector<KronTask>& tasks, double
       for (int e = 0; e < d; ++e) P *= op->nout[e];
       for (int e = d + 1; e < D; ++e) Q *= op->nin[e];
       const bool last = d == D - 1;
+      if (kf.bw > 0) {
+        BandProb b{};
+        b.X = d == 0 ? tm.x : tm.T[(d - 1) % 2];
+        b.Y = last ? tm.part : tm.T[d % 2];
+        b.Wb = kf.Wb;
+        b.lo = kf.lo;
+        b.bw = kf.bw;
+        b.P = (int)P;
+        b.nin = kf.nin;
+        b.nout = kf.nout;
+        b.Q = (int)Q;
+        b.alpha = last ? tm.scale : 1.0;
+        b.beta = 0.0;
+        bands.push_back(b);
+        continue;
+      }
       ModeProb p{};
       p.X = d == 0 ? tm.x : tm.T[(d - 1) % 2];
       p.Y = last ? tm.part : tm.T[d % 2];
@@ -260,7 +361,8 @@ static cudaError_t enqueue_kron_tasks(const std::vector<KronTask>& tasks, double
       probs.push_back(p);
       cfgs.push_back(kf.cfg);
     }
-    cudaError_t e = launch_stage(probs, cfgs, d == 0, s, nullptr, nullptr);
+    cudaError_t e = probs.empty() ? cudaSuccess : launch_stage(probs, cfgs, d == 0, s, nullptr, nullptr);
+    if (e == cudaSuccess && !bands.empty()) e = launch_band_probs(bands, s);
     if (e != cudaSuccess) return e;
   }
   std::vector<std::pair<double*, long long>> outs;

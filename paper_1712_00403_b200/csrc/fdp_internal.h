@@ -220,6 +220,25 @@ cudaError_t launch_mode_plane(const PlaneGroup& g, int NT, size_t smem, cudaStre
 cudaError_t prepare_mode_plane(int NT, size_t smem);
 cudaError_t prepare_mode_small(int NT);
 
+// Banded m-mode products (kernels/kron_band.cu): factor rows stored as their nonzero band.
+struct BandProb {
+  const double* X;
+  double* Y;
+  const double* Wb;   // nout x bw: Wb[a*bw + j] = F[a][lo[a] + j]
+  const int* lo;      // first input index of row a's band (lo[a] + bw <= nin)
+  int bw, P, nin, nout, Q;
+  double alpha, beta; // Y = alpha * result + beta * Y
+  int blk_begin;
+};
+constexpr int kBandMax = 32;
+struct BandGroup {
+  BandProb prob[kBandMax];
+  int count;
+  int total_blocks;
+};
+cudaError_t launch_kron_band(const BandGroup& g, cudaStream_t s);
+int kron_band_blocks(long long outputs);
+
 // y[b*ys + i] = x[b*xs + i] * s[i], i < N  (P^G pre-scaling), over `batch` items.
 cudaError_t launch_scale(const double* x, double* y, const double* s, long long N, long long batch,
                          long long xs, long long ys, cudaStream_t st);

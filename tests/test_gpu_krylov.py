@@ -44,6 +44,36 @@ def test_kron_op_rectangular_terms(nin, nout):
         assert rel(Y[b].cpu().numpy(), ref) < 1e-13
 
 
+@pytest.mark.parametrize("nin,nout,bw", [((130, 9, 7), (128, 9, 5), 5), ((9, 200, 6), (11, 190, 6), 9),
+                                         ((7, 5, 300), (6, 4, 301), 3)])
+def test_kron_op_banded_factors(nin, nout, bw):
+    """Banded factors (K4 path: nonzeros in a band of width <= bw around a skewed diagonal, the
+    B-spline Gram / mixed-matrix pattern) on the single and the grouped apply, vs the oracle."""
+    rng = np.random.default_rng(sum(nin) + bw)
+
+    def banded(o, i):
+        F = rng.standard_normal((o, i))
+        for a in range(o):
+            c = int(round(a * (i - 1) / max(o - 1, 1)))
+            lo, hi = max(0, c - bw // 2), min(i, c - bw // 2 + bw)
+            F[a, :lo] = 0.0
+            F[a, hi:] = 0.0
+        return F
+
+    terms = [[banded(o, i) for i, o in zip(nin, nout)] for _ in range(2)]
+    coef = [0.75, -1.25]
+    op = fdp.KronOp(terms, coef)
+    x = rng.standard_normal(int(np.prod(nin)))
+    y0 = rng.standard_normal(int(np.prod(nout)))
+    ref = 0.5 * y0 + 2.0 * sum(c * okron.kron_matvec(list(reversed(T)), x) for c, T in zip(coef, terms))
+    Y = dev(y0)
+    op.apply(dev(x), Y, alpha=2.0, beta=0.5)
+    assert rel(Y.cpu().numpy(), ref) < 1e-13
+    Y = dev(y0)
+    fdp.KronOp.apply_group([op], [dev(x)], [Y], [2.0], beta=0.5)
+    assert rel(Y.cpu().numpy(), ref) < 1e-13
+
+
 def test_kron_ops_grouped_matches_single():
     """kron_ops_apply: shared outputs accumulate, distinct outputs stay separate, beta applies once."""
     rng = np.random.default_rng(11)
@@ -74,8 +104,13 @@ def _coef(op):
     return op._coef
 
 
+@pytest.mark.parametrize("band", [None, "1", "0"])
 @pytest.mark.parametrize("cid", [1, 2, 3])
-def test_stokes_operator_matches_oracle(cid):
+def test_stokes_operator_matches_oracle(cid, band, monkeypatch):
+    """The GPU Stokes operator (grouped and per-operator) vs the oracle's; band: the banded K4
+    factors forced on ("1", every factor of these configs is banded) or off ("0")."""
+    if band is not None:
+        monkeypatch.setenv("FDP_KRON_BAND", band)
     w = synth.CONFIGS[cid]
     nu_o = ostokes.config3_nu_terms(w.dim) if w.variable_nu else None
     nu_g = synth.viscosity_separable(w.dim) if w.variable_nu else None
