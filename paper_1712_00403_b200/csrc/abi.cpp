@@ -648,7 +648,16 @@ long long pp_sync_ints(const std::vector<const fdp_fd_s*>& hs, int64_t batch, in
 static int plane_nt(const std::vector<const fdp_fd_s*>& hs, const PresPlane* pq) {
   if (std::getenv("FDP_NO_PLANE") || std::getenv("FDP_NO_FUSE") || std::getenv("FDP_NO_SMALL"))
     return 0;
-  if (hs.empty() || hs.size() + (pq ? 1 : 0) > (size_t)kPlaneMax || hs[0]->D != 3) return 0;
+  if (hs.empty() || hs.size() + (pq ? 1 : 0) > (size_t)kPlaneMax) return 0;
+  if (hs[0]->D == 2) {  // the whole component is the plane: both modes folded, one kernel NT
+    const int nt = hs[0]->fold_nt[0];
+    for (const fdp_fd_s* h : hs)
+      if (h->D != 2 || h->fold[0] != 1 || h->fold[1] != 1 || h->fold_nt[0] != nt || h->fold_nt[1] != nt)
+        return 0;
+    if (pq && !(pq->q_fold[0] && pq->q_fold[1])) return 0;
+    return nt;
+  }
+  if (hs[0]->D != 3) return 0;
   const int nt = hs[0]->fold_nt[1];
   for (const fdp_fd_s* h : hs) {
     if (h->fold[0] != 1 || h->fold[1] != 1 || h->fold[2] != 1) return 0;
@@ -656,6 +665,14 @@ static int plane_nt(const std::vector<const fdp_fd_s*>& hs, const PresPlane* pq)
   }
   if (pq && !(pq->q_fold[0] && pq->q_fold[1] && pq->q_fold[2])) return 0;
   return nt;
+}
+
+// Plane buffer rows: n3, or more when an odd count of 8-row tiles makes the last (masked) 16-row
+// tile of the row step read past row n3, or that of the column step read past the last row's
+// end (columns up to 16 * t16(n2) - 1 of the last row).
+static int plane_rows(int n2, int n3, int sp) {
+  auto t16 = [](int n) { return ((n >> 3) + 1) >> 1; };
+  return std::max({n3, 16 * t16(n3), n3 - 1 + (16 * t16(n2) + sp - 1) / sp});
 }
 
 bool plane_path(const std::vector<const fdp_fd_s*>& hs, const PresPlane* pq, int64_t batch) {
@@ -672,6 +689,84 @@ static cudaError_t enqueue_fd_plane(const std::vector<const fdp_fd_s*>& hs,
                                     int nt, cudaStream_t s, int* nlaunch, Recorder* rec,
                                     const PresPlane* pq, bool fuse_prescale) {
   const size_t K = hs.size();
+  if (hs[0]->D == 2) {  // one launch: each component (and P_Q) a plane per batch item
+    PlaneGroup g{};
+    int sp = 4, rows = 8, begin = 0;
+    double fl = 0.0, by = 0.0;
+    for (size_t k = 0; k < K; ++k) {
+      const fdp_fd_s* h = hs[k];
+      PlaneProb& q = g.prob[g.count++];
+      q.kind = 2;
+      q.X = in[k];
+      q.xbs = ibs;
+      q.pre = fuse_prescale ? dscale[k] : nullptr;
+      q.Y = out[k];
+      q.ybs = obs;
+      q.scale = dscale[k];
+      q.W2 = h->WfF[0];
+      q.W3 = h->WfF[1];
+      q.ldw2 = h->ldwF[0];
+      q.foldh2 = h->foldh[0];
+      q.ldw3 = h->ldwF[1];
+      q.foldh3 = h->foldh[1];
+      q.lam2 = h->lamcF[0];  // Lambda = lambda_1[row of the column step] + lambda_2[column]
+      q.lam3 = h->lamcF[1];
+      q.n1 = 1;
+      q.n2 = h->n[0];
+      q.n3 = h->n[1];
+      q.batch = (int)batch;
+      q.sp = plane_stride(q.n2);
+      q.plane_begin = begin;
+      begin += (int)batch;
+      sp = std::max(sp, q.sp);
+      rows = std::max(rows, plane_rows(q.n2, q.n3, q.sp));
+      for (int d = 0; d < 2; ++d) {
+        const double ne = (h->n[d] + 1) / 2, no = h->n[d] / 2;
+        fl += 2.0 * 2.0 * (double)(h->N / h->n[d]) * batch * (ne * ne + no * no);
+      }
+      by += 16.0 * h->N * batch;
+    }
+    if (pq) {
+      PlaneProb& q = g.prob[g.count++];
+      q.kind = 3;
+      q.X = pq->rq;
+      q.xbs = pq->rbs;
+      q.pre = fuse_prescale ? pq->pre : nullptr;
+      q.Y = pq->out;
+      q.ybs = pq->obs;
+      q.scale = pq->scale;
+      q.W2 = pq->Wq[0];
+      q.W3 = pq->Wq[1];
+      q.ldw2 = pq->q_ldw[0];
+      q.foldh2 = pq->q_foldh[0];
+      q.ldw3 = pq->q_ldw[1];
+      q.foldh3 = pq->q_foldh[1];
+      q.n1 = 1;
+      q.n2 = pq->n[0];
+      q.n3 = pq->n[1];
+      q.batch = (int)batch;
+      q.sp = plane_stride(q.n2);
+      q.plane_begin = begin;
+      begin += (int)batch;
+      sp = std::max(sp, q.sp);
+      rows = std::max(rows, plane_rows(q.n2, q.n3, q.sp));
+      by += 16.0 * pq->n[0] * pq->n[1] * batch;
+    }
+    g.total = begin;
+    const size_t smem = plane_smem_bytes(nt, sp, rows);
+    if (smem > 227 * 1024) return cudaErrorInvalidValue;
+    const int per_sm = smem <= 112 * 1024 ? 2 : 1;
+    g.grid = std::min(g.total, per_sm * num_sms());
+    if (rec) {
+      cudaError_t e0 = rec->before(0, fl, by);
+      if (e0 != cudaSuccess) return e0;
+    }
+    g.trace = nullptr;
+    cudaError_t e = launch_mode_plane(g, nt, smem, s);
+    if (e != cudaSuccess) return e;
+    if (nlaunch) ++*nlaunch;
+    return cudaSuccess;
+  }
   // L1: mode-1 forward, plane-major output (velocity into T[k], pressure M_1^{-1} into Tq)
   {
     std::vector<ModeProb> probs;
@@ -742,7 +837,7 @@ static cudaError_t enqueue_fd_plane(const std::vector<const fdp_fd_s*>& hs,
       q.plane_begin = begin;
       begin += q.n1 * (int)batch;
       sp = std::max(sp, q.sp);
-      rows = std::max(rows, q.n3);  // full tiles and leftover rows never read past row n3
+      rows = std::max(rows, plane_rows(q.n2, q.n3, q.sp));
       for (int d = 1; d < 3; ++d) {  // forward + backward folded transforms of modes 2 and 3
         const double ne = (h->n[d] + 1) / 2, no = h->n[d] / 2;
         fl += 2.0 * 2.0 * (double)(h->N / h->n[d]) * batch * (ne * ne + no * no);
@@ -771,7 +866,7 @@ static cudaError_t enqueue_fd_plane(const std::vector<const fdp_fd_s*>& hs,
       q.plane_begin = begin;
       begin += q.n1 * (int)batch;
       sp = std::max(sp, q.sp);
-      rows = std::max(rows, q.n3);
+      rows = std::max(rows, plane_rows(q.n2, q.n3, q.sp));
       by += 16.0 * pq->n[0] * pq->n[1] * pq->n[2] * batch;
     }
     g.total = begin;

@@ -190,7 +190,7 @@ static cudaError_t enqueue_block(fdp_block h, const double* r, double* s, int64_
   const double* rq = r + h->off[D];
   // plane path with P^G: the D^{-1/2} pre-scaling rides in the mode-1 pass's loads
   PresPlane pq{};
-  const bool pplane = h->pres_dense && D == 3;
+  const bool pplane = h->pres_dense && (D == 3 || D == 2);
   if (pplane) {
     pq.n = h->pres->n;
     pq.Tq = Tq1;

@@ -182,10 +182,12 @@ cudaError_t launch_mode_pp(const ModeGroup& g1, const ModeGroup& g2, const Plane
 // then 2 * ceil(ceil(n/2) / 8) (even).
 cudaError_t launch_mode_small(const ModeGroup& g, int NT, bool kmaj, cudaStream_t s);
 
-// Plane kernel (D = 3, kernels/mode_plane.cu): per plane a1 of a plane-major tensor (written by a
+// Plane kernel (kernels/mode_plane.cu). D = 3: per plane a1 of a plane-major tensor (written by a
 // TIO_OUT_T mode-1 pass), the folded mode-2 forward, mode-3 forward / Lambda^{-1} / backward and
 // mode-2 backward in shared memory (kind 0, in place), or the FOLD_SYM mode-2 and mode-3 passes
-// of P_Q with the result stored in the natural layout (kind 1).
+// of P_Q with the result stored in the natural layout (kind 1). D = 2: the whole component is one
+// plane (rows = i2 lines): the complete folded FD apply (kind 2) or P_Q (kind 3) in one launch,
+// natural-layout input and output.
 struct PlaneProb {
   double* T;              // plane-major tensor: item b, plane a1 at T + b * tbs + a1 * n2 * n3
   long long tbs;
@@ -198,10 +200,15 @@ struct PlaneProb {
   int n1, n2, n3, batch;
   int sp;                 // shared-memory row stride of the plane
   int kind;
-  double* Y;              // kind 1: output (natural layout), batch stride ybs, optional scale
+  double* Y;              // kinds 1-3: output (natural layout), batch stride ybs, optional scale
   long long ybs;
   const double* scale;
   int plane_begin;        // first plane of this problem in the grouped grid
+  // kinds 2 / 3 (D = 2, the whole component is the plane): input in the natural layout (i1
+  // fastest = the plane's rows), batch stride xbs, optional pre-scaling
+  const double* X;
+  long long xbs;
+  const double* pre;
 };
 constexpr int kPlaneMax = 8;
 struct PlaneGroup {

@@ -479,8 +479,9 @@ __global__ void __launch_bounds__(PTH, 2) mode_plane_kernel(const __grid_constan
   // the eigenvalues next to W (a cold-L2 apply otherwise pays an HBM round trip per warp in the
   // Lambda epilogue)
   auto load_lam = [&](const PlaneProb& pb) {
-    if (pb.kind != 0) return;
-    for (int i = tid; i < pb.n1; i += PTH) cp_async8(&Lm[i], pb.lam1 + i);
+    if (pb.kind != 0 && pb.kind != 2) return;
+    if (pb.lam1)
+      for (int i = tid; i < pb.n1; i += PTH) cp_async8(&Lm[i], pb.lam1 + i);
     for (int i = tid; i < pb.n2; i += PTH) cp_async8(&Lm[96 + i], pb.lam2 + i);
     for (int i = tid; i < pb.n3; i += PTH) cp_async8(&Lm[192 + i], pb.lam3 + i);
   };
@@ -526,23 +527,33 @@ __global__ void __launch_bounds__(PTH, 2) mode_plane_kernel(const __grid_constan
     const int Mi = n2 * n3;
     const int local = gp - pb.plane_begin;
     const int a1 = local % n1, b = local / n1;
-    const double* src = pb.T + pb.tbs * (long long)b + (long long)a1 * Mi;
-    for (int e = tid; e < Mi; e += PTH) {
-      const int i3 = e / n2, i2 = e - i3 * n2;
-      cp_async8(&Pl[i3 * sp + i2], src + e);
+    const bool d2 = pb.kind >= 2;  // D = 2: natural-layout input, optional pre-scaling
+    const double* src = d2 ? pb.X + pb.xbs * (long long)b
+                           : pb.T + pb.tbs * (long long)b + (long long)a1 * Mi;
+    if (d2 && pb.pre) {
+      for (int e = tid; e < Mi; e += PTH) {
+        const int i3 = e / n2, i2 = e - i3 * n2;
+        Pl[i3 * sp + i2] = __ldg(src + e) * __ldg(pb.pre + e);
+      }
+    } else {
+      for (int e = tid; e < Mi; e += PTH) {
+        const int i3 = e / n2, i2 = e - i3 * n2;
+        cp_async8(&Pl[i3 * sp + i2], src + e);
+      }
     }
     commit();
     wait_all();
     __syncthreads();
     if (tr) tr[2] = gtimer();
 
-    const bool fd = pb.kind == 0;
+    const bool fd = pb.kind == 0 || pb.kind == 2;
     // mode 2 on the i3 rows
     plane_step<NT>(Pl, sp, 1, n3, n2, W2, fd ? PT_FWD : PT_SYM, 0.0, nullptr, nullptr, Sc, warp, lane, grp.eo);
     __syncthreads();
     if (tr) tr[3] = gtimer();
-    // mode 3 on the a2 columns (FD: forward, Lambda, backward)
-    const double lb = fd ? Lm[a1] : 0.0;
+    // mode 3 on the a2 columns (FD: forward, Lambda, backward; D = 2: Lambda = lambda_1[row]
+    // + lambda_2[column], no plane term)
+    const double lb = pb.kind == 0 ? Lm[a1] : 0.0;
     plane_step<NT>(Pl, 1, sp, n2, n3, W3, fd ? PT_FUSED : PT_SYM, lb, Lm + 96, Lm + 192, Sc, warp, lane, grp.eo);
     __syncthreads();
     if (tr) tr[4] = gtimer();
@@ -550,6 +561,15 @@ __global__ void __launch_bounds__(PTH, 2) mode_plane_kernel(const __grid_constan
       plane_step<NT>(Pl, sp, 1, n3, n2, W2, PT_BWDT, 0.0, nullptr, nullptr, Sc, warp, lane, grp.eo);
       __syncthreads();
       if (tr) tr[5] = gtimer();
+    }
+    if (d2) {  // D = 2: natural-layout output, optional post-scaling
+      double* dst = pb.Y + pb.ybs * (long long)b;
+      for (int e = tid; e < Mi; e += PTH) {
+        const int i3 = e / n2, i2 = e - i3 * n2;
+        const double v = Pl[i3 * sp + i2];
+        dst[e] = pb.scale ? v * __ldg(pb.scale + e) : v;
+      }
+    } else if (fd) {
       double* dst = pb.T + pb.tbs * (long long)b + (long long)a1 * Mi;  // in place
       for (int e = tid; e < Mi; e += PTH) {
         const int i3 = e / n2, i2 = e - i3 * n2;

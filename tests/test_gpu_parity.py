@@ -70,6 +70,8 @@ def _rand_persym_spd(n, rng, shift):
     ((300, 2), (1.0, 3.0), 2, False),            # 2D, K1 folded even extent
     ((40, 66, 71), (1.0, 1.0, 2.0), 3, True),    # plane path, n2 != n3 (one kernel NT), batch 3
     ((9, 57, 64), (2.0, 1.0, 1.0), 1, False),    # plane path, leftover rows in both plane steps
+    ((40, 45), (2.0, 1.0), 3, True),             # 2D one-launch plane path, P^G, batch 3
+    ((65, 66), (1.0, 2.0), 1, False),            # 2D one-launch plane path, odd / even
 ])
 def test_fd_apply_folded_persymmetric(dims, coef, batch, dscale):
     """Even-odd folded transforms on random persymmetric SPD pencils: the folded
