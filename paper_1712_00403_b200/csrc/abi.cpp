@@ -676,7 +676,14 @@ static int plane_rows(int n2, int n3, int sp) {
 }
 
 bool plane_path(const std::vector<const fdp_fd_s*>& hs, const PresPlane* pq, int64_t batch) {
-  return plane_nt(hs, pq) > 0 && (long long)hs[0]->N * batch < (1LL << 31);
+  if (plane_nt(hs, pq) <= 0 || (long long)hs[0]->N * batch >= (1LL << 31)) return false;
+  if (hs[0]->D == 2) return true;
+  // 3D: at least one plane per SM, else the five small-path passes spread the work wider (one
+  // config-2 component alone: 36 us in five passes against 40 us with its 65 planes)
+  long long planes = 0;
+  for (const fdp_fd_s* h : hs) planes += (long long)h->n[0] * batch;
+  if (pq) planes += (long long)pq->n[0] * batch;
+  return planes >= num_sms();
 }
 
 // fuse_prescale: the inputs are not yet scaled by D^{-1/2} (dscale[k] / pq->pre): the mode-1
