@@ -34,6 +34,10 @@ constexpr int BK = FDP_K1_BK;
 #define FDP_K1F_BK 8
 #endif
 constexpr int kFoldBK = FDP_K1F_BK;
+#ifndef FDP_K1F_STAGES
+#define FDP_K1F_STAGES 2
+#endif
+constexpr int kFoldStages = FDP_K1F_STAGES;
 constexpr int STAGES = FDP_K1_STAGES;
 constexpr int WARPS = kK1Warps;
 constexpr int THREADS = WARPS * 32;
@@ -266,7 +270,7 @@ struct SmemF {
   static constexpr int SB = ((BN + 15) / 16) * 16 + 4;
   static constexpr int B_ELEMS = BKF * SB;
   static constexpr int STAGE = A_ELEMS + B_ELEMS;
-  static constexpr size_t BYTES = sizeof(double) * STAGE * STAGES;
+  static constexpr size_t BYTES = sizeof(double) * STAGE * kFoldStages;
 };
 
 template <int MT, int NT, bool KMAJ, int FOLD, int BKF, bool SC = false>
@@ -376,19 +380,19 @@ mode_contract_fold_kernel(const __grid_constant__ ModeGroupT<kSmallGroup> grp) {
   auto kloop = [&](double (&c)[MT][NT][2], int K, int aoff, int wrow0, double sgn) {
     const int KT = (K + BKF - 1) / BKF;
 #pragma unroll
-    for (int st = 0; st < STAGES - 1; ++st) {
+    for (int st = 0; st < kFoldStages - 1; ++st) {
       if (st < KT) load_stage(st, st * BKF, aoff, wrow0);
       cp_async_commit();
     }
     for (int kt = 0; kt < KT; ++kt) {
-      cp_async_wait<STAGES - 2>();
+      cp_async_wait<kFoldStages - 2>();
       __syncthreads();
       {
-        const int nk = kt + STAGES - 1;
-        if (nk < KT) load_stage(nk % STAGES, nk * BKF, aoff, wrow0);
+        const int nk = kt + kFoldStages - 1;
+        if (nk < KT) load_stage(nk % kFoldStages, nk * BKF, aoff, wrow0);
         cp_async_commit();
       }
-      const double* As = smem + (kt % STAGES) * SF::STAGE;
+      const double* As = smem + (kt % kFoldStages) * SF::STAGE;
       const double* As2 = As + S::A1;
       const double* Bs = As + SF::A_ELEMS;
       const int kvalid = min(BKF, K - kt * BKF);
