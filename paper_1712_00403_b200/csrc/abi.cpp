@@ -780,9 +780,11 @@ static cudaError_t enqueue_fd_plane(const std::vector<const fdp_fd_s*>& hs,
     std::vector<TileCfg> cfgs;
     for (size_t k = 0; k < K; ++k) {
       const fdp_fd_s* h = hs[k];
-      ModeProb p = make_mode_prob(h, 0, true, in[k], ibs, T[k], Npad(h), batch, EPI_NONE, nullptr,
-                                  h->n[0], h->n[0]);
+      const long long Mi = (long long)h->n[1] * h->n[2], Mp = Mi + (Mi & 1);
+      ModeProb p = make_mode_prob(h, 0, true, in[k], ibs, T[k], h->n[0] * Mp, batch, EPI_NONE,
+                                  nullptr, h->n[0], h->n[0]);
       p.tio = TIO_OUT_T;
+      p.tio_ld = (int)Mp;
       p.vy = 0;
       if (fuse_prescale) p.pre = dscale[k];
       probs.push_back(p);
@@ -794,13 +796,15 @@ static cudaError_t enqueue_fd_plane(const std::vector<const fdp_fd_s*>& hs,
       ModeProb p{};
       p.X = pq->rq;
       p.xbs = pq->rbs;
+      const long long Mqi = (long long)pq->n[1] * pq->n[2], Mqp = Mqi + (Mqi & 1);
       p.Y = pq->Tq;
-      p.ybs = pq->tqbs;
+      p.ybs = pq->n[0] * Mqp;
       p.W = pq->Wq[0];
       p.ldw = pq->q_ldw[0];
       p.foldh = pq->q_foldh[0];
       p.fold = FOLD_SYM;
       p.tio = TIO_OUT_T;
+      p.tio_ld = (int)Mqp;
       p.N = (long long)pq->n[0] * pq->n[1] * pq->n[2];
       p.P = 1;
       p.n = p.nout = pq->n[0];
@@ -824,8 +828,10 @@ static cudaError_t enqueue_fd_plane(const std::vector<const fdp_fd_s*>& hs,
     for (size_t k = 0; k < K; ++k) {
       const fdp_fd_s* h = hs[k];
       PlaneProb& q = g.prob[g.count++];
+      const long long Mi = (long long)h->n[1] * h->n[2], Mp = Mi + (Mi & 1);
       q.T = T[k];
-      q.tbs = Npad(h);
+      q.tbs = h->n[0] * Mp;
+      q.pstride = (int)Mp;
       q.W2 = h->WfF[1];
       q.W3 = h->WfF[2];
       q.ldw2 = h->ldwF[1];
@@ -853,8 +859,10 @@ static cudaError_t enqueue_fd_plane(const std::vector<const fdp_fd_s*>& hs,
     }
     if (pq) {
       PlaneProb& q = g.prob[g.count++];
+      const long long Mqi = (long long)pq->n[1] * pq->n[2], Mqp = Mqi + (Mqi & 1);
       q.T = pq->Tq;
-      q.tbs = pq->tqbs;
+      q.tbs = pq->n[0] * Mqp;
+      q.pstride = (int)Mqp;
       q.W2 = pq->Wq[1];
       q.W3 = pq->Wq[2];
       q.ldw2 = pq->q_ldw[1];
@@ -908,12 +916,17 @@ static cudaError_t enqueue_fd_plane(const std::vector<const fdp_fd_s*>& hs,
     for (size_t k = 0; k < K; ++k) {
       const fdp_fd_s* h = hs[k];
       const bool sc = dscale[k] != nullptr;
-      ModeProb p = make_mode_prob(h, 0, false, T[k], Npad(h), out[k], obs, batch,
+      const long long Mi = (long long)h->n[1] * h->n[2], Mp = Mi + (Mi & 1);
+      ModeProb p = make_mode_prob(h, 0, false, T[k], h->n[0] * Mp, out[k], obs, batch,
                                   sc ? EPI_SCALE : EPI_NONE, dscale[k], h->n[0], h->n[0]);
-      p.P = h->n[1] * h->n[2];
+      // rows = the even plane stride (pad row masked at the store): 16-byte row-pair loads
+      p.P = (int)Mp;
       p.Q = 1;
-      p.vx = p.vy = 0;
+      p.vx = (reinterpret_cast<uintptr_t>(T[k]) & 15) == 0 && ((h->n[0] * Mp) % 2 == 0) &&
+             std::getenv("FDP_NO_VEC") == nullptr;
+      p.vy = 0;
       p.tio = TIO_OUT_K;
+      p.tio_rows = (int)Mi;
       probs.push_back(p);
       TileCfg c = h->cfg[0];
       c.NT = h->fold_nt[0];

@@ -71,6 +71,9 @@ struct ModeProb {
   // row within its item, Mi = P * Q rows per item); TIO_OUT_K (non-KMAJ kernel reading a
   // plane-major tensor as P = Mi, Q = 1): output at Y[item * ybs + yld * mi + a].
   int tio;
+  int tio_ld;             // TIO_OUT_T: column stride of the output (the plane stride, even)
+  int tio_rows;           // TIO_OUT_K: rows per item that exist (rows >= tio_rows are the
+                          // plane-major layout's pad row: computed, never stored)
   // KMAJ small-path loads: optional input scaling x <- pre o x (pre indexed like the input within
   // one item: the P^G pre-scaling D^{-1/2} fused into the first pass)
   const double* pre;
@@ -198,6 +201,7 @@ struct PlaneProb {
   const double* lam2;
   const double* lam3;
   int n1, n2, n3, batch;
+  int pstride;            // plane stride of the plane-major tensor (n2 n3 rounded up to even)
   int sp;                 // shared-memory row stride of the plane
   int kind;
   double* Y;              // kinds 1-3: output (natural layout), batch stride ybs, optional scale

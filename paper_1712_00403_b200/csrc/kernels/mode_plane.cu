@@ -529,7 +529,7 @@ __global__ void __launch_bounds__(PTH, 2) mode_plane_kernel(const __grid_constan
     const int a1 = local % n1, b = local / n1;
     const bool d2 = pb.kind >= 2;  // D = 2: natural-layout input, optional pre-scaling
     const double* src = d2 ? pb.X + pb.xbs * (long long)b
-                           : pb.T + pb.tbs * (long long)b + (long long)a1 * Mi;
+                           : pb.T + pb.tbs * (long long)b + (long long)a1 * pb.pstride;
     if (d2 && pb.pre) {
       for (int e = tid; e < Mi; e += PTH) {
         const int i3 = e / n2, i2 = e - i3 * n2;
@@ -570,7 +570,7 @@ __global__ void __launch_bounds__(PTH, 2) mode_plane_kernel(const __grid_constan
         dst[e] = pb.scale ? v * __ldg(pb.scale + e) : v;
       }
     } else if (fd) {
-      double* dst = pb.T + pb.tbs * (long long)b + (long long)a1 * Mi;  // in place
+      double* dst = pb.T + pb.tbs * (long long)b + (long long)a1 * pb.pstride;  // in place
       for (int e = tid; e < Mi; e += PTH) {
         const int i3 = e / n2, i2 = e - i3 * n2;
         dst[e] = Pl[i3 * sp + i2];

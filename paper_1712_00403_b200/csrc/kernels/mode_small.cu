@@ -549,12 +549,17 @@ __device__ __forceinline__ void tile_compute_store_fold(const ModeProb& pb, cons
       // output addressing: row base sidx, column stride cs; kout = rows contiguous in the output
       if (pb.tio != TIO_NONE) {
         const int mi = m - item[i] * g.Mi;
-        if (pb.tio == TIO_OUT_T) { sidx[i] = mi; cs = g.Mi; kout = false; }
-        else { sidx[i] = pb.yld * mi; cs = 1; kout = true; }
+        if (pb.tio == TIO_OUT_T) { sidx[i] = mi; cs = pb.tio_ld; kout = false; }
+        else {
+          sidx[i] = pb.yld * mi;
+          cs = 1;
+          kout = true;
+          if (mi >= pb.tio_rows) mv[i] = false;  // the plane-major pad row
+        }
       }
     }
   }
-  if (pb.tio == TIO_OUT_T) { cs = g.Mi; kout = false; }
+  if (pb.tio == TIO_OUT_T) { cs = pb.tio_ld; kout = false; }
   else if (pb.tio == TIO_OUT_K) { cs = 1; kout = true; }
   const bool vrow = !KMAJ && pb.vy && pb.tio == TIO_NONE;  // 16-byte row-pair stores
 
