@@ -654,7 +654,7 @@ static int plane_nt(const std::vector<const fdp_fd_s*>& hs, const PresPlane* pq)
     for (const fdp_fd_s* h : hs)
       if (h->D != 2 || h->fold[0] != 1 || h->fold[1] != 1 || h->fold_nt[0] != nt || h->fold_nt[1] != nt)
         return 0;
-    if (pq && !(pq->q_fold[0] && pq->q_fold[1])) return 0;
+    if (pq && !(pq->q_fold[0] == 1 && pq->q_fold[1] == 1)) return 0;
     return nt;
   }
   if (hs[0]->D != 3) return 0;
@@ -663,7 +663,7 @@ static int plane_nt(const std::vector<const fdp_fd_s*>& hs, const PresPlane* pq)
     if (h->fold[0] != 1 || h->fold[1] != 1 || h->fold[2] != 1) return 0;
     if (h->fold_nt[1] != nt || h->fold_nt[2] != nt || h->fold_nt[0] != hs[0]->fold_nt[0]) return 0;
   }
-  if (pq && !(pq->q_fold[0] && pq->q_fold[1] && pq->q_fold[2])) return 0;
+  if (pq && !(pq->q_fold[0] == 1 && pq->q_fold[1] == 1 && pq->q_fold[2] == 1)) return 0;
   return nt;
 }
 

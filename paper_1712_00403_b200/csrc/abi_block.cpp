@@ -110,6 +110,26 @@ extern "C" fdp_status block_precond_setup(int D, const fdp_fd* vel, fdp_mass pre
           raw->q_ldw[d] = 4 * nt;
           raw->q_tiles_n[d] = 1;
           fold_sym_matrix(nq, X.data(), 4 * nt, 4 * nt, &w);
+        } else if (nq > kSmallMaxN && std::getenv("FDP_NO_FOLD") == nullptr &&
+                   persymmetric(nq, X.data(), 1e-10)) {
+          // a K1-sized factor: the folded K1 kernel's FOLD_SYM pass (own launch, two
+          // accumulator sets, column tiles of <= 6 n8-tiles over the ceil(n/2) outputs)
+          const int ne = (nq + 1) / 2, n8e = (ne + 7) / 8;
+          TileCfg c{};
+          c.MT = 2;
+          c.NT = (n8e + (n8e + 5) / 6 - 1) / ((n8e + 5) / 6);
+          c.tiles_n = (n8e + c.NT - 1) / c.NT;
+          c.ldw = c.tiles_n * 8 * c.NT;
+          c.kpad = kpad;
+          const int foldh = ((ne + 31) / 32) * 32;
+          raw->q_fold[d] = 2;
+          raw->q_foldh[d] = foldh;
+          raw->q_ldw[d] = c.ldw;
+          raw->q_tiles_n[d] = c.tiles_n;
+          raw->q_cfgF[d] = c;
+          fold_sym_matrix(nq, X.data(), foldh, c.ldw, &w);
+          if (cudaError_t e = prepare_mode_kernels(c); e != cudaSuccess)
+            st = cuda_fail(e, "block_precond_setup: prepare");
         } else {
           w.assign((size_t)kpad * raw->q_ldw[d], 0.0);
           for (int k = 0; k < nq; ++k)
@@ -261,7 +281,12 @@ static cudaError_t enqueue_block(fdp_block h, const double* r, double* s, int64_
       if (h->q_fold[d]) {
         p.fold = FOLD_SYM;
         p.foldh = h->q_foldh[d];
-        qc.NT = h->vel[0]->fold_nt[d];
+        if (h->q_fold[d] == 2) {
+          p.fold_k1 = 1;
+          qc = h->q_cfgF[d];
+        } else {
+          qc.NT = h->vel[0]->fold_nt[d];
+        }
       }
       probs.push_back(p);
       cfgs.push_back(qc);
@@ -507,7 +532,12 @@ static cudaError_t enqueue_unit(fdp_block h, int k, const double* r, double* s, 
       if (h->q_fold[d]) {
         p.fold = FOLD_SYM;
         p.foldh = h->q_foldh[d];
-        qc.NT = h->vel[0]->fold_nt[d];
+        if (h->q_fold[d] == 2) {
+          p.fold_k1 = 1;
+          qc = h->q_cfgF[d];
+        } else {
+          qc.NT = h->vel[0]->fold_nt[d];
+        }
       }
       std::vector<ModeProb> probs{p};
       std::vector<TileCfg> cfgs{qc};

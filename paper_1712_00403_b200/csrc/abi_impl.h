@@ -206,6 +206,8 @@ struct fdp_block_s {
   int q_tiles_n[3] = {0, 0, 0};
   int q_ldw[3] = {0, 0, 0};
   int q_fold[3] = {0, 0, 0};   // M_d^{-1} is centrosymmetric: folded (FOLD_SYM) pass, Wq = E | O
+                               // (1: small path, riding in the velocity launch; 2: folded K1)
+  TileCfg q_cfgF[3];           // q_fold == 2: tile shape of the folded K1 pass
   int q_foldh[3] = {0, 0, 0};
   cudaStream_t cap = nullptr;  // private capture stream
   // graph cache

@@ -266,7 +266,7 @@ struct SmemF {
   static constexpr int BN = 8 * NT;
   static constexpr int SA = KMAJ ? (BKF + 4) : (BM + 4);
   static constexpr int A1 = KMAJ ? BM * SA : BKF * SA;       // one A tile
-  static constexpr int A_ELEMS = A1 * (FOLD == FOLD_FWD ? 2 : 1);
+  static constexpr int A_ELEMS = A1 * (FOLD == FOLD_FWD || FOLD == FOLD_SYM ? 2 : 1);
   static constexpr int SB = ((BN + 15) / 16) * 16 + 4;
   static constexpr int B_ELEMS = BKF * SB;
   static constexpr int STAGE = A_ELEMS + B_ELEMS;
@@ -353,7 +353,7 @@ mode_contract_fold_kernel(const __grid_constant__ ModeGroupT<kSmallGroup> grp) {
     double* As = smem + stage * SF::STAGE;
     double* Bs = As + SF::A_ELEMS;
     load_a(As, aoff + k0);
-    if (FOLD == FOLD_FWD) load_a(As + S::A1, n - k0 - BKF);
+    if (FOLD == FOLD_FWD || FOLD == FOLD_SYM) load_a(As + S::A1, n - k0 - BKF);
     constexpr int CHUNKS = BKF * BN / 2;
 #pragma unroll
     for (int c = tid; c < CHUNKS; c += THREADS) {
@@ -364,12 +364,13 @@ mode_contract_fold_kernel(const __grid_constant__ ModeGroupT<kSmallGroup> grp) {
 
   const int fr = lane >> 2, fc = lane & 3;
   const int wm = warp * 8 * MT;
-  double acc[MT][NT][2], acc2[FOLD == FOLD_BWD ? MT : 1][FOLD == FOLD_BWD ? NT : 1][2];
+  constexpr bool TWO = FOLD == FOLD_BWD || FOLD == FOLD_SYM;  // e and o accumulator sets
+  double acc[MT][NT][2], acc2[TWO ? MT : 1][TWO ? NT : 1][2];
 #pragma unroll
   for (int i = 0; i < MT; ++i)
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  if constexpr (FOLD == FOLD_BWD) {
+  if constexpr (TWO) {
 #pragma unroll
     for (int i = 0; i < MT; ++i)
 #pragma unroll
@@ -405,7 +406,7 @@ mode_contract_fold_kernel(const __grid_constant__ ModeGroupT<kSmallGroup> grp) {
             const int mr = wm + 8 * i + fr;
             const int kk = k4 + fc;
             a[i] = KMAJ ? As[mr * S::SA + kk] : As[kk * S::SA + mr];
-            if (FOLD == FOLD_FWD) {
+            if (FOLD == FOLD_FWD || FOLD == FOLD_SYM) {
               const int km = BKF - 1 - kk;  // mirror block holds n-k0-BKF .. n-k0-1
               a[i] += sgn * (KMAJ ? As2[mr * S::SA + km] : As2[km * S::SA + mr]);
             }
@@ -425,6 +426,9 @@ mode_contract_fold_kernel(const __grid_constant__ ModeGroupT<kSmallGroup> grp) {
 
   if constexpr (FOLD == FOLD_FWD) {
     kloop(acc, isE ? ne : no, 0, isE ? 0 : pb.foldh, isE ? 1.0 : -1.0);
+  } else if constexpr (FOLD == FOLD_SYM) {  // y = A x, A centrosymmetric: e = W_E^T s, o = W_O^T d
+    kloop(acc, ne, 0, 0, 1.0);
+    kloop(acc2, no, 0, pb.foldh, -1.0);
   } else {
     kloop(acc, ne, 0, 0, 0.0);              // e over the E half of the spectral row
     kloop(acc2, no, ne, pb.foldh, 0.0);     // o over the O half
@@ -523,6 +527,10 @@ cudaError_t launch_t(const ModeGroup* g, cudaStream_t s) {
       e = cudaFuncSetAttribute(mode_contract_fold_kernel<MT, NT, KMAJ, FOLD_BWD, BK>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)SmemF<MT, NT, KMAJ, FOLD_BWD, BK>::BYTES);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(mode_contract_fold_kernel<MT, NT, KMAJ, FOLD_SYM, kFoldBK>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)SmemF<MT, NT, KMAJ, FOLD_SYM, kFoldBK>::BYTES);
     if (!KMAJ && e == cudaSuccess)
       e = cudaFuncSetAttribute(mode_contract_fold_kernel<MT, NT, false, FOLD_FWD, kFoldBK, true>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -535,7 +543,13 @@ cudaError_t launch_t(const ModeGroup* g, cudaStream_t s) {
   }
   if (g->prob[0].fold != FOLD_NONE) {  // folded K1 group (host-checked: all problems, one kind)
     const int f = g->prob[0].fold;
-    if (g->count > kSmallGroup || (f != FOLD_FWD && f != FOLD_BWD)) return cudaErrorInvalidValue;
+    if (g->count > kSmallGroup || (f != FOLD_FWD && f != FOLD_BWD && f != FOLD_SYM))
+      return cudaErrorInvalidValue;
+    if (f == FOLD_SYM) {  // the dense P_Q passes of a K1-sized pressure factor
+      mode_contract_fold_kernel<MT, NT, KMAJ, FOLD_SYM, kFoldBK>
+          <<<g->total_ctas, THREADS, SmemF<MT, NT, KMAJ, FOLD_SYM, kFoldBK>::BYTES, s>>>(narrow_group<kSmallGroup>(*g));
+      return cudaGetLastError();
+    }
     const bool bk16 = std::getenv("FDP_K1F_BK16") != nullptr;  // experiment switch
     bool scf = false;
     for (int i = 0; i < g->count; ++i) scf = scf || g->prob[i].peers != nullptr;

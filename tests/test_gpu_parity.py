@@ -519,3 +519,22 @@ def test_config3_literal_c3_reading():
     o = od.offsets()
     for k in range(len(o) - 1):
         assert rel(s[0, o[k]:o[k + 1]], ref[0, o[k]:o[k + 1]]) < TOL, k
+
+
+@pytest.mark.parametrize("env", [{}, {"FDP_NO_FOLD": "1"}])
+def test_block_precond_k1_sized_pressure(env, monkeypatch):
+    """2D TH p=2 on 100 elements: velocity extents 200 (folded K1 transforms) and pressure
+    extents 102 > 96, whose dense M_d^{-1} passes take the folded K1 FOLD_SYM kernel."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    od = ospaces.build(2, "TH", 2, 100)
+    gd = fdp.discretization(2, "TH", 2, 100)
+    assert gd.q_dims == [102, 102]
+    P = fdp.build_block(gd)
+    r = np.random.default_rng(31).standard_normal((2, od.n_total))
+    s = P.apply(dev(r), batch=2).cpu().numpy()
+    ref = oprec.BlockPrecond(od).apply(r)
+    o = od.offsets()
+    for i in range(2):
+        for k in range(len(o) - 1):
+            assert rel(s[i, o[k]:o[k + 1]], ref[i, o[k]:o[k + 1]]) < TOL, (env, k)
