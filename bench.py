@@ -494,10 +494,20 @@ def main():
     traffic = traffic_src = None
     ncu_json = os.path.join(ROOT, "profiles", f"r01_ncu_cfg{cid}.json")
     if os.path.exists(ncu_json):
-        ks = [k for k in json.load(open(ncu_json)).get("kernels", []) if "mode_" in k["kernel"]]
+        # the dominant launch's kernel: the plane kernel (plane path) or the folded K1 forward
+        # (FOLD = 1, the fourth template argument); else every FD-transform kernel captured
+        allk = [k for k in json.load(open(ncu_json)).get("kernels", []) if "mode_" in k["kernel"]]
+        ks = [k for k in allk if "mode_plane" in k["kernel"]]
+        if not ks:
+            ks = [k for k in allk if "fold_kernel<" in k["kernel"]
+                  and k["kernel"].split("fold_kernel<")[1].split(",")[3].strip() == "1"]
+        what = "dominant kernel"
+        if not ks:
+            ks, what = allk, "all captured FD-transform kernels"
         if ks:
             traffic = float(np.mean([(k["dram_read_bytes"] or 0) + (k["dram_write_bytes"] or 0) for k in ks]))
-            traffic_src = f"{os.path.relpath(ncu_json, ROOT)} (mean of {len(ks)} K1 launches, bytes per launch)"
+            traffic_src = (f"{os.path.relpath(ncu_json, ROOT)} (DRAM read + write per launch, mean of "
+                           f"{len(ks)} captured launches of the {what}; ncu --set full, cold cache)")
     launches = P.launch_count(batch)
     roof_kind = "per-launch CUDA events of K1 inside the apply graph"
     if slab:
