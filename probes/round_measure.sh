@@ -17,6 +17,13 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:mode
   -o /tmp/ncu/full_cfg2 -f python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full2.log 2>&1
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:mode_contract --launch-skip 7 -c 7 \
   -o /tmp/ncu/full_cfg4 -f python bench.py --config 4 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full4.log 2>&1
+timeout 900 ncu --set full --clock-control none -k regex:mode_ --launch-skip 6 -c 3 \
+  -o /tmp/ncu/full_cfg3 -f python bench.py --config 3 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full3.log 2>&1
+timeout 1500 ncu --set full --clock-control none -k regex:mode_contract --launch-skip 9 -c 7 \
+  -o /tmp/ncu/full_cfg5 -f python bench.py --config 5 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full5.log 2>&1
+python tools/ncu_summary.py /tmp/ncu/full_cfg3.ncu-rep --tag r01_ncu_cfg3 > gpurun_out/sum3.log 2>&1
+python tools/ncu_summary.py /tmp/ncu/full_cfg5.ncu-rep --tag r01_ncu_cfg5 > gpurun_out/sum5.log 2>&1
+cp profiles/r01_ncu_cfg3.md profiles/r01_ncu_cfg3.json profiles/r01_ncu_cfg5.md profiles/r01_ncu_cfg5.json gpurun_out/ 2>/dev/null
 python tools/ncu_summary.py /tmp/ncu/full_cfg2.ncu-rep --launches gpurun_out/launches_cfg2.csv --tag r01_ncu_cfg2 > gpurun_out/sum2.log 2>&1
 python tools/ncu_summary.py /tmp/ncu/full_cfg4.ncu-rep --tag r01_ncu_cfg4 > gpurun_out/sum4.log 2>&1
 cp profiles/r01_ncu_cfg2.md profiles/r01_ncu_cfg2.json profiles/r01_ncu_cfg4.md profiles/r01_ncu_cfg4.json gpurun_out/ 2>/dev/null
