@@ -4,13 +4,16 @@ applications/s and DOF/s in FP64, % of the FP64 tensor-core roofline).
 
 One step = one block_precond_apply (P_D^{-1} r, or (P_D^G)^{-1} r for config 3) over one batch of
 synthetic RHS already resident in HBM: the whole hot path. Default workload
-= BASELINE.json configs[1] (config 2: 3D Taylor-Hood p=3, 32^3 elements). --config selects others.
+= BASELINE.json configs[4] (config 5: 3D Raviart-Thomas p=4, 512^3 elements, 548.8 M dofs), the
+largest configuration that fits one GPU and the one the FP64 tensor-core target is about (SURVEY.md
+§8(d) D-3); --config selects the others (parity-test cases, not bench lines).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl {fdp,reference}]
 
-N > 1 runs under torchrun, one rank per GPU. Configs 1-3 have no natural sharding ("replicas
-only": each rank applies the preconditioner to its own RHS stream); config 4 shards its batch of
-8 RHS across ranks (weak in per-rank work only when 8 % N == 0; reported as "strong").
+N > 1 runs under torchrun, one rank per GPU. Config 5 is slab-decomposed (i3 planes split over
+the ranks, exchanges fused into the contraction epilogues as NVLink peer stores; strong scaling);
+configs 1-3 have no natural sharding ("replicas only": each rank applies the preconditioner to its
+own RHS stream); config 4 shards its batch of 8 RHS across ranks.
 --impl reference times the CPU oracle (the reference arm of this tier) on the same workload.
 """
 from __future__ import annotations
@@ -37,9 +40,9 @@ L2_FLUSH_BYTES = 512 << 20  # > 126 MB L2
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--rt-reading", default="paper", choices=["paper", "literal"],
                     help="RT own-direction regularity: the paper's alpha+1 (default) or configs 3/5's "
                          "literal 'C^3' wording, alpha (SURVEY.md C-3; a secondary row)")
@@ -67,7 +70,28 @@ def RT_OWN_ALPHA(w):
     return (w.p - 1) if (_RT_LITERAL and w.disc == "RT") else None
 
 
-def workload_config(cid, w, n_total, batch_total, gpus, flush):
+def l2_policy(n_total, batch):
+    """L2 handling of the timed loop, a function of the workload only (the same string in both
+    arms): working sets below 2x the 126 MB L2 are flushed before every timed step."""
+    ws = 2 * 8 * n_total * batch
+    if ws < 2 * (126 << 20):
+        return True, "flushed before every timed step (512 MB written, then read back)"
+    return False, f"working set {ws / 1e9:.2f} GB > L2 (126 MB): no flush needed"
+
+
+def batch_layout(cid, w, gpus, rank=0):
+    """(items of this rank, global batch) -- config 5 at N > 1: one RHS slab-sharded; config 4:
+    its 8 RHS dealt round-robin; configs 1-3: every rank its own replica stream."""
+    if cid == 5 and gpus > 1:
+        return [0], 1
+    if cid == 4:
+        return list(range(rank, w.batch, gpus)), w.batch
+    return list(range(w.batch)), w.batch * gpus
+
+
+def workload_config(cid, w, n_total, gpus):
+    items, batch_total = batch_layout(cid, w, gpus)
+    _, l2 = l2_policy(n_total, len(items))
     return {
         "workload": w.name + ("_literal_c3" if (_RT_LITERAL and w.disc == "RT") else ""),
         "config_index": cid,
@@ -77,7 +101,7 @@ def workload_config(cid, w, n_total, batch_total, gpus, flush):
         "global_batch": batch_total,
         "parallelism": (("slab-" + os.environ.get("FDP_SLAB_EXCHANGE", "peer")) if cid == 5 and gpus > 1
                         else "batch-shard" if cid == 4 else "replicas") + f"x{gpus}",
-        "l2": flush,
+        "l2": l2,
         "rhs": f"numpy default_rng(seed={w.seed}).standard_normal, FP64",
     }
 
@@ -206,7 +230,7 @@ def run_reference(args, w, cid):
     except Exception:
         pass
     # each step = one oracle application to one RHS (bounded: the whole run stays within minutes)
-    steps, warm = args.steps, args.warmup
+    steps, warm = args.steps, max(args.warmup, 3)  # the GPU arm's warm-up floor
     from oracle import precond, spaces
     od = spaces.build(w.dim, w.disc, w.p, w.n_el, rt_own_alpha=RT_OWN_ALPHA(w))
     dv = dq = None
@@ -214,16 +238,11 @@ def run_reference(args, w, cid):
         dv, dq = spaces.nu_scalings(od, synth.viscosity)
     P = precond.BlockPrecond(od, dv, dq)
     r = synth.rhs(w.seed, od.n_total, 1)[0]
-    # bound the whole run to a few minutes: the warm-up and timed counts shrink (to >= 1 each)
-    # when one oracle application is slow (configs 4 and 5 take seconds to tens of seconds)
-    budget_s = 150.0
-    t0 = time.perf_counter()
-    P.apply(r)
-    t_one = time.perf_counter() - t0
-    warm = max(1, min(warm, int(0.2 * budget_s / max(t_one, 1e-9))))
-    for _ in range(warm - 1):
+    # every step is one full oracle application to one RHS of the workload (batch item 0): the run
+    # honours --steps / --warmup exactly, so its line is comparable step for step with the GPU
+    # arm's (config 5: ~24 s per application on 16 host cores, ~10 min for 20 + 5 steps)
+    for _ in range(warm):
         P.apply(r)
-    steps = max(1, min(steps, int(0.8 * budget_s / max(t_one, 1e-9))))
     t0 = time.perf_counter()
     for _ in range(steps):
         P.apply(r)
@@ -241,9 +260,11 @@ def run_reference(args, w, cid):
         "vs_baseline_source": ("BASELINE.md §2.1: 59.9 ms per P_D apply at config 2's size (paper, "
                                "MATLAB, one Haswell-E thread)") if cid == 2 else None, "dtype": "f64", "data": "synthetic",
         "dof_per_s": value * od.n_total,
-        "config": workload_config(cid, w, od.n_total, 1, 1, "n/a (CPU)"),
+        "config": workload_config(cid, w, od.n_total, args.gpus),
         "cpu_baseline": {"value": value, "unit": "apply/s", "cores": cores, "kind": "oracle",
-                         "sample": f"{steps} oracle applications to one RHS of {w.name} (batch item 0)"},
+                         "sample": f"{steps} oracle applications (numpy/scipy FP64) to one RHS of {w.name} "
+                                   f"(batch item 0), after {warm} untimed ones; one application = one "
+                                   f"step of the GPU arm's workload per RHS"},
         "e2e": {"value": value, "unit": "apply/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -287,7 +308,7 @@ def main():
     gd = fdp.discretization(w.dim, w.disc, w.p, w.n_el, rt_own_alpha=RT_OWN_ALPHA(w))
     dv = dq = None
     if w.variable_nu:
-        dv, dq = fdp.nu_scalings(gd, synth.viscosity)
+        dv, dq = fdp.nu_scalings(gd, synth.viscosity_separable(gd.D))
     P = fdp.build_block(gd, device=dev, dscale_vel=dv, dscale_pres=dq)
     setup_s = time.perf_counter() - t0
     n_total = gd.n_total
@@ -318,15 +339,7 @@ def main():
         if SB is None:
             SB = fdist.SlabBlockPrecond(P)
     # batch per rank: config 4 shards its 8 RHS across ranks; others replicate one RHS stream
-    if slab:
-        items = [0]
-        batch_total = 1
-    elif cid == 4:
-        items = list(range(rank, w.batch, world))
-        batch_total = w.batch
-    else:
-        items = list(range(w.batch))
-        batch_total = w.batch * world
+    items, batch_total = batch_layout(cid, w, world, rank)
     batch = len(items)
     if batch == 0:
         raise SystemExit("more ranks than RHS for this config")
@@ -342,8 +355,7 @@ def main():
         ws = P.workspace(batch)
     r = torch.from_numpy(r_host).to(dev)
     s = torch.empty_like(r)
-    working_set = 2 * r.numel() * 8 + ws.numel() * 8
-    flush = working_set < 2 * (126 << 20)
+    flush, _ = l2_policy(n_total, batch)
     flush_buf = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev) if flush else None
     stream = torch.cuda.current_stream()
 
@@ -492,7 +504,9 @@ def main():
     dense_equiv = (dense_fl * len(prof_runs) / (k1_ms * 1e-3)) / 1e12 if k1_ms > 0 else None
     # DRAM traffic per K1 launch from the committed ncu --set full capture of this config
     traffic = traffic_src = None
-    ncu_json = os.path.join(ROOT, "profiles", f"r01_ncu_cfg{cid}.json")
+    ncu_json = os.path.join(ROOT, "profiles", f"r02_ncu_cfg{cid}.json")
+    if not os.path.exists(ncu_json):
+        ncu_json = os.path.join(ROOT, "profiles", f"r01_ncu_cfg{cid}.json")
     if os.path.exists(ncu_json):
         # the dominant launch's kernel: the plane kernel (plane path) or the folded K1 forward
         # (FOLD = 1, the fourth template argument); else every FD-transform kernel captured
@@ -556,9 +570,7 @@ def main():
         "dtype": "f64",
         "data": "synthetic",
         "dof_per_s": value * n_total,
-        "config": workload_config(cid, w, n_total, batch_total, world,
-                                  "flushed before every timed step (512 MB written, then read back)" if flush
-                                  else "working set > L2"),
+        "config": workload_config(cid, w, n_total, world),
         "roofline": {
             "bound": "tensor",
             "kernel": "the dominant FD-transform launch of the step (config 2/3: the plane kernel "

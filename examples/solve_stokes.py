@@ -22,7 +22,7 @@ w = synth.CONFIGS[cid]
 d = fdp.discretization(w.dim, w.disc, w.p, w.n_el)                  # pencils of P_V,k and P_Q
 dv = dq = None
 if w.variable_nu:                                                   # config 3: P_D^G scalings
-    dv, dq = fdp.nu_scalings(d, synth.viscosity)
+    dv, dq = fdp.nu_scalings(d, synth.viscosity_separable(d.D))
 P = fdp.build_block(d, dscale_vel=dv, dscale_pres=dq)               # libfdp handles
 A = krylov.StokesOperator(w.dim, w.disc, w.p, w.n_el,
                           nu_terms=synth.viscosity_separable(w.dim) if w.variable_nu else None)

@@ -75,6 +75,17 @@ fdp_status iga_univariate(int deg, int alpha, int n_el, int flags, double c_pen,
  * g: host array of at least n doubles, or NULL to query n. */
 fdp_status iga_greville(int deg, int alpha, int n_el, int flags, double* g, int32_t* n_out);
 
+/* Diagonal scaling sampled at dofs from a coefficient written as a sum of separable terms,
+ * nu(x) = sum_t c[t] prod_d f_td(x_d) (config 3's nu = 1 + 0.5 sin(2 pi x) sin(2 pi y) sin(2 pi z),
+ * DESIGN.md C-6): out[i] = v_i (invert = 0) or 1 / v_i (invert = 1), with
+ * v_i = sum_t c[t] prod_d f[t*D + d][i_d], i = i_1 + n_1 (i_2 + n_2 i_3) (vec order, i1 fastest,
+ * P:382-386). f[t*D + d]: host array of n[d] values of the factor at the direction-d dof points
+ * (e.g. iga_greville), or NULL for a factor identically 1. D in [1, 3], T >= 1; out: host array
+ * of prod n[d] doubles. Errors: FDP_ERR_SHAPE (D, T or n out of range), FDP_ERR_INVALID_ARG
+ * (NULL out / n / c / f, or a zero sum with invert = 1). */
+fdp_status fdp_kron_diag(int D, const int32_t* n, int T, const double* const* f, const double* c,
+                         int invert, double* out);
+
 /* Generalized symmetric-definite eigenproblem K U = M U diag(lambda), U^T M U = I (Algorithm 1
  * step 1), host only: the routine fd_setup uses. K, M: host column-major n x n, M SPD;
  * U (n*n, column j = eigenvector j, largest-magnitude entry positive) and lambda (n, ascending)

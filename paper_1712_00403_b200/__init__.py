@@ -48,6 +48,7 @@ def _load():
         "iga_univariate": (i32, [i32, i32, i32, i32, ctypes.c_double, i32, vp, vp, _c_int32_p]),
         "iga_greville": (i32, [i32, i32, i32, i32, vp, _c_int32_p]),
         "fdp_gen_eig": (i32, [i32, vp, vp, vp, vp]),
+        "fdp_kron_diag": (i32, [i32, vp, i32, vp, vp, i32, vp]),
         "fd_setup": (i32, [i32, vp, vp, vp, vp, i32, i64, ctypes.POINTER(vp)]),
         "fd_get_eigs": (i32, [vp, i32, vp, vp]),
         "fd_size": (i64, [vp]),
@@ -697,15 +698,39 @@ def discretization(D: int, disc: str, p: int, n_el: int, rt_own_alpha: int | Non
     return out
 
 
-def _grid(f, grevs):
-    G = np.meshgrid(*grevs, indexing="ij")
-    return np.reshape(f(*G), -1, order="F")
+def kron_diag(dims, terms, invert: bool = False) -> np.ndarray:
+    """libfdp fdp_kron_diag: sum_t c_t prod_d f_td(x_d) sampled on a tensor grid of dof points.
+    terms: [(c_t, [values of f_td at direction d's points, or None for 1])]."""
+    D = len(dims)
+    n = (ctypes.c_int32 * D)(*dims)
+    keep = []
+    fp = (ctypes.c_void_p * (D * len(terms)))()
+    for t, (_, fs) in enumerate(terms):
+        for d in range(D):
+            v = None if fs is None else fs[d]
+            if v is not None:
+                v = np.ascontiguousarray(v, dtype=np.float64)
+                assert v.shape == (dims[d],)
+                keep.append(v)
+                fp[t * D + d] = v.ctypes.data
+    c = np.array([ct for ct, _ in terms], dtype=np.float64)
+    out = np.empty(int(np.prod(dims)), dtype=np.float64)
+    _check(lib.fdp_kron_diag(D, n, len(terms), fp, _ptr(c), int(invert), _ptr(out)))
+    return out
 
 
-def nu_scalings(d: Discretization, nu):
-    """Config 3: D_V = nu at velocity dof Greville points, D_Q = 1/nu at pressure dofs (C-6)."""
-    dv = np.concatenate([_grid(nu, g) for g in d.grev])
-    dq = 1.0 / _grid(nu, d.grev_q)
+def nu_scalings(d: Discretization, terms):
+    """Config 3 (C-6): D_V = nu at the velocity dofs' Greville points, D_Q = 1/nu at the
+    pressure dofs', for nu given as separable terms [(c_t, [w_t1, .., w_tD])] (w = None: 1),
+    e.g. synth.viscosity_separable(D); the tensor-grid sampling runs in libfdp (fdp_kron_diag)."""
+    if callable(terms):
+        raise TypeError("nu_scalings takes nu as separable terms (synth.viscosity_separable)")
+
+    def sampled(grevs):
+        return [(c, None if ws is None else [w(g) for w, g in zip(ws, grevs)]) for c, ws in terms]
+
+    dv = np.concatenate([kron_diag([len(g) for g in gr], sampled(gr)) for gr in d.grev])
+    dq = kron_diag([len(g) for g in d.grev_q], sampled(d.grev_q), invert=True)
     return dv, dq
 
 

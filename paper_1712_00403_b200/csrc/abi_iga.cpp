@@ -35,6 +35,44 @@ extern "C" fdp_status iga_greville(int deg, int alpha, int n_el, int flags, doub
   }
 }
 
+extern "C" fdp_status fdp_kron_diag(int D, const int32_t* n, int T, const double* const* f,
+                                    const double* c, int invert, double* out) {
+  try {
+    if (!n || !f || !c || !out) return fail(FDP_ERR_INVALID_ARG, "fdp_kron_diag: NULL argument");
+    if (D < 1 || D > 3 || T < 1) return fail(FDP_ERR_SHAPE, "fdp_kron_diag: D in [1,3], T >= 1");
+    int nn[3] = {1, 1, 1};
+    long long N = 1;
+    for (int d = 0; d < D; ++d) {
+      if (n[d] < 1) return fail(FDP_ERR_SHAPE, "fdp_kron_diag: n[d] < 1");
+      nn[d] = n[d];
+      N *= n[d];
+    }
+    // per term: the outer product of the direction factors, accumulated slice by slice
+    std::fill(out, out + N, 0.0);
+    std::vector<double> row((size_t)nn[0]);
+    for (int t = 0; t < T; ++t) {
+      const double* f1 = f[(size_t)t * D];
+      const double* f2 = D > 1 ? f[(size_t)t * D + 1] : nullptr;
+      const double* f3 = D > 2 ? f[(size_t)t * D + 2] : nullptr;
+      for (int i1 = 0; i1 < nn[0]; ++i1) row[i1] = c[t] * (f1 ? f1[i1] : 1.0);
+      for (int i3 = 0; i3 < nn[2]; ++i3)
+        for (int i2 = 0; i2 < nn[1]; ++i2) {
+          const double w = (f2 ? f2[i2] : 1.0) * (f3 ? f3[i3] : 1.0);
+          double* o = out + ((long long)i3 * nn[1] + i2) * nn[0];
+          for (int i1 = 0; i1 < nn[0]; ++i1) o[i1] += row[i1] * w;
+        }
+    }
+    if (invert)
+      for (long long i = 0; i < N; ++i) {
+        if (out[i] == 0.0) return fail(FDP_ERR_INVALID_ARG, "fdp_kron_diag: zero value with invert");
+        out[i] = 1.0 / out[i];
+      }
+    return FDP_OK;
+  } catch (...) {
+    return abi_exception(__func__);
+  }
+}
+
 extern "C" fdp_status fdp_gen_eig(int n, const double* K, const double* M, double* U,
                                   double* lambda) {
   try {

@@ -18,7 +18,7 @@ for cid in cids:
     dv = dq = None
     nu = synth.viscosity_separable(w.dim) if w.variable_nu else None
     if w.variable_nu:
-        dv, dq = fdp.nu_scalings(gd, synth.viscosity)
+        dv, dq = fdp.nu_scalings(gd, synth.viscosity_separable(gd.D))
     gop = krylov.StokesOperator(w.dim, w.disc, w.p, w.n_el, nu_terms=nu)
     P = fdp.build_block(gd, dscale_vel=dv, dscale_pres=dq)
     f = synth.rhs(w.seed, gop.n, 1)[0]

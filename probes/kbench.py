@@ -19,7 +19,7 @@ def run(cid, batch, iters=50):
     gd = fdp.discretization(w.dim, w.disc, w.p, w.n_el)
     dv = dq = None
     if w.variable_nu:
-        dv, dq = fdp.nu_scalings(gd, synth.viscosity)
+        dv, dq = fdp.nu_scalings(gd, synth.viscosity_separable(gd.D))
     P = fdp.build_block(gd, dscale_vel=dv, dscale_pres=dq)
     r = torch.randn(batch, gd.n_total, dtype=torch.float64, device="cuda")
     s = torch.empty_like(r)

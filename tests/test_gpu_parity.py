@@ -147,7 +147,7 @@ def test_block_precond_configs(cfg_id):
     dv = dq = None
     if w.variable_nu:
         dv, dq = ospaces.nu_scalings(od, synth.viscosity)
-        gdv, gdq = fdp.nu_scalings(gd, synth.viscosity)
+        gdv, gdq = fdp.nu_scalings(gd, synth.viscosity_separable(gd.D))
         assert np.max(np.abs(gdv - dv)) < 1e-14 and np.max(np.abs(gdq - dq)) < 1e-14
     P = fdp.build_block(gd, dscale_vel=dv, dscale_pres=dq)
     s = P.apply(dev(r), batch=w.batch).cpu().numpy()
@@ -510,7 +510,7 @@ def test_config3_literal_c3_reading():
     assert gd.comp_dims == [c.dims for c in od.comps] and gd.q_dims == od.q_dims
     assert gd.comp_dims[0] == [130, 68, 68] and od.n_total == 2117792
     dv, dq = ospaces.nu_scalings(od, synth.viscosity)
-    gdv, gdq = fdp.nu_scalings(gd, synth.viscosity)
+    gdv, gdq = fdp.nu_scalings(gd, synth.viscosity_separable(gd.D))
     assert np.max(np.abs(gdv - dv)) < 1e-14 and np.max(np.abs(gdq - dq)) < 1e-14
     P = fdp.build_block(gd, dscale_vel=dv, dscale_pres=dq)
     r = synth.rhs(w.seed, od.n_total, 1)

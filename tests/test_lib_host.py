@@ -225,3 +225,42 @@ def test_mass_diag_factor_matches_oracle():
         assert np.max(np.abs(F - ref)) < 1e-14
         _, M = univariate.stiffness_mass(deg, alpha, n_el)
         assert np.max(np.abs(F.sum(axis=1) - np.diag(M))) < 1e-14
+
+
+def test_library_nu_scalings_pinned_axis_asymmetric():
+    """libfdp's D_V / D_Q sampling (fdp_kron_diag over iga_greville points, a different code path
+    from the oracle's meshgrid) against the same hand-evaluated RT p = 2, n_el = 2 values as
+    tests/test_oracle_mass_block.py (C-6)."""
+    g_own, g_tan = [1 / 6, 1 / 2, 5 / 6], [0.0, 1 / 4, 3 / 4, 1.0]
+    nu = lambda x, y, z: 1.0 + x + 10.0 * y + 100.0 * z
+    ident = lambda x: np.asarray(x, dtype=float)
+    terms = [(1.0, None), (1.0, [ident, None, None]), (10.0, [None, ident, None]),
+             (100.0, [None, None, ident])]
+    terms = [(c, None if ws is None else [w if w is not None else (lambda x: np.ones(len(x)))
+                                          for w in ws]) for c, ws in terms]
+    gd = fdp.discretization(3, "RT", 2, 2)
+    dv, dq = fdp.nu_scalings(gd, terms)
+    off = 0
+    for k in range(3):
+        g = [g_own if d == k else g_tan for d in range(3)]
+        exp = [nu(g[0][i1], g[1][i2], g[2][i3])
+               for i3 in range(len(g[2])) for i2 in range(len(g[1])) for i1 in range(len(g[0]))]
+        np.testing.assert_allclose(dv[off:off + len(exp)], exp, rtol=1e-14)
+        off += len(exp)
+    expq = [1 / nu(g_tan[i1], g_tan[i2], g_tan[i3]) for i3 in range(4) for i2 in range(4) for i1 in range(4)]
+    np.testing.assert_allclose(dq, expq, rtol=1e-14)
+    with pytest.raises(TypeError):
+        fdp.nu_scalings(gd, nu)
+
+
+def test_library_nu_scalings_config3_matches_oracle():
+    """Config-3-shaped sampling (RT p = 4, small n_el) of synth's nu: library (separable terms,
+    fdp_kron_diag) vs oracle (nu evaluated on the meshgrid)."""
+    import synth
+    from oracle import spaces
+    gd = fdp.discretization(3, "RT", 4, 5)
+    od = spaces.build(3, "RT", 4, 5)
+    dv, dq = fdp.nu_scalings(gd, synth.viscosity_separable(3))
+    odv, odq = spaces.nu_scalings(od, synth.viscosity)
+    np.testing.assert_allclose(dv, odv, rtol=1e-14, atol=1e-15)
+    np.testing.assert_allclose(dq, odq, rtol=1e-14)

@@ -102,3 +102,47 @@ def test_greville_scaling_constant_nu():
     disc = spaces.build(3, "RT", 2, 2)
     dv, dq = spaces.nu_scalings(disc, lambda x, y, z: 3.0 + 0 * x)
     assert np.allclose(dv, 3.0) and np.allclose(dq, 1.0 / 3.0)
+
+
+# Hand-evaluated Greville abscissae (xi_{j+1} + ... + xi_{j+deg}) / deg for RT p = 2 (alpha = 1),
+# n_el = 2 (C-6, C-8):
+#   own direction S^3_2, knots [0,0,0,0,1/2,1,1,1,1] -> [0, 1/6, 1/2, 5/6, 1], interior (first
+#     and last dropped): [1/6, 1/2, 5/6];
+#   tangential S^2_1 (full), knots [0,0,0,1/2,1,1,1] -> [0, 1/4, 3/4, 1];
+#   pressure S^2_1 (full): [0, 1/4, 3/4, 1].
+_G_OWN = [1 / 6, 1 / 2, 5 / 6]
+_G_TAN = [0.0, 1 / 4, 3 / 4, 1.0]
+
+
+def _nu_asym(x, y, z):
+    """An axis-asymmetric coefficient: each direction carries a different weight, so a swapped
+    Greville set, a kept boundary dof or a C-order reshape changes the sampled values."""
+    return 1.0 + x + 10.0 * y + 100.0 * z
+
+
+def test_nu_scalings_pinned_axis_asymmetric():
+    """Config 3's D_V / D_Q sampling (C-6: D_V[i] = nu(Greville point of dof i), D_Q = 1/nu) on RT
+    p = 2, n_el = 2 against hand-evaluated values at named dofs and against the full tensor grid
+    typed out from the hand Greville lists (vec order i1 fastest)."""
+    disc = spaces.build(3, "RT", 2, 2)
+    assert [c.dims for c in disc.comps] == [[3, 4, 4], [4, 3, 4], [4, 4, 3]]
+    dv, dq = spaces.nu_scalings(disc, _nu_asym)
+    o = disc.offsets()
+    # named dofs: component 1, (i1, i2, i3) = (1, 2, 3) -> (1/2, 3/4, 1): 1 + .5 + 7.5 + 100
+    assert dv[o[0] + 1 + 3 * 2 + 12 * 3] == pytest.approx(109.0, rel=1e-15)
+    # component 2, (3, 0, 1) -> (1, 1/6, 1/4): 1 + 1 + 10/6 + 25
+    assert dv[o[1] + 3 + 4 * 0 + 12 * 1] == pytest.approx(1 + 1 + 10 / 6 + 25, rel=1e-15)
+    # component 3, (1, 2, 2) -> (1/4, 3/4, 5/6): 1 + 1/4 + 7.5 + 500/6
+    assert dv[o[2] + 1 + 4 * 2 + 16 * 2] == pytest.approx(1 + 0.25 + 7.5 + 500 / 6, rel=1e-15)
+    # component 1's first dof sits at the first INTERIOR own-direction point: (1/6, 0, 0)
+    assert dv[o[0]] == pytest.approx(1 + 1 / 6, rel=1e-15)
+    # pressure (2, 1, 3) -> (3/4, 1/4, 1): 1/(1 + .75 + 2.5 + 100)
+    assert dq[2 + 4 * 1 + 16 * 3] == pytest.approx(1 / 104.25, rel=1e-15)
+    for k in range(3):
+        g = [_G_OWN if d == k else _G_TAN for d in range(3)]
+        exp = [_nu_asym(g[0][i1], g[1][i2], g[2][i3])
+               for i3 in range(len(g[2])) for i2 in range(len(g[1])) for i1 in range(len(g[0]))]
+        np.testing.assert_allclose(dv[o[k]:o[k + 1]], exp, rtol=1e-15)
+    expq = [1 / _nu_asym(_G_TAN[i1], _G_TAN[i2], _G_TAN[i3])
+            for i3 in range(4) for i2 in range(4) for i1 in range(4)]
+    np.testing.assert_allclose(dq, expq, rtol=1e-15)
