@@ -185,6 +185,12 @@ fdp_status block_precond_destroy(fdp_block h);
  * handle or batch <= 0, -1 on an internal error. */
 int fdp_block_launch_count(fdp_block h, int64_t batch);
 
+/* Diagnostics: the number of kernel launches since library load that took the TMA-fed folded
+ * transform kernel K1t, and the number that took the round-1 cp.async folded
+ * kernel K1f instead (operands no tensor map can describe, or FDP_NO_TMA=1). Host-side counters
+ * of enqueued launches (a CUDA-graph replay does not count again). */
+int64_t fdp_debug_k1_launches(int tma);
+
 /* Per-launch timing of block_precond_apply (roofline diagnostics). With enable != 0 every later
  * apply records a CUDA event on its stream before each kernel launch and after the last one (the
  * events become nodes of the cached graph, which is re-captured when the flag changes).

@@ -123,6 +123,8 @@ static void free_fd(fdp_fd h) {
     cudaFree(h->WfF[d]);
     cudaFree(h->WbF[d]);
     cudaFree(h->lamcF[d]);
+    cudaFree(h->WtF[d]);
+    cudaFree(h->WtB[d]);
   }
   cudaFree(h->ws);
   cudaFree(h->sync);
@@ -245,6 +247,22 @@ extern "C" fdp_status fd_setup(int D, const int32_t* n, const double* const* K,
           free_fd(raw);
           return fail((fdp_status)fst, "fd_setup (folded): " + err);
         }
+        if (k1_fold) {  // K1t fragment-native chunks (mode 1 is the KMAJ pass)
+          const std::vector<double> tf = tma_wt_build(nd, foldh, ldwf, wff, d == 0);
+          const std::vector<double> tb = tma_wt_build(nd, foldh, ldwb, wbf, d == 0);
+          fdp_status as;
+          if ((as = dalloc(&raw->WtF[d], tf.size())) || (as = dalloc(&raw->WtB[d], tb.size()))) {
+            free_fd(raw);
+            return as;
+          }
+          cudaError_t e;
+          if ((e = cudaMemcpy(raw->WtF[d], tf.data(), tf.size() * 8, cudaMemcpyHostToDevice)) ||
+              (e = cudaMemcpy(raw->WtB[d], tb.data(), tb.size() * 8, cudaMemcpyHostToDevice)) ||
+              (e = prepare_mode_tma())) {
+            free_fd(raw);
+            return cuda_fail(e, "fd_setup: K1t chunks");
+          }
+        }
         raw->fold[d] = small_fold ? 1 : 2;
         raw->fold_nt[d] = nt;
         raw->foldh[d] = foldh;
@@ -302,7 +320,7 @@ extern "C" fdp_status fd_setup(int D, const int32_t* n, const double* const* K,
       raw->sync_batch = sb;
     }
     if (max_batch > 0) {
-      fdp_status st = dalloc(&raw->ws, (size_t)(2 * max_batch * Npad(raw)));
+      fdp_status st = dalloc(&raw->ws, (size_t)(2 * max_batch * Npad(raw) + kWsSlack));
       if (st) {
         free_fd(raw);
         return st;
@@ -386,7 +404,7 @@ extern "C" fdp_status fd_operator_diagonal(fdp_fd h, double* out) {
 extern "C" int64_t fd_size(fdp_fd h) { return h ? h->N : 0; }
 extern "C" size_t fd_workspace_bytes(fdp_fd h, int64_t batch) {
   try {
-    return h && batch > 0 ? (size_t)(2 * batch * Npad(h)) * sizeof(double) : 0;
+    return h && batch > 0 ? (size_t)(2 * batch * Npad(h) + kWsSlack) * sizeof(double) : 0;
   } catch (...) {
     return 0;
   }
@@ -448,6 +466,7 @@ static ModeProb make_mode_prob(const fdp_fd_s* h, int d, bool fwd, const double*
       p.fold_k1 = 1;
       p.tiles_n = fwd ? h->cfgFf[d].tiles_n : h->cfgFb[d].tiles_n;
       p.tiles_ne = h->tiles_ne[d];
+      p.Wt = fwd ? h->WtF[d] : h->WtB[d];
     }
   }
   return p;
@@ -573,7 +592,13 @@ cudaError_t launch_stage(std::vector<ModeProb>& probs_in, const std::vector<Tile
         g_trace_used += need;
       }
     }
+    // folded K1 problems whose operands a tensor map can describe: the TMA kernel K1t
+    bool tma = !small && g.prob[0].fold_k1 && g.count <= kTmaMaxProbs;
+    for (int j = 0; j < g.count && tma; ++j)
+      tma = tma_eligible(g.prob[j], kmaj) && tma_input_ok(g.prob[j], kmaj);
+    if (!small && !tma && g.prob[0].fold_k1) ++g_k1_launches[0];
     cudaError_t e = small ? launch_mode_small(g, cfgs[i].NT, kmaj, s)
+                    : tma ? launch_tma_stage(g.prob, g.count, kmaj, s)
                           : launch_mode_group(g, cfgs[i], kmaj, s);
     if (e != cudaSuccess) return e;
     if (nlaunch) ++*nlaunch;
@@ -1000,6 +1025,22 @@ cudaError_t enqueue_fd(const std::vector<const fdp_fd_s*>& hs,
       if (hs[k]->fold[d] == 1) c.NT = hs[k]->fold_nt[d];
       if (hs[k]->fold[d] == 2) c = st.fwd ? hs[k]->cfgFf[d] : hs[k]->cfgFb[d];
       cfgs.push_back(c);
+      // K1t reads its first pass through a tensor map: a C-ABI input with odd rows or an
+      // unaligned base is first copied into the second intermediate with padded rows
+      ModeProb& pk = probs.back();
+      if (first && d == 0 && tma_eligible(pk, true) && !tma_input_ok(pk, true)) {
+        const long long rows = hs[k]->N / hs[k]->n[0];
+        if (rec) {
+          cudaError_t e0 = rec->before(1, 0.0, 16.0 * hs[k]->N * batch);
+          if (e0 != cudaSuccess) return e0;
+        }
+        cudaError_t e = launch_pad_rows(src, sbs, buf1, np, hs[k]->n[0], n1pad(hs[k]), rows, batch, s);
+        if (e != cudaSuccess) return e;
+        if (nlaunch) ++*nlaunch;
+        pk.X = buf1;
+        pk.xld = n1pad(hs[k]);
+        pk.xbs = np;
+      }
     }
     if (hook) hook(pass, st.fwd, d, probs, cfgs);
     if (pp && (pass == 0 || pass == 3)) {

@@ -171,7 +171,7 @@ extern "C" int64_t block_precond_size(fdp_block h) { return h ? h->size : 0; }
 static long long block_ws_elems(const fdp_block_s* h, int64_t batch) {
   long long v = 0;
   for (const fdp_fd_s* f : h->vel) v += 2 * Npad(f);
-  return batch * (v + (h->pres_dense ? 2 * h->pres->N : 0));
+  return batch * (v + (h->pres_dense ? 2 * h->pres->N : 0)) + kWsSlack;
 }
 extern "C" size_t block_precond_workspace_bytes(fdp_block h, int64_t batch) {
   try {

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "fdp_internal.h"
+#include "mode_tma.h"
 
 
 // ------------------------------------------------------------------------------------------------
@@ -164,6 +165,9 @@ struct fdp_fd_s {
   double* WfF[3] = {nullptr, nullptr, nullptr};
   double* WbF[3] = {nullptr, nullptr, nullptr};
   double* lamcF[3] = {nullptr, nullptr, nullptr};
+  // K1t fragment-native chunks of the folded forward / backward matrices (fold[d] == 2)
+  double* WtF[3] = {nullptr, nullptr, nullptr};
+  double* WtB[3] = {nullptr, nullptr, nullptr};
   double* ws = nullptr;
   int64_t ws_batch = 0;
   int* sync = nullptr;        // plane-pipeline counters (zeroed, self-resetting)
@@ -268,6 +272,21 @@ struct fdp_kron_s {
 // ------------------------------------------------------------------------------------------------
 // launch orchestration shared by the ABI files (abi_fd.cpp)
 // ------------------------------------------------------------------------------------------------
+// K1t host side (abi_tma.cpp)
+#include <atomic>
+namespace fdp {
+extern std::atomic<long long> g_k1_launches[2];  // [0] K1f folded launches, [1] K1t
+int tma_ctiles(int ne);
+std::vector<double> tma_wt_build(int n, int foldh, int ldw, const std::vector<double>& w, bool kmaj);
+bool tma_eligible(const ModeProb& p, bool kmaj);
+bool tma_input_ok(const ModeProb& p, bool kmaj);
+cudaError_t launch_tma_stage(const ModeProb* probs, int count, bool kmaj, cudaStream_t s);
+cudaError_t launch_pad_rows(const double* x, long long xbs, double* y, long long ybs, int n1,
+                            int n1p, long long rows, long long batch, cudaStream_t s);
+}  // namespace fdp
+// Workspace slack (doubles): K1t's non-KMAJ tensor maps read up to 15 elements past the end of a
+// tensor in the last (partial) p-group (computed, never stored); every workspace size adds this.
+constexpr long long kWsSlack = 32;
 // Even-odd folding helpers (abi.cpp). fold_nt: the small-kernel NT of a folded extent n.
 bool persymmetric(int n, const double* A, double rtol);
 inline int fold_nt(int n) { return 2 * (((n + 1) / 2 + 7) / 8); }

@@ -77,6 +77,9 @@ struct ModeProb {
   // KMAJ small-path loads: optional input scaling x <- pre o x (pre indexed like the input within
   // one item: the P^G pre-scaling D^{-1/2} fused into the first pass)
   const double* pre;
+  // K1t (kernels/mode_tma.cu): fragment-native folded W chunks of this transform, or NULL when
+  // the TMA kernel cannot take it (see mode_tma.h)
+  const double* Wt;
   // Peer-store scatter (slab exchange fused into the epilogue): when peers != NULL,
   // output element (GEMM row m, column a) of a batch-1, non-KMAJ problem is stored at
   // peers[o] + r + sc_n1 * ((a - lo_o) * (sc_a0 + sc_a1 * len_o) + (q + sc_qoff) * (sc_q0 + sc_q1 * len_o))

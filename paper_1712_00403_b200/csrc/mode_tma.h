@@ -1,0 +1,64 @@
+// K1t (kernels/mode_tma.cu): the TMA-fed, warp-specialised even-odd folded FD transform.
+// Shared by the kernel and the host orchestration (abi.cpp); nothing here crosses the C ABI.
+#pragma once
+
+#include <cuda.h>
+
+#include "fdp_internal.h"
+
+namespace fdp {
+
+#ifndef FDP_K1T_BM
+#define FDP_K1T_BM 64
+#endif
+#ifndef FDP_K1T_CPS
+#define FDP_K1T_CPS 2
+#endif
+constexpr int kTmaBM = FDP_K1T_BM;           // rows of a CTA tile
+constexpr int kTmaCtasPerSM = FDP_K1T_CPS;   // independent CTAs per SM (DESIGN.md §5 "K1t")
+constexpr int kTmaBK = 16;             // k per pipeline stage
+constexpr int kTmaMaxNT = 9;           // n8 tiles per role and column tile
+constexpr int kTmaWChunk = 4 * 5 * 32 * 2;  // doubles of one role's W chunk per stage
+constexpr int kTmaMaxProbs = 4;
+
+// One folded transform problem of a grouped launch.
+//   A operand (read by TMA through map[i]):
+//     KMAJ (mode 1): 3-D map {n (k, contiguous), Q (rows, stride xld), batch (stride xbs)},
+//       box {16, kTmaBM, 1}; a row tile = kTmaBM consecutive rows of one batch item.
+//     otherwise: 5-D map {16 (p_lo), n (k, stride P), ceil(P/16) (p_hi, stride 16), Q (stride
+//       P n), batch (stride xbs)}, box {16, 16, bp, bq, 1} with bp * bq = kTmaBM / 16; a row tile = bp
+//       16-row p-groups times bq q-lines. Rows p >= P of the last p-group alias the next k line
+//       (read, computed, never stored).
+//   Wt: fragment-native folded eigenvector chunks, [role E/O][ctile][stage][j 4][n8 pair 5]
+//       [lane 32][2] (tmat_build in abi.cpp).
+//   Output Y as ModeProb (KMAJ row stride yld; otherwise column stride P), epilogues EPI_NONE,
+//   EPI_LAMBDA (forward) or EPI_SCALE (backward).
+struct TmaProb {
+  const double* Wt;
+  double* Y;
+  const double* scale;
+  const double* lam0;
+  const double* lam1;
+  const double* lamcol;
+  long long ybs;
+  int n, ne, no, n8h, ctiles, kst;
+  int P, Q, bp, bq, tiles_p, tiles_q;
+  int yld, n1, n1v, epi;
+  int a1odd;      // KMAJ: the second A tile starts at an odd column (odd n FWD / odd ne BWD)
+  int tile_begin;
+};
+
+struct TmaGroup {
+  CUtensorMap map[kTmaMaxProbs];
+  CUtensorMap map2[kTmaMaxProbs];  // KMAJ: the same tensor, box {2, kTmaBM, 1}, no swizzle
+  TmaProb prob[kTmaMaxProbs];
+  int count;
+  int total_tiles;
+  int ct_uniform;  // column tiles of every problem when equal (grid a multiple of it), else 0
+  int dbg;         // timing experiments of the -DFDP_K1T_PROF build (FDP_K1T_DBG)
+};
+
+cudaError_t launch_mode_tma(const TmaGroup& g, bool kmaj, int fold, int grid, cudaStream_t s);
+cudaError_t prepare_mode_tma();
+
+}  // namespace fdp

@@ -156,6 +156,7 @@ def test_block_precond_configs(cfg_id):
     for i in range(w.batch):
         for k in range(len(o) - 1):
             assert rel(s[i, o[k]:o[k + 1]], ref[i, o[k]:o[k + 1]]) < TOL, (cfg_id, k)
+            assert relmax(s[i, o[k]:o[k + 1]], ref[i, o[k]:o[k + 1]]) < TOL, (cfg_id, k)
 
 
 def test_block_precond_plain_vs_scaled_config3():
@@ -238,16 +239,41 @@ def test_fd_eigs_match_oracle_spectrum():
 
 @pytest.mark.slow
 def test_block_precond_config4_full_size_bench_launch():
-    """Config 4 at full size in the bench launch configuration (batch 8 in one call); items 0 and
-    7 compared with the oracle element by element."""
+    """Config 4 at full size in the bench launch configuration (batch 8 in one call, the K1t
+    folded transforms of DESIGN.md §5): all 8 items compared with the oracle element by element,
+    per block, in relative L2 and max-abs (north_star: <= 1e-9)."""
     w, od, gd = _both(4)
     r = synth.rhs(w.seed, od.n_total, w.batch)
     P = fdp.build_block(gd)
     s = P.apply(dev(r), batch=w.batch)
     ref = oprec.BlockPrecond(od)
-    for i in (0, w.batch - 1):
+    o = od.offsets()
+    for i in range(w.batch):
         si = s[i].cpu().numpy()
-        assert rel(si, ref.apply(r[i])) < TOL
+        ri = ref.apply(r[i])
+        for k in range(len(o) - 1):
+            assert rel(si[o[k]:o[k + 1]], ri[o[k]:o[k + 1]]) < TOL, (i, k)
+            assert relmax(si[o[k]:o[k + 1]], ri[o[k]:o[k + 1]]) < TOL, (i, k)
+
+
+@pytest.mark.slow
+def test_config5_full_size_oracle_parity():
+    """Config 5 (548.8 M dofs, RT p = 4, 512^3) at full size in the bench launch configuration:
+    every block of the GPU apply against the oracle's Algorithm 1 (its own eigensolver, numpy
+    mode products, banded pressure solve) element by element -- relative L2 and max-abs <= 1e-9
+    (north_star). This covers the K1t tiles of n = 515 / 516 (odd-start mirror tiles, 4 column
+    tiles of 9 / 8 n8 tiles) that the random-pencil cases reach only at smaller sizes."""
+    w, od, gd = _both(5)
+    b = synth.rhs(w.seed, od.n_total, 1)[0]
+    P = fdp.build_block(gd)
+    x = P.apply(dev(b)).cpu().numpy()
+    del P
+    torch.cuda.empty_cache()
+    ref = oprec.BlockPrecond(od).apply(b)
+    o = od.offsets()
+    for k in range(len(o) - 1):
+        assert rel(x[o[k]:o[k + 1]], ref[o[k]:o[k + 1]]) < TOL, k
+        assert relmax(x[o[k]:o[k + 1]], ref[o[k]:o[k + 1]]) < TOL, k
 
 
 @pytest.mark.parametrize("env", [{"FDP_NO_SMALL": "1"}, {"FDP_NO_FUSE": "1"}, {"FDP_PRESSURE": "banded"},
@@ -538,3 +564,49 @@ def test_block_precond_k1_sized_pressure(env, monkeypatch):
     for i in range(2):
         for k in range(len(o) - 1):
             assert rel(s[i, o[k]:o[k + 1]], ref[i, o[k]:o[k + 1]]) < TOL, (env, k)
+
+
+def relmax(a, b):
+    """max |a - b| / max |b|: a single wrong element fails it even when the L2 norm hides it."""
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.max(np.abs(a - b)) / np.max(np.abs(b)))
+
+
+@pytest.mark.parametrize("dims,coef,batch,dscale", [
+    ((516, 9, 7), (2.0, 1.0, 1.0), 1, False),   # config 5's even extent in mode 1 (KMAJ K1t)
+    ((516, 9, 7), (2.0, 1.0, 1.0), 2, True),    # ... batch 2, P^G (odd item stride: pad pass)
+    ((7, 515, 9), (1.0, 2.0, 1.0), 1, True),    # config 5's odd extent in mode 2 (5-D maps)
+    ((7, 515, 9), (1.0, 2.0, 1.0), 2, False),
+    ((9, 7, 516), (1.0, 1.0, 2.0), 1, False),   # mode 3: Lambda epilogue on K1t
+    ((9, 7, 516), (1.0, 1.0, 2.0), 3, True),
+    ((259, 130, 97), (2.0, 1.0, 1.0), 2, True), # config 4's extent, odd n1 (pad pass), 3 folded K1 modes
+    ((260, 131, 99), (1.0, 2.0, 1.0), 1, False),# even n1: the input read in place by TMA
+    ((130, 300, 97), (1.0, 1.0, 2.0), 2, False),# several column tiles and p-groups, batch 2
+    ((97, 2), (2.0, 1.0), 2, True),             # 2D, KMAJ only
+])
+def test_k1t_folded_transforms(dims, coef, batch, dscale):
+    """K1t (TMA + mbarrier folded transform) on random persymmetric pencils whose
+    folded modes exceed the small path: element-wise against the oracle's dense Algorithm 1
+    (rel. L2 and max-abs <= 1e-9, north_star) and against the cp.async K1f path (FDP_NO_TMA=1,
+    <= 1e-12); the TMA kernel must actually have run."""
+    import os
+    rng = np.random.default_rng(sum(dims) + 11 * batch)
+    Ks = [_rand_persym_spd(n, rng, 1.0) for n in dims]
+    Ms = [_rand_persym_spd(n, rng, 2.0) for n in dims]
+    N = int(np.prod(dims))
+    b = rng.standard_normal((batch, N))
+    dsc = rng.uniform(0.5, 1.5, N) if dscale else None
+    kw = {"dscale": dev(1.0 / np.sqrt(dsc))} if dscale else {}
+    t0 = int(fdp.lib.fdp_debug_k1_launches(1))
+    x = fdp.FD(Ks, Ms, coef).apply(dev(b), batch=batch, **kw).cpu().numpy()
+    assert int(fdp.lib.fdp_debug_k1_launches(1)) > t0, "K1t did not run"
+    os.environ["FDP_NO_TMA"] = "1"
+    try:
+        x_f = fdp.FD(Ks, Ms, coef).apply(dev(b), batch=batch, **kw).cpu().numpy()
+    finally:
+        del os.environ["FDP_NO_TMA"]
+    ref = ofd.FDSolver(Ks, Ms, coef)
+    for i in range(batch):
+        r = ofd.scaled_apply(ref, b[i], dsc) if dscale else ref.apply(b[i])
+        assert rel(x[i], r) < TOL and relmax(x[i], r) < TOL
+        assert rel(x[i], x_f[i]) < 1e-12
