@@ -66,6 +66,7 @@ def _load():
         "block_precond_apply_host": (i32, [vp, vp, vp, i64, vp]),
         "block_precond_destroy": (i32, [vp]),
         "fdp_block_launch_count": (i32, [vp, i64]),
+        "fdp_debug_k1_launches": (i64, [i32]),
         "block_precond_profile": (i32, [vp, i32]),
         "fdp_slab_range": (i32, [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
         "kron_op_setup": (i32, [i32, i32, vp, vp, vp, vp, i32, ctypes.POINTER(vp)]),

@@ -127,7 +127,6 @@ static void free_fd(fdp_fd h) {
     cudaFree(h->WtB[d]);
   }
   cudaFree(h->ws);
-  cudaFree(h->sync);
   delete h;
 }
 
@@ -302,22 +301,6 @@ extern "C" fdp_status fd_setup(int D, const int32_t* n, const double* const* K,
         free_fd(raw);
         return cuda_fail(e, "fd_setup: upload");
       }
-    }
-    {
-      const int64_t sb = std::max<int64_t>(1, max_batch);
-      const long long cap = 2 * ((long long)raw->n[2] * sb + 1);
-      fdp_status st = dalloc(&raw->sync, (size_t)cap);
-      if (st) {
-        free_fd(raw);
-        return st;
-      }
-      cudaError_t e = cudaMemset(raw->sync, 0, cap * sizeof(int));
-      if (e != cudaSuccess) {
-        free_fd(raw);
-        return cuda_fail(e, "fd_setup: sync init");
-      }
-      raw->sync_cap = cap;
-      raw->sync_batch = sb;
     }
     if (max_batch > 0) {
       fdp_status st = dalloc(&raw->ws, (size_t)(2 * max_batch * Npad(raw) + kWsSlack));
@@ -606,64 +589,6 @@ cudaError_t launch_stage(std::vector<ModeProb>& probs_in, const std::vector<Tile
   return cudaSuccess;
 }
 
-// Plane pipeline: phase-1 problems probs1 (mode 0 fwd or mode 1 bwd) and phase-2 problems probs2
-// (mode 1 fwd or mode 0 bwd) of the same tensors in one launch (D = 3, small path, NT <= 10).
-// sync: zero-initialised ints (self-resetting), capacity sync_cap.
-static cudaError_t launch_pp_stage(std::vector<ModeProb>& probs1, std::vector<ModeProb>& probs2,
-                                   int NT, bool kmaj1, int* sync, long long sync_cap,
-                                   cudaStream_t s, int* nlaunch, Recorder* rec) {
-  if (probs1.size() > (size_t)kSmallGroup || probs2.size() != probs1.size()) return cudaErrorInvalidValue;
-  ModeGroup g1{}, g2{};
-  g1.count = g2.count = (int)probs1.size();
-  std::vector<double> w(g1.count);
-  PlaneSync ps{};
-  long long off = 0;
-  for (int j = 0; j < g1.count; ++j) {
-    ModeProb a = probs1[j], b = probs2[j];
-    a.tiles_m = (int)(((long long)a.P * a.Q * a.batch + 7) / 8);
-    b.tiles_m = (int)(((long long)b.P * b.Q * b.batch + 7) / 8);
-    w[j] = (double)a.tiles_m * ((a.n + 3) / 4) + (double)b.tiles_m * ((b.n + 3) / 4);
-    g1.prob[j] = a;
-    g2.prob[j] = b;
-    // planes = the (i3, item) slices; rows per plane of each phase
-    const int rpp1 = kmaj1 ? b.n : a.P, rpp2 = kmaj1 ? b.P : a.n, planes = kmaj1 ? b.Q : a.Q;
-    ps.cnt_off[j] = (int)off;
-    ps.rows_per_plane1[j] = rpp1;
-    ps.rows_per_plane2[j] = rpp2;
-    off += (long long)planes * a.batch;
-  }
-  if (off + 1 > sync_cap) return cudaErrorInvalidValue;
-  alloc_small_ctas(g1, w);
-  for (int j = 0; j < g1.count; ++j) {
-    g2.prob[j].ctas = g1.prob[j].ctas;
-    g2.prob[j].cta_begin = g1.prob[j].cta_begin;
-  }
-  g2.total_ctas = g1.total_ctas;
-  ps.cnt = sync;
-  ps.done = sync + off;
-  ps.cnt_total = (int)off;
-  if (rec) {
-    double fl = 0.0, by = 0.0;
-    for (int j = 0; j < g1.count; ++j) {
-      fl += recorded_flops(g1.prob[j]) + recorded_flops(g2.prob[j]);
-      by += recorded_bytes(g1.prob[j]) + recorded_bytes(g2.prob[j]);
-    }
-    cudaError_t e0 = rec->before(0, fl, by);
-    if (e0 != cudaSuccess) return e0;
-  }
-  cudaError_t e = launch_mode_pp(g1, g2, ps, NT, kmaj1, s);
-  if (e != cudaSuccess) return e;
-  if (nlaunch) ++*nlaunch;
-  return cudaSuccess;
-}
-
-long long pp_sync_ints(const std::vector<const fdp_fd_s*>& hs, int64_t batch, int extra_n3) {
-  long long n = 0;
-  for (const fdp_fd_s* h : hs) n += (long long)h->n[2] * batch;
-  n += (long long)extra_n3 * batch;
-  return n + 1;  // + done counter
-}
-
 // Enqueue FD solves for several handles (block components) on stream s.
 // in[k], out[k] with batch strides ibs/obs; T[k] workspace with stride N_k. dscale[k] may be NULL.
 // Pre-scaling (if any) must already have been applied by the caller (into out[k]) and `in` point
@@ -910,10 +835,6 @@ static cudaError_t enqueue_fd_plane(const std::vector<const fdp_fd_s*>& hs,
       by += 16.0 * pq->n[0] * pq->n[1] * pq->n[2] * batch;
     }
     g.total = begin;
-    {  // E / O warp pairs: opt-in (measured slower: config 2 53.8 vs 50.3 us, config 3 64.5 vs 59.4)
-      const char* eo = std::getenv("FDP_PLANE_EO");
-      g.eo = eo && eo[0] == '1';
-    }
     const size_t smem = plane_smem_bytes(nt, sp, rows);
     if (smem > 227 * 1024) return cudaErrorInvalidValue;
     const int per_sm = smem <= 112 * 1024 ? 2 : 1;
@@ -968,8 +889,8 @@ cudaError_t enqueue_fd(const std::vector<const fdp_fd_s*>& hs,
                               const std::vector<double*>& out, long long obs,
                               const std::vector<double*>& T,
                               const std::vector<const double*>& dscale, int64_t batch,
-                              cudaStream_t s, int* nlaunch, Recorder* rec, const StageHook& hook, int* sync,
-                              long long sync_cap, const PresPlane* pq, bool fuse_prescale) {
+                              cudaStream_t s, int* nlaunch, Recorder* rec, const StageHook& hook,
+                              const PresPlane* pq, bool fuse_prescale) {
   const int D = hs[0]->D;
   const size_t K = hs.size();
   if ((pq || !hook) && plane_path(hs, pq, batch))
@@ -989,15 +910,6 @@ cudaError_t enqueue_fd(const std::vector<const fdp_fd_s*>& hs,
   for (int d = D - 1; d >= 0; --d)
     if (!(fuse && d == D - 1)) stages.push_back({d, false, false});
   const int npass = (int)stages.size();
-  // plane pipeline (D = 3): passes (0, 1) and (3, 4) each become one launch
-  // (opt-in, FDP_PP=1: with about one 8-row tile per warp per pass at batch 1 the two passes
-  // cannot overlap, so the separate launches are as fast)
-  bool pp = fuse && D == 3 && sync != nullptr && std::getenv("FDP_PP") != nullptr;
-  for (size_t k = 0; k < K; ++k)
-    for (int d = 0; d < 2; ++d)
-      pp = pp && hs[k]->cfg[d].NT <= kPPMaxNT && hs[k]->cfg[d].NT == hs[0]->cfg[0].NT &&
-           !hs[k]->fold[d];
-  std::vector<ModeProb> held;  // phase-1 problems waiting for their phase-2 partners
   for (int pass = 0; pass < npass; ++pass) {
     const Stage& st = stages[pass];
     const int d = st.d;
@@ -1043,35 +955,6 @@ cudaError_t enqueue_fd(const std::vector<const fdp_fd_s*>& hs,
       }
     }
     if (hook) hook(pass, st.fwd, d, probs, cfgs);
-    if (pp && (pass == 0 || pass == 3)) {
-      bool ok = probs.size() <= (size_t)kSmallGroup;
-      for (const ModeProb& p : probs) ok = ok && small_ok(p);
-      if (ok) {
-        held = probs;
-        continue;
-      }
-      pp = false;  // fall back to one launch per pass
-    }
-    if (pp && (pass == 1 || pass == 4)) {
-      bool ok = probs.size() == held.size();
-      for (const ModeProb& p : probs) ok = ok && small_ok(p);
-      if (ok) {
-        const int sync_half = (int)(sync_cap / 2);
-        int* sy = pass == 1 ? sync : sync + sync_half;
-        cudaError_t e = launch_pp_stage(held, probs, cfgs[0].NT, pass == 1, sy, sync_half, s,
-                                        nlaunch, rec);
-        if (e == cudaSuccess) {
-          held.clear();
-          continue;
-        }
-        if (e != cudaErrorInvalidValue) return e;
-      }
-      // could not pipeline: launch the held pass, then this one
-      std::vector<TileCfg> hc(held.size(), cfgs[0]);
-      cudaError_t e = launch_stage(held, hc, pass == 1, s, nlaunch, rec);
-      if (e != cudaSuccess) return e;
-      held.clear();
-    }
     cudaError_t e = launch_stage(probs, cfgs, d == 0, s, nlaunch, rec);
     if (e != cudaSuccess) return e;
   }
@@ -1104,9 +987,8 @@ extern "C" fdp_status fd_apply(fdp_fd h, const double* b, double* x, const doubl
       FDP_CUDA(launch_scale(b, x, dscale, h->N, batch, h->N, h->N, s), "fd_apply: prescale");
       src = x;
     }
-    const bool sy = batch <= h->sync_batch;
     FDP_CUDA(enqueue_fd({h}, {src}, h->N, {x}, h->N, {T}, {dscale}, batch, s, nullptr, nullptr,
-                        nullptr, sy ? h->sync : nullptr, sy ? h->sync_cap : 0, nullptr, fuse),
+                        nullptr, nullptr, fuse),
              "fd_apply");
     return FDP_OK;
   } catch (...) {

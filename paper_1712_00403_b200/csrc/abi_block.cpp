@@ -9,7 +9,6 @@
 static void free_block(fdp_block h) {
   if (!h) return;
   for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
-  cudaFree(h->sync);
   for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);
   if (h->cap) cudaStreamDestroy(h->cap);
   cudaFree(h->dv);
@@ -293,14 +292,12 @@ static cudaError_t enqueue_block(fdp_block h, const double* r, double* s, int64_
       (void)pass;
     };
   }
-  const long long need = 2 * pp_sync_ints(h->vel, batch, h->pres_dense && D == 3 ? h->pres->n[2] : 0);
-  const bool sy = h->sync && h->sync_cap >= need;
   if (pplane) {
     pq.rq = rq;
     pq.rbs = sz;
   }
   cudaError_t e = enqueue_fd(h->vel, in, sz, out, sz, T, dsc, batch, st, nlaunch, rec, hook,
-                             sy ? h->sync : nullptr, sy ? need : 0, pplane ? &pq : nullptr, fuse_pre);
+                             pplane ? &pq : nullptr, fuse_pre);
   if (e != cudaSuccess) return e;
   if (!h->pres_dense) {
     // pressure block by banded per-mode solves: r_p -> s_p
@@ -381,11 +378,6 @@ extern "C" int fdp_block_launch_count(fdp_block h, int64_t batch) {
     for (int k = 0; k < D; ++k)
       for (int d = 0; d < D; ++d) fuse = fuse && h->vel[k]->n[d] <= kSmallMaxN && h->vel[k]->cfg[d].tiles_n == 1;
     if (fuse) n -= 1;
-    bool pp = fuse && D == 3 && std::getenv("FDP_PP") != nullptr;
-    for (int k = 0; k < D; ++k)
-      for (int d = 0; d < 2; ++d)
-        pp = pp && h->vel[k]->cfg[d].NT <= kPPMaxNT && h->vel[k]->cfg[d].NT == h->vel[0]->cfg[0].NT;
-    if (pp) n -= 2;
     if (!h->pres_dense) n += h->pres->D;
     else if (h->dall) n += h->dv ? 0 : 1;
     return n;
@@ -415,20 +407,6 @@ extern "C" fdp_status block_precond_apply(fdp_block h, const double* r, double* 
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     FDP_CUDA(cudaStreamIsCapturing(st, &cs), "block_precond_apply: capture query");
-    if (!same && cs != cudaStreamCaptureStatusActive) {
-      const long long need =
-          2 * pp_sync_ints(h->vel, batch, h->pres_dense && h->D == 3 ? h->pres->n[2] : 0);
-      if (h->sync_cap < need) {
-        FDP_CUDA(cudaStreamSynchronize(st), "block_precond_apply: sync before realloc");
-        cudaFree(h->sync);
-        h->sync = nullptr;
-        h->sync_cap = 0;
-        fdp_status s2 = dalloc(&h->sync, (size_t)need);
-        if (s2) return s2;
-        FDP_CUDA(cudaMemset(h->sync, 0, need * sizeof(int)), "block_precond_apply: sync init");
-        h->sync_cap = need;
-      }
-    }
     if (cs == cudaStreamCaptureStatusActive) {
       FDP_CUDA(enqueue_block(h, r, s, batch, static_cast<double*>(workspace), st, nullptr),
                "block_precond_apply");

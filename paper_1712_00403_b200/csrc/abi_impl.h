@@ -170,9 +170,6 @@ struct fdp_fd_s {
   double* WtB[3] = {nullptr, nullptr, nullptr};
   double* ws = nullptr;
   int64_t ws_batch = 0;
-  int* sync = nullptr;        // plane-pipeline counters (zeroed, self-resetting)
-  long long sync_cap = 0;
-  int64_t sync_batch = 0;
 };
 
 // Intermediate tensors between passes use an even leading dimension n1p (16-byte aligned rows
@@ -229,8 +226,6 @@ struct fdp_block_s {
   std::vector<std::pair<int64_t, int>> launch_counts;  // (batch, kernels) of captured applies
   unsigned long long tick = 0;
   // plane-pipeline counters (zeroed at allocation, self-resetting)
-  int* sync = nullptr;
-  long long sync_cap = 0;
   // profiling
   bool prof = false;
   std::vector<cudaEvent_t> ev;
@@ -297,7 +292,6 @@ using StageHook = std::function<void(int pass, bool fwd, int d, std::vector<Mode
                                      std::vector<TileCfg>&)>;
 cudaError_t launch_stage(std::vector<ModeProb>& probs_in, const std::vector<TileCfg>& cfgs_in,
                          bool kmaj, cudaStream_t s, int* nlaunch, Recorder* rec);
-long long pp_sync_ints(const std::vector<const fdp_fd_s*>& hs, int64_t batch, int extra_n3);
 // Dense P_Q riding in the plane path (D = 3, every M_d^{-1} folded): mode 1 (FOLD_SYM, plane-major
 // output into Tq) joins the velocity mode-1 forward launch, modes 2 and 3 are planes of kind 1
 // in the plane launch, which stores s_p (optionally scaled) at out.
@@ -325,8 +319,7 @@ cudaError_t enqueue_fd(const std::vector<const fdp_fd_s*>& hs,
                        const std::vector<double*>& T,
                        const std::vector<const double*>& dscale, int64_t batch,
                        cudaStream_t s, int* nlaunch, Recorder* rec = nullptr,
-                       const StageHook& hook = nullptr, int* sync = nullptr,
-                       long long sync_cap = 0, const PresPlane* pq = nullptr,
+                       const StageHook& hook = nullptr, const PresPlane* pq = nullptr,
                        bool fuse_prescale = false);
 cudaError_t enqueue_mass(const fdp_mass_s* h, int mode, const double* in, double* out,
                          long long bs, const double* dscale, int64_t batch, cudaStream_t s,

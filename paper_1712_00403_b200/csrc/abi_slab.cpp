@@ -588,7 +588,11 @@ extern "C" size_t kron_mass_slab_workspace_bytes(fdp_mass h, int nranks, int ran
     if (!h || h->D != 3 || nranks < 1 || rank < 0 || rank >= nranks) return 0;
     long long z0, nz;
     part_range(h->n[2], nranks, rank, &z0, &nz);
-    return (size_t)((long long)h->n[0] * h->n[1] * nz) * sizeof(double);
+    long long y0, ny;
+    part_range(h->n[1], nranks, rank, &y0, &ny);
+    // phase 0 stages the z-slab (n1 n2 nz), phase 1 the y-slab (n1 ny n3): the larger of the two
+    return (size_t)std::max((long long)h->n[0] * h->n[1] * nz, (long long)h->n[0] * ny * h->n[2]) *
+           sizeof(double);
   } catch (...) {
     return 0;
   }

@@ -169,21 +169,7 @@ cudaError_t launch_mode_group(const ModeGroup& g, const TileCfg& cfg, bool kmaj,
 // backward in one pass (the middle of Algorithm 1). The caller fills prob[i].ctas
 // (CTAs per problem, sum = total_ctas) and prob[i].tiles_m = ceil(M/8).
 constexpr int kSmallMaxN = 96;
-constexpr int kPPMaxNT = 10;  // plane pipeline keeps two W tiles in shared memory
 
-// Per-plane completion counters of the plane pipeline (D = 3): problem i's counters start at
-// cnt + cnt_off[i] (batch * n3 ints); a phase-2 row's plane is row / rows_per_plane2[i] and is
-// ready when its counter reaches rows_per_plane1[i]. Self-resetting (last CTA zeroes them).
-struct PlaneSync {
-  int* cnt;
-  int* done;
-  int cnt_off[kSmallGroup];
-  int rows_per_plane1[kSmallGroup];
-  int rows_per_plane2[kSmallGroup];
-  int cnt_total;
-};
-cudaError_t launch_mode_pp(const ModeGroup& g1, const ModeGroup& g2, const PlaneSync& ps, int NT,
-                           bool kmaj1, cudaStream_t s);
 // Folded problems (prob.fold != 0, every problem of the group) take the even-odd kernel; NT is
 // then 2 * ceil(ceil(n/2) / 8) (even).
 cudaError_t launch_mode_small(const ModeGroup& g, int NT, bool kmaj, cudaStream_t s);
@@ -226,7 +212,6 @@ struct PlaneGroup {
   // diagnostics: thread 0 of every CTA records %globaltimer at 8 points of its first plane into
   // trace[blockIdx * 8 + point] when non-null
   unsigned long long* trace;
-  int eo;                 // 16-row tiles split over E / O warp pairs (opt-in, FDP_PLANE_EO=1)
 };
 size_t plane_smem_bytes(int NT, int sp, int rows);
 int plane_stride(int n2);

@@ -520,10 +520,6 @@ cudaError_t launch_t(const ModeGroup* g, cudaStream_t s) {
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)SmemF<MT, NT, KMAJ, FOLD_FWD, kFoldBK>::BYTES);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(mode_contract_fold_kernel<MT, NT, KMAJ, FOLD_FWD, BK>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)SmemF<MT, NT, KMAJ, FOLD_FWD, BK>::BYTES);
-    if (e == cudaSuccess)
       e = cudaFuncSetAttribute(mode_contract_fold_kernel<MT, NT, KMAJ, FOLD_BWD, BK>,
                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)SmemF<MT, NT, KMAJ, FOLD_BWD, BK>::BYTES);
@@ -550,7 +546,6 @@ cudaError_t launch_t(const ModeGroup* g, cudaStream_t s) {
           <<<g->total_ctas, THREADS, SmemF<MT, NT, KMAJ, FOLD_SYM, kFoldBK>::BYTES, s>>>(narrow_group<kSmallGroup>(*g));
       return cudaGetLastError();
     }
-    const bool bk16 = std::getenv("FDP_K1F_BK16") != nullptr;  // experiment switch
     bool scf = false;
     for (int i = 0; i < g->count; ++i) scf = scf || g->prob[i].peers != nullptr;
     if (scf) {  // peer-store problems: non-KMAJ, batch 1
@@ -563,12 +558,9 @@ cudaError_t launch_t(const ModeGroup* g, cudaStream_t s) {
             <<<g->total_ctas, THREADS, SmemF<MT, NT, false, FOLD_BWD, BK>::BYTES, s>>>(narrow_group<kSmallGroup>(*g));
       return cudaGetLastError();
     }
-    if (f == FOLD_FWD && !bk16)
+    if (f == FOLD_FWD)
       mode_contract_fold_kernel<MT, NT, KMAJ, FOLD_FWD, kFoldBK>
           <<<g->total_ctas, THREADS, SmemF<MT, NT, KMAJ, FOLD_FWD, kFoldBK>::BYTES, s>>>(narrow_group<kSmallGroup>(*g));
-    else if (f == FOLD_FWD)
-      mode_contract_fold_kernel<MT, NT, KMAJ, FOLD_FWD, BK>
-          <<<g->total_ctas, THREADS, SmemF<MT, NT, KMAJ, FOLD_FWD, BK>::BYTES, s>>>(narrow_group<kSmallGroup>(*g));
     else
       mode_contract_fold_kernel<MT, NT, KMAJ, FOLD_BWD, BK>
           <<<g->total_ctas, THREADS, SmemF<MT, NT, KMAJ, FOLD_BWD, BK>::BYTES, s>>>(narrow_group<kSmallGroup>(*g));

@@ -298,165 +298,16 @@ __device__ __noinline__ void plane_row(double* Pl, int rs, int ks, int r, int n,
   __syncwarp();
 }
 
-// A 16-row tile split over a warp pair (role 0: the E half, role 1: the O half of every
-// transform), so twice as many warps carry DMMA chains as with plane_tile<NT, 2> at the same B
-// fragment reuse. The halves meet only at the row butterflies: the O warp leaves its o_c in the
-// row's own O region (position n-1-c, c < no), the E warp combines x_c = e_c + o_c,
-// x_{n-1-c} = e_c - o_c. Pair barrier `bar` (64 threads) wherever one warp's writes could meet
-// the other's reads.
-__device__ __forceinline__ void pair_sync(int bar) {
-  asm volatile("bar.sync %0, 64;" ::"r"(bar) : "memory");
-}
-template <int NT>
-__device__ __noinline__ void plane_tile_eo(double* Pl, int rs, int ks, int r0, int nrows, int n,
-                                           const double* W, int step, double lbase,
-                                           const double* lrowv, const double* lamcol, int lane,
-                                           int role, int bar) {
-  constexpr int MT = 2;
-  using S = PS<NT>;
-  constexpr int NTE = S::NTE, SBF = S::SBF;
-  const double* Wr = role == 0 ? W : W + S::KPF * SBF;  // this warp's block
-  const int ne = (n + 1) >> 1, no = n >> 1;
-  const int nh = role == 0 ? ne : no;                  // columns / K of this warp's half
-  const int ntj = (nh + 7) >> 3;                        // column tiles with work
-  const int fr = lane >> 2, fc = lane & 3;
-  double* Ar[MT];
-  bool rv[MT];
-#pragma unroll
-  for (int i = 0; i < MT; ++i) {
-    const int r = r0 + 8 * i + fr;
-    rv[i] = r < nrows;
-    Ar[i] = Pl + (long long)r * rs;
-  }
-  double acc[MT][NTE][2];
-#pragma unroll
-  for (int i = 0; i < MT; ++i)
-#pragma unroll
-    for (int j = 0; j < NTE; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-  if (step != PT_BWDT) {  // forward-style: s (E) or d (O) against this half's matrix
-    const double sg = role == 0 ? 1.0 : -1.0;
-    const int k4n = (nh + 3) >> 2;
-#pragma unroll 2
-    for (int k4 = 0; k4 < k4n; ++k4) {
-      const int k = 4 * k4 + fc;
-      double v[MT];
-#pragma unroll
-      for (int i = 0; i < MT; ++i) v[i] = Ar[i][k * ks] + sg * Ar[i][(n - 1 - k) * ks];
-      double b[NTE];
-#pragma unroll
-      for (int j = 0; j < NTE; ++j) b[j] = Wr[k * SBF + 8 * j + fr];
-#pragma unroll
-      for (int j = 0; j < NTE; ++j)
-        if (j < ntj)
-#pragma unroll
-          for (int i = 0; i < MT; ++i) dmma(acc[i][j], v[i], b[j]);
-    }
-    pair_sync(bar);  // both halves have read the whole rows
-    if (step == PT_FWD || step == PT_FUSED) {
-      const int off = role == 0 ? 0 : ne;
-#pragma unroll
-      for (int i = 0; i < MT; ++i) {
-        if (!rv[i]) continue;
-        const double lrow = step == PT_FUSED ? lbase + lrowv[r0 + 8 * i + fr] : 0.0;
-#pragma unroll
-        for (int j = 0; j < NTE; ++j)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int a = 8 * j + 2 * fc + h;
-            if (a < nh)
-              Ar[i][(off + a) * ks] = step == PT_FUSED ? fdp_div(acc[i][j][h], lrow + lamcol[off + a])
-                                                       : acc[i][j][h];
-          }
-      }
-      __syncwarp();
-      if (step == PT_FWD) return;
-    }
-  }
-  if (step != PT_SYM) {  // backward: e = W_E z_E (role 0) or o = W_O z_O (role 1), W read transposed
-#pragma unroll
-    for (int i = 0; i < MT; ++i)
-#pragma unroll
-      for (int j = 0; j < NTE; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    const int off = role == 0 ? 0 : ne;
-    const int k4n = (nh + 3) >> 2;
-#pragma unroll 2
-    for (int k4 = 0; k4 < k4n; ++k4) {
-      const int k = 4 * k4 + fc;
-      double a[MT];
-#pragma unroll
-      for (int i = 0; i < MT; ++i) a[i] = off + k < n ? Ar[i][(off + k) * ks] : 0.0;
-      double b[NTE];
-#pragma unroll
-      for (int j = 0; j < NTE; ++j) b[j] = Wr[(8 * j + fr) * SBF + k];
-#pragma unroll
-      for (int j = 0; j < NTE; ++j)
-#pragma unroll
-        for (int i = 0; i < MT; ++i) dmma(acc[i][j], a[i], b[j]);
-    }
-    __syncwarp();
-  } else {
-    pair_sync(bar);  // FOLD_SYM: the E warp finished reading the O region of the rows
-  }
-  // the butterfly: o_c parked at position n-1-c by the O warp, combined by the E warp
-  if (role == 1) {
-#pragma unroll
-    for (int i = 0; i < MT; ++i) {
-      if (!rv[i]) continue;
-#pragma unroll
-      for (int j = 0; j < NTE; ++j)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int c = 8 * j + 2 * fc + h;
-          if (c < no) Ar[i][(n - 1 - c) * ks] = acc[i][j][h];
-        }
-    }
-  }
-  pair_sync(bar);
-  if (role == 0) {
-    const bool mid2 = step != PT_SYM && (n & 1);
-#pragma unroll
-    for (int i = 0; i < MT; ++i) {
-      if (!rv[i]) continue;
-#pragma unroll
-      for (int j = 0; j < NTE; ++j)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int c = 8 * j + 2 * fc + h;
-          if (c < ne) {
-            const double e = (mid2 && c == no) ? 2.0 * acc[i][j][h] : acc[i][j][h];
-            const double o = c < no ? Ar[i][(n - 1 - c) * ks] : 0.0;
-            Ar[i][c * ks] = e + o;
-            Ar[i][(n - 1 - c) * ks] = e - o;
-          }
-        }
-    }
-  }
-  __syncwarp();
-}
-
-// All rows of one plane step: full 8-row tiles on the DMMA pipe, dealt over the warps, then the
-// leftover rows (nrows % 8) one per warp on the FMA pipe -- a ragged last tile would cost a full
-// tile's DMMAs on one warp while the others wait at the next barrier.
 template <int NT>
 __device__ __forceinline__ void plane_step(double* Pl, int rs, int ks, int nrows, int n,
                                            const double* W, int step, double lbase,
                                            const double* lrowv, const double* lamcol,
-                                           double* scratch, int warp, int lane, bool eo) {
+                                           double* scratch, int warp, int lane) {
   // 16-row tiles over the full 8-row tiles (an odd last one masked to its 8 rows), the leftover
   // rows (nrows % 8) on the FMA pipe by the warps without a tile
   const int full = nrows >> 3;
   const int t16 = (full + 1) >> 1;
   int first;
-  if (eo) {  // 16-row tiles split over warp pairs (E / O halves); leftover rows to the O warps
-    for (int t = warp >> 1; t < t16; t += PW / 2)
-      plane_tile_eo<NT>(Pl, rs, ks, 16 * t, 8 * full, n, W, step, lbase, lrowv, lamcol, lane,
-                        warp & 1, 1 + (warp >> 1));
-    const int o = (warp & 1) ? (warp >> 1) : PW / 2 + (warp >> 1);  // O warps first
-    for (int r = 8 * full + o; r < nrows; r += PW)
-      plane_row<NT>(Pl, rs, ks, r, n, W, step, lbase, lrowv, lamcol, scratch + warp * 96, lane);
-    return;
-  }
   for (int t = warp; t < t16; t += PW)
     plane_tile<NT, 2>(Pl, rs, ks, 16 * t, 8 * full, n, W, step, lbase, lrowv, lamcol, lane);
   first = t16 % PW;
@@ -548,17 +399,17 @@ __global__ void __launch_bounds__(PTH, 2) mode_plane_kernel(const __grid_constan
 
     const bool fd = pb.kind == 0 || pb.kind == 2;
     // mode 2 on the i3 rows
-    plane_step<NT>(Pl, sp, 1, n3, n2, W2, fd ? PT_FWD : PT_SYM, 0.0, nullptr, nullptr, Sc, warp, lane, grp.eo);
+    plane_step<NT>(Pl, sp, 1, n3, n2, W2, fd ? PT_FWD : PT_SYM, 0.0, nullptr, nullptr, Sc, warp, lane);
     __syncthreads();
     if (tr) tr[3] = gtimer();
     // mode 3 on the a2 columns (FD: forward, Lambda, backward; D = 2: Lambda = lambda_1[row]
     // + lambda_2[column], no plane term)
     const double lb = pb.kind == 0 ? Lm[a1] : 0.0;
-    plane_step<NT>(Pl, 1, sp, n2, n3, W3, fd ? PT_FUSED : PT_SYM, lb, Lm + 96, Lm + 192, Sc, warp, lane, grp.eo);
+    plane_step<NT>(Pl, 1, sp, n2, n3, W3, fd ? PT_FUSED : PT_SYM, lb, Lm + 96, Lm + 192, Sc, warp, lane);
     __syncthreads();
     if (tr) tr[4] = gtimer();
     if (fd) {  // mode-2 backward on the i3 rows
-      plane_step<NT>(Pl, sp, 1, n3, n2, W2, PT_BWDT, 0.0, nullptr, nullptr, Sc, warp, lane, grp.eo);
+      plane_step<NT>(Pl, sp, 1, n3, n2, W2, PT_BWDT, 0.0, nullptr, nullptr, Sc, warp, lane);
       __syncthreads();
       if (tr) tr[5] = gtimer();
     }

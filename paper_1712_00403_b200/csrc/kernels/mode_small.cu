@@ -12,11 +12,6 @@
 //   * EPI_FUSED: mode-D forward contraction, division by Lambda (step 3) and the mode-D
 //     backward contraction in one pass: the 8 x n intermediate stays in shared memory and the
 //     second GEMM reads U_D^T as a transposed view of the same W tile;
-//   * mode_pp_kernel ("plane pipeline", D = 3): the mode-1 and mode-2 contractions of one
-//     direction (forward, or backward in reverse order) in ONE launch. Both contractions are
-//     local to an i3-plane, so a phase-2 tile only waits (per-plane completion counters,
-//     release/acquire) for the phase-1 rows of its plane(s): the loads, DMMAs and stores of the
-//     two passes overlap across warps instead of being separated by a kernel boundary.
 #include <cstdlib>
 
 #include "../fdp_internal.h"
@@ -44,11 +39,6 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "+d"(c[0]), "+d"(c[1])
                : "d"(a), "d"(b));
 }
-__device__ __forceinline__ int ld_acquire(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 
 template <int NT>
 struct SS {
@@ -59,7 +49,6 @@ struct SS {
   static constexpr int ABUF = 8 * SA;
   static constexpr int W_ELEMS = KP * SB;
   static constexpr size_t BYTES = sizeof(double) * (W_ELEMS + SW * ABUF);
-  static constexpr size_t BYTES_PP = sizeof(double) * (2 * W_ELEMS + SW * ABUF);
   // folded W (NT = 2 * NTE): blocks E and O of KPF rows x 8*NTE columns, row stride SBF
   static constexpr int KPF = 4 * NT;
   static constexpr int SBF = ((KPF + 15) / 16) * 16 + 4;
@@ -143,48 +132,6 @@ template <int NT, bool KMAJ, int MT = 1>
 __device__ __forceinline__ void tile_compute_store_fold(const ModeProb& pb, const Geo& g,
                                                         const double* Ws, double* A, long long t,
                                                         int lane, unsigned long long* tr);
-
-// Asynchronous panel load (8-byte cp.async with zero fill beyond n / M) into A ([8][SA]); one
-// commit group.
-__device__ __forceinline__ void cp_async8z(void* smem, const void* gmem, bool valid) {
-  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  int sz = valid ? 8 : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
-}
-template <int NT, bool KMAJ>
-__device__ __forceinline__ void load_panel_async(const ModeProb& pb, const Geo& g, double* A,
-                                                 long long t, int lane) {
-  using S = SS<NT>;
-  const double* __restrict__ X = pb.X;
-  const int m0 = (int)(t * 8);
-  if (KMAJ) {
-    int w0, b0;
-    row_index<true>(g, m0, w0, b0, 1, 0);
-    int mi = w0;
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const bool rv = (long long)m0 + r < g.M;
-      const double* src = X + ((long long)pb.xld * mi + pb.xbs * b0);
-      for (int k = lane; k < g.kpad; k += 32) {
-        const bool v = rv && k < g.n;
-        cp_async8z(&A[r * S::SA + k], v ? src + k : X, v);
-      }
-      if (++mi == g.Mi) { mi = 0; ++b0; }
-    }
-  } else {
-    const int r = lane & 7;
-    const int m = m0 + r;
-    const bool rv = (long long)m < g.M;
-    int w = 0, b = 0;
-    if (rv) row_index<false>(g, m, w, b, 0, g.Pn);
-    const double* src = X + (w + pb.xbs * b);
-    for (int k = lane >> 3; k < g.kpad; k += 4) {
-      const bool v = rv && k < g.n;
-      cp_async8z(&A[r * S::SA + k], v ? src + (long long)g.P * k : X, v);
-    }
-  }
-  commit();
-}
 
 // One 8-row tile: panel load (LDG -> STS, zero fill beyond n / M), DMMAs, epilogue.
 // COHERENT: the input was written earlier in the same launch (plane pipeline): L2-coherent loads.
@@ -775,186 +722,9 @@ __global__ void __launch_bounds__(STH, 1) mode_small_kernel(const __grid_constan
     do_tile<NT, KMAJ, false, SC, FOLD>(pb, g, Ws, A, t, lane, (trace && lane == 0 && t == gw) ? trace : nullptr);
 }
 
-// Folded transforms with 16-row warp tiles: two 8-row DMMA tiles share every B fragment (half the
-// shared-memory B loads per DMMA, two independent accumulator chains); 8 warps per CTA so the
-// panels fit the same shared memory as 16 warps of 8-row panels.
-constexpr int SW2 = 8;
-template <int NT, bool KMAJ>
-__global__ void __launch_bounds__(SW2 * 32, 1)
-mode_small_fold2_kernel(const __grid_constant__ ModeGroupT<kSmallGroup> grp) {
-  using S = SS<NT>;
-  extern __shared__ __align__(16) double sm[];
-  double* Ws = sm;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double* A = sm + S::W_ELEMS + warp * 2 * S::ABUF;  // this warp's 16-row panel ([16][SA])
-  int pi = 0;
-#pragma unroll
-  for (int i = 1; i < kSmallGroup; ++i)
-    if (i < grp.count && (int)blockIdx.x >= grp.prob[i].cta_begin) pi = i;
-  const ModeProb& pb = grp.prob[pi];
-  const Geo g(pb);
-  load_w_fold<NT, SW2 * 32>(Ws, pb, tid);  // independent of the previous kernel
-  for (int i = lane; i < 2 * S::ABUF; i += 32) A[i] = 0.0;  // panel pad columns read as zeros
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-  wait_group<0>();
-  __syncthreads();
-  const int gw = (blockIdx.x - pb.cta_begin) + pb.ctas * warp;
-  const int nw = pb.ctas * SW2;
-  const long long tiles16 = (pb.tiles_m + 1) / 2;
-  for (long long u = gw; u < tiles16; u += nw) {
-    load_tile_rows<NT, KMAJ, false>(pb, g, A, 2 * u, lane);
-    load_tile_rows<NT, KMAJ, false>(pb, g, A + 8 * S::SA, 2 * u + 1, lane);  // zero past M
-    __syncwarp();
-    tile_compute_store_fold<NT, KMAJ, 2>(pb, g, Ws, A, u, lane, nullptr);
-  }
-}
-
-// Prefetching variant: SWP = 8 warps per CTA, two panels per warp; the next tile's panel streams
-// in (cp.async) while the current tile's DMMAs and epilogue run.
-constexpr int SWP = 8;
-template <int NT>
-constexpr size_t bytes_prefetch() { return sizeof(double) * (SS<NT>::W_ELEMS + SWP * 2 * SS<NT>::ABUF); }
-
-template <int NT, bool KMAJ, int G>
-__global__ void __launch_bounds__(SWP * 32, 1)
-mode_small_pf_kernel(const __grid_constant__ ModeGroupT<G> grp) {
-  using S = SS<NT>;
-  extern __shared__ __align__(16) double sm[];
-  double* Ws = sm;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double* A0 = sm + S::W_ELEMS + warp * 2 * S::ABUF;
-
-  int pi = 0;
-#pragma unroll
-  for (int i = 1; i < G; ++i)
-    if (i < grp.count && (int)blockIdx.x >= grp.prob[i].cta_begin) pi = i;
-  const ModeProb& pb = grp.prob[pi];
-  const Geo g(pb);
-  unsigned long long* trace = grp.trace ? grp.trace + ((size_t)blockIdx.x * SW + warp) * kTracePhases : nullptr;
-  if (trace && lane == 0) trace[0] = gtimer();
-  {  // W: all threads, own group
-    const int kpad = g.kpad;
-    const int rows = (pb.epi == EPI_FUSED && S::BN > kpad) ? S::BN : kpad;
-    const int chunks = rows * (S::BN / 2);
-    for (int c = tid; c < chunks; c += SWP * 32) {
-      const int r = c / (S::BN / 2), cc = (c % (S::BN / 2)) * 2;
-      cp_async16g(&Ws[r * S::SB + cc], pb.W + (size_t)r * pb.ldw + cc);
-    }
-    commit();
-  }
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-  if (trace && lane == 0) trace[1] = gtimer();
-
-  const int gw = (blockIdx.x - pb.cta_begin) + pb.ctas * warp;
-  const int nw = pb.ctas * SWP;
-  long long t = gw;
-  if (t < pb.tiles_m) load_panel_async<NT, KMAJ>(pb, g, A0, t, lane);
-  wait_group<0>();  // W and the first panel
-  __syncthreads();
-  if (trace && lane == 0) trace[2] = gtimer();
-  int buf = 0;
-  for (; t < pb.tiles_m; t += nw) {
-    double* A = A0 + buf * S::ABUF;
-    const long long tn = t + nw;
-    if (tn < pb.tiles_m) {
-      load_panel_async<NT, KMAJ>(pb, g, A0 + (buf ^ 1) * S::ABUF, tn, lane);
-      wait_group<1>();
-    } else {
-      wait_group<0>();
-    }
-    __syncwarp();
-    unsigned long long* tr = (trace && lane == 0 && t == gw) ? trace : nullptr;
-    if (tr) tr[3] = gtimer();
-    tile_compute_store<NT, KMAJ>(pb, g, Ws, A, t, lane, tr);
-    buf ^= 1;
-  }
-}
-
-// ------------------------------------------------------------------------------------------------
-// plane pipeline: phase 1 = grp1 (mode a), phase 2 = grp2 (mode b) of the same problems, D = 3.
-// ------------------------------------------------------------------------------------------------
-template <int NT, bool KMAJ1, bool KMAJ2>
-__global__ void __launch_bounds__(STH, 1)
-mode_pp_kernel(const __grid_constant__ ModeGroupT<kSmallGroup> grp1,
-               const __grid_constant__ ModeGroupT<kSmallGroup> grp2,
-               const __grid_constant__ PlaneSync ps) {
-  using S = SS<NT>;
-  extern __shared__ __align__(16) double sm[];
-  double* W1 = sm;
-  double* W2 = sm + S::W_ELEMS;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double* A = sm + 2 * S::W_ELEMS + warp * S::ABUF;
-
-  int pi = 0;
-#pragma unroll
-  for (int i = 1; i < kSmallGroup; ++i)
-    if (i < grp1.count && (int)blockIdx.x >= grp1.prob[i].cta_begin) pi = i;
-  const ModeProb& p1 = grp1.prob[pi];
-  const ModeProb& p2 = grp2.prob[pi];
-  const Geo g1(p1), g2(p2);
-  int* cnt = ps.cnt + ps.cnt_off[pi];
-  const int rpp1 = ps.rows_per_plane1[pi], rpp2 = ps.rows_per_plane2[pi];
-
-  load_w<NT>(W1, p1, tid);
-  load_w<NT>(W2, p2, tid);
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-  wait_group<0>();
-  __syncthreads();
-
-  const int gw = (blockIdx.x - p1.cta_begin) + p1.ctas * warp;
-  const int nw = p1.ctas * SW;
-  // phase 1: never waits, so every phase-1 tile completes (no deadlock whatever the schedule)
-  for (long long t = gw; t < p1.tiles_m; t += nw) {
-    do_tile<NT, KMAJ1, false>(p1, g1, W1, A, t, lane, nullptr);
-    // publish: rows of this tile per plane (a tile spans at most two planes since rpp1 >= 8
-    // is not required: loop over the rows' planes)
-    __threadfence();
-    __syncwarp();
-    if (lane == 0) {
-      const long long r0 = t * 8, r1 = min(g1.M, r0 + 8);
-      long long r = r0;
-      while (r < r1) {
-        const long long plane = r / rpp1;
-        const long long end = min(r1, (plane + 1) * rpp1);
-        atomicAdd(&cnt[plane], (int)(end - r));
-        r = end;
-      }
-    }
-  }
-  // phase 2: wait for the planes this tile reads, then consume with L2-coherent loads
-  for (long long t = gw; t < p2.tiles_m; t += nw) {
-    if (lane == 0) {
-      const long long r0 = t * 8, r1 = min(g2.M, r0 + 8);
-      const long long pa = r0 / rpp2, pb_ = (r1 - 1) / rpp2;
-      for (long long pl = pa; pl <= pb_; ++pl)
-        while (ld_acquire(&cnt[pl]) < rpp1) __nanosleep(64);
-    }
-    __syncwarp();
-    do_tile<NT, KMAJ2, true>(p2, g2, W2, A, t, lane, nullptr);
-  }
-
-  // self-reset: the last CTA to finish zeroes the counters for the next application
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    const int done = atomicAdd(ps.done, 1);
-    if (done == gridDim.x - 1) {
-      for (int i = 0; i < ps.cnt_total; ++i) ps.cnt[i] = 0;
-      __threadfence();
-      *ps.done = 0;
-    }
-  }
-}
-
 template <int NT, bool KMAJ>
 cudaError_t launch_s(const ModeGroup* g, cudaStream_t s) {
   using S = SS<NT>;
-  // 16 single-buffered warps beat 8 double-buffered ones at these sizes (measured, r01), so the
-  // prefetching variant is opt-in (FDP_SMALL_PF=1)
-  const bool pf = bytes_prefetch<NT>() <= 227 * 1024 && std::getenv("FDP_SMALL_PF") != nullptr;
   if (!g) {
     cudaError_t e = cudaFuncSetAttribute(mode_small_kernel<NT, KMAJ, kSmallGroup>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES);
@@ -968,18 +738,13 @@ cudaError_t launch_s(const ModeGroup* g, cudaStream_t s) {
       if (e == cudaSuccess)
         e = cudaFuncSetAttribute(mode_small_kernel<NT, KMAJ, kSmallGroup, false, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES);
-      if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(mode_small_fold2_kernel<NT, KMAJ>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES);
     }
-    if (e != cudaSuccess || bytes_prefetch<NT>() > 227 * 1024) return e;
-    return cudaFuncSetAttribute(mode_small_pf_kernel<NT, KMAJ, kSmallGroup>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes_prefetch<NT>());
+    return e;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(g->total_ctas);
-  cfg.blockDim = dim3(pf ? SWP * 32 : STH);
-  cfg.dynamicSmemBytes = pf ? bytes_prefetch<NT>() : S::BYTES;
+  cfg.blockDim = dim3(STH);
+  cfg.dynamicSmemBytes = S::BYTES;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -990,18 +755,7 @@ cudaError_t launch_s(const ModeGroup* g, cudaStream_t s) {
   for (int i = 0; i < g->count; ++i) sc = sc || g->prob[i].peers != nullptr;
   if (g->prob[0].fold != FOLD_NONE) {  // even-odd folded group (host-checked: all problems)
     if (sc || NT % 2 || g->count > kSmallGroup) return cudaErrorInvalidValue;
-    cfg.blockDim = dim3(STH);
-    cfg.dynamicSmemBytes = S::BYTES;
-    // 16-row warp tiles are opt-in (FDP_SMALL_MT=2): with about one 8-row tile per warp at batch
-    // 1 they halve the busy warps and measured slower (config 2 54.8 vs 49.4 us, config 1 16.6
-    // vs 12.5 us), unlike in the plane kernel
-    const char* mt = std::getenv("FDP_SMALL_MT");
-    const bool mt2 = mt && mt[0] == '2' && g->trace == nullptr;
     if constexpr (NT % 2 == 0) {
-      if (mt2) {
-        cfg.blockDim = dim3(SW2 * 32);
-        return cudaLaunchKernelEx(&cfg, mode_small_fold2_kernel<NT, KMAJ>, narrow_group<kSmallGroup>(*g));
-      }
       return cudaLaunchKernelEx(&cfg, mode_small_kernel<NT, KMAJ, kSmallGroup, false, true>,
                                 narrow_group<kSmallGroup>(*g));
     }
@@ -1009,40 +763,14 @@ cudaError_t launch_s(const ModeGroup* g, cudaStream_t s) {
   }
   if (sc) {  // peer-store problems (slab exchange): non-KMAJ, single-buffered kernel
     if (KMAJ || g->count > kSmallGroup) return cudaErrorInvalidValue;
-    cfg.blockDim = dim3(STH);
-    cfg.dynamicSmemBytes = S::BYTES;
     return cudaLaunchKernelEx(&cfg, mode_small_kernel<NT, false, kSmallGroup, true>,
                               narrow_group<kSmallGroup>(*g));
   }
   if (g->count <= kSmallGroup) {
-    const ModeGroupT<kSmallGroup> gs = narrow_group<kSmallGroup>(*g);
-    if (pf) return cudaLaunchKernelEx(&cfg, mode_small_pf_kernel<NT, KMAJ, kSmallGroup>, gs);
-    return cudaLaunchKernelEx(&cfg, mode_small_kernel<NT, KMAJ, kSmallGroup>, gs);
+    return cudaLaunchKernelEx(&cfg, mode_small_kernel<NT, KMAJ, kSmallGroup>,
+                              narrow_group<kSmallGroup>(*g));
   }
-  cfg.blockDim = dim3(STH);
-  cfg.dynamicSmemBytes = S::BYTES;
   return cudaLaunchKernelEx(&cfg, mode_small_kernel<NT, KMAJ, kMaxGroup>, *g);
-}
-
-template <int NT, bool K1, bool K2>
-cudaError_t launch_pp(const ModeGroup* g1, const ModeGroup* g2, const PlaneSync* ps, cudaStream_t s) {
-  using S = SS<NT>;
-  if (!g1)
-    return cudaFuncSetAttribute(mode_pp_kernel<NT, K1, K2>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES_PP);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(g1->total_ctas);
-  cfg.blockDim = dim3(STH);
-  cfg.dynamicSmemBytes = S::BYTES_PP;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (g1->count > kSmallGroup) return cudaErrorInvalidValue;
-  return cudaLaunchKernelEx(&cfg, mode_pp_kernel<NT, K1, K2>, narrow_group<kSmallGroup>(*g1),
-                            narrow_group<kSmallGroup>(*g2), *ps);
 }
 
 template <bool KMAJ>
@@ -1064,24 +792,6 @@ cudaError_t dispatch_small(const ModeGroup* g, int NT, cudaStream_t s) {
   }
 }
 
-template <bool K1, bool K2>
-cudaError_t dispatch_pp(const ModeGroup* g1, const ModeGroup* g2, const PlaneSync* ps, int NT,
-                        cudaStream_t s) {
-  switch (NT) {
-    case 1: return launch_pp<1, K1, K2>(g1, g2, ps, s);
-    case 2: return launch_pp<2, K1, K2>(g1, g2, ps, s);
-    case 3: return launch_pp<3, K1, K2>(g1, g2, ps, s);
-    case 4: return launch_pp<4, K1, K2>(g1, g2, ps, s);
-    case 5: return launch_pp<5, K1, K2>(g1, g2, ps, s);
-    case 6: return launch_pp<6, K1, K2>(g1, g2, ps, s);
-    case 7: return launch_pp<7, K1, K2>(g1, g2, ps, s);
-    case 8: return launch_pp<8, K1, K2>(g1, g2, ps, s);
-    case 9: return launch_pp<9, K1, K2>(g1, g2, ps, s);
-    case 10: return launch_pp<10, K1, K2>(g1, g2, ps, s);
-    default: return cudaErrorInvalidValue;
-  }
-}
-
 }  // namespace
 
 cudaError_t launch_mode_small(const ModeGroup& g, int NT, bool kmaj, cudaStream_t s) {
@@ -1089,21 +799,10 @@ cudaError_t launch_mode_small(const ModeGroup& g, int NT, bool kmaj, cudaStream_
   return kmaj ? dispatch_small<true>(&g, NT, s) : dispatch_small<false>(&g, NT, s);
 }
 
-cudaError_t launch_mode_pp(const ModeGroup& g1, const ModeGroup& g2, const PlaneSync& ps, int NT,
-                           bool kmaj1, cudaStream_t s) {
-  if (g1.total_ctas <= 0) return cudaSuccess;
-  return kmaj1 ? dispatch_pp<true, false>(&g1, &g2, &ps, NT, s)
-               : dispatch_pp<false, true>(&g1, &g2, &ps, NT, s);
-}
-
 cudaError_t prepare_mode_small(int NT) {
   cudaError_t e;
   if ((e = dispatch_small<true>(nullptr, NT, 0)) != cudaSuccess) return e;
   if ((e = dispatch_small<false>(nullptr, NT, 0)) != cudaSuccess) return e;
-  if (NT <= kPPMaxNT) {
-    if ((e = dispatch_pp<true, false>(nullptr, nullptr, nullptr, NT, 0)) != cudaSuccess) return e;
-    if ((e = dispatch_pp<false, true>(nullptr, nullptr, nullptr, NT, 0)) != cudaSuccess) return e;
-  }
   return cudaSuccess;
 }
 

@@ -184,7 +184,7 @@ __device__ __forceinline__ void kloop(double (&acc)[kMT][9][2], int nt, int kst,
       const long long w1 = clock64();
       atomicAdd(&g_k1t_prof[pslot][0], (unsigned long long)(w1 - w0));
       atomicAdd(&g_k1t_wwait[pslot][threadIdx.x >> 5], (unsigned long long)(w1 - w0));
-      if (s == 0) atomicAdd(&g_k1t_prof2[pslot][0], (unsigned long long)(w1 - w0));
+
       if (threadIdx.x == 0) {
         atomicAdd(&g_k1t_prof2[pslot][1], (unsigned long long)(w0 - t_issue[stage]));
         atomicAdd(&g_k1t_prof2[pslot][2], (unsigned long long)(w1 - t_issue[stage]));
@@ -334,7 +334,13 @@ __global__ void __launch_bounds__(kThreads, kTmaCtasPerSM) mode_tma_kernel(const
     // every warp finishes the stage together (measured faster than letting warps run ahead
     // through the ring: the sub-partition arbiter favours high warp ids, the leaders then stall
     // on refills gated by the slowest warp while the laggards run alone)
+#ifdef FDP_K1T_PROF
+    const long long b0 = clock64();
     named_bar(15, kThreads);
+    if (lane == 0) atomicAdd(&g_k1t_prof2[0][0], (unsigned long long)(clock64() - b0));
+#else
+    named_bar(15, kThreads);
+#endif
     if (threadIdx.x == 0) {
       {
 #else

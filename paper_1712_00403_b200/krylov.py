@@ -257,6 +257,23 @@ def nu_scalings_paper(gd, op: "StokesOperator", nu, q: int, device: int = 0):
 _DEV_MINRES = {}
 
 
+def _fid(f):
+    """Cache-key part of a callable: bound methods are new objects on every attribute access, so
+    key them by (instance, function)."""
+    return (id(getattr(f, "__self__", f)), getattr(getattr(f, "__func__", f), "__qualname__", ""))
+
+
+def _refs(*fs):
+    """Strong references to the callables' owners (and functions), kept in a cached graph's entry:
+    while an entry lives its owners cannot be collected, so their ids cannot be reused."""
+    return tuple((getattr(f, "__self__", f), getattr(f, "__func__", f)) for f in fs)
+
+
+def _same_callables(ent, *fs):
+    return all(o is getattr(f, "__self__", f) and fn is getattr(f, "__func__", f)
+               for (o, fn), f in zip(ent["refs"], fs))
+
+
 def minres_device(apply_A, apply_P, b, tol: float = 1e-8, maxit: int = 20000, unroll: int = 6):
     """MINRES with the scalar recurrence on the GPU (fdp_minres_scalars): `unroll` whole
     iterations (operator, preconditioner, dots, recurrence, vector updates) are captured into one
@@ -271,15 +288,17 @@ def minres_device(apply_A, apply_P, b, tol: float = 1e-8, maxit: int = 20000, un
     n = b.numel()
     dev = b.device
     # bound methods are new objects on every attribute access: key them by (instance, function)
-    fid = lambda f: (id(getattr(f, "__self__", f)), getattr(getattr(f, "__func__", f), "__qualname__", ""))
-    key = (n, str(dev), unroll, fid(apply_A), fid(apply_P))
+    key = (n, str(dev), unroll, _fid(apply_A), _fid(apply_P))
     ent = _DEV_MINRES.get(key)
+    if ent is not None and not _same_callables(ent, apply_A, apply_P):
+        ent = None  # an id reused by a new object: the cached graph belongs to the old one
     if ent is None:
         _DEV_MINRES.clear()
         vecs = [torch.zeros(n, dtype=torch.float64, device=dev) for _ in range(8)]
         state = torch.zeros(32, dtype=torch.float64, device=dev)
         hist = torch.zeros(maxit + 1, dtype=torch.float64, device=dev)
-        ent = {"vecs": vecs, "state": state, "hist": hist, "graph": None}
+        ent = {"vecs": vecs, "state": state, "hist": hist, "graph": None,
+               "refs": _refs(apply_A, apply_P)}
         _DEV_MINRES[key] = ent
     x, r1, r2, y, v, w, w1, w2 = ent["vecs"]
     state, hist = ent["state"], ent["hist"]
@@ -439,9 +458,10 @@ def gmres_device(apply_A, apply_P, b, tol: float = 1e-8, maxit: int = 500, unrol
     n = b.numel()
     dev = b.device
     m = min(maxit, n)
-    fid = lambda f: (id(getattr(f, "__self__", f)), getattr(getattr(f, "__func__", f), "__qualname__", ""))
-    key = (n, m, str(dev), unroll, fid(apply_A), fid(apply_P))
+    key = (n, m, str(dev), unroll, _fid(apply_A), _fid(apply_P))
     ent = _DEV_GMRES.get(key)
+    if ent is not None and not _same_callables(ent, apply_A, apply_P):
+        ent = None
     st = lambda: torch.cuda.current_stream().cuda_stream
     if ent is None:
         _DEV_GMRES.clear()
@@ -454,6 +474,7 @@ def gmres_device(apply_A, apply_P, b, tol: float = 1e-8, maxit: int = 500, unrol
             "is": torch.zeros(5, dtype=torch.int32, device=dev),
             "scr": torch.empty(max(1, int(lib.fdp_vec_multidot_workspace_bytes(m + 1)) // 8), **f64),
             "graph": None,
+            "refs": _refs(apply_A, apply_P),
         }
         _DEV_GMRES[key] = ent
     V, vin, t, w = ent["V"], ent["vin"], ent["t"], ent["w"]

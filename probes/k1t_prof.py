@@ -30,7 +30,7 @@ for i in range(8):
     if tiles == 0:
         continue
     w0, slack, ready, cnt = list(buf)[32 + 4 * i:32 + 4 * i + 4]
-    print(json.dumps({"cfg": cid, "kind": names[i], "wait_at_stage0_frac": round(w0 / max(wait, 1), 3),
+    print(json.dumps({"cfg": cid, "kind": names[i],
                       "issue_to_need_cyc": round(slack / max(cnt, 1)), "issue_to_ready_cyc": round(ready / max(cnt, 1)),
                       "warp_tiles": tiles, "wait_frac_of_kloop": round(wait / kl, 3),
                       "epi_frac": round(epi / (kl + epi), 3), "kloop_cyc": round(kl / tiles), "epi_cyc": round(epi / tiles)}))
@@ -39,3 +39,5 @@ b = list(buf)
 for i in (0, 4):
     ww = b[64 + 32 * i:64 + 32 * i + 16]
     print(names[i], "per-warp wait (M cycles):", [round(x / 1e6) for x in ww])
+print("named-barrier cycles (all kinds) as a fraction of all K-loop cycles:",
+      round(b[32] / max(1, sum(b[4 * i + 1] for i in range(8))), 3))

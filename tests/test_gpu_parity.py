@@ -277,7 +277,7 @@ def test_config5_full_size_oracle_parity():
 
 
 @pytest.mark.parametrize("env", [{"FDP_NO_SMALL": "1"}, {"FDP_NO_FUSE": "1"}, {"FDP_PRESSURE": "banded"},
-                                 {"FDP_PRESSURE": "dense"}, {"FDP_PP": "1"}, {"FDP_SMALL_PF": "1"},
+                                 {"FDP_PRESSURE": "dense"},
                                  {"FDP_NO_FOLD": "1"}, {"FDP_NO_PLANE": "1"}, {}])
 @pytest.mark.parametrize("cfg_id", [1, 2, 3])
 def test_block_precond_kernel_paths(cfg_id, env, monkeypatch):
@@ -318,9 +318,9 @@ def test_fd_apply_small_path_edges(dims):
         assert rel(x[i], ref.apply(b[i])) < TOL
 
 
-def test_plane_pipeline_repeated_applies_and_batch_growth(monkeypatch):
-    """Self-resetting plane counters: many applies in a row, then a larger batch (re-allocation)."""
-    monkeypatch.setenv("FDP_PP", "1")
+def test_repeated_applies_and_batch_growth():
+    """Many applies in a row on the same handle (graph replays), then a larger batch (a new
+    captured graph and workspace)."""
     w, od, gd = _both(2)
     P = fdp.build_block(gd)
     ref = oprec.BlockPrecond(od)
@@ -610,3 +610,18 @@ def test_k1t_folded_transforms(dims, coef, batch, dscale):
         r = ofd.scaled_apply(ref, b[i], dsc) if dscale else ref.apply(b[i])
         assert rel(x[i], r) < TOL and relmax(x[i], r) < TOL
         assert rel(x[i], x_f[i]) < 1e-12
+
+
+def test_kron_mass_slab_workspace_covers_both_phases():
+    """kron_mass_slab_workspace_bytes covers phase 0's z-slab and phase 1's y-slab (ADVICE r01:
+    n2 != n3 with an uneven split, e.g. n2 = 11, n3 = 10, G = 2)."""
+    rng = np.random.default_rng(3)
+    dims = (4, 11, 10)
+    Ms = [_rand_spd(n, rng, 2.0) for n in dims]
+    Mb = fdp.KronMass(Ms)
+    for G in (1, 2, 3):
+        for rk in range(G):
+            nb = int(fdp.lib.kron_mass_slab_workspace_bytes(Mb.h, G, rk))
+            z = [10 // G + (1 if i < 10 % G else 0) for i in range(G)][rk]
+            y = [11 // G + (1 if i < 11 % G else 0) for i in range(G)][rk]
+            assert nb >= 8 * max(4 * 11 * z, 4 * y * 10), (G, rk, nb)
