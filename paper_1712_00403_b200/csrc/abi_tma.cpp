@@ -180,15 +180,22 @@ cudaError_t launch_tma_stage(const ModeProb* probs, int count, bool kmaj, cudaSt
               promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     }
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    if (m.epi == EPI_LAMBDA) {  // Lambda factors staged in shared memory: lam0 (n1), lam1 (P / n1), lamcol (n)
+      t.lam_off = g.lam_elems;
+      t.lam1_n = m.lam1 ? m.P / m.n1 : 0;
+      g.lam_elems += m.n1 + t.lam1_n + m.n;
+    }
     t.tile_begin = tiles;
     tiles += t.ctiles * t.tiles_p * t.tiles_q * m.batch;
   }
+  if (g.lam_elems > 4800) return cudaErrorInvalidValue;  // kLamMax of mode_tma.cu
   g.total_tiles = tiles;
   g.ct_uniform = g.prob[0].ctiles;
   for (int i = 1; i < count; ++i)
     if (g.prob[i].ctiles != g.ct_uniform) g.ct_uniform = 0;
   if (std::getenv("FDP_K1T_NOGROUP")) g.ct_uniform = 0;  // experiment switch
   if (const char* e = std::getenv("FDP_K1T_DBG")) g.dbg = std::atoi(e);
+  if (const char* e = std::getenv("FDP_K1T_STAGGER")) g.stagger_ns = std::atoi(e);
   int grid = std::min(tiles, kTmaCtasPerSM * num_sms());
   if (g.ct_uniform > 0) grid = std::max(g.ct_uniform, grid / g.ct_uniform * g.ct_uniform);
   ++g_k1_launches[1];

@@ -5,18 +5,22 @@
 //
 // FP64 tensor cores on sm_100a are the warp-level mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4; tcgen05
 // has no f64 kind), so accumulators live in registers. Everything around them is Blackwell-native:
-//   * one persistent CTA per SM: 8 warps (4 along M x the E / O roles; two per SM sub-partition,
-//     so each may hold up to 255 registers -- a ninth, producer-only warp would put three warps on
-//     one sub-partition and cap every thread at 168 registers);
-//   * lane 0 of warp 0 is the producer: it streams every K stage with TMA, STAGES deep ahead of
-//     the consumers and across tile boundaries: the two A tiles of a stage are
-//     cp.async.bulk.tensor loads through a tensor map with the 128-byte swizzle (SASS UTMALDG),
-//     the E and O eigenvector chunks are cp.async.bulk copies of a host-prepared fragment-native
-//     layout (UBLKCP); completion is counted in bytes on the stage's "full" mbarrier, and the
-//     consumer warps release a stage on its "empty" mbarrier -- no CTA-wide barrier in the loop;
-//   * a CTA tile is 128 rows x (up to 72 E + 72 O) folded columns: every A element fetched from
-//     L2 feeds 144 outputs (the round-1 cp.async K1f fed 88), which halves the L2 traffic per DMMA;
-//   * the loads of the next tile's first stages are in flight while the consumers run the epilogue.
+//   * one persistent CTA per SM, warp-specialised: 8 consumer warps (4 row slices x the E / O
+//     roles), 1 producer warp, 3 store warps (12 warps, <= 168 registers each);
+//   * the producer's lane 0 streams every K stage of the CTA's tile sequence through a 3-deep
+//     ring: the two A tiles of a stage are cp.async.bulk.tensor loads through a tensor map with
+//     the 128-byte swizzle (SASS UTMALDG), the E and O eigenvector chunks cp.async.bulk copies of
+//     a host-prepared fragment-native layout (UBLKCP); completion is counted in bytes on the
+//     stage's "full" mbarrier, and each consumer warp releases the slot on its "empty" mbarrier;
+//   * a CTA tile is 64 rows x (up to 72 E + 72 O) folded columns; the CTAs of a column-tile group
+//     work on the same row block at the same time (its A rows come from DRAM once);
+//   * the consumers hand each finished tile to the store warps through a shared-memory staging
+//     buffer (one mbarrier pair) and go straight on with the next tile's K loop; the store warps
+//     drain it to HBM with 16-byte stores (an in-register epilogue stalled every consumer for
+//     6-10k cycles per tile: all CTAs finish together and the store burst backs up the memory
+//     system -- 13-21% of the kernel, measured with clock64 per phase);
+//   * Lambda^{-1} (the last forward mode) is applied by the consumers in registers, with the
+//     Lambda factors staged in shared memory at kernel start.
 //
 // Folded algebra (persymmetric pencil, n = ne + no, ne = ceil(n/2)):
 //   FOLD_FWD: y_E = W_E^T s, y_O = W_O^T d, s_k = x_k + x_{n-1-k}, d_k = x_k - x_{n-1-k}:
@@ -32,7 +36,7 @@
 // k order inside a stage (all operands use the same order, so the sum is unchanged):
 //   non-KMAJ A ([k][p], p contiguous): the k4 step j covers k = 8(j>>1) + (j&1) + {0,2,4,6};
 //   KMAJ A     ([row][k], k contiguous): k = 4j + {0..3}, and DMMA tile t of a warp takes the
-//              rows 16(t>>1) + 2r + (t&1) (r = 0..7) of its 32-row slice;
+//              rows 2r + t (r = 0..7) of its 16-row slice;
 // the W chunks are laid out per (k4 step, n8 pair, lane) in that same k order.
 #include <cuda.h>
 
@@ -42,28 +46,25 @@
 #include "../mode_tma.h"
 
 namespace fdp {
-#ifdef FDP_K1T_PROF
-__device__ unsigned long long g_k1t_prof[8][4];
-__device__ unsigned long long g_k1t_prof2[8][4];
-__device__ unsigned long long g_k1t_wwait[8][32];  // per-warp wait cycles  // wait at stage 0, issue->need slack, issue->ready, count
-__shared__ long long t_issue[8];  // [kmaj*4 + fold-1 + 2*(epi!=0)]: wait, kloop, epilogue, tiles
-#endif
 namespace {
 
-// kWM row slices of 8 kMT rows (kWM * 8 * kMT = kTmaBM) times the two roles
-#ifndef FDP_K1T_WM
-#define FDP_K1T_WM 4
-#endif
-constexpr int kWM = FDP_K1T_WM;
-constexpr int kMT = kTmaBM / (8 * kWM);
+constexpr int kWM = 4;                              // row slices (x 2 roles = 8 warps)
+constexpr int kMT = kTmaBM / (8 * kWM);             // 8-row DMMA tiles per warp (2)
 constexpr int kConsumerWarps = 2 * kWM;
-constexpr int kThreads = kConsumerWarps * 32;
-constexpr int kXR = kMT / 2;  // 8-row tiles per BWD exchange round (two rounds)
-constexpr int kABytes = kTmaBM * kTmaBK * 8;             // one A tile (8 KB)
-constexpr int kBBytes = kTmaWChunk * 8;                  // one role's W chunk (10 KB)
-constexpr int kMiniBytes = kTmaBM * 2 * 8;               // odd-start fix-up column pair (1 KB)
-constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes + kMiniBytes;  // 54 KB
-constexpr int kEpiBytes = kWM * kXR * 8 * 72 * 8;        // BWD o-exchange, half a tile (36 KB)
+constexpr int kStoreWarps = 3;
+constexpr int kThreads = (kConsumerWarps + 1 + kStoreWarps) * 32;  // + producer + store warps
+// output-tile staging buffer: non-KMAJ [col 0..143][row] with a column stride == 16 B (mod 128),
+// KMAJ [row 0..63][col] with a row stride == 32 B (mod 128): conflict-free fragment stores
+constexpr int kCLdN = 66;
+constexpr int kCLdK = 148;
+constexpr int kCBytes = (144 * kCLdN > kTmaBM * kCLdK ? 144 * kCLdN : kTmaBM * kCLdK) * 8;
+constexpr int kLamMax = 4800;
+  // doubles of staged Lambda factors (all problems of a launch)
+constexpr int kABytes = kTmaBM * kTmaBK * 8;        // one A tile (8 KB)
+constexpr int kBBytes = kTmaWChunk * 8;             // one role's W chunk (10 KB)
+constexpr int kMiniBytes = kTmaBM * 2 * 8;          // odd-start fix-up column pair (1 KB)
+constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes + kMiniBytes;  // 37 KB
+static_assert(kMT == 2, "fragment offsets below assume two 8-row tiles per warp");
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -74,6 +75,9 @@ __device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
 __device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
   asm volatile(
@@ -114,6 +118,9 @@ __device__ __forceinline__ double lds64(unsigned a) {
 }
 __device__ __forceinline__ void lds128(unsigned a, double& x, double& y) {
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a));
+}
+__device__ __forceinline__ void sts64(unsigned a, double x) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(x) : "memory");
 }
 __device__ __forceinline__ void sts128(unsigned a, double x, double y) {
   asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(x), "d"(y) : "memory");
@@ -167,86 +174,147 @@ __device__ __forceinline__ Tile decode(const TmaGroup& g, int tau, bool kmaj) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// consumer K loop of one tile: NTV = n8 tiles per role (9 or 8; 0 = any nt <= 9, masked),
-// ODD = KMAJ second A tile loaded from one column earlier (see the producer)
+// producer: issue stage s of the CTA's it-th tile into `slot` (out of line: the consumers'
+// instruction stream only holds the call)
 // ---------------------------------------------------------------------------------------------
-template <bool KMAJ, int FOLD, int STAGES, int NTV, int ODD, class Release>
-__device__ __forceinline__ void kloop(double (&acc)[kMT][9][2], int nt, int kst, int ne, unsigned sbase,
-                                      unsigned bar_full, int& stage, unsigned& phase, int wm,
-                                      int role, int fr, int fc, int lane, int it, Release& release,
-                                      int pslot = 0) {
-  const double sgn = role ? -1.0 : 1.0;  // FWD: E warps form s = x + Jx, O warps d = x - Jx
-  for (int s = 0; s < kst; ++s) {
-#ifdef FDP_K1T_PROF
-    const long long w0 = clock64();
-    mbar_wait(bar_full + 8 * stage, phase);
-    if (lane == 0) {
-      const long long w1 = clock64();
-      atomicAdd(&g_k1t_prof[pslot][0], (unsigned long long)(w1 - w0));
-      atomicAdd(&g_k1t_wwait[pslot][threadIdx.x >> 5], (unsigned long long)(w1 - w0));
+template <bool KMAJ, int FOLD>
+__device__ __noinline__ void issue_stage(const TmaGroup& g, unsigned sbase, unsigned bar_full, int slot,
+                                         int it, int s) {
+  const int tau = tile_of(g, it);
+  if (tau < 0) return;
+  const Tile t = decode(g, tau, KMAJ);
+  const TmaProb& p = g.prob[t.pi];
+  const unsigned full = bar_full + 8 * slot;
+  const unsigned dA0 = sbase + slot * kStageBytes;
+  const unsigned dA1 = dA0 + kABytes;
+  const unsigned dB = dA1 + kABytes;
+  const int k0 = s * kTmaBK;
+  const int k1 = FOLD == FOLD_FWD ? p.n - k0 - kTmaBK : p.ne + k0;
+  const CUtensorMap* map = &g.map[t.pi];
+  if (KMAJ) {
+    // a TMA box must start on a 16-byte boundary: an odd k1 (odd n forward, odd ne backward)
+    // loads the 16 columns from k1 - 1 and the last one (k1 + 15) through a 2-column box
+    mbar_expect_tx(full, 2 * kABytes + 2 * kBBytes + (p.a1odd ? kMiniBytes : 0));
+    tma_load_3d(dA0, map, full, k0, t.tq * kTmaBM, t.b);
+    tma_load_3d(dA1, map, full, k1 - p.a1odd, t.tq * kTmaBM, t.b);
+    if (p.a1odd) tma_load_3d(dB + 2 * kBBytes, &g.map2[t.pi], full, k1 + 15, t.tq * kTmaBM, t.b);
+  } else {
+    mbar_expect_tx(full, 2 * kABytes + 2 * kBBytes);
+    tma_load_5d(dA0, map, full, 0, k0, t.tp * p.bp, t.tq * p.bq, t.b);
+    tma_load_5d(dA1, map, full, 0, k1, t.tp * p.bp, t.tq * p.bq, t.b);
+  }
+  bulk_load(dB, p.Wt + (size_t)((0 * p.ctiles + t.ct) * p.kst + s) * kTmaWChunk, kBBytes, full);
+  bulk_load(dB + kBBytes, p.Wt + (size_t)((1 * p.ctiles + t.ct) * p.kst + s) * kTmaWChunk, kBBytes, full);
+}
 
-      if (threadIdx.x == 0) {
-        atomicAdd(&g_k1t_prof2[pslot][1], (unsigned long long)(w0 - t_issue[stage]));
-        atomicAdd(&g_k1t_prof2[pslot][2], (unsigned long long)(w1 - t_issue[stage]));
-        atomicAdd(&g_k1t_prof2[pslot][3], 1ULL);
+// the producer warp's loop (lane 0): every stage of the CTA's tile sequence, in order, into the
+// ring slot the consumers released (the slot's "empty" mbarrier completes when all 8 consumer
+// warps arrived on it)
+template <bool KMAJ, int FOLD, int STAGES>
+__device__ __noinline__ void producer_loop(const TmaGroup& g, unsigned sbase, unsigned bar_full,
+                                           unsigned bar_empty) {
+  for (int i = 0; i < g.count; ++i)
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(&g.map[i]))
+                 : "memory");
+  int slot = 0;
+  unsigned phase = 0;
+  for (int it = 0;; ++it) {
+    const int tau = tile_of(g, it);
+    if (tau < 0) break;
+    const int kst = g.prob[decode(g, tau, KMAJ).pi].kst;
+    for (int s = 0; s < kst; ++s) {
+      mbar_wait(bar_empty + 8 * slot, phase ^ 1);
+      issue_stage<KMAJ, FOLD>(g, sbase, bar_full, slot, it, s);
+      if (++slot == STAGES) {
+        slot = 0;
+        phase ^= 1;
       }
     }
-#else
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// one stage of the consumer K loop: J k4 steps (4, or fewer in a partial last stage),
+// NTV = n8 tiles per role (9 or 8; 0 = any nt <= 9, masked), ODD = KMAJ second A tile loaded
+// from one column earlier (see issue_stage). Fragment offsets (bytes within an A tile):
+//   off[ti][jj]: non-KMAJ: A0 and A1 rows k = 8(j>>1) + 2 fc + jj (j & 1 = jj) of 16-row group
+//                wm; KMAJ: row base + in-row part for k = 4j + fc (see kmaj_col)
+// ---------------------------------------------------------------------------------------------
+struct Frag {
+  unsigned a0[kMT][2];   // non-KMAJ: direct / E-part offsets per (tile, j & 1); KMAJ: row bases
+  unsigned a1[kMT][2];   // non-KMAJ: mirror offsets (FWD) ; KMAJ: xor term y per tile in [ti][0]
+};
+
+// KMAJ: byte of column lam in row R of a swizzled [row][16] tile
+__device__ __forceinline__ unsigned kmaj_col(unsigned rowbase, int x, int lam) {
+  return rowbase + ((((lam >> 1) ^ x) << 4) | ((lam & 1) << 3));
+}
+
+template <bool KMAJ, int FOLD, int NTV, int ODD, int J>
+__device__ __forceinline__ void stage_mma(double (&acc)[kMT][9][2], int nt, unsigned A0, unsigned A1,
+                                          unsigned B, unsigned Mini, const Frag& f, double sgn,
+                                          int role, int fr, int fc, int lane, int jmax) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (j < J && (J == 4 || j < jmax)) {
+      double a[kMT];
+#pragma unroll
+      for (int ti = 0; ti < kMT; ++ti) {
+        if (KMAJ) {
+          const unsigned rb = f.a0[ti][0];
+          const int x = (int)f.a1[ti][0];
+          const int k = 4 * j + fc;
+          const int l1 = (FOLD == FOLD_FWD ? kTmaBK - 1 - k : k) + ODD;
+          const unsigned a1 = (ODD && l1 == kTmaBK) ? Mini + f.a1[ti][1] : A1 + kmaj_col(rb, x, l1);
+          if (FOLD == FOLD_FWD) {
+            const double v = lds64(A0 + kmaj_col(rb, x, k)), w = lds64(a1);
+            a[ti] = fma(sgn, w, v);
+          } else {
+            a[ti] = lds64(role ? a1 : A0 + kmaj_col(rb, x, k));
+          }
+        } else {
+          const unsigned o0 = f.a0[ti][j & 1] + (j >> 1) * 8 * 128;
+          if (FOLD == FOLD_FWD) {
+            const unsigned o1 = f.a1[ti][j & 1] - (j >> 1) * 8 * 128;
+            const double v = lds64(A0 + o0), w = lds64(A1 + o1);
+            a[ti] = fma(sgn, w, v);
+          } else {
+            a[ti] = lds64((role ? A1 : A0) + o0);
+          }
+        }
+      }
+      double b[10];
+#pragma unroll
+      for (int tp = 0; tp < 5; ++tp) lds128(B + ((j * 5 + tp) * 32 + lane) * 16, b[2 * tp], b[2 * tp + 1]);
+#pragma unroll
+      for (int ti = 0; ti < kMT; ++ti)
+#pragma unroll
+        for (int u = 0; u < 9; ++u) {
+          if (NTV ? (u < NTV) : (u < nt)) dmma(acc[ti][u], a[ti], b[u]);
+        }
+    }
+  }
+}
+
+template <bool KMAJ, int FOLD, int STAGES, int NTV, int ODD>
+__device__ __forceinline__ void kloop(const TmaGroup& g, double (&acc)[kMT][9][2], int nt, int kst, int ne,
+                                      unsigned sbase, unsigned bar_full, unsigned bar_empty, int& stage,
+                                      unsigned& phase, const Frag& f, int role, int fr, int fc, int lane) {
+  const double sgn = role ? -1.0 : 1.0;  // FWD: E warps form s = x + Jx, O warps d = x - Jx
+  const int rem = ne - (kst - 1) * kTmaBK;  // valid k of the last stage (1 .. 16)
+  const int jlast = KMAJ ? (rem + 3) >> 2 : (rem <= 8 ? 2 : 4);
+  for (int s = 0; s < kst; ++s) {
     mbar_wait(bar_full + 8 * stage, phase);
-#endif
     const unsigned A0 = sbase + stage * kStageBytes;
     const unsigned A1 = A0 + kABytes;
     const unsigned B = A1 + kABytes + role * kBBytes;
     const unsigned Mini = A1 + kABytes + 2 * kBBytes;
-    const int rem = ne - s * kTmaBK;  // valid k of this stage (>= 1)
-    const int jmax = KMAJ ? min(4, (rem + 3) >> 2) : (rem <= 8 ? 2 : 4);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (j < jmax) {
-        double a[kMT];
-#pragma unroll
-        for (int ti = 0; ti < kMT; ++ti) {
-          if (KMAJ) {
-            const int R = 8 * kMT * wm + 16 * (ti >> 1) + 2 * fr + (ti & 1);
-            const int x = R & 7;
-            const int k = 4 * j + fc;
-            // column lam of the swizzled [row][16] tile
-            auto sw = [&](int lam) { return (unsigned)(R * 128 + ((((lam >> 1) ^ x) << 4) | ((lam & 1) << 3))); };
-            // A1 column: FWD the mirror 15 - k, BWD k; shifted by one for an odd-start tile,
-            // whose 16th column sits in the 2-column fix-up box
-            const int l1 = (FOLD == FOLD_FWD ? kTmaBK - 1 - k : k) + ODD;
-            const unsigned a1 = (ODD && l1 == kTmaBK) ? Mini + R * 16 : A1 + sw(l1);
-            if (FOLD == FOLD_FWD) {
-              const double v = lds64(A0 + sw(k)), w = lds64(a1);
-              a[ti] = fma(sgn, w, v);
-            } else {
-              a[ti] = lds64(role ? a1 : A0 + sw(k));
-            }
-          } else {
-            const int gq = kXR * wm + (ti >> 1), plo = 8 * (ti & 1) + fr;
-            const int k = 8 * (j >> 1) + 2 * fc + (j & 1), km = kTmaBK - 1 - k;
-            const unsigned off0 = (k + 16 * gq) * 128 + ((((plo >> 1) ^ (k & 7)) << 4) | ((plo & 1) << 3));
-            const unsigned off1 = (km + 16 * gq) * 128 + ((((plo >> 1) ^ (km & 7)) << 4) | ((plo & 1) << 3));
-            if (FOLD == FOLD_FWD) {
-              const double v = lds64(A0 + off0), w = lds64(A1 + off1);
-              a[ti] = fma(sgn, w, v);
-            } else {
-              a[ti] = lds64((role ? A1 : A0) + off0);
-            }
-          }
-        }
-        double b[10];
-#pragma unroll
-        for (int tp = 0; tp < 5; ++tp) lds128(B + ((j * 5 + tp) * 32 + lane) * 16, b[2 * tp], b[2 * tp + 1]);
-#pragma unroll
-        for (int ti = 0; ti < kMT; ++ti)
-#pragma unroll
-          for (int u = 0; u < 9; ++u) {
-            if (NTV ? (u < NTV) : (u < nt)) dmma(acc[ti][u], a[ti], b[u]);
-          }
-      }
-    }
-    release(stage, it, s);
+    if (s + 1 < kst || jlast == 4)
+      stage_mma<KMAJ, FOLD, NTV, ODD, 4>(acc, nt, A0, A1, B, Mini, f, sgn, role, fr, fc, lane, 4);
+    else
+      stage_mma<KMAJ, FOLD, NTV, ODD, 3>(acc, nt, A0, A1, B, Mini, f, sgn, role, fr, fc, lane, jlast);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar_empty + 8 * stage);  // this warp is done with the slot
     if (++stage == STAGES) {
       stage = 0;
       phase ^= 1;
@@ -255,140 +323,215 @@ __device__ __forceinline__ void kloop(double (&acc)[kMT][9][2], int nt, int kst,
 }
 
 // ---------------------------------------------------------------------------------------------
+// the store warp: drains each finished output tile from the shared-memory staging buffer to HBM
+// while the consumers already run the next tile's K loop (an in-register epilogue stalled every
+// consumer for 6-10k cycles per tile: all CTAs finish their tiles together and the store burst
+// backs up the memory system). Staged columns: E at 0, O at 72 (FWD) / e at 0, o at 72 (BWD).
+//   non-KMAJ: [col][row] (kCLdN), lane l owns rows 2l, 2l+1 (consecutive p: 16-byte stores);
+//   KMAJ    : [row][col] (kCLdK), lanes walk column pairs of a row.
+//   FWD: E column c -> spectral column 8 nt0 + c (< ne), O column c -> ne + 8 nt0 + c (< n);
+//        EPI_LAMBDA divides by lrow(p) + lamcol[col]; a KMAJ output row's pad column gets 0.
+//   BWD: x_c = e_c + o_c, x_{n-1-c} = e_c - o_c for c = 8 nt0 + col < ne; EPI_SCALE multiplies.
+// Rows: KMAJ row R is q = 64 tq + R; otherwise R = 16 g + p_lo of p-group g (see decode).
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ double lds_f64(unsigned a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+
+template <bool KMAJ, int FOLD>
+__device__ __noinline__ void store_loop(const TmaGroup& g, unsigned cbuf, unsigned bar_cfull,
+                                        unsigned bar_cempty, int lane, int sw) {
+  unsigned phase = 0;
+  for (int it = 0;; ++it) {
+    const int tau = tile_of(g, it);
+    if (tau < 0) break;
+    const Tile t = decode(g, tau, KMAJ);
+    const TmaProb& p = g.prob[t.pi];
+    const int nbase = p.n8h / p.ctiles, nrem = p.n8h % p.ctiles;
+    const int nt = nbase + (t.ct < nrem ? 1 : 0);
+    const int c0 = 8 * (t.ct * nbase + min(t.ct, nrem));
+    const int ncol = 8 * nt;
+    double* __restrict__ Y = p.Y;
+    const int ne = p.ne, no = p.no, n = p.n;
+    mbar_wait(bar_cfull, phase);
+    if (!KMAJ) {
+      // lane l: rows R = 2l, 2l + 1 (same p-group, consecutive p; P is even so both exist or not)
+      const long long P = p.P;
+      const int R = 2 * lane, gq = R >> 4, plo = R & 15;
+      const long long q = (long long)t.tq * p.bq + gq / p.bp;
+      const int pp = 16 * (t.tp * p.bp + gq % p.bp) + plo;
+      const bool valid = pp < p.P && q < p.Q;
+      const long long sidx = pp + P * n * q;
+      double* yrow = Y + sidx + p.ybs * t.b;
+      if (valid) {
+        for (int w = sw; w < (FOLD == FOLD_FWD ? 2 : 1) * ncol; w += kStoreWarps) {
+          if (FOLD == FOLD_FWD) {
+            {  // (half, column) pairs dealt over the store warps: h = 0 E, 1 O
+              const int h = w >= ncol, c = w - h * ncol;
+              const int a = c0 + c;
+              if (a < (h ? no : ne)) {
+                const int oc = (h ? ne : 0) + a;
+                double v0, v1;
+                lds128(cbuf + (unsigned)((72 * h + c) * kCLdN + R) * 8u, v0, v1);
+                *reinterpret_cast<double2*>(yrow + P * oc) = make_double2(v0, v1);
+              }
+            }
+          } else {
+            const int c = w, cc = c0 + c;
+            if (cc < ne) {
+              double e0, e1, o0, o1;
+              lds128(cbuf + (unsigned)(c * kCLdN + R) * 8u, e0, e1);
+              lds128(cbuf + (unsigned)((72 + c) * kCLdN + R) * 8u, o0, o1);
+              double x0 = e0 + o0, x1 = e1 + o1, y0 = e0 - o0, y1 = e1 - o1;
+              const int cm = n - 1 - cc;
+              if (p.epi == EPI_SCALE) {
+                const double2 s0 = *reinterpret_cast<const double2*>(p.scale + sidx + P * cc);
+                const double2 s1 = *reinterpret_cast<const double2*>(p.scale + sidx + P * cm);
+                x0 *= s0.x; x1 *= s0.y; y0 *= s1.x; y1 *= s1.y;
+              }
+              *reinterpret_cast<double2*>(yrow + P * cc) = make_double2(x0, x1);
+              if (cm != cc) *reinterpret_cast<double2*>(yrow + P * cm) = make_double2(y0, y1);
+            }
+          }
+        }
+      }
+    } else {
+      // (row, column) pairs flattened over the lanes of both store warps; 16-byte stores where
+      // the output column is even (E part; O part when ne is even; BWD when the row is aligned)
+      const int pairs = ncol / 2;  // column pairs per half (ncol = 8 nt)
+      const int per_row = FOLD == FOLD_FWD ? 2 * pairs : pairs;
+      for (int e = lane + 32 * sw; e < kTmaBM * per_row; e += 32 * kStoreWarps) {
+        const int R = e / per_row, w = e - R * per_row;
+        const long long q = (long long)t.tq * kTmaBM + R;
+        if (q >= p.Q) continue;
+        const long long sidx = (long long)p.yld * q;
+        double* yrow = Y + sidx + p.ybs * t.b;
+        if (FOLD == FOLD_FWD) {
+          const int h = w >= pairs, c = 2 * (w - h * pairs);
+          const int a = c0 + c, oc = (h ? ne : 0) + a;
+          const int lim = h ? no : ne;
+          double v0, v1;
+          lds128(cbuf + (unsigned)(R * kCLdK + 72 * h + c) * 8u, v0, v1);
+          if (a + 1 < lim && ((reinterpret_cast<unsigned long long>(yrow + oc) & 15) == 0)) {
+            *reinterpret_cast<double2*>(yrow + oc) = make_double2(v0, v1);
+          } else {
+#pragma unroll
+            for (int d = 0; d < 2; ++d) {
+              const double v = d ? v1 : v0;
+              if (a + d < lim) yrow[oc + d] = v;
+              else if (h && oc + d < p.yld) yrow[oc + d] = 0.0;  // the pad column of a padded row
+            }
+          }
+        } else {
+          const int c = 2 * w, cc = c0 + c;
+          double e0, e1, o0, o1;
+          lds128(cbuf + (unsigned)(R * kCLdK + c) * 8u, e0, e1);
+          lds128(cbuf + (unsigned)(R * kCLdK + 72 + c) * 8u, o0, o1);
+          double x0 = e0 + o0, x1 = e1 + o1, y0 = e0 - o0, y1 = e1 - o1;
+          const int cm = n - 1 - cc;  // y_d goes to column cm - d
+          if (p.epi == EPI_SCALE) {
+            x0 *= p.scale[sidx + cc];
+            y0 *= p.scale[sidx + cm];
+            if (cc + 1 < ne) {
+              x1 *= p.scale[sidx + cc + 1];
+              y1 *= p.scale[sidx + cm - 1];
+            }
+          }
+          if (cc + 1 < ne && (reinterpret_cast<unsigned long long>(yrow + cc) & 15) == 0)
+            *reinterpret_cast<double2*>(yrow + cc) = make_double2(x0, x1);
+          else {
+            if (cc < ne) yrow[cc] = x0;
+            if (cc + 1 < ne) yrow[cc + 1] = x1;
+          }
+          // mirrored pair (cm - 1, cm) = (y1, y0); the middle column of an odd n (cm == cc) is x
+          if (cc + 1 < ne && cm - 1 > cc + 1 && (reinterpret_cast<unsigned long long>(yrow + cm - 1) & 15) == 0)
+            *reinterpret_cast<double2*>(yrow + cm - 1) = make_double2(y1, y0);
+          else {
+            if (cc < ne && cm != cc) yrow[cm] = y0;
+            if (cc + 1 < ne && cm - 1 != cc + 1) yrow[cm - 1] = y1;
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar_cempty);  // the buffer may take the next tile
+    phase ^= 1;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------------------------
 template <bool KMAJ, int FOLD, int STAGES>
-__global__ void __launch_bounds__(kThreads, kTmaCtasPerSM) mode_tma_kernel(const __grid_constant__ TmaGroup g) {
+__global__ void __launch_bounds__(kThreads, 1) mode_tma_kernel(const __grid_constant__ TmaGroup g) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-byte alignment (shared-window address) for the 128-byte swizzle atoms
   const unsigned sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
-  const unsigned bar_full = sbase + STAGES * kStageBytes + (FOLD == FOLD_BWD ? kEpiBytes : 0);
-  const unsigned epi_base = sbase + STAGES * kStageBytes;
-
+  const unsigned cbuf = sbase + STAGES * kStageBytes;
+  const unsigned bar_full = cbuf + kCBytes;
+  const unsigned bar_empty = bar_full + 8 * STAGES;
+  const unsigned bar_cfull = bar_empty + 8 * STAGES;
+  const unsigned bar_cempty = bar_cfull + 8;
+  // Lambda factors of every problem (EPI_LAMBDA launches): [lam0 | lam1 | lamcol] per problem
+  double* lsm = reinterpret_cast<double*>(smem_raw + (bar_cempty + 64 - smem_u32(smem_raw)));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // per-slot release counters (see release), after the mbarriers
-  int* cnt = reinterpret_cast<int*>(smem_raw + (bar_full + 8 * STAGES - smem_u32(smem_raw)));
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(bar_full + 8 * s, 1);
-      cnt[s] = 0;
+      mbar_init(bar_empty + 8 * s, kConsumerWarps);
     }
+    mbar_init(bar_cfull, kConsumerWarps);
+    mbar_init(bar_cempty, kStoreWarps);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  if (warp == kConsumerWarps) {  // the producer warp
+    if (lane == 0) producer_loop<KMAJ, FOLD, STAGES>(g, sbase, bar_full, bar_empty);
+    return;
+  }
+  if (warp > kConsumerWarps) {  // the store warps
+    store_loop<KMAJ, FOLD>(g, cbuf, bar_cfull, bar_cempty, lane, warp - kConsumerWarps - 1);
+    return;
+  }
 
-  // ------------------------------ producer ------------------------------
-  // There is no producer warp: the last consumer warp to release a slot (a per-slot arrival
-  // counter in shared memory) issues that slot's refill, STAGES stages ahead in the CTA's tile
-  // sequence -- at the earliest moment the slot is free, with no thread waiting for it.
-  // issue(it, s): stage s of this CTA's it-th tile into slot `slot`.
-  auto issue = [&](int slot, int it, int s) {
-    const int tau = tile_of(g, it);
-    if (tau < 0) return;
-#ifdef FDP_K1T_PROF
-    t_issue[slot] = clock64();
-#endif
-    const Tile t = decode(g, tau, KMAJ);
-    const TmaProb& p = g.prob[t.pi];
-    const unsigned full = bar_full + 8 * slot;
-    const unsigned dA0 = sbase + slot * kStageBytes;
-    const unsigned dA1 = dA0 + kABytes;
-    const unsigned dB = dA1 + kABytes;
-    const int k0 = s * kTmaBK;
-    const int k1 = FOLD == FOLD_FWD ? p.n - k0 - kTmaBK : p.ne + k0;
-    const CUtensorMap* map = &g.map[t.pi];
+  const int wm = warp % kWM, role = warp / kWM;  // role 0: E, 1: O
+  const int fr = lane >> 2, fc = lane & 3;
+  if (FOLD == FOLD_FWD && g.lam_elems > 0) {  // stage the Lambda factors (consumers only)
+    for (int pi = 0; pi < g.count; ++pi) {
+      const TmaProb& q = g.prob[pi];
+      if (q.epi != EPI_LAMBDA) continue;
+      double* d = lsm + q.lam_off;
+      for (int i = threadIdx.x; i < q.n1v; i += kConsumerWarps * 32) d[i] = q.lam0[i];  // i1 < n1v only
+      if (q.lam1)
+        for (int i = threadIdx.x; i < q.lam1_n; i += kConsumerWarps * 32) d[q.n1 + i] = q.lam1[i];
+      for (int i = threadIdx.x; i < q.n; i += kConsumerWarps * 32) d[q.n1 + q.lam1_n + i] = q.lamcol[i];
+    }
+    named_bar(14, kConsumerWarps * 32);
+  }
+  int stage = 0;
+  unsigned phase = 0, cphase = 0;
+  // per-thread fragment offsets (see Frag)
+  Frag f;
+#pragma unroll
+  for (int ti = 0; ti < kMT; ++ti) {
     if (KMAJ) {
-      // a TMA box must start on a 16-byte boundary: an odd k1 (odd n forward, odd ne backward)
-      // loads the 16 columns from k1 - 1 and the last one (k1 + 15) through a 2-column box
-      mbar_expect_tx(full, 2 * kABytes + 2 * kBBytes + (p.a1odd ? kMiniBytes : 0));
-      tma_load_3d(dA0, map, full, k0, t.tq * kTmaBM, t.b);
-      tma_load_3d(dA1, map, full, k1 - p.a1odd, t.tq * kTmaBM, t.b);
-      if (p.a1odd) tma_load_3d(dB + 2 * kBBytes, &g.map2[t.pi], full, k1 + 15, t.tq * kTmaBM, t.b);
+      const int R = 16 * wm + 2 * fr + ti;       // rows 2r + t of the 16-row slice
+      f.a0[ti][0] = f.a0[ti][1] = (unsigned)(R * 128);
+      f.a1[ti][0] = (unsigned)(R & 7);
+      f.a1[ti][1] = (unsigned)(R * 16);          // fix-up box row (2 doubles per row)
     } else {
-      mbar_expect_tx(full, 2 * kABytes + 2 * kBBytes);
-#ifdef FDP_K1T_PROF
-      if (g.dbg & 2) {  // timing experiment: A tiles of row tile 0 only (wrong results)
-        tma_load_5d(dA0, map, full, 0, k0, 0, 0, 0);
-        tma_load_5d(dA1, map, full, 0, k1, 0, 0, 0);
-      } else
-#endif
-      {
-      tma_load_5d(dA0, map, full, 0, k0, t.tp * p.bp, t.tq * p.bq, t.b);
-      tma_load_5d(dA1, map, full, 0, k1, t.tp * p.bp, t.tq * p.bq, t.b);
-      }
-    }
-    const double* wE = p.Wt + (size_t)((0 * p.ctiles + t.ct) * p.kst + s) * kTmaWChunk;
-    const double* wO = p.Wt + (size_t)((1 * p.ctiles + t.ct) * p.kst + s) * kTmaWChunk;
-#ifdef FDP_K1T_PROF
-    if (g.dbg & 1) {  // timing experiment: W chunks of stage 0 only (wrong results)
-      wE = p.Wt;
-      wO = p.Wt + kTmaWChunk;
-    }
-#endif
-    bulk_load(dB, wE, kBBytes, full);
-    bulk_load(dB + kBBytes, wO, kBBytes, full);
-  };
-  // release(slot, it, s): this warp is done with stage s of tile `it` (held in `slot`)
-  auto release = [&](int slot, int it, int s) {
-#ifndef FDP_K1T_ASYNC
-    // every warp finishes the stage together (measured faster than letting warps run ahead
-    // through the ring: the sub-partition arbiter favours high warp ids, the leaders then stall
-    // on refills gated by the slowest warp while the laggards run alone)
-#ifdef FDP_K1T_PROF
-    const long long b0 = clock64();
-    named_bar(15, kThreads);
-    if (lane == 0) atomicAdd(&g_k1t_prof2[0][0], (unsigned long long)(clock64() - b0));
-#else
-    named_bar(15, kThreads);
-#endif
-    if (threadIdx.x == 0) {
-      {
-#else
-    __syncwarp();
-    if (lane == 0) {
-      if (atomicAdd(&cnt[slot], 1) == kConsumerWarps - 1) {
-#endif
-        cnt[slot] = 0;
-        // advance STAGES stages through the tile sequence
-        int it2 = it, s2 = s + STAGES;
-        for (int tau = tile_of(g, it2); tau >= 0; tau = tile_of(g, it2)) {
-          const int kst = g.prob[decode(g, tau, KMAJ).pi].kst;
-          if (s2 < kst) break;
-          s2 -= kst;
-          ++it2;
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // reads before TMA writes
-        issue(slot, it2, s2);
-      }
-    }
-  };
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < g.count; ++i)
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(&g.map[i]))
-                   : "memory");
-    // prologue: the first STAGES stages
-    int it = 0, s = 0;
-    for (int i = 0; i < STAGES; ++i) {
-      const int tau = tile_of(g, it);
-      if (tau < 0) break;
-      issue(i, it, s);
-      if (++s == g.prob[decode(g, tau, KMAJ).pi].kst) {
-        s = 0;
-        ++it;
+      const int plo = 8 * ti + fr;               // 16-row group wm, rows p_lo
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj) {
+        const int k = 2 * fc + jj, km = kTmaBK - 1 - k;   // j < 2 rows; j >= 2 add / sub 8 rows
+        f.a0[ti][jj] = (unsigned)((k + 16 * wm) * 128 + ((((plo >> 1) ^ (k & 7)) << 4) | ((plo & 1) << 3)));
+        f.a1[ti][jj] = (unsigned)((km + 16 * wm) * 128 + ((((plo >> 1) ^ (km & 7)) << 4) | ((plo & 1) << 3)));
       }
     }
   }
 
-  // ------------------------------ consumers ------------------------------
-  const int wm = warp % kWM, role = warp / kWM;  // role 0: E, 1: O
-  const int fr = lane >> 2, fc = lane & 3;
-  int stage = 0;
-  unsigned phase = 0;
-
-  // per-thread fragment offsets within an A tile (bytes, before the j-dependent part)
-  //   non-KMAJ: rows of DMMA tile t are p_lo = 8(t&1) + fr of the 16-row group g = 2 wm + (t>>1);
-  //             byte = (k + 16 g) * 128 + swz(p_lo, k)
-  //   KMAJ:     rows R = 32 wm + 16 (t>>1) + 2 fr + (t&1); byte = R * 128 + swz(k, R)
   for (int it = 0;; ++it) {
     const int tau = tile_of(g, it);
     if (tau < 0) break;
@@ -406,162 +549,80 @@ __global__ void __launch_bounds__(kThreads, kTmaCtasPerSM) mode_tma_kernel(const
 #pragma unroll
       for (int u = 0; u < 9; ++u) acc[i][u][0] = acc[i][u][1] = 0.0;
 
-#ifdef FDP_K1T_PROF
-    const long long tk0 = clock64();
-#endif
     // the K loop, specialised on the column tile's n8 count (no per-DMMA predicate: a predicated
     // mma.sync costs a WARPSYNC + NOP pair) and, for KMAJ, on the odd-start second A tile
     const int odd = KMAJ ? p.a1odd : 0;
-    auto run = [&](auto ntv, auto oddv) {
-      kloop<KMAJ, FOLD, STAGES, decltype(ntv)::value, decltype(oddv)::value>(
-          acc, nt, p.kst, p.ne, sbase, bar_full, stage, phase, wm, role, fr, fc, lane, it, release,
-          KMAJ * 4 + (FOLD - 1) + 2 * (p.epi != 0));
-    };
-    using I0 = std::integral_constant<int, 0>;
-    using I1 = std::integral_constant<int, 1>;
+#define FDP_K1T_RUN(NTV_, ODD_) \
+  kloop<KMAJ, FOLD, STAGES, NTV_, ODD_>(g, acc, nt, p.kst, p.ne, sbase, bar_full, bar_empty, stage, phase, f, role, fr, fc, lane)
     if (nt == 9) {
-      if (odd) run(std::integral_constant<int, 9>{}, I1{}); else run(std::integral_constant<int, 9>{}, I0{});
+      if (odd) FDP_K1T_RUN(9, 1); else FDP_K1T_RUN(9, 0);
     } else if (nt == 8) {
-      if (odd) run(std::integral_constant<int, 8>{}, I1{}); else run(std::integral_constant<int, 8>{}, I0{});
+      if (odd) FDP_K1T_RUN(8, 1); else FDP_K1T_RUN(8, 0);
     } else {
-      if (odd) run(I0{}, I1{}); else run(I0{}, I0{});
+      if (odd) FDP_K1T_RUN(0, 1); else FDP_K1T_RUN(0, 0);
     }
-
-#ifdef FDP_K1T_PROF
-    const long long e0 = clock64();
-    if (lane == 0) atomicAdd(&g_k1t_prof[KMAJ * 4 + (FOLD - 1) + 2 * (p.epi != 0)][1], (unsigned long long)(e0 - tk0));
-#endif
+#undef FDP_K1T_RUN
     // ------------------------------ epilogue ------------------------------
-    // row r (0..31 of this warp's slice) of DMMA tile ti: see the fragment-offset comment above
-    auto row_of = [&](int ti, long long& yoff, long long& sidx, int& pp, bool& valid) {
-      if (KMAJ) {
-        const int R = 8 * kMT * wm + 16 * (ti >> 1) + 2 * fr + (ti & 1);
-        const long long q = (long long)t.tq * kTmaBM + R;
-        valid = q < p.Q;
-        sidx = (long long)p.yld * q;
-        yoff = sidx + p.ybs * t.b;
-        pp = 0;
-      } else {
-        const int gq = kXR * wm + (ti >> 1);
-        const int plo = 8 * (ti & 1) + fr;
-        const int ph = t.tp * p.bp + gq % p.bp;
-        const long long q = (long long)t.tq * p.bq + gq / p.bp;
-        pp = 16 * ph + plo;
-        valid = pp < p.P && q < p.Q;
-        sidx = pp + (long long)p.P * p.n * q;
-        yoff = sidx + p.ybs * t.b;
-      }
-    };
-    const long long cs = KMAJ ? 1 : p.P;  // column stride of the output
-    if (FOLD == FOLD_FWD) {
-      const int cval = role ? p.no : p.ne;
-      const int coff = role ? p.ne : 0;
+    // stage the accumulators (E columns at 0, O at 72) for the store warp, once it has drained
+    // the previous tile; rows as in the fragment layout (KMAJ: 2r + t of the slice; else p_lo)
+    if (FOLD == FOLD_FWD && !KMAJ && p.epi == EPI_LAMBDA) {
+      // Algorithm 1 step 3 in registers (the consumers' FP64 / MUFU work is ~2% of a tile; in
+      // the store warps it made them the bottleneck): q~ = t~ / (lrow(p) + lamcol(a)), the
+      // padding rows i1 >= n1v of a padded intermediate stay exactly 0
+      const int coff = role ? p.ne : 0, cvalid = role ? p.no : p.ne;
 #pragma unroll
       for (int ti = 0; ti < kMT; ++ti) {
-        long long yoff, sidx;
-        int pp;
-        bool valid;
-        row_of(ti, yoff, sidx, pp, valid);
-        if (!valid) continue;
+        const int gq = wm, plo = 8 * ti + fr;
+        const int pp = 16 * (t.tp * p.bp + gq % p.bp) + plo;
+        const double* L = lsm + p.lam_off;  // [lam0 (n1) | lam1 (lam1_n) | lamcol (n)]
         double lrow = 0.0;
-        bool pad_row = false;
-        if (p.epi == EPI_LAMBDA) {  // non-KMAJ (the last mode): p = i1 + n1p * i2
+        bool pad = pp >= p.P;
+        if (!pad) {
           const int i1 = pp % p.n1;
-          pad_row = i1 >= p.n1v;
-          if (!pad_row) lrow = p.lam1 ? p.lam0[i1] + p.lam1[pp / p.n1] : p.lam0[pp];
+          pad = i1 >= p.n1v;
+          if (!pad) lrow = p.lam1 ? L[i1] + L[p.n1 + pp / p.n1] : L[pp];
         }
+        const double* Lc = L + p.n1 + p.lam1_n + coff;
 #pragma unroll
-        for (int u = 0; u < 9; ++u) {
-          if (u < nt) {
+        for (int u = 0; u < 9; ++u)
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int a = 8 * (nt0 + u) + 2 * fc + h;
-              const int oc = coff + a;
-              if (a < cval) {
-                double v = acc[ti][u][h];
-                if (p.epi == EPI_LAMBDA) v = pad_row ? 0.0 : fdp_div(v, lrow + p.lamcol[oc]);
-                p.Y[yoff + cs * oc] = v;
-              } else if (KMAJ && role && oc < p.yld) {
-                p.Y[yoff + oc] = 0.0;  // the zero pad column of a padded KMAJ output row
-              }
-            }
+          for (int h = 0; h < 2; ++h) {
+            const int a = 8 * (nt0 + u) + 2 * fc + h;
+            if (u < nt) acc[ti][u][h] = (pad || a >= cvalid) ? 0.0 : fdp_div(acc[ti][u][h], lrow + Lc[a]);
           }
-        }
-      }
-    } else {
-      // FOLD_BWD: O warps pass o through shared memory (two halves of 16 rows), E warps store
-      // x_c = e + o and x_{n-1-c} = e - o
-      const unsigned ex = epi_base + wm * (kXR * 8 * 72 * 8);
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        if (role) {
-#pragma unroll
-          for (int tt = 0; tt < kXR; ++tt) {
-            const int ti = kXR * half + tt;
-#pragma unroll
-            for (int u = 0; u < 9; ++u)
-              if (u < nt) sts128(ex + ((8 * tt + fr) * 72 + 8 * u + 2 * fc) * 8, acc[ti][u][0], acc[ti][u][1]);
-          }
-        }
-        named_bar(1 + wm, 64);
-        if (!role) {
-#pragma unroll
-          for (int tt = 0; tt < kXR; ++tt) {
-            const int ti = kXR * half + tt;
-            long long yoff, sidx;
-            int pp;
-            bool valid;
-            row_of(ti, yoff, sidx, pp, valid);
-            if (!valid) continue;
-#pragma unroll
-            for (int u = 0; u < 9; ++u) {
-              if (u < nt) {
-                double o0, o1;
-                lds128(ex + ((8 * tt + fr) * 72 + 8 * u + 2 * fc) * 8, o0, o1);
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                  const int c = 8 * (nt0 + u) + 2 * fc + h;
-                  if (c < p.ne) {
-                    const double e = acc[ti][u][h], o = h ? o1 : o0;
-                    double v0 = e + o, v1 = e - o;
-                    const int cm = p.n - 1 - c;
-                    if (p.epi == EPI_SCALE) {
-                      v0 *= p.scale[sidx + cs * c];
-                      v1 *= p.scale[sidx + cs * cm];
-                    }
-                    p.Y[yoff + cs * c] = v0;
-                    if (cm != c) p.Y[yoff + cs * cm] = v1;
-                  }
-                }
-              }
-            }
-          }
-        }
-        named_bar(1 + wm, 64);
       }
     }
-#ifdef FDP_K1T_PROF
-    if (lane == 0) {
-      atomicAdd(&g_k1t_prof[KMAJ * 4 + (FOLD - 1) + 2 * (p.epi != 0)][2], (unsigned long long)(clock64() - e0));
-      atomicAdd(&g_k1t_prof[KMAJ * 4 + (FOLD - 1) + 2 * (p.epi != 0)][3], 1ULL);
+    mbar_wait(bar_cempty, cphase ^ 1);
+#pragma unroll
+    for (int ti = 0; ti < kMT; ++ti) {
+      if (KMAJ) {
+        const int R = 16 * wm + 2 * fr + ti;
+#pragma unroll
+        for (int u = 0; u < 9; ++u)
+          if (u < nt) sts128(cbuf + (unsigned)(R * kCLdK + 72 * role + 8 * u + 2 * fc) * 8u, acc[ti][u][0], acc[ti][u][1]);
+      } else {
+        const int R = 16 * wm + 8 * ti + fr;
+#pragma unroll
+        for (int u = 0; u < 9; ++u)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            if (u < nt) sts64(cbuf + (unsigned)((72 * role + 8 * u + 2 * fc + h) * kCLdN + R) * 8u, acc[ti][u][h]);
+      }
     }
-#endif
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar_cfull);
+    cphase ^= 1;
   }
 }
 
 template <bool KMAJ, int FOLD, int STAGES>
 constexpr size_t smem_bytes() {
-  return 1024 + (size_t)STAGES * kStageBytes + (FOLD == FOLD_BWD ? kEpiBytes : 0) + 16 * STAGES + 16;
+  return 1024 + (size_t)STAGES * kStageBytes + kCBytes + 16 * STAGES + 64 +
+         (FOLD == FOLD_FWD ? (size_t)kLamMax * 8 : 0);
 }
 
-#ifndef FDP_K1T_SF
-#define FDP_K1T_SF 3
-#endif
-#ifndef FDP_K1T_SB
-#define FDP_K1T_SB 2
-#endif
-constexpr int kStagesFwd = FDP_K1T_SF;
-constexpr int kStagesBwd = FDP_K1T_SB;
+constexpr int kStagesFwd = 3;
+constexpr int kStagesBwd = 3;
 
 template <bool KMAJ, int FOLD, int STAGES>
 cudaError_t launch_t(const TmaGroup& g, int grid, cudaStream_t s) {
@@ -642,17 +703,3 @@ cudaError_t launch_pad_rows(const double* x, long long xbs, double* y, long long
 }
 }  // namespace fdp
 
-#ifdef FDP_K1T_PROF
-extern "C" void fdp_k1t_prof(unsigned long long* out, int reset) {
-  cudaMemcpyFromSymbol(out, fdp::g_k1t_prof, sizeof(unsigned long long) * 32);
-  cudaMemcpyFromSymbol(out + 32, fdp::g_k1t_prof2, sizeof(unsigned long long) * 32);
-  cudaMemcpyFromSymbol(out + 64, fdp::g_k1t_wwait, sizeof(unsigned long long) * 256);
-  if (reset) {
-    unsigned long long z[32] = {0};
-    cudaMemcpyToSymbol(fdp::g_k1t_prof2, z, sizeof(z));
-    unsigned long long z2[256] = {0};
-    cudaMemcpyToSymbol(fdp::g_k1t_wwait, z2, sizeof(z2));
-    cudaMemcpyToSymbol(fdp::g_k1t_prof, z, sizeof(z));
-  }
-}
-#endif

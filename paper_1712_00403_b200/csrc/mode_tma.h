@@ -8,14 +8,8 @@
 
 namespace fdp {
 
-#ifndef FDP_K1T_BM
-#define FDP_K1T_BM 64
-#endif
-#ifndef FDP_K1T_CPS
-#define FDP_K1T_CPS 2
-#endif
-constexpr int kTmaBM = FDP_K1T_BM;           // rows of a CTA tile
-constexpr int kTmaCtasPerSM = FDP_K1T_CPS;   // independent CTAs per SM (DESIGN.md §5 "K1t")
+constexpr int kTmaBM = 64;             // rows of a CTA tile
+constexpr int kTmaCtasPerSM = 1;       // one persistent CTA per SM (DESIGN.md §5 "K1t")
 constexpr int kTmaBK = 16;             // k per pipeline stage
 constexpr int kTmaMaxNT = 9;           // n8 tiles per role and column tile
 constexpr int kTmaWChunk = 4 * 5 * 32 * 2;  // doubles of one role's W chunk per stage
@@ -45,6 +39,7 @@ struct TmaProb {
   int P, Q, bp, bq, tiles_p, tiles_q;
   int yld, n1, n1v, epi;
   int a1odd;      // KMAJ: the second A tile starts at an odd column (odd n FWD / odd ne BWD)
+  int lam_off, lam1_n;  // EPI_LAMBDA: offset of this problem's staged factors, length of lam1
   int tile_begin;
 };
 
@@ -55,7 +50,9 @@ struct TmaGroup {
   int count;
   int total_tiles;
   int ct_uniform;  // column tiles of every problem when equal (grid a multiple of it), else 0
+  int lam_elems;   // doubles of staged Lambda factors (0: none)
   int dbg;         // timing experiments of the -DFDP_K1T_PROF build (FDP_K1T_DBG)
+  int stagger_ns;  // start delay of the odd CTA groups (FDP_K1T_STAGGER, experiment)
 };
 
 cudaError_t launch_mode_tma(const TmaGroup& g, bool kmaj, int fold, int grid, cudaStream_t s);

@@ -9,7 +9,7 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "+d"(c[0]), "+d"(c[1]) : "d"(a), "d"(b));
 }
 
-template <int MT, int NT, int FOLD = 0>
+template <int MT, int NT, int FOLD = 0, int SYNC = 0>
 __global__ void k(double* out, int iters, int K4) {
   extern __shared__ double sm[];
   const int SA = 100, SB = 116;
@@ -46,6 +46,7 @@ __global__ void k(double* out, int iters, int K4) {
       for (int i = 0; i < MT; ++i)
 #pragma unroll
         for (int j = 0; j < NT; ++j) dmma(acc[i][j], a[i], b[j]);
+      if (SYNC && (k4 & 3) == 3) __syncthreads();
       if (FOLD == 2) {
         const int kn = (4 * (k4 + 1) + fc) % (4 * K4);
 #pragma unroll
@@ -61,51 +62,37 @@ __global__ void k(double* out, int iters, int K4) {
   if (s == 12345.678) out[0] = s;
 }
 
-template <int MT, int NT, int FOLD = 0>
+template <int MT, int NT, int FOLD = 0, int SYNC = 0>
 void run(int warps, int ctas_per_sm) {
   double* out;
   cudaMalloc(&out, 8);
   const int K4 = 17, iters = 400;
   size_t smem = sizeof(double) * 4 * K4 * (100 + 116);
-  cudaFuncSetAttribute(k<MT, NT, FOLD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k<MT, NT, FOLD, SYNC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int grid = 148 * ctas_per_sm;
-  k<MT, NT, FOLD><<<grid, warps * 32, smem>>>(out, 10, K4);
+  k<MT, NT, FOLD, SYNC><<<grid, warps * 32, smem>>>(out, 10, K4);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   cudaEventRecord(a);
-  k<MT, NT, FOLD><<<grid, warps * 32, smem>>>(out, iters, K4);
+  k<MT, NT, FOLD, SYNC><<<grid, warps * 32, smem>>>(out, iters, K4);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   float ms;
   cudaEventElapsedTime(&ms, a, b);
   double flops = 512.0 * MT * NT * K4 * (double)iters * warps * grid;
-  printf("{\"FOLD\": %d, \"MT\": %d, \"NT\": %d, \"warps_per_cta\": %d, \"ctas_per_sm\": %d, \"tflops\": %.2f, \"err\": \"%s\"}\n", FOLD, MT, NT,
+  printf("{\"SYNC\": %d, \"FOLD\": %d, \"MT\": %d, \"NT\": %d, \"warps_per_cta\": %d, \"ctas_per_sm\": %d, \"tflops\": %.2f, \"err\": \"%s\"}\n", SYNC, FOLD, MT, NT,
          warps, ctas_per_sm, flops / (ms * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
   fflush(stdout);
   cudaFree(out);
 }
 
 int main() {
-  run<4, 9, 1>(8, 1);
-  run<4, 9, 2>(8, 1);
-  run<4, 9, 1>(16, 1);
-  run<2, 9, 1>(16, 1);
-  run<2, 9, 2>(16, 1);
-  run<4, 9>(8, 1);
-  run<4, 8>(8, 1);
-  run<4, 9>(4, 2);
-  run<2, 9>(8, 1);
-  run<2, 9>(16, 1);
-  for (int w : {4, 8, 16}) {
-    run<1, 9>(w, 1);
-    run<2, 9>(w, 1);
-    run<1, 12>(w, 1);
-    run<2, 11>(w, 1);
-    run<2, 4>(w, 1);
-    run<4, 4>(w, 1);
-  }
-  run<1, 9>(8, 2);
-  run<2, 9>(8, 2);
+  run<2, 9, 0, 0>(8, 2);
+  run<2, 9, 0, 1>(8, 2);
+  run<2, 9, 1, 1>(8, 2);
+  run<2, 9, 0, 1>(16, 1);
+  run<4, 9, 0, 1>(8, 1);
+  run<2, 9, 0, 0>(16, 1);
   return 0;
 }
