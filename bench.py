@@ -512,6 +512,9 @@ def main():
         # (FOLD = 1, the fourth template argument); else every FD-transform kernel captured
         allk = [k for k in json.load(open(ncu_json)).get("kernels", []) if "mode_" in k["kernel"]]
         ks = [k for k in allk if "mode_plane" in k["kernel"]]
+        if not ks:  # K1t forward transforms: mode_tma_kernel<KMAJ, FOLD_FWD = 1, STAGES>
+            ks = [k for k in allk if "mode_tma_kernel<" in k["kernel"]
+                  and k["kernel"].split("mode_tma_kernel<")[1].split(",")[1].strip() == "1"]
         if not ks:
             ks = [k for k in allk if "fold_kernel<" in k["kernel"]
                   and k["kernel"].split("fold_kernel<")[1].split(",")[3].strip() == "1"]
@@ -574,8 +577,9 @@ def main():
         "roofline": {
             "bound": "tensor",
             "kernel": "the dominant FD-transform launch of the step (config 2/3: the plane kernel "
-                      "mode_plane_kernel; configs 4/5: a folded K1 mode_contract_fold_kernel; FP64 "
-                      "mma.sync m8n8k4 -> DMMA)",
+                      "mode_plane_kernel; configs 4/5: the TMA-fed folded transform mode_tma_kernel "
+                      "(K1t), the last forward mode with the Lambda division; FP64 mma.sync m8n8k4 "
+                      "-> DMMA)",
             "achieved": achieved,
             "dominant_launch": dom,
             "k1_family": {"achieved": k1_family,
