@@ -5,7 +5,7 @@ SRC := $(PKG)/csrc
 LIB := $(PKG)/libfdp.so
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -O3 --expt-relaxed-constexpr
-OBJ := build/mode_tma.o build/abi_tma.o build/mode_contract.o build/mode_small.o build/mode_plane.o build/kron_band.o build/kron_mass.o build/slab.o build/vec.o build/abi.o build/abi_block.o build/abi_slab.o build/abi_iga.o build/abi_kron.o build/abi_krylov.o build/host_eig.o build/host_iga.o build/host_geo.o
+OBJ := build/mode_tma.o build/abi_tma.o build/mode_contract.o build/mode_small.o build/mode_plane.o build/kron_band.o build/kron_mass.o build/slab.o build/vec.o build/abi.o build/abi_block.o build/abi_slab.o build/abi_iga.o build/abi_kron.o build/abi_krylov.o build/host_eig.o build/host_iga.o build/host_geo.o build/nccl_dl.o
 HDR := $(SRC)/fdp_internal.h $(SRC)/abi_impl.h $(SRC)/mode_tma.h include/fdp.h
 
 all: $(LIB)
@@ -19,7 +19,7 @@ build/%.o: $(SRC)/%.cpp $(HDR)
 	$(NVCC) $(NVFLAGS) -x cu -c $< -o $@
 
 $(LIB): $(OBJ)
-	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJ)
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJ) -ldl
 
 clean:
 	rm -rf build $(LIB)

@@ -39,7 +39,7 @@ typedef enum {
   FDP_ERR_SINGULAR = 4,    /* Kronecker-sum spectrum: sum_d c_d min(lambda_d) <= 1e-12 sum_d c_d max(lambda_d) */
   FDP_ERR_CUDA = 5,        /* CUDA runtime error (launch, copy, graph) */
   FDP_ERR_OOM = 6,         /* device or host allocation failed */
-  FDP_ERR_NCCL = 7,        /* reserved: multi-GPU exchange */
+  FDP_ERR_NCCL = 7,        /* NCCL unavailable (libnccl.so.2 not loadable) or an NCCL call failed */
   FDP_ERR_UNSUPPORTED = 8  /* valid request this build does not implement (e.g. D > 3) */
 } fdp_status;
 
@@ -281,22 +281,55 @@ fdp_status fdp_peer_open(const void* ipc_handle, int device, void** dev_ptr);
 fdp_status fdp_peer_close(void* dev_ptr);
 fdp_status fdp_peer_free(void* dev_ptr);
 
-/* ---- Sharded block apply (SURVEY.md §8(b) multi-GPU row, §8(e) config 5) ----
- * A communicator for one block preconditioner P (D = 3) over nranks processes (one GPU each):
+/* ---- Sharded applies (SURVEY.md §8(b) multi-GPU row, §8(e) config 5) ----
+ * Slab decomposition of the last axis: rank g of nranks owns planes fdp_slab_range(n3, nranks, g)
+ * of every block (its z-slab, vec order); mode 3 runs on y-slabs between two all-to-all
+ * exchanges. Two kinds of communicator (fdp_comm), freed with fdp_comm_destroy:
+ *
+ * NCCL (the paper-independent baseline): rank 0 calls fdp_nccl_unique_id (128
+ * bytes, host), the caller distributes them (e.g. the torch.distributed store), every rank calls
+ * fdp_comm_init(nranks, rank, id, device). libfdp loads NCCL at run time (libnccl.so.2; in a
+ * process that imported torch, torch's copy): FDP_ERR_NCCL when it cannot be loaded or a call
+ * fails (fdp_last_error has NCCL's message). The exchanges are grouped ncclSend / ncclRecv of the
+ * packed slab pieces (one NCCL group per exchange for all blocks). Such a comm serves any handle:
+ *   fd_apply_sharded: x = D^{-1/2} U Lambda^{-1} U^T D^{-1/2} b on this rank's z-slab (b, x,
+ *     dscale: device, n1 n2 nz doubles; dscale = the slab's slice of the length-N D, or NULL;
+ *     x must not alias b); workspace >= fd_sharded_workspace_bytes(h, c) (0 for a peer comm).
+ *   block_precond_apply_sharded (below).
+ *
+ * Peer-store (the exchanges fused into the contraction epilogues), for one block preconditioner P
+ * (D = 3):
  *   1. fdp_comm_create: allocates this rank's exchange buffers (per block a y-slab and a z-slab,
  *      plus an nranks-slot barrier flag array) and writes its blob of CUDA IPC handles
  *      (fdp_comm_blob_bytes(P, nranks) bytes, host memory owned by the caller);
  *   2. the caller all-gathers the blobs (e.g. torch.distributed; rank-major, host);
  *   3. fdp_comm_connect maps every peer's buffers (P2P over NVLink / NVSwitch).
- * block_precond_apply_sharded then applies P_D^{-1} (or (P_D^G)^{-1}: the block's D scalings,
- * sliced to the rank's slab) to this rank's slabs: r, s device, block_precond_sharded_size
- * doubles laid out [u_1 z-slab | .. | u_D z-slab | p z-slab] (z-slab of block b: planes
- * fdp_slab_range(n3_b, nranks, rank) of the block in vec order). All blocks' phases run with
- * the exchanges fused into the epilogues (fd_apply_slab_peer, kron_mass_apply_slab_peer) and
- * an fdp_peer_barrier after each phase; no host synchronisation, graph-capturable. Every rank
- * must make the same calls in the same order. The communicator is not thread- or stream-safe.
- * workspace: device, >= block_precond_sharded_workspace_bytes. */
+ *   Phases are separated by fdp_peer_barrier kernels; no NCCL call in the apply.
+ *
+ * block_precond_apply_sharded applies P_D^{-1} (or (P_D^G)^{-1}: the block's D scalings, sliced
+ * to the rank's slab) to this rank's slabs: r, s device, block_precond_sharded_size doubles laid
+ * out [u_1 z-slab | .. | u_D z-slab | p z-slab]. In every phase the steps of all blocks run side
+ * by side (step i of the velocity blocks is one grouped launch). No host synchronisation;
+ * graph-capturable (NCCL: as NCCL's own calls are). Every rank must make the same calls in the
+ * same order. A communicator is not thread- or stream-safe; destroy every CUDA graph that
+ * captured an apply on an NCCL communicator before fdp_comm_destroy (NCCL's teardown waits for
+ * the graphs' resources). workspace: device, >=
+ * block_precond_sharded_workspace_bytes(P, c) (per-block regions; NCCL comms also hold the
+ * send / receive slabs there). */
 typedef struct fdp_comm_s* fdp_comm;
+#define FDP_NCCL_ID_BYTES 128
+/* Host only: per-peer element counts of exchange 1 (z-slab pieces -> y-slab) or 2 (the reverse)
+ * of a block with extents dims[0..2] for rank `rank` of nranks, in rank order (send_counts,
+ * recv_counts: host arrays of nranks). Exchange 1 sends rank h the planes i2 in its y-range of my
+ * z-slab (dims[0] ny_h nz doubles, packed in rank order) and receives its z-planes of my y-range
+ * (dims[0] ny nz_h). FDP_ERR_INVALID_ARG on bad arguments. */
+fdp_status fdp_slab_exchange_counts(const int32_t* dims, int nranks, int rank, int exchange,
+                                    int64_t* send_counts, int64_t* recv_counts);
+fdp_status fdp_nccl_unique_id(void* id);
+fdp_status fdp_comm_init(int nranks, int rank, const void* nccl_unique_id, int device, fdp_comm* out);
+size_t fd_sharded_workspace_bytes(fdp_fd h, fdp_comm c);
+fdp_status fd_apply_sharded(fdp_fd h, fdp_comm c, const double* b, double* x, const double* dscale,
+                            void* workspace, void* stream);
 size_t fdp_comm_blob_bytes(fdp_block P, int nranks);
 fdp_status fdp_comm_create(fdp_block P, int nranks, int rank, fdp_comm* out, void* blob);
 fdp_status fdp_comm_connect(fdp_comm c, const void* all_blobs);

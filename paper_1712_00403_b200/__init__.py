@@ -111,6 +111,11 @@ def _load():
         "block_precond_sharded_workspace_bytes": (sz, [vp, vp]),
         "block_precond_apply_sharded": (i32, [vp, vp, vp, vp, vp, vp]),
         "fdp_comm_destroy": (i32, [vp]),
+        "fdp_nccl_unique_id": (i32, [vp]),
+        "fdp_slab_exchange_counts": (i32, [vp, i32, i32, i32, vp, vp]),
+        "fdp_comm_init": (i32, [i32, i32, vp, i32, ctypes.POINTER(vp)]),
+        "fd_sharded_workspace_bytes": (sz, [vp, vp]),
+        "fd_apply_sharded": (i32, [vp, vp, vp, vp, vp, vp, vp]),
         "fdp_peer_alloc": (i32, [sz, i32, ctypes.POINTER(vp), vp]),
         "fdp_peer_open": (i32, [vp, i32, ctypes.POINTER(vp)]),
         "fdp_peer_close": (i32, [vp]),
@@ -469,6 +474,15 @@ def slab_range(n: int, nranks: int, rank: int):
     lo, ln = ctypes.c_int64(), ctypes.c_int64()
     _check(lib.fdp_slab_range(n, nranks, rank, ctypes.byref(lo), ctypes.byref(ln)))
     return lo.value, ln.value
+
+
+def slab_exchange_counts(dims, nranks: int, rank: int, exchange: int):
+    """fdp_slab_exchange_counts: (send counts, recv counts) per peer of exchange 1 or 2."""
+    d = np.ascontiguousarray(dims, dtype=np.int32)
+    sc = np.zeros(nranks, dtype=np.int64)
+    rc = np.zeros(nranks, dtype=np.int64)
+    _check(lib.fdp_slab_exchange_counts(_ptr(d), nranks, rank, exchange, _ptr(sc), _ptr(rc)))
+    return [int(v) for v in sc], [int(v) for v in rc]
 
 
 def fd_apply_slab(h, phase: int, nranks: int, rank: int, x_in, x_out, dscale, workspace, stream=None):

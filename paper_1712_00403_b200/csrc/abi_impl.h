@@ -327,3 +327,17 @@ cudaError_t enqueue_mass(const fdp_mass_s* h, int mode, const double* in, double
 void kron_diag_accumulate(int D, const int* n, const std::vector<const double*>& f, double c,
                           double* out);
 cudaError_t run1(ModeProb p, const TileCfg& c, bool kmaj, cudaStream_t s);
+// NCCL loaded at run time (nccl_dl.cpp): the exchanges of the NCCL-communicator sharded applies.
+namespace fdp {
+struct NcclXfer {
+  const double* buf;  // send: source; recv: destination
+  long long count;    // doubles (0: skipped)
+  int peer;
+  bool send;
+};
+fdp_status nccl_unique_id(void* id);
+fdp_status nccl_comm_init(void** comm, int nranks, int rank, const void* id);
+void nccl_comm_destroy(void* comm);
+// one grouped set of point-to-point transfers (ncclGroupStart .. ncclGroupEnd) on stream s
+fdp_status nccl_exchange(void* comm, const std::vector<NcclXfer>& xs, cudaStream_t s, const char* where);
+}  // namespace fdp

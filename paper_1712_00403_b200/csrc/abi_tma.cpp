@@ -36,7 +36,8 @@ std::vector<double> tma_wt_build(int n, int foldh, int ldw, const std::vector<do
             for (int lane = 0; lane < 32; ++lane)
               for (int h = 0; h < 2; ++h) {
                 const int u = 2 * pr + h, r = lane >> 2, c = lane & 3;
-                const int k = kTmaBK * s + (kmaj ? 4 * j + c : 8 * (j >> 1) + 2 * c + (j & 1));
+                const bool nat = kmaj || (s == KS - 1 && tma_last_nat(ne, false));
+                const int k = kTmaBK * s + (nat ? 4 * j + c : 8 * (j >> 1) + 2 * c + (j & 1));
                 const int a = 8 * (nt0 + u) + r;
                 double v = 0.0;
                 if (u < nt && k < kv && a < av) v = w[(size_t)(r0 + k) * ldw + a];
@@ -71,17 +72,11 @@ EncodeFn encoder() {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-CUtensorMapL2promotion promotion() {
-  const char* e = std::getenv("FDP_K1T_PROMO");  // experiment switch: 0, 64, 128, 256 (default)
-  if (!e) return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-  const int v = std::atoi(e);
-  return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
-         : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
-         : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-}
+CUtensorMapL2promotion promotion() { return CU_TENSOR_MAP_L2_PROMOTION_L2_256B; }
 
 }  // namespace
 
+// A tensor map can describe the A operand (else: the first pass's input is row-padded first).
 bool tma_input_ok(const ModeProb& p, bool kmaj) {
   if (!aligned16(p.X)) return false;
   if (p.batch > 1 && (p.xbs & 1)) return false;
@@ -94,6 +89,7 @@ bool tma_eligible(const ModeProb& p, bool kmaj) {
   if (!p.Wt || !p.fold_k1 || p.peers || p.tio) return false;
   if (p.fold != FOLD_FWD && p.fold != FOLD_BWD) return false;
   if (p.fold == FOLD_FWD && p.epi != EPI_NONE && p.epi != EPI_LAMBDA) return false;
+  if (kmaj && p.epi == EPI_LAMBDA) return false;  // Lambda^{-1} is applied on the non-KMAJ store path
   if (p.fold == FOLD_BWD && p.epi != EPI_NONE && p.epi != EPI_SCALE) return false;
   if (p.nout != p.n || p.n < 8) return false;
   if (kmaj && p.P != 1) return false;
@@ -110,6 +106,7 @@ cudaError_t launch_tma_stage(const ModeProb* probs, int count, bool kmaj, cudaSt
   g.count = count;
   int tiles = 0;
   const int fold = probs[0].fold;
+
   for (int i = 0; i < count; ++i) {
     const ModeProb& m = probs[i];
     if (m.fold != fold) return cudaErrorInvalidValue;
@@ -193,9 +190,6 @@ cudaError_t launch_tma_stage(const ModeProb* probs, int count, bool kmaj, cudaSt
   g.ct_uniform = g.prob[0].ctiles;
   for (int i = 1; i < count; ++i)
     if (g.prob[i].ctiles != g.ct_uniform) g.ct_uniform = 0;
-  if (std::getenv("FDP_K1T_NOGROUP")) g.ct_uniform = 0;  // experiment switch
-  if (const char* e = std::getenv("FDP_K1T_DBG")) g.dbg = std::atoi(e);
-  if (const char* e = std::getenv("FDP_K1T_STAGGER")) g.stagger_ns = std::atoi(e);
   int grid = std::min(tiles, kTmaCtasPerSM * num_sms());
   if (g.ct_uniform > 0) grid = std::max(g.ct_uniform, grid / g.ct_uniform * g.ct_uniform);
   ++g_k1_launches[1];

@@ -19,8 +19,9 @@
 //     drain it to HBM with 16-byte stores (an in-register epilogue stalled every consumer for
 //     6-10k cycles per tile: all CTAs finish together and the store burst backs up the memory
 //     system -- 13-21% of the kernel, measured with clock64 per phase);
-//   * Lambda^{-1} (the last forward mode) is applied by the consumers in registers, with the
-//     Lambda factors staged in shared memory at kernel start.
+//   * Lambda^{-1} (the last forward mode) is applied by the store warps on the way out, with the
+//     Lambda factors staged in shared memory at kernel start (in the consumers its MUFU / FP64
+//     work idled the DMMA pipe ~5k cycles per tile: 11-20% of that pass, measured).
 //
 // Folded algebra (persymmetric pencil, n = ne + no, ne = ceil(n/2)):
 //   FOLD_FWD: y_E = W_E^T s, y_O = W_O^T d, s_k = x_k + x_{n-1-k}, d_k = x_k - x_{n-1-k}:
@@ -250,10 +251,16 @@ __device__ __forceinline__ unsigned kmaj_col(unsigned rowbase, int x, int lam) {
   return rowbase + ((((lam >> 1) ^ x) << 4) | ((lam & 1) << 3));
 }
 
-template <bool KMAJ, int FOLD, int NTV, int ODD, int J>
+// NAT: the natural k order k = 4 j + c in a non-KMAJ last stage (tma_last_nat; offsets computed
+// here, the same bank-conflicted order in the host's W chunk of that stage)
+__device__ __forceinline__ unsigned swz(int plo, int k) {
+  return (unsigned)((((plo >> 1) ^ (k & 7)) << 4) | ((plo & 1) << 3));
+}
+
+template <bool KMAJ, int FOLD, int NTV, int ODD, int J, bool NAT = false>
 __device__ __forceinline__ void stage_mma(double (&acc)[kMT][9][2], int nt, unsigned A0, unsigned A1,
                                           unsigned B, unsigned Mini, const Frag& f, double sgn,
-                                          int role, int fr, int fc, int lane, int jmax) {
+                                          int role, int wm, int fr, int fc, int lane, int jmax) {
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     if (j < J && (J == 4 || j < jmax)) {
@@ -271,6 +278,16 @@ __device__ __forceinline__ void stage_mma(double (&acc)[kMT][9][2], int nt, unsi
             a[ti] = fma(sgn, w, v);
           } else {
             a[ti] = lds64(role ? a1 : A0 + kmaj_col(rb, x, k));
+          }
+        } else if (NAT) {
+          const int k = 4 * j + fc, km = kTmaBK - 1 - k, plo = 8 * ti + fr;
+          const unsigned o0 = (unsigned)((k + 16 * wm) * 128) + swz(plo, k);
+          if (FOLD == FOLD_FWD) {
+            const unsigned o1 = (unsigned)((km + 16 * wm) * 128) + swz(plo, km);
+            const double v = lds64(A0 + o0), w = lds64(A1 + o1);
+            a[ti] = fma(sgn, w, v);
+          } else {
+            a[ti] = lds64((role ? A1 : A0) + o0);
           }
         } else {
           const unsigned o0 = f.a0[ti][j & 1] + (j >> 1) * 8 * 128;
@@ -299,10 +316,11 @@ __device__ __forceinline__ void stage_mma(double (&acc)[kMT][9][2], int nt, unsi
 template <bool KMAJ, int FOLD, int STAGES, int NTV, int ODD>
 __device__ __forceinline__ void kloop(const TmaGroup& g, double (&acc)[kMT][9][2], int nt, int kst, int ne,
                                       unsigned sbase, unsigned bar_full, unsigned bar_empty, int& stage,
-                                      unsigned& phase, const Frag& f, int role, int fr, int fc, int lane) {
+                                      unsigned& phase, const Frag& f, int role, int wm, int fr, int fc, int lane) {
   const double sgn = role ? -1.0 : 1.0;  // FWD: E warps form s = x + Jx, O warps d = x - Jx
   const int rem = ne - (kst - 1) * kTmaBK;  // valid k of the last stage (1 .. 16)
-  const int jlast = KMAJ ? (rem + 3) >> 2 : (rem <= 8 ? 2 : 4);
+  const bool nat = tma_last_nat(ne, KMAJ);
+  const int jlast = KMAJ || nat ? (rem + 3) >> 2 : (rem <= 8 ? 2 : 4);
   for (int s = 0; s < kst; ++s) {
     mbar_wait(bar_full + 8 * stage, phase);
     const unsigned A0 = sbase + stage * kStageBytes;
@@ -310,9 +328,11 @@ __device__ __forceinline__ void kloop(const TmaGroup& g, double (&acc)[kMT][9][2
     const unsigned B = A1 + kABytes + role * kBBytes;
     const unsigned Mini = A1 + kABytes + 2 * kBBytes;
     if (s + 1 < kst || jlast == 4)
-      stage_mma<KMAJ, FOLD, NTV, ODD, 4>(acc, nt, A0, A1, B, Mini, f, sgn, role, fr, fc, lane, 4);
+      stage_mma<KMAJ, FOLD, NTV, ODD, 4>(acc, nt, A0, A1, B, Mini, f, sgn, role, wm, fr, fc, lane, 4);
+    else if (!KMAJ && nat)
+      stage_mma<KMAJ, FOLD, NTV, ODD, 3, true>(acc, nt, A0, A1, B, Mini, f, sgn, role, wm, fr, fc, lane, jlast);
     else
-      stage_mma<KMAJ, FOLD, NTV, ODD, 3>(acc, nt, A0, A1, B, Mini, f, sgn, role, fr, fc, lane, jlast);
+      stage_mma<KMAJ, FOLD, NTV, ODD, 3>(acc, nt, A0, A1, B, Mini, f, sgn, role, wm, fr, fc, lane, jlast);
     __syncwarp();
     if (lane == 0) mbar_arrive(bar_empty + 8 * stage);  // this warp is done with the slot
     if (++stage == STAGES) {
@@ -342,7 +362,22 @@ __device__ __forceinline__ double lds_f64(unsigned a) {
 
 template <bool KMAJ, int FOLD>
 __device__ __noinline__ void store_loop(const TmaGroup& g, unsigned cbuf, unsigned bar_cfull,
-                                        unsigned bar_cempty, int lane, int sw) {
+                                        unsigned bar_cempty, double* lsm, int lane, int sw) {
+  const unsigned lsa = smem_u32(lsm);
+  if (FOLD == FOLD_FWD && !KMAJ && g.lam_elems > 0) {
+    // stage the Lambda factors of every EPI_LAMBDA problem: [lam0 (n1v of n1) | lam1 | lamcol]
+    for (int pi = 0; pi < g.count; ++pi) {
+      const TmaProb& q = g.prob[pi];
+      if (q.epi != EPI_LAMBDA) continue;
+      double* d = lsm + q.lam_off;
+      const int tid = lane + 32 * sw;
+      for (int i = tid; i < q.n1v; i += kStoreWarps * 32) d[i] = q.lam0[i];
+      if (q.lam1)
+        for (int i = tid; i < q.lam1_n; i += kStoreWarps * 32) d[q.n1 + i] = q.lam1[i];
+      for (int i = tid; i < q.n; i += kStoreWarps * 32) d[q.n1 + q.lam1_n + i] = q.lamcol[i];
+    }
+    named_bar(14, kStoreWarps * 32);
+  }
   unsigned phase = 0;
   for (int it = 0;; ++it) {
     const int tau = tile_of(g, it);
@@ -365,20 +400,44 @@ __device__ __noinline__ void store_loop(const TmaGroup& g, unsigned cbuf, unsign
       const bool valid = pp < p.P && q < p.Q;
       const long long sidx = pp + P * n * q;
       double* yrow = Y + sidx + p.ybs * t.b;
-      if (valid) {
-        for (int w = sw; w < (FOLD == FOLD_FWD ? 2 : 1) * ncol; w += kStoreWarps) {
-          if (FOLD == FOLD_FWD) {
-            {  // (half, column) pairs dealt over the store warps: h = 0 E, 1 O
-              const int h = w >= ncol, c = w - h * ncol;
-              const int a = c0 + c;
-              if (a < (h ? no : ne)) {
-                const int oc = (h ? ne : 0) + a;
-                double v0, v1;
-                lds128(cbuf + (unsigned)((72 * h + c) * kCLdN + R) * 8u, v0, v1);
-                *reinterpret_cast<double2*>(yrow + P * oc) = make_double2(v0, v1);
-              }
+      if (valid && FOLD == FOLD_FWD) {
+        // Algorithm 1 step 3 on the way out (EPI_LAMBDA): q~ = t~ / (lrow(p) +
+        // lamcol(a)), Lambda formed from its factors; the padding rows i1 >= n1v of a padded
+        // intermediate stay exactly 0. Off the consumers' path: the division's MUFU / FP64 work
+        // overlaps the next tile's DMMAs (in the consumers it idled the DMMA pipe ~5k cycles a tile)
+        const bool lam = p.epi == EPI_LAMBDA;
+        double lr[2] = {0.0, 0.0};
+        bool zr[2] = {false, false};
+        if (lam) {
+          const unsigned L = lsa + 8u * (unsigned)p.lam_off;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int ppx = pp + h, i1 = ppx % p.n1;
+            zr[h] = i1 >= p.n1v;
+            if (!zr[h]) lr[h] = p.lam1 ? lds_f64(L + 8u * i1) + lds_f64(L + 8u * (p.n1 + ppx / p.n1)) : lds_f64(L + 8u * ppx);
+          }
+        }
+        const unsigned Lc = lsa + 8u * (unsigned)(p.lam_off + p.n1 + p.lam1_n);
+#pragma unroll 4
+        for (int w = sw; w < 2 * ncol; w += kStoreWarps) {
+          // (half, column) pairs dealt over the store warps: h = 0 E, 1 O
+          const int h = w >= ncol, c = w - h * ncol;
+          const int a = c0 + c;
+          if (a < (h ? no : ne)) {
+            const int oc = (h ? ne : 0) + a;
+            double v0, v1;
+            lds128(cbuf + (unsigned)((72 * h + c) * kCLdN + R) * 8u, v0, v1);
+            if (lam) {
+              const double lc = lds_f64(Lc + 8u * oc);
+              v0 = zr[0] ? 0.0 : fdp_div(v0, lr[0] + lc);
+              v1 = zr[1] ? 0.0 : fdp_div(v1, lr[1] + lc);
             }
-          } else {
+            *reinterpret_cast<double2*>(yrow + P * oc) = make_double2(v0, v1);
+          }
+        }
+      } else if (valid) {
+        for (int w = sw; w < ncol; w += kStoreWarps) {
+          {
             const int c = w, cc = c0 + c;
             if (cc < ne) {
               double e0, e1, o0, o1;
@@ -492,24 +551,12 @@ __global__ void __launch_bounds__(kThreads, 1) mode_tma_kernel(const __grid_cons
     return;
   }
   if (warp > kConsumerWarps) {  // the store warps
-    store_loop<KMAJ, FOLD>(g, cbuf, bar_cfull, bar_cempty, lane, warp - kConsumerWarps - 1);
+    store_loop<KMAJ, FOLD>(g, cbuf, bar_cfull, bar_cempty, lsm, lane, warp - kConsumerWarps - 1);
     return;
   }
 
   const int wm = warp % kWM, role = warp / kWM;  // role 0: E, 1: O
   const int fr = lane >> 2, fc = lane & 3;
-  if (FOLD == FOLD_FWD && g.lam_elems > 0) {  // stage the Lambda factors (consumers only)
-    for (int pi = 0; pi < g.count; ++pi) {
-      const TmaProb& q = g.prob[pi];
-      if (q.epi != EPI_LAMBDA) continue;
-      double* d = lsm + q.lam_off;
-      for (int i = threadIdx.x; i < q.n1v; i += kConsumerWarps * 32) d[i] = q.lam0[i];  // i1 < n1v only
-      if (q.lam1)
-        for (int i = threadIdx.x; i < q.lam1_n; i += kConsumerWarps * 32) d[q.n1 + i] = q.lam1[i];
-      for (int i = threadIdx.x; i < q.n; i += kConsumerWarps * 32) d[q.n1 + q.lam1_n + i] = q.lamcol[i];
-    }
-    named_bar(14, kConsumerWarps * 32);
-  }
   int stage = 0;
   unsigned phase = 0, cphase = 0;
   // per-thread fragment offsets (see Frag)
@@ -526,8 +573,8 @@ __global__ void __launch_bounds__(kThreads, 1) mode_tma_kernel(const __grid_cons
 #pragma unroll
       for (int jj = 0; jj < 2; ++jj) {
         const int k = 2 * fc + jj, km = kTmaBK - 1 - k;   // j < 2 rows; j >= 2 add / sub 8 rows
-        f.a0[ti][jj] = (unsigned)((k + 16 * wm) * 128 + ((((plo >> 1) ^ (k & 7)) << 4) | ((plo & 1) << 3)));
-        f.a1[ti][jj] = (unsigned)((km + 16 * wm) * 128 + ((((plo >> 1) ^ (km & 7)) << 4) | ((plo & 1) << 3)));
+        f.a0[ti][jj] = (unsigned)((k + 16 * wm) * 128) + swz(plo, k);
+        f.a1[ti][jj] = (unsigned)((km + 16 * wm) * 128) + swz(plo, km);
       }
     }
   }
@@ -541,7 +588,6 @@ __global__ void __launch_bounds__(kThreads, 1) mode_tma_kernel(const __grid_cons
     // any, multiplies zero W columns)
     const int nbase = p.n8h / p.ctiles, nrem = p.n8h % p.ctiles;
     const int nt = nbase + (t.ct < nrem ? 1 : 0);
-    const int nt0 = t.ct * nbase + min(t.ct, nrem);
 
     double acc[kMT][9][2];
 #pragma unroll
@@ -553,7 +599,7 @@ __global__ void __launch_bounds__(kThreads, 1) mode_tma_kernel(const __grid_cons
     // mma.sync costs a WARPSYNC + NOP pair) and, for KMAJ, on the odd-start second A tile
     const int odd = KMAJ ? p.a1odd : 0;
 #define FDP_K1T_RUN(NTV_, ODD_) \
-  kloop<KMAJ, FOLD, STAGES, NTV_, ODD_>(g, acc, nt, p.kst, p.ne, sbase, bar_full, bar_empty, stage, phase, f, role, fr, fc, lane)
+  kloop<KMAJ, FOLD, STAGES, NTV_, ODD_>(g, acc, nt, p.kst, p.ne, sbase, bar_full, bar_empty, stage, phase, f, role, wm, fr, fc, lane)
     if (nt == 9) {
       if (odd) FDP_K1T_RUN(9, 1); else FDP_K1T_RUN(9, 0);
     } else if (nt == 8) {
@@ -563,35 +609,9 @@ __global__ void __launch_bounds__(kThreads, 1) mode_tma_kernel(const __grid_cons
     }
 #undef FDP_K1T_RUN
     // ------------------------------ epilogue ------------------------------
-    // stage the accumulators (E columns at 0, O at 72) for the store warp, once it has drained
-    // the previous tile; rows as in the fragment layout (KMAJ: 2r + t of the slice; else p_lo)
-    if (FOLD == FOLD_FWD && !KMAJ && p.epi == EPI_LAMBDA) {
-      // Algorithm 1 step 3 in registers (the consumers' FP64 / MUFU work is ~2% of a tile; in
-      // the store warps it made them the bottleneck): q~ = t~ / (lrow(p) + lamcol(a)), the
-      // padding rows i1 >= n1v of a padded intermediate stay exactly 0
-      const int coff = role ? p.ne : 0, cvalid = role ? p.no : p.ne;
-#pragma unroll
-      for (int ti = 0; ti < kMT; ++ti) {
-        const int gq = wm, plo = 8 * ti + fr;
-        const int pp = 16 * (t.tp * p.bp + gq % p.bp) + plo;
-        const double* L = lsm + p.lam_off;  // [lam0 (n1) | lam1 (lam1_n) | lamcol (n)]
-        double lrow = 0.0;
-        bool pad = pp >= p.P;
-        if (!pad) {
-          const int i1 = pp % p.n1;
-          pad = i1 >= p.n1v;
-          if (!pad) lrow = p.lam1 ? L[i1] + L[p.n1 + pp / p.n1] : L[pp];
-        }
-        const double* Lc = L + p.n1 + p.lam1_n + coff;
-#pragma unroll
-        for (int u = 0; u < 9; ++u)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int a = 8 * (nt0 + u) + 2 * fc + h;
-            if (u < nt) acc[ti][u][h] = (pad || a >= cvalid) ? 0.0 : fdp_div(acc[ti][u][h], lrow + Lc[a]);
-          }
-      }
-    }
+    // stage the accumulators (E columns at 0, O at 72) for the store warps, once they have
+    // drained the previous tile; rows as in the fragment layout (KMAJ: 2r + t of the slice; else
+    // p_lo). The epilogue arithmetic (Lambda^{-1}, butterflies, D^{-1/2}) is the store warps'.
     mbar_wait(bar_cempty, cphase ^ 1);
 #pragma unroll
     for (int ti = 0; ti < kMT; ++ti) {
@@ -638,21 +658,19 @@ cudaError_t launch_t(const TmaGroup& g, int grid, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+template <bool KMAJ, int FOLD, int STAGES>
+cudaError_t set_smem_attr() {
+  return cudaFuncSetAttribute(mode_tma_kernel<KMAJ, FOLD, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)smem_bytes<KMAJ, FOLD, STAGES>());
+}
+
 }  // namespace
 
 cudaError_t prepare_mode_tma() {
   // set the shared-memory attributes outside any stream capture
-  const int fwd = (int)smem_bytes<true, FOLD_FWD, kStagesFwd>();
-  const int bwd = (int)smem_bytes<true, FOLD_BWD, kStagesBwd>();
   cudaError_t e;
-  if ((e = cudaFuncSetAttribute(mode_tma_kernel<true, FOLD_FWD, kStagesFwd>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, fwd)) ||
-      (e = cudaFuncSetAttribute(mode_tma_kernel<false, FOLD_FWD, kStagesFwd>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, fwd)) ||
-      (e = cudaFuncSetAttribute(mode_tma_kernel<true, FOLD_BWD, kStagesBwd>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, bwd)) ||
-      (e = cudaFuncSetAttribute(mode_tma_kernel<false, FOLD_BWD, kStagesBwd>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, bwd)))
+  if ((e = set_smem_attr<true, FOLD_FWD, kStagesFwd>()) || (e = set_smem_attr<false, FOLD_FWD, kStagesFwd>()) ||
+      (e = set_smem_attr<true, FOLD_BWD, kStagesBwd>()) || (e = set_smem_attr<false, FOLD_BWD, kStagesBwd>()))
     return e;
   return cudaSuccess;
 }
@@ -660,46 +678,62 @@ cudaError_t prepare_mode_tma() {
 cudaError_t launch_mode_tma(const TmaGroup& g, bool kmaj, int fold, int grid, cudaStream_t s) {
   if (g.total_tiles <= 0) return cudaSuccess;
   if (fold == FOLD_FWD)
-    return kmaj ? launch_t<true, FOLD_FWD, kStagesFwd>(g, grid, s)
-                : launch_t<false, FOLD_FWD, kStagesFwd>(g, grid, s);
+    return kmaj ? launch_t<true, FOLD_FWD, kStagesFwd>(g, grid, s) : launch_t<false, FOLD_FWD, kStagesFwd>(g, grid, s);
   if (fold == FOLD_BWD)
-    return kmaj ? launch_t<true, FOLD_BWD, kStagesBwd>(g, grid, s)
-                : launch_t<false, FOLD_BWD, kStagesBwd>(g, grid, s);
+    return kmaj ? launch_t<true, FOLD_BWD, kStagesBwd>(g, grid, s) : launch_t<false, FOLD_BWD, kStagesBwd>(g, grid, s);
   return cudaErrorInvalidValue;
 }
 
-}  // namespace fdp
-
 // ---------------------------------------------------------------------------------------------
-// Row padding for K1t's first pass: y (rows of n1p, pad entries zero) <- x (rows of n1), batch
-// items at strides xbs / ybs. HBM streaming (16 B per element); used only when the C-ABI input
-// cannot be read through a tensor map (odd row length or a base not 16-byte aligned).
+// Row padding for K1t's first pass: y (rows of n1p = n1 + 1, pad entry zero) <- x (rows of odd
+// n1), batch items at strides xbs / ybs (even). Used only when the C-ABI input cannot be read
+// through a tensor map (odd row length or a base not 16-byte aligned: a TMA box starts on a
+// 16-byte boundary and strides are multiples of 16 B). HBM streaming, 16 B per element: each
+// thread writes output pairs with 16-byte stores, four independent pairs in flight.
 // ---------------------------------------------------------------------------------------------
-namespace fdp {
 namespace {
 __global__ void pad_rows_kernel(const double* __restrict__ x, long long xbs, double* __restrict__ y,
                                 long long ybs, int n1, int n1p, long long rows, long long batch) {
-  const long long per = rows * n1p, total = per * batch;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const long long b = i / per, j = i - b * per;
-    const long long r = j / n1p;
-    const int c = (int)(j - r * n1p);
-    y[b * ybs + j] = c < n1 ? x[b * xbs + r * n1 + c] : 0.0;
+  const long long pairs_item = rows * n1p / 2, total = pairs_item * batch;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < total; i0 += 4 * stride) {
+    double v[4][2];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long i = i0 + u * stride;
+      v[u][0] = v[u][1] = 0.0;
+      if (i < total) {
+        const long long b = i / pairs_item, j = 2 * (i - b * pairs_item);
+        const long long r = j / n1p;
+        const int c = (int)(j - r * n1p);
+        const double* src = x + b * xbs + r * n1 + c;
+        v[u][0] = c < n1 ? __ldg(src) : 0.0;
+        v[u][1] = c + 1 < n1 ? __ldg(src + 1) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long i = i0 + u * stride;
+      if (i < total) {
+        const long long b = i / pairs_item, j = 2 * (i - b * pairs_item);
+        *reinterpret_cast<double2*>(y + b * ybs + j) = make_double2(v[u][0], v[u][1]);
+      }
+    }
   }
 }
 }  // namespace
 
 cudaError_t launch_pad_rows(const double* x, long long xbs, double* y, long long ybs, int n1,
                             int n1p, long long rows, long long batch, cudaStream_t s) {
-  const long long total = rows * n1p * batch;
+  const long long total = rows * n1p / 2 * batch;
   if (total == 0) return cudaSuccess;
+  if ((n1p & 1) || (ybs & 1) || (reinterpret_cast<uintptr_t>(y) & 15)) return cudaErrorInvalidValue;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int blocks = (int)std::min<long long>((total + 255) / 256, (long long)sms * 8);
+  const int blocks = (int)std::min<long long>((total + 1023) / 1024, (long long)sms * 8);
   pad_rows_kernel<<<blocks, 256, 0, s>>>(x, xbs, y, ybs, n1, n1p, rows, batch);
   return cudaGetLastError();
 }
-}  // namespace fdp
 
+}  // namespace fdp

@@ -15,6 +15,15 @@ constexpr int kTmaMaxNT = 9;           // n8 tiles per role and column tile
 constexpr int kTmaWChunk = 4 * 5 * 32 * 2;  // doubles of one role's W chunk per stage
 constexpr int kTmaMaxProbs = 4;
 
+// The last (partial) K stage of a non-KMAJ problem takes the natural k order k = 4 j + c (one k4
+// step per 4 valid k) instead of the bank-conflict-free order k = 8 (j >> 1) + 2 c + (j & 1)
+// (one k4 step pair per 8) when that saves a k4 step: valid k in the stage (rem = ne - 16 (KS - 1))
+// of 1-4 or 9-12. KMAJ stages always use the natural order.
+inline __host__ __device__ bool tma_last_nat(int ne, bool kmaj) {
+  const int rem = ne - kTmaBK * ((ne + kTmaBK - 1) / kTmaBK - 1);
+  return !kmaj && ((rem - 1) & 7) < 4;
+}
+
 // One folded transform problem of a grouped launch.
 //   A operand (read by TMA through map[i]):
 //     KMAJ (mode 1): 3-D map {n (k, contiguous), Q (rows, stride xld), batch (stride xbs)},
@@ -51,8 +60,6 @@ struct TmaGroup {
   int total_tiles;
   int ct_uniform;  // column tiles of every problem when equal (grid a multiple of it), else 0
   int lam_elems;   // doubles of staged Lambda factors (0: none)
-  int dbg;         // timing experiments of the -DFDP_K1T_PROF build (FDP_K1T_DBG)
-  int stagger_ns;  // start delay of the odd CTA groups (FDP_K1T_STAGGER, experiment)
 };
 
 cudaError_t launch_mode_tma(const TmaGroup& g, bool kmaj, int fold, int grid, cudaStream_t s);

@@ -75,64 +75,101 @@ class BlockPlan:
         return n1 * n2 * self.z[0]
 
 
-class SlabBlockPrecond:
-    """P_D^{-1} with every block slab-decomposed over a torch.distributed process group.
+def nccl_comm(group=None, device: int = 0):
+    """A libfdp NCCL communicator over a torch.distributed group (fdp_comm_init): rank 0 of the
+    group draws the ncclUniqueId (fdp_nccl_unique_id), the group broadcasts its 128 bytes
+    (torch.distributed is plumbing here), every rank initialises. Returns the fdp_comm handle."""
+    import ctypes
 
-    The local vector layout is [u_1 z-slab | ... | u_D z-slab | p z-slab]. D = 3 only."""
+    import torch.distributed as dist
+    from . import _check, lib
+
+    G, g = dist.get_world_size(group), dist.get_rank(group)
+    uid = ctypes.create_string_buffer(128)
+    if g == 0:
+        _check(lib.fdp_nccl_unique_id(uid))
+    box = [uid.raw if g == 0 else None]
+    dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                               group=group)
+    uid = ctypes.create_string_buffer(box[0], 128)
+    c = ctypes.c_void_p()
+    _check(lib.fdp_comm_init(G, g, uid, device, ctypes.byref(c)))
+    return c
+
+
+class SlabBlockPrecond:
+    """P_D^{-1} (or (P_D^G)^{-1} with the block's own scalings) with every block slab-decomposed
+    over a torch.distributed process group, exchanges through libfdp's NCCL communicator
+    (fdp_comm_init + block_precond_apply_sharded: all blocks' phases as grouped launches, one
+    grouped NCCL send/recv all-to-all per exchange). The local vector layout is
+    [u_1 z-slab | ... | u_D z-slab | p z-slab]. D = 3 only."""
 
     def __init__(self, block, group=None):
         import torch
         import torch.distributed as dist
-        from . import fd_apply_slab, kron_mass_apply_slab  # noqa: F401
+        from . import lib
 
         self.torch = torch
-        self.dist = dist
         self.group = group
         self.G = dist.get_world_size(group)
         self.g = dist.get_rank(group)
         self.block = block
         self.fds = block.fds
         self.mass = block.mass
-        dev = f"cuda:{block.device}"
         self.plans = [BlockPlan(tuple(f.dims), self.G, self.g) for f in self.fds]
         self.plans.append(BlockPlan(tuple(self.mass.dims), self.G, self.g))
         self.local_sizes = [p.zslab_size for p in self.plans]
         self.local_off = np.concatenate([[0], np.cumsum(self.local_sizes)]).astype(np.int64)
         self.local_n = int(self.local_off[-1])
-        zs = lambda p: torch.empty(p.zslab_size, dtype=torch.float64, device=dev)
-        ys = lambda p: torch.empty(p.yslab_size, dtype=torch.float64, device=dev)
-        self.send = [zs(p) for p in self.plans]
-        self.ybuf = [ys(p) for p in self.plans]
-        self.recv = [zs(p) for p in self.plans]
-        from . import lib
-        wsb = [lib.fd_slab_workspace_bytes(f.h, self.G, self.g) for f in self.fds]
-        wsb.append(lib.kron_mass_slab_workspace_bytes(self.mass.h, self.G, self.g))
-        self.ws = torch.empty(max(wsb) // 8 + 1, dtype=torch.float64, device=dev)
+        assert self.local_n == int(lib.block_precond_sharded_size(block.h, self.G, self.g))
+        self.comm = nccl_comm(group, block.device)
+        wsb = int(lib.block_precond_sharded_workspace_bytes(block.h, self.comm))
+        self.ws = torch.empty(wsb // 8 + 1, dtype=torch.float64, device=f"cuda:{block.device}")
 
-    def _exchange(self, k, src, dst, splits):
-        send, recv = splits
-        self.dist.all_to_all_single(dst, src, output_split_sizes=recv, input_split_sizes=send,
-                                    group=self.group)
-
-    def apply(self, r, s, dscale_vel=None, dscale_pres=None, stream=None):
-        from . import fd_apply_slab, kron_mass_apply_slab
-        G, g = self.G, self.g
-        o = self.local_off
-        nk = len(self.fds)
-        for k, f in enumerate(self.fds):
-            fd_apply_slab(f, 0, G, g, r[o[k]:o[k + 1]], self.send[k], None, self.ws, stream)
-        kron_mass_apply_slab(self.mass, 0, G, g, r[o[nk]:o[nk + 1]], self.send[nk], None, self.ws, stream)
-        for k, p in enumerate(self.plans):
-            self._exchange(k, self.send[k], self.ybuf[k], p.ex1_splits())
-        for k, f in enumerate(self.fds):
-            fd_apply_slab(f, 1, G, g, self.ybuf[k], self.ybuf[k], None, self.ws, stream)
-        kron_mass_apply_slab(self.mass, 1, G, g, self.ybuf[nk], self.ybuf[nk], None, None, stream)
-        for k, p in enumerate(self.plans):
-            self._exchange(k, self.ybuf[k], self.recv[k], p.ex2_splits())
-        for k, f in enumerate(self.fds):
-            fd_apply_slab(f, 2, G, g, self.recv[k], s[o[k]:o[k + 1]], None, self.ws, stream)
-        kron_mass_apply_slab(self.mass, 2, G, g, self.recv[nk], s[o[nk]:o[nk + 1]], None, None, stream)
+    def apply(self, r, s, stream=None):
+        from . import _check, _dev, _stream, lib
+        _check(lib.block_precond_apply_sharded(self.block.h, self.comm, _dev(r, "r", self.local_n),
+                                               _dev(s, "s", self.local_n), _dev(self.ws, "workspace"),
+                                               _stream(stream)))
         return s
+
+    def close(self):
+        from . import lib
+        if getattr(self, "comm", None):
+            lib.fdp_comm_destroy(self.comm)
+            self.comm = None
+
+
+class ShardedFD:
+    """One FD solve slab-decomposed over a process group (fd_apply_sharded, NCCL communicator):
+    x = D^{-1/2} U Lambda^{-1} U^T D^{-1/2} b on this rank's z-slab (planes
+    slab_range(n3, G, g) of the vec-ordered tensor)."""
+
+    def __init__(self, fd, group=None):
+        import torch
+        import torch.distributed as dist
+        from . import lib
+
+        self.fd = fd
+        self.G, self.g = dist.get_world_size(group), dist.get_rank(group)
+        self.plan = BlockPlan(tuple(fd.dims), self.G, self.g)
+        self.local_n = self.plan.zslab_size
+        self.comm = nccl_comm(group, fd.device)
+        wsb = int(lib.fd_sharded_workspace_bytes(fd.h, self.comm))
+        self.ws = torch.empty(wsb // 8 + 1, dtype=torch.float64, device=f"cuda:{fd.device}")
+
+    def apply(self, b, x, dscale=None, stream=None):
+        from . import _check, _dev, _stream, lib
+        _check(lib.fd_apply_sharded(self.fd.h, self.comm, _dev(b, "b", self.local_n), _dev(x, "x", self.local_n),
+                                    None if dscale is None else _dev(dscale, "dscale", self.local_n),
+                                    _dev(self.ws, "workspace"), _stream(stream)))
+        return x
+
+    def close(self):
+        from . import lib
+        if getattr(self, "comm", None):
+            lib.fdp_comm_destroy(self.comm)
+            self.comm = None
 
 
 def emulate_slab_apply(block, r_full, G: int):

@@ -126,6 +126,51 @@ def _sharded_fd(rank, world):
     return float(np.max(np.abs(X - ref)) / np.max(np.abs(ref)))
 
 
+def _exchange_roundtrip_libfdp(rank, world):
+    """The exchange plan of libfdp's NCCL sharded apply (fdp_slab_exchange_counts: the per-peer
+    counts its grouped ncclSend / ncclRecv use, pieces at cumulative offsets) driven through real
+    all-to-alls: exchange 1 must deliver exactly the y-slab, exchange 2 the packed z-slab back."""
+    import paper_1712_00403_b200 as fdp
+    ok = True
+    for dims in ((5, 7, 9), (4, 3, 10), (6, 11, 2)):
+        full = np.random.default_rng(sum(dims)).standard_normal(int(np.prod(dims)))
+        T = full.reshape(dims, order="F")
+        plan = fdist.BlockPlan(dims, world, rank)
+        z0, nz = plan.z
+        y0, ny = plan.y
+        zslab = np.reshape(T[:, :, z0:z0 + nz], -1, order="F")
+        s1, r1 = fdp.slab_exchange_counts(dims, world, rank, 1)
+        s2, r2 = fdp.slab_exchange_counts(dims, world, rank, 2)
+        ybuf = torch.empty(sum(r1), dtype=torch.float64)
+        dist.all_to_all_single(ybuf, torch.from_numpy(_pack(zslab, plan)), output_split_sizes=r1,
+                               input_split_sizes=s1)
+        ok = ok and np.array_equal(ybuf.numpy(), np.reshape(T[:, y0:y0 + ny, :], -1, order="F"))
+        back = torch.empty(sum(r2), dtype=torch.float64)
+        dist.all_to_all_single(back, ybuf, output_split_sizes=r2, input_split_sizes=s2)
+        ok = ok and np.array_equal(_unpack(back.numpy(), plan), zslab)
+    return bool(ok)
+
+
+def test_libfdp_exchange_counts_roundtrip_gloo():
+    for world in (2, 3):
+        res = _run(_exchange_roundtrip_libfdp, world)
+        assert res == {r: True for r in range(world)}, res
+
+
+@pytest.mark.parametrize("dims", [(5, 7, 9), (515, 516, 516), (133, 133, 133), (3, 2, 1)])
+@pytest.mark.parametrize("G", [1, 2, 3, 8])
+def test_libfdp_exchange_counts_match_plan(dims, G):
+    """fdp_slab_exchange_counts agrees with the Python BlockPlan for every rank, and exchange 2 is
+    exchange 1 reversed; the counts conserve the z-slab and the y-slab."""
+    import paper_1712_00403_b200 as fdp
+    for g in range(G):
+        plan = fdist.BlockPlan(dims, G, g)
+        s1, r1 = fdp.slab_exchange_counts(dims, G, g, 1)
+        s2, r2 = fdp.slab_exchange_counts(dims, G, g, 2)
+        assert (s1, r1) == tuple(plan.ex1_splits()) and (s2, r2) == tuple(plan.ex2_splits())
+        assert sum(s1) == plan.zslab_size and sum(r1) == plan.yslab_size
+
+
 def test_slab_exchange_roundtrip_gloo():
     res = _run(_exchange_roundtrip)
     assert res == {0: True, 1: True}

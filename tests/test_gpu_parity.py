@@ -367,9 +367,12 @@ def test_slab_decomposed_config3_size(env, monkeypatch):
 
 
 def test_slab_block_precond_nccl_single_rank():
-    """SlabBlockPrecond through a real NCCL process group (world size 1 on this box: the
-    all-to-all exchanges degenerate to device copies; multi-rank exchange logic is covered by
-    tests/test_dist_cpu.py and the emulated-rank tests above)."""
+    """SlabBlockPrecond through libfdp's NCCL communicator (fdp_nccl_unique_id broadcast over a
+    torch.distributed group, fdp_comm_init, block_precond_apply_sharded: grouped phases, one
+    grouped ncclSend/ncclRecv all-to-all per exchange). World size 1 on this box: the exchanges
+    are NCCL self send/recv; multi-rank exchange counts are covered by tests/test_dist_cpu.py and
+    the slab phases by the emulated-rank tests. Repeated, inside a CUDA graph, and with the
+    block's P^G scalings (config 3, D_V = nu, D_Q = 1/nu)."""
     import os
     import socket
     import torch.distributed as tdist
@@ -381,22 +384,67 @@ def test_slab_block_precond_nccl_single_rank():
     os.environ.update({"MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
     created = False
     if not tdist.is_initialized():
-        tdist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+        tdist.init_process_group("gloo", rank=0, world_size=1)
         created = True
     try:
         w, od, gd = _both(3)
         P = fdp.build_block(gd)
         SB = fdist.SlabBlockPrecond(P)
         assert SB.local_n == od.n_total
-        r = synth.rhs(w.seed, od.n_total, 1)[0]
-        rt = dev(r)
-        st = torch.empty_like(rt)
-        SB.apply(rt, st)
-        ref = oprec.BlockPrecond(od).apply(r)
-        assert rel(st.cpu().numpy(), ref) < TOL
+        ref = oprec.BlockPrecond(od)
+        rng = np.random.default_rng(9)
+        for _ in range(2):
+            r = rng.standard_normal(od.n_total)
+            rt = dev(r)
+            st = torch.empty_like(rt)
+            SB.apply(rt, st)
+            assert rel(st.cpu().numpy(), ref.apply(r)) < TOL
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            SB.apply(rt, st)
+        r = rng.standard_normal(od.n_total)
+        rt.copy_(dev(r))
+        g.replay()
+        torch.cuda.synchronize()
+        assert rel(st.cpu().numpy(), ref.apply(r)) < TOL
+        del g  # a graph holding NCCL work must go before its communicator (ncclCommDestroy waits)
+        torch.cuda.synchronize()
+        SB.close()
+        dv, dq = ospaces.nu_scalings(od, synth.viscosity)
+        PG = fdp.build_block(gd, dscale_vel=dv, dscale_pres=dq)
+        SG = fdist.SlabBlockPrecond(PG)
+        SG.apply(rt, st)
+        assert rel(st.cpu().numpy(), oprec.BlockPrecond(od, dv, dq).apply(r)) < TOL
+        SG.close()
+        # one FD solve through fd_apply_sharded, with a D scaling
+        comp = od.comps[1]
+        F = fdp.FD(gd.Ks[1], gd.Ms[1], gd.coef[1])
+        SF = fdist.ShardedFD(F)
+        N = int(np.prod(F.dims))
+        b = rng.standard_normal(N)
+        dsc = rng.uniform(0.5, 1.5, N)
+        x = SF.apply(dev(b), torch.empty(N, dtype=torch.float64, device="cuda"),
+                     dscale=dev(1.0 / np.sqrt(dsc))).cpu().numpy()
+        xr = ofd.scaled_apply(ofd.FDSolver(comp.Ks, comp.Ms, comp.coef), b, dsc)
+        assert rel(x, xr) < TOL and relmax(x, xr) < TOL
+        SF.close()
     finally:
         if created:
             tdist.destroy_process_group()
+
+
+def test_sharded_errors():
+    """A peer-store communicator cannot serve fd_apply_sharded; bad communicator arguments are
+    reported, not crashed on."""
+    import ctypes
+    rng = np.random.default_rng(3)
+    F = fdp.FD([_rand_spd(n, rng, 1.0) for n in (9, 8, 7)], [_rand_spd(n, rng, 2.0) for n in (9, 8, 7)],
+               (1.0, 1.0, 1.0))
+    c = ctypes.c_void_p()
+    uid = ctypes.create_string_buffer(128)
+    assert fdp.lib.fdp_comm_init(1, 1, uid, 0, ctypes.byref(c)) == 1   # rank >= nranks
+    assert fdp.lib.fdp_comm_init(1, 0, None, 0, ctypes.byref(c)) == 1
+    assert fdp.lib.fd_sharded_workspace_bytes(F.h, None) == 0
 
 
 @pytest.mark.parametrize("G", [1, 2, 3, 5, 8])
