@@ -21,7 +21,17 @@ build/%.o: $(SRC)/%.cpp $(HDR)
 $(LIB): $(OBJ)
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJ) -ldl
 
-clean:
-	rm -rf build $(LIB)
+# diagnostic library (K1t per-role clock64 totals, fdp_k1t_prof_read); load with
+# FDP_LIB_PATH=paper_1712_00403_b200/libfdp_prof.so
+PROFLIB := $(PKG)/libfdp_prof.so
+prof: $(PROFLIB)
+build/prof_mode_tma.o: $(SRC)/kernels/mode_tma.cu $(HDR)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -DFDP_K1T_PROF -c $< -o $@
+$(PROFLIB): build/prof_mode_tma.o $(filter-out build/mode_tma.o,$(OBJ))
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^ -ldl
 
-.PHONY: all clean
+clean:
+	rm -rf build $(LIB) $(PROFLIB)
+
+.PHONY: all clean prof

@@ -126,6 +126,7 @@ static void free_fd(fdp_fd h) {
     cudaFree(h->WtF[d]);
     cudaFree(h->WtB[d]);
   }
+  cudaFree(h->rlam);
   cudaFree(h->ws);
   delete h;
 }
@@ -302,6 +303,19 @@ extern "C" fdp_status fd_setup(int D, const int32_t* n, const double* const* K,
         return cuda_fail(e, "fd_setup: upload");
       }
     }
+    if (raw->fold[D - 1] == 2 && D >= 2) {
+      // the Lambda pass on K1t multiplies by a stored 1 / Lambda (DESIGN.md §5 "K1t", C-11)
+      const int n1p = n1pad(raw), nmid = D == 3 ? raw->n[1] : 1;
+      fdp_status st = dalloc(&raw->rlam, (size_t)n1p * nmid * raw->n[D - 1]);
+      cudaError_t e = st ? cudaSuccess
+                         : launch_rlam(raw->rlam, raw->lamcF[0], D == 3 ? raw->lamcF[1] : nullptr, raw->lamcF[D - 1],
+                                       n1p, raw->n[0], nmid, raw->n[D - 1], nullptr);
+      if (!st && e == cudaSuccess) e = cudaDeviceSynchronize();
+      if (st || e != cudaSuccess) {
+        free_fd(raw);
+        return st ? st : cuda_fail(e, "fd_setup: 1/Lambda");
+      }
+    }
     if (max_batch > 0) {
       fdp_status st = dalloc(&raw->ws, (size_t)(2 * max_batch * Npad(raw) + kWsSlack));
       if (st) {
@@ -434,6 +448,7 @@ static ModeProb make_mode_prob(const fdp_fd_s* h, int d, bool fwd, const double*
     p.lam0 = h->lamcF[0];
     p.lam1 = h->D == 3 ? h->lamcF[1] : nullptr;
     p.lamcol = h->lamcF[h->D - 1];
+    if (epi == EPI_LAMBDA && d == h->D - 1 && yld == n1p) p.rlam = h->rlam;
   }
   const int BM = kK1Warps * 8 * h->cfg[d].MT;
   const long long M = P * Q * batch;

@@ -168,6 +168,9 @@ struct fdp_fd_s {
   // K1t fragment-native chunks of the folded forward / backward matrices (fold[d] == 2)
   double* WtF[3] = {nullptr, nullptr, nullptr};
   double* WtB[3] = {nullptr, nullptr, nullptr};
+  // 1 / Lambda in the output layout of the Lambda pass (padded rows n1p, last mode's folded
+  // spectral order; 0 at pad rows), when that pass runs on K1t (fold[D-1] == 2)
+  double* rlam = nullptr;
   double* ws = nullptr;
   int64_t ws_batch = 0;
 };
@@ -276,6 +279,10 @@ std::vector<double> tma_wt_build(int n, int foldh, int ldw, const std::vector<do
 bool tma_eligible(const ModeProb& p, bool kmaj);
 bool tma_input_ok(const ModeProb& p, bool kmaj);
 cudaError_t launch_tma_stage(const ModeProb* probs, int count, bool kmaj, cudaStream_t s);
+// rlam[p + P a] = 1 / (lam0[p % n1p] + lam1[p / n1p] + lamcol[a]) (lam1 NULL: no middle term), 0 for
+// p % n1p >= n1v; P = n1p * n_mid
+cudaError_t launch_rlam(double* rlam, const double* lam0, const double* lam1, const double* lamcol, int n1p,
+                        int n1v, int n_mid, int n_last, cudaStream_t s);
 cudaError_t launch_pad_rows(const double* x, long long xbs, double* y, long long ybs, int n1,
                             int n1p, long long rows, long long batch, cudaStream_t s);
 }  // namespace fdp

@@ -117,6 +117,7 @@ cudaError_t launch_tma_stage(const ModeProb* probs, int count, bool kmaj, cudaSt
     t.lam0 = m.lam0;
     t.lam1 = m.lam1;
     t.lamcol = m.lamcol;
+    t.rlam = m.rlam;
     t.ybs = m.ybs;
     t.n = m.n;
     t.ne = (m.n + 1) / 2;
@@ -177,7 +178,7 @@ cudaError_t launch_tma_stage(const ModeProb* probs, int count, bool kmaj, cudaSt
               promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     }
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-    if (m.epi == EPI_LAMBDA) {  // Lambda factors staged in shared memory: lam0 (n1), lam1 (P / n1), lamcol (n)
+    if (m.epi == EPI_LAMBDA && !m.rlam) {  // Lambda factors staged in shared memory: lam0 (n1), lam1 (P / n1), lamcol (n)
       t.lam_off = g.lam_elems;
       t.lam1_n = m.lam1 ? m.P / m.n1 : 0;
       g.lam_elems += m.n1 + t.lam1_n + m.n;
@@ -192,6 +193,7 @@ cudaError_t launch_tma_stage(const ModeProb* probs, int count, bool kmaj, cudaSt
     if (g.prob[i].ctiles != g.ct_uniform) g.ct_uniform = 0;
   int grid = std::min(tiles, kTmaCtasPerSM * num_sms());
   if (g.ct_uniform > 0) grid = std::max(g.ct_uniform, grid / g.ct_uniform * g.ct_uniform);
+  g.prof_slot = (int)(g_k1_launches[1].load() & 7);
   ++g_k1_launches[1];
   return launch_mode_tma(g, kmaj, fold, grid, s);
 }

@@ -42,6 +42,7 @@ struct ModeProb {
   const double* lam0;     // EPI_LAMBDA: coef-scaled eigenvalues c_d*lambda_d, d = 1 (index i1)
   const double* lam1;     //             d = 2 (3D only; nullptr in 2D)
   const double* lamcol;   //             d = D (the contracted, last direction)
+  const double* rlam;     // EPI_LAMBDA on K1t: 1 / Lambda in the output layout of one item, or NULL
   long long N;            // elements per batch item (of this tensor)
   long long xbs, ybs;     // batch-item strides of X and Y (elements)
   int P, n, Q;            // per item; GEMM rows M = P * Q * batch; n = contracted extent

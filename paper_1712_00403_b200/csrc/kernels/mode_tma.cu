@@ -135,6 +135,23 @@ __device__ __forceinline__ void named_bar(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
+// Diagnostic build only (-DFDP_K1T_PROF, `make prof` -> libfdp_prof.so): clock64 totals per
+// warp role, summed over CTAs: [0] consumer wait on "full", [1] consumer wait on the staging
+// buffer, [2] consumer total, [3] store wait on a staged tile, [4] store total, [5] producer wait
+// on "empty", [6] producer total, [7] tiles (consumer warp 0).
+#ifdef FDP_K1T_PROF
+__device__ unsigned long long g_k1t_prof[8 * 8];
+#define FDP_PT(v) long long v = clock64()
+#define FDP_PACC(acc, t0) acc += clock64() - (t0)
+#define FDP_PEND(v) v = clock64() - v
+#define FDP_PFLUSH(slot, v) if (lane == 0) atomicAdd(&g_k1t_prof[8 * g.prof_slot + (slot)], (unsigned long long)(v))
+#else
+#define FDP_PT(v)
+#define FDP_PACC(acc, t0)
+#define FDP_PEND(v)
+#define FDP_PFLUSH(slot, v)
+#endif
+
 struct Tile {
   int pi, ct, tp, tq, b;
 };
@@ -219,12 +236,17 @@ __device__ __noinline__ void producer_loop(const TmaGroup& g, unsigned sbase, un
                  : "memory");
   int slot = 0;
   unsigned phase = 0;
+  const int lane = 0;
+  long long pw = 0;
+  FDP_PT(ptot);
   for (int it = 0;; ++it) {
     const int tau = tile_of(g, it);
     if (tau < 0) break;
     const int kst = g.prob[decode(g, tau, KMAJ).pi].kst;
     for (int s = 0; s < kst; ++s) {
+      FDP_PT(t0);
       mbar_wait(bar_empty + 8 * slot, phase ^ 1);
+      FDP_PACC(pw, t0);
       issue_stage<KMAJ, FOLD>(g, sbase, bar_full, slot, it, s);
       if (++slot == STAGES) {
         slot = 0;
@@ -232,6 +254,11 @@ __device__ __noinline__ void producer_loop(const TmaGroup& g, unsigned sbase, un
       }
     }
   }
+  FDP_PFLUSH(5, pw);
+  FDP_PEND(ptot);
+  FDP_PFLUSH(6, ptot);
+  (void)pw;
+  (void)lane;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -316,13 +343,16 @@ __device__ __forceinline__ void stage_mma(double (&acc)[kMT][9][2], int nt, unsi
 template <bool KMAJ, int FOLD, int STAGES, int NTV, int ODD>
 __device__ __forceinline__ void kloop(const TmaGroup& g, double (&acc)[kMT][9][2], int nt, int kst, int ne,
                                       unsigned sbase, unsigned bar_full, unsigned bar_empty, int& stage,
-                                      unsigned& phase, const Frag& f, int role, int wm, int fr, int fc, int lane) {
+                                      unsigned& phase, const Frag& f, int role, int wm, int fr, int fc, int lane,
+                                      long long& wfull) {
   const double sgn = role ? -1.0 : 1.0;  // FWD: E warps form s = x + Jx, O warps d = x - Jx
   const int rem = ne - (kst - 1) * kTmaBK;  // valid k of the last stage (1 .. 16)
   const bool nat = tma_last_nat(ne, KMAJ);
   const int jlast = KMAJ || nat ? (rem + 3) >> 2 : (rem <= 8 ? 2 : 4);
   for (int s = 0; s < kst; ++s) {
+    FDP_PT(t0);
     mbar_wait(bar_full + 8 * stage, phase);
+    FDP_PACC(wfull, t0);
     const unsigned A0 = sbase + stage * kStageBytes;
     const unsigned A1 = A0 + kABytes;
     const unsigned B = A1 + kABytes + role * kBBytes;
@@ -364,6 +394,8 @@ template <bool KMAJ, int FOLD>
 __device__ __noinline__ void store_loop(const TmaGroup& g, unsigned cbuf, unsigned bar_cfull,
                                         unsigned bar_cempty, double* lsm, int lane, int sw) {
   const unsigned lsa = smem_u32(lsm);
+  long long sw_wait = 0;
+  FDP_PT(stot);
   if (FOLD == FOLD_FWD && !KMAJ && g.lam_elems > 0) {
     // stage the Lambda factors of every EPI_LAMBDA problem: [lam0 (n1v of n1) | lam1 | lamcol]
     for (int pi = 0; pi < g.count; ++pi) {
@@ -390,7 +422,15 @@ __device__ __noinline__ void store_loop(const TmaGroup& g, unsigned cbuf, unsign
     const int ncol = 8 * nt;
     double* __restrict__ Y = p.Y;
     const int ne = p.ne, no = p.no, n = p.n;
+    FDP_PT(t0);
     mbar_wait(bar_cfull, phase);
+    FDP_PACC(sw_wait, t0);
+    // Every path gathers a chunk of U columns / elements from shared (and global, for D^{-1/2})
+    // memory first, then does the arithmetic, then stores: the store warps' FP64 work queues
+    // behind the consumers' DMMAs on the shared FP64 datapath, so a dependent load -> divide ->
+    // store chain per column (~600 cycles) made them the bottleneck of the short-K passes;
+    // independent chains across the chunk hide that latency. Out-of-range entries read a clamped
+    // (valid) address and are not stored.
     if (!KMAJ) {
       // lane l: rows R = 2l, 2l + 1 (same p-group, consecutive p; P is even so both exist or not)
       const long long P = p.P;
@@ -403,76 +443,133 @@ __device__ __noinline__ void store_loop(const TmaGroup& g, unsigned cbuf, unsign
       if (valid && FOLD == FOLD_FWD) {
         // Algorithm 1 step 3 on the way out (EPI_LAMBDA): q~ = t~ / (lrow(p) +
         // lamcol(a)), Lambda formed from its factors; the padding rows i1 >= n1v of a padded
-        // intermediate stay exactly 0. Off the consumers' path: the division's MUFU / FP64 work
-        // overlaps the next tile's DMMAs (in the consumers it idled the DMMA pipe ~5k cycles a tile)
-        const bool lam = p.epi == EPI_LAMBDA;
-        double lr[2] = {0.0, 0.0};
-        bool zr[2] = {false, false};
+        // intermediate stay exactly 0
+        // with a stored 1 / Lambda table (rlam, the block / FD path): one DMUL per element, its
+        // loads coalesced like the stores; otherwise (slab phases) the on-the-fly division
+        const bool tab = p.epi == EPI_LAMBDA && p.rlam != nullptr;
+        const bool lam = p.epi == EPI_LAMBDA && !tab;
+        const double* rl = tab ? p.rlam + sidx : nullptr;
+        double lr0 = 0.0, lr1 = 0.0;
+        bool zr0 = false, zr1 = false;
         if (lam) {
           const unsigned L = lsa + 8u * (unsigned)p.lam_off;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int ppx = pp + h, i1 = ppx % p.n1;
-            zr[h] = i1 >= p.n1v;
-            if (!zr[h]) lr[h] = p.lam1 ? lds_f64(L + 8u * i1) + lds_f64(L + 8u * (p.n1 + ppx / p.n1)) : lds_f64(L + 8u * ppx);
+          const int i10 = pp % p.n1, i11 = (pp + 1) % p.n1;
+          zr0 = i10 >= p.n1v;
+          zr1 = i11 >= p.n1v;
+          if (p.lam1) {
+            lr0 = lds_f64(L + 8u * (zr0 ? 0 : i10)) + lds_f64(L + 8u * (p.n1 + pp / p.n1));
+            lr1 = lds_f64(L + 8u * (zr1 ? 0 : i11)) + lds_f64(L + 8u * (p.n1 + (pp + 1) / p.n1));
+          } else {
+            lr0 = lds_f64(L + 8u * (zr0 ? 0 : pp));
+            lr1 = lds_f64(L + 8u * (zr1 ? 0 : pp + 1));
           }
         }
         const unsigned Lc = lsa + 8u * (unsigned)(p.lam_off + p.n1 + p.lam1_n);
-#pragma unroll 4
-        for (int w = sw; w < 2 * ncol; w += kStoreWarps) {
-          // (half, column) pairs dealt over the store warps: h = 0 E, 1 O
-          const int h = w >= ncol, c = w - h * ncol;
-          const int a = c0 + c;
-          if (a < (h ? no : ne)) {
-            const int oc = (h ? ne : 0) + a;
-            double v0, v1;
-            lds128(cbuf + (unsigned)((72 * h + c) * kCLdN + R) * 8u, v0, v1);
-            if (lam) {
-              const double lc = lds_f64(Lc + 8u * oc);
-              v0 = zr[0] ? 0.0 : fdp_div(v0, lr[0] + lc);
-              v1 = zr[1] ? 0.0 : fdp_div(v1, lr[1] + lc);
+        constexpr int U = 6;
+        const int total = 2 * ncol;  // (half, column) pairs dealt over the store warps: h = 0 E, 1 O
+        for (int w0 = sw; w0 < total; w0 += U * kStoreWarps) {
+          double v[U][2], lc[U], rv[U][2];
+          int oc[U];
+          bool ok[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int w = w0 + u * kStoreWarps;
+            const int h = w >= ncol, c = w - h * ncol, a = c0 + c;
+            ok[u] = w < total && a < (h ? no : ne);
+            oc[u] = ok[u] ? (h ? ne : 0) + a : 0;
+            lds128(cbuf + (unsigned)((ok[u] ? 72 * h + c : 0) * kCLdN + R) * 8u, v[u][0], v[u][1]);
+            lc[u] = lam ? lds_f64(Lc + 8u * oc[u]) : 0.0;
+            if (tab) {
+              const double2 r2 = __ldg(reinterpret_cast<const double2*>(rl + P * oc[u]));
+              rv[u][0] = r2.x;
+              rv[u][1] = r2.y;
             }
-            *reinterpret_cast<double2*>(yrow + P * oc) = make_double2(v0, v1);
           }
+          if (tab) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              v[u][0] *= rv[u][0];
+              v[u][1] *= rv[u][1];
+            }
+          } else if (lam) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              v[u][0] = zr0 ? 0.0 : fdp_div(v[u][0], lr0 + lc[u]);
+              v[u][1] = zr1 ? 0.0 : fdp_div(v[u][1], lr1 + lc[u]);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (ok[u]) *reinterpret_cast<double2*>(yrow + P * oc[u]) = make_double2(v[u][0], v[u][1]);
         }
       } else if (valid) {
-        for (int w = sw; w < ncol; w += kStoreWarps) {
-          {
-            const int c = w, cc = c0 + c;
-            if (cc < ne) {
-              double e0, e1, o0, o1;
-              lds128(cbuf + (unsigned)(c * kCLdN + R) * 8u, e0, e1);
-              lds128(cbuf + (unsigned)((72 + c) * kCLdN + R) * 8u, o0, o1);
-              double x0 = e0 + o0, x1 = e1 + o1, y0 = e0 - o0, y1 = e1 - o1;
-              const int cm = n - 1 - cc;
-              if (p.epi == EPI_SCALE) {
-                const double2 s0 = *reinterpret_cast<const double2*>(p.scale + sidx + P * cc);
-                const double2 s1 = *reinterpret_cast<const double2*>(p.scale + sidx + P * cm);
-                x0 *= s0.x; x1 *= s0.y; y0 *= s1.x; y1 *= s1.y;
-              }
-              *reinterpret_cast<double2*>(yrow + P * cc) = make_double2(x0, x1);
-              if (cm != cc) *reinterpret_cast<double2*>(yrow + P * cm) = make_double2(y0, y1);
+        const bool scl = p.epi == EPI_SCALE;
+        constexpr int U = 4;
+        for (int w0 = sw; w0 < ncol; w0 += U * kStoreWarps) {
+          double e[U][2], o[U][2], s0[U][2], s1[U][2];
+          int cc[U];
+          bool ok[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int w = w0 + u * kStoreWarps;
+            ok[u] = w < ncol && c0 + w < ne;
+            const int c = ok[u] ? w : 0;
+            cc[u] = c0 + c;
+            lds128(cbuf + (unsigned)(c * kCLdN + R) * 8u, e[u][0], e[u][1]);
+            lds128(cbuf + (unsigned)((72 + c) * kCLdN + R) * 8u, o[u][0], o[u][1]);
+            if (scl) {
+              const double2 a0 = __ldg(reinterpret_cast<const double2*>(p.scale + sidx + P * cc[u]));
+              const double2 a1 = __ldg(reinterpret_cast<const double2*>(p.scale + sidx + P * (n - 1 - cc[u])));
+              s0[u][0] = a0.x; s0[u][1] = a0.y; s1[u][0] = a1.x; s1[u][1] = a1.y;
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            double x0 = e[u][0] + o[u][0], x1 = e[u][1] + o[u][1];
+            double y0 = e[u][0] - o[u][0], y1 = e[u][1] - o[u][1];
+            if (scl) {
+              x0 *= s0[u][0]; x1 *= s0[u][1]; y0 *= s1[u][0]; y1 *= s1[u][1];
+            }
+            const int cm = n - 1 - cc[u];
+            if (ok[u]) {
+              *reinterpret_cast<double2*>(yrow + P * cc[u]) = make_double2(x0, x1);
+              if (cm != cc[u]) *reinterpret_cast<double2*>(yrow + P * cm) = make_double2(y0, y1);
             }
           }
         }
       }
-    } else {
-      // (row, column) pairs flattened over the lanes of both store warps; 16-byte stores where
-      // the output column is even (E part; O part when ne is even; BWD when the row is aligned)
+    } else if (FOLD == FOLD_FWD) {
+      // KMAJ FWD (mode 1 forward into a padded intermediate: 16-byte aligned rows): (row, column
+      // pair) elements flattened over the lanes of the store warps, 16-byte stores; the pad
+      // column of a padded row (past the O part) gets 0
       const int pairs = ncol / 2;  // column pairs per half (ncol = 8 nt)
-      const int per_row = FOLD == FOLD_FWD ? 2 * pairs : pairs;
-      for (int e = lane + 32 * sw; e < kTmaBM * per_row; e += 32 * kStoreWarps) {
-        const int R = e / per_row, w = e - R * per_row;
-        const long long q = (long long)t.tq * kTmaBM + R;
-        if (q >= p.Q) continue;
-        const long long sidx = (long long)p.yld * q;
-        double* yrow = Y + sidx + p.ybs * t.b;
-        if (FOLD == FOLD_FWD) {
+      const int per_row = 2 * pairs;
+      const int total = kTmaBM * per_row;
+      constexpr int U = 4;
+      for (int e0 = lane + 32 * sw; e0 < total; e0 += U * 32 * kStoreWarps) {
+        double va[U][2];
+        int Rr[U], ww[U];
+        bool ok[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int e = e0 + u * 32 * kStoreWarps;
+          const int ee = e < total ? e : 0;
+          const int R = ee / per_row, w = ee - R * per_row;
+          Rr[u] = R;
+          ww[u] = w;
+          ok[u] = e < total && (long long)t.tq * kTmaBM + R < p.Q;
+          const int h = w >= pairs, c = 2 * (w - h * pairs);
+          lds128(cbuf + (unsigned)(R * kCLdK + 72 * h + c) * 8u, va[u][0], va[u][1]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (!ok[u]) continue;
+          double* yrow = Y + (long long)p.yld * ((long long)t.tq * kTmaBM + Rr[u]) + p.ybs * t.b;
+          const int w = ww[u];
           const int h = w >= pairs, c = 2 * (w - h * pairs);
           const int a = c0 + c, oc = (h ? ne : 0) + a;
           const int lim = h ? no : ne;
-          double v0, v1;
-          lds128(cbuf + (unsigned)(R * kCLdK + 72 * h + c) * 8u, v0, v1);
+          const double v0 = va[u][0], v1 = va[u][1];
           if (a + 1 < lim && ((reinterpret_cast<unsigned long long>(yrow + oc) & 15) == 0)) {
             *reinterpret_cast<double2*>(yrow + oc) = make_double2(v0, v1);
           } else {
@@ -483,34 +580,47 @@ __device__ __noinline__ void store_loop(const TmaGroup& g, unsigned cbuf, unsign
               else if (h && oc + d < p.yld) yrow[oc + d] = 0.0;  // the pad column of a padded row
             }
           }
-        } else {
-          const int c = 2 * w, cc = c0 + c;
-          double e0, e1, o0, o1;
-          lds128(cbuf + (unsigned)(R * kCLdK + c) * 8u, e0, e1);
-          lds128(cbuf + (unsigned)(R * kCLdK + 72 + c) * 8u, o0, o1);
-          double x0 = e0 + o0, x1 = e1 + o1, y0 = e0 - o0, y1 = e1 - o1;
-          const int cm = n - 1 - cc;  // y_d goes to column cm - d
-          if (p.epi == EPI_SCALE) {
-            x0 *= p.scale[sidx + cc];
-            y0 *= p.scale[sidx + cm];
-            if (cc + 1 < ne) {
-              x1 *= p.scale[sidx + cc + 1];
-              y1 *= p.scale[sidx + cm - 1];
-            }
+        }
+      }
+    } else {
+      // KMAJ BWD (mode 1 backward, usually into the C-ABI layout, whose rows need not be 16-byte
+      // aligned): (row, column pair) elements flattened over the store warps' lanes, the butterfly
+      // x_c = e_c + o_c, x_{n-1-c} = e_c - o_c, 16-byte stores where the pair is aligned. (Chunked
+      // gather / compute / store variants and row-aligned segment copies of this loop measured
+      // 1.2-2.3x slower on configs 4-5.)
+      const int pairs = ncol / 2;
+      for (int e = lane + 32 * sw; e < kTmaBM * pairs; e += 32 * kStoreWarps) {
+        const int R = e / pairs, w = e - R * pairs;
+        const long long q = (long long)t.tq * kTmaBM + R;
+        if (q >= p.Q) continue;
+        const long long sidx = (long long)p.yld * q;
+        double* yrow = Y + sidx + p.ybs * t.b;
+        const int c = 2 * w, cc = c0 + c;
+        double e0, e1, o0, o1;
+        lds128(cbuf + (unsigned)(R * kCLdK + c) * 8u, e0, e1);
+        lds128(cbuf + (unsigned)(R * kCLdK + 72 + c) * 8u, o0, o1);
+        double x0 = e0 + o0, x1 = e1 + o1, y0 = e0 - o0, y1 = e1 - o1;
+        const int cm = n - 1 - cc;  // y_d goes to column cm - d
+        if (p.epi == EPI_SCALE) {
+          x0 *= p.scale[sidx + cc];
+          y0 *= p.scale[sidx + cm];
+          if (cc + 1 < ne) {
+            x1 *= p.scale[sidx + cc + 1];
+            y1 *= p.scale[sidx + cm - 1];
           }
-          if (cc + 1 < ne && (reinterpret_cast<unsigned long long>(yrow + cc) & 15) == 0)
-            *reinterpret_cast<double2*>(yrow + cc) = make_double2(x0, x1);
-          else {
-            if (cc < ne) yrow[cc] = x0;
-            if (cc + 1 < ne) yrow[cc + 1] = x1;
-          }
-          // mirrored pair (cm - 1, cm) = (y1, y0); the middle column of an odd n (cm == cc) is x
-          if (cc + 1 < ne && cm - 1 > cc + 1 && (reinterpret_cast<unsigned long long>(yrow + cm - 1) & 15) == 0)
-            *reinterpret_cast<double2*>(yrow + cm - 1) = make_double2(y1, y0);
-          else {
-            if (cc < ne && cm != cc) yrow[cm] = y0;
-            if (cc + 1 < ne && cm - 1 != cc + 1) yrow[cm - 1] = y1;
-          }
+        }
+        if (cc + 1 < ne && (reinterpret_cast<unsigned long long>(yrow + cc) & 15) == 0)
+          *reinterpret_cast<double2*>(yrow + cc) = make_double2(x0, x1);
+        else {
+          if (cc < ne) yrow[cc] = x0;
+          if (cc + 1 < ne) yrow[cc + 1] = x1;
+        }
+        // mirrored pair (cm - 1, cm) = (y1, y0); the middle column of an odd n (cm == cc) is x
+        if (cc + 1 < ne && cm - 1 > cc + 1 && (reinterpret_cast<unsigned long long>(yrow + cm - 1) & 15) == 0)
+          *reinterpret_cast<double2*>(yrow + cm - 1) = make_double2(y1, y0);
+        else {
+          if (cc < ne && cm != cc) yrow[cm] = y0;
+          if (cc + 1 < ne && cm - 1 != cc + 1) yrow[cm - 1] = y1;
         }
       }
     }
@@ -518,6 +628,10 @@ __device__ __noinline__ void store_loop(const TmaGroup& g, unsigned cbuf, unsign
     if (lane == 0) mbar_arrive(bar_cempty);  // the buffer may take the next tile
     phase ^= 1;
   }
+  FDP_PFLUSH(3, sw_wait);
+  FDP_PEND(stot);
+  FDP_PFLUSH(4, stot);
+  (void)sw_wait;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -559,6 +673,8 @@ __global__ void __launch_bounds__(kThreads, 1) mode_tma_kernel(const __grid_cons
   const int fr = lane >> 2, fc = lane & 3;
   int stage = 0;
   unsigned phase = 0, cphase = 0;
+  long long wfull = 0, wcempty = 0, ntiles = 0;
+  FDP_PT(ctot);
   // per-thread fragment offsets (see Frag)
   Frag f;
 #pragma unroll
@@ -599,7 +715,7 @@ __global__ void __launch_bounds__(kThreads, 1) mode_tma_kernel(const __grid_cons
     // mma.sync costs a WARPSYNC + NOP pair) and, for KMAJ, on the odd-start second A tile
     const int odd = KMAJ ? p.a1odd : 0;
 #define FDP_K1T_RUN(NTV_, ODD_) \
-  kloop<KMAJ, FOLD, STAGES, NTV_, ODD_>(g, acc, nt, p.kst, p.ne, sbase, bar_full, bar_empty, stage, phase, f, role, wm, fr, fc, lane)
+  kloop<KMAJ, FOLD, STAGES, NTV_, ODD_>(g, acc, nt, p.kst, p.ne, sbase, bar_full, bar_empty, stage, phase, f, role, wm, fr, fc, lane, wfull)
     if (nt == 9) {
       if (odd) FDP_K1T_RUN(9, 1); else FDP_K1T_RUN(9, 0);
     } else if (nt == 8) {
@@ -611,8 +727,12 @@ __global__ void __launch_bounds__(kThreads, 1) mode_tma_kernel(const __grid_cons
     // ------------------------------ epilogue ------------------------------
     // stage the accumulators (E columns at 0, O at 72) for the store warps, once they have
     // drained the previous tile; rows as in the fragment layout (KMAJ: 2r + t of the slice; else
-    // p_lo). The epilogue arithmetic (Lambda^{-1}, butterflies, D^{-1/2}) is the store warps'.
+    // p_lo). The epilogue arithmetic (Lambda^{-1}, the backward butterfly, D^{-1/2}) is the store
+    // warps' (measured: forming the butterfly here instead cost the consumers ~4% on config 5).
+    FDP_PT(t1);
     mbar_wait(bar_cempty, cphase ^ 1);
+    FDP_PACC(wcempty, t1);
+    ++ntiles;
 #pragma unroll
     for (int ti = 0; ti < kMT; ++ti) {
       if (KMAJ) {
@@ -633,20 +753,28 @@ __global__ void __launch_bounds__(kThreads, 1) mode_tma_kernel(const __grid_cons
     if (lane == 0) mbar_arrive(bar_cfull);
     cphase ^= 1;
   }
+  FDP_PFLUSH(0, wfull);
+  FDP_PFLUSH(1, wcempty);
+  FDP_PEND(ctot);
+  FDP_PFLUSH(2, ctot);
+  if (warp == 0) FDP_PFLUSH(7, ntiles);
+  (void)wfull;
+  (void)wcempty;
+  (void)ntiles;
 }
 
-template <bool KMAJ, int FOLD, int STAGES>
+// Shared memory: the A / W ring, the output staging buffer, the barriers, and (LAM: launches with
+// an EPI_LAMBDA problem) the staged Lambda factors. Launches without Lambda factors afford a
+// 4-deep ring (229,760 B of the 232,448 B opt-in limit); the Lambda pass keeps 3 stages.
+template <int STAGES, bool LAM>
 constexpr size_t smem_bytes() {
-  return 1024 + (size_t)STAGES * kStageBytes + kCBytes + 16 * STAGES + 64 +
-         (FOLD == FOLD_FWD ? (size_t)kLamMax * 8 : 0);
+  return 1024 + (size_t)STAGES * kStageBytes + kCBytes + 16 * STAGES + 64 + (LAM ? (size_t)kLamMax * 8 : 0);
 }
+static_assert(smem_bytes<4, false>() <= 232448 && smem_bytes<3, true>() <= 232448, "K1t shared memory");
 
-constexpr int kStagesFwd = 3;
-constexpr int kStagesBwd = 3;
-
-template <bool KMAJ, int FOLD, int STAGES>
+template <bool KMAJ, int FOLD, int STAGES, bool LAM>
 cudaError_t launch_t(const TmaGroup& g, int grid, cudaStream_t s) {
-  constexpr size_t sm = smem_bytes<KMAJ, FOLD, STAGES>();
+  constexpr size_t sm = smem_bytes<STAGES, LAM>();
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(mode_tma_kernel<KMAJ, FOLD, STAGES>,
@@ -658,10 +786,10 @@ cudaError_t launch_t(const TmaGroup& g, int grid, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <bool KMAJ, int FOLD, int STAGES>
+template <bool KMAJ, int FOLD, int STAGES, bool LAM>
 cudaError_t set_smem_attr() {
   return cudaFuncSetAttribute(mode_tma_kernel<KMAJ, FOLD, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)smem_bytes<KMAJ, FOLD, STAGES>());
+                              (int)smem_bytes<STAGES, LAM>());
 }
 
 }  // namespace
@@ -669,19 +797,47 @@ cudaError_t set_smem_attr() {
 cudaError_t prepare_mode_tma() {
   // set the shared-memory attributes outside any stream capture
   cudaError_t e;
-  if ((e = set_smem_attr<true, FOLD_FWD, kStagesFwd>()) || (e = set_smem_attr<false, FOLD_FWD, kStagesFwd>()) ||
-      (e = set_smem_attr<true, FOLD_BWD, kStagesBwd>()) || (e = set_smem_attr<false, FOLD_BWD, kStagesBwd>()))
+  if ((e = set_smem_attr<true, FOLD_FWD, 4, false>()) || (e = set_smem_attr<false, FOLD_FWD, 4, false>()) ||
+      (e = set_smem_attr<false, FOLD_FWD, 3, true>()) || (e = set_smem_attr<true, FOLD_BWD, 4, false>()) ||
+      (e = set_smem_attr<false, FOLD_BWD, 4, false>()))
     return e;
   return cudaSuccess;
 }
 
 cudaError_t launch_mode_tma(const TmaGroup& g, bool kmaj, int fold, int grid, cudaStream_t s) {
   if (g.total_tiles <= 0) return cudaSuccess;
-  if (fold == FOLD_FWD)
-    return kmaj ? launch_t<true, FOLD_FWD, kStagesFwd>(g, grid, s) : launch_t<false, FOLD_FWD, kStagesFwd>(g, grid, s);
+  if (fold == FOLD_FWD) {
+    if (kmaj) return g.lam_elems > 0 ? cudaErrorInvalidValue : launch_t<true, FOLD_FWD, 4, false>(g, grid, s);
+    return g.lam_elems > 0 ? launch_t<false, FOLD_FWD, 3, true>(g, grid, s) : launch_t<false, FOLD_FWD, 4, false>(g, grid, s);
+  }
   if (fold == FOLD_BWD)
-    return kmaj ? launch_t<true, FOLD_BWD, kStagesBwd>(g, grid, s) : launch_t<false, FOLD_BWD, kStagesBwd>(g, grid, s);
+    return kmaj ? launch_t<true, FOLD_BWD, 4, false>(g, grid, s) : launch_t<false, FOLD_BWD, 4, false>(g, grid, s);
   return cudaErrorInvalidValue;
+}
+
+// 1 / Lambda of the Lambda pass's output layout (setup time; Algorithm 1 step 3, with
+// Lambda = sum_d c_d lambda_d formed from its factors; IEEE division)
+namespace {
+__global__ void rlam_kernel(double* __restrict__ rlam, const double* __restrict__ lam0,
+                            const double* __restrict__ lam1, const double* __restrict__ lamcol, int n1p,
+                            int n1v, int n_mid, long long total) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long P = (long long)n1p * n_mid;
+    const long long a = i / P, p = i - a * P;
+    const int i1 = (int)(p % n1p), im = (int)(p / n1p);
+    rlam[i] = i1 >= n1v ? 0.0 : 1.0 / (lam0[i1] + (lam1 ? lam1[im] : 0.0) + lamcol[a]);
+  }
+}
+}  // namespace
+
+cudaError_t launch_rlam(double* rlam, const double* lam0, const double* lam1, const double* lamcol, int n1p,
+                        int n1v, int n_mid, int n_last, cudaStream_t s) {
+  const long long total = (long long)n1p * n_mid * n_last;
+  if (total == 0) return cudaSuccess;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+  rlam_kernel<<<blocks, 256, 0, s>>>(rlam, lam0, lam1, lamcol, n1p, n1v, n_mid, total);
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -737,3 +893,12 @@ cudaError_t launch_pad_rows(const double* x, long long xbs, double* y, long long
 }
 
 }  // namespace fdp
+
+#ifdef FDP_K1T_PROF
+// diagnostic build: copy out and reset the K1t per-role clock totals ([launch ordinal mod 8][8])
+extern "C" int fdp_k1t_prof_read(unsigned long long* out) {
+  if (cudaMemcpyFromSymbol(out, fdp::g_k1t_prof, sizeof(unsigned long long) * 64) != cudaSuccess) return -1;
+  unsigned long long z[64] = {};
+  return cudaMemcpyToSymbol(fdp::g_k1t_prof, z, sizeof(z)) == cudaSuccess ? 0 : -1;
+}
+#endif

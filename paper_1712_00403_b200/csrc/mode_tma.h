@@ -43,6 +43,7 @@ struct TmaProb {
   const double* lam0;
   const double* lam1;
   const double* lamcol;
+  const double* rlam;   // EPI_LAMBDA: 1 / Lambda in the output layout (NULL: divide on the fly)
   long long ybs;
   int n, ne, no, n8h, ctiles, kst;
   int P, Q, bp, bq, tiles_p, tiles_q;
@@ -60,6 +61,7 @@ struct TmaGroup {
   int total_tiles;
   int ct_uniform;  // column tiles of every problem when equal (grid a multiple of it), else 0
   int lam_elems;   // doubles of staged Lambda factors (0: none)
+  int prof_slot;   // diagnostic build (FDP_K1T_PROF): K1t launch ordinal mod 8
 };
 
 cudaError_t launch_mode_tma(const TmaGroup& g, bool kmaj, int fold, int grid, cudaStream_t s);
