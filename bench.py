@@ -496,7 +496,10 @@ def main():
             ms_i, fl_i, _, idx = max(k1)
             dom = {"launch_index": idx, "mean_ms": ms_i, "flops_per_launch": fl_i,
                    "share_of_step": ms_i / (tot_ms / len(prof_runs)) if tot_ms else None,
-                   "achieved": fl_i / (ms_i * 1e-3) / 1e12}
+                   "achieved": fl_i / (ms_i * 1e-3) / 1e12,
+                   # ordinal among the step's FD-transform launches (K1t on configs 4-5: forward
+                   # modes 1, 2, 3 (Lambda), backward modes 3, 2, 1)
+                   "transform_ordinal": [m[3] for m in k1].index(idx)}
     achieved = dom["achieved"] if dom else k1_family
     # the dense FD's work (4 N_k sum_d n_d per component and RHS) at the same
     # K1 time: what the even-odd folding saves shows as dense_equiv > achieved
@@ -512,9 +515,19 @@ def main():
         # (FOLD = 1, the fourth template argument); else every FD-transform kernel captured
         allk = [k for k in json.load(open(ncu_json)).get("kernels", []) if "mode_" in k["kernel"]]
         ks = [k for k in allk if "mode_plane" in k["kernel"]]
-        if not ks:  # K1t forward transforms: mode_tma_kernel<KMAJ, FOLD_FWD = 1, STAGES>
-            ks = [k for k in allk if "mode_tma_kernel<" in k["kernel"]
-                  and k["kernel"].split("mode_tma_kernel<")[1].split(",")[1].strip() == "1"]
+        if not ks and dom is not None and dom.get("transform_ordinal", 9) < 6:
+            # K1t: the captures of the dominant pass's kernel mode_tma_kernel<KMAJ, FOLD, STAGES>
+            # (passes: fwd 1 <1,1>, fwd 2 <0,1>, fwd 3 + Lambda <0,1> (also reads the 1/Lambda
+            # table: DRAM reads > 1.5x writes), bwd 3 <0,2>, bwd 2 <0,2>, bwd 1 <1,2>)
+            o = dom["transform_ordinal"]
+            km, fo = [("1", "1"), ("0", "1"), ("0", "1"), ("0", "2"), ("0", "2"), ("1", "2")][o]
+            def targ(k):
+                a = k["kernel"].split("mode_tma_kernel<")[1].split(",")
+                return a[0].strip(), a[1].strip()
+            ks = [k for k in allk if "mode_tma_kernel<" in k["kernel"] and targ(k) == (km, fo)]
+            if o in (1, 2):
+                lam = lambda k: (k["dram_read_bytes"] or 0) > 1.5 * (k["dram_write_bytes"] or 1)
+                ks = [k for k in ks if lam(k) == (o == 2)]
         if not ks:
             ks = [k for k in allk if "fold_kernel<" in k["kernel"]
                   and k["kernel"].split("fold_kernel<")[1].split(",")[3].strip() == "1"]
@@ -576,10 +589,11 @@ def main():
         "config": workload_config(cid, w, n_total, world),
         "roofline": {
             "bound": "tensor",
-            "kernel": "the dominant FD-transform launch of the step (config 2/3: the plane kernel "
-                      "mode_plane_kernel; configs 4/5: the TMA-fed folded transform mode_tma_kernel "
-                      "(K1t), the last forward mode with the Lambda division; FP64 mma.sync m8n8k4 "
-                      "-> DMMA)",
+            "kernel": "the dominant FD-transform launch of the step, the one with the largest mean "
+                      "time (config 2/3: the plane kernel mode_plane_kernel; configs 4/5: a pass of "
+                      "the TMA-fed folded transform mode_tma_kernel (K1t), dominant_launch."
+                      "transform_ordinal = fwd modes 1, 2, 3, bwd modes 3, 2, 1); FP64 mma.sync "
+                      "m8n8k4 -> DMMA",
             "achieved": achieved,
             "dominant_launch": dom,
             "k1_family": {"achieved": k1_family,
