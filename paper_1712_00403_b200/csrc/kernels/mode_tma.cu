@@ -138,13 +138,14 @@ __device__ __forceinline__ void named_bar(int id, int count) {
 // Diagnostic build only (-DFDP_K1T_PROF, `make prof` -> libfdp_prof.so): clock64 totals per
 // warp role, summed over CTAs: [0] consumer wait on "full", [1] consumer wait on the staging
 // buffer, [2] consumer total, [3] store wait on a staged tile, [4] store total, [5] producer wait
-// on "empty", [6] producer total, [7] tiles (consumer warp 0).
+// on "empty", [6] producer total, [7] tiles (consumer warp 0), [8] consumer wait on the first
+// stage of a tile, [9] producer time issuing (tile decode + copies).
 #ifdef FDP_K1T_PROF
-__device__ unsigned long long g_k1t_prof[8 * 8];
+__device__ unsigned long long g_k1t_prof[8 * 16];
 #define FDP_PT(v) long long v = clock64()
 #define FDP_PACC(acc, t0) acc += clock64() - (t0)
 #define FDP_PEND(v) v = clock64() - v
-#define FDP_PFLUSH(slot, v) if (lane == 0) atomicAdd(&g_k1t_prof[8 * g.prof_slot + (slot)], (unsigned long long)(v))
+#define FDP_PFLUSH(slot, v) if (lane == 0) atomicAdd(&g_k1t_prof[16 * g.prof_slot + (slot)], (unsigned long long)(v))
 #else
 #define FDP_PT(v)
 #define FDP_PACC(acc, t0)
@@ -237,7 +238,7 @@ __device__ __noinline__ void producer_loop(const TmaGroup& g, unsigned sbase, un
   int slot = 0;
   unsigned phase = 0;
   const int lane = 0;
-  long long pw = 0;
+  long long pw = 0, pis = 0;
   FDP_PT(ptot);
   for (int it = 0;; ++it) {
     const int tau = tile_of(g, it);
@@ -247,7 +248,9 @@ __device__ __noinline__ void producer_loop(const TmaGroup& g, unsigned sbase, un
       FDP_PT(t0);
       mbar_wait(bar_empty + 8 * slot, phase ^ 1);
       FDP_PACC(pw, t0);
+      FDP_PT(t2);
       issue_stage<KMAJ, FOLD>(g, sbase, bar_full, slot, it, s);
+      FDP_PACC(pis, t2);
       if (++slot == STAGES) {
         slot = 0;
         phase ^= 1;
@@ -255,6 +258,8 @@ __device__ __noinline__ void producer_loop(const TmaGroup& g, unsigned sbase, un
     }
   }
   FDP_PFLUSH(5, pw);
+  FDP_PFLUSH(9, pis);
+  (void)pis;
   FDP_PEND(ptot);
   FDP_PFLUSH(6, ptot);
   (void)pw;
@@ -344,7 +349,7 @@ template <bool KMAJ, int FOLD, int STAGES, int NTV, int ODD>
 __device__ __forceinline__ void kloop(const TmaGroup& g, double (&acc)[kMT][9][2], int nt, int kst, int ne,
                                       unsigned sbase, unsigned bar_full, unsigned bar_empty, int& stage,
                                       unsigned& phase, const Frag& f, int role, int wm, int fr, int fc, int lane,
-                                      long long& wfull) {
+                                      long long& wfull, long long& wfirst) {
   const double sgn = role ? -1.0 : 1.0;  // FWD: E warps form s = x + Jx, O warps d = x - Jx
   const int rem = ne - (kst - 1) * kTmaBK;  // valid k of the last stage (1 .. 16)
   const bool nat = tma_last_nat(ne, KMAJ);
@@ -353,6 +358,7 @@ __device__ __forceinline__ void kloop(const TmaGroup& g, double (&acc)[kMT][9][2
     FDP_PT(t0);
     mbar_wait(bar_full + 8 * stage, phase);
     FDP_PACC(wfull, t0);
+    if (s == 0) FDP_PACC(wfirst, t0);
     const unsigned A0 = sbase + stage * kStageBytes;
     const unsigned A1 = A0 + kABytes;
     const unsigned B = A1 + kABytes + role * kBBytes;
@@ -673,7 +679,7 @@ __global__ void __launch_bounds__(kThreads, 1) mode_tma_kernel(const __grid_cons
   const int fr = lane >> 2, fc = lane & 3;
   int stage = 0;
   unsigned phase = 0, cphase = 0;
-  long long wfull = 0, wcempty = 0, ntiles = 0;
+  long long wfull = 0, wcempty = 0, ntiles = 0, wfirst = 0;
   FDP_PT(ctot);
   // per-thread fragment offsets (see Frag)
   Frag f;
@@ -715,7 +721,7 @@ __global__ void __launch_bounds__(kThreads, 1) mode_tma_kernel(const __grid_cons
     // mma.sync costs a WARPSYNC + NOP pair) and, for KMAJ, on the odd-start second A tile
     const int odd = KMAJ ? p.a1odd : 0;
 #define FDP_K1T_RUN(NTV_, ODD_) \
-  kloop<KMAJ, FOLD, STAGES, NTV_, ODD_>(g, acc, nt, p.kst, p.ne, sbase, bar_full, bar_empty, stage, phase, f, role, wm, fr, fc, lane, wfull)
+  kloop<KMAJ, FOLD, STAGES, NTV_, ODD_>(g, acc, nt, p.kst, p.ne, sbase, bar_full, bar_empty, stage, phase, f, role, wm, fr, fc, lane, wfull, wfirst)
     if (nt == 9) {
       if (odd) FDP_K1T_RUN(9, 1); else FDP_K1T_RUN(9, 0);
     } else if (nt == 8) {
@@ -755,6 +761,8 @@ __global__ void __launch_bounds__(kThreads, 1) mode_tma_kernel(const __grid_cons
   }
   FDP_PFLUSH(0, wfull);
   FDP_PFLUSH(1, wcempty);
+  FDP_PFLUSH(8, wfirst);
+  (void)wfirst;
   FDP_PEND(ctot);
   FDP_PFLUSH(2, ctot);
   if (warp == 0) FDP_PFLUSH(7, ntiles);
@@ -897,8 +905,8 @@ cudaError_t launch_pad_rows(const double* x, long long xbs, double* y, long long
 #ifdef FDP_K1T_PROF
 // diagnostic build: copy out and reset the K1t per-role clock totals ([launch ordinal mod 8][8])
 extern "C" int fdp_k1t_prof_read(unsigned long long* out) {
-  if (cudaMemcpyFromSymbol(out, fdp::g_k1t_prof, sizeof(unsigned long long) * 64) != cudaSuccess) return -1;
-  unsigned long long z[64] = {};
+  if (cudaMemcpyFromSymbol(out, fdp::g_k1t_prof, sizeof(unsigned long long) * 128) != cudaSuccess) return -1;
+  unsigned long long z[128] = {};
   return cudaMemcpyToSymbol(fdp::g_k1t_prof, z, sizeof(z)) == cudaSuccess ? 0 : -1;
 }
 #endif
