@@ -198,131 +198,6 @@ mass_solve_mode1_kernel(const MassMode mm) {
   }
 }
 
-// Staged solve (the default where a bundle fits shared memory): a CTA loads a bundle of F fibers
-// whole into shared memory with coalesced loads (modes >= 2: F consecutive p, each element row a
-// 128-byte segment; mode 1 (P == 1): F consecutive fibers, one contiguous chunk), F threads run
-// the forward and back substitutions in shared memory, and the CTA stores the bundle back: every
-// element crosses HBM once each way (16 B per element and mode instead of the fiber kernels'
-// 32 B: they write y and read it back). The recurrence adds the y_{i-1} term last, so its critical
-// path is one FMA and one multiply per step. In place is fine (a bundle is read before written).
-// Layout: P >= F: [i][t] (stride F); P == 1: [t][i] with an odd row stride S = n | 1
-// (conflict-free 8-byte accesses across the F threads).
-constexpr int kStageF = 16;
-constexpr int kStageThreads = 128;
-
-template <int BAND>
-__global__ void __launch_bounds__(kStageThreads)
-mass_stage_kernel(const MassMode mm, long long nbundles) {
-  extern __shared__ double sh[];
-  const int P = mm.P, n = mm.n;
-  const bool m1 = P == 1;
-  const int S = n | 1;
-  const long long pgroups = m1 ? 1 : (P + kStageF - 1) / kStageF;
-  const long long nfib = (long long)mm.Q * mm.batch;  // fibers per p (mode 1: all fibers)
-  const double* __restrict__ Lb = mm.Lb;
-  const double* __restrict__ invd = mm.invd;
-  for (long long bidx = blockIdx.x; bidx < nbundles; bidx += gridDim.x) {
-    // bundle: modes >= 2: (p-group pg, fiber r); mode 1: fibers r0 .. r0 + F - 1
-    const long long pg = m1 ? 0 : bidx % pgroups, rb = m1 ? bidx * kStageF : bidx / pgroups;
-    const int nfb = m1 ? (int)min((long long)kStageF, nfib - rb) : min(kStageF, P - (int)pg * kStageF);
-    // element i of bundle fiber t: global offset off(t) + P * i, index within its batch item
-    auto goff = [&](int t, long long* sidx) -> long long {
-      const long long r = m1 ? rb + t : rb, p = m1 ? 0 : pg * kStageF + t;
-      const long long q = r % mm.Q, b = r / mm.Q;
-      *sidx = p + (long long)P * n * q;
-      return *sidx + mm.bs * b;
-    };
-    // load (pre-scaled)
-    if (m1) {
-      long long si0;
-      const long long g0 = goff(0, &si0);  // fibers rb .. consecutive: one chunk when they share an item
-      const bool one = (rb % mm.Q) + nfb <= mm.Q;
-      for (int j = threadIdx.x; j < nfb * n; j += kStageThreads) {
-        const int t = j / n, i = j - t * n;
-        long long si, g;
-        if (one) { g = g0 + j; si = si0 + j; } else { g = goff(t, &si) + i; si += i; }
-        double v = mm.in[g];
-        if (mm.pre) v *= mm.pre[si];
-        sh[t * S + i] = v;
-      }
-    } else {
-      long long si0;
-      const long long g0 = goff(0, &si0);
-      for (int j = threadIdx.x; j < kStageF * n; j += kStageThreads) {
-        const int t = j & (kStageF - 1), i = j / kStageF;
-        if (t < nfb) {
-          double v = mm.in[g0 + t + (long long)P * i];
-          if (mm.pre) v *= mm.pre[si0 + t + (long long)P * i];
-          sh[i * kStageF + t] = v;
-        }
-      }
-    }
-    __syncthreads();
-    const int t = threadIdx.x;
-    if (t < nfb) {
-      const int es = m1 ? 1 : kStageF;               // element stride of this thread's fiber
-      double* f = sh + (m1 ? t * S : t);
-      double ring[BAND > 0 ? BAND : 1];  // ring[0] = y_{i-1}, ring[1] = y_{i-2}, ...
-#pragma unroll
-      for (int j = 0; j < BAND; ++j) ring[j] = 0.0;
-      // forward substitution L y = x
-      for (int i = 0; i < n; ++i) {
-        const double* Li = Lb + (size_t)i * (BAND + 1);
-        double v = f[i * es];
-#pragma unroll
-        for (int j = BAND; j >= 1; --j) v -= Li[BAND - j] * ring[j - 1];
-        v *= invd[i];
-#pragma unroll
-        for (int j = BAND - 1; j > 0; --j) ring[j] = ring[j - 1];
-        if (BAND > 0) ring[0] = v;
-        f[i * es] = v;
-      }
-      // back substitution L^T z = y
-#pragma unroll
-      for (int j = 0; j < BAND; ++j) ring[j] = 0.0;
-      for (int i = n - 1; i >= 0; --i) {
-        double v = f[i * es];
-#pragma unroll
-        for (int j = BAND; j >= 1; --j) {
-          if (i + j < n) v -= Lb[(size_t)(i + j) * (BAND + 1) + (BAND - j)] * ring[j - 1];
-        }
-        v *= invd[i];
-#pragma unroll
-        for (int j = BAND - 1; j > 0; --j) ring[j] = ring[j - 1];
-        if (BAND > 0) ring[0] = v;
-        f[i * es] = v;
-      }
-    }
-    __syncthreads();
-    // store (post-scaled)
-    if (m1) {
-      long long si0;
-      const long long g0 = goff(0, &si0);
-      const bool one = (rb % mm.Q) + nfb <= mm.Q;
-      for (int j = threadIdx.x; j < nfb * n; j += kStageThreads) {
-        const int t2 = j / n, i = j - t2 * n;
-        long long si, g;
-        if (one) { g = g0 + j; si = si0 + j; } else { g = goff(t2, &si) + i; si += i; }
-        double v = sh[t2 * S + i];
-        if (mm.post) v *= mm.post[si];
-        mm.out[g] = v;
-      }
-    } else {
-      long long si0;
-      const long long g0 = goff(0, &si0);
-      for (int j = threadIdx.x; j < kStageF * n; j += kStageThreads) {
-        const int t2 = j & (kStageF - 1), i = j / kStageF;
-        if (t2 < nfb) {
-          double v = sh[i * kStageF + t2];
-          if (mm.post) v *= mm.post[si0 + t2 + (long long)P * i];
-          mm.out[g0 + t2 + (long long)P * i] = v;
-        }
-      }
-    }
-    __syncthreads();
-  }
-}
-
 // y = M x along fibers (FDP_MASS_FORWARD); out must not alias in.
 template <int BAND>
 __global__ void mass_forward_kernel(const MassMode mm) {
@@ -349,31 +224,8 @@ cudaError_t launch_b(const MassMode& m, cudaStream_t s) {
   const int threads = 128;
   const long long blocks = (nf + threads - 1) / threads;
   if (blocks == 0) return cudaSuccess;
-  if (m.forward) {
-    mass_forward_kernel<BAND><<<(unsigned)blocks, threads, 0, s>>>(m);
-    return cudaGetLastError();
-  }
-  // staged bundles (shared memory of a bundle <= 112 KB: at least two CTAs per SM; config 5's
-  // n = 516: 66 KB, three); FDP_MASS_FIBER=1 keeps the fiber kernels (measurements)
-  const size_t smem = (size_t)kStageF * (m.n | 1) * sizeof(double);
-  constexpr size_t kStageSmemMax = 112 * 1024;
-  if ((m.P == 1 || m.P >= kStageF) && smem <= kStageSmemMax && std::getenv("FDP_MASS_FIBER") == nullptr) {
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(mass_stage_kernel<BAND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)kStageSmemMax);
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
-    const long long fibers = (long long)m.Q * m.batch;
-    const long long nb = m.P == 1 ? (fibers + kStageF - 1) / kStageF
-                                  : fibers * ((m.P + kStageF - 1) / kStageF);
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const long long grid = std::min<long long>(nb, (long long)sms * 16);
-    mass_stage_kernel<BAND><<<(unsigned)grid, kStageThreads, smem, s>>>(m, nb);
-  } else if (m.P == 1) {
+  if (m.forward) mass_forward_kernel<BAND><<<(unsigned)blocks, threads, 0, s>>>(m);
+  else if (m.P == 1) {
     const long long warps = (nf + 31) / 32;
     mass_solve_mode1_kernel<BAND><<<(unsigned)((warps + kM1Warps - 1) / kM1Warps), kM1Warps * 32, 0, s>>>(m);
   }
