@@ -105,8 +105,11 @@ typedef struct fdp_fd_s* fdp_fd;
 /* D in {2,3}; n[d] in [1, 2048]; K[d], M[d]: host, column-major n[d] x n[d], symmetric to
  * 1e-12 relative, M[d] SPD; coef[d] > 0. Performs the D generalized eigensolves on the host
  * (Algorithm 1 step 1: Cholesky + Householder tridiagonalisation + implicit QL),
- * uploads U_d, U_d^T (zero padded) and lambda_d to `device`, and allocates a workspace for
- * up to max_batch right-hand sides (0 = none; then fd_apply needs a caller workspace).
+ * uploads U_d, U_d^T (zero padded; for persymmetric pencils the even-odd folded blocks and
+ * their TMA-fragment layout) and lambda_d to `device`, and allocates a workspace for up to
+ * max_batch right-hand sides (0 = none; then fd_apply needs a caller workspace). When the last
+ * mode is longer than 96 and folded, the handle also holds 1 / Lambda in the Lambda pass's
+ * output layout (n1p * n2 * n3 doubles, n1p = n1 rounded up to even; C-11).
  * Errors: FDP_ERR_SHAPE, FDP_ERR_NOT_SPD, FDP_ERR_SINGULAR, FDP_ERR_OOM, FDP_ERR_CUDA. */
 fdp_status fd_setup(int D, const int32_t* n, const double* const* K, const double* const* M,
                     const double* coef, int device, int64_t max_batch, fdp_fd* out);
