@@ -86,7 +86,10 @@ bool tma_input_ok(const ModeProb& p, bool kmaj) {
 // The folded K1 problems of one grouped stage can run on K1t.
 bool tma_eligible(const ModeProb& p, bool kmaj) {
   if (std::getenv("FDP_NO_TMA")) return false;
-  if (!p.Wt || !p.fold_k1 || p.peers || p.tio) return false;
+  if (!p.Wt || !p.fold_k1 || p.tio) return false;
+  // K1t scatters from non-KMAJ batch-1 stores, a lane's row pair contiguous and 16-byte aligned in
+  // the owner's buffer (sc_n1 even)
+  if (p.peers && (kmaj || p.batch != 1 || (p.sc_n1 & 1))) return false;
   if (p.fold != FOLD_FWD && p.fold != FOLD_BWD) return false;
   if (p.fold == FOLD_FWD && p.epi != EPI_NONE && p.epi != EPI_LAMBDA) return false;
   if (kmaj && p.epi == EPI_LAMBDA) return false;  // Lambda^{-1} is applied on the non-KMAJ store path
@@ -117,6 +120,15 @@ cudaError_t launch_tma_stage(const ModeProb* probs, int count, bool kmaj, cudaSt
     t.lam0 = m.lam0;
     t.lam1 = m.lam1;
     t.lamcol = m.lamcol;
+    t.peers = m.peers;
+    t.sc_G = m.sc_G;
+    t.sc_na = m.sc_na;
+    t.sc_n1 = m.sc_n1;
+    t.sc_qoff = m.sc_qoff;
+    t.sc_a0 = m.sc_a0;
+    t.sc_a1 = m.sc_a1;
+    t.sc_q0 = m.sc_q0;
+    t.sc_q1 = m.sc_q1;
     t.rlam = m.rlam;
     t.ybs = m.ybs;
     t.n = m.n;

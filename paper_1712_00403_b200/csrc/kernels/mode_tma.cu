@@ -157,6 +157,20 @@ struct Tile {
   int pi, ct, tp, tq, b;
 };
 
+// peer-store scatter target of output (GEMM row m, column a) of a batch-1 problem: the rank o
+// owning a under the even split of sc_na over sc_G ranks, at its buffer offset (scatter_ptr's
+// addressing, fdp_internal.h)
+__device__ __forceinline__ double* tma_scatter_ptr(const TmaProb& p, long long m, int a) {
+  const int G = p.sc_G, na = p.sc_na;
+  const int q = na / G, rem = na % G;
+  const int o = (q == 0 || a < rem * (q + 1)) ? a / (q + 1) : rem + (a - rem * (q + 1)) / q;
+  const int lo = o * q + (o < rem ? o : rem);
+  const int len = q + (o < rem ? 1 : 0);
+  const long long r = m % p.sc_n1, qq = m / p.sc_n1;
+  return p.peers[o] + r +
+         (long long)p.sc_n1 * ((long long)(a - lo) * (p.sc_a0 + p.sc_a1 * len) + (qq + p.sc_qoff) * (p.sc_q0 + p.sc_q1 * len));
+}
+
 // Tile of this CTA's it-th iteration (-1: done). With a uniform column-tile count CT (grid a
 // multiple of CT) the CT CTAs of a group work on the column tiles of the same row block at the
 // same time -- its A rows are fetched from DRAM once and hit L2 for the others -- and rotate
@@ -540,8 +554,12 @@ __device__ __noinline__ void store_loop(const TmaGroup& g, unsigned cbuf, unsign
             }
           }
 #pragma unroll
-          for (int u = 0; u < U; ++u)
-            if (ok[u]) *reinterpret_cast<double2*>(yrow + P * oc[u]) = make_double2(v[u][0], v[u][1]);
+          for (int u = 0; u < U; ++u) {
+            if (!ok[u]) continue;
+            // the peer-store exchange: rows pp, pp + 1 of the same i1-row land contiguously
+            double* dst = p.peers ? tma_scatter_ptr(p, pp + P * q, oc[u]) : yrow + P * oc[u];
+            *reinterpret_cast<double2*>(dst) = make_double2(v[u][0], v[u][1]);
+          }
         }
       } else if (valid) {
         const bool scl = p.epi == EPI_SCALE;
@@ -573,8 +591,12 @@ __device__ __noinline__ void store_loop(const TmaGroup& g, unsigned cbuf, unsign
             }
             const int cm = n - 1 - cc[u];
             if (ok[u]) {
-              *reinterpret_cast<double2*>(yrow + P * cc[u]) = make_double2(x0, x1);
-              if (cm != cc[u]) *reinterpret_cast<double2*>(yrow + P * cm) = make_double2(y0, y1);
+              double* dx = p.peers ? tma_scatter_ptr(p, pp + P * q, cc[u]) : yrow + P * cc[u];
+              *reinterpret_cast<double2*>(dx) = make_double2(x0, x1);
+              if (cm != cc[u]) {
+                double* dy = p.peers ? tma_scatter_ptr(p, pp + P * q, cm) : yrow + P * cm;
+                *reinterpret_cast<double2*>(dy) = make_double2(y0, y1);
+              }
             }
           }
         }

@@ -51,6 +51,10 @@ struct TmaProb {
   int a1odd;      // KMAJ: the second A tile starts at an odd column (odd n FWD / odd ne BWD)
   int lam_off, lam1_n;  // EPI_LAMBDA: offset of this problem's staged factors, length of lam1
   int tile_begin;
+  // peer-store scatter of a non-KMAJ, batch-1 problem (the slab exchange fused into the store,
+  // DESIGN.md §9; same addressing as ModeProb / scatter_ptr); peers == NULL: store into Y
+  double* const* peers;
+  int sc_G, sc_na, sc_n1, sc_qoff, sc_a0, sc_a1, sc_q0, sc_q1;
 };
 
 struct TmaGroup {

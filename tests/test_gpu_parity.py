@@ -673,3 +673,22 @@ def test_kron_mass_slab_workspace_covers_both_phases():
             z = [10 // G + (1 if i < 10 % G else 0) for i in range(G)][rk]
             y = [11 // G + (1 if i < 11 % G else 0) for i in range(G)][rk]
             assert nb >= 8 * max(4 * 11 * z, 4 * y * 10), (G, rk, nb)
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_slab_peer_store_k1t_scatter(G):
+    """K1t's peer-store scatter: RT p = 4, n_el = 100 (component extents 103 / 104,
+    all on the K1-path fold), G virtual ranks with NaN-poisoned receive buffers; the components
+    with an even n1 run the scattering passes (phase 0's mode 2, phase 1's mode-3 backward) on
+    K1t, the odd one on K1f. Against the oracle, every element."""
+    from paper_1712_00403_b200 import dist as fdist
+    od = ospaces.build(3, "RT", 4, 100)
+    gd = fdp.discretization(3, "RT", 4, 100)
+    P = fdp.build_block(gd)
+    r = np.random.default_rng(50 + G).standard_normal(od.n_total)
+    t0 = int(fdp.lib.fdp_debug_k1_launches(1))
+    s = fdist.emulate_slab_apply_peer(P, dev(r), G).cpu().numpy()
+    assert int(fdp.lib.fdp_debug_k1_launches(1)) > t0
+    ref = oprec.BlockPrecond(od).apply(r)
+    assert np.all(np.isfinite(s))
+    assert rel(s, ref) < TOL and relmax(s, ref) < TOL
