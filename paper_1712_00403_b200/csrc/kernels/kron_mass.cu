@@ -10,8 +10,11 @@
 namespace fdp {
 namespace {
 
+// <= 64 registers (eight 128-thread blocks per SM): config 5's 266,256 fibers per mode then take
+// two waves of 1,184 blocks instead of three of 1,036 (a fiber is a long sequential unit, so a
+// nearly empty third wave costs a whole fiber time)
 template <int BAND, int U>
-__global__ void mass_solve_kernel(const MassMode mm) {
+__global__ void __launch_bounds__(128, 8) mass_solve_kernel(const MassMode mm) {
   const long long f = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long nf = (long long)mm.P * mm.Q * mm.batch;
   if (f >= nf) return;
