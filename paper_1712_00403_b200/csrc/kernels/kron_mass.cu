@@ -135,7 +135,33 @@ mass_solve_mode1_kernel(const MassMode mm) {
     for (int r = 0; r < 32; ++r) T[r][lane] = v[r];
     __syncwarp();
     const int kend = min(32, n - k0);
-    for (int kk = 0; kk < kend; ++kk) {
+    // steps in groups of 4 whose tile values and band coefficients are loaded before the group's
+    // dependent chain (one step at a time, the L1 latency of the coefficient loads sat on the
+    // chain: 51% of the warps' stalls were long-scoreboard waits)
+    int kk = 0;
+    for (; kk + 4 <= kend; kk += 4) {
+      double xv[4], cf[4][BAND > 0 ? BAND : 1], dv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = k0 + kk + u;
+        xv[u] = T[lane][kk + u];
+        dv[u] = __ldg(invd + i);
+#pragma unroll
+        for (int j = 1; j <= BAND; ++j) cf[u][j - 1] = __ldg(Lb + (size_t)i * (BAND + 1) + (BAND - j));
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        double x = xv[u];
+#pragma unroll
+        for (int j = 1; j <= BAND; ++j) x -= cf[u][j - 1] * ring[j - 1];
+        x *= dv[u];
+#pragma unroll
+        for (int j = BAND - 1; j > 0; --j) ring[j] = ring[j - 1];
+        if (BAND > 0) ring[0] = x;
+        T[lane][kk + u] = x;
+      }
+    }
+    for (; kk < kend; ++kk) {
       const int i = k0 + kk;
       double x = T[lane][kk];
       const double* Li = Lb + (size_t)i * (BAND + 1);
@@ -172,7 +198,31 @@ mass_solve_mode1_kernel(const MassMode mm) {
     for (int r = 0; r < 32; ++r) T[r][lane] = v[r];
     __syncwarp();
     const int kend = min(32, n - k0);
-    for (int kk = kend - 1; kk >= 0; --kk) {
+    int kk = kend - 1;
+    for (; kk - 3 >= 0; kk -= 4) {  // groups of 4 steps, inputs loaded first (see above)
+      double xv[4], cf[4][BAND > 0 ? BAND : 1], dv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = k0 + kk - u;
+        xv[u] = T[lane][kk - u];
+        dv[u] = __ldg(invd + i);
+#pragma unroll
+        for (int j = 1; j <= BAND; ++j)
+          cf[u][j - 1] = i + j < n ? __ldg(Lb + (size_t)(i + j) * (BAND + 1) + (BAND - j)) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        double x = xv[u];
+#pragma unroll
+        for (int j = 1; j <= BAND; ++j) x -= cf[u][j - 1] * ring[j - 1];
+        x *= dv[u];
+#pragma unroll
+        for (int j = BAND - 1; j > 0; --j) ring[j] = ring[j - 1];
+        if (BAND > 0) ring[0] = x;
+        T[lane][kk - u] = x;
+      }
+    }
+    for (; kk >= 0; --kk) {
       const int i = k0 + kk;
       double x = T[lane][kk];
 #pragma unroll
