@@ -1046,6 +1046,8 @@ static void free_mass(fdp_mass h) {
     cudaFree(h->Lb[d]);
     cudaFree(h->invd[d]);
     cudaFree(h->Mb[d]);
+    cudaFree(h->cf[d]);
+    cudaFree(h->cb[d]);
   }
   delete h;
 }
@@ -1086,15 +1088,29 @@ extern "C" fdp_status kron_mass_setup(int D, const int32_t* n, const double* con
     for (int d = 0; d < D; ++d) raw->Lb_host[d] = Lb[d];
     for (int d = 0; d < D; ++d) {
       fdp_status st;
+      // K3t coefficients: the band rows scaled by 1 / L_ii (forward by row, backward by column)
+      const int b = raw->band[d], nd = raw->n[d], cs = mass_coef_stride(b);
+      std::vector<double> cf((size_t)nd * cs, 0.0), cb((size_t)nd * cs, 0.0);
+      for (int i = 0; i < nd; ++i) {
+        for (int k = 0; k < b; ++k) {
+          cf[(size_t)i * cs + k] = Lb[d][(size_t)i * (b + 1) + k] * invd[d][i];
+          const int i2 = i + b - k;
+          if (i2 < nd) cb[(size_t)i * cs + k] = Lb[d][(size_t)i2 * (b + 1) + k] * invd[d][i];
+        }
+        cf[(size_t)i * cs + b] = cb[(size_t)i * cs + b] = invd[d][i];
+      }
       if ((st = dalloc(&raw->Lb[d], Lb[d].size())) || (st = dalloc(&raw->invd[d], invd[d].size())) ||
-          (st = dalloc(&raw->Mb[d], Mb[d].size()))) {
+          (st = dalloc(&raw->Mb[d], Mb[d].size())) || (st = dalloc(&raw->cf[d], cf.size())) ||
+          (st = dalloc(&raw->cb[d], cb.size()))) {
         free_mass(raw);
         return st;
       }
       cudaError_t e;
       if ((e = cudaMemcpy(raw->Lb[d], Lb[d].data(), Lb[d].size() * 8, cudaMemcpyHostToDevice)) ||
           (e = cudaMemcpy(raw->invd[d], invd[d].data(), invd[d].size() * 8, cudaMemcpyHostToDevice)) ||
-          (e = cudaMemcpy(raw->Mb[d], Mb[d].data(), Mb[d].size() * 8, cudaMemcpyHostToDevice))) {
+          (e = cudaMemcpy(raw->Mb[d], Mb[d].data(), Mb[d].size() * 8, cudaMemcpyHostToDevice)) ||
+          (e = cudaMemcpy(raw->cf[d], cf.data(), cf.size() * 8, cudaMemcpyHostToDevice)) ||
+          (e = cudaMemcpy(raw->cb[d], cb.data(), cb.size() * 8, cudaMemcpyHostToDevice))) {
         free_mass(raw);
         return cuda_fail(e, "kron_mass_setup: upload");
       }
@@ -1122,6 +1138,8 @@ cudaError_t enqueue_mass(const fdp_mass_s* h, int mode, const double* in, double
     m.Lb = h->Lb[d];
     m.invd = h->invd[d];
     m.Mb = h->Mb[d];
+    m.cf = h->cf[d];
+    m.cb = h->cb[d];
     m.pre = (d == 0 && mode == FDP_MASS_INVERSE) ? dscale : nullptr;
     m.post = (d == h->D - 1 && mode == FDP_MASS_INVERSE) ? dscale : nullptr;
     m.N = h->N;

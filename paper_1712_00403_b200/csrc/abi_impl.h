@@ -189,6 +189,8 @@ struct fdp_mass_s {
   double* Lb[3] = {nullptr, nullptr, nullptr};
   double* invd[3] = {nullptr, nullptr, nullptr};
   double* Mb[3] = {nullptr, nullptr, nullptr};
+  double* cf[3] = {nullptr, nullptr, nullptr};  // K3t coefficients (MassMode::cf / cb)
+  double* cb[3] = {nullptr, nullptr, nullptr};
   std::vector<double> Lb_host[3];
 };
 

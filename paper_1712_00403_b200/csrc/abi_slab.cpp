@@ -257,6 +257,8 @@ SlabOps mass_slab_ops(const fdp_mass_s* h, int phase, int G, int g, const double
     m.Lb = h->Lb[d];
     m.invd = h->invd[d];
     m.Mb = h->Mb[d];
+    m.cf = h->cf[d];
+    m.cb = h->cb[d];
     m.pre = pre;
     m.N = P * h->n[d] * Q;
     m.bs = 0;

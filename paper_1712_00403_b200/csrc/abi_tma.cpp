@@ -100,6 +100,22 @@ bool tma_eligible(const ModeProb& p, bool kmaj) {
   return encoder() != nullptr;
 }
 
+bool mass_tile_map(CUtensorMap* map, const double* X, int P, int n, long long Q, long long batch, long long bs,
+                   int F, int boxn) {
+  EncodeFn enc = encoder();
+  if (!enc || !aligned16(X) || (P & 1) || (F & 1) || boxn < 1 || boxn > 256) return false;
+  const unsigned long long qstride = (unsigned long long)P * n * 8;
+  const unsigned long long bstride = batch > 1 ? (unsigned long long)bs * 8 : qstride * Q + 16;
+  if (bstride & 15) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)P, (cuuint64_t)n, (cuuint64_t)Q, (cuuint64_t)batch};
+  cuuint64_t strides[3] = {(cuuint64_t)P * 8, qstride, (cuuint64_t)(bstride & ~15ULL)};
+  cuuint32_t box[4] = {(cuuint32_t)F, (cuuint32_t)boxn, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(X), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promotion(),
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 cudaError_t launch_tma_stage(const ModeProb* probs, int count, bool kmaj, cudaStream_t s) {
   if (count < 1 || count > kTmaMaxProbs) return cudaErrorInvalidValue;
   EncodeFn enc = encoder();

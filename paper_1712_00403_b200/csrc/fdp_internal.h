@@ -7,6 +7,7 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "../../include/fdp.h"
@@ -324,6 +325,11 @@ struct MassMode {
   const double* Lb;
   const double* invd;
   const double* Mb;       // FORWARD: band of M, Mb[i*(2b+1) + (j-i+b)] = M[i][j]
+  // K3t scaled coefficients, rows of mass_coef_stride(band) doubles (NULL: the sweep kernels):
+  // cf[i][k] = L[i][i-band+k] / L[i][i], cb[i][k] = L[i+band-k][i] / L[i][i] (0 past n-1),
+  // cf[i][band] = cb[i][band] = 1 / L[i][i]
+  const double* cf;
+  const double* cb;
   const double* pre;
   const double* post;
   long long N;            // elements per batch item
@@ -333,6 +339,11 @@ struct MassMode {
   int forward;            // 1: y = M x along fibers (FDP_MASS_FORWARD)
 };
 cudaError_t launch_mass_mode(const MassMode& m, cudaStream_t s);
+inline int mass_coef_stride(int band) { return (band + 2) & ~1; }
+// K3t tensor map (abi_tma.cpp) of the (P, n, Q, batch) fiber view of X with box {F, boxn, 1, 1};
+// false when the encoder is unavailable or the view breaks a tensor-map rule.
+bool mass_tile_map(CUtensorMap* map, const double* X, int P, int n, long long Q, long long batch,
+                   long long bs, int F, int boxn);
 
 // ---------------------------------------------------------------------------------------------
 // Host numerics (host_eig.cpp, host_iga.cpp): own implementations, no LAPACK.

@@ -7,6 +7,13 @@
 // solution values live in registers (shift register, BAND is a template parameter).
 #include "../fdp_internal.h"
 
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+
 namespace fdp {
 namespace {
 
@@ -251,6 +258,345 @@ mass_solve_mode1_kernel(const MassMode mm) {
   }
 }
 
+// K3t: the whole solve of a tile of F fibers in shared memory — one HBM read and one HBM write
+// per element instead of the two of each that the forward/back sweeps above cost (y round-trips
+// through `out`). One warp per CTA. Mode 1 (P == 1): lane 0 arms an mbarrier and the lanes issue
+// one bulk copy per fiber (n doubles) into a fiber-major tile whose fiber stride NP is 2 mod 4
+// doubles (16-byte aligned rows; the 14-16 fibers' accesses spread over the bank groups); modes
+// >= 2: lane 0 issues `nbox` 4-D TMA tensor-map boxes {F fibers, boxn rows} (tile element (i, r)
+// at i F + r; a ragged last p-block is zero-filled on load and clipped on store). Lanes r < nf
+// run fiber r's recurrences in place and the tile leaves with bulk stores. The scaled band
+// coefficients cf / cb (kron_mass_setup) make each step one multiply and BAND FMAs whose
+// dependent chain is a single FMA on the newest value:
+//   forward  y_i = x_i d_i - sum_{j=BAND..1} (L_{i,i-j} d_i) y_{i-j}
+//   backward z_i = y_i d_i - sum_{j=BAND..1} (L_{i+j,i} d_i) z_{i+j},   d_i = 1 / L_ii
+// (the same solve as mass_solve_kernel up to rounding order; a right-looking column form with
+// the same per-sum order measured no faster: the warps stall on the FP64 chain either way).
+// Steps go in groups of G = 4 whose
+// tile values and coefficients sit in one of three register buffers loaded two groups ahead (one
+// group ahead, the compiler sank the loads onto the consumers and the warps stalled on them).
+// F = 14 leaves the L1 room for both coefficient arrays next to three tiles per SM.
+__device__ __forceinline__ unsigned k3_smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void k3_bulk_load(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void k3_bulk_store(void* dst, unsigned src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void k3_map_load(unsigned dst, const CUtensorMap* map, unsigned bar, int c0, int c1,
+                                            int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void k3_map_store(const CUtensorMap* map, unsigned src, int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
+          reinterpret_cast<unsigned long long>(map)),
+      "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(src)
+      : "memory");
+}
+
+struct TileArgs {
+  int NP;     // mode 1: fiber stride of the tile (doubles)
+  int boxn;   // modes >= 2: rows per tensor-map box
+  int nbox;   // boxes per tile
+};
+
+template <int BAND, int F, bool M1, bool SC>
+__global__ void __launch_bounds__(32) mass_tile_kernel(const MassMode mm, const __grid_constant__ CUtensorMap map_in,
+                                                      const __grid_constant__ CUtensorMap map_out,
+                                                      const TileArgs ta) {
+  extern __shared__ __align__(128) double T[];
+  __shared__ __align__(8) unsigned long long bar;
+  constexpr int CS = (BAND + 2) & ~1;  // coefficient row: BAND band values then d_i (padded even)
+  constexpr int G = 4;
+  const int lane = threadIdx.x;
+  const int n = mm.n;
+  const long long P = mm.P;
+  long long gbase = 0, sbase = 0;  // lane's own fiber (M1) / the tile's first fiber (modes >= 2)
+  int nf, p0 = 0, q = 0, bi = 0;
+  if (M1) {
+    const long long nfib = (long long)mm.Q * mm.batch, f0 = (long long)blockIdx.x * F;
+    nf = (int)min((long long)F, nfib - f0);
+    if (lane < nf) {
+      const long long f = f0 + lane;
+      sbase = (long long)n * (f % mm.Q);
+      gbase = sbase + mm.bs * (f / mm.Q);
+    }
+  } else {
+    const long long pblocks = (P + F - 1) / F, t = blockIdx.x;
+    p0 = (int)((t % pblocks) * F);
+    const long long rest = t / pblocks;
+    q = (int)(rest % mm.Q);
+    bi = (int)(rest / mm.Q);
+    nf = (int)min((long long)F, P - p0);
+    sbase = p0 + P * n * q;
+  }
+  const unsigned tb = k3_smem_u32(T), bb = k3_smem_u32(&bar);
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bb));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const unsigned bytes = M1 ? (unsigned)(n * nf * 8) : (unsigned)(ta.nbox * ta.boxn * F * 8);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bb), "r"(bytes) : "memory");
+    if (!M1)
+      for (int k = 0; k < ta.nbox; ++k)
+        k3_map_load(tb + (unsigned)(k * ta.boxn * F * 8), &map_in, bb, p0, k * ta.boxn, q, bi);
+  }
+  __syncwarp();
+  if (M1 && lane < nf) k3_bulk_load(tb + (unsigned)(lane * ta.NP * 8), mm.in + gbase, (unsigned)n * 8, bb);
+  asm volatile(
+      "{\n.reg .pred p;\nK3W_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+      "@!p bra K3W_%=;\n}\n" ::"r"(bb)
+      : "memory");
+
+  if (lane < nf) {
+    const int r = lane;
+    double* const Tr = M1 ? T + r * ta.NP : T + r;  // element i at Tr[i * ist]
+    const int ist = M1 ? 1 : F;
+    const long long pofs = M1 ? sbase : sbase + r;  // pre / post scaling offset
+    const long long pstr = M1 ? 1 : P;
+    const double* __restrict__ pre = SC ? mm.pre : nullptr;  // SC: a P^G scaling is present
+    const double* __restrict__ post = SC ? mm.post : nullptr;
+    double ring[BAND];  // ring[j-1] = value j steps back
+    struct Buf {
+      double x[G];
+      double c[G][CS];
+    };
+    Buf A, B, C;
+    const int ng = n / G;
+    // ---- forward ----
+    const double* __restrict__ cf = mm.cf;
+    auto load_f = [&](Buf& bf, int g) {
+#pragma unroll
+      for (int u = 0; u < G; ++u) {
+        const int i = g * G + u;
+        if (M1) {  // fiber-major tile: element pairs as 16-byte shared loads (i even, NP even)
+          if ((u & 1) == 0) {
+            const double2 t = *reinterpret_cast<const double2*>(Tr + i);
+            bf.x[u] = t.x;
+            bf.x[u + 1] = t.y;
+          }
+        } else {
+          bf.x[u] = Tr[i * ist];
+        }
+        if (pre) bf.x[u] *= __ldg(pre + pofs + pstr * i);
+#pragma unroll
+        for (int k = 0; k < CS; k += 2) {
+          const double2 v = __ldg(reinterpret_cast<const double2*>(cf + (size_t)i * CS + k));
+          bf.c[u][k] = v.x;
+          bf.c[u][k + 1] = v.y;
+        }
+      }
+    };
+    double Tf1 = 0.0;  // M1: the previous output of the pair being assembled
+    auto step_f = [&](const Buf& bf, int g) {
+#pragma unroll
+      for (int u = 0; u < G; ++u) {
+        double v = bf.x[u] * bf.c[u][BAND];
+#pragma unroll
+        for (int k = 0; k < BAND; ++k) v = fma(-bf.c[u][k], ring[BAND - 1 - k], v);
+#pragma unroll
+        for (int j = BAND - 1; j > 0; --j) ring[j] = ring[j - 1];
+        ring[0] = v;
+        if (M1) {
+          if (u & 1) *reinterpret_cast<double2*>(Tr + g * G + u - 1) = make_double2(Tf1, v);
+          Tf1 = v;
+        } else {
+          Tr[(g * G + u) * ist] = v;
+        }
+      }
+    };
+#pragma unroll
+    for (int j = 0; j < BAND; ++j) ring[j] = 0.0;
+    if (ng > 0) load_f(A, 0);
+    if (ng > 1) load_f(B, 1);
+    int g = 0;
+    for (; g + 3 <= ng; g += 3) {
+      load_f(C, g + 2);
+      step_f(A, g);
+      load_f(A, min(g + 3, ng - 1));
+      step_f(B, g + 1);
+      load_f(B, min(g + 4, ng - 1));
+      step_f(C, g + 2);
+    }
+    if (g < ng) step_f(A, g);
+    if (g + 1 < ng) step_f(B, g + 1);
+    for (int i = ng * G; i < n; ++i) {
+      double v = Tr[i * ist];
+      if (pre) v *= __ldg(pre + pofs + pstr * i);
+      const double* c = cf + (size_t)i * CS;
+      v *= __ldg(c + BAND);
+#pragma unroll
+      for (int k = 0; k < BAND; ++k) v = fma(-__ldg(c + k), ring[BAND - 1 - k], v);
+#pragma unroll
+      for (int j = BAND - 1; j > 0; --j) ring[j] = ring[j - 1];
+      ring[0] = v;
+      Tr[i * ist] = v;
+    }
+    // ---- backward: the n % G top steps singly, then groups h = ng-1 .. 0 (steps 4h+3 .. 4h) ----
+    const double* __restrict__ cb = mm.cb;
+#pragma unroll
+    for (int j = 0; j < BAND; ++j) ring[j] = 0.0;
+    for (int i = n - 1; i >= ng * G; --i) {
+      const double* c = cb + (size_t)i * CS;
+      double v = Tr[i * ist] * __ldg(c + BAND);
+#pragma unroll
+      for (int k = 0; k < BAND; ++k) v = fma(-__ldg(c + k), ring[BAND - 1 - k], v);
+#pragma unroll
+      for (int j = BAND - 1; j > 0; --j) ring[j] = ring[j - 1];
+      ring[0] = v;
+      Tr[i * ist] = post ? v * __ldg(post + pofs + pstr * i) : v;
+    }
+    auto load_b = [&](Buf& bf, int h) {
+#pragma unroll
+      for (int u = 0; u < G; ++u) {
+        const int i = h * G + G - 1 - u;
+        if (M1) {  // steps i, i - 1 from one 16-byte load at i - 1 (i odd)
+          if ((u & 1) == 0) {
+            const double2 t = *reinterpret_cast<const double2*>(Tr + i - 1);
+            bf.x[u] = t.y;
+            bf.x[u + 1] = t.x;
+          }
+        } else {
+          bf.x[u] = Tr[i * ist];
+        }
+#pragma unroll
+        for (int k = 0; k < CS; k += 2) {
+          const double2 v = __ldg(reinterpret_cast<const double2*>(cb + (size_t)i * CS + k));
+          bf.c[u][k] = v.x;
+          bf.c[u][k + 1] = v.y;
+        }
+      }
+    };
+    double Tr1 = 0.0;  // M1: the previous (higher-i) output of the pair being assembled
+    auto step_b = [&](const Buf& bf, int h) {
+#pragma unroll
+      for (int u = 0; u < G; ++u) {
+        const int i = h * G + G - 1 - u;
+        double v = bf.x[u] * bf.c[u][BAND];
+#pragma unroll
+        for (int k = 0; k < BAND; ++k) v = fma(-bf.c[u][k], ring[BAND - 1 - k], v);
+#pragma unroll
+        for (int j = BAND - 1; j > 0; --j) ring[j] = ring[j - 1];
+        ring[0] = v;
+        const double o = post ? v * __ldg(post + pofs + pstr * i) : v;
+        if (M1) {  // (i, i + 1) written together at the odd step u (i even)
+          if (u & 1) *reinterpret_cast<double2*>(Tr + i) = make_double2(o, Tr1);
+          Tr1 = o;
+        } else {
+          Tr[i * ist] = o;
+        }
+      }
+    };
+    if (ng > 0) load_b(A, ng - 1);
+    if (ng > 1) load_b(B, ng - 2);
+    int h = ng - 1;
+    for (; h - 2 >= 0; h -= 3) {
+      load_b(C, h - 2);
+      step_b(A, h);
+      load_b(A, max(h - 3, 0));
+      step_b(B, h - 1);
+      load_b(B, max(h - 4, 0));
+      step_b(C, h - 2);
+    }
+    if (h >= 0) step_b(A, h);
+    if (h - 1 >= 0) step_b(B, h - 1);
+  }
+  // generic-proxy smem writes -> visible to the bulk-copy (async) proxy, then the stores
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (M1) {
+    if (lane < nf) k3_bulk_store(mm.out + gbase, tb + (unsigned)(lane * ta.NP * 8), (unsigned)n * 8);
+  } else if (lane == 0) {
+    for (int k = 0; k < ta.nbox; ++k)
+      k3_map_store(&map_out, tb + (unsigned)(k * ta.boxn * F * 8), p0, k * ta.boxn, q, bi);
+  }
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem stays valid until read
+}
+
+// K3t applies when the copies' 16-byte rules hold (mode 1: n even; modes >= 2: P even, for the
+// tensor maps' strides; 16-byte aligned in / out, even batch stride), BAND <= kTileMaxBand and
+// the tile fits the per-CTA shared memory.
+constexpr int kTileMaxSmem = 227 * 1024;
+constexpr int kTileMaxBand = 8;
+inline int tile_f() {
+  static const int f = [] {
+    const char* e = std::getenv("FDP_K3_F");
+    const int v = e ? std::atoi(e) : 14;
+    return v == 16 ? 16 : 14;
+  }();
+  return f;
+}
+inline int tile_np(int n) { return (n / 2) % 2 ? n : n + 2; }  // n even: n or n + 2, = 2 mod 4
+inline TileArgs tile_args(const MassMode& m) {
+  TileArgs ta{};
+  ta.NP = tile_np(m.n);
+  ta.nbox = (m.n + 255) / 256;
+  // rows per box a multiple of 8: every box's shared-memory destination 128-byte aligned (F even)
+  ta.boxn = ((m.n + ta.nbox - 1) / ta.nbox + 7) / 8 * 8;
+  return ta;
+}
+inline size_t tile_smem(const MassMode& m, int F) {
+  const TileArgs ta = tile_args(m);
+  return m.P == 1 ? (size_t)F * ta.NP * 8 : (size_t)F * ta.boxn * ta.nbox * 8;
+}
+inline bool tile_ok(const MassMode& m) {
+  static const bool sweep = std::getenv("FDP_K3_SWEEP") != nullptr;  // diagnostic: the sweep kernels
+  static const bool all = std::getenv("FDP_K3_TILE_ALL") != nullptr;  // diagnostic: K3t in modes >= 2
+  if (m.forward || !m.cf || !m.cb || sweep || m.band < 1 || m.band > kTileMaxBand) return false;
+  // modes >= 2: the coalesced sweep kernel (0.9 ms per config-5 mode at 4.4 GB) beats K3t (1.2 ms
+  // at 2.2 GB: three 14-fiber tiles per SM leave the recurrences issue-bound)
+  if (m.P != 1 && !all) return false;
+  const bool a16 = ((reinterpret_cast<uintptr_t>(m.in) | reinterpret_cast<uintptr_t>(m.out)) & 15) == 0;
+  if (!a16 || (m.batch > 1 && (m.bs & 1))) return false;
+  if (m.P == 1 ? (m.n & 1) : (m.P & 1)) return false;
+  if ((long long)m.Q * m.batch >= (1LL << 31)) return false;
+  return tile_smem(m, tile_f()) <= (size_t)kTileMaxSmem;
+}
+
+template <int BAND, int F>
+cudaError_t launch_tile(const MassMode& m, cudaStream_t s) {
+  const TileArgs ta = tile_args(m);
+  const size_t smem = tile_smem(m, F);
+  const bool m1 = m.P == 1;
+  CUtensorMap map_in, map_out;
+  std::memset(&map_in, 0, sizeof(map_in));
+  std::memset(&map_out, 0, sizeof(map_out));
+  if (!m1 && (!mass_tile_map(&map_in, m.in, m.P, m.n, m.Q, m.batch, m.bs, F, ta.boxn) ||
+              !mass_tile_map(&map_out, m.out, m.P, m.n, m.Q, m.batch, m.bs, F, ta.boxn)))
+    return cudaErrorNotSupported;
+  const long long tiles = m1 ? ((long long)m.Q * m.batch + F - 1) / F
+                             : ((long long)m.P + F - 1) / F * m.Q * m.batch;
+  const bool sc = m.pre || m.post;
+  auto kern = m1 ? (sc ? mass_tile_kernel<BAND, F, true, true> : mass_tile_kernel<BAND, F, true, false>)
+                 : (sc ? mass_tile_kernel<BAND, F, false, true> : mass_tile_kernel<BAND, F, false, false>);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // the smallest carveout that holds three tiles (the rest of the 256 KB is L1, where the forward
+  // and backward coefficient arrays live: 2 x 24.8 KB at n = 516, band 4)
+  const int pct = (int)std::min<size_t>(100, (3 * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+  if (e != cudaSuccess) return e;
+  kern<<<(unsigned)tiles, 32, smem, s>>>(m, map_in, map_out, ta);
+  return cudaGetLastError();
+}
+
+template <int BAND>
+cudaError_t launch_tile_b(const MassMode& m, cudaStream_t s) {
+  if constexpr (BAND >= 1 && BAND <= kTileMaxBand)
+    return tile_f() == 16 ? launch_tile<BAND, 16>(m, s) : launch_tile<BAND, 14>(m, s);
+  return cudaErrorNotSupported;
+}
+
 // y = M x along fibers (FDP_MASS_FORWARD); out must not alias in.
 template <int BAND>
 __global__ void mass_forward_kernel(const MassMode mm) {
@@ -277,12 +623,16 @@ cudaError_t launch_b(const MassMode& m, cudaStream_t s) {
   const int threads = 128;
   const long long blocks = (nf + threads - 1) / threads;
   if (blocks == 0) return cudaSuccess;
-  if (m.forward) mass_forward_kernel<BAND><<<(unsigned)blocks, threads, 0, s>>>(m);
-  else if (m.P == 1) {
+  if (m.forward) {
+    mass_forward_kernel<BAND><<<(unsigned)blocks, threads, 0, s>>>(m);
+  } else if (tile_ok(m) && launch_tile_b<BAND>(m, s) != cudaErrorNotSupported) {
+    // K3t launched (or failed to launch: the error is read below)
+  } else if (m.P == 1) {
     const long long warps = (nf + 31) / 32;
     mass_solve_mode1_kernel<BAND><<<(unsigned)((warps + kM1Warps - 1) / kM1Warps), kM1Warps * 32, 0, s>>>(m);
+  } else {
+    mass_solve_kernel<BAND, 8><<<(unsigned)blocks, threads, 0, s>>>(m);
   }
-  else mass_solve_kernel<BAND, 8><<<(unsigned)blocks, threads, 0, s>>>(m);
   return cudaGetLastError();
 }
 
