@@ -304,6 +304,16 @@ __device__ __forceinline__ void k3_map_store(const CUtensorMap* map, unsigned sr
       : "memory");
 }
 
+__device__ __forceinline__ void k3_bulk_prefetch(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void k3_map_prefetch(const CUtensorMap* map, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
+                   reinterpret_cast<unsigned long long>(map)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
+
 struct TileArgs {
   int NP;     // mode 1: fiber stride of the tile (doubles)
   int boxn;   // modes >= 2: rows per tensor-map box
@@ -597,6 +607,381 @@ cudaError_t launch_tile_b(const MassMode& m, cudaStream_t s) {
   return cudaErrorNotSupported;
 }
 
+// K3u: K3t rebuilt around the instruction stream. The ncu source view of K3t shows one warp per
+// sub-partition issuing an instruction every ~3.7 cycles: three of every twelve are coefficient
+// loads through L1 with 64-bit address arithmetic, and each costs ~4 issue cycles, so a step takes
+// ~40 cycles where its five FP64 instructions need 10. K3u is one persistent 4-warp CTA per SM:
+//   * the scaled band rows R_i = (L_{i,i-BAND..i-1} d_i, d_i) (`cf`, the only table: both
+//     substitutions read ROW i at step i) are copied to shared memory once per CTA and read with
+//     warp-uniform 16-byte loads, no L1 and no per-step address arithmetic;
+//   * each warp owns a tile of 12 fibers (4 x 12 x n doubles + the table fill the 227 KB) and walks
+//     its own tile sequence with its own mbarrier, so the four warps' loads, solves and stores
+//     overlap each other;
+//   * both substitutions are right-looking, so the BAND FMAs of a step are independent of each
+//     other and the dependent chain is the single FMA on the newest value:
+//       forward   y_i = A_i - R_{i,BAND-1} y_{i-1};  A_{i+m} -= R_{i+m,BAND-1-m} y_{i-1} (m < BAND-1);
+//                 A_{i+BAND-1} = x_{i+BAND-1} d_{i+BAND-1} - R_{i+BAND-1,0} y_{i-1}
+//       backward  (z_i = d_i r_i)  r_j = A_j;  A_{j-m} -= R_{j,BAND-m} r_j (m = 1..BAND-1);
+//                 A_{j-BAND} = y_{j-BAND} - R_{j,0} r_j
+//     (the forward sums accumulate in K3t's order; the backward works on r = z / d so that the
+//     row-scaled table serves it too).
+// Steps go in groups of G = 4 rows whose tile values and coefficients sit in one of three register
+// buffers loaded ahead. Needs n % 4 == 0, n >= 16, 1 <= BAND <= 5 (the forward window of BAND rows
+// spans two groups); other shapes keep K3t / the sweeps.
+constexpr int kUWarps = 4;  // measured: 6 warps x 8 fibers 3.30 ms, 8 x 6 3.87 ms vs 2.36 ms (config 5, all modes)
+constexpr int kUF = 12;
+struct UArgs {
+  int NP;         // mode 1: fiber stride of the tile (doubles)
+  int boxn;       // modes >= 2: rows per tensor-map box
+  int nbox;       // boxes per tile
+  int tile_d;     // doubles per warp tile (128-byte multiple)
+  int tab_d;      // doubles of the coefficient table region (128-byte multiple)
+  long long tiles;
+  int prefetch;   // prefetch the warp's next tile into L2 (FDP_K3_NO_PF=1: off, diagnostic)
+};
+
+template <int BAND, bool M1, bool SC>
+__global__ void __launch_bounds__(kUWarps * 32, 1)
+    mass_utile_kernel(const MassMode mm, const __grid_constant__ CUtensorMap map_in,
+                      const __grid_constant__ CUtensorMap map_out, const UArgs ua) {
+  extern __shared__ __align__(128) double S[];
+  __shared__ __align__(8) unsigned long long bars[kUWarps];
+  constexpr int CS = (BAND + 2) & ~1;
+  constexpr int G = 4;
+  constexpr int F = kUF;
+  const int n = mm.n;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long P = mm.P;
+  {
+    const double2* __restrict__ src = reinterpret_cast<const double2*>(mm.cf);
+    double2* dst = reinterpret_cast<double2*>(S);
+    for (int i = threadIdx.x; i < n * CS / 2; i += kUWarps * 32) dst[i] = __ldg(src + i);
+  }
+  const double* const R = S;
+  double* const T = S + ua.tab_d + (size_t)warp * ua.tile_d;
+  const unsigned tb = k3_smem_u32(T), bb = k3_smem_u32(&bars[warp]);
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bb));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int ng = n / G;
+  const double* __restrict__ pre = SC ? mm.pre : nullptr;
+  const double* __restrict__ post = SC ? mm.post : nullptr;
+  unsigned phase = 0;
+  for (long long t = (long long)blockIdx.x * kUWarps + warp; t < ua.tiles; t += (long long)gridDim.x * kUWarps) {
+    long long gbase = 0, sbase = 0;  // lane's own fiber (M1) / the tile's first fiber (modes >= 2)
+    int nf, p0 = 0, q = 0, bi = 0;
+    if (M1) {
+      const long long nfib = (long long)mm.Q * mm.batch, f0 = t * F;
+      nf = (int)min((long long)F, nfib - f0);
+      if (lane < nf) {
+        const long long f = f0 + lane;
+        sbase = (long long)n * (f % mm.Q);
+        gbase = sbase + mm.bs * (f / mm.Q);
+      }
+    } else {
+      const long long pblocks = (P + F - 1) / F;
+      p0 = (int)((t % pblocks) * F);
+      const long long rest = t / pblocks;
+      q = (int)(rest % mm.Q);
+      bi = (int)(rest / mm.Q);
+      nf = (int)min((long long)F, P - p0);
+      sbase = p0 + P * n * q;
+    }
+    if (lane == 0) {
+      const unsigned bytes = M1 ? (unsigned)(n * nf * 8) : (unsigned)(ua.nbox * ua.boxn * F * 8);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bb), "r"(bytes) : "memory");
+      if (!M1)
+        for (int k = 0; k < ua.nbox; ++k)
+          k3_map_load(tb + (unsigned)(k * ua.boxn * F * 8), &map_in, bb, p0, k * ua.boxn, q, bi);
+    }
+    __syncwarp();
+    if (M1 && lane < nf) k3_bulk_load(tb + (unsigned)(lane * ua.NP * 8), mm.in + gbase, (unsigned)n * 8, bb);
+    {  // the warp's next tile on its way into L2 while this one is solved
+      const long long tn = t + (long long)gridDim.x * kUWarps;
+      if (ua.prefetch && tn < ua.tiles) {
+        if (M1) {
+          const long long nfib = (long long)mm.Q * mm.batch, f = tn * F + lane;
+          if (lane < F && f < nfib)
+            k3_bulk_prefetch(mm.in + (long long)n * (f % mm.Q) + mm.bs * (f / mm.Q), (unsigned)n * 8);
+        } else if (lane == 0) {
+          const long long pblocks = (P + F - 1) / F, rest = tn / pblocks;
+          for (int k = 0; k < ua.nbox; ++k)
+            k3_map_prefetch(&map_in, (int)((tn % pblocks) * F), k * ua.boxn, (int)(rest % mm.Q), (int)(rest / mm.Q));
+        }
+      }
+    }
+    asm volatile(
+        "{\n.reg .pred p;\nK3U_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra K3U_%=;\n}\n" ::"r"(bb),
+        "r"(phase)
+        : "memory");
+    phase ^= 1u;
+
+    if (lane < nf) {
+      const int r = lane;
+      double* const Tr = M1 ? T + r * ua.NP : T + r;  // element i at Tr[i * ist]
+      constexpr int ist = M1 ? 1 : F;
+      const long long pofs = M1 ? sbase : sbase + r;  // pre / post scaling offset
+      const long long pstr = M1 ? 1 : P;
+      struct Buf {
+        double x[G];      // forward: x_i (then x_i d_i); backward: y_{j-BAND}
+        double c[G][CS];  // R_i (unused in the constant-row phases)
+      };
+      Buf A, B, C;
+      auto load_c = [&](Buf& bf, int i, int u) {
+#pragma unroll
+        for (int k = 0; k < CS; k += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(R + (size_t)i * CS + k);
+          bf.c[u][k] = v.x;
+          bf.c[u][k + 1] = v.y;
+        }
+      };
+      // ---------------- forward ----------------
+      auto load_f = [&](Buf& bf, int g) {
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+          const int i = g * G + u;
+          load_c(bf, i, u);
+          if (M1) {
+            if ((u & 1) == 0) {
+              const double2 v = *reinterpret_cast<const double2*>(Tr + i);
+              bf.x[u] = v.x;
+              bf.x[u + 1] = v.y;
+            }
+          } else {
+            bf.x[u] = Tr[i * ist];
+          }
+        }
+        if (pre) {
+#pragma unroll
+          for (int u = 0; u < G; ++u) bf.x[u] *= __ldg(pre + pofs + pstr * (g * G + u));
+        }
+      };
+      // x_i d_i of a buffer, a group after its loads were issued (next to the loads, the multiplies
+      // stalled the warp on the load latency)
+      auto scale_f = [&](Buf& bf) {
+#pragma unroll
+        for (int u = 0; u < G; ++u) bf.x[u] *= bf.c[u][BAND];
+      };
+      double acc[BAND > 1 ? BAND - 1 : 1];
+      double yp = 0.0, ylo = 0.0;
+      auto step_f = [&](const Buf& cur, Buf& nxt, int g) {
+        scale_f(nxt);
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+          // row i + m of the window: cur for u + m < G, else nxt
+          auto cf_ = [&](int m, int k) { return (u + m < G) ? cur.c[(u + m) % G][k] : nxt.c[(u + m) % G][k]; };
+          double y;
+          if (BAND == 1) {
+            y = fma(-cf_(0, 0), yp, cur.x[u]);
+          } else {
+            y = fma(-cf_(0, BAND - 1), yp, acc[0]);
+#pragma unroll
+            for (int m = 1; m < BAND - 1; ++m) acc[m - 1] = fma(-cf_(m, BAND - 1 - m), yp, acc[m]);
+            const double xn = (u + BAND - 1 < G) ? cur.x[(u + BAND - 1) % G] : nxt.x[(u + BAND - 1) % G];
+            acc[BAND - 2] = fma(-cf_(BAND - 1, 0), yp, xn);
+          }
+          yp = y;
+          if (M1) {
+            if (u & 1) *reinterpret_cast<double2*>(Tr + g * G + u - 1) = make_double2(ylo, y);
+            ylo = y;
+          } else {
+            Tr[(g * G + u) * ist] = y;
+          }
+        }
+      };
+      // groups g0 .. g1-1 right-looking, three register buffers loaded two groups ahead
+      auto run_f = [&](int g0, int g1) {
+        load_f(A, g0);
+        load_f(B, min(g0 + 1, ng - 1));
+        scale_f(A);
+        int g = g0;
+        for (; g + 3 <= g1; g += 3) {
+          load_f(C, min(g + 2, ng - 1));
+          step_f(A, B, g);
+          load_f(A, min(g + 3, ng - 1));
+          step_f(B, C, g + 1);
+          load_f(B, min(g + 4, ng - 1));
+          step_f(C, A, g + 2);
+        }
+        if (g < g1) {
+          load_f(C, min(g + 2, ng - 1));
+          step_f(A, B, g);
+          if (g + 1 < g1) step_f(B, C, g + 1);
+        }
+      };
+      {
+        const int ngm = ng - 1;  // groups 0 .. ng-2 run right-looking (their windows end in group ng-1)
+#pragma unroll
+        for (int m = 0; m < BAND - 1; ++m) {
+          double v = Tr[m * ist] * R[(size_t)m * CS + BAND];
+          if (pre) v *= __ldg(pre + pofs + pstr * m);
+          acc[m] = v;
+        }
+        run_f(0, ngm);
+        // the last group left-looking from the tile
+        for (int i = ngm * G; i < n; ++i) {
+          const double* cr = R + (size_t)i * CS;
+          double v = Tr[i * ist];
+          if (pre) v *= __ldg(pre + pofs + pstr * i);
+          v *= cr[BAND];
+#pragma unroll
+          for (int k = 0; k < BAND; ++k) {
+            const int j = i - BAND + k;
+            if (j >= 0) v = fma(-cr[k], Tr[j * ist], v);
+          }
+          Tr[i * ist] = v;
+        }
+      }
+      // ---------------- backward ----------------
+      auto load_b = [&](Buf& bf, int h) {
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+          const int j = h * G + G - 1 - u;
+          load_c(bf, j, u);
+          if (M1 && (BAND & 1) == 0) {  // rows j - BAND, j - BAND - 1 from one 16-byte load (j odd at even u)
+            if ((u & 1) == 0) {
+              const double2 v = *reinterpret_cast<const double2*>(Tr + max(j - 1 - BAND, 0));
+              bf.x[u] = v.y;
+              bf.x[u + 1] = v.x;
+            }
+          } else {
+            bf.x[u] = Tr[max(j - BAND, 0) * ist];
+          }
+        }
+      };
+      double ab[BAND];
+      double ohi = 0.0;
+      auto step_b = [&](const Buf& bf, int h) {
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+          const int j = h * G + G - 1 - u;
+          auto cb_ = [&](int k) { return bf.c[u][k]; };
+          const double rj = ab[0];
+#pragma unroll
+          for (int m = 1; m < BAND; ++m) ab[m - 1] = fma(-cb_(BAND - m), rj, ab[m]);
+          ab[BAND - 1] = fma(-cb_(0), rj, bf.x[u]);
+          double o = rj * cb_(BAND);
+          if (post) o *= __ldg(post + pofs + pstr * j);
+          if (M1) {  // (j, j + 1) written together at the odd step u (j even)
+            if (u & 1) *reinterpret_cast<double2*>(Tr + j) = make_double2(o, ohi);
+            ohi = o;
+          } else {
+            Tr[j * ist] = o;
+          }
+        }
+      };
+      // groups h1-1 .. h0, descending
+      auto run_b = [&](int h0, int h1) {
+        load_b(A, h1 - 1);
+        load_b(B, max(h1 - 2, 0));
+        int h = h1 - 1;
+        for (; h - 2 >= h0; h -= 3) {
+          load_b(C, h - 2);
+          step_b(A, h);
+          load_b(A, max(h - 3, 0));
+          step_b(B, h - 1);
+          load_b(B, max(h - 4, 0));
+          step_b(C, h - 2);
+        }
+        if (h >= h0) step_b(A, h);
+        if (h - 1 >= h0) step_b(B, h - 1);
+      };
+      {
+#pragma unroll
+        for (int m = 0; m < BAND; ++m) ab[m] = Tr[(n - 1 - m) * ist];
+        run_b(0, ng);
+      }
+    }
+    // generic-proxy smem writes -> visible to the bulk-copy (async) proxy, then the stores
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (M1) {
+      if (lane < nf) k3_bulk_store(mm.out + gbase, tb + (unsigned)(lane * ua.NP * 8), (unsigned)n * 8);
+    } else if (lane == 0) {
+      for (int k = 0; k < ua.nbox; ++k)
+        k3_map_store(&map_out, tb + (unsigned)(k * ua.boxn * F * 8), p0, k * ua.boxn, q, bi);
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // the tile is free for the next load
+    __syncwarp();
+  }
+}
+
+inline int utile_mode() {  // FDP_K3_U: 0 off, 1 mode 1 only, 2 every mode (default)
+  static const int v = [] {
+    const char* e = std::getenv("FDP_K3_U");
+    return e ? std::atoi(e) : 2;
+  }();
+  return v;
+}
+inline int sm_count() {
+  static const int v = [] {
+    int dev = 0, c = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      c = 148;
+    return c > 0 ? c : 148;
+  }();
+  return v;
+}
+inline UArgs utile_args(const MassMode& m) {
+  UArgs ua{};
+  const int cs = mass_coef_stride(m.band);
+  ua.NP = tile_np(m.n);
+  ua.nbox = (m.n + 255) / 256;
+  ua.boxn = ((m.n + ua.nbox - 1) / ua.nbox + 7) / 8 * 8;
+  const long long td = m.P == 1 ? (long long)kUF * ua.NP : (long long)kUF * ua.boxn * ua.nbox;
+  ua.tile_d = (int)((td + 15) / 16 * 16);
+  ua.tab_d = (m.n * cs + 15) / 16 * 16;
+  static const bool nopf = std::getenv("FDP_K3_NO_PF") != nullptr;
+  ua.prefetch = nopf ? 0 : 1;
+  ua.tiles = m.P == 1 ? ((long long)m.Q * m.batch + kUF - 1) / kUF
+                      : ((long long)m.P + kUF - 1) / kUF * m.Q * m.batch;
+  return ua;
+}
+inline bool utile_ok(const MassMode& m) {
+  static const bool sweep = std::getenv("FDP_K3_SWEEP") != nullptr;
+  const int um = utile_mode();
+  if (m.forward || !m.cf || sweep || um < 1 || m.band < 1 || m.band > 5) return false;
+  if (m.P != 1 && um < 2) return false;
+  if ((m.n & 3) || m.n < 16 || m.n > (1 << 16)) return false;
+  const bool a16 = ((reinterpret_cast<uintptr_t>(m.in) | reinterpret_cast<uintptr_t>(m.out)) & 15) == 0;
+  if (!a16 || (m.batch > 1 && (m.bs & 1))) return false;
+  if (m.P != 1 && (m.P & 1)) return false;
+  const UArgs ua = utile_args(m);
+  if (ua.tiles < 1 || ua.tiles >= (1LL << 31) * kUF) return false;
+  return ((size_t)ua.tab_d + (size_t)kUWarps * ua.tile_d) * 8 <= (size_t)kTileMaxSmem;
+}
+
+template <int BAND>
+cudaError_t launch_utile(const MassMode& m, cudaStream_t s) {
+  if constexpr (BAND >= 1 && BAND <= 5) {
+    const UArgs ua = utile_args(m);
+    const size_t smem = ((size_t)ua.tab_d + (size_t)kUWarps * ua.tile_d) * 8;
+    const bool m1 = m.P == 1;
+    CUtensorMap map_in, map_out;
+    std::memset(&map_in, 0, sizeof(map_in));
+    std::memset(&map_out, 0, sizeof(map_out));
+    if (!m1 && (!mass_tile_map(&map_in, m.in, m.P, m.n, m.Q, m.batch, m.bs, kUF, ua.boxn) ||
+                !mass_tile_map(&map_out, m.out, m.P, m.n, m.Q, m.batch, m.bs, kUF, ua.boxn)))
+      return cudaErrorNotSupported;
+    const bool sc = m.pre || m.post;
+    auto kern = m1 ? (sc ? mass_utile_kernel<BAND, true, true> : mass_utile_kernel<BAND, true, false>)
+                   : (sc ? mass_utile_kernel<BAND, false, true> : mass_utile_kernel<BAND, false, false>);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+    const long long ctas = std::min<long long>(sm_count(), (ua.tiles + kUWarps - 1) / kUWarps);
+    kern<<<(unsigned)ctas, kUWarps * 32, smem, s>>>(m, map_in, map_out, ua);
+    return cudaGetLastError();
+  }
+  return cudaErrorNotSupported;
+}
+
 // y = M x along fibers (FDP_MASS_FORWARD); out must not alias in.
 template <int BAND>
 __global__ void mass_forward_kernel(const MassMode mm) {
@@ -625,6 +1010,8 @@ cudaError_t launch_b(const MassMode& m, cudaStream_t s) {
   if (blocks == 0) return cudaSuccess;
   if (m.forward) {
     mass_forward_kernel<BAND><<<(unsigned)blocks, threads, 0, s>>>(m);
+  } else if (utile_ok(m) && launch_utile<BAND>(m, s) != cudaErrorNotSupported) {
+    // K3u launched (or failed to launch: the error is read below)
   } else if (tile_ok(m) && launch_tile_b<BAND>(m, s) != cudaErrorNotSupported) {
     // K3t launched (or failed to launch: the error is read below)
   } else if (m.P == 1) {

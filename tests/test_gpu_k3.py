@@ -85,3 +85,38 @@ def test_k3_tile_config5_pressure_sampled_fibers():
         # the i1 = 7 plane holds y1[7] * (y3 (x) y2)
         plane = x[:, :, 7].cpu().numpy()
         _check(plane, y1[7] * np.outer(y3, y2))
+
+
+# K3u (mass_utile_kernel): the persistent 4-warp kernel with the coefficient rows in shared memory
+# and right-looking substitutions; taken when n % 4 == 0, n >= 16, band <= 5 (mode 1: any fiber
+# count; modes >= 2: even P). The cases cover both tile layouts, ragged last tiles (fiber counts and
+# P not multiples of 12), several tiles per warp (the mbarrier phase flips), band 1..5, batch > 1,
+# the P^G scaling and in-place calls.
+K3U_CASES = [
+    (((4, 512), (4, 12), (4, 16)), 1),    # n = 516, 16, 20: config 5's extent in mode 1
+    (((2, 62), (2, 126), (2, 126)), 1),   # 1366 / 768 / 683 tiles on 592 warps: 2-3 tiles per warp
+    (((3, 25), (2, 30), (1, 19)), 2),     # n = 28, 32, 20: P = 28 ragged p-blocks, mixed bands, batch
+    (((1, 39), (1, 15), (1, 19)), 3),     # band 1
+    (((5, 35), (5, 15), (5, 11)), 1),     # band 5 (the forward window spans two groups)
+    (((4, 60), (4, 28)), 2),              # 2D
+    (((4, 252), (4, 20)), 1),             # 2D, n = 256: whole groups only, P = 256 ragged (21 x 12 + 4)
+]
+
+
+@pytest.mark.parametrize("pn,batch", K3U_CASES)
+def test_k3u_inverse_vs_oracle(pn, batch):
+    test_k3_tile_inverse_vs_oracle(pn, batch)
+
+
+def test_k3t_cases_with_k3u_disabled():
+    """FDP_K3_U is read once per process: re-run the K3t and K3u cases in a child with K3u off, so
+    the K3t tile kernel and the sweeps stay covered on the shapes K3u now takes."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FDP_K3_U="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", os.path.abspath(__file__),
+                        "-k", "inverse_vs_oracle or sampled_fibers"], cwd=root, env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
