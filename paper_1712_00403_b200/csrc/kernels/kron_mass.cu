@@ -652,12 +652,26 @@ __global__ void __launch_bounds__(kUWarps * 32, 1)
   const int n = mm.n;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long P = mm.P;
-  {
+  // the table in shared memory. BAND odd: the rows of cf as they are (BAND coefficients and d_i,
+  // 16-byte aligned); BAND even: the d_i split off into their own array behind the rows, so that a
+  // group of four rows costs BAND / 2 loads per row plus two for its four d_i (instead of a padded
+  // third load per row)
+  constexpr bool SPLIT = (BAND & 1) == 0;
+  constexpr int RS = SPLIT ? BAND : CS;  // row stride
+  if (SPLIT) {
+    for (int i = threadIdx.x; i < n * CS; i += kUWarps * 32) {
+      const int row = i / CS, k = i - row * CS;
+      const double v = __ldg(mm.cf + i);
+      if (k < BAND) S[row * BAND + k] = v;
+      else if (k == BAND) S[n * BAND + row] = v;
+    }
+  } else {
     const double2* __restrict__ src = reinterpret_cast<const double2*>(mm.cf);
     double2* dst = reinterpret_cast<double2*>(S);
     for (int i = threadIdx.x; i < n * CS / 2; i += kUWarps * 32) dst[i] = __ldg(src + i);
   }
   const double* const R = S;
+  const double* const E = S + (size_t)n * BAND;  // SPLIT: d_i
   double* const T = S + ua.tab_d + (size_t)warp * ua.tile_d;
   const unsigned tb = k3_smem_u32(T), bb = k3_smem_u32(&bars[warp]);
   if (lane == 0) {
@@ -734,12 +748,25 @@ __global__ void __launch_bounds__(kUWarps * 32, 1)
       Buf A, B, C;
       auto load_c = [&](Buf& bf, int i, int u) {
 #pragma unroll
-        for (int k = 0; k < CS; k += 2) {
-          const double2 v = *reinterpret_cast<const double2*>(R + (size_t)i * CS + k);
+        for (int k = 0; k < RS; k += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(R + (size_t)i * RS + k);
           bf.c[u][k] = v.x;
           bf.c[u][k + 1] = v.y;
         }
       };
+      // SPLIT: the d_i of rows 4 gq .. 4 gq + 3 into slots u = 0..3 (rev: 3..0)
+      auto load_e = [&](Buf& bf, int gq, bool rev) {
+        if (SPLIT) {
+          const double2 a = *reinterpret_cast<const double2*>(E + gq * G);
+          const double2 b = *reinterpret_cast<const double2*>(E + gq * G + 2);
+          bf.c[rev ? 3 : 0][BAND] = a.x;
+          bf.c[rev ? 2 : 1][BAND] = a.y;
+          bf.c[rev ? 1 : 2][BAND] = b.x;
+          bf.c[rev ? 0 : 3][BAND] = b.y;
+        }
+      };
+      auto coef = [&](int i, int k) { return R[(size_t)i * RS + k]; };
+      auto dinv = [&](int i) { return SPLIT ? E[i] : R[(size_t)i * RS + BAND]; };
       // ---------------- forward ----------------
       auto load_f = [&](Buf& bf, int g) {
 #pragma unroll
@@ -756,6 +783,7 @@ __global__ void __launch_bounds__(kUWarps * 32, 1)
             bf.x[u] = Tr[i * ist];
           }
         }
+        load_e(bf, g, false);
         if (pre) {
 #pragma unroll
           for (int u = 0; u < G; ++u) bf.x[u] *= __ldg(pre + pofs + pstr * (g * G + u));
@@ -818,21 +846,20 @@ __global__ void __launch_bounds__(kUWarps * 32, 1)
         const int ngm = ng - 1;  // groups 0 .. ng-2 run right-looking (their windows end in group ng-1)
 #pragma unroll
         for (int m = 0; m < BAND - 1; ++m) {
-          double v = Tr[m * ist] * R[(size_t)m * CS + BAND];
+          double v = Tr[m * ist] * dinv(m);
           if (pre) v *= __ldg(pre + pofs + pstr * m);
           acc[m] = v;
         }
         run_f(0, ngm);
         // the last group left-looking from the tile
         for (int i = ngm * G; i < n; ++i) {
-          const double* cr = R + (size_t)i * CS;
           double v = Tr[i * ist];
           if (pre) v *= __ldg(pre + pofs + pstr * i);
-          v *= cr[BAND];
+          v *= dinv(i);
 #pragma unroll
           for (int k = 0; k < BAND; ++k) {
             const int j = i - BAND + k;
-            if (j >= 0) v = fma(-cr[k], Tr[j * ist], v);
+            if (j >= 0) v = fma(-coef(i, k), Tr[j * ist], v);
           }
           Tr[i * ist] = v;
         }
@@ -853,6 +880,7 @@ __global__ void __launch_bounds__(kUWarps * 32, 1)
             bf.x[u] = Tr[max(j - BAND, 0) * ist];
           }
         }
+        load_e(bf, h, true);
       };
       double ab[BAND];
       double ohi = 0.0;
@@ -936,7 +964,7 @@ inline UArgs utile_args(const MassMode& m) {
   ua.boxn = ((m.n + ua.nbox - 1) / ua.nbox + 7) / 8 * 8;
   const long long td = m.P == 1 ? (long long)kUF * ua.NP : (long long)kUF * ua.boxn * ua.nbox;
   ua.tile_d = (int)((td + 15) / 16 * 16);
-  ua.tab_d = (m.n * cs + 15) / 16 * 16;
+  ua.tab_d = (m.n * ((m.band & 1) ? cs : m.band + 1) + 15) / 16 * 16;
   static const bool nopf = std::getenv("FDP_K3_NO_PF") != nullptr;
   ua.prefetch = nopf ? 0 : 1;
   ua.tiles = m.P == 1 ? ((long long)m.Q * m.batch + kUF - 1) / kUF
