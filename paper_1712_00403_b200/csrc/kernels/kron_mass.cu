@@ -270,8 +270,9 @@ mass_solve_mode1_kernel(const MassMode mm) {
 // dependent chain is a single FMA on the newest value:
 //   forward  y_i = x_i d_i - sum_{j=BAND..1} (L_{i,i-j} d_i) y_{i-j}
 //   backward z_i = y_i d_i - sum_{j=BAND..1} (L_{i+j,i} d_i) z_{i+j},   d_i = 1 / L_ii
-// (the same solve as mass_solve_kernel up to rounding order; a right-looking column form with
-// the same per-sum order measured no faster: the warps stall on the FP64 chain either way).
+// (the same solve as mass_solve_kernel up to rounding order). Round 2's ncu source view: the warp
+// issues one instruction per ~3.7 cycles and a quarter of them are the coefficient loads through
+// L1 (~4 issue cycles each); K3u below keeps the rows in shared memory and takes the shapes it can.
 // Steps go in groups of G = 4 whose
 // tile values and coefficients sit in one of three register buffers loaded two groups ahead (one
 // group ahead, the compiler sank the loads onto the consumers and the warps stalled on them).
@@ -637,7 +638,7 @@ struct UArgs {
   int tile_d;     // doubles per warp tile (128-byte multiple)
   int tab_d;      // doubles of the coefficient table region (128-byte multiple)
   long long tiles;
-  int prefetch;   // prefetch the warp's next tile into L2 (FDP_K3_NO_PF=1: off, diagnostic)
+  int prefetch;   // L2 prefetch of the warp's next tile: 0 off, 1 at load time, 2 between the substitutions
 };
 
 template <int BAND, bool M1, bool SC>
@@ -713,9 +714,12 @@ __global__ void __launch_bounds__(kUWarps * 32, 1)
     }
     __syncwarp();
     if (M1 && lane < nf) k3_bulk_load(tb + (unsigned)(lane * ua.NP * 8), mm.in + gbase, (unsigned)n * 8, bb);
-    {  // the warp's next tile on its way into L2 while this one is solved
+    // the warp's next tile on its way into L2 while this one is solved; issued between the two
+    // substitutions: at load time (a whole tile solve, ~13 us, ahead) ncu showed 1.25-1.6x the
+    // algorithmic DRAM reads - part of the prefetched lines were evicted before their load
+    auto prefetch_next = [&]() {
       const long long tn = t + (long long)gridDim.x * kUWarps;
-      if (ua.prefetch && tn < ua.tiles) {
+      if (tn < ua.tiles) {
         if (M1) {
           const long long nfib = (long long)mm.Q * mm.batch, f = tn * F + lane;
           if (lane < F && f < nfib)
@@ -726,7 +730,8 @@ __global__ void __launch_bounds__(kUWarps * 32, 1)
             k3_map_prefetch(&map_in, (int)((tn % pblocks) * F), k * ua.boxn, (int)(rest % mm.Q), (int)(rest / mm.Q));
         }
       }
-    }
+    };
+    if (ua.prefetch == 1) prefetch_next();
     asm volatile(
         "{\n.reg .pred p;\nK3U_%=:\n"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
@@ -864,6 +869,7 @@ __global__ void __launch_bounds__(kUWarps * 32, 1)
           Tr[i * ist] = v;
         }
       }
+      if (ua.prefetch == 2) prefetch_next();
       // ---------------- backward ----------------
       auto load_b = [&](Buf& bf, int h) {
 #pragma unroll
@@ -965,8 +971,12 @@ inline UArgs utile_args(const MassMode& m) {
   const long long td = m.P == 1 ? (long long)kUF * ua.NP : (long long)kUF * ua.boxn * ua.nbox;
   ua.tile_d = (int)((td + 15) / 16 * 16);
   ua.tab_d = (m.n * ((m.band & 1) ? cs : m.band + 1) + 15) / 16 * 16;
-  static const bool nopf = std::getenv("FDP_K3_NO_PF") != nullptr;
-  ua.prefetch = nopf ? 0 : 1;
+  static const int pf = [] {  // FDP_K3_NO_PF=1: off; FDP_K3_PF=1: at load time (diagnostics)
+    if (std::getenv("FDP_K3_NO_PF")) return 0;
+    const char* e = std::getenv("FDP_K3_PF");
+    return e ? std::atoi(e) : 2;
+  }();
+  ua.prefetch = pf;
   ua.tiles = m.P == 1 ? ((long long)m.Q * m.batch + kUF - 1) / kUF
                       : ((long long)m.P + kUF - 1) / kUF * m.Q * m.batch;
   return ua;

@@ -1,7 +1,7 @@
 #!/bin/bash
 # One-shot measurement pass on a GPU box (round 2): GPU test suite + smoke, per-launch stage times,
 # bench lines of every config (config 5 = the default) and the reference arm, the ncu launch
-# list of the default bench, and ncu --set full captures of the K1t launches of configs 5 and 4
+# list of the default bench, and ncu --set full captures of the K1t launches of configs 5 and 4 and of the pressure-solve launches of config 5
 # summarised on the box (the .ncu-rep files are too large to bring back). Outputs in gpurun_out/.
 set -u
 mkdir -p gpurun_out /tmp/ncu
@@ -25,6 +25,14 @@ timeout 1200 ncu --set full --clock-control none --import-source on -k regex:mod
   -o /tmp/ncu/full_cfg4 -f python bench.py --config 4 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/${T}_ncu_full4.log 2>&1
 python tools/ncu_summary.py /tmp/ncu/full_cfg4.ncu-rep --tag ${T}_ncu_cfg4 > gpurun_out/${T}_sum4.log 2>&1
 cp profiles/${T}_ncu_cfg4.md profiles/${T}_ncu_cfg4.json gpurun_out/ 2>/dev/null
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:mass_ -s 6 -c 3 \
+  -o /tmp/ncu/full_k3 -f python bench.py --config 5 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/${T}_ncu_fullk3.log 2>&1
+python tools/ncu_summary.py /tmp/ncu/full_k3.ncu-rep --tag ${T}_ncu_k3_cfg5 > gpurun_out/${T}_sumk3.log 2>&1
+cp profiles/${T}_ncu_k3_cfg5.md profiles/${T}_ncu_k3_cfg5.json gpurun_out/ 2>/dev/null
+ncu -i /tmp/ncu/full_k3.ncu-rep --page source --csv --print-units base --print-source sass > /tmp/srck3.csv 2>/dev/null
+python probes/ncu_loop.py /tmp/srck3.csv 0 > gpurun_out/${T}_k3u_stalls.txt 2>&1
+timeout 300 python probes/k3_bench.py > gpurun_out/${T}_k3_bench.txt 2>&1
+FDP_K3_U=0 timeout 300 python probes/k3_bench.py >> gpurun_out/${T}_k3_bench.txt 2>&1
 ncu -i /tmp/ncu/full_cfg5.ncu-rep --page source --csv --print-units base --print-source sass > /tmp/src5.csv 2>/dev/null
 python probes/ncu_src_top.py /tmp/src5.csv > gpurun_out/${T}_src_top_cfg5.txt 2>&1
 echo done
