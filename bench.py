@@ -507,9 +507,11 @@ def main():
     dense_equiv = (dense_fl * len(prof_runs) / (k1_ms * 1e-3)) / 1e12 if k1_ms > 0 else None
     # DRAM traffic per K1 launch from the committed ncu --set full capture of this config
     traffic = traffic_src = None
-    ncu_json = os.path.join(ROOT, "profiles", f"r02_ncu_cfg{cid}.json")
-    if not os.path.exists(ncu_json):
-        ncu_json = os.path.join(ROOT, "profiles", f"r01_ncu_cfg{cid}.json")
+    ncu_json = ""
+    for tag in ("r02f", "r02", "r01"):  # the newest committed capture of this config
+        ncu_json = os.path.join(ROOT, "profiles", f"{tag}_ncu_cfg{cid}.json")
+        if os.path.exists(ncu_json):
+            break
     if os.path.exists(ncu_json):
         # the dominant launch's kernel: the plane kernel (plane path) or the folded K1 forward
         # (FOLD = 1, the fourth template argument); else every FD-transform kernel captured
