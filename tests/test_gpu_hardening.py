@@ -146,6 +146,36 @@ def test_banded_mass_guards():
     assert rel(x, ref) < TOL and relmax(x, ref) < TOL
 
 
+@pytest.mark.parametrize("pn,batch,scaled", [
+    (((3, 25), (2, 30), (1, 19)), 2, False),  # n = 28, 32, 20: ragged 12-fiber tiles in every mode, batch
+    (((4, 124), (4, 124)), 1, True),          # 2D, n = 128 x 128: ragged tiles (128 = 10 x 12 + 8), P^G scaling
+])
+def test_k3u_tile_kernel_guards(pn, batch, scaled):
+    """K3u (the persistent tile kernel of the banded pressure solve: bulk copies and tensor-map
+    boxes in and out of shared memory) on 16-byte-aligned guarded buffers: margins intact, every
+    output finite and equal to the oracle's."""
+    from oracle import univariate
+    Mq = [univariate.pressure_mass(p, ne) for p, ne in pn]
+    M = fdp.KronMass(Mq)
+    n = int(np.prod([m.shape[0] for m in Mq]))
+    rng = np.random.default_rng(11)
+    b = rng.standard_normal((batch, n))
+    dq = rng.uniform(0.5, 2.0, n)
+    bb, bv, bo = _guarded(n * batch, b, False)
+    xb, xv, xo = _guarded(n * batch, None, False)
+    db, dvw, do = _guarded(n, 1.0 / np.sqrt(dq), False)
+    xv.view(torch.int64).fill_(SENT)
+    M.apply(bv, xv, dscale=dvw if scaled else None, batch=batch)
+    torch.cuda.synchronize()
+    assert _margins_intact(bb, bo, n * batch) and _margins_intact(xb, xo, n * batch) and _margins_intact(db, do, n)
+    x = xv.cpu().numpy().reshape(batch, n)
+    assert np.all(np.isfinite(x))
+    km = omass.KronMass(Mq)
+    for i in range(batch):
+        ref = km.scaled_inverse(b[i], dq) if scaled else km.inverse(b[i])
+        assert rel(x[i], ref) < TOL and relmax(x[i], ref) < TOL
+
+
 @pytest.mark.slow
 def test_config4_bench_launch_guards():
     """Config 4 at full size in the bench launch (batch 8, 436 M doubles per vector): guards and a
