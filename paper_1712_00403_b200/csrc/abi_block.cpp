@@ -11,6 +11,9 @@ static void free_block(fdp_block h) {
   for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
   for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);
   if (h->cap) cudaStreamDestroy(h->cap);
+  if (h->side) cudaStreamDestroy(h->side);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
   cudaFree(h->dv);
   cudaFree(h->dq);
   cudaFree(h->dall);
@@ -153,6 +156,9 @@ extern "C" fdp_status block_precond_setup(int D, const fdp_fd* vel, fdp_mass pre
     }
     if (!st) {
       cudaError_t e = cudaStreamCreateWithFlags(&raw->cap, cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&raw->side, cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&raw->ev_fork, cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&raw->ev_join, cudaEventDisableTiming);
       if (e != cudaSuccess) st = cuda_fail(e, "block_precond_setup: stream");
     }
     if (st) {
@@ -296,11 +302,29 @@ static cudaError_t enqueue_block(fdp_block h, const double* r, double* s, int64_
     pq.rq = rq;
     pq.rbs = sz;
   }
-  cudaError_t e = enqueue_fd(h->vel, in, sz, out, sz, T, dsc, batch, st, nlaunch, rec, hook,
-                             pplane ? &pq : nullptr, fuse_pre);
+  // pressure block by banded per-mode solves: r_p -> s_p. Inside a stream capture
+  // (every apply but the profiled one) it goes first and on a forked branch, so that the graph
+  // may run it next to the velocity path's launches; the profiled apply keeps one stream, where
+  // per-launch events mean what they say.
+  cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+  static const bool nofork = std::getenv("FDP_NO_FORK") != nullptr;
+  const bool fork = !h->pres_dense && !rec && !nofork && h->side &&
+                    cudaStreamIsCapturing(st, &cst) == cudaSuccess && cst == cudaStreamCaptureStatusActive;
+  cudaError_t e;
+  if (fork) {
+    if ((e = cudaEventRecord(h->ev_fork, st)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(h->side, h->ev_fork, 0)) != cudaSuccess) return e;
+    e = enqueue_mass(h->pres, FDP_MASS_INVERSE, r + h->off[D], s + h->off[D], sz, h->dq, batch, h->side,
+                     nlaunch, nullptr);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaEventRecord(h->ev_join, h->side)) != cudaSuccess) return e;
+  }
+  e = enqueue_fd(h->vel, in, sz, out, sz, T, dsc, batch, st, nlaunch, rec, hook,
+                 pplane ? &pq : nullptr, fuse_pre);
   if (e != cudaSuccess) return e;
-  if (!h->pres_dense) {
-    // pressure block by banded per-mode solves: r_p -> s_p
+  if (fork) {
+    if ((e = cudaStreamWaitEvent(st, h->ev_join, 0)) != cudaSuccess) return e;
+  } else if (!h->pres_dense) {
     e = enqueue_mass(h->pres, FDP_MASS_INVERSE, r + h->off[D], s + h->off[D], sz, h->dq, batch, st,
                      nlaunch, rec);
     if (e != cudaSuccess) return e;

@@ -216,6 +216,11 @@ struct fdp_block_s {
   TileCfg q_cfgF[3];           // q_fold == 2: tile shape of the folded K1 pass
   int q_foldh[3] = {0, 0, 0};
   cudaStream_t cap = nullptr;  // private capture stream
+  // banded pressure solve on its own branch of a captured apply (enqueue_block): the pressure
+  // block is independent of the velocity blocks, and the velocity path's memory-bound first
+  // launch (the row-padding pass) fits under the issue-bound pressure kernels
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // graph cache
   std::mutex mu;
   struct GraphEntry {
