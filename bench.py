@@ -508,7 +508,7 @@ def main():
     # DRAM traffic per K1 launch from the committed ncu --set full capture of this config
     traffic = traffic_src = None
     ncu_json = ""
-    for tag in ("r02f", "r02", "r01"):  # the newest committed capture of this config
+    for tag in ("r02g", "r02", "r01"):  # the newest committed capture of this config
         ncu_json = os.path.join(ROOT, "profiles", f"{tag}_ncu_cfg{cid}.json")
         if os.path.exists(ncu_json):
             break
